@@ -1,0 +1,236 @@
+/*
+ * hwwg — B200-native engine for the hybrid weight-window time-dependent Monte
+ * Carlo history loop (arxiv 2512.19925).  C ABI: plain pointers and sizes, no
+ * exceptions, no C++ or torch types.  Every entry point returns an int status
+ * (HWWG_OK == 0, negative on error; hwwg_last_error() holds the message) unless
+ * stated otherwise.  All host pointers are caller-owned and never retained.
+ *
+ * Boundary:
+ *   hwwg_run_segment_parallel  replaces  hww::run_segment_parallel
+ *       proj/include/hww/transport.hpp:117-120 / proj/src/transport.cpp:209-237
+ *       (and its serial twin transport.hpp:109-111) — same inputs (StepContext,
+ *       source span, h_begin, nullable window grid) and the same accumulate-into-
+ *       caller semantics for TallySet / StepOutcome; std::invalid_argument
+ *       becomes HWWG_EINVAL.
+ *   hwwg_driver_*              replaces  hww::run / hww::run_step
+ *       proj/include/hww/driver.hpp:80-88 (device-resident time-step loop:
+ *       comb -> LOSM windows -> segments with mid-step updates -> finalize).
+ *   hwwg_losm_assemble_solve   replaces  hww::assemble_solve
+ *       proj/include/hww/losm.hpp:77-80 (single-CTA device solve).
+ *   hwwg_build_centers         replaces  hww::build_centers  proj/include/hww/ww.hpp:34-35
+ *   hwwg_moving_average        replaces  hww::moving_average proj/include/hww/filters.hpp:30
+ *   hwwg_uniform_comb          replaces  hww::uniform_comb   proj/include/hww/popctrl.hpp:22
+ *
+ * Calls on one context are single-threaded; device work runs on the context's
+ * own CUDA stream; calls that return host data synchronise that stream.
+ */
+#ifndef HWWG_H
+#define HWWG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HWWG_OK 0
+#define HWWG_EINVAL (-1)    /* invalid argument (reference: std::invalid_argument) */
+#define HWWG_ECUDA (-2)     /* CUDA runtime failure or no device */
+#define HWWG_ENOMEM (-3)    /* device allocation failed */
+#define HWWG_ESTATE (-4)    /* call out of order */
+#define HWWG_ESINGULAR (-5) /* LOSM system singular (reference: std::runtime_error) */
+#define HWWG_ENOSPC (-6)    /* caller buffer too small; *needed is set */
+#define HWWG_ESTACK (-7)    /* exact-mode daughter stack exceeded its run capacity */
+
+#define HWWG_RNG_EXACT 0  /* replay the reference's xoshiro256** streams bit-for-bit */
+#define HWWG_RNG_PHILOX 1 /* event-based throughput mode, counter-based Philox4x32-10 */
+
+typedef struct hwwg_ctx hwwg_ctx;
+typedef struct hwwg_driver hwwg_driver;
+
+/* == hww::Particle (proj/include/hww/particle.hpp:9-14), 32 bytes. */
+typedef struct { double x, mu, w, t; } hwwg_particle;
+
+/* == hww::Material (proj/include/hww/material.hpp:9-18). */
+typedef struct { double sigma_t, sigma_s, sigma_f, nu_f, speed; } hwwg_material;
+
+/* == hww::StepCounters (proj/include/hww/transport.hpp:37-63). */
+typedef struct {
+  uint64_t collisions, splits, split_daughters, capped_splits, roulette_kills,
+      roulette_survivals, census_count, event_cap_aborts, nan_aborts;
+  double leakage_weight, aborted_weight;
+} hwwg_counters;
+
+/* == hww::StepContext (proj/include/hww/transport.hpp:83-94); the mesh is given
+ * by its I+1 strictly increasing edges, materials per cell. */
+typedef struct {
+  const double* edges;
+  int32_t cells;
+  int32_t batches;
+  const hwwg_material* materials;
+  double t_begin, t_end;
+  uint64_t seed;
+  int32_t step_index;
+  int32_t pad_;
+  uint64_t histories_total;
+} hwwg_step_context;
+
+/* == hww::WeightWindowGrid (proj/include/hww/ww.hpp:13-27); NULL grid = analog. */
+typedef struct {
+  const double* centers; /* I */
+  double rho;
+  double eps_min;
+} hwwg_window_grid;
+
+/* == hww::TallySet (proj/include/hww/tally.hpp:16-45), caller-owned arrays that
+ * the engine ACCUMULATES into (any array pointer may be NULL to skip it). */
+typedef struct {
+  double* track_flux;          /* I   */
+  double* track_flux_batch;    /* B*I */
+  double* census_phi;          /* I   */
+  double* census_current;      /* I   */
+  double* census_closure;      /* I   */
+  double* census_weight_batch; /* B   */
+  double* edge_current;        /* I+1 */
+  double boundary_closure_left;
+  double boundary_closure_right;
+  uint64_t histories_scored;
+  uint64_t grazing_discarded;
+} hwwg_tally_set;
+
+/* == hww::StepOutcome (proj/include/hww/transport.hpp:67-80): the census is
+ * APPENDED at census[census_size...] (reference emission order), counters and
+ * tracks_per_cell are summed.  If census_capacity is too small the call fails
+ * with HWWG_ENOSPC, sets census_needed and leaves every output untouched. */
+typedef struct {
+  hwwg_particle* census;
+  uint64_t census_size;
+  uint64_t census_capacity;
+  uint64_t census_needed;
+  hwwg_counters counters;
+  uint64_t* tracks_per_cell; /* I */
+} hwwg_step_outcome;
+
+/* Engine construction: the problem that stays resident on the device. */
+typedef struct {
+  int32_t device;        /* CUDA ordinal */
+  int32_t rng_mode;      /* HWWG_RNG_EXACT or HWWG_RNG_PHILOX */
+  uint64_t bank_capacity;/* initial particle capacity of each device bank (grows) */
+} hwwg_options;
+
+const char* hwwg_last_error(void);
+const char* hwwg_version(void);
+
+int hwwg_create(const hwwg_options* opts, hwwg_ctx** out);
+void hwwg_destroy(hwwg_ctx* ctx);
+
+/* Drop-in for hww::run_segment_parallel (transport.hpp:117-120): histories
+ * [h_begin, h_begin + n) of step ctx->step_index, source[0..n) on the HOST.
+ * Copies the source to the device, runs the history loop, accumulates the
+ * tallies/counters/tracks and appends the census in reference order. */
+int hwwg_run_segment_parallel(hwwg_ctx* ctx, const hwwg_step_context* step,
+                              const hwwg_particle* source, uint64_t n, uint64_t h_begin,
+                              const hwwg_window_grid* ww, hwwg_tally_set* tallies,
+                              hwwg_step_outcome* outcome);
+
+/* ------------------------------------------------------------------ driver */
+/* == hww::RunConfig (proj/include/hww/config.hpp:33-66) plus engine options. */
+typedef struct {
+  int32_t mode; /* 0 analog, 1 lww, 2 hww, 3 hww_ma, 4 hww_fourier */
+  int32_t u_ww;
+  uint64_t histories_per_step;
+  double theta, rho, eps_min;
+  int32_t n_fractions;
+  int32_t ma_base_k;
+  double fractions[8];
+  int32_t fourier_cutoff;
+  int32_t batches;
+  uint64_t seed;
+  uint64_t target_population;
+  double comb_overflow_factor;
+  double x0, t0, strength;
+  double sigma_t, sigma_s, sigma_f, nu_f, speed;
+  double x_min, x_max;
+  int32_t cells;
+  int32_t time_steps;
+  double t_end;
+  int32_t threads; /* accepted for config-file parity; unused */
+  int32_t host_bank; /* 1: bank round-trips through host memory each step (e2e) */
+} hwwg_run_config;
+
+/* == hww::StepRecord scalars (proj/include/hww/driver.hpp:41-56). */
+typedef struct {
+  int32_t step;
+  int32_t updates_applied;
+  int32_t hybrid_solve_failed;
+  int32_t n_thresholds;
+  uint64_t thresholds[8];
+  double t_begin, t_end, tau;
+  uint64_t histories;
+  uint64_t comb_in, comb_out;
+  double comb_in_weight, comb_out_weight;
+  hwwg_counters counters;
+  uint64_t segments; /* sum of tracks_per_cell: the throughput unit */
+  uint64_t census_size;
+  double census_weight, census_weight_sigma;
+  double boundary_closure_left, boundary_closure_right;
+  double fom_sigma_l2;
+  int32_t sigma_valid;
+  int32_t has_windows;
+  int32_t has_hybrid;
+  int32_t pad_;
+  double device_ms;    /* CUDA-event time of the whole step on the engine stream */
+  double transport_ms; /* CUDA-event time of the transport (history) kernels only */
+  uint64_t transport_launches; /* transport kernel launches in the step */
+  uint64_t kernel_launches;    /* all engine kernel launches in the step */
+  uint64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by the step (host_bank mode) */
+} hwwg_step_record;
+
+int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts,
+                       hwwg_driver** out);
+void hwwg_driver_destroy(hwwg_driver* d);
+/* Runs the next time step (driver.cpp:99-284); fills *rec. */
+int hwwg_driver_step(hwwg_driver* d, hwwg_step_record* rec);
+/* Per-cell arrays of the last step (any pointer may be NULL). */
+int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma,
+                       double* phi_census, double* current_census, double* closure_census,
+                       double* edge_current, double* ww_centers, double* phi_hybrid,
+                       uint64_t* tracks_per_cell);
+/* Census bank after the last step (the next step's comb input), reference
+ * order.  Returns HWWG_ENOSPC with *n = size when cap is too small. */
+int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t* n);
+/* Key = value config file (proj/tools/hww_main.cpp:20-92 key names). */
+int hwwg_load_config_file(const char* path, hwwg_run_config* cfg);
+/* Reference defaults (config.hpp:33-66). */
+void hwwg_default_config(hwwg_run_config* cfg);
+/* validate_config (proj/src/config.cpp:27-69): number of violations, messages
+ * joined with '\n' into buf. */
+int hwwg_validate_config(const hwwg_run_config* cfg, char* buf, uint64_t buf_len);
+
+/* ----------------------------------------------------- device components */
+/* hww::assemble_solve (losm.cpp:143-165) on the device, single CTA.
+ * phi_prev/F_* are I+2 long, J_prev I+1, q I (NULL = zero).  implicit != 0
+ * selects ClosureInput::implicit. */
+int hwwg_losm_assemble_solve(hwwg_ctx* ctx, int32_t cells, const double* edges,
+                             const hwwg_material* materials, const double* phi_prev,
+                             const double* J_prev, double J_L, double J_R, int32_t implicit,
+                             const double* F_now, double PL_now, double PR_now,
+                             const double* F_prev, double PL_prev, double PR_prev,
+                             double theta, double dt, const double* q, double* phi_out,
+                             double* J_out);
+/* hww::build_centers (ww.cpp:8-32); returns 1 on uniform fallback, 0 otherwise. */
+int hwwg_build_centers(hwwg_ctx* ctx, const double* phi, int32_t n, double eps_min,
+                       double rho, double* centers);
+/* hww::moving_average (filters.cpp:11-24). */
+int hwwg_moving_average(hwwg_ctx* ctx, const double* g, int32_t n, int32_t k, double* out);
+/* hww::uniform_comb (popctrl.cpp:7-42) with stream (seed, stream_id). */
+int hwwg_uniform_comb(hwwg_ctx* ctx, const hwwg_particle* bank, uint64_t n, uint64_t target,
+                      uint64_t seed, uint64_t stream_id, hwwg_particle* out,
+                      double* in_weight, double* out_weight);
+/* Bit-exact device replay of the host libm log (csrc/libm_log.h) on n inputs. */
+int hwwg_device_log(hwwg_ctx* ctx, const double* x, uint64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HWWG_H */

@@ -84,6 +84,11 @@ void orc_stream_u64(uint64_t seed, uint64_t id, uint64_t n, uint64_t* out) {
   for (uint64_t i = 0; i < n; ++i) out[i] = rng_u64(&r);
 }
 
+/* The reference's log, element-wise (std::log, transport.cpp:26). */
+void orc_log_array(const double* x, uint64_t n, double* out) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = log(x[i]);
+}
+
 /* --------------------------------------------------------------- mesh --- */
 typedef struct {
   const double* edges;
@@ -478,6 +483,8 @@ static void tallies_zero(owned_tallies* o, int I, int B) {
   o->t.histories_scored = o->t.grazing_discarded = 0;
 }
 
+uint32_t orc_max_stack_runs_seen = 0; /* diagnostics: deepest RLE stack so far */
+
 /* transport.cpp:209-237 (chunk > 0) or :194-207 (chunk <= 0). */
 static int run_segment_ctx(const seg_ctx* c, const orc_particle* src, uint64_t n,
                            uint64_t h_begin, int chunk, orc_tallies* t, orc_counters* k,
@@ -516,6 +523,7 @@ static int run_segment_ctx(const seg_ctx* c, const orc_particle* src, uint64_t n
     free(ct.block);
   }
   if (max_runs) *max_runs = st.max_n > *max_runs ? st.max_n : *max_runs;
+  if (st.max_n > orc_max_stack_runs_seen) orc_max_stack_runs_seen = st.max_n;
   free(st.r);
   return rc;
 }

@@ -103,6 +103,9 @@ void orc_stream_uniforms(uint64_t seed, uint64_t stream_id, uint64_t n, double* 
 void orc_stream_u64(uint64_t seed, uint64_t stream_id, uint64_t n, uint64_t* out);
 uint64_t orc_stream_id(uint64_t step, uint64_t history, uint64_t purpose);
 
+/* std::log as the reference calls it (transport.cpp:26) */
+void orc_log_array(const double* x, uint64_t n, double* out);
+
 /* mesh.cpp:26-50 */
 void orc_uniform_edges(double x_min, double x_max, int32_t cells, double* out);
 int32_t orc_locate(const double* edges, int32_t cells, double x);

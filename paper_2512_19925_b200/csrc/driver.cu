@@ -1,0 +1,582 @@
+// hwwg_driver: the reference's time-step loop (hww::run / hww::run_step,
+// proj/src/driver.cpp:99-342) with every per-step array resident on the GPU.
+//
+// One step = comb -> start-of-step LOSM windows -> u_ww+1 transport segments
+// with a single-CTA snapshot/filter/solve/centres kernel at each update
+// barrier -> finalize -> census sort.  The host only computes the update
+// thresholds (driver.cpp:170-177) and reads the step record back once, at the
+// end of the step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "capi_util.h"
+#include "common.cuh"
+#include "device_state.cuh"
+#include "driver_host.h"
+#include "engine.cuh"
+#include "low_order.cuh"
+#include "transport.cuh"
+
+using namespace hwwg;
+
+namespace {
+
+__global__ void k_bank_weight(const hwwg_particle* bank, uint64_t n, double* out) {
+  double w = 0.0;  // total_weight (particle.hpp:18-22), sequential
+  for (uint64_t i = 0; i < n; ++i) w += bank[i].w;
+  *out = w;
+}
+
+__global__ void k_active_from_fallback(int* flags) { flags[0] = flags[5] ? 0 : 1; }
+
+}  // namespace
+
+namespace hwwg {
+void set_active_from_fallback(int* flags, cudaStream_t s) {
+  k_active_from_fallback<<<1, 1, 0, s>>>(flags);
+  HWWG_CUDA(cudaGetLastError());
+}
+}  // namespace hwwg
+
+struct hwwg_driver {
+  hwwg_run_config cfg{};
+  hwwg_options opt{};
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DeviceProblem prob;
+  DeviceTallies tal;
+  HostTallies host_tal;
+  std::vector<double> layers;
+  int I = 0, B = 0;
+  uint64_t target = 0;
+  int next_step = 1;
+
+  // particle banks: `bank` holds the previous census (reference order)
+  DevBuf<hwwg_particle> bank, source;
+  uint64_t bank_n = 0;
+  // host_bank mode (e2e): the bank round-trips through pinned host memory
+  hwwg_particle* host_bank = nullptr;
+  uint64_t host_bank_n = 0, host_bank_cap = 0;
+  std::vector<cudaEvent_t> seg_ev;  // transport-kernel timing (2 per segment)
+  uint64_t launches = 0;
+  CensusStage stage;
+  DevBuf<double> comb_mem;  // scalars[4] + prefix
+  DevBuf<unsigned long long> counter;
+  DevBuf<DevError> err;
+
+  // low-order state
+  DevBuf<double> lo_mem;
+  DevBuf<int> lo_flags;
+  LowOrderState lo{};
+  DevBuf<double> centers_backup;
+  DevBuf<int> flags_backup;
+  // finalize outputs: two report buffers, current and previous
+  DevBuf<double> rep_mem[2];
+  int rep_cur = 0;
+  bool has_prev_report = false;
+
+  // host copies of the last StepRecord arrays
+  std::vector<double> h_phi_track, h_sigma, h_phi_census, h_current, h_closure, h_edge,
+      h_centers, h_hybrid;
+  std::vector<unsigned long long> h_tracks;
+  bool h_has_centers = false, h_has_hybrid = false;
+
+  ~hwwg_driver() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    for (auto e : seg_ev) cudaEventDestroy(e);
+    if (host_bank) cudaFreeHost(host_bank);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  double* rep(int which, int field) {  // field: 0 phi_track,1 sigma,2 phi_census,3 current,
+                                       // 4 closure,5 edge(I+1),6 scalars(8)
+    return rep_mem[which].p + (size_t)field * (I + 1);
+  }
+
+  bool hybrid() const { return cfg.mode >= 2; }
+};
+
+namespace {
+
+void init_driver(hwwg_driver* d) {
+  const hwwg_run_config& c = d->cfg;
+  d->I = c.cells;
+  d->B = c.batches;
+  d->target = c.target_population ? c.target_population : c.histories_per_step;
+  HWWG_CUDA(cudaSetDevice(d->opt.device));
+  HWWG_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  HWWG_CUDA(cudaEventCreate(&d->ev0));
+  HWWG_CUDA(cudaEventCreate(&d->ev1));
+  const int I = d->I;
+  // mesh and time grid (config.hpp:87-88; mesh.cpp:42-50; time_grid.hpp:22-29)
+  std::vector<double> edges(I + 1);
+  const double w = (c.x_max - c.x_min) / I;
+  for (int e = 0; e <= I; ++e) edges[e] = c.x_min + e * w;
+  edges[I] = c.x_max;
+  std::vector<hwwg_material> mats(I, hwwg_material{c.sigma_t, c.sigma_s, c.sigma_f, c.nu_f, c.speed});
+  std::string why;
+  if (!d->prob.set(edges.data(), I, mats.data(), d->stream, why)) throw ApiError(HWWG_EINVAL, why);
+  d->layers.resize(c.time_steps + 1);
+  const double dt = (c.t_end - 0.0) / c.time_steps;
+  for (int n = 0; n <= c.time_steps; ++n) d->layers[n] = 0.0 + n * dt;
+  d->layers[c.time_steps] = c.t_end;
+  d->tal.shape(I, d->B);
+
+  // low-order state
+  const int n = 2 * I + 3;
+  const size_t lo_words = (size_t)(I + 2) * 3 + (I + 1) + 2 + 3 * (size_t)I + 2 + 2 * (size_t)I +
+                          6 * (size_t)n + (I + 2);
+  d->lo_mem.reserve(lo_words);
+  HWWG_CUDA(cudaMemsetAsync(d->lo_mem.p, 0, lo_words * 8, d->stream));
+  double* q = d->lo_mem.p;
+  LowOrderState& s = d->lo;
+  s.phi_prev = q; q += I + 2;
+  s.J_prev = q; q += I + 1;
+  s.F_prev = q; q += I + 2;
+  s.PLPR_prev = q; q += 2;
+  s.rep_phi_census = nullptr;  // bound per step to the previous report
+  s.rep_current = nullptr;
+  s.rep_closure = nullptr;
+  s.rep_PLPR = nullptr;
+  s.centers = q; q += I;
+  s.phi_hybrid = q; q += I;
+  s.sys = q; q += 6 * (size_t)n;
+  s.F_now = q; q += I + 2;
+  d->lo_flags.reserve(8);
+  HWWG_CUDA(cudaMemsetAsync(d->lo_flags.p, 0, 8 * sizeof(int), d->stream));
+  s.flags = d->lo_flags.p;
+  d->centers_backup.reserve(I);
+  d->flags_backup.reserve(8);
+  for (auto& r : d->rep_mem) {
+    r.reserve((size_t)7 * (I + 1) + 8);
+    HWWG_CUDA(cudaMemsetAsync(r.p, 0, ((size_t)7 * (I + 1) + 8) * 8, d->stream));
+  }
+  d->counter.reserve(1);
+  d->err.reserve(1);
+  d->comb_mem.reserve(4);
+
+  // source sampling (driver.cpp:309-316) on the host: one sequential stream
+  std::vector<hwwg_particle> src(c.histories_per_step);
+  sample_pulse_source_host(c.seed, c.histories_per_step, c.x0,
+                           c.strength * (double)c.histories_per_step, 0.0, src.data());
+  d->bank.reserve(std::max<uint64_t>(src.size(), 1));
+  HWWG_CUDA(cudaMemcpyAsync(d->bank.p, src.data(), src.size() * sizeof(hwwg_particle),
+                            cudaMemcpyHostToDevice, d->stream));
+  d->bank_n = src.size();
+  if (c.host_bank) {
+    d->host_bank_cap = std::max<uint64_t>(src.size(), 1);
+    HWWG_CUDA(cudaMallocHost(&d->host_bank, d->host_bank_cap * sizeof(hwwg_particle)));
+    std::memcpy(d->host_bank, src.data(), src.size() * sizeof(hwwg_particle));
+    d->host_bank_n = src.size();
+  }
+  d->seg_ev.resize(32);
+  for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
+  d->stage.ensure(4 * d->target + 4096);
+  HWWG_CUDA(cudaStreamSynchronize(d->stream));
+}
+
+// One time step (driver.cpp:99-284).
+void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
+  const hwwg_run_config& c = d->cfg;
+  const int I = d->I, B = d->B;
+  const int step = d->next_step;
+  cudaStream_t s = d->stream;
+  std::memset(rec, 0, sizeof(*rec));
+  d->launches = 0;
+  rec->step = step;
+  rec->t_begin = d->layers[step - 1];
+  rec->t_end = d->layers[step];
+  const double dt = d->layers[step] - d->layers[step - 1];
+  const auto t0 = std::chrono::steady_clock::now();
+  HWWG_CUDA(cudaEventRecord(d->ev0, s));
+
+  if (c.host_bank) {  // e2e: the bank lives in host memory between steps
+    d->bank.reserve(std::max<uint64_t>(d->host_bank_n, 1));
+    HWWG_CUDA(cudaMemcpyAsync(d->bank.p, d->host_bank, d->host_bank_n * sizeof(hwwg_particle),
+                              cudaMemcpyHostToDevice, s));
+    d->bank_n = d->host_bank_n;
+    rec->h2d_bytes += d->host_bank_n * sizeof(hwwg_particle);
+  }
+
+  // ---- population control (driver.cpp:111-129)
+  const double bank_cap = c.comb_overflow_factor * (double)d->target;
+  const bool do_comb = c.comb_overflow_factor <= 1.0 || (double)d->bank_n > bank_cap;
+  uint64_t H;
+  if (do_comb) {
+    if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
+    d->source.reserve(d->target);
+    d->comb_mem.reserve(4 + d->bank_n);
+    CombArgs a{};
+    a.bank = d->bank.p;
+    a.n = d->bank_n;
+    a.target = d->target;
+    a.seed = c.seed;
+    a.stream = stream_id_host(step, 0, 3);
+    a.prefix = d->comb_mem.p + 4;
+    a.scalars = d->comb_mem.p;
+    a.out = d->source.p;
+    a.exact_out_weight = 1;
+    launch_comb(a, s);
+    d->launches += 2;
+    H = d->target;
+    rec->comb_in = d->bank_n;
+    rec->comb_out = d->target;
+  } else {
+    d->source.reserve(std::max<uint64_t>(d->bank_n, 1));
+    HWWG_CUDA(cudaMemcpyAsync(d->source.p, d->bank.p, d->bank_n * sizeof(hwwg_particle),
+                              cudaMemcpyDeviceToDevice, s));
+    k_bank_weight<<<1, 1, 0, s>>>(d->bank.p, d->bank_n, d->comb_mem.p);
+    ++d->launches;
+    H = d->bank_n;
+    rec->comb_in = rec->comb_out = d->bank_n;
+  }
+
+  // backup of the windows so an overflowing step can be replayed exactly
+  HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
+  HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+
+  // ---- thresholds (driver.cpp:170-177)
+  std::vector<uint64_t> thr;
+  if (d->hybrid() && c.u_ww > 0) {
+    for (int i = 0; i < c.n_fractions; ++i) {
+      const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)H);
+      if (h >= H) continue;
+      if (!thr.empty() && h <= thr.back()) continue;
+      thr.push_back(h);
+    }
+  }
+  rec->n_thresholds = (int)thr.size();
+  for (size_t i = 0; i < thr.size() && i < 8; ++i) rec->thresholds[i] = thr[i];
+
+  const double theta_eff = step == 1 ? 1.0 : c.theta;
+  const int ma_k = c.mode == 3 ? c.ma_base_k : 0;
+  const int prev = d->rep_cur ^ 1;  // report of the previous step lives in the other buffer
+
+  unsigned long long count = 0;
+  DevError derr{};
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if (attempt) {  // replay: restore the windows the step started from
+      HWWG_CUDA(cudaMemcpyAsync(d->lo.centers, d->centers_backup.p, I * 8, cudaMemcpyDeviceToDevice, s));
+      HWWG_CUDA(cudaMemcpyAsync(d->lo.flags, d->flags_backup.p, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    }
+    // per-step record flags: has_hybrid, updates_applied, failed, status
+    HWWG_CUDA(cudaMemsetAsync(d->lo.flags + 1, 0, 4 * sizeof(int), s));
+
+    // ---- windows (driver.cpp:136-167)
+    if (c.mode == 1) {  // lww: lagged track-length flux of the previous step
+      HWWG_CUDA(cudaMemsetAsync(d->lo.flags, 0, sizeof(int), s));
+      if (d->has_prev_report) {
+        launch_build_centers(d->rep(prev, 0), I, c.eps_min, c.rho, d->lo.centers,
+                             d->lo.flags + 5, s);
+        set_active_from_fallback(d->lo.flags, s);
+        d->launches += 2;
+      }
+    } else if (d->hybrid()) {
+      LowOrderArgs a{};
+      a.I = I;
+      a.edges = d->prob.view.edges;
+      a.cells = d->prob.view.cells;
+      a.theta = theta_eff;
+      a.dt = dt;
+      a.eps_min = c.eps_min;
+      a.rho = c.rho;
+      a.ma_k = ma_k;
+      a.mode = 0;
+      a.analytic = step == 1;
+      if (step == 1) {
+        const int cell = locate_host(d->prob.edges, c.x0);
+        a.pulse_cell = cell;
+        a.pulse_value = c.speed * c.strength / (d->prob.edges[cell + 1] - d->prob.edges[cell]);
+      }
+      a.s = d->lo;
+      a.s.rep_phi_census = d->rep(prev, 2);
+      a.s.rep_current = d->rep(prev, 3);
+      a.s.rep_closure = d->rep(prev, 4);
+      a.s.rep_PLPR = d->rep(prev, 6);
+      launch_low_order_update(a, s);
+      ++d->launches;
+    }
+
+    // ---- segments with window-update barriers (driver.cpp:181-219)
+    d->tal.zero(s);
+    HWWG_CUDA(cudaMemsetAsync(d->counter.p, 0, sizeof(unsigned long long), s));
+    HWWG_CUDA(cudaMemsetAsync(d->err.p, 0, sizeof(DevError), s));
+    ExactArgs ea{};
+    ea.mesh = d->prob.view;
+    ea.t_begin = rec->t_begin;
+    ea.t_end = rec->t_end;
+    ea.inv_dt = 1.0 / dt;
+    ea.seed = c.seed;
+    ea.step = (uint64_t)step;
+    ea.H = H;
+    ea.B = B;
+    const bool windows = c.mode != 0;
+    ea.centers = windows ? d->lo.centers : nullptr;
+    ea.active = windows ? d->lo.flags : nullptr;
+    ea.rho = c.rho;
+    ea.t = d->tal.p;
+    ea.census = d->stage.records.p;
+    ea.census_keys = d->stage.keys.p;
+    ea.census_count = d->counter.p;
+    ea.census_cap = d->stage.records.n;
+    ea.err = d->err.p;
+    uint64_t h_done = 0;
+    for (size_t u = 0; u <= thr.size(); ++u) {
+      const uint64_t h_stop = u < thr.size() ? thr[u] : H;
+      ea.src = d->source.p + h_done;
+      ea.n = h_stop - h_done;
+      ea.h_begin = h_done;
+      const int nseg = (int)u;
+      HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
+      launch_exact_segment(ea, s);
+      HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg + 1], s));
+      if (ea.n) ++d->launches;
+      h_done = h_stop;
+      if (u == thr.size()) break;
+      // partial_snapshot + implicit closure update (driver.cpp:206-217)
+      LowOrderArgs a{};
+      a.I = I;
+      a.edges = d->prob.view.edges;
+      a.cells = d->prob.view.cells;
+      a.theta = theta_eff;
+      a.dt = dt;
+      a.eps_min = c.eps_min;
+      a.rho = c.rho;
+      a.ma_k = ma_k;
+      a.mode = 1;
+      a.closure_tally = d->tal.p.census_closure;
+      a.bclosure_tally = d->tal.p.boundary_closure;
+      const double effective = (double)c.histories_per_step * (double)h_done / (double)H;
+      a.snapshot_inv_norm = 1.0 / effective;
+      a.s = d->lo;
+      launch_low_order_update(a, s);
+      ++d->launches;
+    }
+    HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
+    HWWG_CUDA(cudaMemcpyAsync(&derr, d->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
+    HWWG_CUDA(cudaStreamSynchronize(s));
+    if (derr.code || count <= ea.census_cap) break;
+    d->stage.ensure(count + count / 4 + 4096);
+  }
+  if (derr.code == HWWG_EINVAL)
+    throw ApiError(HWWG_EINVAL, "history " + std::to_string(derr.history) +
+                                    " starts outside the mesh or the time step");
+  if (derr.code == HWWG_ESTACK)
+    throw ApiError(HWWG_ESTACK, "history " + std::to_string(derr.history) +
+                                    " exceeded the daughter-stack run capacity");
+
+  // ---- finalize (driver.cpp:221-222)
+  FinalizeArgs f{};
+  f.I = I;
+  f.B = B;
+  f.t = d->tal.p;
+  f.histories = H;
+  f.normalization = (double)c.histories_per_step;
+  const int cur = d->rep_cur;
+  f.phi_track = d->rep(cur, 0);
+  f.sigma = d->rep(cur, 1);
+  f.phi_census = d->rep(cur, 2);
+  f.current = d->rep(cur, 3);
+  f.closure = d->rep(cur, 4);
+  f.edge = d->rep(cur, 5);
+  f.scalars = d->rep(cur, 6);
+  launch_finalize(f, s);
+  ++d->launches;
+
+  // ---- census -> next bank in reference order
+  d->bank.reserve(std::max<unsigned long long>(count, 1));
+  d->stage.sort_into(d->bank.p, count, ((unsigned long long)H << 24) | 0xffffffULL, s);
+  if (count) d->launches += 2;  // iota + gather (the radix sort itself is CUB's)
+  d->bank_n = count;
+  HWWG_CUDA(cudaEventRecord(d->ev1, s));
+
+  // ---- read the step record back (one sync)
+  std::vector<double> rep_h((size_t)7 * (I + 1) + 8);
+  HWWG_CUDA(cudaMemcpyAsync(rep_h.data(), d->rep_mem[cur].p, rep_h.size() * 8, cudaMemcpyDeviceToHost, s));
+  int flags[8];
+  HWWG_CUDA(cudaMemcpyAsync(flags, d->lo.flags, sizeof flags, cudaMemcpyDeviceToHost, s));
+  double comb_sc[4];
+  HWWG_CUDA(cudaMemcpyAsync(comb_sc, d->comb_mem.p, sizeof comb_sc, cudaMemcpyDeviceToHost, s));
+  d->h_centers.resize(I);
+  d->h_hybrid.resize(I);
+  HWWG_CUDA(cudaMemcpyAsync(d->h_centers.data(), d->lo.centers, I * 8, cudaMemcpyDeviceToHost, s));
+  HWWG_CUDA(cudaMemcpyAsync(d->h_hybrid.data(), d->lo.phi_hybrid, I * 8, cudaMemcpyDeviceToHost, s));
+  if (c.host_bank) {
+    if (count > d->host_bank_cap) {
+      HWWG_CUDA(cudaStreamSynchronize(s));
+      if (d->host_bank) HWWG_CUDA(cudaFreeHost(d->host_bank));
+      d->host_bank_cap = count + count / 4;
+      HWWG_CUDA(cudaMallocHost(&d->host_bank, d->host_bank_cap * sizeof(hwwg_particle)));
+    }
+    d->host_bank_n = count;
+    rec->d2h_bytes += count * sizeof(hwwg_particle);
+    HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, count * sizeof(hwwg_particle),
+                              cudaMemcpyDeviceToHost, s));
+  }
+  d->host_tal.fetch(d->tal, s);  // synchronises the stream
+  float ms = 0.f;
+  HWWG_CUDA(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
+  rec->device_ms = ms;
+  double tms = 0.0;
+  for (size_t u = 0; u <= thr.size(); ++u) {
+    float e = 0.f;
+    HWWG_CUDA(cudaEventElapsedTime(&e, d->seg_ev[2 * u], d->seg_ev[2 * u + 1]));
+    tms += e;
+    if (u < thr.size() ? thr[u] > (u ? thr[u - 1] : 0) : H > (thr.empty() ? 0 : thr.back()))
+      ++rec->transport_launches;
+  }
+  rec->transport_ms = tms;
+  rec->kernel_launches = d->launches;
+  rec->d2h_bytes += rep_h.size() * 8 + sizeof flags + sizeof comb_sc + 2 * (size_t)I * 8 +
+                    d->tal.words() * 8;
+
+  const HostTallies& h = d->host_tal;
+  if (h.ucount()[kHistoriesScored] != 0) { /* unused: histories counted on host */ }
+  const unsigned long long* u = h.ucount();
+  rec->counters.collisions = u[kCollisions];
+  rec->counters.splits = u[kSplits];
+  rec->counters.split_daughters = u[kSplitDaughters];
+  rec->counters.capped_splits = u[kCappedSplits];
+  rec->counters.roulette_kills = u[kRouletteKills];
+  rec->counters.roulette_survivals = u[kRouletteSurvivals];
+  rec->counters.census_count = u[kCensusCount];
+  rec->counters.event_cap_aborts = u[kEventCapAborts];
+  rec->counters.nan_aborts = u[kNanAborts];
+  rec->counters.leakage_weight = h.dcount()[0];
+  rec->counters.aborted_weight = h.dcount()[1];
+  d->h_tracks.assign(h.tracks(), h.tracks() + I);
+  uint64_t seg = 0;
+  for (int i = 0; i < I; ++i) seg += d->h_tracks[i];
+  rec->segments = seg;
+  rec->histories = H;
+  rec->census_size = count;
+  rec->comb_in_weight = comb_sc[0];
+  rec->comb_out_weight = do_comb ? comb_sc[3] : comb_sc[0];
+  auto field = [&](int f) { return rep_h.data() + (size_t)f * (I + 1); };
+  d->h_phi_track.assign(field(0), field(0) + I);
+  d->h_sigma.assign(field(1), field(1) + I);
+  d->h_phi_census.assign(field(2), field(2) + I);
+  d->h_current.assign(field(3), field(3) + I);
+  d->h_closure.assign(field(4), field(4) + I);
+  d->h_edge.assign(field(5), field(5) + I + 1);
+  const double* sc = field(6);
+  rec->boundary_closure_left = sc[0];
+  rec->boundary_closure_right = sc[1];
+  rec->census_weight = sc[2];
+  rec->census_weight_sigma = sc[3];
+  rec->sigma_valid = sc[4] != 0.0;
+  rec->has_windows = (c.mode != 0 && flags[0]) ? 1 : 0;
+  rec->has_hybrid = flags[1];
+  rec->updates_applied = flags[2];
+  rec->hybrid_solve_failed = flags[3];
+  d->h_has_centers = rec->has_windows;
+  d->h_has_hybrid = flags[1] != 0;
+  rec->tau = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // FOM without a reference (driver.cpp:272-275; metrics.cpp:34-55)
+  rec->fom_sigma_l2 = NAN;
+  if (rec->sigma_valid) {
+    const double tau = std::max(rec->tau, 1e-9);
+    double sum = 0.0;
+    for (int i = 0; i < I; ++i) {
+      if (d->h_sigma[i] == 0.0) continue;
+      const double fv = 1.0 / (tau * d->h_sigma[i] * d->h_sigma[i]);
+      sum += fv * fv * (d->prob.edges[i + 1] - d->prob.edges[i]);
+    }
+    rec->fom_sigma_l2 = std::sqrt(sum);
+  }
+  // state hand-off (driver.cpp:278-281)
+  d->has_prev_report = true;
+  d->rep_cur ^= 1;
+  ++d->next_step;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hwwg_driver** out) {
+  HWWG_API_BEGIN
+  if (!cfg || !out) return fail(HWWG_EINVAL, "NULL argument");
+  *out = nullptr;
+  char buf[1024];
+  if (hwwg_validate_config(cfg, buf, sizeof buf) != 0)
+    return fail(HWWG_EINVAL, std::string("invalid configuration:\n") + buf);
+  if (cfg->mode == 4) return fail(HWWG_EINVAL, "hww_fourier is out of scope for this engine");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(HWWG_ECUDA, "no CUDA device available");
+  }
+  auto d = new hwwg_driver();
+  d->cfg = *cfg;
+  if (opts) d->opt = *opts;
+  if (d->opt.rng_mode != HWWG_RNG_EXACT) {
+    delete d;
+    return fail(HWWG_EINVAL, "driver: only HWWG_RNG_EXACT is available in this build");
+  }
+  try {
+    init_driver(d);
+  } catch (...) {
+    delete d;
+    throw;
+  }
+  *out = d;
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+void hwwg_driver_destroy(hwwg_driver* d) { delete d; }
+
+int hwwg_driver_step(hwwg_driver* d, hwwg_step_record* rec) {
+  HWWG_API_BEGIN
+  if (!d || !rec) return fail(HWWG_EINVAL, "NULL argument");
+  if (d->next_step > d->cfg.time_steps) return fail(HWWG_ESTATE, "run already complete");
+  HWWG_CUDA(cudaSetDevice(d->opt.device));
+  driver_step(d, rec);
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma, double* phi_census,
+                       double* current_census, double* closure_census, double* edge_current,
+                       double* ww_centers, double* phi_hybrid, uint64_t* tracks_per_cell) {
+  HWWG_API_BEGIN
+  if (!d) return fail(HWWG_EINVAL, "NULL driver");
+  if (d->next_step == 1) return fail(HWWG_ESTATE, "no step has run yet");
+  auto cp = [](double* dst, const std::vector<double>& v) {
+    if (dst) std::memcpy(dst, v.data(), v.size() * 8);
+  };
+  cp(phi_track, d->h_phi_track);
+  cp(phi_sigma, d->h_sigma);
+  cp(phi_census, d->h_phi_census);
+  cp(current_census, d->h_current);
+  cp(closure_census, d->h_closure);
+  cp(edge_current, d->h_edge);
+  if (d->h_has_centers) cp(ww_centers, d->h_centers);
+  if (d->h_has_hybrid) cp(phi_hybrid, d->h_hybrid);
+  if (tracks_per_cell)
+    for (int i = 0; i < d->I; ++i) tracks_per_cell[i] = d->h_tracks[i];
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t* n) {
+  HWWG_API_BEGIN
+  if (!d || !n) return fail(HWWG_EINVAL, "NULL argument");
+  *n = d->bank_n;
+  if (!out || cap < d->bank_n) return fail(HWWG_ENOSPC, "bank buffer too small");
+  HWWG_CUDA(cudaMemcpyAsync(out, d->bank.p, d->bank_n * sizeof(hwwg_particle), cudaMemcpyDeviceToHost,
+                            d->stream));
+  HWWG_CUDA(cudaStreamSynchronize(d->stream));
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+}  // extern "C"

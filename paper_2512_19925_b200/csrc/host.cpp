@@ -1,0 +1,219 @@
+// Host pieces of the engine: RunConfig defaults/validation/key=value loader
+// (proj/include/hww/config.hpp:33-93, proj/src/config.cpp:27-69,
+// proj/tools/hww_main.cpp:20-92) and the driver's sequential helpers.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "capi_util.h"
+#include "driver_host.h"
+#include "hwwg.h"
+#include "rng.cuh"
+
+namespace hwwg {
+
+void sample_pulse_source_host(uint64_t seed, uint64_t histories, double x0, double total_weight,
+                              double t0, hwwg_particle* out) {
+  Xoshiro r;
+  r.seed(seed, stream_id(0, 0, kSource));
+  const double w = total_weight / (double)histories;
+  for (uint64_t h = 0; h < histories; ++h) out[h] = hwwg_particle{x0, r.uniform_pm1(), w, t0};
+}
+
+uint64_t stream_id_host(uint64_t step, uint64_t history, uint64_t purpose) {
+  return stream_id(step, history, purpose);
+}
+
+int locate_host(const std::vector<double>& e, double x) {
+  const int I = (int)e.size() - 1;
+  if (x < e.front() || x > e.back()) return -1;
+  if (x == e.back()) return I - 1;
+  const double w0 = e[1] - e[0];
+  bool uniform = true;
+  for (int c = 0; c < I; ++c)
+    if (!(std::abs((e[c + 1] - e[c]) - w0) <= 1e-12 * w0)) uniform = false;
+  if (uniform) {
+    int c = (int)((x - e.front()) / w0);
+    if (c >= I) c = I - 1;
+    if (x < e[c]) --c;
+    else if (x >= e[c + 1]) ++c;
+    return c;
+  }
+  int a = 0, b = I + 1;
+  while (a < b) {
+    const int m = (a + b) / 2;
+    if (e[m] > x) b = m;
+    else a = m + 1;
+  }
+  return a - 1;
+}
+
+}  // namespace hwwg
+
+using namespace hwwg;
+
+extern "C" {
+
+void hwwg_default_config(hwwg_run_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->mode = 2;  // hww
+  c->histories_per_step = 10000;
+  c->theta = 0.5;
+  c->rho = 1.25;
+  c->eps_min = 1e-3;
+  c->u_ww = 3;
+  c->n_fractions = 3;
+  c->fractions[0] = 0.25;
+  c->fractions[1] = 0.5;
+  c->fractions[2] = 0.75;
+  c->ma_base_k = 3;
+  c->fourier_cutoff = 30;
+  c->batches = 20;
+  c->seed = 1;
+  c->target_population = 0;
+  c->comb_overflow_factor = 1.0;
+  c->x0 = 0.0;
+  c->t0 = 0.0;
+  c->strength = 1.0;
+  c->sigma_t = 1.0;
+  c->sigma_s = 1.0 / 3.0;
+  c->sigma_f = 1.0 / 3.0;
+  c->nu_f = 2.3;
+  c->speed = 1.0;
+  c->x_min = -20.5;
+  c->x_max = 20.5;
+  c->cells = 201;
+  c->t_end = 20.0;
+  c->time_steps = 20;
+}
+
+int hwwg_validate_config(const hwwg_run_config* c, char* buf, uint64_t buf_len) {
+  std::vector<std::string> v;
+  // Material::validate (material.hpp:20-32)
+  if (!(c->sigma_t > 0)) v.push_back("sigma_t must be > 0");
+  if (c->sigma_s < 0 || c->sigma_s > c->sigma_t) v.push_back("sigma_s must lie in [0, sigma_t]");
+  if (c->sigma_f < 0 || c->sigma_f > c->sigma_t) v.push_back("sigma_f must lie in [0, sigma_t]");
+  if (c->sigma_s + c->sigma_f > c->sigma_t) v.push_back("sigma_s + sigma_f must not exceed sigma_t");
+  if (c->nu_f < 0) v.push_back("nu_f must be >= 0");
+  if (!(c->speed > 0)) v.push_back("speed must be > 0");
+  // config.cpp:30-66
+  if (c->histories_per_step < 1) v.push_back("histories_per_step must be >= 1");
+  if (!(c->theta >= 0.5 && c->theta <= 1.0)) v.push_back("theta must lie in [1/2, 1]");
+  if (!(c->rho >= 1.0)) v.push_back("rho must be >= 1");
+  if (!(c->eps_min > 0.0 && c->eps_min < 1.0)) v.push_back("eps_min must lie in (0,1)");
+  if (c->u_ww < 0) v.push_back("u_ww must be >= 0");
+  if (c->mode < 0 || c->mode > 4) v.push_back("unknown mode");
+  if (c->mode >= 2) {
+    if (c->n_fractions != c->u_ww) v.push_back("update_fractions count must equal u_ww");
+    double prev = 0.0;
+    for (int i = 0; i < c->n_fractions && i < 8; ++i) {
+      const double f = c->fractions[i];
+      if (!(f > 0.0 && f < 1.0)) {
+        v.push_back("update fractions must lie in (0,1)");
+        break;
+      }
+      if (!(f > prev)) {
+        v.push_back("update fractions must increase");
+        break;
+      }
+      prev = f;
+    }
+  }
+  if (c->n_fractions < 0 || c->n_fractions > 8) v.push_back("at most 8 update fractions");
+  if (c->mode == 3 && c->ma_base_k < 0) v.push_back("ma_base_k must be >= 0");
+  if (c->mode == 4 && c->fourier_cutoff < 0) v.push_back("fourier_cutoff must be >= 0");
+  if (c->batches < 2) v.push_back("batches must be >= 2");
+  if (!(c->x_min < c->x_max)) v.push_back("x_min must be < x_max");
+  if (c->cells < 1) v.push_back("cells must be >= 1");
+  if (!(c->t_end > 0.0)) v.push_back("t_end must be > 0");
+  if (c->time_steps < 1) v.push_back("time_steps must be >= 1");
+  if (!(c->strength > 0.0)) v.push_back("source strength must be > 0");
+  if (c->x0 < c->x_min || c->x0 > c->x_max) v.push_back("source x0 must lie inside the mesh");
+  std::string joined;
+  for (size_t i = 0; i < v.size(); ++i) joined += (i ? "\n" : "") + v[i];
+  if (buf && buf_len) {
+    std::strncpy(buf, joined.c_str(), buf_len - 1);
+    buf[buf_len - 1] = 0;
+  }
+  return (int)v.size();
+}
+
+// Key = value file mirroring the RunConfig field names (hww_main.cpp:20-92).
+int hwwg_load_config_file(const char* path, hwwg_run_config* c) {
+  HWWG_API_BEGIN
+  std::ifstream in(path);
+  if (!in) return fail(HWWG_EINVAL, std::string("cannot open config file: ") + path);
+  std::string line;
+  int line_no = 0;
+  auto trim = [](const std::string& s) {
+    const auto b = s.find_first_not_of(" \t\r");
+    const auto e = s.find_last_not_of(" \t\r");
+    return b == std::string::npos ? std::string() : s.substr(b, e - b + 1);
+  };
+  while (std::getline(in, line)) {
+    ++line_no;
+    const auto hash = line.find('#');
+    if (hash != std::string::npos) line = line.substr(0, hash);
+    const auto eq = line.find('=');
+    if (eq == std::string::npos) {
+      if (line.find_first_not_of(" \t\r") != std::string::npos)
+        return fail(HWWG_EINVAL, "line " + std::to_string(line_no) + ": expected key = value");
+      continue;
+    }
+    const std::string key = trim(line.substr(0, eq));
+    const std::string val = trim(line.substr(eq + 1));
+    try {
+      if (key == "mode") {
+        static const char* names[] = {"analog", "lww", "hww", "hww_ma", "hww_fourier"};
+        int m = -1;
+        for (int i = 0; i < 5; ++i)
+          if (val == names[i]) m = i;
+        if (m < 0) throw std::invalid_argument("unknown mode '" + val + "'");
+        c->mode = m;
+      } else if (key == "histories_per_step") c->histories_per_step = std::stoull(val);
+      else if (key == "theta") c->theta = std::stod(val);
+      else if (key == "rho") c->rho = std::stod(val);
+      else if (key == "eps_min") c->eps_min = std::stod(val);
+      else if (key == "u_ww") c->u_ww = std::stoi(val);
+      else if (key == "update_fractions") {
+        c->n_fractions = 0;
+        std::stringstream ss(val);
+        std::string tok;
+        while (std::getline(ss, tok, ',')) {
+          if (c->n_fractions == 8) throw std::invalid_argument("at most 8 update fractions");
+          c->fractions[c->n_fractions++] = std::stod(tok);
+        }
+      } else if (key == "ma_base_k") c->ma_base_k = std::stoi(val);
+      else if (key == "fourier_cutoff") c->fourier_cutoff = std::stoi(val);
+      else if (key == "batches") c->batches = std::stoi(val);
+      else if (key == "seed") c->seed = std::stoull(val);
+      else if (key == "target_population") c->target_population = std::stoull(val);
+      else if (key == "comb_overflow_factor") c->comb_overflow_factor = std::stod(val);
+      else if (key == "source_x0") c->x0 = std::stod(val);
+      else if (key == "source_strength") c->strength = std::stod(val);
+      else if (key == "sigma_t") c->sigma_t = std::stod(val);
+      else if (key == "sigma_s") c->sigma_s = std::stod(val);
+      else if (key == "sigma_f") c->sigma_f = std::stod(val);
+      else if (key == "nu_f") c->nu_f = std::stod(val);
+      else if (key == "speed") c->speed = std::stod(val);
+      else if (key == "x_min") c->x_min = std::stod(val);
+      else if (key == "x_max") c->x_max = std::stod(val);
+      else if (key == "cells") c->cells = std::stoi(val);
+      else if (key == "t_end") c->t_end = std::stod(val);
+      else if (key == "time_steps") c->time_steps = std::stoi(val);
+      else if (key == "threads") c->threads = std::stoi(val);
+      else if (key == "reference" || key == "out_dir") { /* host tooling keys: accepted */ }
+      else throw std::invalid_argument("unknown key '" + key + "'");
+    } catch (const std::exception& e) {
+      return fail(HWWG_EINVAL, "line " + std::to_string(line_no) + ": " + e.what());
+    }
+  }
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+}  // extern "C"

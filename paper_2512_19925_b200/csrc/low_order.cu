@@ -1,0 +1,536 @@
+// Device low-order pipeline, finalize and comb (see low_order.cuh).
+//
+// Single-CTA kernels: the per-update work is O(I) with I <= 4000, far below one
+// wave, so one CTA that keeps every intermediate in L1/L2 (and the system in
+// shared memory when it fits) beats any multi-kernel split, and there is no
+// host round-trip between snapshot, filter, solve and centres.
+//
+// Parity: compiled with -fmad=false; assembly follows losm.cpp:68-139 term by
+// term, the pivoted elimination follows banded.cpp:8-38 on one thread (the
+// recurrence is serial), the moving average sums l = -k..k in order and
+// divides once (filters.cpp:11-24).
+#include <cfloat>
+
+#include "common.cuh"
+#include "libm_log.h"
+#include "low_order.cuh"
+#include "rng.cuh"
+
+namespace hwwg {
+
+namespace {
+
+constexpr int kCtaThreads = 512;
+
+__device__ __forceinline__ double ghost_width(const double* edges, int I, int i) {
+  return (i <= 0 || i >= I + 1) ? 0.0 : edges[i] - edges[i - 1];  // mesh.hpp:30-33
+}
+
+__device__ __forceinline__ double removal_of(const CellInfo& c) {
+  return c.sigma_t - c.sigma_s - c.nu_f * c.sigma_f;  // material.hpp:15
+}
+
+// losm.cpp:68-139: rows of the interleaved (phi_0, J_0, ..., J_I, phi_I+1) system.
+__device__ void assemble_rows(int I, const double* edges, const CellInfo* cells,
+                              const double* phi_prev, const double* J_prev, double J_L,
+                              double J_R, const double* Fs, double PLs, double PRs,
+                              const double* F_prev, double theta, double dt, const double* q,
+                              double* lo, double* di, double* up, double* rh) {
+  const int n = 2 * I + 3;
+  for (int m = threadIdx.x; m < n; m += blockDim.x) {
+    double l = 0.0, d = 0.0, u = 0.0, r = 0.0;
+    if (m == 0) {  // left boundary: J_0 + phi_0/2 = 2 J_L + P_L
+      d = 0.5;
+      u = 1.0;
+      r = 2.0 * J_L + PLs;
+    } else if (m == n - 1) {  // right boundary: J_I - phi_I+1/2 = 2 J_R - P_R
+      l = 1.0;
+      d = -0.5;
+      r = 2.0 * J_R - PRs;
+    } else if ((m & 1) == 0) {  // balance over cell i
+      const int i = m >> 1;
+      const double dx = ghost_width(edges, I, i);
+      const CellInfo c = cells[i - 1];
+      const double tau = dx / (c.speed * dt);
+      const double rem = removal_of(c);
+      const double qi = q ? q[i - 1] : 0.0;
+      l = -theta;
+      d = tau + theta * rem * dx;
+      u = theta;
+      r = tau * phi_prev[i] + theta * qi +
+          (theta - 1.0) * (J_prev[i] - J_prev[i - 1] + rem * dx * phi_prev[i] - qi);
+    } else {  // first moment over the half cells around edge i
+      const int i = (m - 1) >> 1;
+      const double dx_l = ghost_width(edges, I, i);
+      const double dx_r = ghost_width(edges, I, i + 1);
+      const double dx_hat = 0.5 * (dx_r + dx_l);
+      double num_sig = 0.0, num_vel = 0.0;
+      if (dx_l > 0.0) {
+        num_sig += cells[i - 1].sigma_t * dx_l;
+        num_vel += dx_l / cells[i - 1].speed;
+      }
+      if (dx_r > 0.0) {
+        num_sig += cells[i].sigma_t * dx_r;
+        num_vel += dx_r / cells[i].speed;
+      }
+      const double sig_hat = num_sig / (dx_l + dx_r);
+      const double inv_speed_hat = num_vel / (dx_l + dx_r);
+      const double tau = dx_hat * inv_speed_hat / dt;
+      l = -theta / 3.0;
+      d = tau + theta * sig_hat * dx_hat;
+      u = theta / 3.0;
+      r = tau * J_prev[i] + theta * (Fs[i + 1] - Fs[i]) +
+          (theta - 1.0) * ((phi_prev[i + 1] - phi_prev[i]) / 3.0 + sig_hat * dx_hat * J_prev[i] -
+                           (F_prev[i + 1] - F_prev[i]));
+    }
+    lo[m] = l;
+    di[m] = d;
+    up[m] = u;
+    rh[m] = r;
+  }
+}
+
+// banded.cpp:8-38 on one thread. Returns 0, or 1 + pivot row when singular.
+__device__ int solve_pivoted_serial(int n, double* a, double* b, double* c, double* r,
+                                    double* fill, double* x) {
+  for (int k = 0; k < n; ++k) fill[k] = 0.0;
+  for (int k = 0; k + 1 < n; ++k) {
+    if (fabs(a[k + 1]) > fabs(b[k])) {
+      double t;
+      t = b[k]; b[k] = a[k + 1]; a[k + 1] = t;
+      t = c[k]; c[k] = b[k + 1]; b[k + 1] = t;
+      if (k + 2 < n) { t = fill[k]; fill[k] = c[k + 1]; c[k + 1] = t; }
+      t = r[k]; r[k] = r[k + 1]; r[k + 1] = t;
+    }
+    if (b[k] == 0.0) return 1 + k;
+    const double m = a[k + 1] / b[k];
+    a[k + 1] = 0.0;
+    b[k + 1] -= m * c[k];
+    if (k + 2 < n) c[k + 1] -= m * fill[k];
+    r[k + 1] -= m * r[k];
+  }
+  if (b[n - 1] == 0.0) return n;
+  x[n - 1] = r[n - 1] / b[n - 1];
+  if (n >= 2) x[n - 2] = (r[n - 2] - c[n - 2] * x[n - 1]) / b[n - 2];
+  for (int k = n - 3; k >= 0; --k) x[k] = (r[k] - c[k] * x[k + 1] - fill[k] * x[k + 2]) / b[k];
+  return 0;
+}
+
+// Block max of per-thread partial maxima. The partials start at 0.0 and only
+// grow through '>' (ww.cpp:13-15), so NaN never enters and max is exact.
+__device__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// ww.cpp:8-32 over the block; returns true on uniform fallback.
+__device__ bool build_centers_cta(const double* phi, int n, double eps_min, double* centers,
+                                  double* red) {
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (phi[i] > mx) mx = phi[i];
+  mx = block_max(mx, red);
+  const bool fallback = !(mx > 0.0) || !isfinite(mx);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (fallback) {
+      centers[i] = 1.0;
+    } else {
+      const double cl = phi[i] > 0.0 ? phi[i] : 0.0;
+      centers[i] = (cl / mx) * (1.0 - eps_min) + eps_min;
+    }
+  }
+  __syncthreads();
+  return fallback;
+}
+
+// filters.cpp:11-24, out-of-place over the block.
+__device__ void moving_average_cta(const double* g, int M, int k, double* out) {
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    int km = k;
+    if (m < km) km = m;
+    if (M - 1 - m < km) km = M - 1 - m;
+    double sum = 0.0;
+    for (int l = -km; l <= km; ++l) sum += g[m + l];
+    out[m] = sum / (2 * km + 1);
+  }
+  __syncthreads();
+}
+
+// In-place MA via scratch: filter_cell_avg_with_boundary (interior) or filter_edge (all).
+__device__ void filter_inplace(double* g, int len, int interior, int k, double* tmp) {
+  if (k <= 0) return;
+  if (interior) {
+    if (len <= 2) return;
+    moving_average_cta(g + 1, len - 2, k, tmp);
+    for (int i = threadIdx.x; i < len - 2; i += blockDim.x) g[i + 1] = tmp[i];
+  } else {
+    moving_average_cta(g, len, k, tmp);
+    for (int i = threadIdx.x; i < len; i += blockDim.x) g[i] = tmp[i];
+  }
+  __syncthreads();
+}
+
+__device__ bool all_finite(const double* v, int n) {
+  bool bad = false;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (!isfinite(v[i])) bad = true;
+  return __syncthreads_or(bad ? 1 : 0) == 0;
+}
+
+// driver.cpp:72-95 hybrid_windows + ww.cpp build_centers, given prepared
+// inputs. Solves into the sys scratch; on failure keeps the previous windows.
+__device__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double PLs, double PRs,
+                                 bool implicit, double* red) {
+  const LowOrderState& s = a.s;
+  const int I = a.I, n = 2 * I + 3;
+  double* lo = s.sys;
+  double* di = lo + n;
+  double* up = di + n;
+  double* rh = up + n;
+  double* fill = rh + n;
+  double* x = fill + n;
+  __shared__ int status;
+  // check_inputs (losm.cpp:43-66): finite previous state and lagged closures
+  const bool ok_in = all_finite(s.phi_prev, I + 2) && all_finite(s.J_prev, I + 1) &&
+                     all_finite(s.F_prev, I + 2);
+  if (ok_in) {
+    assemble_rows(I, a.edges, a.cells, s.phi_prev, s.J_prev, 0.0, 0.0, Fs, PLs, PRs, s.F_prev,
+                  a.theta, a.dt, nullptr, lo, di, up, rh);
+    __syncthreads();
+    if (threadIdx.x == 0) status = solve_pivoted_serial(n, lo, di, up, rh, fill, x) ? 2 : 0;
+  } else if (threadIdx.x == 0) {
+    status = 1;
+  }
+  __syncthreads();
+  const int st = status;
+  if (st == 0) {
+    for (int i = threadIdx.x; i < I; i += blockDim.x) s.phi_hybrid[i] = x[2 * (i + 1)];
+    __syncthreads();
+    build_centers_cta(s.phi_hybrid, I, a.eps_min, s.centers, red);
+    if (threadIdx.x == 0) {
+      s.flags[0] = 1;
+      s.flags[1] = 1;
+      if (implicit) ++s.flags[2];
+    }
+  } else {
+    const bool was_active = s.flags[0] != 0;
+    __syncthreads();
+    if (!was_active)
+      for (int i = threadIdx.x; i < I; i += blockDim.x) s.centers[i] = 1.0;
+    if (threadIdx.x == 0) {
+      s.flags[0] = 1;
+      s.flags[3] = 1;
+    }
+  }
+  if (threadIdx.x == 0) s.flags[4] = st;
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_low_order_update(LowOrderArgs a) {
+  __shared__ double red[32];
+  const LowOrderState& s = a.s;
+  const int I = a.I;
+  double* tmp = s.sys;  // MA scratch (before assembly)
+  if (a.mode == 0) {
+    if (a.analytic) {  // analytic_pulse_inputs, driver.cpp:51-61
+      for (int i = threadIdx.x; i < I + 2; i += blockDim.x) {
+        s.phi_prev[i] = (i == a.pulse_cell + 1) ? a.pulse_value : 0.0;
+        s.F_prev[i] = 0.0;
+      }
+      for (int i = threadIdx.x; i < I + 1; i += blockDim.x) s.J_prev[i] = 0.0;
+      if (threadIdx.x == 0) {
+        s.PLPR_prev[0] = 0.0;
+        s.PLPR_prev[1] = 0.0;
+      }
+    } else {  // hybrid_inputs_from_report, driver.cpp:41-49; losm.cpp:12-32
+      for (int i = threadIdx.x; i < I + 2; i += blockDim.x) {
+        const int j = i == 0 ? 0 : (i == I + 1 ? I - 1 : i - 1);
+        s.phi_prev[i] = s.rep_phi_census[j];
+        s.F_prev[i] = s.rep_closure[j];
+      }
+      for (int e = threadIdx.x; e < I + 1; e += blockDim.x) {
+        double v;
+        if (e == 0) v = s.rep_current[0];
+        else if (e == I) v = s.rep_current[I - 1];
+        else {
+          const double xl = 0.5 * (a.edges[e - 1] + a.edges[e]);
+          const double xr = 0.5 * (a.edges[e] + a.edges[e + 1]);
+          const double t = (a.edges[e] - xl) / (xr - xl);
+          v = (1.0 - t) * s.rep_current[e - 1] + t * s.rep_current[e];
+        }
+        s.J_prev[e] = v;
+      }
+      if (threadIdx.x == 0) {
+        s.PLPR_prev[0] = s.rep_PLPR[0];
+        s.PLPR_prev[1] = s.rep_PLPR[1];
+      }
+    }
+    __syncthreads();
+    // apply_filter_pipeline(nullptr, F_prev, phi_prev, J_prev), filters.cpp:76-84
+    filter_inplace(s.F_prev, I + 2, 1, a.ma_k, tmp);
+    filter_inplace(s.phi_prev, I + 2, 1, a.ma_k, tmp);
+    filter_inplace(s.J_prev, I + 1, 0, a.ma_k, tmp);
+    solve_and_center(a, s.F_prev, s.PLPR_prev[0], s.PLPR_prev[1], false, red);
+  } else {
+    // partial_snapshot (tally.cpp:116-128) -> with_boundary_extrapolated -> filter
+    double* F = s.F_now;
+    for (int i = threadIdx.x; i < I + 2; i += blockDim.x) {
+      const int j = i == 0 ? 0 : (i == I + 1 ? I - 1 : i - 1);
+      F[i] = a.closure_tally[j] * a.snapshot_inv_norm;
+    }
+    __syncthreads();
+    filter_inplace(F, I + 2, 1, a.ma_k, tmp);
+    const double PL = a.bclosure_tally[0] * a.snapshot_inv_norm;
+    const double PR = a.bclosure_tally[1] * a.snapshot_inv_norm;
+    solve_and_center(a, F, PL, PR, true, red);
+  }
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_raw_losm(RawLosmArgs a) {
+  const int I = a.I, n = 2 * I + 3;
+  double* lo = a.sys;
+  double* di = lo + n;
+  double* up = di + n;
+  double* rh = up + n;
+  double* fill = rh + n;
+  double* x = fill + n;
+  const bool ok = all_finite(a.phi_prev, I + 2) && all_finite(a.J_prev, I + 1) &&
+                  all_finite(a.F_prev, I + 2);
+  if (!ok) {
+    if (threadIdx.x == 0) *a.status = 1;
+    return;
+  }
+  assemble_rows(I, a.edges, a.cells, a.phi_prev, a.J_prev, a.J_L, a.J_R,
+                a.implicit ? a.F_now : a.F_prev, a.implicit ? a.PL_now : a.PL_prev,
+                a.implicit ? a.PR_now : a.PR_prev, a.F_prev, a.theta, a.dt, a.q, lo, di, up, rh);
+  __syncthreads();
+  __shared__ int st;
+  if (threadIdx.x == 0) st = solve_pivoted_serial(n, lo, di, up, rh, fill, x);
+  __syncthreads();
+  if (st) {
+    if (threadIdx.x == 0) *a.status = 1 + st;
+    return;
+  }
+  for (int i = threadIdx.x; i <= I + 1; i += blockDim.x) a.phi_out[i] = x[2 * i];
+  for (int i = threadIdx.x; i <= I; i += blockDim.x) a.J_out[i] = x[2 * i + 1];
+  if (threadIdx.x == 0) *a.status = 0;
+}
+
+// tally.cpp:43-48
+__device__ __forceinline__ uint64_t batch_size(uint64_t H, int B, int b) {
+  const uint64_t lo = ((uint64_t)b * H + (uint64_t)B - 1) / (uint64_t)B;
+  const uint64_t hi = ((uint64_t)(b + 1) * H + (uint64_t)B - 1) / (uint64_t)B;
+  return hi - lo;
+}
+
+// tally.cpp:68-114
+__global__ void k_finalize(FinalizeArgs a) {
+  const int I = a.I, B = a.B;
+  const double inv_h = 1.0 / a.normalization;
+  const bool sigma_valid = B >= 2 && a.histories >= (uint64_t)B;
+  const double scale = (double)a.histories / a.normalization;
+  const double ih = 1.0 / (double)a.histories;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < I) {
+    a.phi_track[i] = a.t.track_flux[i] * inv_h;
+    a.phi_census[i] = a.t.census_phi[i] * inv_h;
+    a.current[i] = a.t.census_current[i] * inv_h;
+    a.closure[i] = a.t.census_closure[i] * inv_h;
+    double sg = 0.0;
+    if (sigma_valid) {
+      const double mean = a.t.track_flux[i] * ih;
+      double ss = 0.0;
+      for (int b = 0; b < B; ++b) {
+        const uint64_t nb = batch_size(a.histories, B, b);
+        const double inv_nb = nb ? 1.0 / (double)nb : 0.0;
+        const double bm = a.t.track_flux_batch[(size_t)b * I + i] * inv_nb;
+        const double d = bm - mean;
+        ss += d * d;
+      }
+      sg = scale * sqrt(ss / ((double)B * (B - 1)));
+    }
+    a.sigma[i] = sg;
+  }
+  if (i <= I) a.edge[i] = a.t.edge_current[i] * inv_h;
+  if (i == 0) {
+    a.scalars[0] = a.t.boundary_closure[0] * inv_h;
+    a.scalars[1] = a.t.boundary_closure[1] * inv_h;
+    double cw = 0.0;
+    for (int b = 0; b < B; ++b) cw += a.t.census_weight_batch[b];
+    a.scalars[2] = cw * inv_h;
+    double cws = 0.0;
+    if (sigma_valid) {
+      const double wmean = cw * ih;
+      double ss = 0.0;
+      for (int b = 0; b < B; ++b) {
+        const uint64_t nb = batch_size(a.histories, B, b);
+        const double inv_nb = nb ? 1.0 / (double)nb : 0.0;
+        const double bm = a.t.census_weight_batch[b] * inv_nb;
+        const double d = bm - wmean;
+        ss += d * d;
+      }
+      cws = scale * sqrt(ss / ((double)B * (B - 1)));
+    }
+    a.scalars[3] = cws;
+    a.scalars[4] = sigma_valid ? 1.0 : 0.0;
+  }
+}
+
+// popctrl.cpp:15-30 — the cumulative-weight walk, sequential in bank order.
+// One thread carries the fp64 running sum; the other 255 threads of the CTA
+// stage the next weights into shared memory so the serial chain never waits
+// on HBM.
+__global__ void __launch_bounds__(256) k_comb_prefix(CombArgs a) {
+  constexpr int kTile = 2048;
+  __shared__ double w[2][kTile];
+  double cum = 0.0;
+  const uint64_t tiles = (a.n + kTile - 1) / kTile;
+  auto load = [&](uint64_t tile, int buf) {
+    const uint64_t base = tile * kTile;
+    for (int j = threadIdx.x; j < kTile; j += blockDim.x) {
+      const uint64_t k = base + j;
+      w[buf][j] = k < a.n ? a.bank[k].w : 0.0;
+    }
+  };
+  if (tiles) load(0, 0);
+  __syncthreads();
+  for (uint64_t tl = 0; tl < tiles; ++tl) {
+    const int buf = (int)(tl & 1);
+    if (threadIdx.x == 0) {
+      const uint64_t base = tl * kTile;
+      const uint64_t m = a.n - base < (uint64_t)kTile ? a.n - base : (uint64_t)kTile;
+      for (uint64_t j = 0; j < m; ++j) {
+        cum += w[buf][j];
+        a.prefix[base + j] = cum;
+      }
+    } else if (tl + 1 < tiles) {
+      // threads 1.. stage the next tile
+      const uint64_t base = (tl + 1) * kTile;
+      for (int j = threadIdx.x - 1; j < kTile; j += blockDim.x - 1) {
+        const uint64_t k = base + j;
+        w[buf ^ 1][j] = k < a.n ? a.bank[k].w : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // total_weight(bank) (particle.hpp:18-22) is the same sequential sum
+    const double W = cum;
+    const double spacing = W / (double)a.target;
+    Xoshiro r;
+    r.seed(a.seed, a.stream);
+    const double offset = r.uniform() * spacing;
+    a.scalars[0] = W;
+    a.scalars[1] = spacing;
+    a.scalars[2] = offset;
+    if (a.exact_out_weight) {
+      double ow = 0.0;  // total_weight(result.bank), every tooth carries `spacing`
+      for (uint64_t k = 0; k < a.target; ++k) ow += spacing;
+      a.scalars[3] = ow;
+    } else {
+      a.scalars[3] = spacing * (double)a.target;
+    }
+  }
+}
+
+// Tooth k lands on the first particle whose cumulative weight exceeds
+// offset + k * spacing (the while loop of popctrl.cpp:24-29 is exactly this
+// because teeth and the prefix are both non-decreasing); stranded teeth copy
+// bank.back() (popctrl.cpp:31-37).
+__global__ void k_comb_teeth(CombArgs a) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= a.target) return;
+  const double spacing = a.scalars[1];
+  const double T = a.scalars[2] + (double)k * spacing;
+  uint64_t lo = 0, hi = a.n;  // first index with T < prefix[idx]
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (T < a.prefix[mid]) hi = mid;
+    else lo = mid + 1;
+  }
+  const uint64_t src = lo < a.n ? lo : a.n - 1;
+  const double2* s = reinterpret_cast<const double2*>(a.bank) + 2 * src;
+  double2* d = reinterpret_cast<double2*>(a.out) + 2 * k;
+  const double2 s1 = s[1];
+  d[0] = s[0];
+  d[1] = make_double2(spacing, s1.y);
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_build_centers(const double* phi, int n,
+                                                               double eps_min, double* centers,
+                                                               int* fallback) {
+  __shared__ double red[32];
+  const bool fb = build_centers_cta(phi, n, eps_min, centers, red);
+  if (threadIdx.x == 0) *fallback = fb ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_moving_average(const double* g, int n, int k,
+                                                                double* out) {
+  if (k == 0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = g[i];
+    return;
+  }
+  moving_average_cta(g, n, k, out);
+}
+
+__global__ void k_device_log(const double* x, uint64_t n, double* out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = hwwg_libm_log(x[i]);
+}
+
+}  // namespace
+
+void launch_low_order_update(const LowOrderArgs& a, cudaStream_t st) {
+  k_low_order_update<<<1, kCtaThreads, 0, st>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
+  const int blocks = (a.I + 1 + 255) / 256;
+  k_finalize<<<blocks, 256, 0, st>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_comb(const CombArgs& a, cudaStream_t st) {
+  k_comb_prefix<<<1, 256, 0, st>>>(a);
+  const unsigned blocks = (unsigned)((a.target + 255) / 256);
+  k_comb_teeth<<<blocks, 256, 0, st>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_build_centers(const double* phi, int n, double eps_min, double rho, double* centers,
+                          int* fallback, cudaStream_t st) {
+  (void)rho;
+  k_build_centers<<<1, kCtaThreads, 0, st>>>(phi, n, eps_min, centers, fallback);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_moving_average(const double* g, int n, int k, double* out, cudaStream_t st) {
+  k_moving_average<<<1, kCtaThreads, 0, st>>>(g, n, k, out);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_raw_losm(const RawLosmArgs& a, cudaStream_t st) {
+  k_raw_losm<<<1, kCtaThreads, 0, st>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_device_log(const double* x, uint64_t n, double* out, cudaStream_t st) {
+  if (!n) return;
+  k_device_log<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, out);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+}  // namespace hwwg

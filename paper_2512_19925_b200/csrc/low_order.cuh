@@ -1,0 +1,107 @@
+// Between-segment pipeline on the device:
+// partial snapshot -> boundary extrapolation -> moving-average filter ->
+// LOSM assembly -> tridiagonal solve -> weight-window centres, all in ONE
+// single-CTA kernel launch per window update, plus the step-end finalize and
+// the comb.  Compiled with -fmad=false: every value is bit-identical to the
+// reference given identical inputs (tests/test_gpu_components.py).
+#pragma once
+
+#include "common.cuh"
+
+namespace hwwg {
+
+// Persistent per-run low-order state on the device.
+struct LowOrderState {
+  // filtered HybridInputs of the current step (driver.hpp:15-21)
+  double* phi_prev;  // I+2
+  double* J_prev;    // I+1
+  double* F_prev;    // I+2
+  double* PLPR_prev; // 2
+  // previous step's report (census moments, tally.cpp means) feeding the next step
+  double* rep_phi_census;  // I
+  double* rep_current;     // I
+  double* rep_closure;     // I
+  double* rep_PLPR;        // 2
+  // windows (WeightWindowGrid) and the last hybrid solution
+  double* centers;    // I
+  double* phi_hybrid; // I
+  int* flags;         // [0] windows active, [1] has_hybrid, [2] updates_applied, [3] failed,
+                      // [4] last solve status (0 ok, 1 invalid, 2 singular)
+  // scratch for the n = 2I+3 system (lower, diag, upper, rhs, fill, x) and F_now
+  double* sys;   // 6 * (2I+3)
+  double* F_now; // I+2
+};
+
+struct LowOrderArgs {
+  int I;
+  const double* edges;
+  const CellInfo* cells;
+  double theta, dt;
+  double eps_min, rho;
+  int ma_k;  // moving-average half-width, 0 = no filter
+  // mode 0: start-of-step lagged solve; inputs from analytic pulse (step 1) or
+  //         from the previous report.  mode 1: mid-step implicit solve from the
+  //         partial snapshot of the live tallies.
+  int mode;
+  int analytic;        // mode 0: step 1 cold start
+  int pulse_cell;      // analytic: cell of the source point
+  double pulse_value;  // analytic: speed * strength / dx
+  const double* closure_tally;  // mode 1: census_closure accumulator (I)
+  const double* bclosure_tally; // mode 1: boundary closure accumulators (2)
+  double snapshot_inv_norm;     // mode 1: 1 / (H_cfg * h_done / H)
+  LowOrderState s;
+};
+
+void launch_low_order_update(const LowOrderArgs& a, cudaStream_t st);
+
+// tally.cpp:68-128 finalize on the device (one CTA per 256 cells).
+struct FinalizeArgs {
+  int I, B;
+  TallyPtrs t;
+  uint64_t histories;
+  double normalization;
+  // outputs (device)
+  double *phi_track, *sigma, *phi_census, *current, *closure, *edge;  // I / I+1
+  double* scalars;  // PL, PR, census_weight, census_weight_sigma, sigma_valid
+};
+void launch_finalize(const FinalizeArgs& a, cudaStream_t st);
+
+// popctrl.cpp:7-42 on the device.  Exact mode: the cumulative weight walk is
+// evaluated sequentially (the reference's fp64 summation order), teeth are
+// then placed in parallel by binary search over the exact prefix.
+struct CombArgs {
+  const hwwg_particle* bank;
+  uint64_t n;
+  uint64_t target;
+  uint64_t seed, stream;
+  double* prefix;    // n scratch
+  double* scalars;   // [0] W, [1] spacing, [2] offset, [3] output weight
+  hwwg_particle* out;
+  int exact_out_weight;
+};
+void launch_comb(const CombArgs& a, cudaStream_t st);
+
+// Component entry points used by the C ABI (hwwg_build_centers etc.).
+void launch_build_centers(const double* phi, int n, double eps_min, double rho,
+                          double* centers, int* fallback, cudaStream_t st);
+void launch_moving_average(const double* g, int n, int k, double* out, cudaStream_t st);
+struct RawLosmArgs {
+  int I;
+  const double* edges;
+  const CellInfo* cells;
+  const double *phi_prev, *J_prev;
+  double J_L, J_R;
+  int implicit;
+  const double* F_now;
+  double PL_now, PR_now;
+  const double* F_prev;
+  double PL_prev, PR_prev, theta, dt;
+  const double* q;  // may be null
+  double* sys;      // 6*(2I+3) scratch
+  double *phi_out, *J_out;
+  int* status;
+};
+void launch_raw_losm(const RawLosmArgs& a, cudaStream_t st);
+void launch_device_log(const double* x, uint64_t n, double* out, cudaStream_t st);
+
+}  // namespace hwwg

@@ -1,0 +1,456 @@
+"""Python mirror of the reference's public API for the history-loop path.
+
+Same names, argument meaning and error behaviour as the reference's C++
+(proj/include/hww/*.hpp), executed by the sm_100a engine through the C ABI:
+
+* ``run_segment_parallel(ctx, source, h_begin, ww, tallies, outcome)`` —
+  transport.hpp:117-120; accumulates into ``tallies``/``outcome``; raises
+  ``ValueError`` where the reference throws ``std::invalid_argument``.
+* ``RunConfig`` / ``Driver`` / ``run`` — config.hpp:33-66, driver.hpp:80-88.
+* ``assemble_solve``, ``build_centers``, ``moving_average``, ``uniform_comb`` —
+  losm.hpp:77-80, ww.hpp:34-35, filters.hpp:30, popctrl.hpp:22.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi as A
+from ._capi import PARTICLE_DT, RNG_EXACT, RNG_PHILOX, HwwgError
+
+MODES = ("analog", "lww", "hww", "hww_ma", "hww_fourier")
+
+
+def _raise(rc):
+    if rc < 0:
+        msg = A.lib().hwwg_last_error().decode()
+        if rc in (A.HWWG_EINVAL, A.HWWG_ESINGULAR):
+            raise ValueError(msg)
+        raise HwwgError(rc, msg)
+    return rc
+
+
+# ------------------------------------------------------------------ core types
+@dataclass
+class Material:
+    """hww::Material (material.hpp:9-18)."""
+    sigma_t: float = 1.0
+    sigma_s: float = 0.0
+    sigma_f: float = 0.0
+    nu_f: float = 0.0
+    speed: float = 1.0
+
+    def removal(self):
+        return self.sigma_t - self.sigma_s - self.nu_f * self.sigma_f
+
+
+class Mesh1D:
+    """hww::Mesh1D (mesh.hpp:12-58): strictly increasing edges."""
+
+    def __init__(self, edges):
+        e = np.ascontiguousarray(edges, np.float64)
+        if e.size < 2:
+            raise ValueError("mesh needs at least one cell")
+        if not np.all(e[1:] > e[:-1]):
+            raise ValueError("mesh edges must be strictly increasing")
+        self.edges = e
+
+    @staticmethod
+    def from_edges(edges):
+        return Mesh1D(edges)
+
+    def cells(self):
+        return self.edges.size - 1
+
+    def width(self, c):
+        return self.edges[c + 1] - self.edges[c]
+
+    def center(self, c):
+        return 0.5 * (self.edges[c] + self.edges[c + 1])
+
+
+def build_uniform_mesh(x_min, x_max, cells):
+    """mesh.cpp:42-50."""
+    if cells < 1:
+        raise ValueError("cell count must be positive")
+    if not x_min < x_max:
+        raise ValueError("x_min must be < x_max")
+    w = (x_max - x_min) / cells
+    e = x_min + np.arange(cells + 1) * w
+    e[-1] = x_max
+    return Mesh1D(e)
+
+
+def _materials_array(materials, cells):
+    if isinstance(materials, Material):
+        materials = [materials] * cells
+    if isinstance(materials, np.ndarray) and materials.dtype == A.MATERIAL_DT:
+        arr = np.ascontiguousarray(materials)
+    else:
+        rows = []
+        for m in materials:
+            if isinstance(m, Material):
+                rows.append((m.sigma_t, m.sigma_s, m.sigma_f, m.nu_f, m.speed))
+            else:
+                rows.append(tuple(float(v) for v in m))
+        arr = np.array(rows, dtype=A.MATERIAL_DT)
+    if arr.size != cells:
+        raise ValueError("materials must have one entry per cell")
+    return arr
+
+
+@dataclass
+class StepContext:
+    """hww::StepContext (transport.hpp:83-94)."""
+    mesh: Mesh1D
+    materials: object
+    t_begin: float = 0.0
+    t_end: float = 1.0
+    seed: int = 0
+    step_index: int = 1
+    histories_total: int = 0
+    batches: int = 1
+
+    def dt(self):
+        return self.t_end - self.t_begin
+
+
+@dataclass
+class WeightWindowGrid:
+    """hww::WeightWindowGrid (ww.hpp:13-27)."""
+    centers: np.ndarray
+    rho: float = 1.25
+    eps_min: float = 1e-3
+    uniform_fallback: bool = False
+
+    def window(self, cell):
+        c = self.centers[cell]
+        return (c / self.rho, c, c * self.rho)
+
+
+class TallySet:
+    """hww::TallySet (tally.hpp:16-45) as numpy arrays; the engine accumulates."""
+
+    def __init__(self, cells, batches):
+        self.cells, self.batches = cells, batches
+        self.track_flux = np.zeros(cells)
+        self.track_flux_batch = np.zeros(batches * cells)
+        self.census_phi = np.zeros(cells)
+        self.census_current = np.zeros(cells)
+        self.census_closure = np.zeros(cells)
+        self.census_weight_batch = np.zeros(batches)
+        self.edge_current = np.zeros(cells + 1)
+        self.boundary_closure_left = 0.0
+        self.boundary_closure_right = 0.0
+        self.histories_scored = 0
+        self.grazing_discarded = 0
+
+    def _to_c(self):
+        t = A.TallySetC()
+        for n in ("track_flux", "track_flux_batch", "census_phi", "census_current",
+                  "census_closure", "census_weight_batch", "edge_current"):
+            setattr(t, n, A.as_dptr(getattr(self, n)))
+        t.boundary_closure_left = self.boundary_closure_left
+        t.boundary_closure_right = self.boundary_closure_right
+        t.histories_scored = self.histories_scored
+        t.grazing_discarded = self.grazing_discarded
+        return t
+
+    def _from_c(self, t):
+        self.boundary_closure_left = t.boundary_closure_left
+        self.boundary_closure_right = t.boundary_closure_right
+        self.histories_scored = t.histories_scored
+        self.grazing_discarded = t.grazing_discarded
+
+
+class StepOutcome:
+    """hww::StepOutcome (transport.hpp:67-80)."""
+
+    def __init__(self, cells=0):
+        self.census = np.zeros(0, PARTICLE_DT)
+        self.counters = A.Counters()
+        self.tracks_per_cell = np.zeros(cells, np.uint64)
+
+
+# ------------------------------------------------------------------- engine
+class Engine:
+    """A device context (hwwg_ctx) on one GPU."""
+
+    def __init__(self, device=0, rng_mode=RNG_EXACT, bank_capacity=0):
+        L = A.lib()
+        self._h = C.c_void_p()
+        opts = A.Options(device, rng_mode, bank_capacity)
+        _raise(L.hwwg_create(C.byref(opts), C.byref(self._h)))
+        self.device, self.rng_mode = device, rng_mode
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            A.lib().hwwg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # transport.hpp:117-120
+    def run_segment_parallel(self, ctx: StepContext, source, h_begin: int,
+                             ww: Optional[WeightWindowGrid], tallies: TallySet,
+                             outcome: StepOutcome):
+        L = A.lib()
+        mesh = ctx.mesh
+        I = mesh.cells()
+        mats = _materials_array(ctx.materials, I)
+        src = np.ascontiguousarray(source, PARTICLE_DT)
+        sc = A.StepContextC()
+        sc.edges = A.as_dptr(mesh.edges)
+        sc.cells = I
+        sc.batches = ctx.batches
+        sc.materials = mats.ctypes.data
+        sc.t_begin, sc.t_end = ctx.t_begin, ctx.t_end
+        sc.seed = ctx.seed
+        sc.step_index = ctx.step_index
+        sc.histories_total = ctx.histories_total
+        wg = None
+        if ww is not None:
+            cen = np.ascontiguousarray(ww.centers, np.float64)
+            if cen.size != I:
+                raise ValueError("window centers must have one value per cell")
+            wg = A.WindowGridC(A.as_dptr(cen), ww.rho, ww.eps_min)
+        tc = tallies._to_c()
+        if outcome.tracks_per_cell.size != I:
+            outcome.tracks_per_cell = np.zeros(I, np.uint64)
+        base = outcome.census.size
+        cap = max(base + 2 * src.size + 1024, base)
+        buf = np.zeros(cap, PARTICLE_DT)
+        buf[:base] = outcome.census
+        oc = A.StepOutcomeC()
+        oc.census_size = base
+        oc.counters = outcome.counters
+        oc.tracks_per_cell = A.as_u64ptr(outcome.tracks_per_cell)
+        while True:
+            oc.census = buf.ctypes.data
+            oc.census_capacity = buf.size
+            rc = L.hwwg_run_segment_parallel(self._h, C.byref(sc), src.ctypes.data, src.size,
+                                             h_begin, C.byref(wg) if wg else None,
+                                             C.byref(tc), C.byref(oc))
+            if rc == A.HWWG_ENOSPC:
+                nb = np.zeros(int(oc.census_needed), PARTICLE_DT)
+                nb[:base] = buf[:base]
+                buf = nb
+                continue
+            _raise(rc)
+            break
+        tallies._from_c(tc)
+        outcome.counters = oc.counters
+        outcome.census = buf[: oc.census_size].copy()
+        return outcome
+
+    # losm.hpp:77-80
+    def assemble_solve(self, mesh: Mesh1D, materials, phi_prev, J_prev, F_prev, theta, dt,
+                       PL_prev=0.0, PR_prev=0.0, F_now=None, PL_now=0.0, PR_now=0.0,
+                       J_L=0.0, J_R=0.0, q=None):
+        I = mesh.cells()
+        mats = _materials_array(materials, I)
+        f = lambda a: np.ascontiguousarray(a, np.float64) if a is not None else None
+        phi_prev, J_prev, F_prev, F_now, q = f(phi_prev), f(J_prev), f(F_prev), f(F_now), f(q)
+        phi = np.zeros(I + 2)
+        J = np.zeros(I + 1)
+        _raise(A.lib().hwwg_losm_assemble_solve(
+            self._h, I, A.as_dptr(mesh.edges), mats.ctypes.data, A.as_dptr(phi_prev),
+            A.as_dptr(J_prev), J_L, J_R, 1 if F_now is not None else 0, A.as_dptr(F_now),
+            PL_now, PR_now, A.as_dptr(F_prev), PL_prev, PR_prev, theta, dt, A.as_dptr(q),
+            A.as_dptr(phi), A.as_dptr(J)))
+        return phi, J
+
+    # ww.hpp:34-35
+    def build_centers(self, phi_tilde, eps_min, rho) -> WeightWindowGrid:
+        phi = np.ascontiguousarray(phi_tilde, np.float64)
+        out = np.ones(phi.size)
+        rc = _raise(A.lib().hwwg_build_centers(self._h, A.as_dptr(phi), phi.size, eps_min, rho,
+                                               A.as_dptr(out)))
+        return WeightWindowGrid(out, rho, eps_min, uniform_fallback=(rc == 1))
+
+    # filters.hpp:30
+    def moving_average(self, g, k):
+        g = np.ascontiguousarray(g, np.float64)
+        out = np.zeros(g.size)
+        _raise(A.lib().hwwg_moving_average(self._h, A.as_dptr(g), g.size, k, A.as_dptr(out)))
+        return out
+
+    # popctrl.hpp:22
+    def uniform_comb(self, bank, target, seed, stream_id):
+        b = np.ascontiguousarray(bank, PARTICLE_DT)
+        out = np.zeros(target, PARTICLE_DT)
+        iw, ow = C.c_double(), C.c_double()
+        _raise(A.lib().hwwg_uniform_comb(self._h, b.ctypes.data if b.size else None, b.size,
+                                         target, seed, stream_id, out.ctypes.data,
+                                         C.byref(iw), C.byref(ow)))
+        return out, iw.value, ow.value
+
+    def device_log(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(x.size)
+        _raise(A.lib().hwwg_device_log(self._h, A.as_dptr(x), x.size, A.as_dptr(out)))
+        return out
+
+
+_default_engine = None
+
+
+def default_engine() -> Engine:
+    global _default_engine
+    if _default_engine is None:
+        _default_engine = Engine()
+    return _default_engine
+
+
+def run_segment_parallel(ctx, source, h_begin, ww, tallies, outcome, engine=None):
+    """hww::run_segment_parallel (transport.hpp:117-120) on the GPU."""
+    return (engine or default_engine()).run_segment_parallel(ctx, source, h_begin, ww, tallies,
+                                                             outcome)
+
+
+# ------------------------------------------------------------------- driver
+@dataclass
+class RunConfig:
+    """hww::RunConfig (config.hpp:33-66) with the reference defaults."""
+    mode: str = "hww"
+    histories_per_step: int = 10000
+    theta: float = 0.5
+    rho: float = 1.25
+    eps_min: float = 1e-3
+    u_ww: int = 3
+    update_fractions: Sequence[float] = (0.25, 0.5, 0.75)
+    ma_base_k: int = 3
+    fourier_cutoff: int = 30
+    batches: int = 20
+    seed: int = 1
+    target_population: int = 0
+    comb_overflow_factor: float = 1.0
+    source_x0: float = 0.0
+    source_t0: float = 0.0
+    source_strength: float = 1.0
+    material: Material = field(default_factory=lambda: Material(1.0, 1.0 / 3.0, 1.0 / 3.0, 2.3, 1.0))
+    x_min: float = -20.5
+    x_max: float = 20.5
+    cells: int = 201
+    t_end: float = 20.0
+    time_steps: int = 20
+    threads: int = 0
+    host_bank: bool = False
+
+    def comb_target(self):
+        return self.target_population or self.histories_per_step
+
+    def to_c(self) -> A.RunConfigC:
+        c = A.RunConfigC()
+        c.mode = MODES.index(self.mode) if isinstance(self.mode, str) else int(self.mode)
+        c.u_ww = self.u_ww
+        c.histories_per_step = self.histories_per_step
+        c.theta, c.rho, c.eps_min = self.theta, self.rho, self.eps_min
+        c.n_fractions = len(self.update_fractions)
+        for i, f in enumerate(self.update_fractions[:8]):
+            c.fractions[i] = f
+        c.ma_base_k, c.fourier_cutoff, c.batches = self.ma_base_k, self.fourier_cutoff, self.batches
+        c.seed, c.target_population = self.seed, self.target_population
+        c.comb_overflow_factor = self.comb_overflow_factor
+        c.x0, c.t0, c.strength = self.source_x0, self.source_t0, self.source_strength
+        m = self.material
+        c.sigma_t, c.sigma_s, c.sigma_f, c.nu_f, c.speed = (m.sigma_t, m.sigma_s, m.sigma_f,
+                                                            m.nu_f, m.speed)
+        c.x_min, c.x_max, c.cells = self.x_min, self.x_max, self.cells
+        c.t_end, c.time_steps, c.threads = self.t_end, self.time_steps, self.threads
+        c.host_bank = 1 if self.host_bank else 0
+        return c
+
+    @staticmethod
+    def from_file(path) -> "RunConfig":
+        """Key = value loader (hww_main.cpp:20-92 key names)."""
+        L = A.lib()
+        c = A.RunConfigC()
+        L.hwwg_default_config(C.byref(c))
+        _raise(L.hwwg_load_config_file(str(path).encode(), C.byref(c)))
+        return RunConfig(
+            mode=MODES[c.mode], histories_per_step=c.histories_per_step, theta=c.theta,
+            rho=c.rho, eps_min=c.eps_min, u_ww=c.u_ww,
+            update_fractions=tuple(c.fractions[i] for i in range(c.n_fractions)),
+            ma_base_k=c.ma_base_k, fourier_cutoff=c.fourier_cutoff, batches=c.batches,
+            seed=c.seed, target_population=c.target_population,
+            comb_overflow_factor=c.comb_overflow_factor, source_x0=c.x0, source_t0=c.t0,
+            source_strength=c.strength,
+            material=Material(c.sigma_t, c.sigma_s, c.sigma_f, c.nu_f, c.speed),
+            x_min=c.x_min, x_max=c.x_max, cells=c.cells, t_end=c.t_end,
+            time_steps=c.time_steps, threads=c.threads)
+
+    def validate(self):
+        """validate_config (config.cpp:27-69): list of violations."""
+        buf = C.create_string_buffer(4096)
+        n = A.lib().hwwg_validate_config(C.byref(self.to_c()), buf, 4096)
+        return buf.value.decode().split("\n") if n else []
+
+
+class Driver:
+    """Stepwise hww::run (driver.cpp:286-342): device-resident time steps."""
+
+    def __init__(self, config: RunConfig, device=0, rng_mode=RNG_EXACT):
+        self.config = config
+        self._cfg = config.to_c()
+        self._h = C.c_void_p()
+        opts = A.Options(device, rng_mode, 0)
+        _raise(A.lib().hwwg_driver_create(C.byref(self._cfg), C.byref(opts), C.byref(self._h)))
+        self.I = config.cells
+
+    def step(self):
+        rec = A.StepRecordC()
+        _raise(A.lib().hwwg_driver_step(self._h, C.byref(rec)))
+        return rec
+
+    def arrays(self):
+        I = self.I
+        arr = {n: np.full(I, np.nan) for n in ("phi_track", "sigma", "phi_census",
+                                                "current_census", "closure_census",
+                                                "ww_centers", "phi_hybrid")}
+        arr["edge_current"] = np.zeros(I + 1)
+        tracks = np.zeros(I, np.uint64)
+        _raise(A.lib().hwwg_driver_arrays(
+            self._h, A.as_dptr(arr["phi_track"]), A.as_dptr(arr["sigma"]),
+            A.as_dptr(arr["phi_census"]), A.as_dptr(arr["current_census"]),
+            A.as_dptr(arr["closure_census"]), A.as_dptr(arr["edge_current"]),
+            A.as_dptr(arr["ww_centers"]), A.as_dptr(arr["phi_hybrid"]), A.as_u64ptr(tracks)))
+        arr["tracks_per_cell"] = tracks
+        return arr
+
+    def bank(self):
+        n = C.c_uint64()
+        A.lib().hwwg_driver_bank(self._h, None, 0, C.byref(n))
+        out = np.zeros(n.value, PARTICLE_DT)
+        _raise(A.lib().hwwg_driver_bank(self._h, out.ctypes.data if n.value else None, n.value,
+                                        C.byref(n)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            A.lib().hwwg_driver_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run(config: RunConfig, device=0, rng_mode=RNG_EXACT):
+    """hww::run (driver.hpp:88): returns the list of (record, arrays) per step."""
+    d = Driver(config, device, rng_mode)
+    out = []
+    for _ in range(config.time_steps):
+        rec = d.step()
+        out.append((rec, d.arrays()))
+    d.close()
+    return out
