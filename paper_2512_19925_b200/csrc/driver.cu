@@ -69,6 +69,7 @@ struct hwwg_driver {
   DevBuf<double> comb_mem;  // scalars[4] + prefix
   DevBuf<unsigned long long> counter;
   DevBuf<DevError> err;
+  DevBuf<double> chunk_mem;
 
   // low-order state
   DevBuf<double> lo_mem;
@@ -333,6 +334,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       ea.src = d->source.p + h_done;
       ea.n = h_stop - h_done;
       ea.h_begin = h_done;
+      ea.chunks = chunk_layout(ea.n, h_done, H, I, B);
+      d->chunk_mem.reserve(std::max<size_t>((size_t)ea.chunks.count * ea.chunks.stride, 1));
+      ea.chunks.base = d->chunk_mem.p;
       const int nseg = (int)u;
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
       launch_exact_segment(ea, s);

@@ -79,6 +79,7 @@ struct hwwg_ctx {
   DevBuf<int> iscratch;
   DevBuf<hwwg_particle> comb_in, comb_out;
   DevBuf<CellInfo> comp_cells;
+  DevBuf<double> chunk_mem;
 
   ~hwwg_ctx() {
     if (stream) cudaStreamDestroy(stream);
@@ -169,13 +170,38 @@ int hwwg_run_segment_parallel(hwwg_ctx* c, const hwwg_step_context* st,
   a.err = c->err.p;
   a.census_count = c->counter.p;
 
+  // the running TallySet / counters (reference: accumulated in place, chunk sums
+  // merged in order), uploaded so the device adds in the reference's order
+  const ChunkLayout L0 = chunk_layout(n, h_begin, st->histories_total, I, B);
+  c->chunk_mem.reserve(std::max<size_t>((size_t)L0.count * L0.stride, 1));
+  std::vector<double> up(c->tal.words(), 0.0);
+  {
+    double* q = up.data();
+    auto put = [&](const double* srcv, size_t len) {
+      if (srcv) std::memcpy(q, srcv, len * 8);
+      q += len;
+    };
+    put(tallies->track_flux, I);
+    put(tallies->track_flux_batch, (size_t)B * I);
+    put(tallies->census_phi, I);
+    put(tallies->census_current, I);
+    put(tallies->census_closure, I);
+    put(tallies->census_weight_batch, B);
+    put(tallies->edge_current, I + 1);
+    q[0] = tallies->boundary_closure_left;
+    q[1] = tallies->boundary_closure_right;
+    q[2] = outcome->counters.leakage_weight;
+    q[3] = outcome->counters.aborted_weight;
+  }
   unsigned long long count = 0;
   DevError derr{};
   for (int attempt = 0; attempt < 3; ++attempt) {
-    c->tal.zero(s);
+    HWWG_CUDA(cudaMemcpyAsync(c->tal.slab.p, up.data(), up.size() * 8, cudaMemcpyHostToDevice, s));
     HWWG_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned long long), s));
     HWWG_CUDA(cudaMemsetAsync(c->err.p, 0, sizeof(DevError), s));
     a.t = c->tal.p;
+    a.chunks = L0;
+    a.chunks.base = c->chunk_mem.p;
     a.census = c->stage.records.p;
     a.census_keys = c->stage.keys.p;
     a.census_cap = c->stage.records.n;
@@ -204,20 +230,19 @@ int hwwg_run_segment_parallel(hwwg_ctx* c, const hwwg_step_context* st,
                               count * sizeof(hwwg_particle), cudaMemcpyDeviceToHost, s));
   c->host_tal.fetch(c->tal, s);  // synchronises
   const HostTallies& h = c->host_tal;
-  auto acc = [](double* dst, const double* srcv, size_t len) {
-    if (dst)
-      for (size_t i = 0; i < len; ++i) dst[i] += srcv[i];
+  auto put_back = [](double* dst, const double* srcv, size_t len) {
+    if (dst) std::memcpy(dst, srcv, len * 8);
   };
-  acc(tallies->track_flux, h.track_flux(), I);
-  acc(tallies->track_flux_batch, h.track_flux_batch(), (size_t)B * I);
-  acc(tallies->census_phi, h.census_phi(), I);
-  acc(tallies->census_current, h.census_current(), I);
-  acc(tallies->census_closure, h.census_closure(), I);
-  acc(tallies->census_weight_batch, h.census_weight_batch(), B);
-  acc(tallies->edge_current, h.edge_current(), I + 1);
-  tallies->boundary_closure_left += h.boundary_closure()[0];
-  tallies->boundary_closure_right += h.boundary_closure()[1];
-  tallies->histories_scored += n;
+  put_back(tallies->track_flux, h.track_flux(), I);
+  put_back(tallies->track_flux_batch, h.track_flux_batch(), (size_t)B * I);
+  put_back(tallies->census_phi, h.census_phi(), I);
+  put_back(tallies->census_current, h.census_current(), I);
+  put_back(tallies->census_closure, h.census_closure(), I);
+  put_back(tallies->census_weight_batch, h.census_weight_batch(), B);
+  put_back(tallies->edge_current, h.edge_current(), I + 1);
+  tallies->boundary_closure_left = h.boundary_closure()[0];
+  tallies->boundary_closure_right = h.boundary_closure()[1];
+  tallies->histories_scored += h.ucount()[kHistoriesScored];
   tallies->grazing_discarded += h.ucount()[kGrazingDiscarded];
   hwwg_counters& k = outcome->counters;
   const unsigned long long* u = h.ucount();
@@ -230,8 +255,8 @@ int hwwg_run_segment_parallel(hwwg_ctx* c, const hwwg_step_context* st,
   k.census_count += u[kCensusCount];
   k.event_cap_aborts += u[kEventCapAborts];
   k.nan_aborts += u[kNanAborts];
-  k.leakage_weight += h.dcount()[0];
-  k.aborted_weight += h.dcount()[1];
+  k.leakage_weight = h.dcount()[0];
+  k.aborted_weight = h.dcount()[1];
   if (outcome->tracks_per_cell)
     for (int i = 0; i < I; ++i) outcome->tracks_per_cell[i] += h.tracks()[i];
   outcome->census_size += count;

@@ -1,10 +1,25 @@
-// Launch interfaces of the transport kernels (see transport_exact.cu,
+// Launch interfaces of the transport kernels (transport_exact.cu,
 // transport_fast.cu).
 #pragma once
 
 #include "common.cuh"
 
 namespace hwwg {
+
+// The reference's OpenMP chunk (run_segment_parallel's default chunk_size,
+// proj/include/hww/transport.hpp:117-120).
+constexpr int kChunk = 256;
+
+// Chunk-private TallySets of one exact-mode segment: per chunk `stride`
+// doubles = track I | census phi,J,F 3I | edge I+1 | bclosure 2 | leak,aborted 2
+// | census_weight_batch B | track_flux_batch span*I (batches b0..b0+span-1).
+struct ChunkLayout {
+  double* base;
+  size_t stride;
+  int count;
+  int span;
+};
+ChunkLayout chunk_layout(uint64_t n, uint64_t h_begin, uint64_t H, int I, int B);
 
 // One exact-mode segment: histories [h_begin, h_begin + n) of a step.
 struct ExactArgs {
@@ -20,7 +35,8 @@ struct ExactArgs {
   const double* centers;  // NULL: analog
   const int* active;      // optional device flag gating the windows (lww/hww)
   double rho;
-  TallyPtrs t;
+  TallyPtrs t;            // running tallies (accumulated in reference order)
+  ChunkLayout chunks;
   hwwg_particle* census;            // staging records
   unsigned long long* census_keys;  // history << 24 | emission index
   unsigned long long* census_count;

@@ -1,20 +1,29 @@
-// Exact-mode history kernel: bit-exact replay of hww::advance_history
-// (proj/src/transport.cpp:81-192) on sm_100a, one history per thread.
+// Exact-mode history kernel: bit-exact replay of hww::run_segment_parallel
+// (proj/src/transport.cpp:81-237) on sm_100a — events, census AND tallies.
 //
-// Why one history per thread: the reference's daughters share their parent
+// Why it is built this way: the reference's daughters share their parent
 // history's flight/window streams and run depth-first on a LIFO stack
 // (transport.cpp:100-107, 199-202), so a history's event sequence is
-// inherently serial. The stack is run-length encoded: a split pushes its
-// n-1 identical copies as ONE run (entry, n-1) (transport.cpp:65-66), so the
-// pop order is the reference's while storage is O(split events) — measured
-// depth <= 9 runs on BASELINE configs 1/2/4/5 (oracle diagnostics), 64 here.
+// inherently serial; and its fp64 tallies are sums in one specific order —
+// sequential over the events of each 256-history chunk into a fresh TallySet,
+// then chunk sums merged in chunk order (transport.cpp:219-236). One GPU
+// thread per 256-history chunk runs that chunk's histories in order into
+// chunk-private accumulators (plain adds, no atomics), and k_merge_chunks adds
+// the chunk sums into the running tallies in chunk order, so every tally —
+// and hence every LOSM solve and window centre downstream — is bit-identical
+// to the reference, not merely within rounding. Integer tallies (tracks per
+// cell, counters) are order-free and use atomics.
 //
-// Arithmetic parity: this translation unit is compiled with -fmad=false (no
-// FMA contraction, like the reference's x86-64 baseline build), divisions are
-// IEEE div.rn, and log is the bit-exact libm replay in libm_log.h. Census
-// records are appended with a (history << 24 | emission index) key and sorted
-// afterwards, which restores the reference's history-major, depth-first order
-// (transport.cpp:146, 233-236).
+// The daughter stack is run-length encoded: a split pushes its n-1 identical
+// copies as ONE run (entry, n-1) (transport.cpp:65-66), so the pop order is
+// the reference's while storage is O(split events) — measured depth <= 9 runs
+// on BASELINE configs 1/2/4/5 (oracle diagnostics); capacity 64 here.
+//
+// Arithmetic parity: compiled with -fmad=false (no FMA contraction, like the
+// reference's x86-64 baseline build), IEEE div.rn, and log is the bit-exact
+// libm replay in libm_log.h. Census records are appended with a
+// (history << 24 | emission index) key and radix-sorted afterwards, restoring
+// the reference's history-major, depth-first order (transport.cpp:146, 233-236).
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -38,7 +47,20 @@ struct Run {
 
 struct Local {
   unsigned long long u[kNumUCounters];
-  double leak, aborted;
+  double leak, aborted;  // chunk-sequential, like StepCounters of a chunk
+};
+
+// Chunk-private fp64 accumulators (one hww::TallySet per chunk).
+struct Sink {
+  double* track;  // I
+  double* cphi;   // I
+  double* cJ;     // I
+  double* cF;     // I
+  double* edge;   // I+1
+  double* bclo;   // 2
+  double* cwb;    // B
+  double* trackb; // span*I, batch b stored at (b - b0)
+  int b0;
 };
 
 __device__ __forceinline__ void set_error(DevError* e, int code, unsigned long long h) {
@@ -100,7 +122,8 @@ struct History {
   }
 };
 
-__device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk) {
+// advance_history (transport.cpp:81-192) for source index i into sink S.
+__device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, const Sink& S) {
   const unsigned long long h = a.h_begin + i;
   const double2 s0 = reinterpret_cast<const double2*>(a.src)[2 * i];
   const double2 s1 = reinterpret_cast<const double2*>(a.src)[2 * i + 1];
@@ -122,7 +145,7 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk) 
   const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
   const int I = a.mesh.I;
   const double* edges = a.mesh.edges;
-  const TallyPtrs& T = a.t;
+  double* trackb = S.trackb + (size_t)(batch - S.b0) * I;
 
   hs.push(s0.x, s0.y, s1.x, s1.y, start_cell, 1u);
   unsigned long long events = 0;
@@ -162,21 +185,21 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk) 
 
       if (d > 0.0) {  // score_track, tally.hpp:51-56
         const double sc = w * d * (ci.inv_dx * a.inv_dt);
-        atomicAdd(&T.track_flux[cell], sc);
-        atomicAdd(&T.track_flux_batch[(size_t)batch * I + cell], sc);
-        atomicAdd(&T.tracks[cell], 1ULL);
+        S.track[cell] += sc;
+        trackb[cell] += sc;
+        atomicAdd(&a.t.tracks[cell], 1ULL);
       }
 
       if (d == d_census) {  // transport.cpp:141-149
         x += d * mu;
         t = a.t_end;
         const double base = ci.speed * w * ci.inv_dx;  // score_census, tally.hpp:65-72
-        atomicAdd(&T.census_phi[cell], base);
-        atomicAdd(&T.census_current[cell], base * mu);
-        atomicAdd(&T.census_closure[cell], base * (1.0 / 3.0 - mu * mu));
-        atomicAdd(&T.census_weight_batch[batch], w);
+        S.cphi[cell] += base;
+        S.cJ[cell] += base * mu;
+        S.cF[cell] += base * (1.0 / 3.0 - mu * mu);
+        S.cwb[batch] += w;
         ++c.u[kCensusCount];
-        const unsigned long long slot = warp_reserve1(a.census_count);
+        const unsigned long long slot = atomicAdd(a.census_count, 1ULL);
         if (slot < a.census_cap) {
           double2* dst = reinterpret_cast<double2*>(a.census) + 2 * slot;
           dst[0] = make_double2(x, mu);
@@ -192,13 +215,13 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk) 
         x = edges[edge];
         t += d / ci.speed;
         const bool domain = edge == 0 || edge == I;
-        atomicAdd(&T.edge_current[edge], (mu > 0 ? w : -w) * a.inv_dt);  // tally.hpp:77-92
+        S.edge[edge] += (mu > 0 ? w : -w) * a.inv_dt;  // tally.hpp:77-92
         if (domain) {
           const double amu = mu > 0 ? mu : -mu;
           if (amu < kGrazingMu) {
             ++c.u[kGrazingDiscarded];
           } else {
-            atomicAdd(&T.boundary_closure[edge == 0 ? 0 : 1], w * (0.5 - amu) / amu * a.inv_dt);
+            S.bclo[edge == 0 ? 0 : 1] += w * (0.5 - amu) / amu * a.inv_dt;
           }
           c.leak += w;
           alive = false;
@@ -240,39 +263,126 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk) 
   }
 }
 
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ double warp_sum_f64(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
+__device__ __forceinline__ Sink chunk_sink(const ExactArgs& a, int c) {
+  const ChunkLayout& L = a.chunks;
+  double* b = L.base + (size_t)c * L.stride;
+  const int I = a.mesh.I;
+  Sink s;
+  s.track = b;
+  s.cphi = b + I;
+  s.cJ = b + 2 * I;
+  s.cF = b + 3 * I;
+  s.edge = b + 4 * I;
+  s.bclo = b + 5 * I + 1;
+  s.cwb = b + 5 * I + 5;
+  s.trackb = b + 5 * I + 5 + a.B;
+  s.b0 = batch_of(a.h_begin + (uint64_t)c * kChunk, a.H, a.B);
+  return s;
 }
 
-__global__ void __launch_bounds__(128) k_exact_histories(ExactArgs a) {
+// One thread per 256-history chunk (run_segment_serial on the chunk,
+// transport.cpp:194-207), histories in order.
+__global__ void __launch_bounds__(64) k_exact_chunks(ExactArgs a) {
   Run stk[kMaxRuns];
-  Local c;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.chunks.count) return;
+  const Sink S = chunk_sink(a, c);
+  double* dcnt = a.chunks.base + (size_t)c * a.chunks.stride + 5 * a.mesh.I + 3;
+  Local l;
 #pragma unroll
-  for (int k = 0; k < kNumUCounters; ++k) c.u[k] = 0;
-  c.leak = 0.0;
-  c.aborted = 0.0;
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < a.n) run_history(a, i, c, stk);
-  __syncwarp();
-  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < kNumUCounters; ++k) l.u[k] = 0;
+  l.leak = dcnt[0];
+  l.aborted = dcnt[1];
+  const uint64_t lo = (uint64_t)c * kChunk;
+  const uint64_t hi = lo + kChunk < a.n ? lo + kChunk : a.n;
+  for (uint64_t i = lo; i < hi; ++i) run_history(a, i, l, stk, S);
+  dcnt[0] = l.leak;
+  dcnt[1] = l.aborted;
+  l.u[kHistoriesScored] = hi - lo;
 #pragma unroll
-  for (int k = 0; k < kNumUCounters; ++k) {
-    const unsigned long long v = warp_sum_u64(c.u[k]);
-    if (lane == 0 && v) atomicAdd(&a.t.ucount[k], v);
+  for (int k = 0; k < kNumUCounters; ++k)
+    if (l.u[k]) atomicAdd(&a.t.ucount[k], l.u[k]);
+}
+
+// Chunk accumulators start at zero (a fresh TallySet per chunk,
+// transport.cpp:220-227) — or, when the segment is a single chunk, at the
+// running tallies (run_segment_serial straight into them, transport.cpp:216-217).
+__global__ void k_chunk_init(ExactArgs a) {
+  const ChunkLayout& L = a.chunks;
+  const int I = a.mesh.I, B = a.B;
+  const size_t total = (size_t)L.count * L.stride;
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= total) return;
+  double v = 0.0;
+  if (L.count == 1) {
+    const TallyPtrs& T = a.t;
+    const int b0 = batch_of(a.h_begin, a.H, B);
+    if (k < (size_t)I) v = T.track_flux[k];
+    else if (k < 2 * (size_t)I) v = T.census_phi[k - I];
+    else if (k < 3 * (size_t)I) v = T.census_current[k - 2 * I];
+    else if (k < 4 * (size_t)I) v = T.census_closure[k - 3 * I];
+    else if (k < 5 * (size_t)I + 1) v = T.edge_current[k - 4 * I];
+    else if (k < 5 * (size_t)I + 3) v = T.boundary_closure[k - (5 * I + 1)];
+    else if (k < 5 * (size_t)I + 5) v = T.dcount[k - (5 * I + 3)];
+    else if (k < 5 * (size_t)I + 5 + B) v = T.census_weight_batch[k - (5 * I + 5)];
+    else {
+      const size_t j = k - (5 * (size_t)I + 5 + B);
+      const int b = b0 + (int)(j / I);
+      if (b < B) v = T.track_flux_batch[(size_t)b * I + j % I];
+    }
   }
-  const double leak = warp_sum_f64(c.leak);
-  const double ab = warp_sum_f64(c.aborted);
-  if (lane == 0) {
-    if (leak != 0.0) atomicAdd(&a.t.dcount[0], leak);
-    if (ab != 0.0) atomicAdd(&a.t.dcount[1], ab);
+  L.base[k] = v;
+}
+
+// merge_from in chunk order (tally.cpp:8-26; transport.cpp:233-236): one
+// thread per tally slot walks the chunks sequentially.
+__global__ void k_merge_chunks(ExactArgs a) {
+  const ChunkLayout& L = a.chunks;
+  const int I = a.mesh.I, B = a.B;
+  const int slots = 5 * I + 5 + B + B * I;  // chunk-layout slots + the global batch table
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= slots) return;
+  const TallyPtrs& T = a.t;
+  double* dst;
+  int local;  // slot inside a chunk, or -1 for the batch table
+  int b = 0, cell = 0;
+  if (s < 5 * I + 5 + B) {
+    local = s;
+    if (s < I) dst = &T.track_flux[s];
+    else if (s < 2 * I) dst = &T.census_phi[s - I];
+    else if (s < 3 * I) dst = &T.census_current[s - 2 * I];
+    else if (s < 4 * I) dst = &T.census_closure[s - 3 * I];
+    else if (s < 5 * I + 1) dst = &T.edge_current[s - 4 * I];
+    else if (s < 5 * I + 3) dst = &T.boundary_closure[s - (5 * I + 1)];
+    else if (s < 5 * I + 5) dst = &T.dcount[s - (5 * I + 3)];
+    else dst = &T.census_weight_batch[s - (5 * I + 5)];
+  } else {
+    local = -1;
+    const int j = s - (5 * I + 5 + B);
+    b = j / I;
+    cell = j % I;
+    dst = &T.track_flux_batch[(size_t)b * I + cell];
   }
+  if (L.count == 1) {  // accumulated in place from the running values
+    if (local >= 0) {
+      *dst = L.base[local];
+    } else {
+      const int b0 = batch_of(a.h_begin, a.H, B);
+      if (b >= b0 && b < b0 + L.span) *dst = L.base[5 * I + 5 + B + (size_t)(b - b0) * I + cell];
+    }
+    return;
+  }
+  double acc = *dst;
+  for (int c = 0; c < L.count; ++c) {
+    const double* cb = L.base + (size_t)c * L.stride;
+    if (local >= 0) {
+      acc += cb[local];
+    } else {
+      const int b0 = batch_of(a.h_begin + (uint64_t)c * kChunk, a.H, B);
+      if (b >= b0 && b < b0 + L.span) acc += cb[5 * I + 5 + B + (size_t)(b - b0) * I + cell];
+    }
+  }
+  *dst = acc;
 }
 
 __global__ void k_iota(unsigned* v, uint64_t n) {
@@ -291,13 +401,37 @@ __global__ void k_gather(const hwwg_particle* __restrict__ src, const unsigned* 
   }
 }
 
+int host_batch_of(uint64_t h, uint64_t H, int B) {
+  if (H == 0) return 0;
+  const int b = (int)(h * (uint64_t)B / H);
+  return b < B ? b : B - 1;
+}
+
 }  // namespace
+
+ChunkLayout chunk_layout(uint64_t n, uint64_t h_begin, uint64_t H, int I, int B) {
+  ChunkLayout L{};
+  L.count = (int)((n + kChunk - 1) / kChunk);
+  int span = 1;  // batches touched by one chunk (contiguous slices of H/B histories)
+  for (int c = 0; c < L.count; ++c) {
+    const uint64_t lo = h_begin + (uint64_t)c * kChunk;
+    const uint64_t len = n - (uint64_t)c * kChunk < (uint64_t)kChunk ? n - (uint64_t)c * kChunk
+                                                                     : (uint64_t)kChunk;
+    const int sp = host_batch_of(lo + len - 1, H, B) - host_batch_of(lo, H, B) + 1;
+    if (sp > span) span = sp;
+  }
+  L.span = span;
+  L.stride = (size_t)5 * I + 5 + B + (size_t)span * I;
+  return L;
+}
 
 void launch_exact_segment(const ExactArgs& a, cudaStream_t s) {
   if (a.n == 0) return;
-  const unsigned threads = 128;
-  const uint64_t blocks = (a.n + threads - 1) / threads;
-  k_exact_histories<<<(unsigned)blocks, threads, 0, s>>>(a);
+  const size_t total = (size_t)a.chunks.count * a.chunks.stride;
+  k_chunk_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a);
+  k_exact_chunks<<<(unsigned)((a.chunks.count + 63) / 64), 64, 0, s>>>(a);
+  const int slots = 5 * a.mesh.I + 5 + a.B + a.B * a.mesh.I;
+  k_merge_chunks<<<(slots + 255) / 256, 256, 0, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
 
