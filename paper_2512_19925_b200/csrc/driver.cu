@@ -21,6 +21,7 @@
 #include "driver_host.h"
 #include "engine.cuh"
 #include "low_order.cuh"
+#include "fast.cuh"
 #include "transport.cuh"
 
 using namespace hwwg;
@@ -42,6 +43,28 @@ void set_active_from_fallback(int* flags, cudaStream_t s) {
   k_active_from_fallback<<<1, 1, 0, s>>>(flags);
   HWWG_CUDA(cudaGetLastError());
 }
+
+// Owner of a SoA particle bank (fast mode).
+struct FastBankBuf {
+  DevBuf<double2> xm, wt;
+  DevBuf<uint4> meta;
+  void reserve(uint64_t n) {
+    n = n ? n : 1;
+    xm.reserve(n);
+    wt.reserve(n);
+    meta.reserve(n);
+  }
+  uint64_t cap() const { return xm.n; }
+  FastBank view() { return FastBank{xm.p, wt.p, meta.p}; }
+  void swap(FastBankBuf& o) {
+    std::swap(xm.p, o.xm.p);
+    std::swap(xm.n, o.xm.n);
+    std::swap(wt.p, o.wt.p);
+    std::swap(wt.n, o.wt.n);
+    std::swap(meta.p, o.meta.p);
+    std::swap(meta.n, o.meta.n);
+  }
+};
 }  // namespace hwwg
 
 struct hwwg_driver {
@@ -70,6 +93,18 @@ struct hwwg_driver {
   DevBuf<unsigned long long> counter;
   DevBuf<DevError> err;
   DevBuf<double> chunk_mem;
+
+  // throughput (Philox) mode: SoA banks, warp split stacks, refill cursor
+  bool fast = false;
+  uint64_t census_hwm = 0;  // census capacity high-water mark (banks swap each step)
+  FastBankBuf fbank, fsrc, fcensus;
+  DevBuf<FastStackRec> stacks;
+  int stack_cap = 1024;
+  int sms = 148;
+  DevBuf<unsigned long long> src_head;
+  DevBuf<char> comb_temp;
+  DevBuf<FastStackRec> pool_recs;
+  DevBuf<unsigned long long> pool_ctl;
 
   // low-order state
   DevBuf<double> lo_mem;
@@ -179,7 +214,21 @@ void init_driver(hwwg_driver* d) {
   }
   d->seg_ev.resize(32);
   for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
-  d->stage.ensure(4 * d->target + 4096);
+  if (d->fast) {
+    d->fbank.reserve(d->bank_n);
+    launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), 0, d->stream);
+    d->fcensus.reserve(64 * d->target + 4096);  // step 1 cold start splits x60+
+    d->census_hwm = 64 * d->target + 4096;
+    HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
+    const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
+    d->stacks.reserve((size_t)warps * d->stack_cap);
+    d->src_head.reserve(1);
+    d->pool_recs.reserve(1u << 20);  // 64 MB of donated split records per segment
+    HWWG_CUDA(cudaMemsetAsync(d->pool_recs.p, 0, d->pool_recs.n * sizeof(FastStackRec), d->stream));
+    d->pool_ctl.reserve(4);
+  } else {
+    d->stage.ensure(64 * d->target + 4096);
+  }
   HWWG_CUDA(cudaStreamSynchronize(d->stream));
 }
 
@@ -204,13 +253,41 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                               cudaMemcpyHostToDevice, s));
     d->bank_n = d->host_bank_n;
     rec->h2d_bytes += d->host_bank_n * sizeof(hwwg_particle);
+    if (d->fast) {
+      d->fbank.reserve(d->bank_n);
+      launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), 0, s);
+      ++d->launches;
+    }
   }
 
   // ---- population control (driver.cpp:111-129)
   const double bank_cap = c.comb_overflow_factor * (double)d->target;
   const bool do_comb = c.comb_overflow_factor <= 1.0 || (double)d->bank_n > bank_cap;
   uint64_t H;
-  if (do_comb) {
+  if (d->fast) {
+    if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
+    if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
+    d->fsrc.reserve(d->target);
+    d->comb_mem.reserve(4 + d->bank_n);
+    const size_t tb = fast_comb_temp_bytes(d->bank_n);
+    d->comb_temp.reserve(tb);
+    FastCombArgs a{};
+    a.bank = d->fbank.view();
+    a.n = d->bank_n;
+    a.target = d->target;
+    a.seed = c.seed;
+    a.stream = stream_id_host(step, 0, 3);
+    a.prefix = d->comb_mem.p + 4;
+    a.scalars = d->comb_mem.p;
+    a.out = d->fsrc.view();
+    a.temp = d->comb_temp.p;
+    a.temp_bytes = tb;
+    launch_fast_comb(a, s);
+    d->launches += 3;
+    H = d->target;
+    rec->comb_in = d->bank_n;
+    rec->comb_out = d->target;
+  } else if (do_comb) {
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     d->source.reserve(d->target);
     d->comb_mem.reserve(4 + d->bank_n);
@@ -242,6 +319,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // backup of the windows so an overflowing step can be replayed exactly
   HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
   HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+
+  if (d->fast) d->fcensus.reserve(d->census_hwm);  // the swapped-in buffer may be short
 
   // ---- thresholds (driver.cpp:170-177)
   std::vector<uint64_t> thr;
@@ -339,7 +418,50 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       ea.chunks.base = d->chunk_mem.p;
       const int nseg = (int)u;
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
-      launch_exact_segment(ea, s);
+      if (d->fast) {
+        FastArgs fa{};
+        const FastBank src = d->fsrc.view();
+        fa.src = FastBank{src.xm + h_done, src.wt + h_done, src.meta + h_done};
+        fa.n_src = ea.n;
+        fa.src_head = d->src_head.p;
+        fa.census = d->fcensus.view();
+        fa.census_count = d->counter.p;
+        fa.census_cap = d->fcensus.cap();
+        fa.mesh = d->prob.view;
+        fa.t_end = rec->t_end;
+        fa.inv_dt = 1.0 / dt;
+        fa.k0 = (unsigned)c.seed;
+        fa.k1 = (unsigned)(c.seed >> 32) ^ 0x6a09e667u;
+        fa.step = (unsigned)step;
+        fa.H = H;
+        fa.B = B;
+        fa.centers = ea.centers;
+        fa.active = ea.active;
+        fa.rho = c.rho;
+        fa.inv_rho = 1.0 / c.rho;
+        fa.t = d->tal.p;
+        fa.stacks = d->stacks.p;
+        fa.stack_cap = d->stack_cap;
+        fa.pool = FastPool{d->pool_recs.p, d->pool_ctl.p, (unsigned)d->pool_recs.n, 0u};
+        fa.err = d->err.p;
+        // block-private shared-memory tallies over this segment's batch range
+        // when they fit (I <= ~1000 at 20 batches), else global REDs
+        const int b_lo = batch_of_host(h_done, H, B);
+        const int b_hi = batch_of_host(h_stop ? h_stop - 1 : 0, H, B);
+        fa.b_lo = b_lo;
+        fa.nb = b_hi - b_lo + 1;
+        size_t smem = fast_smem_bytes(I, fa.nb);
+        fa.smem_tallies = smem <= 96 * 1024 ? 1 : 0;
+        if (!fa.smem_tallies) smem = 0;
+        const int blocks = d->sms * fast_blocks_per_sm(smem);
+        fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
+        if (ea.n) {
+          launch_fast_segment(fa, blocks, smem, s);
+          d->launches += 1;  // + the segment kernel counted below
+        }
+      } else {
+        launch_exact_segment(ea, s);
+      }
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg + 1], s));
       if (ea.n) ++d->launches;
       h_done = h_stop;
@@ -366,6 +488,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaMemcpyAsync(&derr, d->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaStreamSynchronize(s));
+    if (d->fast) {
+      if (derr.code || count <= d->fcensus.cap()) break;
+      d->census_hwm = count + count / 4 + 4096;
+    d->fcensus.reserve(d->census_hwm);  // replay the step with room
+      continue;
+    }
     if (derr.code || count <= ea.census_cap) break;
     d->stage.ensure(count + count / 4 + 4096);
   }
@@ -377,6 +505,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                                     " exceeded the daughter-stack run capacity");
 
   // ---- finalize (driver.cpp:221-222)
+  if (d->fast) {  // the fast kernels score the batch table only
+    launch_track_from_batches(d->tal.p, I, B, s);
+    ++d->launches;
+  }
   FinalizeArgs f{};
   f.I = I;
   f.B = B;
@@ -395,9 +527,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   ++d->launches;
 
   // ---- census -> next bank in reference order
-  d->bank.reserve(std::max<unsigned long long>(count, 1));
-  d->stage.sort_into(d->bank.p, count, ((unsigned long long)H << 24) | 0xffffffULL, s);
-  if (count) d->launches += 2;  // iota + gather (the radix sort itself is CUB's)
+  if (d->fast) {
+    d->fbank.swap(d->fcensus);  // the census is the next comb's input, already SoA
+    if (c.host_bank) {
+      d->bank.reserve(std::max<unsigned long long>(count, 1));
+      launch_fast_to_aos(d->fbank.view(), count, d->bank.p, s);
+      if (count) ++d->launches;
+    }
+  } else {
+    d->bank.reserve(std::max<unsigned long long>(count, 1));
+    d->stage.sort_into(d->bank.p, count, ((unsigned long long)H << 24) | 0xffffffULL, s);
+    if (count) d->launches += 2;  // iota + gather (the radix sort itself is CUB's)
+  }
   d->bank_n = count;
   HWWG_CUDA(cudaEventRecord(d->ev1, s));
 
@@ -521,9 +662,14 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   auto d = new hwwg_driver();
   d->cfg = *cfg;
   if (opts) d->opt = *opts;
-  if (d->opt.rng_mode != HWWG_RNG_EXACT) {
+  if (d->opt.rng_mode != HWWG_RNG_EXACT && d->opt.rng_mode != HWWG_RNG_PHILOX) {
     delete d;
-    return fail(HWWG_EINVAL, "driver: only HWWG_RNG_EXACT is available in this build");
+    return fail(HWWG_EINVAL, "unknown rng_mode");
+  }
+  d->fast = d->opt.rng_mode == HWWG_RNG_PHILOX;
+  if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
+    delete d;
+    return fail(HWWG_EINVAL, "philox mode: fission and > 65535 cells are not supported");
   }
   try {
     init_driver(d);

@@ -16,6 +16,8 @@ namespace hwwg {
 void sample_pulse_source_host(uint64_t seed, uint64_t histories, double x0, double total_weight,
                               double t0, hwwg_particle* out);
 uint64_t stream_id_host(uint64_t step, uint64_t history, uint64_t purpose);
+// batch_of (tally.hpp:130-134) on the host.
+int batch_of_host(uint64_t h, uint64_t H, int B);
 // Mesh1D::locate (mesh.cpp:26-40) on the host; -1 outside.
 int locate_host(const std::vector<double>& edges, double x);
 // lww: windows active iff build_centers did not fall back (flags[5]).

@@ -1,0 +1,81 @@
+// Throughput (Philox) mode: SoA particle bank, transport and comb interfaces.
+#pragma once
+
+#include "common.cuh"
+
+namespace hwwg {
+
+// 48 B per particle, three 128-bit words.
+struct FastBank {
+  double2* xm;  // {x, mu}
+  double2* wt;  // {w, t}
+  uint4* meta;  // {cell | draw << 16, history, lineage key lo, lineage key hi}
+};
+
+// One run-length-encoded split record (64 B): `count` identical daughters.
+struct FastStackRec {
+  double x, mu, w, t;
+  unsigned cell, hist;
+  unsigned long long key;
+  unsigned ctr, count;
+  unsigned ready, pad;  // ready: set last when the record sits in the global pool
+};
+
+// Global pool of split records shared by all warps of a segment kernel (load
+// balance for heavy split trees) plus the termination counter.
+struct FastPool {
+  FastStackRec* recs;
+  unsigned long long* ctl;  // [0] tail (reserved), [1] head (claimed), [2] active warps
+  unsigned cap;
+  unsigned warps;  // warps in the grid
+};
+
+struct FastArgs {
+  FastBank src;  // this segment's source particles
+  unsigned long long n_src;
+  unsigned long long* src_head;  // refill cursor (zeroed per segment)
+  FastBank census;
+  unsigned long long* census_count;
+  uint64_t census_cap;
+  MeshView mesh;
+  double t_end, inv_dt;
+  unsigned k0, k1, step;  // Philox key (seed) and step
+  uint64_t H;
+  int B;
+  int b_lo, nb;  // batches touched by this segment: [b_lo, b_lo + nb)
+  int smem_tallies;  // 1: block-private shared-memory tallies
+  const double* centers;
+  const int* active;
+  double rho, inv_rho;
+  TallyPtrs t;
+  FastStackRec* stacks;  // per-warp local stacks
+  int stack_cap;
+  FastPool pool;
+  DevError* err;
+};
+
+int fast_blocks_per_sm(size_t smem);
+int fast_threads_per_block();
+size_t fast_smem_bytes(int I, int nb);
+void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);
+void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
+                        uint64_t hist0, cudaStream_t s);
+
+// Parallel comb (popctrl.cpp:7-42 semantics with a parallel fp64 scan).
+struct FastCombArgs {
+  FastBank bank;
+  uint64_t n, target;
+  uint64_t seed, stream;
+  double* prefix;   // n
+  double* scalars;  // [0] W, [1] spacing, [2] offset, [3] output weight
+  FastBank out;
+  void* temp;
+  size_t temp_bytes;
+};
+size_t fast_comb_temp_bytes(uint64_t n);
+void launch_fast_comb(const FastCombArgs& a, cudaStream_t s);
+// track_flux[i] = sum_b track_flux_batch[b][i] (fast mode scores batches only)
+void launch_track_from_batches(TallyPtrs t, int I, int B, cudaStream_t s);
+void launch_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out, cudaStream_t s);
+
+}  // namespace hwwg

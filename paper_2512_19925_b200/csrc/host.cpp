@@ -28,6 +28,12 @@ uint64_t stream_id_host(uint64_t step, uint64_t history, uint64_t purpose) {
   return stream_id(step, history, purpose);
 }
 
+int batch_of_host(uint64_t h, uint64_t H, int B) {
+  if (H == 0) return 0;
+  const int b = (int)(h * (uint64_t)B / H);
+  return b < B ? b : B - 1;
+}
+
 int locate_host(const std::vector<double>& e, double x) {
   const int I = (int)e.size() - 1;
   if (x < e.front() || x > e.back()) return -1;

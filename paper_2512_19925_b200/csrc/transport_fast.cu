@@ -1,0 +1,520 @@
+// Throughput (Philox) mode: event-driven particle transport on sm_100a.
+//
+// The reference's per-history xoshiro streams force history-serial order; this
+// mode instead gives every particle its own counter-based Philox4x32-10
+// stream (counter = {history, lineage key lo, lineage key hi, step<<16 | draw},
+// key = seed), so any particle can advance independently and the result is a
+// statistically equivalent estimator of the same physics (SURVEY.md §7 hard
+// part 1; parity = combined standard errors, tests/test_gpu_statistical.py).
+//
+// Work model — a persistent grid, one particle per lane, one EVENT per loop
+// iteration (free flight -> census | cell crossing | collision), with refill:
+// a lane whose particle terminated takes the next unit of work from
+//   1. its warp's run-length-encoded split stack (LIFO, like the reference),
+//   2. the bank of source particles (one warp-aggregated atomic per refill),
+//   3. the global pool of split records that other warps donated.
+// A split never materialises its daughters: it pushes ONE record (state, n-1
+// copies) and lanes pop daughters from it — the bank-expansion step done by
+// ballot + prefix-popcount inside the warp. A warp whose pending daughters
+// exceed kDonate pushes new records to the global pool instead, so the heavy
+// cold-start split trees (config 2 step 1: p99 1108 segments per history)
+// spread over the whole GPU instead of pinning one warp. Roulette and
+// unchanged windows cost no memory traffic.
+//
+// Tallies: block-private shared-memory histograms over the segment's batch
+// range (track-length by batch and cell, census phi/J/F, edge currents,
+// per-cell track counts), flushed once per block with fp64 REDs; global REDs
+// when the histograms do not fit in shared memory (I = 4000).
+#include "common.cuh"
+#include "fast.cuh"
+#include "rng.cuh"
+
+namespace hwwg {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kThreads = 32 * kWarpsPerBlock;
+constexpr unsigned kDonate = 256;  // pending local daughters above which splits go global
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+struct Lane {
+  double x, mu, w, t, inv_mu;
+  int cell;
+  unsigned hist, ctr;
+  unsigned long long key;
+  bool alive;
+};
+
+__device__ __forceinline__ void draw2(const FastArgs& a, Lane& p, double& u0, double& u1) {
+  const U4 c{p.hist, (unsigned)p.key, (unsigned)(p.key >> 32), (a.step << 16) | (p.ctr & 0xffffu)};
+  ++p.ctr;
+  philox_uniform2(philox4x32_10(c, a.k0, a.k1), u0, u1);
+}
+
+__device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigned j) {
+  p.x = r.x;
+  p.mu = r.mu;
+  p.w = r.w;
+  p.t = r.t;
+  p.cell = (int)r.cell;
+  p.hist = r.hist;
+  p.key = mix64(r.key ^ ((unsigned long long)r.ctr << 40) ^ ((unsigned long long)j << 8) ^
+                0x5bd1e995ULL);
+  p.ctr = 0;
+  p.inv_mu = 1.0 / p.mu;
+  p.alive = true;
+}
+
+// Shared-memory tally views (block-private).
+struct SmemTally {
+  double* trk;    // nb * I, batch b at (b - b_lo)
+  double* cphi;   // I
+  double* cJ;     // I
+  double* cF;     // I
+  double* edge;   // I + 1
+  double* cwb;    // nb
+  double* bclo;   // 2
+  unsigned* trc;  // I
+};
+
+__device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb) {
+  SmemTally s;
+  s.trk = base;
+  s.cphi = s.trk + (size_t)nb * I;
+  s.cJ = s.cphi + I;
+  s.cF = s.cJ + I;
+  s.edge = s.cF + I;
+  s.cwb = s.edge + I + 1;
+  s.bclo = s.cwb + nb;
+  s.trc = reinterpret_cast<unsigned*>(s.bclo + 2);
+  return s;
+}
+
+__global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  FastStackRec* stk = a.stacks + (size_t)gwarp * a.stack_cap;  // per-warp RLE stack (L1/L2)
+  int sp = 0;
+  unsigned pend = 0;  // daughters pending in the local stack (warp-uniform)
+  bool src_done = false;
+  const int I = a.mesh.I;
+  const double* __restrict__ edges = a.mesh.edges;
+  const CellInfo* __restrict__ cells = a.mesh.cells;
+  const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
+  const bool sh = a.smem_tallies != 0;
+  SmemTally S = smem_view(smem, I, a.nb);
+  if (sh) {
+    const size_t words = (size_t)(a.nb + 4) * I + 1 + a.nb + 2 + (I + 1) / 2;
+    for (size_t i = threadIdx.x; i < words; i += blockDim.x) smem[i] = 0.0;
+    __syncthreads();
+  }
+  unsigned long long n_coll = 0, n_split = 0, n_dau = 0, n_rk = 0, n_rs = 0, n_cen = 0,
+                     n_graze = 0, n_capped = 0;
+  double leak = 0.0;
+  volatile unsigned long long* ctl = a.pool.ctl;
+
+  Lane p;
+  p.alive = false;
+  bool holding = true;  // this warp counts in pool.ctl[2] (active warps)
+  unsigned long long ticket = ~0ULL;  // lane 0: pool slot this warp waits on
+
+  while (true) {
+    // ---- refill idle lanes: local split stack, then source bank, then pool
+    unsigned need = __ballot_sync(0xffffffffu, !p.alive);
+    while (need && sp > 0) {
+      FastStackRec& r = stk[sp - 1];
+      const unsigned k = __popc(need);
+      const unsigned cnt = r.count;
+      const unsigned take = k < cnt ? k : cnt;
+      const unsigned rank = __popc(need & lt);
+      if (!p.alive && rank < take) load_rec(p, r, cnt - rank);
+      __syncwarp();
+      if (lane == 0) r.count = cnt - take;
+      __syncwarp();
+      pend -= take;
+      if (cnt == take) --sp;
+      need = __ballot_sync(0xffffffffu, !p.alive);
+    }
+    if (need && !src_done) {
+      const unsigned k = __popc(need);
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(a.src_head, (unsigned long long)k);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + k >= a.n_src) src_done = true;
+      const unsigned rank = __popc(need & lt);
+      if (!p.alive) {
+        const unsigned long long idx = base + rank;
+        if (idx < a.n_src) {
+          const double2 xm = a.src.xm[idx];
+          const double2 wt = a.src.wt[idx];
+          const uint4 m = a.src.meta[idx];
+          p.x = xm.x;
+          p.mu = xm.y;
+          p.w = wt.x;
+          p.t = wt.y;
+          p.cell = (int)(m.x & 0xffffu);
+          p.ctr = m.x >> 16;
+          p.hist = m.y;
+          p.key = ((unsigned long long)m.w << 32) | m.z;
+          p.inv_mu = 1.0 / p.mu;
+          p.alive = p.w > 0.0;
+        }
+      }
+      need = __ballot_sync(0xffffffffu, !p.alive);
+    }
+    const bool any_alive = need != 0xffffffffu;
+    if (!any_alive && sp == 0 && src_done) {
+      // Out of local work: claim a donated record, or leave when no warp can
+      // donate any more (pool drained and no active warp).
+      if (holding) {
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(const_cast<unsigned long long*>(&ctl[2]), ~0ULL);  // active--
+        }
+        holding = false;
+      }
+      // Ticket queue: an idle warp takes the next pool slot (one atomicAdd, no
+      // CAS storms) and waits for a donor to fill it. `active` counts busy
+      // warps PLUS donated records not yet picked up (a donor adds one per
+      // record before publishing it; the consumer inherits that unit), so
+      // active == 0 means nothing can ever fill an outstanding ticket.
+      int got = 0;  // 1: record ready in our slot, -1: finished
+      if (lane == 0) {
+        if (ticket == ~0ULL) ticket = atomicAdd(const_cast<unsigned long long*>(&ctl[1]), 1ULL);
+        if (ticket >= a.pool.cap) {
+          got = -1;
+        } else {
+          const FastStackRec* pr = a.pool.recs + ticket;
+          unsigned backoff = 32;
+          while (true) {
+            if (*(volatile const unsigned*)&pr->ready) {
+              got = 1;
+              break;
+            }
+            if (ctl[2] == 0) {
+              __threadfence();
+              if (*(volatile const unsigned*)&pr->ready) {
+                got = 1;
+                break;
+              }
+              got = -1;
+              break;
+            }
+            __nanosleep(backoff);
+            backoff = backoff < 1024 ? backoff * 2 : 1024;
+          }
+        }
+      }
+      got = __shfl_sync(0xffffffffu, got, 0);
+      if (got < 0) break;
+      const unsigned long long slot = __shfl_sync(0xffffffffu, ticket, 0);
+      ticket = ~0ULL;
+      holding = true;  // the record's active unit is ours now
+      FastStackRec* pr = a.pool.recs + slot;
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) {
+        stk[0] = *pr;
+        stk[0].ready = 0;
+        pr->ready = 0;  // slots are reused by the next segment
+      }
+      __syncwarp();
+      sp = 1;
+      pend = stk[0].count;
+      continue;
+    }
+    if (!any_alive) continue;
+
+    // ---- one event per live lane
+    unsigned split_n = 0;
+    if (p.alive) {
+      const CellInfo ci = cells[p.cell];
+      double u0, u1;
+      draw2(a, p, u0, u1);
+      const double d_census = ci.speed * (a.t_end - p.t);
+      const double d_coll = -log(u0) * ci.inv_sigma_t;
+      double d_b = __longlong_as_double(0x7ff0000000000000LL);
+      int edge = -1;
+      if (p.mu > 0.0) {
+        edge = p.cell + 1;
+        d_b = (edges[edge] - p.x) * p.inv_mu;
+      } else if (p.mu < 0.0) {
+        edge = p.cell;
+        d_b = (edges[edge] - p.x) * p.inv_mu;
+      }
+      double d = d_census;
+      if (d_coll < d) d = d_coll;
+      if (d_b < d) d = d_b;
+      if (d < 0.0) d = 0.0;  // rounding at an edge: zero-length step
+      const int batch = batch_of(p.hist, a.H, a.B);
+      if (d > 0.0) {
+        const double sc = p.w * d * ci.inv_dx * a.inv_dt;
+        if (sh) {
+          atomicAdd(&S.trk[(size_t)(batch - a.b_lo) * I + p.cell], sc);
+          atomicAdd(&S.trc[p.cell], 1u);
+        } else {
+          atomicAdd(&a.t.track_flux_batch[(size_t)batch * I + p.cell], sc);
+          atomicAdd(&a.t.tracks[p.cell], 1ULL);
+        }
+      }
+      bool window_site = false;
+      if (d == d_census) {
+        p.x += d * p.mu;
+        p.t = a.t_end;
+        const double base = ci.speed * p.w * ci.inv_dx;
+        const double cl = base * (1.0 / 3.0 - p.mu * p.mu);
+        if (sh) {
+          atomicAdd(&S.cphi[p.cell], base);
+          atomicAdd(&S.cJ[p.cell], base * p.mu);
+          atomicAdd(&S.cF[p.cell], cl);
+          atomicAdd(&S.cwb[batch - a.b_lo], p.w);
+        } else {
+          atomicAdd(&a.t.census_phi[p.cell], base);
+          atomicAdd(&a.t.census_current[p.cell], base * p.mu);
+          atomicAdd(&a.t.census_closure[p.cell], cl);
+          atomicAdd(&a.t.census_weight_batch[batch], p.w);
+        }
+        ++n_cen;
+        const unsigned long long slot = warp_reserve1(a.census_count);
+        if (slot < a.census_cap) {
+          a.census.xm[slot] = make_double2(p.x, p.mu);
+          a.census.wt[slot] = make_double2(p.w, p.t);
+          a.census.meta[slot] = make_uint4((unsigned)p.cell | (p.ctr << 16), p.hist,
+                                           (unsigned)p.key, (unsigned)(p.key >> 32));
+        }
+        p.alive = false;
+      } else if (d == d_b) {
+        p.x = edges[edge];
+        p.t += d * ci.inv_speed;
+        const bool domain = edge == 0 || edge == I;
+        const double ec = (p.mu > 0 ? p.w : -p.w) * a.inv_dt;
+        if (sh) atomicAdd(&S.edge[edge], ec);
+        else atomicAdd(&a.t.edge_current[edge], ec);
+        if (domain) {
+          const double amu = fabs(p.mu);
+          if (amu < 1e-10) {
+            ++n_graze;
+          } else {
+            const double bc = p.w * (0.5 - amu) / amu * a.inv_dt;
+            if (sh) atomicAdd(&S.bclo[edge == 0 ? 0 : 1], bc);
+            else atomicAdd(&a.t.boundary_closure[edge == 0 ? 0 : 1], bc);
+          }
+          leak += p.w;
+          p.alive = false;
+        } else {
+          p.cell += p.mu > 0.0 ? 1 : -1;
+          window_site = true;
+        }
+      } else {  // collision
+        p.x += d * p.mu;
+        p.t += d * ci.inv_speed;
+        ++n_coll;
+        const double xi = u1 * ci.sigma_t;
+        if (xi < ci.sigma_s) {
+          double v0, v1;
+          draw2(a, p, v0, v1);
+          p.mu = 2.0 * v0 - 1.0;
+          p.inv_mu = 1.0 / p.mu;
+          u1 = v1;  // roulette deviate for the window game below
+          window_site = true;
+        } else {
+          // capture (fission is rejected for this mode at driver creation: the
+          // BASELINE slabs have sigma_f = 0)
+          p.alive = false;
+        }
+      }
+      if (window_site && windows) {  // ww.cpp:46-72 (split conserves, roulette unbiased)
+        const double c = a.centers[p.cell];
+        if (p.w > c * a.rho) {
+          double n = ceil(p.w / c);
+          if (n > 1e6) {
+            n = 1e6;
+            ++n_capped;
+          }
+          split_n = (unsigned)n;
+          p.w = p.w / n;
+          ++n_split;
+          n_dau += split_n - 1;
+        } else if (p.w < c * a.inv_rho) {
+          if (u1 * c < p.w) {
+            p.w = c;
+            ++n_rs;
+          } else {
+            p.alive = false;
+            ++n_rk;
+          }
+        }
+      }
+    }
+    // ---- push split records: local stack while shallow, else donate to the pool
+    const unsigned smask = __ballot_sync(0xffffffffu, split_n > 1);
+    if (smask) {
+      const unsigned dau = split_n > 1 ? split_n - 1 : 0;
+      unsigned tot = dau;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      // donate only a real backlog, and only while idle warps hold open tickets
+      bool donate = pend + tot > kDonate;  // warp-uniform
+      if (donate) {
+        int open = 0;
+        if (lane == 0) open = ctl[1] > ctl[0] ? 1 : 0;
+        donate = __shfl_sync(0xffffffffu, open, 0) != 0;
+      }
+      const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell, p.hist, p.key, p.ctr,
+                             dau, 0u, 0u};
+      bool push_local = dau > 0 && !donate;
+      if (dau > 0 && donate) {
+        atomicAdd(const_cast<unsigned long long*>(&ctl[2]), 1ULL);  // the record's active unit
+        __threadfence();
+        const unsigned long long slot = atomicAdd(const_cast<unsigned long long*>(&ctl[0]), 1ULL);
+        if (slot < a.pool.cap) {
+          FastStackRec* pr = a.pool.recs + slot;
+          *pr = rec;
+          __threadfence();
+          *(volatile unsigned*)&pr->ready = 1u;
+        } else {
+          atomicAdd(const_cast<unsigned long long*>(&ctl[2]), ~0ULL);
+          push_local = true;  // pool full: keep it
+        }
+      }
+      const unsigned lmask = __ballot_sync(0xffffffffu, push_local);
+      if (push_local) {
+        const int slot = sp + (int)__popc(lmask & lt);
+        if (slot < a.stack_cap) stk[slot] = rec;
+        else atomicCAS(&a.err->code, 0, HWWG_ESTACK);
+      }
+      unsigned ld = push_local ? dau : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ld += __shfl_xor_sync(0xffffffffu, ld, o);
+      pend += ld;
+      sp += __popc(lmask);
+      if (sp > a.stack_cap) sp = a.stack_cap;
+      __syncwarp();
+    }
+  }
+
+  // ---- flush block-private tallies
+  if (sh) {
+    __syncthreads();
+    const int nb = a.nb;
+    for (int i = threadIdx.x; i < nb * I; i += blockDim.x) {
+      const double v = S.trk[i];
+      if (v != 0.0) atomicAdd(&a.t.track_flux_batch[(size_t)a.b_lo * I + i], v);
+    }
+    for (int i = threadIdx.x; i < I; i += blockDim.x) {
+      if (S.cphi[i] != 0.0) atomicAdd(&a.t.census_phi[i], S.cphi[i]);
+      if (S.cJ[i] != 0.0) atomicAdd(&a.t.census_current[i], S.cJ[i]);
+      if (S.cF[i] != 0.0) atomicAdd(&a.t.census_closure[i], S.cF[i]);
+      if (S.trc[i]) atomicAdd(&a.t.tracks[i], (unsigned long long)S.trc[i]);
+    }
+    for (int i = threadIdx.x; i <= I; i += blockDim.x)
+      if (S.edge[i] != 0.0) atomicAdd(&a.t.edge_current[i], S.edge[i]);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+      if (S.cwb[i] != 0.0) atomicAdd(&a.t.census_weight_batch[a.b_lo + i], S.cwb[i]);
+    if (threadIdx.x < 2 && S.bclo[threadIdx.x] != 0.0)
+      atomicAdd(&a.t.boundary_closure[threadIdx.x], S.bclo[threadIdx.x]);
+  }
+
+  // ---- counters (warp-aggregated)
+  auto wsum = [](unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+  };
+  n_coll = wsum(n_coll);
+  n_split = wsum(n_split);
+  n_dau = wsum(n_dau);
+  n_rk = wsum(n_rk);
+  n_rs = wsum(n_rs);
+  n_cen = wsum(n_cen);
+  n_graze = wsum(n_graze);
+  n_capped = wsum(n_capped);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) leak += __shfl_down_sync(0xffffffffu, leak, o);
+  if (lane == 0) {
+    unsigned long long* u = a.t.ucount;
+    if (n_coll) atomicAdd(&u[kCollisions], n_coll);
+    if (n_split) atomicAdd(&u[kSplits], n_split);
+    if (n_dau) atomicAdd(&u[kSplitDaughters], n_dau);
+    if (n_capped) atomicAdd(&u[kCappedSplits], n_capped);
+    if (n_rk) atomicAdd(&u[kRouletteKills], n_rk);
+    if (n_rs) atomicAdd(&u[kRouletteSurvivals], n_rs);
+    if (n_cen) atomicAdd(&u[kCensusCount], n_cen);
+    if (n_graze) atomicAdd(&u[kGrazingDiscarded], n_graze);
+    if (leak != 0.0) atomicAdd(&a.t.dcount[0], leak);
+  }
+}
+
+// Source bank from AoS particles (the pulse source, host-bank round trips).
+__global__ void k_aos_to_fast(const hwwg_particle* __restrict__ in, uint64_t n, const MeshView m,
+                              FastBank out, uint64_t hist0) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 a = reinterpret_cast<const double2*>(in)[2 * i];
+  const double2 b = reinterpret_cast<const double2*>(in)[2 * i + 1];
+  out.xm[i] = a;
+  out.wt[i] = b;
+  const int c = locate_cell(m, a.x);
+  out.meta[i] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)(hist0 + i), 0u, 0u);
+}
+
+}  // namespace
+
+size_t fast_smem_bytes(int I, int nb) {
+  return ((size_t)(nb + 4) * I + 1 + nb + 2) * sizeof(double) + (size_t)I * sizeof(unsigned) + 16;
+}
+
+int fast_threads_per_block() { return kThreads; }
+
+void configure_fast_kernel();
+
+int fast_blocks_per_sm(size_t smem) {
+  configure_fast_kernel();
+  int n = 0;
+  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment, kThreads, smem));
+  return n;
+}
+
+namespace {
+__global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src_head,
+                                unsigned long long warps) {
+  ctl[0] = 0;
+  ctl[1] = 0;
+  ctl[2] = warps;  // every warp starts active (holding source work)
+  *src_head = 0;
+}
+}  // namespace
+
+void configure_fast_kernel() {
+  static bool configured = false;
+  if (!configured) {
+    HWWG_CUDA(cudaFuncSetAttribute(k_fast_segment, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
+    configured = true;
+  }
+}
+
+void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
+  configure_fast_kernel();
+  k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head,
+                                  (unsigned long long)blocks * kWarpsPerBlock);
+  k_fast_segment<<<blocks, kThreads, smem, s>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
+                        uint64_t hist0, cudaStream_t s) {
+  if (!n) return;
+  k_aos_to_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, m, out, hist0);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+}  // namespace hwwg

@@ -1,5 +1,4 @@
 set -x
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 600 python bench.py --steps 5 --warmup 3 --histories 100000 --no-cpu-baseline > gpurun_out/bench_small.log 2>&1; echo bench=$?
-tail -15 gpurun_out/pytest_gpu.log
+timeout 300 python bench.py --rng philox --steps 6 --warmup 1 --histories 100000 --no-cpu-baseline > gpurun_out/bench_fast_small.log 2>&1; echo bench_fast_small=$?
+CMD="python bench.py --rng philox --steps 6 --warmup 0 --no-cpu-baseline"
+timeout 300 $CMD > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_fast.csv $CMD > gpurun_out/ncu.log 2>&1; echo ncu=$?

@@ -1,0 +1,76 @@
+"""Throughput (Philox) mode against the reference algorithm: statistical parity.
+
+The Philox mode draws different random numbers than the reference, so it is
+judged as an estimator: tallies agree within a few combined
+standard errors on >= 95% of the well-sampled cells, with sigma from batch
+statistics (step 1, common pulse source) or from independent replicates
+(later steps, where the comb adds inter-step noise the batch sigma misses —
+proj/tests/acceptance_main.cpp:225-231, 270, 283-285)."""
+import numpy as np
+import pytest
+
+import paper_2512_19925_b200 as hw
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg(which, H, steps, seed):
+    if which == 1:
+        return hw.RunConfig(mode="hww_ma", ma_base_k=3, histories_per_step=H, rho=5.0, seed=seed,
+                            material=hw.Material(1.0, 1.0, 0.0, 0.0, 1.0), x_min=-20.0,
+                            x_max=20.0, cells=200, t_end=1.0 * steps, time_steps=steps)
+    return hw.RunConfig(mode="hww_ma", ma_base_k=1, histories_per_step=H, rho=5.0, seed=seed,
+                        material=hw.Material(1.0, 0.9, 0.0, 0.0, 1.0), x_min=-20.0, x_max=20.0,
+                        cells=400, t_end=0.5 * steps, time_steps=steps)
+
+
+def run(c, rng):
+    d = hw.Driver(c, rng_mode=rng)
+    out = []
+    for _ in range(c.time_steps):
+        rec = d.step()
+        out.append((rec, d.arrays()))
+    d.close()
+    return out
+
+
+@pytest.mark.parametrize("which", [1, 2])
+def test_step1_within_batch_sigma(which):
+    H = 200_000
+    ex = run(cfg(which, H, 1, 42), hw.RNG_EXACT)[0]
+    fa = run(cfg(which, H, 1, 43), hw.RNG_PHILOX)[0]
+    a, b = ex[1], fa[1]
+    sig = np.sqrt(a["sigma"] ** 2 + b["sigma"] ** 2)
+    mask = a["phi_track"] > 1e-3 * a["phi_track"].max()
+    z = np.abs(a["phi_track"] - b["phi_track"])[mask] / sig[mask]
+    assert np.mean(z < 3.0) >= 0.95, np.sort(z)[-10:]
+    # census weight per history (the growth law) and the segment count
+    sw = np.hypot(ex[0].census_weight_sigma, fa[0].census_weight_sigma)
+    assert abs(ex[0].census_weight - fa[0].census_weight) <= 4 * sw + 1e-12
+    assert abs(fa[0].segments / ex[0].segments - 1) < (0.02 if which == 1 else 0.1)  # C2 step 1 is heavy-tailed
+
+
+def test_replicates_agree_over_steps():
+    """Config-1 physics, 6 steps, R = 6 seeds per mode: per-cell replicate means of
+    phi_track agree within 3 combined standard errors on >= 95% of cells."""
+    H, N, R = 20_000, 6, 6
+    ex = np.array([[s[1]["phi_track"] for s in run(cfg(1, H, N, 100 + r), hw.RNG_EXACT)]
+                   for r in range(R)])
+    fa = np.array([[s[1]["phi_track"] for s in run(cfg(1, H, N, 200 + r), hw.RNG_PHILOX)]
+                   for r in range(R)])
+    for n in range(N):
+        m_e, m_f = ex[:, n].mean(0), fa[:, n].mean(0)
+        se = np.sqrt(ex[:, n].var(0, ddof=1) / R + fa[:, n].var(0, ddof=1) / R)
+        mask = (m_e > 1e-3 * m_e.max()) & (se > 0)
+        z = np.abs(m_e - m_f)[mask] / se[mask]
+        assert np.mean(z < 3.0) >= 0.95, (n, np.sort(z)[-8:])
+
+
+def test_philox_run_is_conservative():
+    """Weight bookkeeping of one fast step: census + leakage + captured weight
+    matches the analog balance within the batch sigma (c = 1: no capture)."""
+    rec, arr = run(cfg(1, 100_000, 1, 5), hw.RNG_PHILOX)[0]
+    # c = 1, vacuum boundaries: all weight either leaks or is banked at census
+    total = rec.census_weight * 100_000 + rec.counters.leakage_weight
+    assert abs(total / 100_000 - 1.0) < 5 * rec.census_weight_sigma + 1e-3
+    assert rec.census_size == rec.counters.census_count
