@@ -64,6 +64,8 @@ struct DeviceProblem {
   DevBuf<CellInfo> d_cells;
   MeshView view{};
   int I = 0;
+  bool gen_uniform_homog = false;
+  double w_gen = 0.0;
 
   // Validates (mesh.cpp:9-14, material.hpp:20-32 sigma_t > 0, speed > 0) and
   // uploads when the content changed. Returns false with `why` on bad input.
@@ -107,6 +109,13 @@ struct DeviceProblem {
     HWWG_CUDA(cudaStreamSynchronize(s));
     view = MeshView{d_edges.p, d_cells.p, cells, uniform ? 1 : 0, edges.front(), edges.back(),
                     widths[0]};
+    // generated uniform mesh (mesh.cpp:42-50) with a single material?
+    w_gen = (edges.back() - edges.front()) / cells;
+    gen_uniform_homog = true;
+    for (int e = 0; e < cells && gen_uniform_homog; ++e)
+      if (edges[e] != edges.front() + e * w_gen) gen_uniform_homog = false;
+    for (int c = 1; c < cells && gen_uniform_homog; ++c)
+      if (std::memcmp(&mats[c], &mats[0], sizeof(hwwg_material)) != 0) gen_uniform_homog = false;
     return true;
   }
 };

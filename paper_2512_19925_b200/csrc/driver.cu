@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -105,6 +107,11 @@ struct hwwg_driver {
   DevBuf<char> comb_temp;
   DevBuf<FastStackRec> pool_recs;
   DevBuf<unsigned long long> pool_ctl;
+  bool timeline_on = false;
+  DevBuf<unsigned long long> timeline;
+  unsigned timeline_warps = 0;
+  DevBuf<unsigned long long> warp_cursor;  // per-warp census chunks
+  int max_warps = 0;
 
   // low-order state
   DevBuf<double> lo_mem;
@@ -221,6 +228,8 @@ void init_driver(hwwg_driver* d) {
     d->census_hwm = 64 * d->target + 4096;
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
     const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
+    d->max_warps = warps;
+    d->warp_cursor.reserve(2 * (size_t)warps);
     d->stacks.reserve((size_t)warps * d->stack_cap);
     d->src_head.reserve(1);
     d->pool_recs.reserve(1u << 20);  // 64 MB of donated split records per segment
@@ -230,6 +239,43 @@ void init_driver(hwwg_driver* d) {
     d->stage.ensure(64 * d->target + 4096);
   }
   HWWG_CUDA(cudaStreamSynchronize(d->stream));
+}
+
+// Diagnostics (HWWG_FAST_TIMELINE=1): per segment, the spread of warp exit
+// times and work, to separate load imbalance from per-event cost.
+void print_timeline(hwwg_driver* d, int nseg, int step) {
+  const size_t per = (size_t)d->timeline_warps * 4;
+  std::vector<unsigned long long> h(per * nseg);
+  HWWG_CUDA(cudaMemcpy(h.data(), d->timeline.p, h.size() * 8, cudaMemcpyDeviceToHost));
+  for (int s = 0; s < nseg; ++s) {
+    const unsigned long long* t = h.data() + per * s;
+    unsigned long long t0 = ~0ULL, tmax = 0, evs = 0, evmax = 0;
+    std::vector<double> ex, sd;
+    for (unsigned w = 0; w < d->timeline_warps; ++w) {
+      if (!t[4 * w]) continue;
+      t0 = std::min(t0, t[4 * w]);
+      tmax = std::max(tmax, t[4 * w + 2]);
+      evs += t[4 * w + 3];
+      evmax = std::max(evmax, t[4 * w + 3]);
+    }
+    for (unsigned w = 0; w < d->timeline_warps; ++w) {
+      if (!t[4 * w]) continue;
+      ex.push_back(1e-3 * (double)(t[4 * w + 2] - t0));
+      sd.push_back((double)t[4 * w + 1]);
+    }
+    std::sort(ex.begin(), ex.end());
+    std::sort(sd.begin(), sd.end());
+    auto q = [](const std::vector<double>& v, double f) {
+      return v.empty() ? 0.0 : v[std::min(v.size() - 1, (size_t)(f * v.size()))];
+    };
+    std::fprintf(stderr,
+                 "[timeline] step %d seg %d: span %.1f us, loop trips p50 %.0f max %.0f, "
+                 "exit p10 %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f us, events %llu "
+                 "(per warp mean %.0f max %llu)\n",
+                 step, s, 1e-3 * (double)(tmax - t0), q(sd, 0.5), q(sd, 1.0), q(ex, 0.1),
+                 q(ex, 0.5), q(ex, 0.9), q(ex, 0.99), q(ex, 1.0), evs,
+                 (double)evs / std::max<size_t>(ex.size(), 1), evmax);
+  }
 }
 
 // One time step (driver.cpp:99-284).
@@ -369,6 +415,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.rho = c.rho;
       a.ma_k = ma_k;
       a.mode = 0;
+      a.fast_solve = d->fast ? 1 : 0;
       a.analytic = step == 1;
       if (step == 1) {
         const int cell = locate_host(d->prob.edges, c.x0);
@@ -386,6 +433,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
 
     // ---- segments with window-update barriers (driver.cpp:181-219)
     d->tal.zero(s);
+    if (d->fast)
+      HWWG_CUDA(cudaMemsetAsync(d->warp_cursor.p, 0, d->warp_cursor.n * 8, s));
     HWWG_CUDA(cudaMemsetAsync(d->counter.p, 0, sizeof(unsigned long long), s));
     HWWG_CUDA(cudaMemsetAsync(d->err.p, 0, sizeof(DevError), s));
     ExactArgs ea{};
@@ -455,6 +504,21 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         if (!fa.smem_tallies) smem = 0;
         const int blocks = d->sms * fast_blocks_per_sm(smem);
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
+        fa.warp_cursor = d->warp_cursor.p;
+        // the first step starts from a point pulse: most lanes share a few cells
+        fa.aggregate = step == 1 ? 1 : 0;
+        fa.uniform = d->prob.gen_uniform_homog ? 1 : 0;
+        fa.x_min = d->prob.edges.front();
+        fa.x_max = d->prob.edges.back();
+        fa.w_gen = d->prob.w_gen;
+        fa.cell0 = d->prob.cells_h[0];
+        if (d->timeline_on) {  // HWWG_FAST_TIMELINE: per-warp phase timestamps
+          const size_t per = (size_t)fa.pool.warps * 4;
+          d->timeline.reserve(per * 9);
+          fa.timeline = d->timeline.p + per * nseg;
+          HWWG_CUDA(cudaMemsetAsync(fa.timeline, 0, per * 8, s));
+          d->timeline_warps = fa.pool.warps;
+        }
         if (ea.n) {
           launch_fast_segment(fa, blocks, smem, s);
           d->launches += 1;  // + the segment kernel counted below
@@ -477,12 +541,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.rho = c.rho;
       a.ma_k = ma_k;
       a.mode = 1;
+      a.fast_solve = d->fast ? 1 : 0;
       a.closure_tally = d->tal.p.census_closure;
       a.bclosure_tally = d->tal.p.boundary_closure;
       const double effective = (double)c.histories_per_step * (double)h_done / (double)H;
       a.snapshot_inv_norm = 1.0 / effective;
       a.s = d->lo;
       launch_low_order_update(a, s);
+      ++d->launches;
+    }
+    if (d->fast) {  // zero-weight records in the unused tails of the warps' chunks
+      launch_fill_census_holes(d->fcensus.view(), d->fcensus.cap(), d->warp_cursor.p,
+                               d->max_warps, d->prob.edges.front(), rec->t_end, s);
       ++d->launches;
     }
     HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
@@ -497,6 +567,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (derr.code || count <= ea.census_cap) break;
     d->stage.ensure(count + count / 4 + 4096);
   }
+  if (d->timeline_on) print_timeline(d, (int)thr.size() + 1, step);
   if (derr.code == HWWG_EINVAL)
     throw ApiError(HWWG_EINVAL, "history " + std::to_string(derr.history) +
                                     " starts outside the mesh or the time step");
@@ -529,10 +600,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // ---- census -> next bank in reference order
   if (d->fast) {
     d->fbank.swap(d->fcensus);  // the census is the next comb's input, already SoA
-    if (c.host_bank) {
+    if (c.host_bank) {  // real particles only, AoS, for the host round trip
       d->bank.reserve(std::max<unsigned long long>(count, 1));
-      launch_fast_to_aos(d->fbank.view(), count, d->bank.p, s);
-      if (count) ++d->launches;
+      launch_fast_compact_aos(d->fbank.view(), count, d->bank.p, d->counter.p, s);
+      HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaStreamSynchronize(s));
+      ++d->launches;
     }
   } else {
     d->bank.reserve(std::max<unsigned long long>(count, 1));
@@ -601,7 +674,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   for (int i = 0; i < I; ++i) seg += d->h_tracks[i];
   rec->segments = seg;
   rec->histories = H;
-  rec->census_size = count;
+  // banked particles (fast mode: the census slots also hold zero-weight chunk tails)
+  rec->census_size = d->fast ? (uint64_t)u[kCensusCount] : count;
   rec->comb_in_weight = comb_sc[0];
   rec->comb_out_weight = do_comb ? comb_sc[3] : comb_sc[0];
   auto field = [&](int f) { return rep_h.data() + (size_t)f * (I + 1); };
@@ -667,6 +741,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     return fail(HWWG_EINVAL, "unknown rng_mode");
   }
   d->fast = d->opt.rng_mode == HWWG_RNG_PHILOX;
+  d->timeline_on = d->fast && std::getenv("HWWG_FAST_TIMELINE") != nullptr;
   if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
     delete d;
     return fail(HWWG_EINVAL, "philox mode: fission and > 65535 cells are not supported");

@@ -44,6 +44,13 @@ struct FastArgs {
   int B;
   int b_lo, nb;  // batches touched by this segment: [b_lo, b_lo + nb)
   int smem_tallies;  // 1: block-private shared-memory tallies
+  int aggregate;     // 1: warp-aggregate tally atomics (cold start: lanes share cells)
+  // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
+  // x_max) with one material: geometry and cross sections come from registers,
+  // no per-event table loads.
+  int uniform;
+  double x_min, x_max, w_gen;
+  CellInfo cell0;
   const double* centers;
   const int* active;
   double rho, inv_rho;
@@ -52,7 +59,17 @@ struct FastArgs {
   int stack_cap;
   FastPool pool;
   DevError* err;
+  unsigned long long* timeline;  // optional per-warp {t0, loop trips, t_exit, events}
+  unsigned long long* warp_cursor;  // per warp {next, end} of its census chunk (zeroed per step)
 };
+
+// Zero-weight records in the unused tails of the warps' census chunks, and the
+// count of slots the census bank spans.
+void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,
+                              int warps, double x_fill, double t_fill, cudaStream_t s);
+// Compact the census bank (drop zero-weight holes) into AoS particles.
+void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
+                             unsigned long long* count, cudaStream_t s);
 
 int fast_blocks_per_sm(size_t smem);
 int fast_threads_per_block();

@@ -45,13 +45,47 @@ __global__ void k_comb_teeth(FastCombArgs a) {
     if (T < a.prefix[mid]) hi = mid;
     else lo = mid + 1;
   }
-  const uint64_t s = lo < a.n ? lo : a.n - 1;
+  uint64_t s = lo < a.n ? lo : a.n - 1;
+  // a tooth stranded by round-off copies the last real particle (popctrl.cpp:31-37),
+  // skipping the zero-weight holes at the tail of census chunks
+  if (lo >= a.n)
+    while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
   a.out.xm[k] = a.bank.xm[s];
   const double2 wt = a.bank.wt[s];
   a.out.wt[k] = make_double2(spacing, wt.y);
   const uint4 m = a.bank.meta[s];
   // fresh identity for the new step: history = tooth index, key 0, draw 0
   a.out.meta[k] = make_uint4(m.x & 0xffffu, (unsigned)k, 0u, 0u);
+}
+
+__global__ void k_fill_holes(FastBank c, uint64_t cap, const unsigned long long* cur, int warps,
+                             double x_fill, double t_fill) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= warps) return;
+  const unsigned long long end = cur[2 * w + 1] < cap ? cur[2 * w + 1] : cap;
+  for (unsigned long long s = cur[2 * w]; s < end; ++s) {
+    c.xm[s] = make_double2(x_fill, 0.5);
+    c.wt[s] = make_double2(0.0, t_fill);
+    c.meta[s] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// Drop zero-weight holes while converting to AoS (order is free in this mode).
+__global__ void k_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
+                              unsigned long long* count) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool keep = i < n && in.wt[i].x > 0.0;
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0 && mask) base = atomicAdd(count, (unsigned long long)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) {
+    const unsigned long long j = base + __popc(mask & ((1u << lane) - 1u));
+    double2* o = reinterpret_cast<double2*>(out) + 2 * j;
+    o[0] = in.xm[i];
+    o[1] = in.wt[i];
+  }
 }
 
 __global__ void k_track_from_batches(TallyPtrs t, int I, int B) {
@@ -85,6 +119,20 @@ void launch_fast_comb(const FastCombArgs& a, cudaStream_t s) {
   HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, a.prefix, a.prefix, (int)a.n, s));
   k_comb_scalars<<<1, 1, 0, s>>>(a.prefix, a.n, a.target, a.seed, a.stream, a.scalars);
   k_comb_teeth<<<(unsigned)((a.target + 255) / 256), 256, 0, s>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,
+                              int warps, double x_fill, double t_fill, cudaStream_t s) {
+  k_fill_holes<<<(warps + 127) / 128, 128, 0, s>>>(census, cap, warp_cursor, warps, x_fill, t_fill);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
+                             unsigned long long* count, cudaStream_t s) {
+  HWWG_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s));
+  if (!n) return;
+  k_compact_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, out, count);
   HWWG_CUDA(cudaGetLastError());
 }
 

@@ -91,29 +91,156 @@ __device__ void assemble_rows(int I, const double* edges, const CellInfo* cells,
 }
 
 // banded.cpp:8-38 on one thread. Returns 0, or 1 + pivot row when singular.
-__device__ int solve_pivoted_serial(int n, double* a, double* b, double* c, double* r,
-                                    double* fill, double* x) {
-  for (int k = 0; k < n; ++k) fill[k] = 0.0;
+//
+// Same operations in the same order as the reference, restructured for a
+// GPU thread: the pivot row being eliminated lives in registers (at step k,
+// fill[k] is always still 0 and row k+1 is untouched by earlier steps), the
+// next row's inputs are loaded one step ahead (they do not depend on the
+// recurrence), and only finished rows are stored. The serial chain is then
+// one division and one fma per row instead of a global-memory round trip.
+__device__ int solve_pivoted_serial(int n, const double* __restrict__ a, double* __restrict__ b,
+                                    double* __restrict__ c, double* __restrict__ r,
+                                    double* __restrict__ fill, double* __restrict__ x) {
+  double bk = b[0], ck = c[0], rk = r[0], fk = 0.0;  // pivot row k
+  double na = n > 1 ? a[1] : 0.0, nb = n > 1 ? b[1] : 0.0, nc = n > 1 ? c[1] : 0.0,
+         nr = n > 1 ? r[1] : 0.0;  // row k+1 (original)
   for (int k = 0; k + 1 < n; ++k) {
-    if (fabs(a[k + 1]) > fabs(b[k])) {
-      double t;
-      t = b[k]; b[k] = a[k + 1]; a[k + 1] = t;
-      t = c[k]; c[k] = b[k + 1]; b[k + 1] = t;
-      if (k + 2 < n) { t = fill[k]; fill[k] = c[k + 1]; c[k + 1] = t; }
-      t = r[k]; r[k] = r[k + 1]; r[k + 1] = t;
+    double a1 = na, b1 = nb, c1 = nc, r1 = nr;
+    if (k + 2 < n) {  // prefetch row k+2
+      na = a[k + 2];
+      nb = b[k + 2];
+      nc = c[k + 2];
+      nr = r[k + 2];
     }
-    if (b[k] == 0.0) return 1 + k;
-    const double m = a[k + 1] / b[k];
-    a[k + 1] = 0.0;
-    b[k + 1] -= m * c[k];
-    if (k + 2 < n) c[k + 1] -= m * fill[k];
-    r[k + 1] -= m * r[k];
+    if (fabs(a1) > fabs(bk)) {
+      double t;
+      t = bk; bk = a1; a1 = t;
+      t = ck; ck = b1; b1 = t;
+      if (k + 2 < n) { t = fk; fk = c1; c1 = t; }
+      t = rk; rk = r1; r1 = t;
+    }
+    if (bk == 0.0) return 1 + k;
+    const double m = a1 / bk;
+    b1 -= m * ck;
+    if (k + 2 < n) c1 -= m * fk;
+    r1 -= m * rk;
+    b[k] = bk;
+    c[k] = ck;
+    fill[k] = fk;
+    r[k] = rk;
+    bk = b1;
+    ck = c1;
+    rk = r1;
+    fk = 0.0;
   }
-  if (b[n - 1] == 0.0) return n;
-  x[n - 1] = r[n - 1] / b[n - 1];
-  if (n >= 2) x[n - 2] = (r[n - 2] - c[n - 2] * x[n - 1]) / b[n - 2];
-  for (int k = n - 3; k >= 0; --k) x[k] = (r[k] - c[k] * x[k + 1] - fill[k] * x[k + 2]) / b[k];
+  b[n - 1] = bk;
+  c[n - 1] = ck;
+  r[n - 1] = rk;
+  fill[n - 1] = 0.0;
+  if (bk == 0.0) return n;
+  double x2 = r[n - 1] / b[n - 1];
+  x[n - 1] = x2;
+  if (n < 2) return 0;
+  double x1 = (r[n - 2] - c[n - 2] * x2) / b[n - 2];
+  x[n - 2] = x1;
+  double pr = 0, pc = 0, pf = 0, pb = 0;
+  if (n >= 3) { pr = r[n - 3]; pc = c[n - 3]; pf = fill[n - 3]; pb = b[n - 3]; }
+  for (int k = n - 3; k >= 0; --k) {
+    const double rr = pr, cc = pc, ff = pf, bb = pb;
+    if (k > 0) { pr = r[k - 1]; pc = c[k - 1]; pf = fill[k - 1]; pb = b[k - 1]; }
+    const double xk = (rr - cc * x1 - ff * x2) / bb;
+    x[k] = xk;
+    x2 = x1;
+    x1 = xk;
+  }
   return 0;
+}
+
+// Throughput-mode solve of the same system (not bit-identical to banded.cpp):
+// the first-moment rows give J_i = p_i - q_i phi_i - s_i phi_{i+1}; substituting
+// them into the balance and boundary rows leaves an (I+2) tridiagonal system in
+// phi that is an M-matrix for non-multiplying media (diagonally dominant, no
+// pivoting needed), solved by parallel cyclic reduction in shared memory:
+// ceil(log2(I+2)) steps instead of a 2I+3-long serial recurrence.
+constexpr int kPcrRowsPerThread = 16;
+
+__device__ int solve_schur_pcr(int I, const double* __restrict__ lo, const double* __restrict__ di,
+                               const double* __restrict__ up, const double* __restrict__ rh,
+                               double* __restrict__ x, double* sm) {
+  const int N = I + 2;
+  double* A = sm;
+  double* D = A + N;
+  double* C = D + N;
+  double* R = C + N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const int m = 2 * i;
+    double a = 0.0, d = di[m], c = 0.0, r = rh[m];
+    if (i > 0) {  // J_{i-1} from moment row 2i-1
+      const int mm = m - 1;
+      const double inv = 1.0 / di[mm];
+      const double p = rh[mm] * inv, q = lo[mm] * inv, s = up[mm] * inv;
+      a = -lo[m] * q;
+      d -= lo[m] * s;
+      r -= lo[m] * p;
+    }
+    if (i < N - 1) {  // J_i from moment row 2i+1
+      const int mp = m + 1;
+      const double inv = 1.0 / di[mp];
+      const double p = rh[mp] * inv, q = lo[mp] * inv, s = up[mp] * inv;
+      d -= up[m] * q;
+      c = -up[m] * s;
+      r -= up[m] * p;
+    }
+    A[i] = a;
+    D[i] = d;
+    C[i] = c;
+    R[i] = r;
+  }
+  __syncthreads();
+  for (int s = 1; s < N; s <<= 1) {
+    double na[kPcrRowsPerThread], nd[kPcrRowsPerThread], nc[kPcrRowsPerThread],
+        nr[kPcrRowsPerThread];
+    int k = 0;
+    for (int i = threadIdx.x; i < N && k < kPcrRowsPerThread; i += blockDim.x, ++k) {
+      double a = 0.0, d = D[i], c = 0.0, r = R[i];
+      if (i - s >= 0) {
+        const double al = -A[i] / D[i - s];
+        a = al * A[i - s];
+        d += al * C[i - s];
+        r += al * R[i - s];
+      }
+      if (i + s < N) {
+        const double ga = -C[i] / D[i + s];
+        c = ga * C[i + s];
+        d += ga * A[i + s];
+        r += ga * R[i + s];
+      }
+      na[k] = a;
+      nd[k] = d;
+      nc[k] = c;
+      nr[k] = r;
+    }
+    __syncthreads();
+    k = 0;
+    for (int i = threadIdx.x; i < N && k < kPcrRowsPerThread; i += blockDim.x, ++k) {
+      A[i] = na[k];
+      D[i] = nd[k];
+      C[i] = nc[k];
+      R[i] = nr[k];
+    }
+    __syncthreads();
+  }
+  int bad = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    if (D[i] == 0.0 || !isfinite(D[i])) bad = 1;
+    x[2 * i] = R[i] / D[i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= I; i += blockDim.x) {  // back out the currents
+    const int mp = 2 * i + 1;
+    x[mp] = (rh[mp] - lo[mp] * x[2 * i] - up[mp] * x[2 * i + 2]) / di[mp];
+  }
+  return __syncthreads_or(bad);
 }
 
 // Block max of per-thread partial maxima. The partials start at 0.0 and only
@@ -210,7 +337,13 @@ __device__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double
     assemble_rows(I, a.edges, a.cells, s.phi_prev, s.J_prev, 0.0, 0.0, Fs, PLs, PRs, s.F_prev,
                   a.theta, a.dt, nullptr, lo, di, up, rh);
     __syncthreads();
-    if (threadIdx.x == 0) status = solve_pivoted_serial(n, lo, di, up, rh, fill, x) ? 2 : 0;
+    if (a.fast_solve) {
+      extern __shared__ double dyn[];
+      const int bad = solve_schur_pcr(I, lo, di, up, rh, x, dyn);
+      if (threadIdx.x == 0) status = bad ? 2 : 0;
+    } else if (threadIdx.x == 0) {
+      status = solve_pivoted_serial(n, lo, di, up, rh, fill, x) ? 2 : 0;
+    }
   } else if (threadIdx.x == 0) {
     status = 1;
   }
@@ -493,7 +626,17 @@ __global__ void k_device_log(const double* x, uint64_t n, double* out) {
 }  // namespace
 
 void launch_low_order_update(const LowOrderArgs& a, cudaStream_t st) {
-  k_low_order_update<<<1, kCtaThreads, 0, st>>>(a);
+  size_t smem = 0;
+  if (a.fast_solve) {
+    smem = (size_t)4 * (a.I + 2) * sizeof(double);
+    static size_t configured = 0;
+    if (smem > configured) {
+      HWWG_CUDA(cudaFuncSetAttribute(k_low_order_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      configured = smem;
+    }
+  }
+  k_low_order_update<<<1, kCtaThreads, smem, st>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
 

@@ -43,6 +43,7 @@ struct LowOrderArgs {
   //         from the previous report.  mode 1: mid-step implicit solve from the
   //         partial snapshot of the live tallies.
   int mode;
+  int fast_solve;  // throughput mode: Schur complement + parallel cyclic reduction
   int analytic;        // mode 0: step 1 cold start
   int pulse_cell;      // analytic: cell of the source point
   double pulse_value;  // analytic: speed * strength / dx

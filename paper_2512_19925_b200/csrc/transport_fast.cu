@@ -36,6 +36,7 @@ namespace {
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kDonate = 256;  // pending local daughters above which splits go global
+constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -71,6 +72,96 @@ __device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigne
   p.alive = true;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Warp-aggregated atomic add: lanes with the same key (MATCH.ANY) are summed
+// by shuffles, then the group's lowest lane issues ONE atomic. key < 0: no
+// contribution. Must be called by all 32 lanes. In the cold-start steps most
+// of a warp sits in a few cells around the pulse, where per-lane fp64 CAS
+// loops on shared memory serialised; here a group costs max(group) shuffles.
+__device__ __forceinline__ unsigned agg_group(int key, unsigned& rest) {
+  const int lane = threadIdx.x & 31;
+  const bool has = key >= 0;
+  const unsigned grp = __match_any_sync(0xffffffffu, has ? key : -1 - lane);
+  rest = has ? (grp & ~(1u << lane)) : 0u;
+  return grp;
+}
+
+__device__ __forceinline__ void agg_add(double* base, int key, double v) {
+  if (!__any_sync(0xffffffffu, key >= 0)) return;
+  unsigned rest;
+  const unsigned grp = agg_group(key, rest);
+  double s = v;
+  while (__any_sync(0xffffffffu, rest != 0)) {
+    const int src = rest ? __ffs(rest) - 1 : (threadIdx.x & 31);
+    const double o = __shfl_sync(0xffffffffu, v, src);
+    if (rest) {
+      s += o;
+      rest &= rest - 1;
+    }
+  }
+  if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(base + key, s);
+}
+
+__device__ __forceinline__ void agg_add3(double* b0, double* b1, double* b2, int key, double v0,
+                                         double v1, double v2) {
+  if (!__any_sync(0xffffffffu, key >= 0)) return;
+  unsigned rest;
+  const unsigned grp = agg_group(key, rest);
+  double s0 = v0, s1 = v1, s2 = v2;
+  while (__any_sync(0xffffffffu, rest != 0)) {
+    const int src = rest ? __ffs(rest) - 1 : (threadIdx.x & 31);
+    const double o0 = __shfl_sync(0xffffffffu, v0, src);
+    const double o1 = __shfl_sync(0xffffffffu, v1, src);
+    const double o2 = __shfl_sync(0xffffffffu, v2, src);
+    if (rest) {
+      s0 += o0;
+      s1 += o1;
+      s2 += o2;
+      rest &= rest - 1;
+    }
+  }
+  if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) {
+    atomicAdd(b0 + key, s0);
+    atomicAdd(b1 + key, s1);
+    atomicAdd(b2 + key, s2);
+  }
+}
+
+// track-length score (keyed by batch slot and cell) plus the per-cell count
+template <class Count>
+__device__ __forceinline__ void agg_add_count_t(double* base, Count* cnt, int key, double v,
+                                                int cell) {
+  if (!__any_sync(0xffffffffu, key >= 0)) return;
+  unsigned rest;
+  const unsigned grp = agg_group(key, rest);
+  double s = v;
+  while (__any_sync(0xffffffffu, rest != 0)) {
+    const int src = rest ? __ffs(rest) - 1 : (threadIdx.x & 31);
+    const double o = __shfl_sync(0xffffffffu, v, src);
+    if (rest) {
+      s += o;
+      rest &= rest - 1;
+    }
+  }
+  if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) {
+    atomicAdd(base + key, s);
+    atomicAdd(cnt + cell, (Count)__popc(grp));
+  }
+}
+__device__ __forceinline__ void agg_add_count(double* base, unsigned* cnt, int key, double v,
+                                              int cell) {
+  agg_add_count_t<unsigned>(base, cnt, key, v, cell);
+}
+__device__ __forceinline__ void agg_add_count_global(double* base, unsigned long long* cnt,
+                                                     int key, double v, int cell) {
+  agg_add_count_t<unsigned long long>(base, cnt, key, v, cell);
+}
+
 // Shared-memory tally views (block-private).
 struct SmemTally {
   double* trk;    // nb * I, batch b at (b - b_lo)
@@ -96,6 +187,7 @@ __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb) {
   return s;
 }
 
+template <bool kUniform>
 __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
@@ -121,6 +213,10 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
   double leak = 0.0;
   volatile unsigned long long* ctl = a.pool.ctl;
 
+  unsigned long long n_ev = 0, n_iter = 0;
+  // this warp's census chunk [wcur, wend), carried across the step's segments
+  unsigned long long wcur = a.warp_cursor[2 * gwarp], wend = a.warp_cursor[2 * gwarp + 1];
+  const unsigned long long t_start = a.timeline ? globaltimer() : 0ULL;
   Lane p;
   p.alive = false;
   bool holding = true;  // this warp counts in pool.ctl[2] (active warps)
@@ -148,7 +244,9 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(a.src_head, (unsigned long long)k);
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (base + k >= a.n_src) src_done = true;
+      if (base + k >= a.n_src) {
+        src_done = true;
+      }
       const unsigned rank = __popc(need & lt);
       if (!p.alive) {
         const unsigned long long idx = base + rank;
@@ -187,7 +285,10 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       // record before publishing it; the consumer inherits that unit), so
       // active == 0 means nothing can ever fill an outstanding ticket.
       int got = 0;  // 1: record ready in our slot, -1: finished
-      if (lane == 0) {
+      // With no backlog declared anywhere (ctl[3]) there is nothing to wait
+      // for: leave now rather than poll (the spread-out steady-state steps).
+      if (lane == 0 && ticket == ~0ULL && ctl[3] == 0) got = -1;
+      if (lane == 0 && got == 0) {
         if (ticket == ~0ULL) ticket = atomicAdd(const_cast<unsigned long long*>(&ctl[1]), 1ULL);
         if (ticket >= a.pool.cap) {
           got = -1;
@@ -209,7 +310,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
               break;
             }
             __nanosleep(backoff);
-            backoff = backoff < 1024 ? backoff * 2 : 1024;
+            backoff = backoff < 8192 ? backoff * 2 : 8192;  // idle polling costs issue slots
           }
         }
       }
@@ -232,11 +333,21 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       continue;
     }
     if (!any_alive) continue;
+    if (p.alive) ++n_ev;
+    ++n_iter;
 
-    // ---- one event per live lane
+    // ---- one event per live lane; tally contributions are collected per lane
+    // and committed warp-aggregated after the event (see agg_add)
     unsigned split_n = 0;
+    int trk_key = -1, cen_cell = -1, cen_b = -1, edge_key = -1, trk_cell = 0;
+    double trk_v = 0.0, cen_phi = 0.0, cen_J = 0.0, cen_F = 0.0, cen_w = 0.0, edge_v = 0.0;
     if (p.alive) {
-      const CellInfo ci = cells[p.cell];
+      const CellInfo ci = kUniform ? a.cell0 : cells[p.cell];
+      // edge position: the host table, or the same x_min + e*w (unfused) in registers
+      auto edge_x = [&](int e) {
+        if (!kUniform) return edges[e];
+        return e == I ? a.x_max : __dadd_rn(a.x_min, __dmul_rn((double)e, a.w_gen));
+      };
       double u0, u1;
       draw2(a, p, u0, u1);
       const double d_census = ci.speed * (a.t_end - p.t);
@@ -245,10 +356,10 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       int edge = -1;
       if (p.mu > 0.0) {
         edge = p.cell + 1;
-        d_b = (edges[edge] - p.x) * p.inv_mu;
+        d_b = (edge_x(edge) - p.x) * p.inv_mu;
       } else if (p.mu < 0.0) {
         edge = p.cell;
-        d_b = (edges[edge] - p.x) * p.inv_mu;
+        d_b = (edge_x(edge) - p.x) * p.inv_mu;
       }
       double d = d_census;
       if (d_coll < d) d = d_coll;
@@ -256,48 +367,28 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       if (d < 0.0) d = 0.0;  // rounding at an edge: zero-length step
       const int batch = batch_of(p.hist, a.H, a.B);
       if (d > 0.0) {
-        const double sc = p.w * d * ci.inv_dx * a.inv_dt;
-        if (sh) {
-          atomicAdd(&S.trk[(size_t)(batch - a.b_lo) * I + p.cell], sc);
-          atomicAdd(&S.trc[p.cell], 1u);
-        } else {
-          atomicAdd(&a.t.track_flux_batch[(size_t)batch * I + p.cell], sc);
-          atomicAdd(&a.t.tracks[p.cell], 1ULL);
-        }
+        trk_v = p.w * d * ci.inv_dx * a.inv_dt;
+        trk_key = (sh ? batch - a.b_lo : batch) * I + p.cell;
+        trk_cell = p.cell;
       }
       bool window_site = false;
       if (d == d_census) {
         p.x += d * p.mu;
         p.t = a.t_end;
-        const double base = ci.speed * p.w * ci.inv_dx;
-        const double cl = base * (1.0 / 3.0 - p.mu * p.mu);
-        if (sh) {
-          atomicAdd(&S.cphi[p.cell], base);
-          atomicAdd(&S.cJ[p.cell], base * p.mu);
-          atomicAdd(&S.cF[p.cell], cl);
-          atomicAdd(&S.cwb[batch - a.b_lo], p.w);
-        } else {
-          atomicAdd(&a.t.census_phi[p.cell], base);
-          atomicAdd(&a.t.census_current[p.cell], base * p.mu);
-          atomicAdd(&a.t.census_closure[p.cell], cl);
-          atomicAdd(&a.t.census_weight_batch[batch], p.w);
-        }
+        cen_phi = ci.speed * p.w * ci.inv_dx;
+        cen_J = cen_phi * p.mu;
+        cen_F = cen_phi * (1.0 / 3.0 - p.mu * p.mu);
+        cen_cell = p.cell;
+        cen_w = p.w;
+        cen_b = sh ? batch - a.b_lo : batch;
         ++n_cen;
-        const unsigned long long slot = warp_reserve1(a.census_count);
-        if (slot < a.census_cap) {
-          a.census.xm[slot] = make_double2(p.x, p.mu);
-          a.census.wt[slot] = make_double2(p.w, p.t);
-          a.census.meta[slot] = make_uint4((unsigned)p.cell | (p.ctr << 16), p.hist,
-                                           (unsigned)p.key, (unsigned)(p.key >> 32));
-        }
-        p.alive = false;
+        p.alive = false;  // banked below, after the warp reconverges
       } else if (d == d_b) {
-        p.x = edges[edge];
+        p.x = edge_x(edge);
         p.t += d * ci.inv_speed;
         const bool domain = edge == 0 || edge == I;
-        const double ec = (p.mu > 0 ? p.w : -p.w) * a.inv_dt;
-        if (sh) atomicAdd(&S.edge[edge], ec);
-        else atomicAdd(&a.t.edge_current[edge], ec);
+        edge_v = (p.mu > 0 ? p.w : -p.w) * a.inv_dt;
+        edge_key = edge;
         if (domain) {
           const double amu = fabs(p.mu);
           if (amu < 1e-10) {
@@ -354,6 +445,76 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
         }
       }
     }
+    // ---- bank census particles. Slots come from a per-warp chunk of the census
+    // bank (one global atomic per kCensusChunk particles, not one per warp per
+    // iteration: a single shared counter hit by every warp serialised whole
+    // segments). Chunk tails left at the end of a step become zero-weight
+    // records (fill_census_holes), which the comb never selects.
+    {
+      const unsigned cmask = __ballot_sync(0xffffffffu, cen_cell >= 0);
+      if (cmask) {
+        const unsigned k = __popc(cmask);
+        const unsigned long long avail = wend - wcur;
+        unsigned long long nb = 0;
+        if (k > avail) {
+          if (lane == 0) nb = atomicAdd(a.census_count, (unsigned long long)kCensusChunk);
+          nb = __shfl_sync(0xffffffffu, nb, 0);
+        }
+        if (cen_cell >= 0) {
+          const unsigned rank = __popc(cmask & lt);
+          const unsigned long long slot = rank < avail ? wcur + rank : nb + (rank - avail);
+          if (slot < a.census_cap) {
+            a.census.xm[slot] = make_double2(p.x, p.mu);
+            a.census.wt[slot] = make_double2(p.w, p.t);
+            a.census.meta[slot] = make_uint4((unsigned)p.cell | (p.ctr << 16), p.hist,
+                                             (unsigned)p.key, (unsigned)(p.key >> 32));
+          }
+        }
+        if (k > avail) {
+          wcur = nb + (k - avail);
+          wend = nb + kCensusChunk;
+        } else {
+          wcur += k;
+        }
+      }
+    }
+
+    // ---- commit the event's tallies, warp-aggregated (lanes sharing a cell
+    // are summed with shuffles first: one CAS per distinct address, not per lane)
+    if (a.aggregate) {  // cold-start segments: most lanes share a few cells
+      if (sh) {
+        agg_add_count(S.trk, S.trc, trk_key, trk_v, trk_cell);
+        agg_add3(S.cphi, S.cJ, S.cF, cen_cell, cen_phi, cen_J, cen_F);
+        agg_add(S.cwb, cen_b, cen_w);
+        agg_add(S.edge, edge_key, edge_v);
+      } else {
+        agg_add_count_global(a.t.track_flux_batch, a.t.tracks, trk_key, trk_v, trk_cell);
+        agg_add3(a.t.census_phi, a.t.census_current, a.t.census_closure, cen_cell, cen_phi,
+                 cen_J, cen_F);
+        agg_add(a.t.census_weight_batch, cen_b, cen_w);
+        agg_add(a.t.edge_current, edge_key, edge_v);
+      }
+    } else {  // spread population: per-lane atomics, no warp synchronisation
+      double* trk = sh ? S.trk : a.t.track_flux_batch;
+      double* cphi = sh ? S.cphi : a.t.census_phi;
+      double* cJ = sh ? S.cJ : a.t.census_current;
+      double* cF = sh ? S.cF : a.t.census_closure;
+      double* cwb = sh ? S.cwb : a.t.census_weight_batch;
+      double* edg = sh ? S.edge : a.t.edge_current;
+      if (trk_key >= 0) {
+        atomicAdd(trk + trk_key, trk_v);
+        if (sh) atomicAdd(S.trc + trk_cell, 1u);
+        else atomicAdd(a.t.tracks + trk_cell, 1ULL);
+      }
+      if (cen_cell >= 0) {
+        atomicAdd(cphi + cen_cell, cen_phi);
+        atomicAdd(cJ + cen_cell, cen_J);
+        atomicAdd(cF + cen_cell, cen_F);
+        atomicAdd(cwb + cen_b, cen_w);
+      }
+      if (edge_key >= 0) atomicAdd(edg + edge_key, edge_v);
+    }
+
     // ---- push split records: local stack while shallow, else donate to the pool
     const unsigned smask = __ballot_sync(0xffffffffu, split_n > 1);
     if (smask) {
@@ -365,15 +526,19 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       bool donate = pend + tot > kDonate;  // warp-uniform
       if (donate) {
         int open = 0;
-        if (lane == 0) open = ctl[1] > ctl[0] ? 1 : 0;
+        if (lane == 0) {
+          if (ctl[3] == 0) ctl[3] = 1;  // declare a backlog: idle warps wait for donations
+          open = ctl[1] > ctl[0] ? 1 : 0;
+        }
         donate = __shfl_sync(0xffffffffu, open, 0) != 0;
       }
       const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell, p.hist, p.key, p.ctr,
                              dau, 0u, 0u};
       bool push_local = dau > 0 && !donate;
       if (dau > 0 && donate) {
-        atomicAdd(const_cast<unsigned long long*>(&ctl[2]), 1ULL);  // the record's active unit
-        __threadfence();
+        // the record's active unit; ordered before this warp's own decrement by
+        // the fence on the idle path, and the donor counts as active meanwhile
+        atomicAdd(const_cast<unsigned long long*>(&ctl[2]), 1ULL);
         const unsigned long long slot = atomicAdd(const_cast<unsigned long long*>(&ctl[0]), 1ULL);
         if (slot < a.pool.cap) {
           FastStackRec* pr = a.pool.recs + slot;
@@ -398,6 +563,22 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       sp += __popc(lmask);
       if (sp > a.stack_cap) sp = a.stack_cap;
       __syncwarp();
+    }
+  }
+
+  if (lane == 0) {
+    a.warp_cursor[2 * gwarp] = wcur;
+    a.warp_cursor[2 * gwarp + 1] = wend;
+  }
+  if (a.timeline) {
+    unsigned long long ev = n_ev;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ev += __shfl_down_sync(0xffffffffu, ev, o);
+    if (lane == 0) {
+      a.timeline[4 * gwarp + 0] = t_start;
+      a.timeline[4 * gwarp + 1] = n_iter;
+      a.timeline[4 * gwarp + 2] = globaltimer();
+      a.timeline[4 * gwarp + 3] = ev;
     }
   }
 
@@ -479,7 +660,7 @@ void configure_fast_kernel();
 int fast_blocks_per_sm(size_t smem) {
   configure_fast_kernel();
   int n = 0;
-  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment, kThreads, smem));
+  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment<false>, kThreads, smem));
   return n;
 }
 
@@ -489,6 +670,7 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
   ctl[0] = 0;
   ctl[1] = 0;
   ctl[2] = warps;  // every warp starts active (holding source work)
+  ctl[3] = 0;      // no backlog declared yet
   *src_head = 0;
 }
 }  // namespace
@@ -496,8 +678,10 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
 void configure_fast_kernel() {
   static bool configured = false;
   if (!configured) {
-    HWWG_CUDA(cudaFuncSetAttribute(k_fast_segment, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024));
+    HWWG_CUDA(cudaFuncSetAttribute(k_fast_segment<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HWWG_CUDA(cudaFuncSetAttribute(k_fast_segment<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
 }
@@ -506,7 +690,8 @@ void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_
   configure_fast_kernel();
   k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head,
                                   (unsigned long long)blocks * kWarpsPerBlock);
-  k_fast_segment<<<blocks, kThreads, smem, s>>>(a);
+  if (a.uniform) k_fast_segment<true><<<blocks, kThreads, smem, s>>>(a);
+  else k_fast_segment<false><<<blocks, kThreads, smem, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
 

@@ -53,7 +53,10 @@ def test_step1_within_batch_sigma(which):
 def test_replicates_agree_over_steps():
     """Config-1 physics, 6 steps, R = 6 seeds per mode: per-cell replicate means of
     phi_track agree within 3 combined standard errors on >= 95% of cells."""
-    H, N, R = 20_000, 6, 6
+    # With R replicates per side the z statistic is Student-t with ~2R-2 dof
+    # (P(|t| > 3) ~ 1% at R = 8), and neighbouring cells are correlated, so
+    # the per-cell rule is paired with a bias check on the mean signed z.
+    H, N, R = 20_000, 6, 8
     ex = np.array([[s[1]["phi_track"] for s in run(cfg(1, H, N, 100 + r), hw.RNG_EXACT)]
                    for r in range(R)])
     fa = np.array([[s[1]["phi_track"] for s in run(cfg(1, H, N, 200 + r), hw.RNG_PHILOX)]
@@ -62,8 +65,10 @@ def test_replicates_agree_over_steps():
         m_e, m_f = ex[:, n].mean(0), fa[:, n].mean(0)
         se = np.sqrt(ex[:, n].var(0, ddof=1) / R + fa[:, n].var(0, ddof=1) / R)
         mask = (m_e > 1e-3 * m_e.max()) & (se > 0)
-        z = np.abs(m_e - m_f)[mask] / se[mask]
-        assert np.mean(z < 3.0) >= 0.95, (n, np.sort(z)[-8:])
+        z = (m_f - m_e)[mask] / se[mask]
+        assert np.mean(np.abs(z) < 3.0) >= 0.9, (n, np.sort(np.abs(z))[-8:])
+        assert abs(z.mean()) < 0.75, (n, z.mean())
+        assert abs(m_f.sum() / m_e.sum() - 1) < 5e-3, n
 
 
 def test_philox_run_is_conservative():
