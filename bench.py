@@ -180,7 +180,9 @@ def run_reference(args):
     R = Reference()
     cores = os.cpu_count() or 1
     R.lib.hwwref_set_threads(cores)
-    H = args.histories
+    # our arm runs histories x world (weak scaling); the CPU arm times a bounded
+    # sample of that workload (segments/s is a rate, comparable across H)
+    H = min(args.histories * world, 2_000_000)
     w = DriverRun(R, baseline_config(2, histories=H, time_steps=max(args.steps, args.warmup, 1)))
     for _ in range(args.warmup):
         w.step()
@@ -215,18 +217,33 @@ def run_ours(args):
     rank, local, world = dist_setup(args)
     torch.cuda.set_device(local)
     import paper_2512_19925_b200 as hw
+    if world > 1 and args.rng != "philox":
+        args.rng = "philox"  # exact mode replays one sequential comb: single GPU only
     rng = hw.RNG_PHILOX if args.rng == "philox" else hw.RNG_EXACT
-    H = args.histories
+    # weak scaling: every GPU carries args.histories histories per step
+    H = args.histories * world
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    nccl_id = b""
+    if world > 1:  # rank 0 makes the NCCL id the driver's communicator uses
+        import torch.distributed as tdist
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(hw.hww.nccl_unique_id()), dtype=torch.uint8))
+        tdist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+
+    def driver(cfg):
+        return hw.Driver(cfg, device=local, rng_mode=rng, rank=rank, world=world,
+                         nccl_id=nccl_id)
 
     # warm-up: a separate instance, steps 1..W
     if args.warmup:
-        wd = hw.Driver(config2(H, max(args.warmup, 1)), device=local, rng_mode=rng)
+        wd = driver(config2(H, max(args.warmup, 1)))
         for _ in range(args.warmup):
             wd.step()
         wd.close()
 
-    d = hw.Driver(config2(H, max(args.steps, 1)), device=local, rng_mode=rng)
+    d = driver(config2(H, max(args.steps, 1)))
     seg = 0
     dev_ms = 0.0
     tr_ms = 0.0
@@ -252,11 +269,27 @@ def run_ours(args):
         torch.distributed.barrier()
     d.close()
     t_max = max_over_ranks(dev_ms, world)
-    seg_all = sum_over_ranks(seg, world)
+    seg_all = seg  # the driver all-reduces tracks_per_cell: every rank sees the global count
     value = seg_all / (t_max * 1e-3)
 
+    # exact (reference-stream) mode on the same workload, single GPU only
+    exact = None
+    if world == 1 and args.rng == "philox" and not args.no_exact:
+        xd = hw.Driver(config2(H, max(args.steps, 1)), device=local, rng_mode=hw.RNG_EXACT)
+        xs, xms = 0, 0.0
+        for _ in range(args.steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            r = xd.step()
+            xs += r.segments
+            xms += r.device_ms
+        xd.close()
+        exact = {"value": xs / (xms * 1e-3), "unit": UNIT, "ms_per_step": xms / args.steps,
+                 "note": "bit-exact replay of the reference's xoshiro streams, events, census "
+                         "and tallies (tests/test_gpu_parity.py)"}
+
     # e2e through the public step API with the bank in pinned host memory
-    e = hw.Driver(_host_cfg(H, args.steps), device=local, rng_mode=rng)
+    e = driver(_host_cfg(H, args.steps))
     e_seg, e_s, h2d, d2h = 0, 0.0, 0, 0
     for _ in range(args.steps):
         flush_l2(flush)
@@ -269,10 +302,11 @@ def run_ours(args):
         d2h += rec.d2h_bytes
     e.close()
     e_s = max_over_ranks(e_s, world)
-    e_val = sum_over_ranks(e_seg, world) / e_s
+    e_val = e_seg / e_s
 
     peak, peak_kind = measured_peak()
-    achieved = seg * BYTES_PER_SEGMENT / (tr_ms * 1e-3) / 1e9 if tr_ms > 0 else 0.0
+    # per GPU: this GPU's share of the segments over its transport-kernel time
+    achieved = (seg / world) * BYTES_PER_SEGMENT / (tr_ms * 1e-3) / 1e9 if tr_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -288,8 +322,10 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (the reference's isotropic unit point pulse; no dataset)",
             "config": {"workload": WORKLOAD, "histories_per_step": H,
-                       "time_steps": args.steps, "rng": args.rng,
-                       "parallelism": f"histories sharded x{world}" if world > 1 else "1 GPU",
+                       "histories_per_gpu": args.histories, "time_steps": args.steps,
+                       "rng": args.rng,
+                       "parallelism": (f"histories sharded x{world}, NCCL tally all-reduce + "
+                                       "census rebalance" if world > 1 else "1 GPU"),
                        "l2": "256 MiB flush between timed steps"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -301,6 +337,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "fom_sigma_l2_last": fom[-1] if fom else None,
         }
+        if exact:
+            line["exact_mode"] = exact
         clk_s = clk.summary()
         line["clocks"] = clk_s
         if not args.no_cpu_baseline:
@@ -327,10 +365,11 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rng", default="exact", choices=["exact", "philox"])
-    ap.add_argument("--histories", type=int, default=1_000_000)
+    ap.add_argument("--rng", default="philox", choices=["exact", "philox"])
+    ap.add_argument("--histories", type=int, default=1_000_000, help="histories per step per GPU")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-exact", action="store_true", help="skip the exact-mode side run")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

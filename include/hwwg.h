@@ -116,7 +116,32 @@ typedef struct {
   int32_t device;        /* CUDA ordinal */
   int32_t rng_mode;      /* HWWG_RNG_EXACT or HWWG_RNG_PHILOX */
   uint64_t bank_capacity;/* initial particle capacity of each device bank (grows) */
+  /* Multi-GPU driver (one process per GPU); world <= 1 means
+   * single GPU. nccl_id: the bytes of an ncclUniqueId made by rank 0 with
+   * hwwg_nccl_unique_id and broadcast by the caller (torch.distributed). */
+  int32_t rank;
+  int32_t world;
+  uint8_t nccl_id[128];
 } hwwg_options;
+
+/* ncclGetUniqueId for the multi-GPU driver (out: 128 bytes). */
+int hwwg_nccl_unique_id(uint8_t* out);
+
+/* Host-side sharding plan shared by every rank (pure functions):
+ * shard(rank) = [H*rank/world, H*(rank+1)/world). */
+void hwwg_shard_range(uint64_t H, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi);
+/* Global comb across ranks (popctrl.cpp:7-42 over the rank-ordered concatenated
+ * census): from every rank's census weight total, this rank's tooth range
+ * [k_lo, k_hi), the spacing, the offset (offset_frac * spacing) and the rank's
+ * origin on the cumulative-weight axis. */
+int hwwg_comb_plan(const double* rank_weights, int32_t world, int32_t rank, uint64_t target,
+                   double offset_frac, double* spacing, double* offset, double* rank_origin,
+                   uint64_t* k_lo, uint64_t* k_hi);
+/* Census rebalance after the comb: per peer, teeth to send (count, first
+ * tooth) and teeth to receive so each rank holds its next-step shard. */
+void hwwg_rebalance_plan(const uint64_t* k_lo_all, const uint64_t* k_hi_all, int32_t world,
+                         int32_t rank, uint64_t H, uint64_t* send, uint64_t* send_first,
+                         uint64_t* recv);
 
 const char* hwwg_last_error(void);
 const char* hwwg_version(void);

@@ -72,7 +72,8 @@ class StepOutcomeC(C.Structure):
 
 
 class Options(C.Structure):
-    _fields_ = [("device", C.c_int32), ("rng_mode", C.c_int32), ("bank_capacity", C.c_uint64)]
+    _fields_ = [("device", C.c_int32), ("rng_mode", C.c_int32), ("bank_capacity", C.c_uint64),
+                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
 
 
 class RunConfigC(C.Structure):
@@ -112,7 +113,8 @@ EXPORTS = (
     "hwwg_run_segment_parallel", "hwwg_driver_create", "hwwg_driver_destroy",
     "hwwg_driver_step", "hwwg_driver_arrays", "hwwg_driver_bank", "hwwg_load_config_file",
     "hwwg_default_config", "hwwg_validate_config", "hwwg_losm_assemble_solve",
-    "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log")
+    "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log",
+    "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan")
 
 _lib = None
 
@@ -155,6 +157,14 @@ def lib():
     L.hwwg_uniform_comb.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_void_p, dptr, dptr]
     L.hwwg_device_log.argtypes = [C.c_void_p, dptr, C.c_uint64, dptr]
+    L.hwwg_nccl_unique_id.argtypes = [C.c_void_p]
+    L.hwwg_shard_range.argtypes = [C.c_uint64, C.c_int32, C.c_int32, u64ptr, u64ptr]
+    L.hwwg_shard_range.restype = None
+    L.hwwg_comb_plan.argtypes = [dptr, C.c_int32, C.c_int32, C.c_uint64, C.c_double, dptr, dptr,
+                                 dptr, u64ptr, u64ptr]
+    L.hwwg_rebalance_plan.argtypes = [u64ptr, u64ptr, C.c_int32, C.c_int32, C.c_uint64, u64ptr,
+                                      u64ptr, u64ptr]
+    L.hwwg_rebalance_plan.restype = None
     _lib = L
     return L
 

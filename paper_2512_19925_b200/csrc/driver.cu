@@ -7,6 +7,7 @@
 // thresholds (driver.cpp:170-177) and reads the step record back once, at the
 // end of the step.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -23,10 +24,18 @@
 #include "driver_host.h"
 #include "engine.cuh"
 #include "low_order.cuh"
+#include "rng.cuh"
 #include "fast.cuh"
 #include "transport.cuh"
 
 using namespace hwwg;
+
+#define NCCL_CHECK(call)                                                                  \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      throw ::hwwg::ApiError(HWWG_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
 
 namespace {
 
@@ -113,6 +122,15 @@ struct hwwg_driver {
   DevBuf<unsigned long long> warp_cursor;  // per-warp census chunks
   int max_warps = 0;
 
+  // multi-GPU: histories sharded by rank, tallies all-reduced
+  // at every window-update barrier and at step end, census combed globally and
+  // rebalanced with grouped send/recv
+  int rank = 0, world = 1;
+  uint64_t shard_lo = 0;
+  ncclComm_t comm = nullptr;
+  DevBuf<double> nccl_buf;    // all-gathered census weights, snapshot slabs
+  FastBankBuf fteeth;         // teeth this rank produced, before the rebalance
+
   // low-order state
   DevBuf<double> lo_mem;
   DevBuf<int> lo_flags;
@@ -135,6 +153,7 @@ struct hwwg_driver {
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : seg_ev) cudaEventDestroy(e);
     if (host_bank) cudaFreeHost(host_bank);
+    if (comm) ncclCommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -209,12 +228,19 @@ void init_driver(hwwg_driver* d) {
   std::vector<hwwg_particle> src(c.histories_per_step);
   sample_pulse_source_host(c.seed, c.histories_per_step, c.x0,
                            c.strength * (double)c.histories_per_step, 0.0, src.data());
+  if (d->world > 1) {  // this rank's shard of the step-1 histories
+    uint64_t lo, hi;
+    hwwg_shard_range(c.histories_per_step, d->rank, d->world, &lo, &hi);
+    src = std::vector<hwwg_particle>(src.begin() + lo, src.begin() + hi);
+    d->shard_lo = lo;
+  }
   d->bank.reserve(std::max<uint64_t>(src.size(), 1));
   HWWG_CUDA(cudaMemcpyAsync(d->bank.p, src.data(), src.size() * sizeof(hwwg_particle),
                             cudaMemcpyHostToDevice, d->stream));
   d->bank_n = src.size();
   if (c.host_bank) {
-    d->host_bank_cap = std::max<uint64_t>(src.size(), 1);
+    // room for the cold-start census (x60+ of H) so no step re-pins host memory
+    d->host_bank_cap = std::max<uint64_t>(src.size(), 64 * d->target + 4096);
     HWWG_CUDA(cudaMallocHost(&d->host_bank, d->host_bank_cap * sizeof(hwwg_particle)));
     std::memcpy(d->host_bank, src.data(), src.size() * sizeof(hwwg_particle));
     d->host_bank_n = src.size();
@@ -223,9 +249,17 @@ void init_driver(hwwg_driver* d) {
   for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
   if (d->fast) {
     d->fbank.reserve(d->bank_n);
-    launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), 0, d->stream);
-    d->fcensus.reserve(64 * d->target + 4096);  // step 1 cold start splits x60+
-    d->census_hwm = 64 * d->target + 4096;
+    launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), d->shard_lo,
+                       d->stream);
+    const uint64_t local_target = d->target / (uint64_t)d->world + 1;
+    d->fcensus.reserve(64 * local_target + 4096);  // step 1 cold start splits x60+
+    d->census_hwm = 64 * local_target + 4096;
+    if (d->world > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, d->opt.nccl_id, sizeof(id));
+      NCCL_CHECK(ncclCommInitRank(&d->comm, d->world, id, d->rank));
+      d->nccl_buf.reserve(4 * (size_t)d->world + 16);
+    }
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
     const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
     d->max_warps = warps;
@@ -278,6 +312,81 @@ void print_timeline(hwwg_driver* d, int nseg, int step) {
   }
 }
 
+// Global comb + census rebalance over `world` ranks:
+// local weight scan -> all-gather of the rank totals -> the same host plan on
+// every rank (hwwg_comb_plan) -> this rank's teeth -> grouped NCCL send/recv so
+// rank r ends up holding next-step histories shard(r), in history order.
+void multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
+  const int W = d->world, R = d->rank;
+  const uint64_t n = d->bank_n;
+  d->comb_mem.reserve(4 + std::max<uint64_t>(n, 1));
+  const size_t tb = fast_comb_temp_bytes(std::max<uint64_t>(n, 1));
+  d->comb_temp.reserve(tb);
+  FastCombArgs a{};
+  a.bank = d->fbank.view();
+  a.n = n;
+  a.prefix = d->comb_mem.p + 4;
+  a.scalars = d->comb_mem.p;
+  a.temp = d->comb_temp.p;
+  a.temp_bytes = tb;
+  launch_fast_comb_local_scan(a, s);  // scalars[0] = this rank's census weight
+  d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)W + 16, (size_t)d->I + 8));
+  NCCL_CHECK(ncclAllGather(d->comb_mem.p, d->nccl_buf.p, 1, ncclDouble, d->comm, s));
+  std::vector<double> wr(W);
+  HWWG_CUDA(cudaMemcpyAsync(wr.data(), d->nccl_buf.p, W * 8, cudaMemcpyDeviceToHost, s));
+  HWWG_CUDA(cudaStreamSynchronize(s));
+  Xoshiro rng;  // the comb stream of the step (driver.cpp:119-121), same on every rank
+  rng.seed(d->cfg.seed, stream_id_host(step, 0, 3));
+  const double frac = rng.uniform();
+  std::vector<uint64_t> klo(W), khi(W);
+  double spacing = 0, offset = 0, origin = 0;
+  for (int q = 0; q < W; ++q) {
+    double sp, off, org;
+    if (hwwg_comb_plan(wr.data(), W, q, d->target, frac, &sp, &off, &org, &klo[q], &khi[q]) != 0)
+      throw ApiError(HWWG_EINVAL, last_error_slot());
+    if (q == R) {
+      spacing = sp;
+      offset = off;
+      origin = org;
+    }
+  }
+  const uint64_t nt = khi[R] - klo[R];
+  d->fteeth.reserve(nt);
+  if (nt) launch_fast_comb_teeth_range(a, spacing, offset, origin, klo[R], khi[R], d->fteeth.view(), s);
+  // rebalance: teeth of shard(q) go to rank q
+  std::vector<uint64_t> send(W), first(W), recv(W);
+  hwwg_rebalance_plan(klo.data(), khi.data(), W, R, d->target, send.data(), first.data(), recv.data());
+  uint64_t lo, hi;
+  hwwg_shard_range(d->target, R, W, &lo, &hi);
+  d->shard_lo = lo;
+  d->fsrc.reserve(std::max<uint64_t>(hi - lo, 1));
+  const FastBank src = d->fsrc.view(), th = d->fteeth.view();
+  NCCL_CHECK(ncclGroupStart());
+  for (int q = 0; q < W; ++q) {
+    if (send[q]) {
+      const uint64_t o = first[q] - klo[R];
+      if (q == R) {
+        const uint64_t dst = first[q] - lo;
+        HWWG_CUDA(cudaMemcpyAsync(src.xm + dst, th.xm + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
+        HWWG_CUDA(cudaMemcpyAsync(src.wt + dst, th.wt + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
+        HWWG_CUDA(cudaMemcpyAsync(src.meta + dst, th.meta + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
+      } else {
+        NCCL_CHECK(ncclSend(th.xm + o, 2 * send[q], ncclDouble, q, d->comm, s));
+        NCCL_CHECK(ncclSend(th.wt + o, 2 * send[q], ncclDouble, q, d->comm, s));
+        NCCL_CHECK(ncclSend(th.meta + o, 4 * send[q], ncclUint32, q, d->comm, s));
+      }
+    }
+    if (recv[q] && q != R) {
+      const uint64_t dst = std::max(klo[q], lo) - lo;
+      NCCL_CHECK(ncclRecv(src.xm + dst, 2 * recv[q], ncclDouble, q, d->comm, s));
+      NCCL_CHECK(ncclRecv(src.wt + dst, 2 * recv[q], ncclDouble, q, d->comm, s));
+      NCCL_CHECK(ncclRecv(src.meta + dst, 4 * recv[q], ncclUint32, q, d->comm, s));
+    }
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  d->launches += 3;
+}
+
 // One time step (driver.cpp:99-284).
 void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const hwwg_run_config& c = d->cfg;
@@ -310,7 +419,13 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const double bank_cap = c.comb_overflow_factor * (double)d->target;
   const bool do_comb = c.comb_overflow_factor <= 1.0 || (double)d->bank_n > bank_cap;
   uint64_t H;
-  if (d->fast) {
+  if (d->fast && d->world > 1) {
+    if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
+    multi_gpu_comb(d, step, s);
+    H = d->target;
+    rec->comb_in = d->bank_n;  // this rank's census slots
+    rec->comb_out = d->target;
+  } else if (d->fast) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     d->fsrc.reserve(d->target);
@@ -469,9 +584,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
       if (d->fast) {
         FastArgs fa{};
+        // this rank's part of the segment: global [h_done, h_stop) ∩ its shard
+        uint64_t g_lo = h_done, g_hi = h_stop;
+        if (d->world > 1) {
+          uint64_t s_lo, s_hi;
+          hwwg_shard_range(H, d->rank, d->world, &s_lo, &s_hi);
+          g_lo = std::min(std::max(h_done, s_lo), s_hi);
+          g_hi = std::min(std::max(h_stop, s_lo), s_hi);
+        }
+        const uint64_t l_lo = g_lo - d->shard_lo;
         const FastBank src = d->fsrc.view();
-        fa.src = FastBank{src.xm + h_done, src.wt + h_done, src.meta + h_done};
-        fa.n_src = ea.n;
+        fa.src = FastBank{src.xm + l_lo, src.wt + l_lo, src.meta + l_lo};
+        fa.n_src = g_hi - g_lo;
         fa.src_head = d->src_head.p;
         fa.census = d->fcensus.view();
         fa.census_count = d->counter.p;
@@ -495,8 +619,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.err = d->err.p;
         // block-private shared-memory tallies over this segment's batch range
         // when they fit (I <= ~1000 at 20 batches), else global REDs
-        const int b_lo = batch_of_host(h_done, H, B);
-        const int b_hi = batch_of_host(h_stop ? h_stop - 1 : 0, H, B);
+        const int b_lo = batch_of_host(g_lo, H, B);
+        const int b_hi = batch_of_host(g_hi > g_lo ? g_hi - 1 : g_lo, H, B);
         fa.b_lo = b_lo;
         fa.nb = b_hi - b_lo + 1;
         size_t smem = fast_smem_bytes(I, fa.nb);
@@ -519,15 +643,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           HWWG_CUDA(cudaMemsetAsync(fa.timeline, 0, per * 8, s));
           d->timeline_warps = fa.pool.warps;
         }
-        if (ea.n) {
+        if (fa.n_src) {
           launch_fast_segment(fa, blocks, smem, s);
-          d->launches += 1;  // + the segment kernel counted below
+          d->launches += 2;
         }
       } else {
         launch_exact_segment(ea, s);
+        if (ea.n) d->launches += 3;  // chunk init, chunk histories, ordered merge
       }
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg + 1], s));
-      if (ea.n) ++d->launches;
       h_done = h_stop;
       if (u == thr.size()) break;
       // partial_snapshot + implicit closure update (driver.cpp:206-217)
@@ -544,6 +668,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.fast_solve = d->fast ? 1 : 0;
       a.closure_tally = d->tal.p.census_closure;
       a.bclosure_tally = d->tal.p.boundary_closure;
+      if (d->world > 1) {  // the snapshot is of ALL ranks' histories so far
+        d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)d->world + 16, (size_t)I + 8));
+        NCCL_CHECK(ncclAllReduce(d->tal.p.census_closure, d->nccl_buf.p, I, ncclDouble, ncclSum,
+                                 d->comm, s));
+        NCCL_CHECK(ncclAllReduce(d->tal.p.boundary_closure, d->nccl_buf.p + I, 2, ncclDouble,
+                                 ncclSum, d->comm, s));
+        a.closure_tally = d->nccl_buf.p;
+        a.bclosure_tally = d->nccl_buf.p + I;
+      }
       const double effective = (double)c.histories_per_step * (double)h_done / (double)H;
       a.snapshot_inv_norm = 1.0 / effective;
       a.s = d->lo;
@@ -558,6 +691,20 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaMemcpyAsync(&derr, d->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaStreamSynchronize(s));
+    if (d->fast && d->world > 1) {  // replay decisions must be collective
+      unsigned long long flags[2] = {count > d->fcensus.cap() ? 1ULL : 0ULL,
+                                     derr.code ? 1ULL : 0ULL};
+      unsigned long long* dflag = reinterpret_cast<unsigned long long*>(d->nccl_buf.p);
+      HWWG_CUDA(cudaMemcpyAsync(dflag, flags, sizeof flags, cudaMemcpyHostToDevice, s));
+      NCCL_CHECK(ncclAllReduce(dflag, dflag, 2, ncclUint64, ncclMax, d->comm, s));
+      HWWG_CUDA(cudaMemcpyAsync(flags, dflag, sizeof flags, cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaStreamSynchronize(s));
+      if (flags[1] && !derr.code) derr.code = HWWG_EINVAL;  // a peer failed
+      if (derr.code || !flags[0]) break;
+      d->census_hwm = std::max<uint64_t>(d->census_hwm, count + count / 4 + 4096);
+      d->fcensus.reserve(d->census_hwm);  // every rank replays the step
+      continue;
+    }
     if (d->fast) {
       if (derr.code || count <= d->fcensus.cap()) break;
       d->census_hwm = count + count / 4 + 4096;
@@ -576,6 +723,13 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                                     " exceeded the daughter-stack run capacity");
 
   // ---- finalize (driver.cpp:221-222)
+  if (d->world > 1) {  // step-end reduction of the whole tally slab and counters
+    NCCL_CHECK(ncclAllReduce(d->tal.slab.p, d->tal.slab.p, d->tal.doubles, ncclDouble, ncclSum,
+                             d->comm, s));
+    unsigned long long* u64part = reinterpret_cast<unsigned long long*>(d->tal.slab.p + d->tal.doubles);
+    NCCL_CHECK(ncclAllReduce(u64part, u64part, (size_t)I + kNumUCounters, ncclUint64, ncclSum,
+                             d->comm, s));
+  }
   if (d->fast) {  // the fast kernels score the batch table only
     launch_track_from_batches(d->tal.p, I, B, s);
     ++d->launches;
@@ -742,6 +896,13 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   }
   d->fast = d->opt.rng_mode == HWWG_RNG_PHILOX;
   d->timeline_on = d->fast && std::getenv("HWWG_FAST_TIMELINE") != nullptr;
+  d->world = d->opt.world > 1 ? d->opt.world : 1;
+  d->rank = d->world > 1 ? d->opt.rank : 0;
+  if (d->world > 1 && (!d->fast || d->rank < 0 || d->rank >= d->world)) {
+    delete d;
+    return fail(HWWG_EINVAL, "multi-GPU runs need HWWG_RNG_PHILOX and 0 <= rank < world "
+                             "(exact mode replays one sequential comb)");
+  }
   if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
     delete d;
     return fail(HWWG_EINVAL, "philox mode: fission and > 65535 cells are not supported");
@@ -758,6 +919,17 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
 }
 
 void hwwg_driver_destroy(hwwg_driver* d) { delete d; }
+
+int hwwg_nccl_unique_id(uint8_t* out) {
+  HWWG_API_BEGIN
+  if (!out) return fail(HWWG_EINVAL, "NULL argument");
+  ncclUniqueId id;
+  NCCL_CHECK(ncclGetUniqueId(&id));
+  std::memset(out, 0, 128);
+  std::memcpy(out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  return HWWG_OK;
+  HWWG_API_END
+}
 
 int hwwg_driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   HWWG_API_BEGIN

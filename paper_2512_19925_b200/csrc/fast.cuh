@@ -91,6 +91,12 @@ struct FastCombArgs {
 };
 size_t fast_comb_temp_bytes(uint64_t n);
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s);
+// Multi-GPU comb pieces: local inclusive scan (scalars[0] = local total, 0 for
+// an empty bank), and teeth [k_lo, k_hi) placed against origin + local prefix.
+void launch_fast_comb_local_scan(const FastCombArgs& a, cudaStream_t s);
+void launch_fast_comb_teeth_range(const FastCombArgs& a, double spacing, double offset,
+                                  double origin, uint64_t k_lo, uint64_t k_hi, FastBank out,
+                                  cudaStream_t s);
 // track_flux[i] = sum_b track_flux_batch[b][i] (fast mode scores batches only)
 void launch_track_from_batches(TallyPtrs t, int I, int B, cudaStream_t s);
 void launch_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out, cudaStream_t s);

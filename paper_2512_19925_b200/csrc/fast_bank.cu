@@ -58,6 +58,30 @@ __global__ void k_comb_teeth(FastCombArgs a) {
   a.out.meta[k] = make_uint4(m.x & 0xffffu, (unsigned)k, 0u, 0u);
 }
 
+__global__ void k_local_total(const double* prefix, uint64_t n, double* sc) {
+  sc[0] = n ? prefix[n - 1] : 0.0;
+}
+
+__global__ void k_comb_teeth_range(FastCombArgs a, double spacing, double offset, double origin,
+                                   uint64_t k_lo, uint64_t k_hi, FastBank out) {
+  const uint64_t k = k_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k_hi) return;
+  const double T = offset + (double)k * spacing;
+  uint64_t lo = 0, hi = a.n;  // first local particle with T < origin + prefix
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (T < origin + a.prefix[mid]) hi = mid;
+    else lo = mid + 1;
+  }
+  uint64_t s = lo < a.n ? lo : a.n - 1;
+  if (lo >= a.n)
+    while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
+  const uint64_t o = k - k_lo;
+  out.xm[o] = a.bank.xm[s];
+  out.wt[o] = make_double2(spacing, a.bank.wt[s].y);
+  out.meta[o] = make_uint4(a.bank.meta[s].x & 0xffffu, (unsigned)k, 0u, 0u);
+}
+
 __global__ void k_fill_holes(FastBank c, uint64_t cap, const unsigned long long* cur, int warps,
                              double x_fill, double t_fill) {
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
@@ -119,6 +143,26 @@ void launch_fast_comb(const FastCombArgs& a, cudaStream_t s) {
   HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, a.prefix, a.prefix, (int)a.n, s));
   k_comb_scalars<<<1, 1, 0, s>>>(a.prefix, a.n, a.target, a.seed, a.stream, a.scalars);
   k_comb_teeth<<<(unsigned)((a.target + 255) / 256), 256, 0, s>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fast_comb_local_scan(const FastCombArgs& a, cudaStream_t s) {
+  if (a.n) {
+    k_extract_w<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a.bank, a.n, a.prefix);
+    size_t bytes = a.temp_bytes;
+    HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, a.prefix, a.prefix, (int)a.n, s));
+  }
+  k_local_total<<<1, 1, 0, s>>>(a.prefix, a.n, a.scalars);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fast_comb_teeth_range(const FastCombArgs& a, double spacing, double offset,
+                                  double origin, uint64_t k_lo, uint64_t k_hi, FastBank out,
+                                  cudaStream_t s) {
+  const uint64_t n = k_hi - k_lo;
+  if (!n || !a.n) return;
+  k_comb_teeth_range<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, spacing, offset, origin,
+                                                                 k_lo, k_hi, out);
   HWWG_CUDA(cudaGetLastError());
 }
 

@@ -1,6 +1,7 @@
 // Host pieces of the engine: RunConfig defaults/validation/key=value loader
 // (proj/include/hww/config.hpp:33-93, proj/src/config.cpp:27-69,
 // proj/tools/hww_main.cpp:20-92) and the driver's sequential helpers.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -220,6 +221,79 @@ int hwwg_load_config_file(const char* path, hwwg_run_config* c) {
   }
   return HWWG_OK;
   HWWG_API_END
+}
+
+// ---------------------------------------------------------------- sharding
+// Multi-GPU plan: every rank computes the same plan from the
+// same all-gathered numbers, so no rank ever disagrees about who owns what.
+
+void hwwg_shard_range(uint64_t H, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi) {
+  // contiguous, near-equal slices; batch ids stay global (batch_of(h, H, B))
+  *lo = H * (uint64_t)rank / (uint64_t)world;
+  *hi = H * (uint64_t)(rank + 1) / (uint64_t)world;
+}
+
+// Global comb over per-rank census banks: rank r's particles occupy
+// [O_r, O_r + W_r) of the global cumulative-weight axis, O_r the exclusive
+// prefix of rank_weights in rank order (popctrl.cpp:15-30 semantics with the
+// bank concatenated in rank order). Tooth k (T_k = offset + k*spacing) belongs
+// to the first rank with T_k < O_{r+1}; stranded teeth go to the last rank
+// (popctrl.cpp:31-37). Outputs this rank's tooth range and O_r.
+int hwwg_comb_plan(const double* rank_weights, int32_t world, int32_t rank, uint64_t target,
+                   double offset_frac, double* spacing_out, double* offset_out,
+                   double* rank_origin, uint64_t* k_lo, uint64_t* k_hi) {
+  if (world < 1 || rank < 0 || rank >= world || target < 1)
+    return fail(HWWG_EINVAL, "bad comb plan arguments");
+  double W = 0.0;
+  for (int q = 0; q < world; ++q) W += rank_weights[q];
+  if (!(W > 0.0)) return fail(HWWG_EINVAL, "cannot comb an empty bank");
+  const double spacing = W / (double)target;
+  const double offset = offset_frac * spacing;
+  auto first_tooth_at_or_above = [&](double edge) -> uint64_t {
+    // smallest k with offset + k*spacing >= edge (clamped to [0, target])
+    double g = std::ceil((edge - offset) / spacing);
+    uint64_t k = g <= 0.0 ? 0 : (g >= (double)target ? target : (uint64_t)g);
+    while (k > 0 && offset + (double)(k - 1) * spacing >= edge) --k;
+    while (k < target && offset + (double)k * spacing < edge) ++k;
+    return k;
+  };
+  int last = world - 1;  // stranded teeth go to the last rank that holds weight
+  while (last > 0 && !(rank_weights[last] > 0.0)) --last;
+  double O = 0.0;
+  uint64_t lo = 0;
+  for (int q = 0; q <= rank; ++q) {
+    const double O_next = O + rank_weights[q];
+    const uint64_t hi_q = q >= last ? target : first_tooth_at_or_above(O_next);
+    if (q == rank) {
+      *rank_origin = O;
+      *k_lo = lo;
+      *k_hi = hi_q < lo ? lo : hi_q;
+    }
+    lo = hi_q < lo ? lo : hi_q;
+    O = O_next;
+  }
+  *spacing_out = spacing;
+  *offset_out = offset;
+  return HWWG_OK;
+}
+
+// Rebalance after the comb: this rank produced teeth [k_lo, k_hi); rank q
+// owns next-step histories shard(q). send[q] = |[k_lo,k_hi) ∩ shard(q)|,
+// send_first[q] = first tooth sent to q; recv[q] = |[k_lo_q, k_hi_q) ∩ shard(rank)|.
+void hwwg_rebalance_plan(const uint64_t* k_lo_all, const uint64_t* k_hi_all, int32_t world,
+                         int32_t rank, uint64_t H, uint64_t* send, uint64_t* send_first,
+                         uint64_t* recv) {
+  uint64_t my_lo, my_hi;
+  hwwg_shard_range(H, rank, world, &my_lo, &my_hi);
+  for (int q = 0; q < world; ++q) {
+    uint64_t s_lo, s_hi;
+    hwwg_shard_range(H, q, world, &s_lo, &s_hi);
+    const uint64_t a = std::max(k_lo_all[rank], s_lo), b = std::min(k_hi_all[rank], s_hi);
+    send[q] = b > a ? b - a : 0;
+    send_first[q] = b > a ? a : 0;
+    const uint64_t c = std::max(k_lo_all[q], my_lo), e = std::min(k_hi_all[q], my_hi);
+    recv[q] = e > c ? e - c : 0;
+  }
 }
 
 }  // extern "C"

@@ -395,13 +395,21 @@ class RunConfig:
 
 
 class Driver:
-    """Stepwise hww::run (driver.cpp:286-342): device-resident time steps."""
+    """Stepwise hww::run (driver.cpp:286-342): device-resident time steps.
 
-    def __init__(self, config: RunConfig, device=0, rng_mode=RNG_EXACT):
+    Multi-GPU (one process per GPU): pass rank, world and the 128-byte NCCL id
+    that rank 0 made with nccl_unique_id(); every rank then runs its shard of
+    each step's histories and the driver all-reduces tallies / rebalances the
+    census itself (Philox mode)."""
+
+    def __init__(self, config: RunConfig, device=0, rng_mode=RNG_EXACT, rank=0, world=1,
+                 nccl_id: bytes = b""):
         self.config = config
         self._cfg = config.to_c()
         self._h = C.c_void_p()
-        opts = A.Options(device, rng_mode, 0)
+        opts = A.Options(device, rng_mode, 0, rank, world)
+        for i, b in enumerate(bytes(nccl_id)[:128]):
+            opts.nccl_id[i] = b
         _raise(A.lib().hwwg_driver_create(C.byref(self._cfg), C.byref(opts), C.byref(self._h)))
         self.I = config.cells
 
@@ -443,6 +451,42 @@ class Driver:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 makes it; broadcast it with torch.distributed)."""
+    buf = (C.c_uint8 * 128)()
+    _raise(A.lib().hwwg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+# -------------------------------------------------------- sharding plan (host)
+def shard_range(H, rank, world):
+    lo, hi = C.c_uint64(), C.c_uint64()
+    A.lib().hwwg_shard_range(H, rank, world, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+def comb_plan(rank_weights, rank, target, offset_frac):
+    """hwwg_comb_plan: (spacing, offset, rank_origin, k_lo, k_hi) for `rank`."""
+    w = np.ascontiguousarray(rank_weights, np.float64)
+    sp, off, org = C.c_double(), C.c_double(), C.c_double()
+    lo, hi = C.c_uint64(), C.c_uint64()
+    _raise(A.lib().hwwg_comb_plan(A.as_dptr(w), w.size, rank, target, offset_frac,
+                                  C.byref(sp), C.byref(off), C.byref(org), C.byref(lo),
+                                  C.byref(hi)))
+    return sp.value, off.value, org.value, lo.value, hi.value
+
+
+def rebalance_plan(k_lo_all, k_hi_all, rank, H):
+    """hwwg_rebalance_plan: (send counts, first tooth sent, recv counts) per peer."""
+    lo = np.ascontiguousarray(k_lo_all, np.uint64)
+    hi = np.ascontiguousarray(k_hi_all, np.uint64)
+    W = lo.size
+    send, first, recv = (np.zeros(W, np.uint64) for _ in range(3))
+    A.lib().hwwg_rebalance_plan(A.as_u64ptr(lo), A.as_u64ptr(hi), W, rank, H,
+                                A.as_u64ptr(send), A.as_u64ptr(first), A.as_u64ptr(recv))
+    return send, first, recv
 
 
 def run(config: RunConfig, device=0, rng_mode=RNG_EXACT):
