@@ -76,6 +76,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("HWWG_NO_CLOCKS"):
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -101,13 +103,14 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        if not self.rows:
+    def summary(self, first=0, last=None):
+        rows = self.rows[first:last] or self.rows[-3:]  # the timed window (>= 1 sample)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        reasons = sorted({names[i] for r in rows for i in range(4)
                           if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
@@ -236,6 +239,9 @@ def run_ours(args):
         return hw.Driver(cfg, device=local, rng_mode=rng, rank=rank, world=world,
                          nccl_id=nccl_id)
 
+    # the clock sampler starts before the warm-up: nvidia-smi's first NVML
+    # initialisation on a fresh box must not land inside the timed steps
+    clk = ClockSampler(local).__enter__()
     # warm-up: a separate instance, steps 1..W
     if args.warmup:
         wd = driver(config2(H, max(args.warmup, 1)))
@@ -253,18 +259,19 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush_l2(flush)
-            torch.cuda.synchronize()
-            rec = d.step()
-            seg += rec.segments
-            dev_ms += rec.device_ms
-            tr_ms += rec.transport_ms
-            tr_launch += rec.transport_launches
-            launches += rec.kernel_launches
-            fom.append(rec.fom_sigma_l2)
+    clk_first = len(clk.rows)
+    for _ in range(args.steps):
+        flush_l2(flush)
         torch.cuda.synchronize()
+        rec = d.step()
+        seg += rec.segments
+        dev_ms += rec.device_ms
+        tr_ms += rec.transport_ms
+        tr_launch += rec.transport_launches
+        launches += rec.kernel_launches
+        fom.append(rec.fom_sigma_l2)
+    torch.cuda.synchronize()
+    clk_last = len(clk.rows)
     if world > 1:
         torch.distributed.barrier()
     d.close()
@@ -339,8 +346,7 @@ def run_ours(args):
         }
         if exact:
             line["exact_mode"] = exact
-        clk_s = clk.summary()
-        line["clocks"] = clk_s
+        line["clocks"] = clk.summary(clk_first, clk_last)
         if not args.no_cpu_baseline:
             try:
                 v, cores, sample = cpu_baseline(H, args.cpu_steps)
@@ -350,6 +356,7 @@ def run_ours(args):
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0,
                                         "kind": "reference", "sample": f"unavailable: {ex}"}
         print(json.dumps(line))
+    clk.__exit__(None, None, None)
     return 0
 
 
