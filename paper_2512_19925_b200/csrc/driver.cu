@@ -116,6 +116,10 @@ struct hwwg_driver {
   DevBuf<char> comb_temp;
   DevBuf<FastStackRec> pool_recs;
   DevBuf<unsigned long long> pool_ctl;
+  int smem_mode = 1;  // fast tallies (FastArgs::smem_tallies) outside the cold start
+  int scramble = 1;   // FastArgs::scramble outside the cold start
+  int flush_replicas = 0;  // FastArgs::flush_replicas (HWWG_FAST_FLUSH_R; 0 = direct REDs, measured best)
+  DevBuf<double> flush_scratch;
   bool timeline_on = false;
   DevBuf<unsigned long long> timeline;
   unsigned timeline_warps = 0;
@@ -248,12 +252,20 @@ void init_driver(hwwg_driver* d) {
   d->seg_ev.resize(32);
   for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
   if (d->fast) {
-    d->fbank.reserve(d->bank_n);
+    const uint64_t local_target = d->target / (uint64_t)d->world + 1;
+    d->fbank.reserve(std::max<uint64_t>(d->bank_n, 64 * local_target + 4096));
     launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), d->shard_lo,
                        d->stream);
-    const uint64_t local_target = d->target / (uint64_t)d->world + 1;
-    d->fcensus.reserve(64 * local_target + 4096);  // step 1 cold start splits x60+
+    // Everything a step can grow into is allocated here, up front: a cudaMalloc
+    // inside a step synchronises the device (the step-1 census is x60+ of H,
+    // and it becomes step 2's comb input in the other bank of the swap pair).
     d->census_hwm = 64 * local_target + 4096;
+    d->fcensus.reserve(d->census_hwm);
+    d->fbank.reserve(d->census_hwm);
+    d->fsrc.reserve(std::max<uint64_t>(d->target, 1));
+    d->comb_mem.reserve(4 + d->census_hwm);
+    d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
+    if (c.host_bank) d->bank.reserve(d->census_hwm);
     if (d->world > 1) {
       ncclUniqueId id;
       std::memcpy(&id, d->opt.nccl_id, sizeof(id));
@@ -269,6 +281,11 @@ void init_driver(hwwg_driver* d) {
     d->pool_recs.reserve(1u << 20);  // 64 MB of donated split records per segment
     HWWG_CUDA(cudaMemsetAsync(d->pool_recs.p, 0, d->pool_recs.n * sizeof(FastStackRec), d->stream));
     d->pool_ctl.reserve(4);
+    if (d->flush_replicas) {
+      const size_t words = (size_t)d->flush_replicas * fast_flush_stride(I, d->B);
+      d->flush_scratch.reserve(words);
+      HWWG_CUDA(cudaMemsetAsync(d->flush_scratch.p, 0, words * 8, d->stream));
+    }
   } else {
     d->stage.ensure(64 * d->target + 4096);
   }
@@ -577,9 +594,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       ea.src = d->source.p + h_done;
       ea.n = h_stop - h_done;
       ea.h_begin = h_done;
-      ea.chunks = chunk_layout(ea.n, h_done, H, I, B);
-      d->chunk_mem.reserve(std::max<size_t>((size_t)ea.chunks.count * ea.chunks.stride, 1));
-      ea.chunks.base = d->chunk_mem.p;
+      if (!d->fast) {  // chunk-private TallySets of the exact path
+        ea.chunks = chunk_layout(ea.n, h_done, H, I, B);
+        d->chunk_mem.reserve(std::max<size_t>((size_t)ea.chunks.count * ea.chunks.stride, 1));
+        ea.chunks.base = d->chunk_mem.p;
+      }
       const int nseg = (int)u;
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
       if (d->fast) {
@@ -623,14 +642,22 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         const int b_hi = batch_of_host(g_hi > g_lo ? g_hi - 1 : g_lo, H, B);
         fa.b_lo = b_lo;
         fa.nb = b_hi - b_lo + 1;
+        // the first step starts from a point pulse: most lanes share a few cells
+        fa.aggregate = step == 1 ? 1 : 0;
         size_t smem = fast_smem_bytes(I, fa.nb);
         fa.smem_tallies = smem <= 96 * 1024 ? 1 : 0;
+        if (!fa.aggregate && d->smem_mode != 1) {
+          fa.smem_tallies = d->smem_mode;
+          smem = d->smem_mode == 2 ? fast_smem_count_bytes(I) : 0;
+        }
         if (!fa.smem_tallies) smem = 0;
+        fa.scramble = fa.aggregate ? 0 : d->scramble;
         const int blocks = d->sms * fast_blocks_per_sm(smem);
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
         fa.warp_cursor = d->warp_cursor.p;
-        // the first step starts from a point pulse: most lanes share a few cells
-        fa.aggregate = step == 1 ? 1 : 0;
+        fa.flush_scratch = d->flush_scratch.p;
+        fa.flush_stride = fast_flush_stride(I, B);
+        fa.flush_replicas = d->flush_replicas;
         fa.uniform = d->prob.gen_uniform_homog ? 1 : 0;
         fa.x_min = d->prob.edges.front();
         fa.x_max = d->prob.edges.back();
@@ -896,6 +923,9 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   }
   d->fast = d->opt.rng_mode == HWWG_RNG_PHILOX;
   d->timeline_on = d->fast && std::getenv("HWWG_FAST_TIMELINE") != nullptr;
+  if (const char* m = std::getenv("HWWG_FAST_SMEM")) d->smem_mode = std::atoi(m) % 3;
+  if (const char* m = std::getenv("HWWG_FAST_SCRAMBLE")) d->scramble = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
   d->world = d->opt.world > 1 ? d->opt.world : 1;
   d->rank = d->world > 1 ? d->opt.rank : 0;
   if (d->world > 1 && (!d->fast || d->rank < 0 || d->rank >= d->world)) {

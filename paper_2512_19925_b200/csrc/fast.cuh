@@ -17,8 +17,8 @@ struct FastStackRec {
   double x, mu, w, t;
   unsigned cell, hist;
   unsigned long long key;
-  unsigned ctr, count;
-  unsigned ready, pad;  // ready: set last when the record sits in the global pool
+  unsigned ctr, count;  // daughters base+1 .. base+count remain
+  unsigned ready, base;  // ready: set last when the record sits in the global pool
 };
 
 // Global pool of split records shared by all warps of a segment kernel (load
@@ -43,8 +43,9 @@ struct FastArgs {
   uint64_t H;
   int B;
   int b_lo, nb;  // batches touched by this segment: [b_lo, b_lo + nb)
-  int smem_tallies;  // 1: block-private shared-memory tallies
+  int smem_tallies;  // 0 global REDs, 1 shared-memory tallies, 2 fp64 global + counts shared
   int aggregate;     // 1: warp-aggregate tally atomics (cold start: lanes share cells)
+  int scramble;      // 1: claim source particles in bit-reversed order within 1024-blocks
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,
   // no per-event table loads.
@@ -61,7 +62,13 @@ struct FastArgs {
   DevError* err;
   unsigned long long* timeline;  // optional per-warp {t0, loop trips, t_exit, events}
   unsigned long long* warp_cursor;  // per warp {next, end} of its census chunk (zeroed per step)
+  // shared-memory tallies flush into flush_replicas zeroed global replicas
+  // (fast_flush_stride words each), folded in by a reduce kernel; 0: direct
+  double* flush_scratch;
+  size_t flush_stride;
+  int flush_replicas;
 };
+size_t fast_flush_stride(int I, int B);  // words per flush replica (nb <= B)
 
 // Zero-weight records in the unused tails of the warps' census chunks, and the
 // count of slots the census bank spans.
@@ -74,6 +81,7 @@ void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
 int fast_blocks_per_sm(size_t smem);
 int fast_threads_per_block();
 size_t fast_smem_bytes(int I, int nb);
+size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);
 void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
                         uint64_t hist0, cudaStream_t s);

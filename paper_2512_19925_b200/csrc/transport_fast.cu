@@ -33,10 +33,18 @@ namespace hwwg {
 
 namespace {
 
-constexpr int kWarpsPerBlock = 8;
+#ifndef HWWG_FAST_WARPS
+#define HWWG_FAST_WARPS 8  // warps per block (one shared-memory tally set each)
+#endif
+#ifndef HWWG_FAST_MINB
+#define HWWG_FAST_MINB (24 / HWWG_FAST_WARPS)  // resident blocks per SM (register budget)
+#endif
+constexpr int kWarpsPerBlock = HWWG_FAST_WARPS;
 constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kDonate = 256;  // pending local daughters above which splits go global
 constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
+constexpr unsigned kClaim = 32;  // source particles a warp reserves per claim
+constexpr unsigned kShare = 64;  // pending daughters above which a warp shares runs with idle warps
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -47,6 +55,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 struct Lane {
   double x, mu, w, t, inv_mu;
   int cell;
+  int bslot;  // tally batch slot (batch, or batch - b_lo for shared-memory tallies)
   unsigned hist, ctr;
   unsigned long long key;
   bool alive;
@@ -176,19 +185,22 @@ struct SmemTally {
 
 __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb) {
   SmemTally s;
-  s.trk = base;
+  s.trc = reinterpret_cast<unsigned*>(base);  // first: mode 2 keeps only the counts
+  s.trk = base + (I + 1) / 2;
   s.cphi = s.trk + (size_t)nb * I;
   s.cJ = s.cphi + I;
   s.cF = s.cJ + I;
   s.edge = s.cF + I;
   s.cwb = s.edge + I + 1;
   s.bclo = s.cwb + nb;
-  s.trc = reinterpret_cast<unsigned*>(s.bclo + 2);
   return s;
 }
 
-template <bool kUniform>
-__global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
+// kShf: the fp64 tallies live in block-private shared memory (smem_tallies ==
+// 1), statically, so the atomics compile to shared-memory CAS loops with no
+// generic-address dispatch.
+template <bool kUniform, bool kShf>
+__global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastArgs a) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -201,29 +213,111 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
   const double* __restrict__ edges = a.mesh.edges;
   const CellInfo* __restrict__ cells = a.mesh.cells;
   const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
-  const bool sh = a.smem_tallies != 0;
+  // smem_tallies: 0 all global REDs; 1 all block-private shared memory; 2 fp64
+  // tallies as global REDs (native, fire-and-forget) and the integer track
+  // counts in shared memory (shared fp64 adds are CAS loops on sm_100)
+  const bool sh = a.smem_tallies != 0;       // shared memory in use (zero + flush)
+  constexpr bool shf = kShf;                 // fp64 tallies in shared memory
   SmemTally S = smem_view(smem, I, a.nb);
   if (sh) {
-    const size_t words = (size_t)(a.nb + 4) * I + 1 + a.nb + 2 + (I + 1) / 2;
+    const size_t words = shf ? (size_t)(a.nb + 4) * I + 1 + a.nb + 2 + (I + 1) / 2
+                             : (size_t)(I + 1) / 2;
     for (size_t i = threadIdx.x; i < words; i += blockDim.x) smem[i] = 0.0;
     __syncthreads();
   }
-  unsigned long long n_coll = 0, n_split = 0, n_dau = 0, n_rk = 0, n_rs = 0, n_cen = 0,
-                     n_graze = 0, n_capped = 0;
-  double leak = 0.0;
+  // per-lane event counters: 32 bits is plenty within one launch (registers
+  // are what bounds occupancy here)
+  unsigned n_coll = 0, n_cen = 0;
+  // window-game, grazing and leakage events are rare: block counters in shared
+  // memory (native 32-bit ATOMS.ADD) and a global RED for the leaked weight
+  __shared__ unsigned s_rare[6];  // splits, daughters, capped, r.kills, r.survivals, grazing
+  if (threadIdx.x < 6) s_rare[threadIdx.x] = 0u;
+  __syncthreads();
   volatile unsigned long long* ctl = a.pool.ctl;
 
-  unsigned long long n_ev = 0, n_iter = 0;
+  unsigned n_ev = 0, n_iter = 0;
   // this warp's census chunk [wcur, wend), carried across the step's segments
-  unsigned long long wcur = a.warp_cursor[2 * gwarp], wend = a.warp_cursor[2 * gwarp + 1];
+  unsigned long long wcur = a.warp_cursor[2 * gwarp];
+  unsigned wleft = (unsigned)(a.warp_cursor[2 * gwarp + 1] - wcur);  // <= kCensusChunk
   const unsigned long long t_start = a.timeline ? globaltimer() : 0ULL;
   Lane p;
   p.alive = false;
   bool holding = true;  // this warp counts in pool.ctl[2] (active warps)
+  // source reservation (warp-uniform) and the claim in flight (lane 0)
+  // (32-bit: the driver keeps a segment's source below 2^32 - 2^26 particles)
+  const unsigned n_src = (unsigned)a.n_src;
+  unsigned r_lo = (unsigned)gwarp * kClaim, r_hi = r_lo + kClaim;
+  if (r_lo >= n_src) r_lo = r_hi = 0, src_done = true;
+  else if (r_hi > n_src) r_hi = n_src;
+  unsigned r_next = 0;
+  bool r_pend = false;
   unsigned long long ticket = ~0ULL;  // lane 0: pool slot this warp waits on
 
   while (true) {
     // ---- refill idle lanes: local split stack, then source bank, then pool
+    // Work sharing. A backlog on this warp's stack while other warps sit idle
+    // is the tail of a heavy split tree: one split of thousands of daughters,
+    // or a deep tree of small ones, would otherwise drain 32 lanes at a time on
+    // one warp while the grid waits. Hand the idle warps up to one piece each
+    // in a single trip: split the top run into pieces (daughter index ranges
+    // stay disjoint through the base offset) or give away whole records from
+    // the top of the stack, keeping at least one trip of work here.
+    if (pend > kShare && sp > 0) {
+      unsigned open = 0;
+      if (lane == 0) {
+        if (ctl[3] == 0) ctl[3] = 1;  // declare a backlog: idle warps wait for work
+        const unsigned long long t1 = ctl[1], t0 = ctl[0];
+        open = t1 > t0 ? (unsigned)min(t1 - t0, 32ULL) : 0u;
+      }
+      open = __shfl_sync(0xffffffffu, open, 0);
+      if (open) {
+        FastStackRec& top = stk[sp - 1];
+        const unsigned cnt = top.count;
+        const bool split_top = cnt >= 64;
+        unsigned m = split_top ? min(open, cnt / 32 - 1) : min(open, (unsigned)(sp - 1));
+        const unsigned piece = split_top ? cnt / (m + 1) : 0u;
+        unsigned long long s0 = 0;
+        if (m && lane == 0) {
+          atomicAdd(const_cast<unsigned long long*>(&ctl[2]), (unsigned long long)m);
+          s0 = atomicAdd(const_cast<unsigned long long*>(&ctl[0]), (unsigned long long)m);
+          if (s0 + m > a.pool.cap) {  // pool full: donate what fits, return the rest
+            const unsigned fit = s0 < a.pool.cap ? (unsigned)(a.pool.cap - s0) : 0u;
+            atomicAdd(const_cast<unsigned long long*>(&ctl[2]), (unsigned long long)(fit - m));
+          }
+        }
+        s0 = __shfl_sync(0xffffffffu, s0, 0);
+        if (m) {
+          if (s0 + m > a.pool.cap) m = s0 < a.pool.cap ? (unsigned)(a.pool.cap - s0) : 0u;
+          unsigned given = 0;
+          if (lane < (int)m) {
+            FastStackRec g = split_top ? top : stk[sp - 1 - lane];
+            if (split_top) {
+              g.base = top.base + lane * piece;
+              g.count = piece;
+            }
+            given = g.count;
+            g.ready = 0u;
+            FastStackRec* pr = a.pool.recs + s0 + lane;
+            *pr = g;
+            __threadfence();
+            *(volatile unsigned*)&pr->ready = 1u;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) given += __shfl_xor_sync(0xffffffffu, given, o);
+          __syncwarp();
+          if (split_top) {
+            if (lane == 0) {
+              top.count = cnt - m * piece;
+              top.base += m * piece;
+            }
+          } else {
+            sp -= (int)m;
+          }
+          pend -= given;
+          __syncwarp();
+        }
+      }
+    }
     unsigned need = __ballot_sync(0xffffffffu, !p.alive);
     while (need && sp > 0) {
       FastStackRec& r = stk[sp - 1];
@@ -231,7 +325,10 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       const unsigned cnt = r.count;
       const unsigned take = k < cnt ? k : cnt;
       const unsigned rank = __popc(need & lt);
-      if (!p.alive && rank < take) load_rec(p, r, cnt - rank);
+      if (!p.alive && rank < take) {
+        load_rec(p, r, r.base + cnt - rank);
+        p.bslot = batch_of(p.hist, a.H, a.B) - (shf ? a.b_lo : 0);
+      }
       __syncwarp();
       if (lane == 0) r.count = cnt - take;
       __syncwarp();
@@ -239,18 +336,39 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       if (cnt == take) --sp;
       need = __ballot_sync(0xffffffffu, !p.alive);
     }
-    if (need && !src_done) {
-      const unsigned k = __popc(need);
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(a.src_head, (unsigned long long)k);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base + k >= a.n_src) {
-        src_done = true;
+    // Source claims: a warp holds a reservation [r_lo, r_hi) of up to kClaim
+    // particles. Its first reservation is static (no atomic: every warp would
+    // otherwise hit the one counter at launch); later ones are claimed one
+    // trip AHEAD (after the event, see below), so the round trip of the
+    // global atomic overlaps a whole event instead of stalling the refill.
+    for (int pass = 0; pass < 2 && need && !src_done; ++pass) {
+      if (r_lo == r_hi) {
+        unsigned nb = 0;
+        if (lane == 0)
+          nb = r_pend ? r_next : (unsigned)atomicAdd(a.src_head, (unsigned long long)kClaim);
+        nb = __shfl_sync(0xffffffffu, nb, 0);
+        r_pend = false;
+        if (nb >= n_src) {
+          src_done = true;
+          break;
+        }
+        r_lo = nb;
+        r_hi = nb + kClaim < n_src ? nb + kClaim : n_src;
       }
+      const unsigned k = __popc(need);
+      const unsigned avail = r_hi - r_lo;
+      const unsigned take = k < avail ? k : avail;
+      const unsigned base = r_lo;
+      r_lo += take;
       const unsigned rank = __popc(need & lt);
-      if (!p.alive) {
-        const unsigned long long idx = base + rank;
-        if (idx < a.n_src) {
+      if (!p.alive && rank < take) {
+        // Claims walk the source in bit-reversed order inside 1024-particle
+        // blocks: the bank is in census order, i.e. runs of daughters of one
+        // split, and consecutive particles in one warp would collide on the
+        // same tally cells (shared-memory CAS retries).
+        const unsigned k = base + rank;
+        const unsigned idx = a.scramble && (k | 1023u) < n_src ? (k & ~1023u) | (__brev(k) >> 22) : k;
+        {
           const double2 xm = a.src.xm[idx];
           const double2 wt = a.src.wt[idx];
           const uint4 m = a.src.meta[idx];
@@ -263,6 +381,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
           p.hist = m.y;
           p.key = ((unsigned long long)m.w << 32) | m.z;
           p.inv_mu = 1.0 / p.mu;
+          p.bslot = batch_of(p.hist, a.H, a.B) - (shf ? a.b_lo : 0);
           p.alive = p.w > 0.0;
         }
       }
@@ -310,7 +429,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
               break;
             }
             __nanosleep(backoff);
-            backoff = backoff < 8192 ? backoff * 2 : 8192;  // idle polling costs issue slots
+            backoff = backoff < 2048 ? backoff * 2 : 2048;  // idle polling costs issue slots
           }
         }
       }
@@ -365,10 +484,9 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       if (d_coll < d) d = d_coll;
       if (d_b < d) d = d_b;
       if (d < 0.0) d = 0.0;  // rounding at an edge: zero-length step
-      const int batch = batch_of(p.hist, a.H, a.B);
       if (d > 0.0) {
         trk_v = p.w * d * ci.inv_dx * a.inv_dt;
-        trk_key = (sh ? batch - a.b_lo : batch) * I + p.cell;
+        trk_key = p.bslot * I + p.cell;
         trk_cell = p.cell;
       }
       bool window_site = false;
@@ -380,7 +498,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
         cen_F = cen_phi * (1.0 / 3.0 - p.mu * p.mu);
         cen_cell = p.cell;
         cen_w = p.w;
-        cen_b = sh ? batch - a.b_lo : batch;
+        cen_b = p.bslot;
         ++n_cen;
         p.alive = false;  // banked below, after the warp reconverges
       } else if (d == d_b) {
@@ -392,13 +510,13 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
         if (domain) {
           const double amu = fabs(p.mu);
           if (amu < 1e-10) {
-            ++n_graze;
+            atomicAdd(&s_rare[5], 1u);
           } else {
             const double bc = p.w * (0.5 - amu) / amu * a.inv_dt;
-            if (sh) atomicAdd(&S.bclo[edge == 0 ? 0 : 1], bc);
+            if (shf) atomicAdd(&S.bclo[edge == 0 ? 0 : 1], bc);
             else atomicAdd(&a.t.boundary_closure[edge == 0 ? 0 : 1], bc);
           }
-          leak += p.w;
+          atomicAdd(&a.t.dcount[0], p.w);
           p.alive = false;
         } else {
           p.cell += p.mu > 0.0 ? 1 : -1;
@@ -428,22 +546,28 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
           double n = ceil(p.w / c);
           if (n > 1e6) {
             n = 1e6;
-            ++n_capped;
+            atomicAdd(&s_rare[2], 1u);
           }
           split_n = (unsigned)n;
           p.w = p.w / n;
-          ++n_split;
-          n_dau += split_n - 1;
+          atomicAdd(&s_rare[0], 1u);
+          atomicAdd(&s_rare[1], split_n - 1);
         } else if (p.w < c * a.inv_rho) {
           if (u1 * c < p.w) {
             p.w = c;
-            ++n_rs;
+            atomicAdd(&s_rare[4], 1u);
           } else {
             p.alive = false;
-            ++n_rk;
+            atomicAdd(&s_rare[3], 1u);
           }
         }
       }
+    }
+    // ---- look-ahead source claim: the reservation is spent and lanes will need
+    // particles; the atomic's latency hides behind the census and tally work
+    if (r_lo == r_hi && !r_pend && !src_done) {
+      if (lane == 0) r_next = (unsigned)atomicAdd(a.src_head, (unsigned long long)kClaim);
+      r_pend = true;
     }
     // ---- bank census particles. Slots come from a per-warp chunk of the census
     // bank (one global atomic per kCensusChunk particles, not one per warp per
@@ -454,7 +578,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       const unsigned cmask = __ballot_sync(0xffffffffu, cen_cell >= 0);
       if (cmask) {
         const unsigned k = __popc(cmask);
-        const unsigned long long avail = wend - wcur;
+        const unsigned avail = wleft;
         unsigned long long nb = 0;
         if (k > avail) {
           if (lane == 0) nb = atomicAdd(a.census_count, (unsigned long long)kCensusChunk);
@@ -472,9 +596,10 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
         }
         if (k > avail) {
           wcur = nb + (k - avail);
-          wend = nb + kCensusChunk;
+          wleft = kCensusChunk - (k - avail);
         } else {
           wcur += k;
+          wleft -= k;
         }
       }
     }
@@ -482,7 +607,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
     // ---- commit the event's tallies, warp-aggregated (lanes sharing a cell
     // are summed with shuffles first: one CAS per distinct address, not per lane)
     if (a.aggregate) {  // cold-start segments: most lanes share a few cells
-      if (sh) {
+      if (shf) {
         agg_add_count(S.trk, S.trc, trk_key, trk_v, trk_cell);
         agg_add3(S.cphi, S.cJ, S.cF, cen_cell, cen_phi, cen_J, cen_F);
         agg_add(S.cwb, cen_b, cen_w);
@@ -495,12 +620,12 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
         agg_add(a.t.edge_current, edge_key, edge_v);
       }
     } else {  // spread population: per-lane atomics, no warp synchronisation
-      double* trk = sh ? S.trk : a.t.track_flux_batch;
-      double* cphi = sh ? S.cphi : a.t.census_phi;
-      double* cJ = sh ? S.cJ : a.t.census_current;
-      double* cF = sh ? S.cF : a.t.census_closure;
-      double* cwb = sh ? S.cwb : a.t.census_weight_batch;
-      double* edg = sh ? S.edge : a.t.edge_current;
+      double* trk = kShf ? S.trk : a.t.track_flux_batch;
+      double* cphi = kShf ? S.cphi : a.t.census_phi;
+      double* cJ = kShf ? S.cJ : a.t.census_current;
+      double* cF = kShf ? S.cF : a.t.census_closure;
+      double* cwb = kShf ? S.cwb : a.t.census_weight_batch;
+      double* edg = kShf ? S.edge : a.t.edge_current;
       if (trk_key >= 0) {
         atomicAdd(trk + trk_key, trk_v);
         if (sh) atomicAdd(S.trc + trk_cell, 1u);
@@ -533,7 +658,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
         donate = __shfl_sync(0xffffffffu, open, 0) != 0;
       }
       const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell, p.hist, p.key, p.ctr,
-                             dau, 0u, 0u};
+                             dau, 0u, 0u};  // base 0: daughters 1..dau
       bool push_local = dau > 0 && !donate;
       if (dau > 0 && donate) {
         // the record's active unit; ordered before this warp's own decrement by
@@ -568,7 +693,7 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
 
   if (lane == 0) {
     a.warp_cursor[2 * gwarp] = wcur;
-    a.warp_cursor[2 * gwarp + 1] = wend;
+    a.warp_cursor[2 * gwarp + 1] = wcur + wleft;
   }
   if (a.timeline) {
     unsigned long long ev = n_ev;
@@ -583,7 +708,21 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
   }
 
   // ---- flush block-private tallies
-  if (sh) {
+  if (shf && a.flush_replicas) {
+    // into one of R global replicas of the smem layout (R-fold less same-address
+    // contention than every block adding into the one tally set at segment end);
+    // k_flush_reduce folds the replicas into the tallies
+    __syncthreads();
+    double* rep = a.flush_scratch + (size_t)(blockIdx.x % a.flush_replicas) * a.flush_stride;
+    const int nd = (a.nb + 4) * I + 1 + a.nb + 2;
+    for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+      const double v = S.trk[i];
+      if (v != 0.0) atomicAdd(rep + i, v);
+    }
+    unsigned long long* rc = reinterpret_cast<unsigned long long*>(rep + nd);
+    for (int i = threadIdx.x; i < I; i += blockDim.x)
+      if (S.trc[i]) atomicAdd(rc + i, (unsigned long long)S.trc[i]);
+  } else if (shf) {
     __syncthreads();
     const int nb = a.nb;
     for (int i = threadIdx.x; i < nb * I; i += blockDim.x) {
@@ -602,35 +741,68 @@ __global__ void __launch_bounds__(kThreads) k_fast_segment(FastArgs a) {
       if (S.cwb[i] != 0.0) atomicAdd(&a.t.census_weight_batch[a.b_lo + i], S.cwb[i]);
     if (threadIdx.x < 2 && S.bclo[threadIdx.x] != 0.0)
       atomicAdd(&a.t.boundary_closure[threadIdx.x], S.bclo[threadIdx.x]);
+  } else if (sh) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < I; i += blockDim.x)
+      if (S.trc[i]) atomicAdd(&a.t.tracks[i], (unsigned long long)S.trc[i]);
+  } else {
+    __syncthreads();
+  }
+  if (threadIdx.x < 6 && s_rare[threadIdx.x]) {
+    // s_rare[0..4] follow UCounter kSplits..kRouletteSurvivals; [5] is grazing
+    const int slot = threadIdx.x < 5 ? kSplits + (int)threadIdx.x : kGrazingDiscarded;
+    atomicAdd(&a.t.ucount[slot], (unsigned long long)s_rare[threadIdx.x]);
   }
 
   // ---- counters (warp-aggregated)
-  auto wsum = [](unsigned long long v) {
+  auto wsum = [](unsigned v32) {
+    unsigned long long v = v32;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;
   };
-  n_coll = wsum(n_coll);
-  n_split = wsum(n_split);
-  n_dau = wsum(n_dau);
-  n_rk = wsum(n_rk);
-  n_rs = wsum(n_rs);
-  n_cen = wsum(n_cen);
-  n_graze = wsum(n_graze);
-  n_capped = wsum(n_capped);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) leak += __shfl_down_sync(0xffffffffu, leak, o);
+  const unsigned long long coll = wsum(n_coll), cen = wsum(n_cen);
   if (lane == 0) {
     unsigned long long* u = a.t.ucount;
-    if (n_coll) atomicAdd(&u[kCollisions], n_coll);
-    if (n_split) atomicAdd(&u[kSplits], n_split);
-    if (n_dau) atomicAdd(&u[kSplitDaughters], n_dau);
-    if (n_capped) atomicAdd(&u[kCappedSplits], n_capped);
-    if (n_rk) atomicAdd(&u[kRouletteKills], n_rk);
-    if (n_rs) atomicAdd(&u[kRouletteSurvivals], n_rs);
-    if (n_cen) atomicAdd(&u[kCensusCount], n_cen);
-    if (n_graze) atomicAdd(&u[kGrazingDiscarded], n_graze);
-    if (leak != 0.0) atomicAdd(&a.t.dcount[0], leak);
+    if (coll) atomicAdd(&u[kCollisions], coll);
+    if (cen) atomicAdd(&u[kCensusCount], cen);
+  }
+}
+
+// Folds the flush replicas into the tallies and re-zeroes them: one owner per
+// word, so plain adds (the layout is k_fast_segment's shared-memory layout from
+// the track-batch block on: trk[nb*I], cphi, cJ, cF [I], edge[I+1], cwb[nb],
+// bclosure[2], then the track counts as u64[I]).
+__global__ void k_flush_reduce(double* scratch, int R, size_t stride, int I, int nb, int b_lo,
+                               TallyPtrs t) {
+  const int nd = (nb + 4) * I + 1 + nb + 2;
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < nd + I; w += gridDim.x * blockDim.x) {
+    if (w < nd) {
+      double v = 0.0;
+      for (int r = 0; r < R; ++r) {
+        double* q = scratch + (size_t)r * stride + w;
+        v += *q;
+        *q = 0.0;
+      }
+      if (v == 0.0) continue;
+      double* dst;
+      if (w < nb * I) dst = t.track_flux_batch + (size_t)b_lo * I + w;
+      else if (w < (nb + 1) * I) dst = t.census_phi + (w - nb * I);
+      else if (w < (nb + 2) * I) dst = t.census_current + (w - (nb + 1) * I);
+      else if (w < (nb + 3) * I) dst = t.census_closure + (w - (nb + 2) * I);
+      else if (w < (nb + 4) * I + 1) dst = t.edge_current + (w - (nb + 3) * I);
+      else if (w < (nb + 4) * I + 1 + nb) dst = t.census_weight_batch + b_lo + (w - ((nb + 4) * I + 1));
+      else dst = t.boundary_closure + (w - ((nb + 4) * I + 1 + nb));
+      *dst += v;
+    } else {
+      unsigned long long c = 0;
+      for (int r = 0; r < R; ++r) {
+        unsigned long long* q = reinterpret_cast<unsigned long long*>(scratch + (size_t)r * stride + nd) + (w - nd);
+        c += *q;
+        *q = 0ULL;
+      }
+      if (c) t.tracks[w - nd] += c;
+    }
   }
 }
 
@@ -650,8 +822,10 @@ __global__ void k_aos_to_fast(const hwwg_particle* __restrict__ in, uint64_t n, 
 }  // namespace
 
 size_t fast_smem_bytes(int I, int nb) {
-  return ((size_t)(nb + 4) * I + 1 + nb + 2) * sizeof(double) + (size_t)I * sizeof(unsigned) + 16;
+  return ((size_t)(nb + 4) * I + 1 + nb + 2) * sizeof(double) + (size_t)(I + 1) / 2 * 8 + 16;
 }
+size_t fast_smem_count_bytes(int I) { return (size_t)(I + 1) / 2 * 8 + 16; }
+size_t fast_flush_stride(int I, int B) { return (size_t)(B + 4) * I + 1 + B + 2 + I; }
 
 int fast_threads_per_block() { return kThreads; }
 
@@ -660,7 +834,7 @@ void configure_fast_kernel();
 int fast_blocks_per_sm(size_t smem) {
   configure_fast_kernel();
   int n = 0;
-  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment<false>, kThreads, smem));
+  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment<true, true>, kThreads, smem));
   return n;
 }
 
@@ -671,17 +845,16 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
   ctl[1] = 0;
   ctl[2] = warps;  // every warp starts active (holding source work)
   ctl[3] = 0;      // no backlog declared yet
-  *src_head = 0;
+  *src_head = warps * kClaim;  // every warp's first reservation is static
 }
 }  // namespace
 
 void configure_fast_kernel() {
   static bool configured = false;
   if (!configured) {
-    HWWG_CUDA(cudaFuncSetAttribute(k_fast_segment<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    HWWG_CUDA(cudaFuncSetAttribute(k_fast_segment<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto k : {k_fast_segment<false, false>, k_fast_segment<false, true>,
+                   k_fast_segment<true, false>, k_fast_segment<true, true>})
+      HWWG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
 }
@@ -690,9 +863,17 @@ void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_
   configure_fast_kernel();
   k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head,
                                   (unsigned long long)blocks * kWarpsPerBlock);
-  if (a.uniform) k_fast_segment<true><<<blocks, kThreads, smem, s>>>(a);
-  else k_fast_segment<false><<<blocks, kThreads, smem, s>>>(a);
+  const bool shf = a.smem_tallies == 1;
+  if (a.uniform && shf) k_fast_segment<true, true><<<blocks, kThreads, smem, s>>>(a);
+  else if (a.uniform) k_fast_segment<true, false><<<blocks, kThreads, smem, s>>>(a);
+  else if (shf) k_fast_segment<false, true><<<blocks, kThreads, smem, s>>>(a);
+  else k_fast_segment<false, false><<<blocks, kThreads, smem, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
+  if (shf && a.flush_replicas) {
+    k_flush_reduce<<<32, 256, 0, s>>>(a.flush_scratch, a.flush_replicas, a.flush_stride, a.mesh.I,
+                                      a.nb, a.b_lo, a.t);
+    HWWG_CUDA(cudaGetLastError());
+  }
 }
 
 void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
