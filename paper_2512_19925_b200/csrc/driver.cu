@@ -121,6 +121,22 @@ struct hwwg_driver {
   int flush_replicas = 0;  // FastArgs::flush_replicas (HWWG_FAST_FLUSH_R; 0 = direct REDs, measured best)
   DevBuf<double> flush_scratch;
   bool timeline_on = false;
+  // HWWG_PHASES=1: CUDA-event time of the step's non-transport phases (stderr)
+  bool phases_on = false;
+  std::vector<cudaEvent_t> ph_ev;
+  std::vector<const char*> ph_name;
+  size_t ph_n = 0;
+  void ph_mark(const char* name, cudaStream_t s) {  // closes the previous phase, opens `name`
+    if (!phases_on) return;
+    if (ph_n >= ph_ev.size()) {
+      cudaEvent_t e;
+      HWWG_CUDA(cudaEventCreate(&e));
+      ph_ev.push_back(e);
+      ph_name.push_back(name);
+    }
+    ph_name[ph_n] = name;
+    HWWG_CUDA(cudaEventRecord(ph_ev[ph_n++], s));
+  }
   DevBuf<unsigned long long> timeline;
   unsigned timeline_warps = 0;
   DevBuf<unsigned long long> warp_cursor;  // per-warp census chunks
@@ -156,6 +172,7 @@ struct hwwg_driver {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : seg_ev) cudaEventDestroy(e);
+    for (auto e : ph_ev) cudaEventDestroy(e);
     if (host_bank) cudaFreeHost(host_bank);
     if (comm) ncclCommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
@@ -460,7 +477,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.out = d->fsrc.view();
     a.temp = d->comb_temp.p;
     a.temp_bytes = tb;
+    d->ph_mark("comb", s);
     launch_fast_comb(a, s);
+    d->ph_mark("-", s);
     d->launches += 3;
     H = d->target;
     rec->comb_in = d->bank_n;
@@ -519,6 +538,35 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
 
   unsigned long long count = 0;
   DevError derr{};
+  const int cur = d->rep_cur;
+  // finalize (driver.cpp:221-222): device-side from the tallies alone
+  auto enqueue_finalize = [&]() {
+    if (d->fast) {  // the fast kernels score the batch table only
+      launch_track_from_batches(d->tal.p, I, B, s);
+      ++d->launches;
+    }
+    FinalizeArgs f{};
+    f.I = I;
+    f.B = B;
+    f.t = d->tal.p;
+    f.histories = H;
+    f.normalization = (double)c.histories_per_step;
+    f.phi_track = d->rep(cur, 0);
+    f.sigma = d->rep(cur, 1);
+    f.phi_census = d->rep(cur, 2);
+    f.current = d->rep(cur, 3);
+    f.closure = d->rep(cur, 4);
+    f.edge = d->rep(cur, 5);
+    f.scalars = d->rep(cur, 6);
+    launch_finalize(f, s);
+    ++d->launches;
+  };
+  // Single-GPU Philox steps finalize BEFORE the one host sync that reads the
+  // census count and the error word (an overflow, which the up-front census
+  // capacity makes rare, replays the whole step and finalizes again), so the
+  // device never idles on a host round trip in the middle of a step.
+  const bool early_finalize = d->fast && d->world == 1;
+  bool ev1_recorded = false;
   for (int attempt = 0; attempt < 4; ++attempt) {
     if (attempt) {  // replay: restore the windows the step started from
       HWWG_CUDA(cudaMemcpyAsync(d->lo.centers, d->centers_backup.p, I * 8, cudaMemcpyDeviceToDevice, s));
@@ -559,7 +607,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.s.rep_current = d->rep(prev, 3);
       a.s.rep_closure = d->rep(prev, 4);
       a.s.rep_PLPR = d->rep(prev, 6);
+      d->ph_mark("losm0", s);
       launch_low_order_update(a, s);
+      d->ph_mark("-", s);
       ++d->launches;
     }
 
@@ -707,13 +757,29 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       const double effective = (double)c.histories_per_step * (double)h_done / (double)H;
       a.snapshot_inv_norm = 1.0 / effective;
       a.s = d->lo;
+      d->ph_mark("losm1", s);
       launch_low_order_update(a, s);
+      if (std::getenv("HWWG_LOSM_TWICE")) {  // diagnostic: a warm second launch
+        d->ph_mark("losm1b", s);
+        launch_low_order_update(a, s);
+      }
+      d->ph_mark("-", s);
       ++d->launches;
     }
     if (d->fast) {  // zero-weight records in the unused tails of the warps' chunks
+      d->ph_mark("fill", s);
       launch_fill_census_holes(d->fcensus.view(), d->fcensus.cap(), d->warp_cursor.p,
                                d->max_warps, d->prob.edges.front(), rec->t_end, s);
       ++d->launches;
+    }
+    if (early_finalize) {
+      d->ph_mark("finalize", s);
+      enqueue_finalize();
+      d->ph_mark("-", s);
+      if (!c.host_bank) {
+        HWWG_CUDA(cudaEventRecord(d->ev1, s));
+        ev1_recorded = true;
+      }
     }
     HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaMemcpyAsync(&derr, d->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
@@ -742,6 +808,19 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->stage.ensure(count + count / 4 + 4096);
   }
   if (d->timeline_on) print_timeline(d, (int)thr.size() + 1, step);
+  if (d->phases_on) {  // the stream is synchronised here
+    std::string line = "[phases] step " + std::to_string(step) + ":";
+    for (size_t k = 0; k + 1 < d->ph_n; ++k) {
+      if (d->ph_name[k][0] == '-') continue;
+      float ms = 0.f;
+      HWWG_CUDA(cudaEventElapsedTime(&ms, d->ph_ev[k], d->ph_ev[k + 1]));
+      char buf[64];
+      std::snprintf(buf, sizeof buf, " %s %.1f", d->ph_name[k], 1e3 * ms);
+      line += buf;
+    }
+    std::fprintf(stderr, "%s us\n", line.c_str());
+    d->ph_n = 0;
+  }
   if (derr.code == HWWG_EINVAL)
     throw ApiError(HWWG_EINVAL, "history " + std::to_string(derr.history) +
                                     " starts outside the mesh or the time step");
@@ -757,26 +836,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     NCCL_CHECK(ncclAllReduce(u64part, u64part, (size_t)I + kNumUCounters, ncclUint64, ncclSum,
                              d->comm, s));
   }
-  if (d->fast) {  // the fast kernels score the batch table only
-    launch_track_from_batches(d->tal.p, I, B, s);
-    ++d->launches;
-  }
-  FinalizeArgs f{};
-  f.I = I;
-  f.B = B;
-  f.t = d->tal.p;
-  f.histories = H;
-  f.normalization = (double)c.histories_per_step;
-  const int cur = d->rep_cur;
-  f.phi_track = d->rep(cur, 0);
-  f.sigma = d->rep(cur, 1);
-  f.phi_census = d->rep(cur, 2);
-  f.current = d->rep(cur, 3);
-  f.closure = d->rep(cur, 4);
-  f.edge = d->rep(cur, 5);
-  f.scalars = d->rep(cur, 6);
-  launch_finalize(f, s);
-  ++d->launches;
+  if (!early_finalize) enqueue_finalize();
 
   // ---- census -> next bank in reference order
   if (d->fast) {
@@ -794,7 +854,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (count) d->launches += 2;  // iota + gather (the radix sort itself is CUB's)
   }
   d->bank_n = count;
-  HWWG_CUDA(cudaEventRecord(d->ev1, s));
+  if (!ev1_recorded) HWWG_CUDA(cudaEventRecord(d->ev1, s));
 
   // ---- read the step record back (one sync)
   std::vector<double> rep_h((size_t)7 * (I + 1) + 8);
@@ -923,6 +983,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   }
   d->fast = d->opt.rng_mode == HWWG_RNG_PHILOX;
   d->timeline_on = d->fast && std::getenv("HWWG_FAST_TIMELINE") != nullptr;
+  d->phases_on = std::getenv("HWWG_PHASES") != nullptr;
   if (const char* m = std::getenv("HWWG_FAST_SMEM")) d->smem_mode = std::atoi(m) % 3;
   if (const char* m = std::getenv("HWWG_FAST_SCRAMBLE")) d->scramble = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));

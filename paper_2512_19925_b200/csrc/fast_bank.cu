@@ -5,9 +5,10 @@
 // one random offset walk the cumulative-weight axis of the bank — but the
 // cumulative weights come from a parallel fp64 scan (CUB decoupled look-back,
 // deterministic for a given bank order) instead of a serial walk, and each
-// tooth finds its particle by binary search. Teeth land in bank order, so the
-// new source stays grouped by parent history.
+// particle writes the teeth that fall in its cumulative-weight interval.
+// Teeth land in bank order.
 #include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 
 #include "common.cuh"
 #include "fast.cuh"
@@ -22,6 +23,53 @@ __global__ void k_extract_w(FastBank b, uint64_t n, double* w) {
   if (i < n) w[i] = b.wt[i].x;
 }
 
+// Particle-parallel teeth: particle i owns the teeth k with
+// prefix[i-1] <= T_k < prefix[i], T_k = offset + k * spacing — exactly the
+// teeth whose first index with T_k < prefix[idx] is i (the search definition),
+// since cnt(v) = #{k : T_k < v} is evaluated with the same fp64 T_k on both
+// sides of every boundary. Reads and writes are coalesced and there is no
+// search; teeth stranded past the total by round-off go to the last particle
+// with weight (popctrl.cpp:31-37).
+__device__ __forceinline__ uint64_t teeth_below(double v, double offset, double spacing,
+                                                uint64_t target) {
+  double e = ceil((v - offset) / spacing);
+  uint64_t k = e <= 0.0 ? 0 : (e >= (double)target ? target : (uint64_t)e);
+  while (k > 0 && !(offset + (double)(k - 1) * spacing < v)) --k;
+  while (k < target && offset + (double)k * spacing < v) ++k;
+  return k;
+}
+
+__device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src, uint64_t k0,
+                                            uint64_t k1, double spacing) {
+  const double2 xm = a.bank.xm[src];
+  const double2 wt = a.bank.wt[src];
+  const uint4 m = a.bank.meta[src];
+  for (uint64_t k = k0; k < k1; ++k) {
+    a.out.xm[k] = xm;
+    a.out.wt[k] = make_double2(spacing, wt.y);
+    // fresh identity for the new step: history = tooth index, key 0, draw 0
+    a.out.meta[k] = make_uint4(m.x & 0xffffu, (unsigned)k, 0u, 0u);
+  }
+}
+
+__global__ void k_comb_scatter(FastCombArgs a) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const double spacing = a.scalars[1], offset = a.scalars[2];
+  const uint64_t k0 = i ? teeth_below(a.prefix[i - 1], offset, spacing, a.target) : 0;
+  const uint64_t k1 = teeth_below(a.prefix[i], offset, spacing, a.target);
+  if (k0 < k1) write_teeth(a, i, k0, k1, spacing);
+  if (i == a.n - 1 && k1 < a.target) {  // stranded teeth
+    uint64_t s = i;
+    while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
+    write_teeth(a, s, k1, a.target, spacing);
+  }
+}
+
+struct WeightOf {
+  __host__ __device__ double operator()(const double2& v) const { return v.x; }
+};
+
 __global__ void k_comb_scalars(const double* prefix, uint64_t n, uint64_t target, uint64_t seed,
                                uint64_t stream, double* sc) {
   const double W = prefix[n - 1];
@@ -32,30 +80,6 @@ __global__ void k_comb_scalars(const double* prefix, uint64_t n, uint64_t target
   sc[1] = spacing;
   sc[2] = r.uniform() * spacing;
   sc[3] = spacing * (double)target;
-}
-
-__global__ void k_comb_teeth(FastCombArgs a) {
-  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= a.target) return;
-  const double spacing = a.scalars[1];
-  const double T = a.scalars[2] + (double)k * spacing;
-  uint64_t lo = 0, hi = a.n;  // first index with T < prefix[idx]
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (T < a.prefix[mid]) hi = mid;
-    else lo = mid + 1;
-  }
-  uint64_t s = lo < a.n ? lo : a.n - 1;
-  // a tooth stranded by round-off copies the last real particle (popctrl.cpp:31-37),
-  // skipping the zero-weight holes at the tail of census chunks
-  if (lo >= a.n)
-    while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
-  a.out.xm[k] = a.bank.xm[s];
-  const double2 wt = a.bank.wt[s];
-  a.out.wt[k] = make_double2(spacing, wt.y);
-  const uint4 m = a.bank.meta[s];
-  // fresh identity for the new step: history = tooth index, key 0, draw 0
-  a.out.meta[k] = make_uint4(m.x & 0xffffu, (unsigned)k, 0u, 0u);
 }
 
 __global__ void k_local_total(const double* prefix, uint64_t n, double* sc) {
@@ -82,12 +106,14 @@ __global__ void k_comb_teeth_range(FastCombArgs a, double spacing, double offset
   out.meta[o] = make_uint4(a.bank.meta[s].x & 0xffffu, (unsigned)k, 0u, 0u);
 }
 
+// one warp per transport warp's chunk tail (<= kCensusChunk slots), lanes in parallel
 __global__ void k_fill_holes(FastBank c, uint64_t cap, const unsigned long long* cur, int warps,
                              double x_fill, double t_fill) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (w >= warps) return;
   const unsigned long long end = cur[2 * w + 1] < cap ? cur[2 * w + 1] : cap;
-  for (unsigned long long s = cur[2 * w]; s < end; ++s) {
+  for (unsigned long long s = cur[2 * w] + lane; s < end; s += 32) {
     c.xm[s] = make_double2(x_fill, 0.5);
     c.wt[s] = make_double2(0.0, t_fill);
     c.meta[s] = make_uint4(0u, 0u, 0u, 0u);
@@ -130,19 +156,22 @@ __global__ void k_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out) {
 
 }  // namespace
 
+using WeightIt = cub::TransformInputIterator<double, WeightOf, const double2*>;
+
 size_t fast_comb_temp_bytes(uint64_t n) {
-  size_t bytes = 0;
+  size_t bytes = 0, b2 = 0;
   cub::DeviceScan::InclusiveSum(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (int)n);
-  return bytes;
+  cub::DeviceScan::InclusiveSum(nullptr, b2, WeightIt(nullptr, WeightOf()), (double*)nullptr, (int)n);
+  return bytes > b2 ? bytes : b2;
 }
 
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s) {
-  const unsigned bn = (unsigned)((a.n + 255) / 256);
-  k_extract_w<<<bn, 256, 0, s>>>(a.bank, a.n, a.prefix);
+  // inclusive scan of the weights straight from the SoA bank
   size_t bytes = a.temp_bytes;
-  HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, a.prefix, a.prefix, (int)a.n, s));
+  HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, WeightIt(a.bank.wt, WeightOf()), a.prefix,
+                                          (int)a.n, s));
   k_comb_scalars<<<1, 1, 0, s>>>(a.prefix, a.n, a.target, a.seed, a.stream, a.scalars);
-  k_comb_teeth<<<(unsigned)((a.target + 255) / 256), 256, 0, s>>>(a);
+  k_comb_scatter<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
 
@@ -168,7 +197,7 @@ void launch_fast_comb_teeth_range(const FastCombArgs& a, double spacing, double 
 
 void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,
                               int warps, double x_fill, double t_fill, cudaStream_t s) {
-  k_fill_holes<<<(warps + 127) / 128, 128, 0, s>>>(census, cap, warp_cursor, warps, x_fill, t_fill);
+  k_fill_holes<<<(warps + 7) / 8, 256, 0, s>>>(census, cap, warp_cursor, warps, x_fill, t_fill);
   HWWG_CUDA(cudaGetLastError());
 }
 

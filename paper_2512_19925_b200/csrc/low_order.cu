@@ -13,6 +13,8 @@
 
 #include "common.cuh"
 #include "libm_log.h"
+#include <cstdlib>
+
 #include "low_order.cuh"
 #include "rng.cuh"
 
@@ -317,9 +319,16 @@ __device__ bool all_finite(const double* v, int n) {
   return __syncthreads_or(bad ? 1 : 0) == 0;
 }
 
+// HWWG_LOSM_DEBUG: per-phase clock64 stamps of one update (thread 0, printf)
+__device__ unsigned long long g_lp[24];
+#define LP(k)                                              \
+  do {                                                     \
+    if (a.debug && threadIdx.x == 0) g_lp[k] = clock64();  \
+  } while (0)
+
 // driver.cpp:72-95 hybrid_windows + ww.cpp build_centers, given prepared
 // inputs. Solves into the sys scratch; on failure keeps the previous windows.
-__device__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double PLs, double PRs,
+__device__ __noinline__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double PLs, double PRs,
                                  bool implicit, double* red) {
   const LowOrderState& s = a.s;
   const int I = a.I, n = 2 * I + 3;
@@ -330,16 +339,20 @@ __device__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double
   double* fill = rh + n;
   double* x = fill + n;
   __shared__ int status;
+  LP(3);
   // check_inputs (losm.cpp:43-66): finite previous state and lagged closures
   const bool ok_in = all_finite(s.phi_prev, I + 2) && all_finite(s.J_prev, I + 1) &&
                      all_finite(s.F_prev, I + 2);
+  LP(4);
   if (ok_in) {
     assemble_rows(I, a.edges, a.cells, s.phi_prev, s.J_prev, 0.0, 0.0, Fs, PLs, PRs, s.F_prev,
                   a.theta, a.dt, nullptr, lo, di, up, rh);
     __syncthreads();
+    LP(5);
     if (a.fast_solve) {
       extern __shared__ double dyn[];
       const int bad = solve_schur_pcr(I, lo, di, up, rh, x, dyn);
+      LP(6);
       if (threadIdx.x == 0) status = bad ? 2 : 0;
     } else if (threadIdx.x == 0) {
       status = solve_pivoted_serial(n, lo, di, up, rh, fill, x) ? 2 : 0;
@@ -352,7 +365,9 @@ __device__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double
   if (st == 0) {
     for (int i = threadIdx.x; i < I; i += blockDim.x) s.phi_hybrid[i] = x[2 * (i + 1)];
     __syncthreads();
+    LP(7);
     build_centers_cta(s.phi_hybrid, I, a.eps_min, s.centers, red);
+    LP(8);
     if (threadIdx.x == 0) {
       s.flags[0] = 1;
       s.flags[1] = 1;
@@ -371,7 +386,62 @@ __device__ void solve_and_center(const LowOrderArgs& a, const double* Fs, double
   if (threadIdx.x == 0) s.flags[4] = st;
 }
 
+// Shared-memory residency for the whole update (when it fits, host-decided via
+// a.smem_state): the phases below are separated by block barriers, and with
+// the state, the 2I+3 system and the filter scratch in global memory every
+// phase paid an L2 round trip. Same operations on the same values either way.
+constexpr int kSmemStateMaxI = 1200;
+
+__device__ __noinline__ void low_order_update_body(const LowOrderArgs& a);
+
 __global__ void __launch_bounds__(kCtaThreads) k_low_order_update(LowOrderArgs a) {
+  if (!a.smem_state) {
+    low_order_update_body(a);
+    return;
+  }
+  extern __shared__ double dyn[];
+  LP(0);
+  const int I = a.I;
+  const LowOrderState g = a.s;
+  // dyn = [PCR scratch 4(I+2) | sys 6n | phi_prev | F_prev | F_now (I+2 each) | J_prev I+1 | phi_hybrid I]
+  double* q = dyn + (a.fast_solve ? (size_t)4 * (I + 2) : 0);
+  a.s.sys = q; q += (size_t)6 * (2 * I + 3);
+  a.s.phi_prev = q; q += I + 2;
+  a.s.F_prev = q; q += I + 2;
+  a.s.F_now = q; q += I + 2;
+  a.s.J_prev = q; q += I + 1;
+  a.s.phi_hybrid = q;
+  for (int i = threadIdx.x; i < I + 2; i += blockDim.x) {
+    a.s.phi_prev[i] = g.phi_prev[i];
+    a.s.F_prev[i] = g.F_prev[i];
+  }
+  for (int i = threadIdx.x; i < I + 1; i += blockDim.x) a.s.J_prev[i] = g.J_prev[i];
+  for (int i = threadIdx.x; i < I; i += blockDim.x) a.s.phi_hybrid[i] = g.phi_hybrid[i];
+  __syncthreads();
+  LP(1);
+  low_order_update_body(a);
+  __syncthreads();
+  LP(9);
+  if (a.mode == 0) {  // the filtered inputs persist for the step's mid-step solves
+    for (int i = threadIdx.x; i < I + 2; i += blockDim.x) {
+      g.phi_prev[i] = a.s.phi_prev[i];
+      g.F_prev[i] = a.s.F_prev[i];
+    }
+    for (int i = threadIdx.x; i < I + 1; i += blockDim.x) g.J_prev[i] = a.s.J_prev[i];
+  }
+  for (int i = threadIdx.x; i < I; i += blockDim.x) g.phi_hybrid[i] = a.s.phi_hybrid[i];
+  __syncthreads();
+  LP(10);
+  if (a.debug && threadIdx.x == 0) {
+    printf("[losm] mode %d cycles: load %llu prep %llu finite %llu assemble %llu solve %llu "
+           "status %llu centers %llu tail %llu store %llu total %llu\n", a.mode,
+           g_lp[1] - g_lp[0], g_lp[3] - g_lp[1], g_lp[4] - g_lp[3], g_lp[5] - g_lp[4],
+           g_lp[6] - g_lp[5], g_lp[7] - g_lp[6], g_lp[8] - g_lp[7], g_lp[9] - g_lp[8],
+           g_lp[10] - g_lp[9], g_lp[10] - g_lp[0]);
+  }
+}
+
+__device__ __noinline__ void low_order_update_body(const LowOrderArgs& a) {
   __shared__ double red[32];
   const LowOrderState& s = a.s;
   const int I = a.I;
@@ -469,6 +539,7 @@ __device__ __forceinline__ uint64_t batch_size(uint64_t H, int B, int b) {
 }
 
 // tally.cpp:68-114
+constexpr int kMaxFinalizeBatches = 1024;
 __global__ void k_finalize(FinalizeArgs a) {
   const int I = a.I, B = a.B;
   const double inv_h = 1.0 / a.normalization;
@@ -476,6 +547,21 @@ __global__ void k_finalize(FinalizeArgs a) {
   const double scale = (double)a.histories / a.normalization;
   const double ih = 1.0 / (double)a.histories;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // 1/batch size, once per block (64-bit divisions per cell and batch made
+  // this kernel ~20 us)
+  __shared__ double inv_nb_s[kMaxFinalizeBatches];
+  const bool cached = B <= kMaxFinalizeBatches;
+  if (cached)
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+      const uint64_t nb = batch_size(a.histories, B, b);
+      inv_nb_s[b] = nb ? 1.0 / (double)nb : 0.0;
+    }
+  __syncthreads();
+  auto inv_nb_of = [&](int b) {
+    if (cached) return inv_nb_s[b];
+    const uint64_t nb = batch_size(a.histories, B, b);
+    return nb ? 1.0 / (double)nb : 0.0;
+  };
   if (i < I) {
     a.phi_track[i] = a.t.track_flux[i] * inv_h;
     a.phi_census[i] = a.t.census_phi[i] * inv_h;
@@ -486,9 +572,7 @@ __global__ void k_finalize(FinalizeArgs a) {
       const double mean = a.t.track_flux[i] * ih;
       double ss = 0.0;
       for (int b = 0; b < B; ++b) {
-        const uint64_t nb = batch_size(a.histories, B, b);
-        const double inv_nb = nb ? 1.0 / (double)nb : 0.0;
-        const double bm = a.t.track_flux_batch[(size_t)b * I + i] * inv_nb;
+        const double bm = a.t.track_flux_batch[(size_t)b * I + i] * inv_nb_of(b);
         const double d = bm - mean;
         ss += d * d;
       }
@@ -508,9 +592,7 @@ __global__ void k_finalize(FinalizeArgs a) {
       const double wmean = cw * ih;
       double ss = 0.0;
       for (int b = 0; b < B; ++b) {
-        const uint64_t nb = batch_size(a.histories, B, b);
-        const double inv_nb = nb ? 1.0 / (double)nb : 0.0;
-        const double bm = a.t.census_weight_batch[b] * inv_nb;
+        const double bm = a.t.census_weight_batch[b] * inv_nb_of(b);
         const double d = bm - wmean;
         ss += d * d;
       }
@@ -625,16 +707,19 @@ __global__ void k_device_log(const double* x, uint64_t n, double* out) {
 
 }  // namespace
 
-void launch_low_order_update(const LowOrderArgs& a, cudaStream_t st) {
-  size_t smem = 0;
-  if (a.fast_solve) {
-    smem = (size_t)4 * (a.I + 2) * sizeof(double);
-    static size_t configured = 0;
-    if (smem > configured) {
-      HWWG_CUDA(cudaFuncSetAttribute(k_low_order_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-      configured = smem;
-    }
+void launch_low_order_update(const LowOrderArgs& a_in, cudaStream_t st) {
+  LowOrderArgs a = a_in;
+  static const bool dbg = std::getenv("HWWG_LOSM_DEBUG") != nullptr;
+  a.debug = dbg ? 1 : 0;
+  size_t smem = a.fast_solve ? (size_t)4 * (a.I + 2) * sizeof(double) : 0;
+  a.smem_state = a.I <= kSmemStateMaxI ? 1 : 0;
+  if (a.smem_state)
+    smem += ((size_t)6 * (2 * a.I + 3) + (size_t)3 * (a.I + 2) + (a.I + 1) + a.I) * sizeof(double);
+  static size_t configured = 0;
+  if (smem > configured) {
+    HWWG_CUDA(cudaFuncSetAttribute(k_low_order_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    configured = smem;
   }
   k_low_order_update<<<1, kCtaThreads, smem, st>>>(a);
   HWWG_CUDA(cudaGetLastError());

@@ -34,6 +34,8 @@ struct LowOrderState {
 
 struct LowOrderArgs {
   int I;
+  int smem_state;  // set by launch_low_order_update: state + system in shared memory
+  int debug;       // HWWG_LOSM_DEBUG: printf per-phase cycle counts
   const double* edges;
   const CellInfo* cells;
   double theta, dt;

@@ -87,54 +87,62 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Warp-aggregated atomic add: lanes with the same key (MATCH.ANY) are summed
-// by shuffles, then the group's lowest lane issues ONE atomic. key < 0: no
-// contribution. Must be called by all 32 lanes. In the cold-start steps most
-// of a warp sits in a few cells around the pulse, where per-lane fp64 CAS
-// loops on shared memory serialised; here a group costs max(group) shuffles.
-__device__ __forceinline__ unsigned agg_group(int key, unsigned& rest) {
+// Warp-aggregated atomic add: lanes with the same key (MATCH.ANY) are summed,
+// then the group's lowest lane issues ONE atomic. key < 0: no contribution.
+// Must be called by all 32 lanes. In the cold-start steps most of a warp sits
+// in a few cells around the pulse, where per-lane fp64 CAS loops on shared
+// memory serialise.
+__device__ __forceinline__ unsigned agg_group(int key) {
   const int lane = threadIdx.x & 31;
-  const bool has = key >= 0;
-  const unsigned grp = __match_any_sync(0xffffffffu, has ? key : -1 - lane);
-  rest = has ? (grp & ~(1u << lane)) : 0u;
-  return grp;
+  return __match_any_sync(0xffffffffu, key >= 0 ? key : -1 - lane);
+}
+
+// Sum of v over the lanes of `grp` (a MATCH.ANY group holding this lane) with
+// three integer REDUX ops, whatever the group size: every value is put on the
+// fixed-point grid 2^-56 below the group's largest magnitude (finer than the
+// fp64 rounding of any sum that includes that value) and the 64-bit integer
+// sum is exact; one rounding back to fp64. Non-finite groups take shuffles.
+__device__ __forceinline__ double group_sum(unsigned grp, double v) {
+  const unsigned e = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
+  const unsigned emax = __reduce_max_sync(grp, e);
+  if (emax == 0x7ffu) {  // inf/nan somewhere in the group
+    double t = 0.0;
+    for (unsigned m = grp; m; m &= m - 1) t += __shfl_sync(grp, v, __ffs(m) - 1);
+    return t;
+  }
+  if (emax < 64u) return 0.0;  // every |v| < 2^-959
+  const int sh = 56 - ((int)emax - 1023);  // |v * 2^sh| < 2^57: 32 lanes sum below 2^62
+  const long long q = __double2ll_rn(v * __hiloint2double((sh + 1023) << 20, 0));
+  const unsigned lo = (unsigned)q & 0x1fffffu;
+  const unsigned mid = (unsigned)(q >> 21) & 0x1fffffu;
+  const int hi = (int)(q >> 42);
+  const unsigned slo = __reduce_add_sync(grp, lo);
+  const unsigned smid = __reduce_add_sync(grp, mid);
+  const int shi = __reduce_add_sync(grp, hi);
+  const long long tot = ((long long)shi << 42) + ((long long)smid << 21) + (long long)slo;
+  return (double)tot * __hiloint2double((1023 - sh) << 20, 0);
+}
+
+__device__ __forceinline__ bool group_leader(unsigned grp) {
+  return (int)(threadIdx.x & 31) == __ffs(grp) - 1;
 }
 
 __device__ __forceinline__ void agg_add(double* base, int key, double v) {
   if (!__any_sync(0xffffffffu, key >= 0)) return;
-  unsigned rest;
-  const unsigned grp = agg_group(key, rest);
-  double s = v;
-  while (__any_sync(0xffffffffu, rest != 0)) {
-    const int src = rest ? __ffs(rest) - 1 : (threadIdx.x & 31);
-    const double o = __shfl_sync(0xffffffffu, v, src);
-    if (rest) {
-      s += o;
-      rest &= rest - 1;
-    }
-  }
-  if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(base + key, s);
+  const unsigned grp = agg_group(key);
+  const double s = group_sum(grp, key >= 0 ? v : 0.0);
+  if (key >= 0 && group_leader(grp)) atomicAdd(base + key, s);
 }
 
 __device__ __forceinline__ void agg_add3(double* b0, double* b1, double* b2, int key, double v0,
                                          double v1, double v2) {
   if (!__any_sync(0xffffffffu, key >= 0)) return;
-  unsigned rest;
-  const unsigned grp = agg_group(key, rest);
-  double s0 = v0, s1 = v1, s2 = v2;
-  while (__any_sync(0xffffffffu, rest != 0)) {
-    const int src = rest ? __ffs(rest) - 1 : (threadIdx.x & 31);
-    const double o0 = __shfl_sync(0xffffffffu, v0, src);
-    const double o1 = __shfl_sync(0xffffffffu, v1, src);
-    const double o2 = __shfl_sync(0xffffffffu, v2, src);
-    if (rest) {
-      s0 += o0;
-      s1 += o1;
-      s2 += o2;
-      rest &= rest - 1;
-    }
-  }
-  if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) {
+  const unsigned grp = agg_group(key);
+  const bool has = key >= 0;
+  const double s0 = group_sum(grp, has ? v0 : 0.0);
+  const double s1 = group_sum(grp, has ? v1 : 0.0);
+  const double s2 = group_sum(grp, has ? v2 : 0.0);
+  if (has && group_leader(grp)) {
     atomicAdd(b0 + key, s0);
     atomicAdd(b1 + key, s1);
     atomicAdd(b2 + key, s2);
@@ -146,18 +154,9 @@ template <class Count>
 __device__ __forceinline__ void agg_add_count_t(double* base, Count* cnt, int key, double v,
                                                 int cell) {
   if (!__any_sync(0xffffffffu, key >= 0)) return;
-  unsigned rest;
-  const unsigned grp = agg_group(key, rest);
-  double s = v;
-  while (__any_sync(0xffffffffu, rest != 0)) {
-    const int src = rest ? __ffs(rest) - 1 : (threadIdx.x & 31);
-    const double o = __shfl_sync(0xffffffffu, v, src);
-    if (rest) {
-      s += o;
-      rest &= rest - 1;
-    }
-  }
-  if (key >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1) {
+  const unsigned grp = agg_group(key);
+  const double s = group_sum(grp, key >= 0 ? v : 0.0);
+  if (key >= 0 && group_leader(grp)) {
     atomicAdd(base + key, s);
     atomicAdd(cnt + cell, (Count)__popc(grp));
   }
