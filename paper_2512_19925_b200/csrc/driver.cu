@@ -153,6 +153,19 @@ struct hwwg_driver {
 
   // low-order state
   DevBuf<double> lo_mem;
+  DevBuf<double> lo_fac;  // cached LOSM factorization (throughput mode)
+  bool losm_cache = true;  // HWWG_LOSM_NOCACHE=1 disables it
+  bool fac_valid = false;
+  double fac_theta = 0.0, fac_dt = 0.0;
+  // 1 when the cached factorization does not match (theta, dt): the next
+  // update kernel rebuilds it (launches are stream-ordered)
+  int need_refactor(double theta, double dt) {
+    if (fac_valid && fac_theta == theta && fac_dt == dt) return 0;
+    fac_valid = true;
+    fac_theta = theta;
+    fac_dt = dt;
+    return 1;
+  }
   DevBuf<int> lo_flags;
   LowOrderState lo{};
   DevBuf<double> centers_backup;
@@ -232,6 +245,14 @@ void init_driver(hwwg_driver* d) {
   s.phi_hybrid = q; q += I;
   s.sys = q; q += 6 * (size_t)n;
   s.F_now = q; q += I + 2;
+  s.fac = nullptr;
+  if (d->fast && d->losm_cache && lo_fac_words(I)) {  // cached LOSM factorization
+    d->lo_fac.reserve(lo_fac_words(I));
+    s.fac = d->lo_fac.p;
+    static const double kUnbuilt = 2.0;  // state word (last): not built yet
+    HWWG_CUDA(cudaMemcpyAsync(d->lo_fac.p + lo_fac_words(I) - 1, &kUnbuilt, sizeof(double),
+                              cudaMemcpyHostToDevice, d->stream));
+  }
   d->lo_flags.reserve(8);
   HWWG_CUDA(cudaMemsetAsync(d->lo_flags.p, 0, 8 * sizeof(int), d->stream));
   s.flags = d->lo_flags.p;
@@ -596,6 +617,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.ma_k = ma_k;
       a.mode = 0;
       a.fast_solve = d->fast ? 1 : 0;
+      a.refactor = d->need_refactor(theta_eff, dt);
       a.analytic = step == 1;
       if (step == 1) {
         const int cell = locate_host(d->prob.edges, c.x0);
@@ -743,6 +765,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.ma_k = ma_k;
       a.mode = 1;
       a.fast_solve = d->fast ? 1 : 0;
+      a.refactor = d->need_refactor(theta_eff, dt);
       a.closure_tally = d->tal.p.census_closure;
       a.bclosure_tally = d->tal.p.boundary_closure;
       if (d->world > 1) {  // the snapshot is of ALL ranks' histories so far
@@ -984,6 +1007,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   d->fast = d->opt.rng_mode == HWWG_RNG_PHILOX;
   d->timeline_on = d->fast && std::getenv("HWWG_FAST_TIMELINE") != nullptr;
   d->phases_on = std::getenv("HWWG_PHASES") != nullptr;
+  d->losm_cache = std::getenv("HWWG_LOSM_NOCACHE") == nullptr;
   if (const char* m = std::getenv("HWWG_FAST_SMEM")) d->smem_mode = std::atoi(m) % 3;
   if (const char* m = std::getenv("HWWG_FAST_SCRAMBLE")) d->scramble = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
@@ -997,6 +1021,14 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
     delete d;
     return fail(HWWG_EINVAL, "philox mode: fission and > 65535 cells are not supported");
+  }
+  // history ids are 32-bit and the batch of history h is one fp64 division
+  // (exact while h * batches < 2^53)
+  const uint64_t tgt = cfg->target_population ? cfg->target_population : cfg->histories_per_step;
+  if (d->fast && (tgt >= (1ULL << 32) - (1ULL << 26) || cfg->batches > (1 << 20))) {
+    delete d;
+    return fail(HWWG_EINVAL, "philox mode: histories per step must stay below 2^32 - 2^26 "
+                             "and batches below 2^20");
   }
   try {
     init_driver(d);

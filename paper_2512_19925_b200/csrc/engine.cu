@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -406,6 +407,100 @@ int hwwg_uniform_comb(hwwg_ctx* c, const hwwg_particle* bank, uint64_t n, uint64
   if (in_weight) *in_weight = sc[0];
   if (out_weight) *out_weight = sc[3];
   return HWWG_OK;
+  HWWG_API_END
+}
+
+// Test hook (not part of include/hwwg.h): the throughput-mode window update
+// solved through the cached factorization must give bit-identical centres and
+// hybrid flux to the same update rebuilding the factorization. Synthetic
+// smooth inputs on a uniform I-cell slab; returns the number of differing
+// values (or a negative status), *max_abs_diff their largest difference.
+int hwwg_internal_losm_cache_check(hwwg_ctx* c, int32_t I, uint32_t seed, double* max_abs_diff) {
+  HWWG_API_BEGIN
+  if (!c || I < 2 || !max_abs_diff) return fail(HWWG_EINVAL, "bad argument");
+  if (!lo_fac_words(I)) return fail(HWWG_EINVAL, "I too large for the cached factorization");
+  HWWG_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  std::vector<double> edges(I + 1);
+  for (int e = 0; e <= I; ++e) edges[e] = -20.0 + 40.0 * e / I;
+  std::vector<hwwg_material> mats(I, hwwg_material{1.0, 0.9, 0.0, 0.0, 1.0});
+  std::string why;
+  if (!c->prob.set(edges.data(), I, mats.data(), s, why)) return fail(HWWG_EINVAL, why);
+  uint64_t z = seed * 0x9E3779B97F4A7C15ULL + 1;
+  auto rnd = [&]() {  // splitmix64 -> [0, 1)
+    z += 0x9E3779B97F4A7C15ULL;
+    uint64_t t = z;
+    t = (t ^ (t >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    t = (t ^ (t >> 27)) * 0x94D049BB133111EBULL;
+    return (double)((t ^ (t >> 31)) >> 11) * 0x1.0p-53;
+  };
+  const int n = 2 * I + 3;
+  const size_t fw = lo_fac_words(I);
+  // phi_prev I+2 | J_prev I+1 | F_prev I+2 | PLPR 2 | centers I | hybrid I | sys 6n | F_now I+2 |
+  // closure I | bclosure 2 | fac
+  const size_t words = (size_t)(I + 2) * 3 + (I + 1) + 2 + 2 * (size_t)I + 6 * (size_t)n + I + 2 + fw;
+  c->scratch.reserve(words);
+  c->iscratch.reserve(8);
+  std::vector<double> h(words, 0.0);
+  double* q = h.data();
+  for (int i = 0; i < I + 2; ++i) q[i] = std::exp(-0.01 * (i - I / 2) * (i - I / 2)) + 0.01 * rnd();
+  q += I + 2;
+  for (int i = 0; i < I + 1; ++i) q[i] = 0.1 * (rnd() - 0.5);
+  q += I + 1;
+  for (int i = 0; i < I + 2; ++i) q[i] = 0.05 * (rnd() - 0.5);
+  q += I + 2 + 2 + 2 * (size_t)I + 6 * (size_t)n + I + 2;
+  for (int i = 0; i < I; ++i) q[i] = 1e6 * 0.05 * (rnd() - 0.5);  // closure tally
+  q[I] = 1e6 * 0.01;
+  q[I + 1] = -1e6 * 0.01;
+  h[words - 1] = 2.0;  // factorization not built
+  HWWG_CUDA(cudaMemcpyAsync(c->scratch.p, h.data(), words * 8, cudaMemcpyHostToDevice, s));
+  HWWG_CUDA(cudaMemsetAsync(c->iscratch.p, 0, 8 * sizeof(int), s));
+  double* d = c->scratch.p;
+  LowOrderArgs a{};
+  a.I = I;
+  a.edges = c->prob.view.edges;
+  a.cells = c->prob.view.cells;
+  a.theta = 0.5;
+  a.dt = 0.5;
+  a.eps_min = 1e-3;
+  a.rho = 5.0;
+  a.ma_k = 1;
+  a.mode = 1;
+  a.fast_solve = 1;
+  a.s.phi_prev = d; d += I + 2;
+  a.s.J_prev = d; d += I + 1;
+  a.s.F_prev = d; d += I + 2;
+  a.s.PLPR_prev = d; d += 2;
+  a.s.centers = d; d += I;
+  a.s.phi_hybrid = d; d += I;
+  a.s.sys = d; d += 6 * (size_t)n;
+  a.s.F_now = d; d += I + 2;
+  a.closure_tally = d; d += I;
+  a.bclosure_tally = d; d += 2;
+  a.s.fac = d;
+  a.s.flags = c->iscratch.p;
+  a.snapshot_inv_norm = 1e-6;
+  std::vector<double> r1(2 * (size_t)I), r2(2 * (size_t)I);
+  for (int pass = 0; pass < 2; ++pass) {
+    a.refactor = pass == 0 ? 1 : 0;
+    launch_low_order_update(a, s);
+    std::vector<double>& r = pass == 0 ? r1 : r2;
+    HWWG_CUDA(cudaMemcpyAsync(r.data(), a.s.centers, 2 * (size_t)I * 8, cudaMemcpyDeviceToHost, s));
+    HWWG_CUDA(cudaStreamSynchronize(s));
+  }
+  int fl[8];
+  HWWG_CUDA(cudaMemcpy(fl, c->iscratch.p, sizeof fl, cudaMemcpyDeviceToHost));
+  if (fl[4] != 0) return fail(HWWG_ESINGULAR, "synthetic LOSM solve failed");
+  int diff = 0;
+  double mx = 0.0;
+  for (size_t i = 0; i < r1.size(); ++i) {
+    if (std::memcmp(&r1[i], &r2[i], 8) != 0) {
+      ++diff;
+      mx = std::max(mx, std::fabs(r1[i] - r2[i]));
+    }
+  }
+  *max_abs_diff = mx;
+  return diff;
   HWWG_API_END
 }
 

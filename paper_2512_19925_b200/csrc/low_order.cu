@@ -245,6 +245,229 @@ __device__ int solve_schur_pcr(int I, const double* __restrict__ lo, const doubl
   return __syncthreads_or(bad);
 }
 
+// ---- cached factorization (throughput mode) --------------------------------
+// The LOSM matrix depends on the mesh, the materials, theta and dt only, so the
+// Schur complement and every PCR level's elimination multipliers are computed
+// once (per theta/dt) and each later solve only carries the right-hand side
+// through them: two fmas per row and level, no divisions. The cached values
+// are the ones solve_schur_pcr computes, so results are identical to it.
+constexpr int kFacLevels = 9;  // PCR levels for N = I + 2 <= 512 (one row per thread)
+
+struct FacView {
+  double *tau_b, *remdx_b, *lo_b, *di_b, *up_b;           // balance/boundary rows (N)
+  double *tau_m, *sdx_m, *lo_m, *di_m, *up_m, *inv_m;     // moment rows (I + 1)
+  double *al, *ga;                                        // [kFacLevels][N]
+  double* dfin;                                           // N
+  double* bad;                                            // 1
+};
+
+__host__ __device__ inline size_t fac_words_for(int I) {
+  const size_t N = (size_t)I + 2, E = (size_t)I + 1;
+  return 5 * N + 6 * E + 2 * (size_t)kFacLevels * N + N + 1;
+}
+
+__device__ FacView fac_view(double* f, int I) {
+  const int N = I + 2, E = I + 1;
+  FacView v;
+  v.tau_b = f; f += N;
+  v.remdx_b = f; f += N;
+  v.lo_b = f; f += N;
+  v.di_b = f; f += N;
+  v.up_b = f; f += N;
+  v.tau_m = f; f += E;
+  v.sdx_m = f; f += E;
+  v.lo_m = f; f += E;
+  v.di_m = f; f += E;
+  v.up_m = f; f += E;
+  v.inv_m = f; f += E;
+  v.al = f; f += (size_t)kFacLevels * N;
+  v.ga = f; f += (size_t)kFacLevels * N;
+  v.dfin = f; f += N;
+  v.bad = f;
+  return v;
+}
+
+// Builds the cache (same formulas and operation order as assemble_rows and
+// solve_schur_pcr; the matrix rows come from the assembled system lo/di/up).
+__device__ void build_factorization(int I, const double* edges, const CellInfo* cells,
+                                    double theta, double dt, const double* lo, const double* di,
+                                    const double* up, FacView F, double* sm) {
+  const int N = I + 2, n = 2 * I + 3;
+  double* A = sm;
+  double* D = A + N;
+  double* C = D + N;
+  const int i = threadIdx.x;
+  if (i < N) {
+    // RHS constants of the balance row (losm.cpp:68-139 via assemble_rows)
+    double tau = 0.0, remdx = 0.0;
+    if (i >= 1 && i <= I) {
+      const double dx = ghost_width(edges, I, i);
+      const CellInfo c = cells[i - 1];
+      tau = dx / (c.speed * dt);
+      remdx = removal_of(c) * dx;
+    }
+    F.tau_b[i] = tau;
+    F.remdx_b[i] = remdx;
+    const int m = 2 * i;
+    F.lo_b[i] = lo[m];
+    F.di_b[i] = di[m];
+    F.up_b[i] = up[m];
+    if (i <= I) {  // moment row 2i+1
+      const int mp = m + 1;
+      const double dx_l = ghost_width(edges, I, i);
+      const double dx_r = ghost_width(edges, I, i + 1);
+      const double dx_hat = 0.5 * (dx_r + dx_l);
+      double num_sig = 0.0, num_vel = 0.0;
+      if (dx_l > 0.0) {
+        num_sig += cells[i - 1].sigma_t * dx_l;
+        num_vel += dx_l / cells[i - 1].speed;
+      }
+      if (dx_r > 0.0) {
+        num_sig += cells[i].sigma_t * dx_r;
+        num_vel += dx_r / cells[i].speed;
+      }
+      const double sig_hat = num_sig / (dx_l + dx_r);
+      const double inv_speed_hat = num_vel / (dx_l + dx_r);
+      F.tau_m[i] = dx_hat * inv_speed_hat / dt;
+      F.sdx_m[i] = sig_hat * dx_hat;
+      F.lo_m[i] = lo[mp];
+      F.di_m[i] = di[mp];
+      F.up_m[i] = up[mp];
+      F.inv_m[i] = 1.0 / di[mp];
+    }
+    // Schur complement rows (solve_schur_pcr)
+    double a = 0.0, d = di[m], c = 0.0;
+    if (i > 0) {
+      const int mm = m - 1;
+      const double inv = 1.0 / di[mm];
+      const double q = lo[mm] * inv, s = up[mm] * inv;
+      a = -lo[m] * q;
+      d -= lo[m] * s;
+    }
+    if (i < N - 1) {
+      const int mp = m + 1;
+      const double inv = 1.0 / di[mp];
+      const double q = lo[mp] * inv, s = up[mp] * inv;
+      d -= up[m] * q;
+      c = -up[m] * s;
+    }
+    A[i] = a;
+    D[i] = d;
+    C[i] = c;
+  }
+  (void)n;
+  __syncthreads();
+  int l = 0;
+  for (int s = 1; s < N; s <<= 1, ++l) {
+    double na = 0.0, nd = 0.0, nc = 0.0;
+    if (i < N) {
+      double a = 0.0, d = D[i], c = 0.0, al = 0.0, ga = 0.0;
+      if (i - s >= 0) {
+        al = -A[i] / D[i - s];
+        a = al * A[i - s];
+        d += al * C[i - s];
+      }
+      if (i + s < N) {
+        ga = -C[i] / D[i + s];
+        c = ga * C[i + s];
+        d += ga * A[i + s];
+      }
+      F.al[(size_t)l * N + i] = al;
+      F.ga[(size_t)l * N + i] = ga;
+      na = a;
+      nd = d;
+      nc = c;
+    }
+    __syncthreads();
+    if (i < N) {
+      A[i] = na;
+      D[i] = nd;
+      C[i] = nc;
+    }
+    __syncthreads();
+  }
+  int bad = 0;
+  if (i < N) {
+    F.dfin[i] = D[i];
+    if (D[i] == 0.0 || !isfinite(D[i])) bad = 1;
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) *F.bad = bad ? 1.0 : 0.0;
+  __syncthreads();
+}
+
+// One solve through the cached factorization: RHS of assemble_rows (q = 0,
+// J_L = J_R = 0, as the driver calls it), the Schur RHS, the PCR levels, phi
+// and the currents into x (interleaved like the full system). Returns nonzero
+// when the factorization is singular.
+__device__ int solve_cached(int I, FacView F, const double* phi_prev, const double* J_prev,
+                            const double* Fs, double PLs, double PRs, const double* F_prev,
+                            double theta, double* x, double* sm) {
+  const int N = I + 2;
+  double* P = sm;       // N: moment-row RHS * inv diagonal
+  double* R0 = P + N;   // N
+  double* R1 = R0 + N;  // N
+  double* RM = R1 + N;  // N: moment-row RHS
+  const int i = threadIdx.x;
+  double al[kFacLevels], ga[kFacLevels];
+#pragma unroll
+  for (int l = 0; l < kFacLevels; ++l) {
+    al[l] = i < N ? F.al[(size_t)l * N + i] : 0.0;
+    ga[l] = i < N ? F.ga[(size_t)l * N + i] : 0.0;
+  }
+  double rb = 0.0;
+  if (i < N) {
+    const double qi = 0.0;
+    if (i == 0) rb = 2.0 * 0.0 + PLs;
+    else if (i == N - 1) rb = 2.0 * 0.0 - PRs;
+    else
+      rb = F.tau_b[i] * phi_prev[i] + theta * qi +
+           (theta - 1.0) * (J_prev[i] - J_prev[i - 1] + F.remdx_b[i] * phi_prev[i] - qi);
+    if (i <= I) {
+      const double rm = F.tau_m[i] * J_prev[i] + theta * (Fs[i + 1] - Fs[i]) +
+                        (theta - 1.0) * ((phi_prev[i + 1] - phi_prev[i]) / 3.0 +
+                                         F.sdx_m[i] * J_prev[i] - (F_prev[i + 1] - F_prev[i]));
+      RM[i] = rm;
+      P[i] = rm * F.inv_m[i];
+    }
+  }
+  __syncthreads();
+  if (i < N) {
+    double r = rb;
+    if (i > 0) r -= F.lo_b[i] * P[i - 1];
+    if (i < N - 1) r -= F.up_b[i] * P[i];
+    R0[i] = r;
+  }
+  __syncthreads();
+  double* Rc = R0;
+  double* Rn = R1;
+  int l = 0;
+#pragma unroll
+  for (int lv = 0; lv < kFacLevels; ++lv) {
+    const int s = 1 << lv;
+    if (s >= N) break;
+    if (i < N) {
+      double r = Rc[i];
+      if (i - s >= 0) r += al[lv] * Rc[i - s];
+      if (i + s < N) r += ga[lv] * Rc[i + s];
+      Rn[i] = r;
+    }
+    __syncthreads();
+    double* t = Rc;
+    Rc = Rn;
+    Rn = t;
+    ++l;
+  }
+  if (i < N) x[2 * i] = Rc[i] / F.dfin[i];
+  __syncthreads();
+  if (i <= I) {
+    const int mp = 2 * i + 1;
+    x[mp] = (RM[i] - F.lo_m[i] * x[2 * i] - F.up_m[i] * x[2 * i + 2]) / F.di_m[i];
+  }
+  __syncthreads();
+  return *F.bad != 0.0;
+}
+
 // Block max of per-thread partial maxima. The partials start at 0.0 and only
 // grow through '>' (ww.cpp:13-15), so NaN never enters and max is exact.
 __device__ double block_max(double v, double* red) {
@@ -344,11 +567,34 @@ __device__ __noinline__ void solve_and_center(const LowOrderArgs& a, const doubl
   const bool ok_in = all_finite(s.phi_prev, I + 2) && all_finite(s.J_prev, I + 1) &&
                      all_finite(s.F_prev, I + 2);
   LP(4);
-  if (ok_in) {
+  const bool cached = a.fast_solve && s.fac != nullptr && I + 2 <= (int)blockDim.x &&
+                      I + 2 <= (1 << kFacLevels);
+  // factorization state word: 0 ok, 1 singular, 2 not built for the current
+  // (theta, dt) — a refactor request invalidates first, so a solve skipped on
+  // bad inputs leaves the cache marked unbuilt rather than stale
+  bool rebuild = false;
+  if (cached) {
+    const FacView F = fac_view(s.fac, I);
+    if (a.refactor && threadIdx.x == 0) *F.bad = 2.0;
+    __syncthreads();
+    rebuild = *F.bad == 2.0;
+    __syncthreads();
+  }
+  if (ok_in && cached && !rebuild) {
+    extern __shared__ double dyn[];
+    const int bad = solve_cached(I, fac_view(s.fac, I), s.phi_prev, s.J_prev, Fs, PLs, PRs,
+                                 s.F_prev, a.theta, x, dyn);
+    LP(6);
+    if (threadIdx.x == 0) status = bad ? 2 : 0;
+  } else if (ok_in) {
     assemble_rows(I, a.edges, a.cells, s.phi_prev, s.J_prev, 0.0, 0.0, Fs, PLs, PRs, s.F_prev,
                   a.theta, a.dt, nullptr, lo, di, up, rh);
     __syncthreads();
     LP(5);
+    if (cached) {  // (re)build: record the factorization, then solve as before
+      extern __shared__ double dyn[];
+      build_factorization(I, a.edges, a.cells, a.theta, a.dt, lo, di, up, fac_view(s.fac, I), dyn);
+    }
     if (a.fast_solve) {
       extern __shared__ double dyn[];
       const int bad = solve_schur_pcr(I, lo, di, up, rh, x, dyn);
@@ -706,6 +952,8 @@ __global__ void k_device_log(const double* x, uint64_t n, double* out) {
 }
 
 }  // namespace
+
+size_t lo_fac_words(int I) { return I + 2 <= 512 ? fac_words_for(I) : 0; }
 
 void launch_low_order_update(const LowOrderArgs& a_in, cudaStream_t st) {
   LowOrderArgs a = a_in;

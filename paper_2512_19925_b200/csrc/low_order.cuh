@@ -30,7 +30,13 @@ struct LowOrderState {
   // scratch for the n = 2I+3 system (lower, diag, upper, rhs, fill, x) and F_now
   double* sys;   // 6 * (2I+3)
   double* F_now; // I+2
+  // throughput mode: the Schur + PCR factorization of the LOSM matrix, which
+  // depends only on mesh, materials, theta and dt (lo_fac_words(I) doubles;
+  // null = refactor every solve)
+  double* fac;
 };
+// doubles of LowOrderState::fac for I cells (0 when the cached path does not apply)
+size_t lo_fac_words(int I);
 
 struct LowOrderArgs {
   int I;
@@ -46,6 +52,7 @@ struct LowOrderArgs {
   //         partial snapshot of the live tallies.
   int mode;
   int fast_solve;  // throughput mode: Schur complement + parallel cyclic reduction
+  int refactor;    // fast_solve with s.fac: 1 = (re)build the cached factorization
   int analytic;        // mode 0: step 1 cold start
   int pulse_cell;      // analytic: cell of the source point
   double pulse_value;  // analytic: speed * strength / dx

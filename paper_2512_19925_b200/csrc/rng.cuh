@@ -93,6 +93,15 @@ HWWG_HD U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 }
 
 // Two uniforms in (0,1) from one Philox block (53 bits each).
+// One event's deviates from one Philox block: a 53-bit uniform (flight
+// distance) and two 32-bit uniforms (collision type / roulette, scattering).
+HWWG_HD void philox_uniform3(U4 r, double& a, double& b, double& c) {
+  const uint64_t ua = ((uint64_t)r.x << 32 | r.y) >> 11;
+  a = ((double)ua + 0.5) * 0x1.0p-53;
+  b = ((double)r.z + 0.5) * 0x1.0p-32;
+  c = ((double)r.w + 0.5) * 0x1.0p-32;
+}
+
 HWWG_HD void philox_uniform2(U4 r, double& a, double& b) {
   const uint64_t ua = ((uint64_t)r.x << 32 | r.y) >> 11;
   const uint64_t ub = ((uint64_t)r.z << 32 | r.w) >> 11;

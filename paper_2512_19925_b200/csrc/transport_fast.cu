@@ -61,10 +61,22 @@ struct Lane {
   bool alive;
 };
 
-__device__ __forceinline__ void draw2(const FastArgs& a, Lane& p, double& u0, double& u1) {
+// One Philox4x32-10 block per event: flight, collision type and scattering
+// deviates (the roulette deviate after a scatter is the collision-type one
+// recycled: given u1 < sigma_s/sigma_t, u1 * sigma_t / sigma_s is uniform and
+// independent of that decision).
+__device__ __forceinline__ void draw3(const FastArgs& a, Lane& p, double& u0, double& u1,
+                                      double& u2) {
   const U4 c{p.hist, (unsigned)p.key, (unsigned)(p.key >> 32), (a.step << 16) | (p.ctr & 0xffffu)};
   ++p.ctr;
-  philox_uniform2(philox4x32_10(c, a.k0, a.k1), u0, u1);
+  philox_uniform3(philox4x32_10(c, a.k0, a.k1), u0, u1, u2);
+}
+
+// tally.hpp:130-134 batch_of, by one fp64 division: exact while h * B < 2^53
+// (then floor of the correctly rounded quotient is the integer quotient)
+__device__ __forceinline__ int batch_fast(unsigned h, double H, int B) {
+  const int b = (int)(((double)h * (double)B) / H);
+  return b < B ? b : B - 1;
 }
 
 __device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigned j) {
@@ -209,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   unsigned pend = 0;  // daughters pending in the local stack (warp-uniform)
   bool src_done = false;
   const int I = a.mesh.I;
+  const double Hd = (double)a.H;
   const double* __restrict__ edges = a.mesh.edges;
   const CellInfo* __restrict__ cells = a.mesh.cells;
   const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
@@ -326,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       const unsigned rank = __popc(need & lt);
       if (!p.alive && rank < take) {
         load_rec(p, r, r.base + cnt - rank);
-        p.bslot = batch_of(p.hist, a.H, a.B) - (shf ? a.b_lo : 0);
+        p.bslot = batch_fast(p.hist, Hd, a.B) - (shf ? a.b_lo : 0);
       }
       __syncwarp();
       if (lane == 0) r.count = cnt - take;
@@ -380,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           p.hist = m.y;
           p.key = ((unsigned long long)m.w << 32) | m.z;
           p.inv_mu = 1.0 / p.mu;
-          p.bslot = batch_of(p.hist, a.H, a.B) - (shf ? a.b_lo : 0);
+          p.bslot = batch_fast(p.hist, Hd, a.B) - (shf ? a.b_lo : 0);
           p.alive = p.w > 0.0;
         }
       }
@@ -466,8 +479,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         if (!kUniform) return edges[e];
         return e == I ? a.x_max : __dadd_rn(a.x_min, __dmul_rn((double)e, a.w_gen));
       };
-      double u0, u1;
-      draw2(a, p, u0, u1);
+      double u0, u1, u2;
+      draw3(a, p, u0, u1, u2);
       const double d_census = ci.speed * (a.t_end - p.t);
       const double d_coll = -log(u0) * ci.inv_sigma_t;
       double d_b = __longlong_as_double(0x7ff0000000000000LL);
@@ -527,11 +540,9 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         ++n_coll;
         const double xi = u1 * ci.sigma_t;
         if (xi < ci.sigma_s) {
-          double v0, v1;
-          draw2(a, p, v0, v1);
-          p.mu = 2.0 * v0 - 1.0;
+          p.mu = 2.0 * u2 - 1.0;
           p.inv_mu = 1.0 / p.mu;
-          u1 = v1;  // roulette deviate for the window game below
+          u1 = xi / ci.sigma_s;  // recycled roulette deviate for the window game below
           window_site = true;
         } else {
           // capture (fission is rejected for this mode at driver creation: the

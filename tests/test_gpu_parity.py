@@ -202,3 +202,18 @@ def test_component_known_answers(engine):
     assert out.size == 4 and np.allclose(out["w"], 0.25) and abs(ow - 1.0) < 1e-15
     with pytest.raises(ValueError):
         engine.uniform_comb(np.zeros(0, PARTICLE_DT), 10, 1, 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("I,seed", [(400, 1), (37, 2), (510, 3)])
+def test_losm_cached_factorization_is_identical(engine, I, seed):
+    """Throughput mode solves the window update through a cached Schur/PCR
+    factorization; it must reproduce the rebuilt factorization bit for bit."""
+    import ctypes as C
+    from paper_2512_19925_b200 import _capi as A
+    f = A.lib().hwwg_internal_losm_cache_check
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int32, C.c_uint32, C.POINTER(C.c_double)]
+    mx = C.c_double(0.0)
+    rc = f(engine._h, I, seed, C.byref(mx))
+    assert rc == 0, (rc, mx.value)
