@@ -118,6 +118,7 @@ struct hwwg_driver {
   DevBuf<unsigned long long> pool_ctl;
   int smem_mode = 1;  // fast tallies (FastArgs::smem_tallies) outside the cold start
   int scramble = 1;   // FastArgs::scramble outside the cold start
+  int agg_all = 0;    // HWWG_FAST_AGG=1: warp-aggregated tallies in every step
   int flush_replicas = 0;  // FastArgs::flush_replicas (HWWG_FAST_FLUSH_R; 0 = direct REDs, measured best)
   DevBuf<double> flush_scratch;
   bool timeline_on = false;
@@ -313,7 +314,7 @@ void init_driver(hwwg_driver* d) {
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
     const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
     d->max_warps = warps;
-    d->warp_cursor.reserve(2 * (size_t)warps);
+    d->warp_cursor.reserve((size_t)kWarpCursorWords * warps);
     d->stacks.reserve((size_t)warps * d->stack_cap);
     d->src_head.reserve(1);
     d->pool_recs.reserve(1u << 20);  // 64 MB of donated split records per segment
@@ -715,7 +716,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.b_lo = b_lo;
         fa.nb = b_hi - b_lo + 1;
         // the first step starts from a point pulse: most lanes share a few cells
-        fa.aggregate = step == 1 ? 1 : 0;
+        fa.aggregate = (step == 1 || d->agg_all) ? 1 : 0;
         size_t smem = fast_smem_bytes(I, fa.nb);
         fa.smem_tallies = smem <= 96 * 1024 ? 1 : 0;
         if (!fa.aggregate && d->smem_mode != 1) {
@@ -831,6 +832,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->stage.ensure(count + count / 4 + 4096);
   }
   if (d->timeline_on) print_timeline(d, (int)thr.size() + 1, step);
+  unsigned long long fp[8];
+  if (d->timeline_on && fast_prof_read(fp) && fp[5]) {
+    const double t = (double)fp[5];
+    std::fprintf(stderr,
+                 "[fprof] step %d: %llu trips, cycles/trip refill %.0f event %.0f census %.0f "
+                 "tally %.0f split %.0f | tail trips %llu (%.0f cycles each)\n",
+                 step, fp[5], fp[0] / t, fp[1] / t, fp[2] / t, fp[3] / t, fp[4] / t, fp[6],
+                 fp[6] ? (double)fp[7] / (double)fp[6] : 0.0);
+  }
   if (d->phases_on) {  // the stream is synchronised here
     std::string line = "[phases] step " + std::to_string(step) + ":";
     for (size_t k = 0; k + 1 < d->ph_n; ++k) {
@@ -1010,6 +1020,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   d->losm_cache = std::getenv("HWWG_LOSM_NOCACHE") == nullptr;
   if (const char* m = std::getenv("HWWG_FAST_SMEM")) d->smem_mode = std::atoi(m) % 3;
   if (const char* m = std::getenv("HWWG_FAST_SCRAMBLE")) d->scramble = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_FAST_AGG")) d->agg_all = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
   d->world = d->opt.world > 1 ? d->opt.world : 1;
   d->rank = d->world > 1 ? d->opt.rank : 0;

@@ -80,6 +80,9 @@ void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
 
 int fast_blocks_per_sm(size_t smem);
 int fast_threads_per_block();
+// per-warp census cursor words (FastArgs::warp_cursor: next, end)
+constexpr int kWarpCursorWords = 2;
+int fast_prof_read(unsigned long long out[8]);  // -DHWWG_FAST_PROF builds
 size_t fast_smem_bytes(int I, int nb);
 size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);

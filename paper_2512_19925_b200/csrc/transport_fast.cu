@@ -40,6 +40,25 @@ namespace {
 #define HWWG_FAST_MINB (24 / HWWG_FAST_WARPS)  // resident blocks per SM (register budget)
 #endif
 constexpr int kWarpsPerBlock = HWWG_FAST_WARPS;
+
+// -DHWWG_FAST_PROF: per-phase clock64 accounting of the loop (lane 0 of every
+// warp), summed over the grid into g_fprof: [0] refill [1] event [2] census
+// [3] tally [4] split [5] trips [6] tail trips (<= 4 live lanes) [7] tail cycles
+#ifdef HWWG_FAST_PROF
+__device__ unsigned long long g_fprof[8];
+#define FPROF_DECL unsigned long long fp_t = clock64(), fp_c[8] = {0, 0, 0, 0, 0, 0, 0, 0}, fp_trip = 0;
+#define FPROF(k)                          \
+  do {                                    \
+    const unsigned long long t_ = clock64(); \
+    fp_c[k] += t_ - fp_t;                 \
+    fp_t = t_;                            \
+  } while (0)
+#else
+#define FPROF_DECL
+#define FPROF(k) \
+  do {           \
+  } while (0)
+#endif
 constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kDonate = 256;  // pending local daughters above which splits go global
 constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
@@ -265,7 +284,12 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   bool r_pend = false;
   unsigned long long ticket = ~0ULL;  // lane 0: pool slot this warp waits on
 
+  FPROF_DECL
   while (true) {
+#ifdef HWWG_FAST_PROF
+    fp_trip = clock64();
+    fp_t = fp_trip;
+#endif
     // ---- refill idle lanes: local split stack, then source bank, then pool
     // Work sharing. A backlog on this warp's stack while other warps sit idle
     // is the tail of a heavy split tree: one split of thousands of daughters,
@@ -466,6 +490,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     if (!any_alive) continue;
     if (p.alive) ++n_ev;
     ++n_iter;
+    FPROF(0);
+#ifdef HWWG_FAST_PROF
+    const bool fp_tail = __popc(~need) <= 4;
+#endif
 
     // ---- one event per live lane; tally contributions are collected per lane
     // and committed warp-aggregated after the event (see agg_add)
@@ -573,6 +601,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         }
       }
     }
+    FPROF(1);
     // ---- look-ahead source claim: the reservation is spent and lanes will need
     // particles; the atomic's latency hides behind the census and tally work
     if (r_lo == r_hi && !r_pend && !src_done) {
@@ -614,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       }
     }
 
+    FPROF(2);
     // ---- commit the event's tallies, warp-aggregated (lanes sharing a cell
     // are summed with shuffles first: one CAS per distinct address, not per lane)
     if (a.aggregate) {  // cold-start segments: most lanes share a few cells
@@ -650,6 +680,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (edge_key >= 0) atomicAdd(edg + edge_key, edge_v);
     }
 
+    FPROF(3);
     // ---- push split records: local stack while shallow, else donate to the pool
     const unsigned smask = __ballot_sync(0xffffffffu, split_n > 1);
     if (smask) {
@@ -699,7 +730,19 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (sp > a.stack_cap) sp = a.stack_cap;
       __syncwarp();
     }
+    FPROF(4);
+#ifdef HWWG_FAST_PROF
+    fp_c[5] += 1;
+    if (fp_tail) {
+      fp_c[6] += 1;
+      fp_c[7] += clock64() - fp_trip;
+    }
+#endif
   }
+#ifdef HWWG_FAST_PROF
+  if (lane == 0)
+    for (int k = 0; k < 8; ++k) atomicAdd(&g_fprof[k], fp_c[k]);
+#endif
 
   if (lane == 0) {
     a.warp_cursor[2 * gwarp] = wcur;
@@ -838,6 +881,19 @@ size_t fast_smem_count_bytes(int I) { return (size_t)(I + 1) / 2 * 8 + 16; }
 size_t fast_flush_stride(int I, int B) { return (size_t)(B + 4) * I + 1 + B + 2 + I; }
 
 int fast_threads_per_block() { return kThreads; }
+
+// -DHWWG_FAST_PROF builds: read and clear the loop phase accounting (0 otherwise)
+int fast_prof_read(unsigned long long out[8]) {
+#ifdef HWWG_FAST_PROF
+  HWWG_CUDA(cudaMemcpyFromSymbol(out, g_fprof, 8 * sizeof(unsigned long long)));
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  HWWG_CUDA(cudaMemcpyToSymbol(g_fprof, z, sizeof z));
+  return 1;
+#else
+  (void)out;
+  return 0;
+#endif
+}
 
 void configure_fast_kernel();
 
