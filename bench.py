@@ -18,8 +18,11 @@ CUDA-event window.
 value = sum(segments) / sum(step device time); a segment is one increment of
 tracks_per_cell (proj/src/transport.cpp:136-139).  e2e = the same metric with
 the bank round-tripping through pinned host memory every step (hwwg_driver with
-host_bank = 1: H2D of the step's input bank, D2H of its census and record),
-timed on the host clock.
+host_bank = 1: H2D of the step's source bank, D2H of the next step's source and
+of the record), timed on the host clock.  In Philox mode the device combs the
+census before handing it to the host (the comb that opens the next step, with
+that step's stream), so the host holds H particles between steps, not the
+raw census.
 
 --impl reference: the unmodified reference (oracle/_ref/libhww_ref.so, built
 from /root/reference/proj) running hww::run_step on this box's CPU cores with

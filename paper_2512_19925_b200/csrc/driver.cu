@@ -119,6 +119,9 @@ struct hwwg_driver {
   int smem_mode = 1;  // fast tallies (FastArgs::smem_tallies) outside the cold start
   int scramble = 1;   // FastArgs::scramble outside the cold start
   int agg_all = 0;    // HWWG_FAST_AGG=1: warp-aggregated tallies in every step
+  // e2e (host_bank) Philox runs: the bank in host memory is already combed
+  bool host_pre_combed = false;
+  uint64_t pre_comb_in = 0;
   int flush_replicas = 0;  // FastArgs::flush_replicas (HWWG_FAST_FLUSH_R; 0 = direct REDs, measured best)
   DevBuf<double> flush_scratch;
   bool timeline_on = false;
@@ -465,8 +468,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->bank_n = d->host_bank_n;
     rec->h2d_bytes += d->host_bank_n * sizeof(hwwg_particle);
     if (d->fast) {
-      d->fbank.reserve(d->bank_n);
-      launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), 0, s);
+      // a pre-combed bank (see the step end) is already the step's source
+      FastBankBuf& dst = d->host_pre_combed ? d->fsrc : d->fbank;
+      dst.reserve(d->bank_n);
+      launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, dst.view(), 0, s);
       ++d->launches;
     }
   }
@@ -480,6 +485,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     multi_gpu_comb(d, step, s);
     H = d->target;
     rec->comb_in = d->bank_n;  // this rank's census slots
+    rec->comb_out = d->target;
+  } else if (d->fast && c.host_bank && d->host_pre_combed) {
+    H = d->target;  // combed on the device at the end of the previous step
+    rec->comb_in = d->pre_comb_in;
     rec->comb_out = d->target;
   } else if (d->fast) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
@@ -874,7 +883,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // ---- census -> next bank in reference order
   if (d->fast) {
     d->fbank.swap(d->fcensus);  // the census is the next comb's input, already SoA
-    if (c.host_bank) {  // real particles only, AoS, for the host round trip
+    if (c.host_bank && d->world > 1) {  // real particles only, AoS, for the host round trip
       d->bank.reserve(std::max<unsigned long long>(count, 1));
       launch_fast_compact_aos(d->fbank.view(), count, d->bank.p, d->counter.p, s);
       HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
@@ -900,7 +909,37 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   d->h_hybrid.resize(I);
   HWWG_CUDA(cudaMemcpyAsync(d->h_centers.data(), d->lo.centers, I * 8, cudaMemcpyDeviceToHost, s));
   HWWG_CUDA(cudaMemcpyAsync(d->h_hybrid.data(), d->lo.phi_hybrid, I * 8, cudaMemcpyDeviceToHost, s));
-  if (c.host_bank) {
+  d->host_pre_combed = false;
+  if (c.host_bank && d->fast && d->world == 1) {
+    // e2e host round trip: comb the census now, with the NEXT step's stream
+    // (the comb that would open it), and hand the host the combed source —
+    // target particles instead of the raw census (x60 of H after step 1).
+    // Enqueued after the record readbacks above, so they see this step's
+    // comb scalars.
+    const size_t tb = fast_comb_temp_bytes(d->bank_n);
+    FastCombArgs a{};
+    a.bank = d->fbank.view();
+    a.n = d->bank_n;
+    a.target = d->target;
+    a.seed = c.seed;
+    a.stream = stream_id_host(step + 1, 0, 3);
+    a.prefix = d->comb_mem.p + 4;
+    a.scalars = d->comb_mem.p;
+    a.out = d->fsrc.view();
+    a.temp = d->comb_temp.p;
+    a.temp_bytes = tb;
+    if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
+    launch_fast_comb(a, s);
+    launch_fast_to_aos(d->fsrc.view(), d->target, d->bank.p, s);
+    d->launches += 4;
+    d->pre_comb_in = d->bank_n;
+    d->host_pre_combed = true;
+    d->host_bank_n = d->target;
+    d->bank_n = d->target;
+    rec->d2h_bytes += d->target * sizeof(hwwg_particle);
+    HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, d->target * sizeof(hwwg_particle),
+                              cudaMemcpyDeviceToHost, s));
+  } else if (c.host_bank) {
     if (count > d->host_bank_cap) {
       HWWG_CUDA(cudaStreamSynchronize(s));
       if (d->host_bank) HWWG_CUDA(cudaFreeHost(d->host_bank));
@@ -1101,9 +1140,20 @@ int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma, dou
 int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t* n) {
   HWWG_API_BEGIN
   if (!d || !n) return fail(HWWG_EINVAL, "NULL argument");
-  *n = d->bank_n;
-  if (!out || cap < d->bank_n) return fail(HWWG_ENOSPC, "bank buffer too small");
-  HWWG_CUDA(cudaMemcpyAsync(out, d->bank.p, d->bank_n * sizeof(hwwg_particle), cudaMemcpyDeviceToHost,
+  uint64_t count = d->bank_n;
+  if (d->fast && !d->cfg.host_bank && d->next_step > 1) {
+    // Philox mode keeps the census as SoA with zero-weight chunk tails: compact
+    // the real particles into AoS (order is free in this mode)
+    d->bank.reserve(std::max<uint64_t>(d->bank_n, 1));
+    launch_fast_compact_aos(d->fbank.view(), d->bank_n, d->bank.p, d->counter.p, d->stream);
+    unsigned long long c = 0;
+    HWWG_CUDA(cudaMemcpyAsync(&c, d->counter.p, sizeof c, cudaMemcpyDeviceToHost, d->stream));
+    HWWG_CUDA(cudaStreamSynchronize(d->stream));
+    count = c;
+  }
+  *n = count;
+  if (!out || cap < count) return fail(HWWG_ENOSPC, "bank buffer too small");
+  HWWG_CUDA(cudaMemcpyAsync(out, d->bank.p, count * sizeof(hwwg_particle), cudaMemcpyDeviceToHost,
                             d->stream));
   HWWG_CUDA(cudaStreamSynchronize(d->stream));
   return HWWG_OK;

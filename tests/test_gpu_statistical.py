@@ -79,3 +79,32 @@ def test_philox_run_is_conservative():
     total = rec.census_weight * 100_000 + rec.counters.leakage_weight
     assert abs(total / 100_000 - 1.0) < 5 * rec.census_weight_sigma + 1e-3
     assert rec.census_size == rec.counters.census_count
+
+
+def test_philox_bank_and_host_round_trip():
+    """The census bank a Philox driver hands out (compacted real particles) and
+    the e2e host_bank mode, which combs on the device before the host round
+    trip: same bookkeeping, and results within statistics of the device run."""
+    H, steps = 100_000, 4
+    c = cfg(2, H, steps, 9)
+    d = hw.Driver(c, rng_mode=hw.RNG_PHILOX)
+    recs = [d.step() for _ in range(steps)]
+    bank = d.bank()
+    d.close()
+    last = recs[-1]
+    assert len(bank) == last.counters.census_count
+    assert np.all(bank["w"] > 0)
+    np.testing.assert_allclose(bank["w"].sum(), last.census_weight * H, rtol=1e-9)
+
+    c.host_bank = True
+    e = hw.Driver(c, rng_mode=hw.RNG_PHILOX)
+    erecs = [e.step() for _ in range(steps)]
+    e.close()
+    for k in range(1, steps):  # steps 2.. open with the device-side pre-comb
+        assert erecs[k].comb_out == H
+        assert erecs[k].comb_in >= erecs[k - 1].counters.census_count
+        assert erecs[k].h2d_bytes == H * 32
+        np.testing.assert_allclose(erecs[k].comb_out_weight, erecs[k].comb_in_weight, rtol=1e-12)
+    for r, q in zip(recs, erecs):
+        assert abs(q.segments / r.segments - 1) < 0.02
+        assert abs(q.census_weight / r.census_weight - 1) < 0.02
