@@ -322,7 +322,7 @@ void init_driver(hwwg_driver* d) {
     d->src_head.reserve(1);
     d->pool_recs.reserve(1u << 20);  // 64 MB of donated split records per segment
     HWWG_CUDA(cudaMemsetAsync(d->pool_recs.p, 0, d->pool_recs.n * sizeof(FastStackRec), d->stream));
-    d->pool_ctl.reserve(4);
+    d->pool_ctl.reserve(8);  // [0..3] pool control, [4] segment start (diagnostics)
     if (d->flush_replicas) {
       const size_t words = (size_t)d->flush_replicas * fast_flush_stride(I, d->B);
       d->flush_scratch.reserve(words);
@@ -733,10 +733,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           smem = d->smem_mode == 2 ? fast_smem_count_bytes(I) : 0;
         }
         if (!fa.smem_tallies) smem = 0;
+        smem += fast_smem_centers_bytes(I);
         fa.scramble = fa.aggregate ? 0 : d->scramble;
         const int blocks = d->sms * fast_blocks_per_sm(smem);
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
         fa.warp_cursor = d->warp_cursor.p;
+        fa.seg = nseg;
         fa.flush_scratch = d->flush_scratch.p;
         fa.flush_stride = fast_flush_stride(I, B);
         fa.flush_replicas = d->flush_replicas;
@@ -841,14 +843,49 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->stage.ensure(count + count / 4 + 4096);
   }
   if (d->timeline_on) print_timeline(d, (int)thr.size() + 1, step);
-  unsigned long long fp[8];
-  if (d->timeline_on && fast_prof_read(fp) && fp[5]) {
+  unsigned long long fp[12];
+  std::vector<unsigned> fh(kFastHistWords);
+  if (d->timeline_on && fast_prof_read(fp, fh.data()) && fp[5]) {
+    for (int sg = 0; sg < 8; ++sg) {  // trips / live lanes per 5 us bin
+      const unsigned* h = fh.data() + (size_t)sg * 240;
+      unsigned peak = 0;
+      int last = -1;
+      for (int b = 0; b < 120; ++b) {
+        peak = std::max(peak, h[2 * b]);
+        if (h[2 * b]) last = b;
+      }
+      if (last < 0) continue;
+      int t50 = 0;
+      for (int b = 0; b <= last; ++b)
+        if (h[2 * b] * 2 >= peak) t50 = b;
+      double tr_a = 0, ln_a = 0, tr_b = 0, ln_b = 0;
+      for (int b = 0; b <= last; ++b) {
+        (b <= t50 ? tr_a : tr_b) += h[2 * b];
+        (b <= t50 ? ln_a : ln_b) += h[2 * b + 1];
+      }
+      std::string prof = "";
+      for (int b = 0; b <= last; b += std::max(1, (last + 1) / 16)) {
+        char bb[24];
+        std::snprintf(bb, sizeof bb, " %u", h[2 * b]);
+        prof += bb;
+      }
+      std::fprintf(stderr,
+                   "[fhist] step %d seg %d: busy to %d us (peak %u trips/5us), end %d us; lanes/trip "
+                   "%.1f before, %.1f after; trips before %.0f after %.0f; profile%s\n",
+                   step, sg, 5 * (t50 + 1), peak, 5 * (last + 1), tr_a ? ln_a / tr_a : 0.0,
+                   tr_b ? ln_b / tr_b : 0.0, tr_a, tr_b, prof.c_str());
+    }
     const double t = (double)fp[5];
+    const double busy =
+        (double)(fp[0] + fp[1] + fp[2] + fp[3] + fp[4] + fp[8] + fp[9] + fp[10]);
     std::fprintf(stderr,
-                 "[fprof] step %d: %llu trips, cycles/trip refill %.0f event %.0f census %.0f "
-                 "tally %.0f split %.0f | tail trips %llu (%.0f cycles each)\n",
-                 step, fp[5], fp[0] / t, fp[1] / t, fp[2] / t, fp[3] / t, fp[4] / t, fp[6],
-                 fp[6] ? (double)fp[7] / (double)fp[6] : 0.0);
+                 "[fprof] step %d: %llu trips, cycles/trip share %.0f stack %.0f source %.0f "
+                 "check %.0f event %.0f census %.0f tally %.0f split %.0f | warp lifetime: in "
+                 "trips %.1f%%, waiting on the pool %.1f%%, other %.1f%%\n",
+                 step, fp[5], fp[8] / t, fp[9] / t, fp[10] / t, fp[0] / t, fp[1] / t, fp[2] / t,
+                 fp[3] / t, fp[4] / t,
+                 100.0 * busy / (double)fp[7], 100.0 * (double)fp[6] / (double)fp[7],
+                 100.0 * (1.0 - (busy + (double)fp[6]) / (double)fp[7]));
   }
   if (d->phases_on) {  // the stream is synchronised here
     std::string line = "[phases] step " + std::to_string(step) + ":";

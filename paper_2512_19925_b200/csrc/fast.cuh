@@ -60,6 +60,7 @@ struct FastArgs {
   int stack_cap;
   FastPool pool;
   DevError* err;
+  int seg;  // segment index within the step (diagnostics)
   unsigned long long* timeline;  // optional per-warp {t0, loop trips, t_exit, events}
   unsigned long long* warp_cursor;  // per warp {next, end} of its census chunk (zeroed per step)
   // shared-memory tallies flush into flush_replicas zeroed global replicas
@@ -82,9 +83,13 @@ int fast_blocks_per_sm(size_t smem);
 int fast_threads_per_block();
 // per-warp census cursor words (FastArgs::warp_cursor: next, end)
 constexpr int kWarpCursorWords = 2;
-int fast_prof_read(unsigned long long out[8]);  // -DHWWG_FAST_PROF builds
+// -DHWWG_FAST_PROF builds: loop phase sums; hist (optional, 8 x 120 x 2
+// unsigned): trips and live lanes per 5 us bin of each segment
+int fast_prof_read(unsigned long long out[12], unsigned* hist);
+constexpr int kFastHistWords = 8 * 120 * 2;
 size_t fast_smem_bytes(int I, int nb);
 size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
+size_t fast_smem_centers_bytes(int I);  // window centres (after the tallies)
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);
 void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
                         uint64_t hist0, cudaStream_t s);

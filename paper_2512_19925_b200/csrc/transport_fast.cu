@@ -25,6 +25,8 @@
 // range (track-length by batch and cell, census phi/J/F, edge currents,
 // per-cell track counts), flushed once per block with fp64 REDs; global REDs
 // when the histograms do not fit in shared memory (I = 4000).
+#include <vector>
+
 #include "common.cuh"
 #include "fast.cuh"
 #include "rng.cuh"
@@ -43,10 +45,16 @@ constexpr int kWarpsPerBlock = HWWG_FAST_WARPS;
 
 // -DHWWG_FAST_PROF: per-phase clock64 accounting of the loop (lane 0 of every
 // warp), summed over the grid into g_fprof: [0] refill [1] event [2] census
-// [3] tally [4] split [5] trips [6] tail trips (<= 4 live lanes) [7] tail cycles
+// [3] tally [4] split [5] trips [6] idle cycles (waiting on the pool)
+// [7] warp lifetime cycles
 #ifdef HWWG_FAST_PROF
-__device__ unsigned long long g_fprof[8];
-#define FPROF_DECL unsigned long long fp_t = clock64(), fp_c[8] = {0, 0, 0, 0, 0, 0, 0, 0}, fp_trip = 0;
+__device__ unsigned long long g_fprof[12];
+// trips and live lanes per 5 us bin since the segment's reset, per segment (<= 8)
+constexpr int kHistBins = 120;
+__device__ unsigned int g_fhist[8][kHistBins][2];
+#define FPROF_DECL                                                                   \
+  unsigned long long fp_t = clock64(), fp_c[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, fp_trip = 0, \
+                     fp_k0 = fp_t;
 #define FPROF(k)                          \
   do {                                    \
     const unsigned long long t_ = clock64(); \
@@ -60,10 +68,24 @@ __device__ unsigned long long g_fprof[8];
   } while (0)
 #endif
 constexpr int kThreads = 32 * kWarpsPerBlock;
-constexpr unsigned kDonate = 256;  // pending local daughters above which splits go global
+#ifndef HWWG_KDONATE
+#define HWWG_KDONATE 256
+#endif
+#ifndef HWWG_KSHARE
+#define HWWG_KSHARE 64
+#endif
+#ifndef HWWG_BACKOFF
+#define HWWG_BACKOFF 2048
+#endif
+constexpr unsigned kDonate = HWWG_KDONATE;  // pending local daughters above which splits go global
 constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
 constexpr unsigned kClaim = 32;  // source particles a warp reserves per claim
-constexpr unsigned kShare = 64;  // pending daughters above which a warp shares runs with idle warps
+constexpr unsigned kShare = HWWG_KSHARE;
+constexpr int kSmemStack = 8;
+#ifndef HWWG_KPIECE
+#define HWWG_KPIECE 32
+#endif
+constexpr unsigned kPiece = HWWG_KPIECE;  // smallest run piece handed to an idle warp  // split-stack records per warp kept in shared memory  // pending daughters above which a warp shares runs with idle warps
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -235,7 +257,12 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  FastStackRec* stk = a.stacks + (size_t)gwarp * a.stack_cap;  // per-warp RLE stack (L1/L2)
+  // per-warp RLE split stack: the bottom kSmemStack records on chip (steady
+  // state rarely goes deeper), the rest in global memory
+  FastStackRec* stk = a.stacks + (size_t)gwarp * a.stack_cap;
+  __shared__ FastStackRec s_stk[kWarpsPerBlock][kSmemStack];
+  FastStackRec* s_my = s_stk[threadIdx.x >> 5];
+#define STK(i) (*((i) < kSmemStack ? &s_my[(i)] : &stk[(i)]))
   int sp = 0;
   unsigned pend = 0;  // daughters pending in the local stack (warp-uniform)
   bool src_done = false;
@@ -250,12 +277,14 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   const bool sh = a.smem_tallies != 0;       // shared memory in use (zero + flush)
   constexpr bool shf = kShf;                 // fp64 tallies in shared memory
   SmemTally S = smem_view(smem, I, a.nb);
-  if (sh) {
-    const size_t words = shf ? (size_t)(a.nb + 4) * I + 1 + a.nb + 2 + (I + 1) / 2
-                             : (size_t)(I + 1) / 2;
-    for (size_t i = threadIdx.x; i < words; i += blockDim.x) smem[i] = 0.0;
-    __syncthreads();
-  }
+  // dynamic shared memory: [tallies (mode-dependent words) | window centres I]
+  const size_t tally_words = shf ? (size_t)(a.nb + 4) * I + 1 + a.nb + 2 + (I + 1) / 2
+                                 : (sh ? (size_t)(I + 1) / 2 : 0);
+  for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
+  double* s_cent = smem + tally_words;  // read at every window site: keep it on chip
+  if (windows)
+    for (int i = threadIdx.x; i < I; i += blockDim.x) s_cent[i] = a.centers[i];
+  __syncthreads();
   // per-lane event counters: 32 bits is plenty within one launch (registers
   // are what bounds occupancy here)
   unsigned n_coll = 0, n_cen = 0;
@@ -307,10 +336,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       }
       open = __shfl_sync(0xffffffffu, open, 0);
       if (open) {
-        FastStackRec& top = stk[sp - 1];
+        FastStackRec& top = STK(sp - 1);
         const unsigned cnt = top.count;
-        const bool split_top = cnt >= 64;
-        unsigned m = split_top ? min(open, cnt / 32 - 1) : min(open, (unsigned)(sp - 1));
+        const bool split_top = cnt >= 2 * kPiece;
+        unsigned m = split_top ? min(open, cnt / kPiece - 1) : min(open, (unsigned)(sp - 1));
         const unsigned piece = split_top ? cnt / (m + 1) : 0u;
         unsigned long long s0 = 0;
         if (m && lane == 0) {
@@ -326,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           if (s0 + m > a.pool.cap) m = s0 < a.pool.cap ? (unsigned)(a.pool.cap - s0) : 0u;
           unsigned given = 0;
           if (lane < (int)m) {
-            FastStackRec g = split_top ? top : stk[sp - 1 - lane];
+            FastStackRec g = split_top ? top : STK(sp - 1 - lane);
             if (split_top) {
               g.base = top.base + lane * piece;
               g.count = piece;
@@ -354,9 +383,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         }
       }
     }
+    FPROF(8);
     unsigned need = __ballot_sync(0xffffffffu, !p.alive);
     while (need && sp > 0) {
-      FastStackRec& r = stk[sp - 1];
+      FastStackRec& r = STK(sp - 1);
       const unsigned k = __popc(need);
       const unsigned cnt = r.count;
       const unsigned take = k < cnt ? k : cnt;
@@ -372,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (cnt == take) --sp;
       need = __ballot_sync(0xffffffffu, !p.alive);
     }
+    FPROF(9);
     // Source claims: a warp holds a reservation [r_lo, r_hi) of up to kClaim
     // particles. Its first reservation is static (no atomic: every warp would
     // otherwise hit the one counter at launch); later ones are claimed one
@@ -396,6 +427,15 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       const unsigned take = k < avail ? k : avail;
       const unsigned base = r_lo;
       r_lo += take;
+      // warm L1 with the rest of the reservation: the next refills hit on chip
+      if ((unsigned)lane < r_hi - r_lo) {
+        const unsigned kk = r_lo + lane;
+        const unsigned pi =
+            a.scramble && (kk | 1023u) < n_src ? (kk & ~1023u) | (__brev(kk) >> 22) : kk;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.xm + pi));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.wt + pi));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.meta + pi));
+      }
       const unsigned rank = __popc(need & lt);
       if (!p.alive && rank < take) {
         // Claims walk the source in bit-reversed order inside 1024-particle
@@ -423,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       }
       need = __ballot_sync(0xffffffffu, !p.alive);
     }
+    FPROF(10);
     const bool any_alive = need != 0xffffffffu;
     if (!any_alive && sp == 0 && src_done) {
       // Out of local work: claim a donated record, or leave when no warp can
@@ -465,11 +506,14 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
               break;
             }
             __nanosleep(backoff);
-            backoff = backoff < 2048 ? backoff * 2 : 2048;  // idle polling costs issue slots
+            backoff = backoff < HWWG_BACKOFF ? backoff * 2 : HWWG_BACKOFF;  // idle polling costs issue slots
           }
         }
       }
       got = __shfl_sync(0xffffffffu, got, 0);
+#ifdef HWWG_FAST_PROF
+      fp_c[6] += clock64() - fp_trip;
+#endif
       if (got < 0) break;
       const unsigned long long slot = __shfl_sync(0xffffffffu, ticket, 0);
       ticket = ~0ULL;
@@ -478,22 +522,28 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       __syncwarp();
       __threadfence();
       if (lane == 0) {
-        stk[0] = *pr;
-        stk[0].ready = 0;
+        STK(0) = *pr;
+        STK(0).ready = 0;
         pr->ready = 0;  // slots are reused by the next segment
       }
       __syncwarp();
       sp = 1;
-      pend = stk[0].count;
+      pend = STK(0).count;
       continue;
     }
     if (!any_alive) continue;
     if (p.alive) ++n_ev;
     ++n_iter;
-    FPROF(0);
 #ifdef HWWG_FAST_PROF
-    const bool fp_tail = __popc(~need) <= 4;
+    if (lane == 0) {
+      const unsigned long long dt_ns = globaltimer() - ctl[4];
+      const int bin = (int)min(dt_ns / 5000ULL, (unsigned long long)(kHistBins - 1));
+      const int sg = a.seg < 8 ? a.seg : 7;
+      atomicAdd(&g_fhist[sg][bin][0], 1u);
+      atomicAdd(&g_fhist[sg][bin][1], (unsigned)__popc(~need));
+    }
 #endif
+    FPROF(0);
 
     // ---- one event per live lane; tally contributions are collected per lane
     // and committed warp-aggregated after the event (see agg_add)
@@ -579,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         }
       }
       if (window_site && windows) {  // ww.cpp:46-72 (split conserves, roulette unbiased)
-        const double c = a.centers[p.cell];
+        const double c = s_cent[p.cell];
         if (p.w > c * a.rho) {
           double n = ceil(p.w / c);
           if (n > 1e6) {
@@ -719,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       const unsigned lmask = __ballot_sync(0xffffffffu, push_local);
       if (push_local) {
         const int slot = sp + (int)__popc(lmask & lt);
-        if (slot < a.stack_cap) stk[slot] = rec;
+        if (slot < a.stack_cap) STK(slot) = rec;
         else atomicCAS(&a.err->code, 0, HWWG_ESTACK);
       }
       unsigned ld = push_local ? dau : 0;
@@ -733,15 +783,12 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     FPROF(4);
 #ifdef HWWG_FAST_PROF
     fp_c[5] += 1;
-    if (fp_tail) {
-      fp_c[6] += 1;
-      fp_c[7] += clock64() - fp_trip;
-    }
 #endif
   }
 #ifdef HWWG_FAST_PROF
+  fp_c[7] = clock64() - fp_k0;
   if (lane == 0)
-    for (int k = 0; k < 8; ++k) atomicAdd(&g_fprof[k], fp_c[k]);
+    for (int k = 0; k < 12; ++k) atomicAdd(&g_fprof[k], fp_c[k]);
 #endif
 
   if (lane == 0) {
@@ -822,6 +869,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   }
 }
 
+#undef STK
+
 // Folds the flush replicas into the tallies and re-zeroes them: one owner per
 // word, so plain adds (the layout is k_fast_segment's shared-memory layout from
 // the track-batch block on: trk[nb*I], cphi, cJ, cF [I], edge[I+1], cwb[nb],
@@ -878,19 +927,26 @@ size_t fast_smem_bytes(int I, int nb) {
   return ((size_t)(nb + 4) * I + 1 + nb + 2) * sizeof(double) + (size_t)(I + 1) / 2 * 8 + 16;
 }
 size_t fast_smem_count_bytes(int I) { return (size_t)(I + 1) / 2 * 8 + 16; }
+size_t fast_smem_centers_bytes(int I) { return (size_t)I * 8; }
 size_t fast_flush_stride(int I, int B) { return (size_t)(B + 4) * I + 1 + B + 2 + I; }
 
 int fast_threads_per_block() { return kThreads; }
 
 // -DHWWG_FAST_PROF builds: read and clear the loop phase accounting (0 otherwise)
-int fast_prof_read(unsigned long long out[8]) {
+int fast_prof_read(unsigned long long out[12], unsigned* hist) {
 #ifdef HWWG_FAST_PROF
-  HWWG_CUDA(cudaMemcpyFromSymbol(out, g_fprof, 8 * sizeof(unsigned long long)));
-  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (hist) {
+    HWWG_CUDA(cudaMemcpyFromSymbol(hist, g_fhist, sizeof(g_fhist)));
+    std::vector<unsigned> zh(sizeof(g_fhist) / sizeof(unsigned), 0u);
+    HWWG_CUDA(cudaMemcpyToSymbol(g_fhist, zh.data(), sizeof(g_fhist)));
+  }
+  HWWG_CUDA(cudaMemcpyFromSymbol(out, g_fprof, 12 * sizeof(unsigned long long)));
+  const unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   HWWG_CUDA(cudaMemcpyToSymbol(g_fprof, z, sizeof z));
   return 1;
 #else
   (void)out;
+  (void)hist;
   return 0;
 #endif
 }
@@ -911,6 +967,9 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
   ctl[1] = 0;
   ctl[2] = warps;  // every warp starts active (holding source work)
   ctl[3] = 0;      // no backlog declared yet
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  ctl[4] = t;  // segment start (diagnostics)
   *src_head = warps * kClaim;  // every warp's first reservation is static
 }
 }  // namespace
