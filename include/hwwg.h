@@ -232,6 +232,26 @@ void hwwg_default_config(hwwg_run_config* cfg);
  * joined with '\n' into buf. */
 int hwwg_validate_config(const hwwg_run_config* cfg, char* buf, uint64_t buf_len);
 
+/* ---------------------------------------------------------- output files */
+/* The reference's run outputs (proj/src/driver.cpp:355-438), same bytes for
+ * equal records: step_<n>.csv (write_step_csv; ww_centers / phi_hybrid NULL
+ * print as nan, sigma prints as nan unless rec->sigma_valid), summary.csv over
+ * recs[0..n) (write_summary_csv; the S_N error metrics, fom_sigma_mod and alpha
+ * are nan: no reference solution), run.json (write_run_json; "reference" = "").
+ * dir is created if missing. */
+int hwwg_write_step_csv(const char* dir, const hwwg_step_record* rec, int32_t cells,
+                        const double* edges, const double* phi_track, const double* sigma,
+                        const double* phi_census, const double* current, const double* closure,
+                        const double* ww_centers, const double* phi_hybrid,
+                        const uint64_t* tracks, double normalization);
+int hwwg_write_summary_csv(const char* dir, const hwwg_step_record* recs, uint64_t n);
+int hwwg_write_run_json(const char* dir, const hwwg_run_config* cfg, double total_seconds,
+                        uint64_t steps_completed);
+/* hww::run's per-step writing (driver.cpp:318-321): step_<last>.csv and
+ * summary.csv of every step so far; final != 0 also writes run.json with
+ * total_seconds. */
+int hwwg_driver_write(hwwg_driver* d, const char* dir, int32_t final, double total_seconds);
+
 /* ----------------------------------------------------- device components */
 /* hww::assemble_solve (losm.cpp:143-165) on the device, single CTA.
  * phi_prev/F_* are I+2 long, J_prev I+1, q I (NULL = zero).  implicit != 0

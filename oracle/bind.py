@@ -277,6 +277,43 @@ class Reference(_Lib):
         L.hwwref_take_census.argtypes = [C.c_void_p, C.c_uint64]
         L.hwwref_num_threads.restype = C.c_int
         L.hwwref_set_threads.argtypes = [C.c_int]
+        L.hwwref_run_to_dir.argtypes = [C.POINTER(Config), C.c_char_p]
+        L.hwwref_write_outputs.argtypes = [C.c_char_p, C.POINTER(Config), C.c_int32, C.c_int32] + [
+            C.c_void_p] * 11 + [C.c_double]
+
+    def run_to_dir(self, config: Config, out_dir):
+        """hww::run with out_dir: the reference's own output files."""
+        if self.lib.hwwref_run_to_dir(C.byref(config), str(out_dir).encode()) != 0:
+            raise ValueError(self.err())
+
+    def write_outputs(self, out_dir, config: Config, steps, total_seconds):
+        """The reference writers on synthetic records. steps: list of dicts with
+        arrays phi_track, sigma, phi_census, current, closure, centers (or None),
+        hybrid (or None), tracks and scalars t_end, tau, fom_sigma_l2,
+        census_weight, census_weight_sigma, normalization, sigma_valid,
+        hybrid_solve_failed, step, histories, comb_in, comb_out,
+        updates_applied, counters (Counters)."""
+        n, I = len(steps), config.cells
+        def stack(key, dt=np.float64):
+            parts = [np.asarray(s[key] if s[key] is not None else np.zeros(I), dt) for s in steps]
+            return np.ascontiguousarray(np.concatenate(parts) if parts else np.zeros(1, dt))
+        arrs = [stack(k) for k in ("phi_track", "sigma", "phi_census", "current", "closure",
+                                   "centers", "hybrid")]
+        tracks = stack("tracks", np.uint64)
+        sc = np.zeros((max(n, 1), 8)) if not n else np.array([[s[k] for k in ("t_end", "tau", "fom_sigma_l2", "census_weight",
+                                       "census_weight_sigma", "normalization", "sigma_valid",
+                                       "hybrid_solve_failed")] for s in steps], np.float64)
+        ints = np.zeros((1, 6), np.uint64) if not n else np.array([[s["step"], s["histories"], s["comb_in"], s["comb_out"],
+                          s["updates_applied"],
+                          (1 if s["centers"] is not None else 0) |
+                          (2 if s["hybrid"] is not None else 0)] for s in steps], np.uint64)
+        cnt = (Counters * max(n, 1))(*[s["counters"] for s in steps])
+        rc = self.lib.hwwref_write_outputs(
+            str(out_dir).encode(), C.byref(config), n, I, *[a.ctypes.data for a in arrs],
+            tracks.ctypes.data, sc.ctypes.data, ints.ctypes.data, C.addressof(cnt),
+            total_seconds)
+        if rc != 0:
+            raise ValueError(self.err())
 
     def run_segment(self, edges, mats, t_begin, t_end, seed, step, histories_total, batches,
                     source, h_begin, centers=None, rho=1.25, parallel=True, chunk=256,

@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <filesystem>
 #include <memory>
 #include <optional>
 #include <span>
@@ -631,6 +632,76 @@ int32_t hwwref_locate(const double* edges, int32_t cells, double x) {
 }
 
 // hww::build_uniform_mesh edges (proj/src/mesh.cpp:42-50).
+// hww::run with out_dir (proj/src/driver.cpp:286-342): the reference's own
+// writers produce step_<n>.csv, summary.csv and run.json in dir.
+int hwwref_run_to_dir(const hwwref_config* c, const char* dir) {
+  try {
+    hww::RunConfig config = to_config(*c);
+    config.out_dir = dir;
+    hww::run(config);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// The reference writers (driver.cpp:355-438) on records built from arrays:
+// step k of n has cells values per field at phi_track + k*cells etc.;
+// scalars[k*8 + ...] = {t_end, tau, fom_sigma_l2, census_weight,
+// census_weight_sigma, normalization, sigma_valid, hybrid_solve_failed};
+// ints[k*6 + ...] = {step, histories, comb_in, comb_out, updates_applied,
+// has_centers | has_hybrid << 1}. Writes every step_<n>.csv, summary.csv and
+// run.json (total_seconds) to dir.
+int hwwref_write_outputs(const char* dir, const hwwref_config* c, int32_t n, int32_t cells,
+                         const double* phi_track, const double* sigma, const double* phi_census,
+                         const double* current, const double* closure, const double* centers,
+                         const double* hybrid, const uint64_t* tracks, const double* scalars,
+                         const uint64_t* ints, const hwwref_counters* counters,
+                         double total_seconds) {
+  try {
+    std::filesystem::create_directories(dir);  // as hww::run does (driver.cpp:301)
+    hww::RunRecord run;
+    run.config = to_config(*c);
+    run.total_seconds = total_seconds;
+    const hww::Mesh1D mesh = run.config.make_mesh();
+    for (int k = 0; k < n; ++k) {
+      const size_t o = (size_t)k * cells;
+      hww::StepRecord r;
+      r.step = (int)ints[6 * k + 0];
+      r.t_end = scalars[8 * k + 0];
+      r.metrics.tau = scalars[8 * k + 1];
+      r.metrics.fom_sigma_l2 = scalars[8 * k + 2];
+      r.report.census_weight = scalars[8 * k + 3];
+      r.report.census_weight_sigma = scalars[8 * k + 4];
+      r.report.normalization = scalars[8 * k + 5];
+      r.report.sigma_valid = scalars[8 * k + 6] != 0.0;
+      r.hybrid_solve_failed = scalars[8 * k + 7] != 0.0;
+      r.report.histories = ints[6 * k + 1];
+      r.comb.input_count = ints[6 * k + 2];
+      r.comb.output_count = ints[6 * k + 3];
+      r.updates_applied = (int)ints[6 * k + 4];
+      r.report.phi_track.assign(phi_track + o, phi_track + o + cells);
+      r.report.phi_track_sigma.assign(sigma + o, sigma + o + cells);
+      r.report.phi_census.assign(phi_census + o, phi_census + o + cells);
+      r.report.current_census.assign(current + o, current + o + cells);
+      r.report.closure_census.assign(closure + o, closure + o + cells);
+      if (ints[6 * k + 5] & 1) r.ww_centers.assign(centers + o, centers + o + cells);
+      if (ints[6 * k + 5] & 2) r.phi_hybrid.assign(hybrid + o, hybrid + o + cells);
+      r.tracks_per_cell.assign(tracks + o, tracks + o + cells);
+      r.counters = get_counters(&counters[k]);
+      run.steps.push_back(r);
+      hww::write_step_csv(dir, run.steps.back(), mesh);
+    }
+    hww::write_summary_csv(dir, run);
+    hww::write_run_json(dir, run);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 void hwwref_uniform_edges(double x_min, double x_max, int32_t cells, double* out) {
   const auto m = hww::build_uniform_mesh(x_min, x_max, cells);
   std::memcpy(out, m.edges().data(), (cells + 1) * sizeof(double));

@@ -114,7 +114,8 @@ EXPORTS = (
     "hwwg_driver_step", "hwwg_driver_arrays", "hwwg_driver_bank", "hwwg_load_config_file",
     "hwwg_default_config", "hwwg_validate_config", "hwwg_losm_assemble_solve",
     "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log",
-    "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan")
+    "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan",
+    "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write")
 
 _lib = None
 
@@ -165,6 +166,11 @@ def lib():
     L.hwwg_rebalance_plan.argtypes = [u64ptr, u64ptr, C.c_int32, C.c_int32, C.c_uint64, u64ptr,
                                       u64ptr, u64ptr]
     L.hwwg_rebalance_plan.restype = None
+    L.hwwg_write_step_csv.argtypes = [C.c_char_p, C.POINTER(StepRecordC), C.c_int32, dptr, dptr,
+                                      dptr, dptr, dptr, dptr, dptr, dptr, u64ptr, C.c_double]
+    L.hwwg_write_summary_csv.argtypes = [C.c_char_p, C.POINTER(StepRecordC), C.c_uint64]
+    L.hwwg_write_run_json.argtypes = [C.c_char_p, C.POINTER(RunConfigC), C.c_double, C.c_uint64]
+    L.hwwg_driver_write.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_double]
     _lib = L
     return L
 

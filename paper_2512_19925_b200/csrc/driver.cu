@@ -184,6 +184,7 @@ struct hwwg_driver {
       h_centers, h_hybrid;
   std::vector<unsigned long long> h_tracks;
   bool h_has_centers = false, h_has_hybrid = false;
+  std::vector<hwwg_step_record> history;  // every step so far (summary.csv)
 
   ~hwwg_driver() {
     if (ev0) cudaEventDestroy(ev0);
@@ -1064,6 +1065,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   d->has_prev_report = true;
   d->rep_cur ^= 1;
   ++d->next_step;
+  d->history.push_back(*rec);
 }
 
 }  // namespace
@@ -1171,6 +1173,24 @@ int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma, dou
   if (tracks_per_cell)
     for (int i = 0; i < d->I; ++i) tracks_per_cell[i] = d->h_tracks[i];
   return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_driver_write(hwwg_driver* d, const char* dir, int32_t final, double total_seconds) {
+  HWWG_API_BEGIN
+  if (!d || !dir) return fail(HWWG_EINVAL, "NULL argument");
+  if (d->history.empty()) return fail(HWWG_ESTATE, "no step has run yet");
+  const hwwg_run_config& c = d->cfg;
+  int rc = hwwg_write_step_csv(dir, &d->history.back(), d->I, d->prob.edges.data(),
+                               d->h_phi_track.data(), d->h_sigma.data(), d->h_phi_census.data(),
+                               d->h_current.data(), d->h_closure.data(),
+                               d->h_has_centers ? d->h_centers.data() : nullptr,
+                               d->h_has_hybrid ? d->h_hybrid.data() : nullptr,
+                               reinterpret_cast<const uint64_t*>(d->h_tracks.data()),
+                               (double)c.histories_per_step);
+  if (rc == HWWG_OK) rc = hwwg_write_summary_csv(dir, d->history.data(), d->history.size());
+  if (rc == HWWG_OK && final) rc = hwwg_write_run_json(dir, &c, total_seconds, d->history.size());
+  return rc;
   HWWG_API_END
 }
 

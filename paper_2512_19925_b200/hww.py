@@ -316,6 +316,20 @@ def run_segment_parallel(ctx, source, h_begin, ww, tallies, outcome, engine=None
 
 
 # ------------------------------------------------------------------- driver
+def _file_key(path, key):
+    """A host-tooling key of a key = value config file (the C loader accepts
+    and skips it); '' when absent."""
+    val = ""
+    with open(path) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if "=" in line:
+                k, v = (t.strip() for t in line.split("=", 1))
+                if k == key:
+                    val = v
+    return val
+
+
 @dataclass
 class RunConfig:
     """hww::RunConfig (config.hpp:33-66) with the reference defaults."""
@@ -343,6 +357,7 @@ class RunConfig:
     time_steps: int = 20
     threads: int = 0
     host_bank: bool = False
+    out_dir: str = ""  # config.hpp:63: empty -> no file output
 
     def comb_target(self):
         return self.target_population or self.histories_per_step
@@ -385,7 +400,7 @@ class RunConfig:
             source_strength=c.strength,
             material=Material(c.sigma_t, c.sigma_s, c.sigma_f, c.nu_f, c.speed),
             x_min=c.x_min, x_max=c.x_max, cells=c.cells, t_end=c.t_end,
-            time_steps=c.time_steps, threads=c.threads)
+            time_steps=c.time_steps, threads=c.threads, out_dir=_file_key(path, "out_dir"))
 
     def validate(self):
         """validate_config (config.cpp:27-69): list of violations."""
@@ -432,6 +447,12 @@ class Driver:
             A.as_dptr(arr["ww_centers"]), A.as_dptr(arr["phi_hybrid"]), A.as_u64ptr(tracks)))
         arr["tracks_per_cell"] = tracks
         return arr
+
+    def write(self, out_dir, final=False, total_seconds=0.0):
+        """hww::run's output writing (driver.cpp:318-321, 332-336): step_<n>.csv
+        of the last step and summary.csv of all steps; run.json when final."""
+        _raise(A.lib().hwwg_driver_write(self._h, str(out_dir).encode(), 1 if final else 0,
+                                         float(total_seconds)))
 
     def bank(self):
         n = C.c_uint64()
@@ -489,12 +510,31 @@ def rebalance_plan(k_lo_all, k_hi_all, rank, H):
     return send, first, recv
 
 
-def run(config: RunConfig, device=0, rng_mode=RNG_EXACT):
-    """hww::run (driver.hpp:88): returns the list of (record, arrays) per step."""
+def run(config: RunConfig, device=0, rng_mode=RNG_EXACT, out_dir=None):
+    """hww::run (driver.hpp:88, driver.cpp:286-342): returns the list of
+    (record, arrays) per step. With out_dir (or config.out_dir) the reference's
+    files are written as it writes them: step_<n>.csv and summary.csv after every
+    step, run.json at the end, an INCOMPLETE marker if the run aborts."""
+    import os
+    import time
+    out_dir = out_dir if out_dir is not None else getattr(config, "out_dir", "")
     d = Driver(config, device, rng_mode)
     out = []
-    for _ in range(config.time_steps):
-        rec = d.step()
-        out.append((rec, d.arrays()))
-    d.close()
+    t0 = time.perf_counter()
+    try:
+        for _ in range(config.time_steps):
+            rec = d.step()
+            out.append((rec, d.arrays()))
+            if out_dir:
+                d.write(out_dir)
+        if out_dir:
+            d.write(out_dir, final=True, total_seconds=time.perf_counter() - t0)
+    except Exception:
+        if out_dir:
+            os.makedirs(out_dir, exist_ok=True)
+            with open(os.path.join(out_dir, "INCOMPLETE"), "w") as f:
+                f.write("run aborted before completing all steps\n")
+        raise
+    finally:
+        d.close()
     return out
