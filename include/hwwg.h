@@ -19,6 +19,7 @@
  *       proj/include/hww/losm.hpp:77-80 (single-CTA device solve).
  *   hwwg_build_centers         replaces  hww::build_centers  proj/include/hww/ww.hpp:34-35
  *   hwwg_moving_average        replaces  hww::moving_average proj/include/hww/filters.hpp:30
+ *   hwwg_fourier_lowpass       replaces  hww::fourier_lowpass proj/include/hww/filters.hpp:36
  *   hwwg_uniform_comb          replaces  hww::uniform_comb   proj/include/hww/popctrl.hpp:22
  *
  * Calls on one context are single-threaded; device work runs on the context's
@@ -268,6 +269,9 @@ int hwwg_build_centers(hwwg_ctx* ctx, const double* phi, int32_t n, double eps_m
                        double rho, double* centers);
 /* hww::moving_average (filters.cpp:11-24). */
 int hwwg_moving_average(hwwg_ctx* ctx, const double* g, int32_t n, int32_t k, double* out);
+/* hww::fourier_lowpass (filters.cpp:26-52; filters.hpp:36): the hww_fourier
+ * filter, bit-identical to the reference (host-libm twiddles, reference order). */
+int hwwg_fourier_lowpass(hwwg_ctx* ctx, const double* g, int32_t n, int32_t cutoff, double* out);
 /* hww::uniform_comb (popctrl.cpp:7-42) with stream (seed, stream_id). */
 int hwwg_uniform_comb(hwwg_ctx* ctx, const hwwg_particle* bank, uint64_t n, uint64_t target,
                       uint64_t seed, uint64_t stream_id, hwwg_particle* out,

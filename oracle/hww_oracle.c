@@ -808,6 +808,49 @@ int orc_moving_average(const double* g, int32_t M, int32_t k, double* out) {
   return 0;
 }
 
+/* filters.cpp:26-52: direct O(M^2) transform. std::polar(1, a) is (cos a, sin
+ * a); real * complex scales both parts; the synthesis multiplies complex
+ * numbers as (ac - bd) + (ad + bc)i; modes with min(j, M-j) > cutoff are
+ * zeroed and skipped (spectrum == 0+0i). Only the real part is kept. */
+int orc_fourier_lowpass(const double* g, int32_t M, int32_t cutoff, double* out) {
+  if (cutoff < 0) {
+    set_err("fourier cutoff must be >= 0");
+    return -1;
+  }
+  if (M <= 1) {
+    memmove(out, g, sizeof(double) * (size_t)(M > 0 ? M : 0));
+    return 0;
+  }
+  const double w0 = 2.0 * 3.141592653589793 / M; /* std::numbers::pi */
+  double* sre = (double*)calloc((size_t)M, sizeof(double));
+  double* sim = (double*)calloc((size_t)M, sizeof(double));
+  for (int j = 0; j < M; ++j) {
+    const int mj = j < M - j ? j : M - j;
+    if (mj > cutoff) continue;
+    double re = 0.0, im = 0.0;
+    for (int m = 0; m < M; ++m) {
+      const double a = -w0 * j * m;
+      re += g[m] * cos(a);
+      im += g[m] * sin(a);
+    }
+    sre[j] = re;
+    sim[j] = im;
+  }
+  for (int m = 0; m < M; ++m) {
+    double re = 0.0;
+    for (int j = 0; j < M; ++j) {
+      if (sre[j] == 0.0 && sim[j] == 0.0) continue;
+      const double a = w0 * j * m;
+      const double c = cos(a), d = sin(a);
+      re += sre[j] * c - sim[j] * d;
+    }
+    out[m] = re / M;
+  }
+  free(sre);
+  free(sim);
+  return 0;
+}
+
 /* ww.cpp:8-32 */
 int orc_build_centers(const double* phi, int32_t n, double eps_min, double rho,
                       double* centers) {
@@ -901,19 +944,24 @@ static double now_s(void) {
   return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
 
-/* filters.cpp:63-87 (moving average only; Fourier is out of scope). */
+/* filters.cpp:54-87: apply_filter (config.hpp filter(): moving average for
+ * hww_ma, Fourier low-pass for hww_fourier, none otherwise). */
+static int apply_filter(const double* g, int len, const orc_config* c, double* out) {
+  if (c->mode == 3) return orc_moving_average(g, len, c->ma_base_k, out);
+  return orc_fourier_lowpass(g, len, c->fourier_cutoff, out);
+}
 static int filter_interior(double* g, int len, const orc_config* c) {
-  if (c->mode != 3 || len <= 2) return 0; /* FilterSpec::none unless hww_ma */
+  if ((c->mode != 3 && c->mode != 4) || len <= 2) return 0; /* FilterSpec::none */
   double* tmp = (double*)malloc(sizeof(double) * (size_t)len);
-  const int rc = orc_moving_average(g + 1, len - 2, c->ma_base_k, tmp);
+  const int rc = apply_filter(g + 1, len - 2, c, tmp);
   memcpy(g + 1, tmp, sizeof(double) * (size_t)(len - 2));
   free(tmp);
   return rc;
 }
 static int filter_all(double* g, int len, const orc_config* c) {
-  if (c->mode != 3) return 0;
+  if (c->mode != 3 && c->mode != 4) return 0;
   double* tmp = (double*)malloc(sizeof(double) * (size_t)len);
-  const int rc = orc_moving_average(g, len, c->ma_base_k, tmp);
+  const int rc = apply_filter(g, len, c, tmp);
   memcpy(g, tmp, sizeof(double) * (size_t)len);
   free(tmp);
   return rc;
@@ -949,7 +997,7 @@ static int validate(const orc_config* c) {
     }
   }
   if (c->mode == 3 && c->ma_base_k < 0) { set_err("ma_base_k must be >= 0"); return -1; }
-  if (c->mode == 4) { set_err("hww_fourier is not supported by the oracle"); return -1; }
+  if (c->mode == 4 && c->fourier_cutoff < 0) { set_err("fourier_cutoff must be >= 0"); return -1; }
   if (c->batches < 2) { set_err("batches must be >= 2"); return -1; }
   if (!(c->x_min < c->x_max) || c->cells < 1 || !(c->t_end > 0.0) || c->time_steps < 1 ||
       !(c->strength > 0.0) || c->x0 < c->x_min || c->x0 > c->x_max) {

@@ -149,6 +149,7 @@ int orc_edge_currents(const double* census_current, int32_t cells, const double*
                       double* out);
 /* filters.cpp:11-24 */
 int orc_moving_average(const double* g, int32_t n, int32_t k, double* out);
+int orc_fourier_lowpass(const double* g, int32_t n, int32_t cutoff, double* out);
 /* ww.cpp:8-32; returns 1 on uniform fallback */
 int orc_build_centers(const double* phi, int32_t n, double eps_min, double rho,
                       double* centers);

@@ -115,7 +115,7 @@ EXPORTS = (
     "hwwg_default_config", "hwwg_validate_config", "hwwg_losm_assemble_solve",
     "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log",
     "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan",
-    "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write")
+    "hwwg_fourier_lowpass", "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write")
 
 _lib = None
 
@@ -155,6 +155,7 @@ def lib():
         dptr, dptr, dptr]
     L.hwwg_build_centers.argtypes = [C.c_void_p, dptr, C.c_int32, C.c_double, C.c_double, dptr]
     L.hwwg_moving_average.argtypes = [C.c_void_p, dptr, C.c_int32, C.c_int32, dptr]
+    L.hwwg_fourier_lowpass.argtypes = [C.c_void_p, dptr, C.c_int32, C.c_int32, dptr]
     L.hwwg_uniform_comb.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_void_p, dptr, dptr]
     L.hwwg_device_log.argtypes = [C.c_void_p, dptr, C.c_uint64, dptr]

@@ -158,6 +158,7 @@ struct hwwg_driver {
   // low-order state
   DevBuf<double> lo_mem;
   DevBuf<double> lo_fac;  // cached LOSM factorization (throughput mode)
+  DevBuf<double> ftab_cell, ftab_edge;  // hww_fourier twiddles (fourier_tables)
   bool losm_cache = true;  // HWWG_LOSM_NOCACHE=1 disables it
   bool fac_valid = false;
   double fac_theta = 0.0, fac_dt = 0.0;
@@ -251,6 +252,13 @@ void init_driver(hwwg_driver* d) {
   s.sys = q; q += 6 * (size_t)n;
   s.F_now = q; q += I + 2;
   s.fac = nullptr;
+  if (c.mode == 4) {  // hww_fourier: host-libm twiddles for the I- and (I+1)-point transforms
+    const std::vector<double> tc = fourier_tables(I), te = fourier_tables(I + 1);
+    d->ftab_cell.reserve(tc.size());
+    d->ftab_edge.reserve(te.size());
+    HWWG_CUDA(cudaMemcpy(d->ftab_cell.p, tc.data(), tc.size() * 8, cudaMemcpyHostToDevice));
+    HWWG_CUDA(cudaMemcpy(d->ftab_edge.p, te.data(), te.size() * 8, cudaMemcpyHostToDevice));
+  }
   if (d->fast && d->losm_cache && lo_fac_words(I)) {  // cached LOSM factorization
     d->lo_fac.reserve(lo_fac_words(I));
     s.fac = d->lo_fac.p;
@@ -626,6 +634,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.eps_min = c.eps_min;
       a.rho = c.rho;
       a.ma_k = ma_k;
+      a.fourier_tab_cell = c.mode == 4 ? d->ftab_cell.p : nullptr;
+      a.fourier_tab_edge = c.mode == 4 ? d->ftab_edge.p : nullptr;
+      a.fourier_cutoff = c.fourier_cutoff;
       a.mode = 0;
       a.fast_solve = d->fast ? 1 : 0;
       a.refactor = d->need_refactor(theta_eff, dt);
@@ -776,6 +787,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.eps_min = c.eps_min;
       a.rho = c.rho;
       a.ma_k = ma_k;
+      a.fourier_tab_cell = c.mode == 4 ? d->ftab_cell.p : nullptr;
+      a.fourier_tab_edge = c.mode == 4 ? d->ftab_edge.p : nullptr;
+      a.fourier_cutoff = c.fourier_cutoff;
       a.mode = 1;
       a.fast_solve = d->fast ? 1 : 0;
       a.refactor = d->need_refactor(theta_eff, dt);
@@ -1079,7 +1093,6 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   char buf[1024];
   if (hwwg_validate_config(cfg, buf, sizeof buf) != 0)
     return fail(HWWG_EINVAL, std::string("invalid configuration:\n") + buf);
-  if (cfg->mode == 4) return fail(HWWG_EINVAL, "hww_fourier is out of scope for this engine");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();

@@ -376,6 +376,31 @@ int hwwg_moving_average(hwwg_ctx* c, const double* g, int32_t n, int32_t k, doub
   HWWG_API_END
 }
 
+int hwwg_fourier_lowpass(hwwg_ctx* c, const double* g, int32_t n, int32_t cutoff, double* out) {
+  HWWG_API_BEGIN
+  if (!c || (n && (!g || !out))) return fail(HWWG_EINVAL, "NULL argument");
+  if (cutoff < 0) return fail(HWWG_EINVAL, "fourier cutoff must be >= 0");
+  if (n == 0) return HWWG_OK;
+  if (n == 1) {
+    out[0] = g[0];
+    return HWWG_OK;
+  }
+  HWWG_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const std::vector<double> tab = fourier_tables(n);
+  c->scratch.reserve(4 * (size_t)n + tab.size());
+  double* d_g = c->scratch.p;
+  double* d_tmp = d_g + n;
+  double* d_tab = d_tmp + 3 * (size_t)n;
+  HWWG_CUDA(cudaMemcpyAsync(d_g, g, n * 8, cudaMemcpyHostToDevice, s));
+  HWWG_CUDA(cudaMemcpyAsync(d_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s));
+  launch_fourier_lowpass(d_g, n, cutoff, d_tab, d_tmp, s);
+  HWWG_CUDA(cudaMemcpyAsync(out, d_g, n * 8, cudaMemcpyDeviceToHost, s));
+  HWWG_CUDA(cudaStreamSynchronize(s));
+  return HWWG_OK;
+  HWWG_API_END
+}
+
 int hwwg_uniform_comb(hwwg_ctx* c, const hwwg_particle* bank, uint64_t n, uint64_t target,
                       uint64_t seed, uint64_t stream_id, hwwg_particle* out, double* in_weight,
                       double* out_weight) {

@@ -13,7 +13,9 @@
 
 #include "common.cuh"
 #include "libm_log.h"
+#include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "low_order.cuh"
 #include "rng.cuh"
@@ -535,6 +537,65 @@ __device__ void filter_inplace(double* g, int len, int interior, int k, double* 
   __syncthreads();
 }
 
+// filters.cpp:26-52 fourier_lowpass over the block, in place (via scratch).
+// tab = fourier_tables(M) from the host: [fwd cos | fwd sin | inv cos | inv sin],
+// each M*M laid out [m][j], the libm cos/sin of the reference's angles
+// (-w0*j*m and w0*j*m), so the device never evaluates a transcendental. The
+// spectrum sums run over m in order and the synthesis over j in order with the
+// zero-mode skip, complex products as (ac - bd, ad + bc): the reference's
+// operations in the reference's order.
+__device__ void fourier_cta(double* g, int M, int cutoff, const double* __restrict__ tab,
+                            double* tmp) {
+  if (M <= 1) return;
+  const size_t MM = (size_t)M * M;
+  const double* fc = tab;
+  const double* fs = tab + MM;
+  const double* ic = tab + 2 * MM;
+  const double* is = tab + 3 * MM;
+  double* sre = tmp;
+  double* sim = tmp + M;
+  double* out = tmp + 2 * M;
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    double re = 0.0, im = 0.0;
+    if (min(j, M - j) <= cutoff) {
+      for (int m = 0; m < M; ++m) {
+        const double gm = g[m];
+        re = re + gm * fc[(size_t)m * M + j];
+        im = im + gm * fs[(size_t)m * M + j];
+      }
+    }
+    sre[j] = re;
+    sim[j] = im;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    double re = 0.0;
+    for (int j = 0; j < M; ++j) {
+      const double a = sre[j], b = sim[j];
+      if (a == 0.0 && b == 0.0) continue;
+      const double c = ic[(size_t)j * M + m], d = is[(size_t)j * M + m];
+      re = re + (a * c - b * d);
+    }
+    out[m] = re / M;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < M; m += blockDim.x) g[m] = out[m];
+  __syncthreads();
+}
+
+// The step's filter: moving average (k > 0), Fourier low-pass (tab != null), or none.
+__device__ void filter_any(double* g, int len, int interior, const LowOrderArgs& a, double* tmp) {
+  if (a.fourier_tab_cell) {
+    if (interior) {
+      if (len > 2) fourier_cta(g + 1, len - 2, a.fourier_cutoff, a.fourier_tab_cell, tmp);
+    } else {
+      fourier_cta(g, len, a.fourier_cutoff, a.fourier_tab_edge, tmp);
+    }
+    return;
+  }
+  filter_inplace(g, len, interior, a.ma_k, tmp);
+}
+
 __device__ bool all_finite(const double* v, int n) {
   bool bad = false;
   for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -728,9 +789,9 @@ __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a) {
     }
     __syncthreads();
     // apply_filter_pipeline(nullptr, F_prev, phi_prev, J_prev), filters.cpp:76-84
-    filter_inplace(s.F_prev, I + 2, 1, a.ma_k, tmp);
-    filter_inplace(s.phi_prev, I + 2, 1, a.ma_k, tmp);
-    filter_inplace(s.J_prev, I + 1, 0, a.ma_k, tmp);
+    filter_any(s.F_prev, I + 2, 1, a, tmp);
+    filter_any(s.phi_prev, I + 2, 1, a, tmp);
+    filter_any(s.J_prev, I + 1, 0, a, tmp);
     solve_and_center(a, s.F_prev, s.PLPR_prev[0], s.PLPR_prev[1], false, red);
   } else {
     // partial_snapshot (tally.cpp:116-128) -> with_boundary_extrapolated -> filter
@@ -740,7 +801,7 @@ __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a) {
       F[i] = a.closure_tally[j] * a.snapshot_inv_norm;
     }
     __syncthreads();
-    filter_inplace(F, I + 2, 1, a.ma_k, tmp);
+    filter_any(F, I + 2, 1, a, tmp);
     const double PL = a.bclosure_tally[0] * a.snapshot_inv_norm;
     const double PR = a.bclosure_tally[1] * a.snapshot_inv_norm;
     solve_and_center(a, F, PL, PR, true, red);
@@ -990,6 +1051,37 @@ void launch_build_centers(const double* phi, int n, double eps_min, double rho, 
                           int* fallback, cudaStream_t st) {
   (void)rho;
   k_build_centers<<<1, kCtaThreads, 0, st>>>(phi, n, eps_min, centers, fallback);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+// Host: the reference's twiddles for an M-point transform (filters.cpp:33-47):
+// w0 = 2 pi / M, forward angle (-w0 * j) * m, inverse (w0 * j) * m, through the
+// host libm cos/sin (std::polar(1, a) = (cos a, sin a)). Layout: forward
+// [m][j], inverse [j][m].
+std::vector<double> fourier_tables(int M) {
+  const size_t MM = (size_t)M * M;
+  std::vector<double> t(4 * MM);
+  const double w0 = 2.0 * 3.141592653589793 / M;  // std::numbers::pi
+  for (int j = 0; j < M; ++j)
+    for (int m = 0; m < M; ++m) {
+      const double af = -w0 * j * m;
+      const double ai = w0 * j * m;
+      t[(size_t)m * M + j] = std::cos(af);
+      t[MM + (size_t)m * M + j] = std::sin(af);
+      t[2 * MM + (size_t)j * M + m] = std::cos(ai);
+      t[3 * MM + (size_t)j * M + m] = std::sin(ai);
+    }
+  return t;
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_fourier(double* g, int n, int cutoff,
+                                                          const double* tab, double* tmp) {
+  fourier_cta(g, n, cutoff, tab, tmp);
+}
+
+void launch_fourier_lowpass(double* g, int n, int cutoff, const double* tab, double* tmp,
+                            cudaStream_t st) {
+  k_fourier<<<1, kCtaThreads, 0, st>>>(g, n, cutoff, tab, tmp);
   HWWG_CUDA(cudaGetLastError());
 }
 

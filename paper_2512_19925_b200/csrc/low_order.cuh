@@ -6,6 +6,8 @@
 // reference given identical inputs (tests/test_gpu_components.py).
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace hwwg {
@@ -47,6 +49,11 @@ struct LowOrderArgs {
   double theta, dt;
   double eps_min, rho;
   int ma_k;  // moving-average half-width, 0 = no filter
+  // hww_fourier: fourier_tables(I) / fourier_tables(I + 1) on the device (null
+  // = no Fourier filter) and the retained-mode bound
+  const double* fourier_tab_cell;
+  const double* fourier_tab_edge;
+  int fourier_cutoff;
   // mode 0: start-of-step lagged solve; inputs from analytic pulse (step 1) or
   //         from the previous report.  mode 1: mid-step implicit solve from the
   //         partial snapshot of the live tallies.
@@ -95,6 +102,11 @@ void launch_comb(const CombArgs& a, cudaStream_t st);
 void launch_build_centers(const double* phi, int n, double eps_min, double rho,
                           double* centers, int* fallback, cudaStream_t st);
 void launch_moving_average(const double* g, int n, int k, double* out, cudaStream_t st);
+// filters.cpp:26-52 on the device with host twiddles (fourier_tables(n));
+// tmp: 3n doubles of device scratch; g is filtered in place
+std::vector<double> fourier_tables(int M);
+void launch_fourier_lowpass(double* g, int n, int cutoff, const double* tab, double* tmp,
+                            cudaStream_t st);
 struct RawLosmArgs {
   int I;
   const double* edges;

@@ -283,6 +283,14 @@ class Engine:
         return out
 
     # popctrl.hpp:22
+    def fourier_lowpass(self, g, cutoff):
+        """hww::fourier_lowpass (filters.cpp:26-52)."""
+        g = np.ascontiguousarray(g, np.float64)
+        out = np.zeros_like(g)
+        _raise(A.lib().hwwg_fourier_lowpass(self._h, A.as_dptr(g), g.size, cutoff,
+                                            A.as_dptr(out)))
+        return out
+
     def uniform_comb(self, bank, target, seed, stream_id):
         b = np.ascontiguousarray(bank, PARTICLE_DT)
         out = np.zeros(target, PARTICLE_DT)

@@ -217,3 +217,40 @@ def test_losm_cached_factorization_is_identical(engine, I, seed):
     mx = C.c_double(0.0)
     rc = f(engine._h, I, seed, C.byref(mx))
     assert rc == 0, (rc, mx.value)
+
+
+def test_fourier_lowpass_matches_reference_filter(engine, oracle):
+    """hww_fourier's filter on the device: bit-identical to the C restatement
+    (itself pinned to the reference, tests/test_oracle_pin.py)."""
+    import ctypes as C
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    oracle.lib.orc_fourier_lowpass.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32,
+                                               C.POINTER(C.c_double)]
+    rng = np.random.default_rng(8)
+    for M, cut in [(1, 0), (2, 0), (37, 5), (400, 30), (401, 30), (64, 40)]:
+        g = np.ascontiguousarray(rng.standard_normal(M) * np.exp(-np.linspace(-3, 3, M) ** 2))
+        o = np.zeros(M)
+        assert oracle.lib.orc_fourier_lowpass(dp(g), M, cut, dp(o)) == 0
+        assert engine.fourier_lowpass(g, cut).tobytes() == o.tobytes(), (M, cut)
+
+
+def test_fourier_driver_matches_oracle(oracle):
+    """mode hww_fourier end to end in exact mode (the filter runs inside the
+    device LOSM update, twiddles from the host libm)."""
+    kw = dict(histories_per_step=3000, rho=3.0, fourier_cutoff=12, cells=80, x_min=-10.0,
+              x_max=10.0, t_end=2.0, time_steps=4, seed=4)
+    from oracle.bind import make_config
+    od = DriverRun(oracle, make_config(mode="hww_fourier", sigma_t=1.0, sigma_s=0.9,
+                                       sigma_f=0.0, nu_f=0.0, speed=1.0, **kw))
+    d = hw.Driver(hw.RunConfig(mode="hww_fourier", material=hw.Material(1.0, 0.9, 0.0, 0.0, 1.0),
+                               **kw))
+    for s in range(1, kw["time_steps"] + 1):
+        o, oarr = od.step()
+        rec = d.step()
+        arr = d.arrays()
+        ints = [o.segments, o.census_size, o.histories, o.comb_in, o.comb_out,
+                o.updates_applied, o.hybrid_solve_failed, o.n_thresholds, o.sigma_valid,
+                o.has_windows, o.has_hybrid]
+        _check_step(rec, arr, ints, [getattr(o.counters, n) for n in COUNTER_U],
+                    [o.counters.leakage_weight, o.counters.aborted_weight], oarr)
+    census_equal(d.bank(), od.bank(), weights_tol=1e-12)

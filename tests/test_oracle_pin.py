@@ -180,3 +180,36 @@ def test_oracle_matches_live_reference(oracle, seed):
     assert np.array_equal(tro, trr)
     for f in SEG_FIELDS:
         assert np.array_equal(getattr(to, f), getattr(tr_, f)), f
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built (no /root/reference)")
+def test_oracle_fourier_matches_live_reference(oracle):
+    """hww_fourier's filter (filters.cpp:26-52) restated in C: bit-identical."""
+    R = Reference()
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    L = oracle.lib
+    L.orc_fourier_lowpass.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32,
+                                      C.POINTER(C.c_double)]
+    R.lib.hwwref_fourier_lowpass.argtypes = L.orc_fourier_lowpass.argtypes
+    rng = np.random.default_rng(3)
+    for M, cut in [(1, 0), (2, 0), (37, 5), (201, 30), (402, 30), (64, 40)]:
+        g = np.ascontiguousarray(rng.standard_normal(M) * np.exp(-np.linspace(-3, 3, M) ** 2))
+        o, r = np.zeros(M), np.zeros(M)
+        assert L.orc_fourier_lowpass(dp(g), M, cut, dp(o)) == 0
+        assert R.lib.hwwref_fourier_lowpass(dp(g), M, cut, dp(r)) == 0
+        assert o.tobytes() == r.tobytes(), (M, cut)
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built (no /root/reference)")
+def test_oracle_fourier_driver_matches_live_reference(oracle):
+    """A short hww_fourier run: oracle driver == reference driver, bit for bit."""
+    from oracle.bind import DriverRun, make_config
+    cfg = make_config(mode="hww_fourier", histories_per_step=1500, rho=3.0, fourier_cutoff=12,
+                      cells=80, x_min=-10.0, x_max=10.0, t_end=1.5, time_steps=3, seed=4,
+                      sigma_t=1.0, sigma_s=0.9, sigma_f=0.0, nu_f=0.0, speed=1.0)
+    a, b = DriverRun(oracle, cfg), DriverRun(Reference(), cfg)
+    for _ in range(3):
+        (ra, xa), (rb, xb) = a.step(), b.step()
+        for k in xa:
+            assert np.array_equal(xa[k], xb[k], equal_nan=True), k
+        assert ra.counters.collisions == rb.counters.collisions
