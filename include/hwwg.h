@@ -182,6 +182,16 @@ typedef struct {
   double t_end;
   int32_t threads; /* accepted for config-file parity; unused */
   int32_t host_bank; /* 1: bank round-trips through host memory each step (e2e) */
+  /* Config-3 extensions (absent from the reference driver,
+   * DESIGN.md "Config-3 features"): */
+  int32_t n_regions;         /* 0: every cell takes the material above */
+  int32_t no_pulse;          /* 1: no point pulse at t = 0 */
+  double region_x_hi[8];     /* cell i takes the first region with centre < x_hi */
+  double region_mat[8][5];   /* sigma_t, sigma_s, sigma_f, nu_f, speed per region */
+  double vol_x_lo, vol_x_hi; /* isotropic volumetric source box in x ... */
+  double vol_t_lo, vol_t_hi; /* ... and in t */
+  double vol_rate;           /* emitted weight per unit time (same normalisation as strength) */
+  uint64_t vol_histories;    /* particles sampled in every step the box overlaps */
 } hwwg_run_config;
 
 /* == hww::StepRecord scalars (proj/include/hww/driver.hpp:41-56). */

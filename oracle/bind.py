@@ -46,7 +46,12 @@ class Config(C.Structure):
         ("sigma_t", C.c_double), ("sigma_s", C.c_double), ("sigma_f", C.c_double),
         ("nu_f", C.c_double), ("speed", C.c_double), ("x_min", C.c_double),
         ("x_max", C.c_double), ("cells", C.c_int32), ("time_steps", C.c_int32),
-        ("t_end", C.c_double), ("threads", C.c_int32), ("pad_", C.c_int32)]
+        ("t_end", C.c_double), ("threads", C.c_int32), ("pad_", C.c_int32),
+        # config-3 extensions (oracle only; the reference shim reads the prefix)
+        ("n_regions", C.c_int32), ("no_pulse", C.c_int32), ("region_x_hi", C.c_double * 8),
+        ("region_mat", (C.c_double * 5) * 8), ("vol_x_lo", C.c_double), ("vol_x_hi", C.c_double),
+        ("vol_t_lo", C.c_double), ("vol_t_hi", C.c_double), ("vol_rate", C.c_double),
+        ("vol_histories", C.c_uint64)]
 
 
 class StepOut(C.Structure):
@@ -144,6 +149,15 @@ def make_config(**kw) -> Config:
             c.n_fractions = len(v)
             for i, f in enumerate(v):
                 c.fractions[i] = f
+        elif k == "regions":  # [(x_hi, (sigma_t, sigma_s, sigma_f, nu_f, speed)), ...]
+            c.n_regions = len(v)
+            for i, (xh, m) in enumerate(v):
+                c.region_x_hi[i] = xh
+                for j in range(5):
+                    c.region_mat[i][j] = m[j]
+        elif k == "vol":  # (x_lo, x_hi, t_lo, t_hi, rate, histories)
+            (c.vol_x_lo, c.vol_x_hi, c.vol_t_lo, c.vol_t_hi, c.vol_rate,
+             c.vol_histories) = v
         else:
             setattr(c, k, v)
     return c

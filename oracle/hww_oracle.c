@@ -174,6 +174,38 @@ void orc_pulse_source(uint64_t seed, uint64_t histories, double x0, double stren
   }
 }
 
+/* Config-3 extension (the reference driver has
+ * no volumetric source): n particles of the isotropic source box [x_lo, x_hi] x
+ * [ta, tb], one sequential source stream per step (stream (step, 0, source));
+ * per particle x, then t, then mu; weight rate * (tb - ta) * H_cfg / n. */
+void orc_volume_source(uint64_t seed, int step, uint64_t n, double x_lo, double x_hi, double ta,
+                       double tb, double rate, uint64_t h_cfg, orc_particle* out) {
+  orc_rng r;
+  rng_init(&r, seed, orc_stream_id((uint64_t)step, 0, P_SOURCE));
+  const double w = rate * (tb - ta) * (double)h_cfg / (double)n;
+  for (uint64_t h = 0; h < n; ++h) {
+    out[h].x = x_lo + (x_hi - x_lo) * rng_uniform(&r);
+    out[h].t = ta + (tb - ta) * rng_uniform(&r);
+    out[h].mu = rng_pm1(&r);
+    out[h].w = w;
+  }
+}
+
+/* The LOSM source q_i of a step (losm.cpp:101-103 pass-through): the box's
+ * emission integrated over cell i, averaged over the step:
+ * rate * ((tb - ta) / dt) * |cell_i n [x_lo, x_hi]| / (x_hi - x_lo). */
+void orc_volume_q(const double* edges, int I, double x_lo, double x_hi, double ta, double tb,
+                  double dt, double rate, double* q) {
+  const double tfrac = (tb - ta) / dt;
+  const double bw = x_hi - x_lo;
+  for (int i = 0; i < I; ++i) {
+    const double lo = edges[i] > x_lo ? edges[i] : x_lo;
+    const double hi = edges[i + 1] < x_hi ? edges[i + 1] : x_hi;
+    const double len = hi > lo ? hi - lo : 0.0;
+    q[i] = rate * tfrac * len / bw;
+  }
+}
+
 /* --------------------------------------------------------------- bank --- */
 static int bank_push(orc_bank* b, const orc_particle* p) {
   if (b->n == b->cap) {
@@ -936,6 +968,7 @@ typedef struct {
   double *r_centers, *r_hybrid;
   uint64_t* r_tracks;
   int r_has_centers, r_has_hybrid;
+  double* q_step; /* volumetric-source LOSM q of the current step, or NULL */
 } orc_driver;
 
 static double now_s(void) {
@@ -1000,10 +1033,26 @@ static int validate(const orc_config* c) {
   if (c->mode == 4 && c->fourier_cutoff < 0) { set_err("fourier_cutoff must be >= 0"); return -1; }
   if (c->batches < 2) { set_err("batches must be >= 2"); return -1; }
   if (!(c->x_min < c->x_max) || c->cells < 1 || !(c->t_end > 0.0) || c->time_steps < 1 ||
-      !(c->strength > 0.0) || c->x0 < c->x_min || c->x0 > c->x_max) {
+      (!c->no_pulse && (!(c->strength > 0.0) || c->x0 < c->x_min || c->x0 > c->x_max))) {
     set_err("invalid geometry/time/source");
     return -1;
   }
+  if (c->n_regions < 0 || c->n_regions > 8) { set_err("n_regions must lie in [0, 8]"); return -1; }
+  for (int r = 0; r < c->n_regions; ++r) {
+    const double* m = c->region_mat[r];
+    if (!(m[0] > 0) || m[1] < 0 || m[1] + m[2] > m[0] || m[2] < 0 || m[3] < 0 || !(m[4] > 0) ||
+        (r > 0 && !(c->region_x_hi[r] > c->region_x_hi[r - 1]))) {
+      set_err("invalid material region");
+      return -1;
+    }
+  }
+  if (c->vol_rate > 0.0 && (!(c->vol_x_lo < c->vol_x_hi) || c->vol_x_lo < c->x_min ||
+                            c->vol_x_hi > c->x_max || !(c->vol_t_lo < c->vol_t_hi) ||
+                            c->vol_histories < 1)) {
+    set_err("invalid volumetric source");
+    return -1;
+  }
+  if (c->no_pulse && !(c->vol_rate > 0.0)) { set_err("no source at all"); return -1; }
   return 0;
 }
 
@@ -1030,10 +1079,22 @@ void* orc_driver_create(const orc_config* c) {
     d->mats[i].sigma_f = c->sigma_f;
     d->mats[i].nu_f = c->nu_f;
     d->mats[i].speed = c->speed;
+    if (c->n_regions > 0) { /* first region whose upper bound exceeds the cell centre */
+      const double xc = 0.5 * (d->edges[i] + d->edges[i + 1]);
+      int r = 0;
+      while (r < c->n_regions - 1 && !(xc < c->region_x_hi[r])) ++r;
+      d->mats[i].sigma_t = c->region_mat[r][0];
+      d->mats[i].sigma_s = c->region_mat[r][1];
+      d->mats[i].sigma_f = c->region_mat[r][2];
+      d->mats[i].nu_f = c->region_mat[r][3];
+      d->mats[i].speed = c->region_mat[r][4];
+    }
   }
-  d->bank.cap = d->bank.n = c->histories_per_step;
-  d->bank.data = (orc_particle*)malloc(sizeof(orc_particle) * d->bank.n);
-  orc_pulse_source(c->seed, c->histories_per_step, c->x0, c->strength, d->bank.data);
+  if (!c->no_pulse) {
+    d->bank.cap = d->bank.n = c->histories_per_step;
+    d->bank.data = (orc_particle*)malloc(sizeof(orc_particle) * d->bank.n);
+    orc_pulse_source(c->seed, c->histories_per_step, c->x0, c->strength, d->bank.data);
+  }
   d->next_step = 1;
   double** arrs[] = {&d->prev_phi_census, &d->prev_current, &d->prev_closure,
                      &d->prev_phi_track, &d->prev_grid, &d->r_phi_track, &d->r_sigma,
@@ -1073,7 +1134,7 @@ static int hybrid_windows(orc_driver* d, const hyb_inputs* prev, int implicit,
   double* J_out = (double*)malloc(sizeof(double) * (size_t)(I + 1));
   const int rc = orc_assemble_solve(I, d->edges, d->mats, prev->phi, prev->J, 0.0, 0.0,
                                     implicit, F_now, PL_now, PR_now, prev->F, prev->PL,
-                                    prev->PR, theta, dt, NULL, phi_out, J_out);
+                                    prev->PR, theta, dt, d->q_step, phi_out, J_out);
   int ok = 1;
   if (rc == 0) {
     memcpy(phi_hybrid, phi_out + 1, sizeof(double) * (size_t)I);
@@ -1115,7 +1176,10 @@ int orc_driver_step(void* h, orc_step_out* out) {
   /* population control, driver.cpp:111-129 */
   orc_bank source = {0};
   const double bank_cap = c->comb_overflow_factor * (double)target;
-  if (c->comb_overflow_factor <= 1.0 || (double)d->bank.n > bank_cap) {
+  if (d->bank.n == 0 && (c->no_pulse || c->vol_rate > 0.0)) {
+    /* volumetric-source runs before any census exists: nothing to comb */
+    out->comb_in = out->comb_out = 0;
+  } else if (c->comb_overflow_factor <= 1.0 || (double)d->bank.n > bank_cap) {
     if (d->bank.n == 0) {
       set_err("cannot comb an empty bank");
       return -1;
@@ -1136,6 +1200,22 @@ int orc_driver_step(void* h, orc_step_out* out) {
     source = d->bank;
     memset(&d->bank, 0, sizeof d->bank);
   }
+  /* volumetric source particles born in this step follow the combed census */
+  double* qv = NULL;
+  if (c->vol_rate > 0.0) {
+    const double ta = out->t_begin > c->vol_t_lo ? out->t_begin : c->vol_t_lo;
+    const double tb = out->t_end < c->vol_t_hi ? out->t_end : c->vol_t_hi;
+    if (tb > ta) {
+      const uint64_t n0 = source.n, nv = c->vol_histories;
+      source.data = (orc_particle*)realloc(source.data, sizeof(orc_particle) * (n0 + nv));
+      source.n = source.cap = n0 + nv;
+      orc_volume_source(c->seed, step, nv, c->vol_x_lo, c->vol_x_hi, ta, tb, c->vol_rate,
+                        c->histories_per_step, source.data + n0);
+      qv = (double*)malloc(sizeof(double) * (size_t)I);
+      orc_volume_q(d->edges, I, c->vol_x_lo, c->vol_x_hi, ta, tb, dt, c->vol_rate, qv);
+    }
+  }
+  d->q_step = qv;
   const uint64_t H = source.n;
 
   /* windows, driver.cpp:136-167 */
@@ -1156,8 +1236,10 @@ int orc_driver_step(void* h, orc_step_out* out) {
     }
   } else if (hybrid) {
     if (step == 1) { /* analytic_pulse_inputs, driver.cpp:51-61 */
-      const int cell = mesh_locate(&d->mesh, c->x0);
-      fin.phi[cell + 1] = c->speed * c->strength / d->mesh.widths[cell];
+      if (!c->no_pulse) {
+        const int cell = mesh_locate(&d->mesh, c->x0);
+        fin.phi[cell + 1] = c->speed * c->strength / d->mesh.widths[cell];
+      }
     } else { /* hybrid_inputs_from_report, driver.cpp:41-49 */
       extrap(d->prev_phi_census, I, fin.phi);
       extrap(d->prev_closure, I, fin.F);
@@ -1244,6 +1326,8 @@ int orc_driver_step(void* h, orc_step_out* out) {
     free(tl.block);
     orc_bank_free(&census);
     orc_bank_free(&source);
+    free(d->q_step);
+    d->q_step = NULL;
     free(centers);
     free(fin.phi); free(fin.J); free(fin.F);
     return -1;
@@ -1300,6 +1384,8 @@ int orc_driver_step(void* h, orc_step_out* out) {
   }
   free(tl.block);
   orc_bank_free(&source);
+  free(d->q_step);
+  d->q_step = NULL;
   free(centers);
   free(fin.phi); free(fin.J); free(fin.F);
   ++d->next_step;

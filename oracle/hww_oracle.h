@@ -72,6 +72,16 @@ typedef struct {
   double t_end;
   int32_t threads;
   int32_t pad_;
+  /* Config-3 extensions (absent from the reference driver,
+   * DESIGN.md "Config-3 features"): */
+  int32_t n_regions;         /* 0: every cell takes the material above */
+  int32_t no_pulse;          /* 1: no point pulse at t = 0 */
+  double region_x_hi[8];     /* cell i takes the first region with centre < x_hi */
+  double region_mat[8][5];   /* sigma_t, sigma_s, sigma_f, nu_f, speed per region */
+  double vol_x_lo, vol_x_hi; /* isotropic volumetric source box in x ... */
+  double vol_t_lo, vol_t_hi; /* ... and in t */
+  double vol_rate;           /* emitted weight per unit time (same normalisation as strength) */
+  uint64_t vol_histories;    /* particles sampled in every step the box overlaps */
 } orc_config;
 
 typedef struct {
@@ -150,6 +160,10 @@ int orc_edge_currents(const double* census_current, int32_t cells, const double*
 /* filters.cpp:11-24 */
 int orc_moving_average(const double* g, int32_t n, int32_t k, double* out);
 int orc_fourier_lowpass(const double* g, int32_t n, int32_t cutoff, double* out);
+void orc_volume_source(uint64_t seed, int step, uint64_t n, double x_lo, double x_hi, double ta,
+                       double tb, double rate, uint64_t h_cfg, orc_particle* out);
+void orc_volume_q(const double* edges, int I, double x_lo, double x_hi, double ta, double tb,
+                  double dt, double rate, double* q);
 /* ww.cpp:8-32; returns 1 on uniform fallback */
 int orc_build_centers(const double* phi, int32_t n, double eps_min, double rho,
                       double* centers);

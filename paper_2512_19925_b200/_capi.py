@@ -87,7 +87,11 @@ class RunConfigC(C.Structure):
         ("sigma_t", C.c_double), ("sigma_s", C.c_double), ("sigma_f", C.c_double),
         ("nu_f", C.c_double), ("speed", C.c_double), ("x_min", C.c_double),
         ("x_max", C.c_double), ("cells", C.c_int32), ("time_steps", C.c_int32),
-        ("t_end", C.c_double), ("threads", C.c_int32), ("host_bank", C.c_int32)]
+        ("t_end", C.c_double), ("threads", C.c_int32), ("host_bank", C.c_int32),
+        ("n_regions", C.c_int32), ("no_pulse", C.c_int32), ("region_x_hi", C.c_double * 8),
+        ("region_mat", (C.c_double * 5) * 8), ("vol_x_lo", C.c_double), ("vol_x_hi", C.c_double),
+        ("vol_t_lo", C.c_double), ("vol_t_hi", C.c_double), ("vol_rate", C.c_double),
+        ("vol_histories", C.c_uint64)]
 
 
 class StepRecordC(C.Structure):

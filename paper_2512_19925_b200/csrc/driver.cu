@@ -119,6 +119,10 @@ struct hwwg_driver {
   int smem_mode = 1;  // fast tallies (FastArgs::smem_tallies) outside the cold start
   int scramble = 1;   // FastArgs::scramble outside the cold start
   int agg_all = 0;    // HWWG_FAST_AGG=1: warp-aggregated tallies in every step
+  // config-3 volumetric source: the step's LOSM q (device) and particle staging
+  DevBuf<double> q_dev;
+  const double* q_step = nullptr;
+  DevBuf<hwwg_particle> vol_dev;
   // e2e (host_bank) Philox runs: the bank in host memory is already combed
   bool host_pre_combed = false;
   uint64_t pre_comb_in = 0;
@@ -223,6 +227,14 @@ void init_driver(hwwg_driver* d) {
   for (int e = 0; e <= I; ++e) edges[e] = c.x_min + e * w;
   edges[I] = c.x_max;
   std::vector<hwwg_material> mats(I, hwwg_material{c.sigma_t, c.sigma_s, c.sigma_f, c.nu_f, c.speed});
+  if (c.n_regions > 0)  // config-3 regions: the first whose upper bound exceeds the cell centre
+    for (int i = 0; i < I; ++i) {
+      const double xc = 0.5 * (edges[i] + edges[i + 1]);
+      int r = 0;
+      while (r < c.n_regions - 1 && !(xc < c.region_x_hi[r])) ++r;
+      const double* m = c.region_mat[r];
+      mats[i] = hwwg_material{m[0], m[1], m[2], m[3], m[4]};
+    }
   std::string why;
   if (!d->prob.set(edges.data(), I, mats.data(), d->stream, why)) throw ApiError(HWWG_EINVAL, why);
   d->layers.resize(c.time_steps + 1);
@@ -280,9 +292,10 @@ void init_driver(hwwg_driver* d) {
   d->comb_mem.reserve(4);
 
   // source sampling (driver.cpp:309-316) on the host: one sequential stream
-  std::vector<hwwg_particle> src(c.histories_per_step);
-  sample_pulse_source_host(c.seed, c.histories_per_step, c.x0,
-                           c.strength * (double)c.histories_per_step, 0.0, src.data());
+  std::vector<hwwg_particle> src(c.no_pulse ? 0 : c.histories_per_step);
+  if (!c.no_pulse)
+    sample_pulse_source_host(c.seed, c.histories_per_step, c.x0,
+                             c.strength * (double)c.histories_per_step, 0.0, src.data());
   if (d->world > 1) {  // this rank's shard of the step-1 histories
     uint64_t lo, hi;
     hwwg_shard_range(c.histories_per_step, d->rank, d->world, &lo, &hi);
@@ -313,7 +326,7 @@ void init_driver(hwwg_driver* d) {
     d->census_hwm = 64 * local_target + 4096;
     d->fcensus.reserve(d->census_hwm);
     d->fbank.reserve(d->census_hwm);
-    d->fsrc.reserve(std::max<uint64_t>(d->target, 1));
+    d->fsrc.reserve(std::max<uint64_t>(d->target + (c.vol_rate > 0.0 ? c.vol_histories : 0), 1));
     d->comb_mem.reserve(4 + d->census_hwm);
     d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
     if (c.host_bank) d->bank.reserve(d->census_hwm);
@@ -479,7 +492,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (d->fast) {
       // a pre-combed bank (see the step end) is already the step's source
       FastBankBuf& dst = d->host_pre_combed ? d->fsrc : d->fbank;
-      dst.reserve(d->bank_n);
+      dst.reserve(d->bank_n + (c.vol_rate > 0.0 ? c.vol_histories : 0));
       launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, dst.view(), 0, s);
       ++d->launches;
     }
@@ -488,8 +501,16 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // ---- population control (driver.cpp:111-129)
   const double bank_cap = c.comb_overflow_factor * (double)d->target;
   const bool do_comb = c.comb_overflow_factor <= 1.0 || (double)d->bank_n > bank_cap;
+  // config-3 runs: room after the source for the step's volumetric particles
+  const uint64_t vol_cap = c.vol_rate > 0.0 ? c.vol_histories : 0;
   uint64_t H;
-  if (d->fast && d->world > 1) {
+  if (d->bank_n == 0 && (c.no_pulse || c.vol_rate > 0.0)) {
+    // volumetric-source run before any census exists: nothing to comb
+    H = 0;
+    rec->comb_in = rec->comb_out = 0;
+    HWWG_CUDA(cudaMemsetAsync(d->comb_mem.p, 0, 4 * sizeof(double), s));
+    if (!d->fast) d->source.reserve(std::max<uint64_t>(vol_cap, 1));
+  } else if (d->fast && d->world > 1) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
     multi_gpu_comb(d, step, s);
     H = d->target;
@@ -502,7 +523,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   } else if (d->fast) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
-    d->fsrc.reserve(d->target);
+    d->fsrc.reserve(d->target + vol_cap);
     d->comb_mem.reserve(4 + d->bank_n);
     const size_t tb = fast_comb_temp_bytes(d->bank_n);
     d->comb_temp.reserve(tb);
@@ -526,7 +547,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     rec->comb_out = d->target;
   } else if (do_comb) {
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
-    d->source.reserve(d->target);
+    d->source.reserve(d->target + vol_cap);
     d->comb_mem.reserve(4 + d->bank_n);
     CombArgs a{};
     a.bank = d->bank.p;
@@ -544,13 +565,49 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     rec->comb_in = d->bank_n;
     rec->comb_out = d->target;
   } else {
-    d->source.reserve(std::max<uint64_t>(d->bank_n, 1));
+    d->source.reserve(std::max<uint64_t>(d->bank_n + vol_cap, 1));
     HWWG_CUDA(cudaMemcpyAsync(d->source.p, d->bank.p, d->bank_n * sizeof(hwwg_particle),
                               cudaMemcpyDeviceToDevice, s));
     k_bank_weight<<<1, 1, 0, s>>>(d->bank.p, d->bank_n, d->comb_mem.p);
     ++d->launches;
     H = d->bank_n;
     rec->comb_in = rec->comb_out = d->bank_n;
+  }
+
+  // ---- config-3 volumetric source: this step's particles follow the combed
+  // census (histories [H, H + n)); the LOSM gets the step's q
+  d->q_step = nullptr;
+  if (c.vol_rate > 0.0) {
+    const double ta = std::max(rec->t_begin, c.vol_t_lo);
+    const double tb = std::min(rec->t_end, c.vol_t_hi);
+    if (tb > ta) {
+      const uint64_t nv = c.vol_histories;
+      std::vector<hwwg_particle> vh(nv);
+      sample_volume_source_host(c.seed, step, nv, c.vol_x_lo, c.vol_x_hi, ta, tb, c.vol_rate,
+                                c.histories_per_step, vh.data());
+      std::vector<double> qh(I);
+      volume_q_host(d->prob.edges.data(), I, c.vol_x_lo, c.vol_x_hi, ta, tb, dt, c.vol_rate,
+                    qh.data());
+      d->q_dev.reserve(I);
+      HWWG_CUDA(cudaMemcpyAsync(d->q_dev.p, qh.data(), I * 8, cudaMemcpyHostToDevice, s));
+      d->q_step = d->q_dev.p;
+      if (d->fast) {
+        d->vol_dev.reserve(nv);
+        HWWG_CUDA(cudaMemcpyAsync(d->vol_dev.p, vh.data(), nv * sizeof(hwwg_particle),
+                                  cudaMemcpyHostToDevice, s));
+        const FastBank f = d->fsrc.view();
+        launch_aos_to_fast(d->vol_dev.p, nv, d->prob.view, FastBank{f.xm + H, f.wt + H, f.meta + H},
+                           H, s);
+        ++d->launches;
+      } else {
+        HWWG_CUDA(cudaMemcpyAsync(d->source.p + H, vh.data(), nv * sizeof(hwwg_particle),
+                                  cudaMemcpyHostToDevice, s));
+      }
+      // pageable sources: the copies complete before this returns to the loop
+      HWWG_CUDA(cudaStreamSynchronize(s));
+      rec->h2d_bytes += nv * sizeof(hwwg_particle) + I * 8;
+      H += nv;
+    }
   }
 
   // backup of the windows so an overflowing step can be replayed exactly
@@ -637,14 +694,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.fourier_tab_cell = c.mode == 4 ? d->ftab_cell.p : nullptr;
       a.fourier_tab_edge = c.mode == 4 ? d->ftab_edge.p : nullptr;
       a.fourier_cutoff = c.fourier_cutoff;
+      a.q = d->q_step;
       a.mode = 0;
       a.fast_solve = d->fast ? 1 : 0;
       a.refactor = d->need_refactor(theta_eff, dt);
       a.analytic = step == 1;
-      if (step == 1) {
+      if (step == 1 && !c.no_pulse) {
         const int cell = locate_host(d->prob.edges, c.x0);
         a.pulse_cell = cell;
         a.pulse_value = c.speed * c.strength / (d->prob.edges[cell + 1] - d->prob.edges[cell]);
+      } else if (step == 1) {  // no pulse: the analytic initial state is zero
+        a.pulse_cell = -2;
+        a.pulse_value = 0.0;
       }
       a.s = d->lo;
       a.s.rep_phi_census = d->rep(prev, 2);
@@ -790,6 +851,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.fourier_tab_cell = c.mode == 4 ? d->ftab_cell.p : nullptr;
       a.fourier_tab_edge = c.mode == 4 ? d->ftab_edge.p : nullptr;
       a.fourier_cutoff = c.fourier_cutoff;
+      a.q = d->q_step;
       a.mode = 1;
       a.fast_solve = d->fast ? 1 : 0;
       a.refactor = d->need_refactor(theta_eff, dt);
@@ -1119,6 +1181,10 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     delete d;
     return fail(HWWG_EINVAL, "multi-GPU runs need HWWG_RNG_PHILOX and 0 <= rank < world "
                              "(exact mode replays one sequential comb)");
+  }
+  if (d->world > 1 && cfg->vol_rate > 0.0) {
+    delete d;
+    return fail(HWWG_EINVAL, "the volumetric source runs on one GPU");
   }
   if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
     delete d;

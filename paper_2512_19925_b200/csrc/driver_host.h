@@ -16,6 +16,12 @@ namespace hwwg {
 void sample_pulse_source_host(uint64_t seed, uint64_t histories, double x0, double total_weight,
                               double t0, hwwg_particle* out);
 uint64_t stream_id_host(uint64_t step, uint64_t history, uint64_t purpose);
+// Config-3 volumetric source particles of one step and the step's LOSM q.
+void sample_volume_source_host(uint64_t seed, int step, uint64_t n, double x_lo, double x_hi,
+                               double ta, double tb, double rate, uint64_t h_cfg,
+                               hwwg_particle* out);
+void volume_q_host(const double* edges, int I, double x_lo, double x_hi, double ta, double tb,
+                   double dt, double rate, double* q);
 // batch_of (tally.hpp:130-134) on the host.
 int batch_of_host(uint64_t h, uint64_t H, int B);
 // Mesh1D::locate (mesh.cpp:26-40) on the host; -1 outside.

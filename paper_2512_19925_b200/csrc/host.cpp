@@ -25,6 +25,38 @@ void sample_pulse_source_host(uint64_t seed, uint64_t histories, double x0, doub
   for (uint64_t h = 0; h < histories; ++h) out[h] = hwwg_particle{x0, r.uniform_pm1(), w, t0};
 }
 
+// Config-3 volumetric source: n particles of the
+// isotropic box [x_lo, x_hi] x [ta, tb] from the step's source stream (step, 0,
+// source); per particle x, then t, then mu; w = rate * (tb - ta) * h_cfg / n.
+// Same arithmetic as oracle/hww_oracle.c orc_volume_source.
+void sample_volume_source_host(uint64_t seed, int step, uint64_t n, double x_lo, double x_hi,
+                               double ta, double tb, double rate, uint64_t h_cfg,
+                               hwwg_particle* out) {
+  Xoshiro r;
+  r.seed(seed, stream_id((uint64_t)step, 0, kSource));
+  const double w = rate * (tb - ta) * (double)h_cfg / (double)n;
+  for (uint64_t h = 0; h < n; ++h) {
+    const double x = x_lo + (x_hi - x_lo) * r.uniform();
+    const double t = ta + (tb - ta) * r.uniform();
+    const double mu = r.uniform_pm1();
+    out[h] = hwwg_particle{x, mu, w, t};
+  }
+}
+
+// The step's LOSM source q_i (losm.cpp:101-103 pass-through): the box's emission
+// over cell i averaged over the step (orc_volume_q).
+void volume_q_host(const double* edges, int I, double x_lo, double x_hi, double ta, double tb,
+                   double dt, double rate, double* q) {
+  const double tfrac = (tb - ta) / dt;
+  const double bw = x_hi - x_lo;
+  for (int i = 0; i < I; ++i) {
+    const double lo = edges[i] > x_lo ? edges[i] : x_lo;
+    const double hi = edges[i + 1] < x_hi ? edges[i + 1] : x_hi;
+    const double len = hi > lo ? hi - lo : 0.0;
+    q[i] = rate * tfrac * len / bw;
+  }
+}
+
 uint64_t stream_id_host(uint64_t step, uint64_t history, uint64_t purpose) {
   return stream_id(step, history, purpose);
 }
@@ -138,8 +170,27 @@ int hwwg_validate_config(const hwwg_run_config* c, char* buf, uint64_t buf_len) 
   if (c->cells < 1) v.push_back("cells must be >= 1");
   if (!(c->t_end > 0.0)) v.push_back("t_end must be > 0");
   if (c->time_steps < 1) v.push_back("time_steps must be >= 1");
-  if (!(c->strength > 0.0)) v.push_back("source strength must be > 0");
-  if (c->x0 < c->x_min || c->x0 > c->x_max) v.push_back("source x0 must lie inside the mesh");
+  if (!c->no_pulse) {
+    if (!(c->strength > 0.0)) v.push_back("source strength must be > 0");
+    if (c->x0 < c->x_min || c->x0 > c->x_max) v.push_back("source x0 must lie inside the mesh");
+  }
+  // config-3 extensions: regions and the volumetric source
+  if (c->n_regions < 0 || c->n_regions > 8) v.push_back("n_regions must lie in [0, 8]");
+  for (int r = 0; r < c->n_regions && r < 8; ++r) {
+    const double* m = c->region_mat[r];
+    if (!(m[0] > 0) || m[1] < 0 || m[2] < 0 || m[1] + m[2] > m[0] || m[3] < 0 || !(m[4] > 0))
+      v.push_back("region " + std::to_string(r) + ": invalid material");
+    if (r > 0 && !(c->region_x_hi[r] > c->region_x_hi[r - 1]))
+      v.push_back("region upper bounds must increase");
+  }
+  if (c->vol_rate < 0.0) v.push_back("vol_rate must be >= 0");
+  if (c->vol_rate > 0.0) {
+    if (!(c->vol_x_lo < c->vol_x_hi) || c->vol_x_lo < c->x_min || c->vol_x_hi > c->x_max)
+      v.push_back("volumetric source box must be non-empty and inside the mesh");
+    if (!(c->vol_t_lo < c->vol_t_hi)) v.push_back("volumetric source window must be non-empty");
+    if (c->vol_histories < 1) v.push_back("vol_histories must be >= 1");
+  }
+  if (c->no_pulse && !(c->vol_rate > 0.0)) v.push_back("no source: no pulse and no volumetric source");
   std::string joined;
   for (size_t i = 0; i < v.size(); ++i) joined += (i ? "\n" : "") + v[i];
   if (buf && buf_len) {

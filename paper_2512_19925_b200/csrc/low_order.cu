@@ -398,13 +398,13 @@ __device__ void build_factorization(int I, const double* edges, const CellInfo* 
   __syncthreads();
 }
 
-// One solve through the cached factorization: RHS of assemble_rows (q = 0,
-// J_L = J_R = 0, as the driver calls it), the Schur RHS, the PCR levels, phi
+// One solve through the cached factorization: RHS of assemble_rows (J_L = J_R
+// = 0, as the driver calls it; q the config-3 source or null), the Schur RHS, the PCR levels, phi
 // and the currents into x (interleaved like the full system). Returns nonzero
 // when the factorization is singular.
 __device__ int solve_cached(int I, FacView F, const double* phi_prev, const double* J_prev,
                             const double* Fs, double PLs, double PRs, const double* F_prev,
-                            double theta, double* x, double* sm) {
+                            double theta, const double* q, double* x, double* sm) {
   const int N = I + 2;
   double* P = sm;       // N: moment-row RHS * inv diagonal
   double* R0 = P + N;   // N
@@ -419,7 +419,7 @@ __device__ int solve_cached(int I, FacView F, const double* phi_prev, const doub
   }
   double rb = 0.0;
   if (i < N) {
-    const double qi = 0.0;
+    const double qi = (q && i >= 1 && i <= I) ? q[i - 1] : 0.0;
     if (i == 0) rb = 2.0 * 0.0 + PLs;
     else if (i == N - 1) rb = 2.0 * 0.0 - PRs;
     else
@@ -644,12 +644,12 @@ __device__ __noinline__ void solve_and_center(const LowOrderArgs& a, const doubl
   if (ok_in && cached && !rebuild) {
     extern __shared__ double dyn[];
     const int bad = solve_cached(I, fac_view(s.fac, I), s.phi_prev, s.J_prev, Fs, PLs, PRs,
-                                 s.F_prev, a.theta, x, dyn);
+                                 s.F_prev, a.theta, a.q, x, dyn);
     LP(6);
     if (threadIdx.x == 0) status = bad ? 2 : 0;
   } else if (ok_in) {
     assemble_rows(I, a.edges, a.cells, s.phi_prev, s.J_prev, 0.0, 0.0, Fs, PLs, PRs, s.F_prev,
-                  a.theta, a.dt, nullptr, lo, di, up, rh);
+                  a.theta, a.dt, a.q, lo, di, up, rh);
     __syncthreads();
     LP(5);
     if (cached) {  // (re)build: record the factorization, then solve as before

@@ -54,6 +54,7 @@ struct LowOrderArgs {
   const double* fourier_tab_cell;
   const double* fourier_tab_edge;
   int fourier_cutoff;
+  const double* q;  // config-3 volumetric source per cell (I, device) or null (losm.cpp:101-103)
   // mode 0: start-of-step lagged solve; inputs from analytic pulse (step 1) or
   //         from the previous report.  mode 1: mid-step implicit solve from the
   //         partial snapshot of the live tallies.

@@ -366,6 +366,15 @@ class RunConfig:
     threads: int = 0
     host_bank: bool = False
     out_dir: str = ""  # config.hpp:63: empty -> no file output
+    # Config-3 extensions (absent from the
+    # reference driver): material regions [(x_hi, Material), ...] (a cell takes
+    # the first region whose x_hi exceeds its centre), an isotropic volumetric
+    # source (x_lo, x_hi, t_lo, t_hi, rate) sampled with vol_histories particles
+    # in every step it overlaps, and no_pulse to drop the t = 0 point pulse.
+    regions: Sequence = ()
+    volume_source: Optional[tuple] = None
+    vol_histories: int = 0
+    no_pulse: bool = False
 
     def comb_target(self):
         return self.target_population or self.histories_per_step
@@ -389,6 +398,15 @@ class RunConfig:
         c.x_min, c.x_max, c.cells = self.x_min, self.x_max, self.cells
         c.t_end, c.time_steps, c.threads = self.t_end, self.time_steps, self.threads
         c.host_bank = 1 if self.host_bank else 0
+        c.n_regions = len(self.regions)
+        for i, (xh, m) in enumerate(list(self.regions)[:8]):
+            c.region_x_hi[i] = xh
+            for j, v in enumerate((m.sigma_t, m.sigma_s, m.sigma_f, m.nu_f, m.speed)):
+                c.region_mat[i][j] = v
+        if self.volume_source is not None:
+            (c.vol_x_lo, c.vol_x_hi, c.vol_t_lo, c.vol_t_hi, c.vol_rate) = self.volume_source
+            c.vol_histories = self.vol_histories or self.histories_per_step
+        c.no_pulse = 1 if self.no_pulse else 0
         return c
 
     @staticmethod

@@ -254,3 +254,38 @@ def test_fourier_driver_matches_oracle(oracle):
         _check_step(rec, arr, ints, [getattr(o.counters, n) for n in COUNTER_U],
                     [o.counters.leakage_weight, o.counters.aborted_weight], oarr)
     census_equal(d.bank(), od.bank(), weights_tol=1e-12)
+
+
+def _c3(H, steps, mode="hww", cells=120, nv=None):
+    """A reduced BASELINE config 3: three material regions,
+    isotropic volumetric source in x in [0,2], t in [0,1], no pulse."""
+    regions = [(10.0, (1.0, 0.5, 0.0, 0.0, 1.0)), (20.0, (10.0, 1.0, 0.0, 0.0, 1.0)),
+               (30.0, (1.0, 0.99, 0.0, 0.0, 1.0))]
+    kw = dict(histories_per_step=H, rho=4.0, seed=3, cells=cells, x_min=0.0, x_max=30.0,
+              t_end=0.5 * steps, time_steps=steps)
+    from oracle.bind import make_config
+    o = make_config(mode=mode, no_pulse=1, regions=regions, vol=(0.0, 2.0, 0.0, 1.0, 1.0, nv or H),
+                    sigma_t=1.0, sigma_s=0.5, sigma_f=0.0, nu_f=0.0, speed=1.0, **kw)
+    g = hw.RunConfig(mode=mode, no_pulse=True, volume_source=(0.0, 2.0, 0.0, 1.0, 1.0),
+                     vol_histories=nv or H, material=hw.Material(1.0, 0.5, 0.0, 0.0, 1.0),
+                     regions=[(x, hw.Material(*m)) for x, m in regions], **kw)
+    return o, g
+
+
+@pytest.mark.parametrize("mode", ["hww", "analog", "hww_ma"])
+def test_config3_driver_matches_oracle(oracle, mode):
+    """Config-3 features end to end in exact mode: regions, the volumetric
+    source appended after the combed census, the LOSM q."""
+    o_cfg, g_cfg = _c3(2000, 4, mode=mode)
+    od = DriverRun(oracle, o_cfg)
+    d = hw.Driver(g_cfg)
+    for s in range(1, 5):
+        o, oarr = od.step()
+        rec = d.step()
+        arr = d.arrays()
+        ints = [o.segments, o.census_size, o.histories, o.comb_in, o.comb_out,
+                o.updates_applied, o.hybrid_solve_failed, o.n_thresholds, o.sigma_valid,
+                o.has_windows, o.has_hybrid]
+        _check_step(rec, arr, ints, [getattr(o.counters, n) for n in COUNTER_U],
+                    [o.counters.leakage_weight, o.counters.aborted_weight], oarr)
+    census_equal(d.bank(), od.bank(), weights_tol=1e-12)

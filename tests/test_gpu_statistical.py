@@ -108,3 +108,18 @@ def test_philox_bank_and_host_round_trip():
     for r, q in zip(recs, erecs):
         assert abs(q.segments / r.segments - 1) < 0.02
         assert abs(q.census_weight / r.census_weight - 1) < 0.02
+
+
+def test_config3_philox_step1_within_batch_sigma():
+    """Config-3 (regions, volumetric source, LOSM q) in the throughput mode:
+    step-1 track flux within 3 combined batch sigma of the exact mode."""
+    from tests.test_gpu_parity import _c3
+    _, g = _c3(200_000, 1, mode="hww", cells=300)
+    ex = run(g, hw.RNG_EXACT)[0]
+    fa = run(g, hw.RNG_PHILOX)[0]
+    (re, ae), (rf, af) = ex, fa
+    assert re.histories == rf.histories == 200_000
+    m = ae["phi_track"] > 1e-3 * ae["phi_track"].max()
+    z = (af["phi_track"][m] - ae["phi_track"][m]) / np.sqrt(ae["sigma"][m] ** 2 + af["sigma"][m] ** 2)
+    assert np.mean(np.abs(z) < 3) >= 0.95, np.mean(np.abs(z) < 3)
+    assert abs(rf.census_weight / re.census_weight - 1) < 5 * (re.census_weight_sigma + rf.census_weight_sigma) / re.census_weight

@@ -213,3 +213,62 @@ def test_oracle_fourier_driver_matches_live_reference(oracle):
         for k in xa:
             assert np.array_equal(xa[k], xb[k], equal_nan=True), k
         assert ra.counters.collisions == rb.counters.collisions
+
+
+@pytest.mark.skipif(not have_reference(), reason="oracle/_ref not built (no /root/reference)")
+def test_oracle_config3_components_match_live_reference(oracle):
+    """Config-3 pieces on the reference's own components (no
+    reference driver exists, so the pin is per component): the segment
+    transport over three material regions with particles born inside the step,
+    and the LOSM assemble/solve with a source q (losm.cpp:101-103)."""
+    R = Reference()
+    I = 90
+    e = uniform_edges(0.0, 30.0, I)
+    xc = 0.5 * (e[1:] + e[:-1])
+    mats = np.zeros((I, 5))
+    for lo, hi, st, c in ((0, 10, 1.0, 0.5), (10, 20, 10.0, 0.1), (20, 30, 1.0, 0.99)):
+        sel = (xc >= lo) & (xc < hi)
+        mats[sel] = (st, c * st, 0.0, 0.0, 1.0)
+    rng = np.random.default_rng(17)
+    src = np.zeros(1500, PARTICLE_DT)
+    src["x"] = rng.uniform(0, 2, src.size)
+    src["mu"] = rng.uniform(-1, 1, src.size)
+    src["w"] = 0.25
+    src["t"] = rng.uniform(0.5, 1.0, src.size)
+    cen = np.exp(-(xc / 8) ** 2)
+    cen = cen / cen.max() * (1 - 1e-3) + 1e-3
+    to, ko, tro, co, _ = oracle.run_segment(e, mats, 0.5, 1.0, 3, 2, 1500, 20, src, 0,
+                                            centers=cen, rho=4.0, chunk=256)
+    tr_, kr, trr, cr = R.run_segment(e, mats, 0.5, 1.0, 3, 2, 1500, 20, src, 0, centers=cen,
+                                     rho=4.0)
+    assert co.tobytes() == cr.tobytes()
+    assert ko.as_dict() == kr.as_dict()
+    assert np.array_equal(tro, trr)
+    for f in SEG_FIELDS:
+        assert np.array_equal(getattr(to, f), getattr(tr_, f)), f
+
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    q = np.zeros(I)
+    oracle.lib.orc_volume_q.argtypes = [C.POINTER(C.c_double), C.c_int] + [C.c_double] * 6 + [
+        C.POINTER(C.c_double)]
+    oracle.lib.orc_volume_q(dp(e), I, 0.0, 2.0, 0.5, 1.0, 0.5, 1.0, dp(q))
+    assert abs(q.sum() - 1.0) < 1e-12 and np.all(q[xc > 2.0] == 0.0)
+    mc = np.ascontiguousarray(mats)
+    phi = np.ascontiguousarray(np.abs(rng.standard_normal(I + 2)))
+    J = np.ascontiguousarray(0.1 * rng.standard_normal(I + 1))
+    Fp = np.ascontiguousarray(0.05 * rng.standard_normal(I + 2))
+    Fn = np.ascontiguousarray(0.05 * rng.standard_normal(I + 2))
+    args = [C.c_int32, C.POINTER(C.c_double), C.c_void_p] + [C.POINTER(C.c_double)] * 2 + \
+        [C.c_double] * 2 + [C.c_int32, C.POINTER(C.c_double)] + [C.c_double] * 2 + \
+        [C.POINTER(C.c_double)] + [C.c_double] * 4 + [C.POINTER(C.c_double)] * 3
+    oracle.lib.orc_assemble_solve.argtypes = args
+    R.lib.hwwref_assemble_solve.argtypes = args
+    for implicit in (0, 1):
+        out = []
+        for fn in (oracle.lib.orc_assemble_solve, R.lib.hwwref_assemble_solve):
+            po, Jo = np.zeros(I + 2), np.zeros(I + 1)
+            assert fn(I, dp(e), mc.ctypes.data, dp(phi), dp(J), 0.0, 0.0, implicit, dp(Fn),
+                      0.01, -0.02, dp(Fp), 0.0, 0.0, 0.5, 0.5, dp(q), dp(po), dp(Jo)) == 0
+            out.append((po, Jo))
+        assert out[0][0].tobytes() == out[1][0].tobytes()
+        assert out[0][1].tobytes() == out[1][1].tobytes()
