@@ -155,12 +155,13 @@ def sum_over_ranks(x, world):
     return float(t.item())
 
 
-def cpu_baseline(histories, steps):
+def cpu_baseline(histories, steps, threads=None):
     """Reference (oracle/_ref) on this host's cores: steps 1..steps of config 2 at
-    full histories, every OpenMP thread.  Returns (segments/s, cores, sample)."""
+    full histories, every OpenMP thread (or `threads`).  Returns (segments/s,
+    cores, sample)."""
     from oracle.bind import DriverRun, Reference, baseline_config
     R = Reference()
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     R.lib.hwwref_set_threads(cores)
     d = DriverRun(R, baseline_config(2, histories=histories, time_steps=40))
     seg, tau = 0, 0.0
@@ -355,6 +356,11 @@ def run_ours(args):
                 v, cores, sample = cpu_baseline(H, args.cpu_steps)
                 line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores,
                                         "kind": "reference", "sample": sample}
+                # also one thread (the reference's OpenMP path
+                # scales poorly, so both are reported)
+                v1, _, sample1 = cpu_baseline(H, args.cpu_steps, threads=1)
+                line["cpu_baseline_1thread"] = {"value": v1, "unit": UNIT, "cores": 1,
+                                                "kind": "reference", "sample": sample1}
             except Exception as ex:  # the checker is optional on a box without it
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0,
                                         "kind": "reference", "sample": f"unavailable: {ex}"}

@@ -44,6 +44,10 @@ def test_step1_within_batch_sigma(which):
     mask = a["phi_track"] > 1e-3 * a["phi_track"].max()
     z = np.abs(a["phi_track"] - b["phi_track"])[mask] / sig[mask]
     assert np.mean(z < 3.0) >= 0.95, np.sort(z)[-10:]
+    # global chi^2 over the well-sampled cells: E[sum z^2] = n
+    # whatever the cell correlations, which only widen its spread
+    chi2 = float(np.sum(z ** 2)) / z.size
+    assert 0.4 < chi2 < 1.8, chi2
     # census weight per history (the growth law) and the segment count
     sw = np.hypot(ex[0].census_weight_sigma, fa[0].census_weight_sigma)
     assert abs(ex[0].census_weight - fa[0].census_weight) <= 4 * sw + 1e-12
