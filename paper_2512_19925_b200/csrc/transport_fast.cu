@@ -180,26 +180,90 @@ __device__ __forceinline__ bool group_leader(unsigned grp) {
   return (int)(threadIdx.x & 31) == __ffs(grp) - 1;
 }
 
+// (lanes without a contribution are singleton groups and must stay out of the
+// REDUX ops: sync reductions run once per distinct member mask)
 __device__ __forceinline__ void agg_add(double* base, int key, double v) {
   if (!__any_sync(0xffffffffu, key >= 0)) return;
   const unsigned grp = agg_group(key);
-  const double s = group_sum(grp, key >= 0 ? v : 0.0);
-  if (key >= 0 && group_leader(grp)) atomicAdd(base + key, s);
+  if (key >= 0) {
+    const double s = group_sum(grp, v);
+    if (group_leader(grp)) atomicAdd(base + key, s);
+  }
 }
 
 __device__ __forceinline__ void agg_add3(double* b0, double* b1, double* b2, int key, double v0,
                                          double v1, double v2) {
   if (!__any_sync(0xffffffffu, key >= 0)) return;
   const unsigned grp = agg_group(key);
-  const bool has = key >= 0;
-  const double s0 = group_sum(grp, has ? v0 : 0.0);
-  const double s1 = group_sum(grp, has ? v1 : 0.0);
-  const double s2 = group_sum(grp, has ? v2 : 0.0);
-  if (has && group_leader(grp)) {
-    atomicAdd(b0 + key, s0);
-    atomicAdd(b1 + key, s1);
-    atomicAdd(b2 + key, s2);
+  if (key >= 0) {
+    const double s0 = group_sum(grp, v0);
+    const double s1 = group_sum(grp, v1);
+    const double s2 = group_sum(grp, v2);
+    if (group_leader(grp)) {
+      atomicAdd(b0 + key, s0);
+      atomicAdd(b1 + key, s1);
+      atomicAdd(b2 + key, s2);
+    }
   }
+}
+
+// Census scores of one trip, summed over runs of census lanes with equal
+// (batch slot, cell) in lane order, then one set of adds per run. Split copies
+// that reach census without colliding are identical and were handed to
+// adjacent lanes, and every census lane of a warp usually shares the batch
+// slot, so per-lane CAS loops on these addresses serialise (measured: about
+// half of the steady-state transport time). A segmented Hillis-Steele scan
+// over the warp (non-census lanes carry zeros) costs a fixed 5 steps.
+__device__ __forceinline__ void census_runs(double* cphi, double* cJ, double* cF, double* cwb,
+                                            int cell, int b, double v0, double v1, double v2,
+                                            double v3) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const bool c = cell >= 0;
+  const unsigned cm = __ballot_sync(full, c);
+  if (!cm) return;
+  const int key = c ? (b << 16) | cell : -1;  // cell < 2^16 in this mode
+  const unsigned below = cm & ((1u << lane) - 1u);
+  const int prev = below ? 31 - __clz(below) : lane;
+  const int pkey = __shfl_sync(full, key, prev);
+  const bool head = c && (prev == lane || pkey != key);
+  const unsigned heads = __ballot_sync(full, head);
+  const unsigned upto = (2u << lane) - 1u;  // lanes 0..lane (all 32 for lane 31)
+  const unsigned hb = heads & upto;
+  const int start = hb ? 31 - __clz(hb) : 0;
+  double s0 = c ? v0 : 0.0, s1 = c ? v1 : 0.0, s2 = c ? v2 : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t0 = __shfl_up_sync(full, s0, o);
+    const double t1 = __shfl_up_sync(full, s1, o);
+    const double t2 = __shfl_up_sync(full, s2, o);
+    if (lane - o >= start) {
+      s0 += t0;
+      s1 += t1;
+      s2 += t2;
+    }
+  }
+  const unsigned above = cm & ~upto;  // census lanes after this one
+  const int next = above ? __ffs(above) - 1 : -1;
+  if (c && (next < 0 || ((heads >> next) & 1u))) {  // last census lane of its run
+    atomicAdd(cphi + cell, s0);
+    atomicAdd(cJ + cell, s1);
+    atomicAdd(cF + cell, s2);
+  }
+  // the census weight by batch: runs keyed by the batch slot alone (usually one
+  // run per warp: all its census lanes hold histories of one batch)
+  const int pb = __shfl_sync(full, b, prev);
+  const bool hb_head = c && (prev == lane || pb != b);
+  const unsigned bheads = __ballot_sync(full, hb_head);
+  const unsigned bhb = bheads & upto;
+  const int bstart = bhb ? 31 - __clz(bhb) : 0;
+  double w = c ? v3 : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(full, w, o);
+    if (lane - o >= bstart) w += t;
+  }
+  if (c && (next < 0 || ((bheads >> next) & 1u))) atomicAdd(cwb + b, w);
 }
 
 // track-length score (keyed by batch slot and cell) plus the per-cell count
@@ -208,10 +272,12 @@ __device__ __forceinline__ void agg_add_count_t(double* base, Count* cnt, int ke
                                                 int cell) {
   if (!__any_sync(0xffffffffu, key >= 0)) return;
   const unsigned grp = agg_group(key);
-  const double s = group_sum(grp, key >= 0 ? v : 0.0);
-  if (key >= 0 && group_leader(grp)) {
-    atomicAdd(base + key, s);
-    atomicAdd(cnt + cell, (Count)__popc(grp));
+  if (key >= 0) {
+    const double s = group_sum(grp, v);
+    if (group_leader(grp)) {
+      atomicAdd(base + key, s);
+      atomicAdd(cnt + cell, (Count)__popc(grp));
+    }
   }
 }
 __device__ __forceinline__ void agg_add_count(double* base, unsigned* cnt, int key, double v,
@@ -721,12 +787,17 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         if (sh) atomicAdd(S.trc + trk_cell, 1u);
         else atomicAdd(a.t.tracks + trk_cell, 1ULL);
       }
+#if !defined(HWWG_CENSUS_PER_LANE)
+      // census scores: run-aggregated across the warp (census_runs)
+      census_runs(cphi, cJ, cF, cwb, cen_cell, cen_b, cen_phi, cen_J, cen_F, cen_w);
+#else
       if (cen_cell >= 0) {
         atomicAdd(cphi + cen_cell, cen_phi);
         atomicAdd(cJ + cen_cell, cen_J);
         atomicAdd(cF + cen_cell, cen_F);
         atomicAdd(cwb + cen_b, cen_w);
       }
+#endif
       if (edge_key >= 0) atomicAdd(edg + edge_key, edge_v);
     }
 
