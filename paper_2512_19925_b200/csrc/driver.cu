@@ -123,6 +123,9 @@ struct hwwg_driver {
   DevBuf<double> q_dev;
   const double* q_step = nullptr;
   DevBuf<hwwg_particle> vol_dev;
+  // e2e (host_bank): chunked source upload on its own stream (one event per chunk)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> h2d_ev;
   // e2e (host_bank) Philox runs: the bank in host memory is already combed
   bool host_pre_combed = false;
   uint64_t pre_comb_in = 0;
@@ -196,6 +199,8 @@ struct hwwg_driver {
     if (ev1) cudaEventDestroy(ev1);
     for (auto e : seg_ev) cudaEventDestroy(e);
     for (auto e : ph_ev) cudaEventDestroy(e);
+    for (auto e : h2d_ev) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (host_bank) cudaFreeHost(host_bank);
     if (comm) ncclCommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
@@ -315,6 +320,11 @@ void init_driver(hwwg_driver* d) {
   }
   d->seg_ev.resize(32);
   for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
+  if (c.host_bank) {
+    HWWG_CUDA(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
+    d->h2d_ev.resize(9);
+    for (auto& e : d->h2d_ev) HWWG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   if (d->fast) {
     const uint64_t local_target = d->target / (uint64_t)d->world + 1;
     d->fbank.reserve(std::max<uint64_t>(d->bank_n, 64 * local_target + 4096));
@@ -483,7 +493,38 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const auto t0 = std::chrono::steady_clock::now();
   HWWG_CUDA(cudaEventRecord(d->ev0, s));
 
-  if (c.host_bank) {  // e2e: the bank lives in host memory between steps
+  // e2e with a pre-combed host bank: the source crosses PCIe in the chunks the
+  // step's segments consume ([0, h_1), [h_1, h_2), ...) on a copy stream, and
+  // segment u waits only for chunk u, so the later chunks overlap the earlier
+  // segments' transport.
+  size_t n_h2d_chunks = 0;
+  if (c.host_bank && d->fast && d->host_pre_combed && d->world == 1 && !(c.vol_rate > 0.0)) {
+    const uint64_t Hs = d->host_bank_n;
+    std::vector<uint64_t> bounds;
+    if (d->hybrid() && c.u_ww > 0)  // the thresholds below, for the same H
+      for (int i = 0; i < c.n_fractions; ++i) {
+        const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)Hs);
+        if (h >= Hs || (!bounds.empty() && h <= bounds.back())) continue;
+        bounds.push_back(h);
+      }
+    bounds.push_back(Hs);
+    d->bank.reserve(std::max<uint64_t>(Hs, 1));
+    const FastBank f = d->fsrc.view();
+    uint64_t lo = 0;
+    for (size_t u = 0; u < bounds.size() && u < d->h2d_ev.size(); ++u) {
+      const uint64_t hi = bounds[u];
+      HWWG_CUDA(cudaMemcpyAsync(d->bank.p + lo, d->host_bank + lo, (hi - lo) * sizeof(hwwg_particle),
+                                cudaMemcpyHostToDevice, d->copy_stream));
+      launch_aos_to_fast(d->bank.p + lo, hi - lo, d->prob.view,
+                         FastBank{f.xm + lo, f.wt + lo, f.meta + lo}, lo, d->copy_stream);
+      HWWG_CUDA(cudaEventRecord(d->h2d_ev[u], d->copy_stream));
+      ++d->launches;
+      lo = hi;
+      ++n_h2d_chunks;
+    }
+    d->bank_n = Hs;
+    rec->h2d_bytes += Hs * sizeof(hwwg_particle);
+  } else if (c.host_bank) {  // e2e: the bank lives in host memory between steps
     d->bank.reserve(std::max<uint64_t>(d->host_bank_n, 1));
     HWWG_CUDA(cudaMemcpyAsync(d->bank.p, d->host_bank, d->host_bank_n * sizeof(hwwg_particle),
                               cudaMemcpyHostToDevice, s));
@@ -827,6 +868,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           HWWG_CUDA(cudaMemsetAsync(fa.timeline, 0, per * 8, s));
           d->timeline_warps = fa.pool.warps;
         }
+        if (u < n_h2d_chunks) HWWG_CUDA(cudaStreamWaitEvent(s, d->h2d_ev[u], 0));
         if (fa.n_src) {
           launch_fast_segment(fa, blocks, smem, s);
           d->launches += 2;
