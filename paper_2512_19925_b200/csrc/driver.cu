@@ -123,6 +123,9 @@ struct hwwg_driver {
   DevBuf<double> q_dev;
   const double* q_step = nullptr;
   DevBuf<hwwg_particle> vol_dev;
+  // start-of-step window update overlapping the comb (auxiliary stream)
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // e2e (host_bank): chunked source upload on its own stream (one event per chunk)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> h2d_ev;
@@ -200,6 +203,9 @@ struct hwwg_driver {
     for (auto e : seg_ev) cudaEventDestroy(e);
     for (auto e : ph_ev) cudaEventDestroy(e);
     for (auto e : h2d_ev) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (host_bank) cudaFreeHost(host_bank);
     if (comm) ncclCommDestroy(comm);
@@ -320,6 +326,9 @@ void init_driver(hwwg_driver* d) {
   }
   d->seg_ev.resize(32);
   for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
+  HWWG_CUDA(cudaStreamCreateWithFlags(&d->aux_stream, cudaStreamNonBlocking));
+  HWWG_CUDA(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+  HWWG_CUDA(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
   if (c.host_bank) {
     HWWG_CUDA(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
     d->h2d_ev.resize(9);
@@ -492,6 +501,73 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const double dt = d->layers[step] - d->layers[step - 1];
   const auto t0 = std::chrono::steady_clock::now();
   HWWG_CUDA(cudaEventRecord(d->ev0, s));
+  const double theta_eff = step == 1 ? 1.0 : c.theta;
+  const int ma_k = c.mode == 3 ? c.ma_base_k : 0;
+  const int prev = d->rep_cur ^ 1;  // report of the previous step lives in the other buffer
+
+  // ---- the start-of-step windows (driver.cpp:136-167) on stream st: record
+  // flags, then lww centres or the lagged hybrid solve
+  auto enqueue_windows = [&](cudaStream_t st) {
+    // per-step record flags: has_hybrid, updates_applied, failed, status
+    HWWG_CUDA(cudaMemsetAsync(d->lo.flags + 1, 0, 4 * sizeof(int), st));
+    if (c.mode == 1) {  // lww: lagged track-length flux of the previous step
+      HWWG_CUDA(cudaMemsetAsync(d->lo.flags, 0, sizeof(int), st));
+      if (d->has_prev_report) {
+        launch_build_centers(d->rep(prev, 0), I, c.eps_min, c.rho, d->lo.centers,
+                             d->lo.flags + 5, st);
+        set_active_from_fallback(d->lo.flags, st);
+        d->launches += 2;
+      }
+    } else if (d->hybrid()) {
+      LowOrderArgs a{};
+      a.I = I;
+      a.edges = d->prob.view.edges;
+      a.cells = d->prob.view.cells;
+      a.theta = theta_eff;
+      a.dt = dt;
+      a.eps_min = c.eps_min;
+      a.rho = c.rho;
+      a.ma_k = ma_k;
+      a.fourier_tab_cell = c.mode == 4 ? d->ftab_cell.p : nullptr;
+      a.fourier_tab_edge = c.mode == 4 ? d->ftab_edge.p : nullptr;
+      a.fourier_cutoff = c.fourier_cutoff;
+      a.q = d->q_step;
+      a.mode = 0;
+      a.fast_solve = d->fast ? 1 : 0;
+      a.refactor = d->need_refactor(theta_eff, dt);
+      a.analytic = step == 1;
+      if (step == 1 && !c.no_pulse) {
+        const int cell = locate_host(d->prob.edges, c.x0);
+        a.pulse_cell = cell;
+        a.pulse_value = c.speed * c.strength / (d->prob.edges[cell + 1] - d->prob.edges[cell]);
+      } else if (step == 1) {  // no pulse: the analytic initial state is zero
+        a.pulse_cell = -2;
+        a.pulse_value = 0.0;
+      }
+      a.s = d->lo;
+      a.s.rep_phi_census = d->rep(prev, 2);
+      a.s.rep_current = d->rep(prev, 3);
+      a.s.rep_closure = d->rep(prev, 4);
+      a.s.rep_PLPR = d->rep(prev, 6);
+      d->ph_mark("losm0", st);
+      launch_low_order_update(a, st);
+      d->ph_mark("-", st);
+      ++d->launches;
+    }
+  };
+  // Single-GPU Philox steps without a volumetric source (whose q is known only
+  // after the comb): the window update depends on the previous step alone, so
+  // it runs on the auxiliary stream alongside the comb.
+  const bool early_windows = d->fast && d->world == 1 && !(c.vol_rate > 0.0) && !d->phases_on;
+  if (early_windows) {
+    // backup of the windows so an overflowing step can be replayed exactly
+    HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
+    HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    HWWG_CUDA(cudaEventRecord(d->ev_fork, s));
+    HWWG_CUDA(cudaStreamWaitEvent(d->aux_stream, d->ev_fork, 0));
+    enqueue_windows(d->aux_stream);
+    HWWG_CUDA(cudaEventRecord(d->ev_join, d->aux_stream));
+  }
 
   // e2e with a pre-combed host bank: the source crosses PCIe in the chunks the
   // step's segments consume ([0, h_1), [h_1, h_2), ...) on a copy stream, and
@@ -651,9 +727,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     }
   }
 
-  // backup of the windows so an overflowing step can be replayed exactly
-  HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
-  HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  if (!early_windows) {  // backup of the windows so an overflowing step can be replayed exactly
+    HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
+    HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  }
 
   if (d->fast) d->fcensus.reserve(d->census_hwm);  // the swapped-in buffer may be short
 
@@ -670,9 +747,6 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   rec->n_thresholds = (int)thr.size();
   for (size_t i = 0; i < thr.size() && i < 8; ++i) rec->thresholds[i] = thr[i];
 
-  const double theta_eff = step == 1 ? 1.0 : c.theta;
-  const int ma_k = c.mode == 3 ? c.ma_base_k : 0;
-  const int prev = d->rep_cur ^ 1;  // report of the previous step lives in the other buffer
 
   unsigned long long count = 0;
   DevError derr{};
@@ -710,54 +784,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       HWWG_CUDA(cudaMemcpyAsync(d->lo.centers, d->centers_backup.p, I * 8, cudaMemcpyDeviceToDevice, s));
       HWWG_CUDA(cudaMemcpyAsync(d->lo.flags, d->flags_backup.p, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
     }
-    // per-step record flags: has_hybrid, updates_applied, failed, status
-    HWWG_CUDA(cudaMemsetAsync(d->lo.flags + 1, 0, 4 * sizeof(int), s));
-
-    // ---- windows (driver.cpp:136-167)
-    if (c.mode == 1) {  // lww: lagged track-length flux of the previous step
-      HWWG_CUDA(cudaMemsetAsync(d->lo.flags, 0, sizeof(int), s));
-      if (d->has_prev_report) {
-        launch_build_centers(d->rep(prev, 0), I, c.eps_min, c.rho, d->lo.centers,
-                             d->lo.flags + 5, s);
-        set_active_from_fallback(d->lo.flags, s);
-        d->launches += 2;
-      }
-    } else if (d->hybrid()) {
-      LowOrderArgs a{};
-      a.I = I;
-      a.edges = d->prob.view.edges;
-      a.cells = d->prob.view.cells;
-      a.theta = theta_eff;
-      a.dt = dt;
-      a.eps_min = c.eps_min;
-      a.rho = c.rho;
-      a.ma_k = ma_k;
-      a.fourier_tab_cell = c.mode == 4 ? d->ftab_cell.p : nullptr;
-      a.fourier_tab_edge = c.mode == 4 ? d->ftab_edge.p : nullptr;
-      a.fourier_cutoff = c.fourier_cutoff;
-      a.q = d->q_step;
-      a.mode = 0;
-      a.fast_solve = d->fast ? 1 : 0;
-      a.refactor = d->need_refactor(theta_eff, dt);
-      a.analytic = step == 1;
-      if (step == 1 && !c.no_pulse) {
-        const int cell = locate_host(d->prob.edges, c.x0);
-        a.pulse_cell = cell;
-        a.pulse_value = c.speed * c.strength / (d->prob.edges[cell + 1] - d->prob.edges[cell]);
-      } else if (step == 1) {  // no pulse: the analytic initial state is zero
-        a.pulse_cell = -2;
-        a.pulse_value = 0.0;
-      }
-      a.s = d->lo;
-      a.s.rep_phi_census = d->rep(prev, 2);
-      a.s.rep_current = d->rep(prev, 3);
-      a.s.rep_closure = d->rep(prev, 4);
-      a.s.rep_PLPR = d->rep(prev, 6);
-      d->ph_mark("losm0", s);
-      launch_low_order_update(a, s);
-      d->ph_mark("-", s);
-      ++d->launches;
-    }
+    // ---- windows (driver.cpp:136-167): already on the auxiliary stream for the
+    // first attempt of an early-window step, else here
+    if (attempt == 0 && early_windows) HWWG_CUDA(cudaStreamWaitEvent(s, d->ev_join, 0));
+    else enqueue_windows(s);
 
     // ---- segments with window-update barriers (driver.cpp:181-219)
     d->tal.zero(s);
