@@ -1,3 +1,14 @@
-make -s -C paper_2512_19925_b200 >/dev/null 2>&1 || echo build failed
+# tail loop A/B + tests + activity
+for v in "" "-DHWWG_TAIL_LOOP=0"; do
+  touch paper_2512_19925_b200/csrc/transport_fast.cu
+  make -s -C paper_2512_19925_b200 NVEXTRA="$v" >/dev/null 2>&1 || echo build failed
+  timeout 300 python scripts/step_times.py philox 40 > gpurun_out/steps_knob.log 2>&1
+  echo "[$v] $(head -2 gpurun_out/steps_knob.log | tail -1) $(sed -n 4p gpurun_out/steps_knob.log | cut -c1-30) $(sed -n 23p gpurun_out/steps_knob.log | cut -c1-30)"
+done
+touch paper_2512_19925_b200/csrc/transport_fast.cu
+make -s -C paper_2512_19925_b200 >/dev/null 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-timeout 300 python scripts/step_times.py philox 40 > gpurun_out/steps_cur.log 2>&1; echo steps=$?
+touch paper_2512_19925_b200/csrc/transport_fast.cu
+make -s -C paper_2512_19925_b200 NVEXTRA=-DHWWG_FAST_PROF >/dev/null 2>&1 || echo build failed
+REPS=1 HWWG_FAST_TIMELINE=1 timeout 300 python scripts/step_times.py philox 24 > gpurun_out/steps_fprof.log 2>&1; echo fp=$?
+touch paper_2512_19925_b200/csrc/transport_fast.cu
