@@ -81,6 +81,10 @@ constexpr unsigned kDonate = HWWG_KDONATE;  // pending local daughters above whi
 constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
 constexpr unsigned kClaim = 32;  // source particles a warp reserves per claim
 constexpr unsigned kShare = HWWG_KSHARE;
+#ifndef HWWG_POLL_EVERY
+#define HWWG_POLL_EVERY 4
+#endif
+constexpr unsigned kPollEvery = HWWG_POLL_EVERY;  // trips between looks at the pool counters
 constexpr int kSmemStack = 8;
 #ifndef HWWG_KPIECE
 #define HWWG_KPIECE 32
@@ -369,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   Lane p;
   p.alive = false;
   bool holding = true;  // this warp counts in pool.ctl[2] (active warps)
+  bool declared = false;  // this warp has set pool.ctl[3] (backlog declared)
   // source reservation (warp-uniform) and the claim in flight (lane 0)
   // (32-bit: the driver keeps a segment's source below 2^32 - 2^26 particles)
   const unsigned n_src = (unsigned)a.n_src;
@@ -393,13 +398,16 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     // in a single trip: split the top run into pieces (daughter index ranges
     // stay disjoint through the base offset) or give away whole records from
     // the top of the stack, keeping at least one trip of work here.
-    if (pend > kShare && sp > 0) {
+    // (the pool counters are one hot L2 line: a warp with a backlog looks at
+    // them every kPollEvery-th trip, and declares the backlog once)
+    if (pend > kShare && sp > 0 && (n_iter % kPollEvery) == 0) {
       unsigned open = 0;
       if (lane == 0) {
-        if (ctl[3] == 0) ctl[3] = 1;  // declare a backlog: idle warps wait for work
+        if (!declared) ctl[3] = 1;  // declare a backlog: idle warps wait for work
         const unsigned long long t1 = ctl[1], t0 = ctl[0];
         open = t1 > t0 ? (unsigned)min(t1 - t0, 32ULL) : 0u;
       }
+      declared = true;
       open = __shfl_sync(0xffffffffu, open, 0);
       if (open) {
         FastStackRec& top = STK(sp - 1);
@@ -814,9 +822,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (donate) {
         int open = 0;
         if (lane == 0) {
-          if (ctl[3] == 0) ctl[3] = 1;  // declare a backlog: idle warps wait for donations
+          if (!declared) ctl[3] = 1;  // declare a backlog: idle warps wait for donations
           open = ctl[1] > ctl[0] ? 1 : 0;
         }
+        declared = true;
         donate = __shfl_sync(0xffffffffu, open, 0) != 0;
       }
       const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell, p.hist, p.key, p.ctr,

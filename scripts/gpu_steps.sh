@@ -1,5 +1,5 @@
-# tail loop A/B + tests + activity
-for v in "" "-DHWWG_TAIL_LOOP=0"; do
+# pool polling A/B
+for v in "" "-DHWWG_POLL_EVERY=1" "-DHWWG_POLL_EVERY=16"; do
   touch paper_2512_19925_b200/csrc/transport_fast.cu
   make -s -C paper_2512_19925_b200 NVEXTRA="$v" >/dev/null 2>&1 || echo build failed
   timeout 300 python scripts/step_times.py philox 40 > gpurun_out/steps_knob.log 2>&1
@@ -8,7 +8,3 @@ done
 touch paper_2512_19925_b200/csrc/transport_fast.cu
 make -s -C paper_2512_19925_b200 >/dev/null 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-touch paper_2512_19925_b200/csrc/transport_fast.cu
-make -s -C paper_2512_19925_b200 NVEXTRA=-DHWWG_FAST_PROF >/dev/null 2>&1 || echo build failed
-REPS=1 HWWG_FAST_TIMELINE=1 timeout 300 python scripts/step_times.py philox 24 > gpurun_out/steps_fprof.log 2>&1; echo fp=$?
-touch paper_2512_19925_b200/csrc/transport_fast.cu
