@@ -289,3 +289,40 @@ def test_config3_driver_matches_oracle(oracle, mode):
         _check_step(rec, arr, ints, [getattr(o.counters, n) for n in COUNTER_U],
                     [o.counters.leakage_weight, o.counters.aborted_weight], oarr)
     census_equal(d.bank(), od.bank(), weights_tol=1e-12)
+
+
+@pytest.mark.parametrize("which,H,N,kw", [
+    (4, 20000, 3, {}),                                   # I = 4000: global LOSM / tallies paths
+    (5, 20000, 3, dict(rho=2.0, mode="hww")),            # config 5 variants (rho x filter)
+    (5, 20000, 3, dict(rho=10.0, ma_base_k=2)),
+])
+def test_configs_4_5_match_oracle(oracle, which, H, N, kw):
+    """BASELINE configs 4 and 5 at reduced H in exact mode: the large mesh (the
+    low-order state no longer fits shared memory) and the config-5 window/filter
+    variants, bit-exact against the oracle."""
+    oc = baseline_config(which, histories=H, time_steps=N, **kw)
+    od = DriverRun(oracle, oc)
+    cfg = hw.RunConfig(mode=hw.hww.MODES[oc.mode], histories_per_step=oc.histories_per_step,
+                       theta=oc.theta, rho=oc.rho, eps_min=oc.eps_min, u_ww=oc.u_ww,
+                       update_fractions=tuple(oc.fractions[:oc.n_fractions]),
+                       ma_base_k=oc.ma_base_k, batches=oc.batches, seed=oc.seed,
+                       material=hw.Material(oc.sigma_t, oc.sigma_s, oc.sigma_f, oc.nu_f, oc.speed),
+                       x_min=oc.x_min, x_max=oc.x_max, cells=oc.cells, t_end=oc.t_end,
+                       time_steps=oc.time_steps)
+    d = hw.Driver(cfg)
+    for s in range(1, N + 1):
+        o, oarr = od.step()
+        rec = d.step()
+        arr = d.arrays()
+        ints = [o.segments, o.census_size, o.histories, o.comb_in, o.comb_out,
+                o.updates_applied, o.hybrid_solve_failed, o.n_thresholds, o.sigma_valid,
+                o.has_windows, o.has_hybrid]
+        _check_step(rec, arr, ints, [getattr(o.counters, n) for n in COUNTER_U],
+                    [o.counters.leakage_weight, o.counters.aborted_weight], oarr)
+    census_equal(d.bank(), od.bank(), weights_tol=1e-12)
+    # the throughput mode on the same configuration: runs, conserves the census count
+    fd = hw.Driver(cfg, rng_mode=hw.RNG_PHILOX)
+    for s in range(1, N + 1):
+        r = fd.step()
+        assert r.census_size == r.counters.census_count and r.segments > 0
+    fd.close()
