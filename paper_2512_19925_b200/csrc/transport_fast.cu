@@ -6,25 +6,32 @@
 // key = seed), so any particle can advance independently and the result is a
 // statistically equivalent estimator of the same physics (SURVEY.md §7 hard
 // part 1; parity = combined standard errors, tests/test_gpu_statistical.py).
+// One Philox block per event: flight, collision channel and scattering
+// deviates (the roulette deviate after a scatter is the channel one recycled).
 //
-// Work model — a persistent grid, one particle per lane, one EVENT per loop
-// iteration (free flight -> census | cell crossing | collision), with refill:
-// a lane whose particle terminated takes the next unit of work from
-//   1. its warp's run-length-encoded split stack (LIFO, like the reference),
-//   2. the bank of source particles (one warp-aggregated atomic per refill),
-//   3. the global pool of split records that other warps donated.
+// Work model — a persistent grid (3 CTAs of 8 warps per SM), one particle per
+// lane, one EVENT per loop trip (free flight -> census | cell crossing |
+// collision), with refill: a lane whose particle terminated takes the next
+// unit of work from
+//   1. its warp's run-length-encoded split stack (LIFO, like the reference;
+//      the bottom kSmemStack records in shared memory),
+//   2. the source bank, through a per-warp reservation of kClaim particles
+//      claimed one trip ahead (first one static) and prefetched into L1,
+//   3. the global pool of split records other warps donated (ticket queue).
 // A split never materialises its daughters: it pushes ONE record (state, n-1
 // copies) and lanes pop daughters from it — the bank-expansion step done by
-// ballot + prefix-popcount inside the warp. A warp whose pending daughters
-// exceed kDonate pushes new records to the global pool instead, so the heavy
-// cold-start split trees (config 2 step 1: p99 1108 segments per history)
-// spread over the whole GPU instead of pinning one warp. Roulette and
-// unchanged windows cost no memory traffic.
+// ballot + prefix-popcount inside the warp. Backlogs are shared with idle
+// warps (halves of a long run or whole records, up to one per idle warp per
+// trip), so the heavy cold-start split trees (config 2 step 1: p99 1108
+// segments per history) spread over the whole GPU instead of pinning one warp.
+// Roulette and unchanged windows cost no memory traffic.
 //
 // Tallies: block-private shared-memory histograms over the segment's batch
 // range (track-length by batch and cell, census phi/J/F, edge currents,
 // per-cell track counts), flushed once per block with fp64 REDs; global REDs
-// when the histograms do not fit in shared memory (I = 4000).
+// when the histograms do not fit in shared memory (I = 4000). The cold-start
+// step warp-aggregates them (MATCH.ANY groups, REDUX fixed-point sums); census
+// scores are run-aggregated across the warp in every step.
 #include <vector>
 
 #include "common.cuh"
