@@ -246,6 +246,19 @@ class Oracle(_Lib):
         L.orc_bank_free.argtypes = [C.POINTER(Bank)]
         L.orc_stream_id.restype = C.c_uint64
         L.orc_stream_id.argtypes = [C.c_uint64] * 3
+        L.orc_uniform_comb.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                       C.c_uint64, C.c_void_p, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]
+
+    def uniform_comb(self, bank, target, seed, stream_id):
+        """orc_uniform_comb — popctrl.cpp:7-42. Returns (out, in_weight, out_weight)."""
+        b = np.ascontiguousarray(bank, PARTICLE_DT)
+        out = np.zeros(target, PARTICLE_DT)
+        iw, ow = C.c_double(), C.c_double()
+        if self.lib.orc_uniform_comb(b.ctypes.data, b.size, target, seed, stream_id,
+                                     out.ctypes.data, C.byref(iw), C.byref(ow)) != 0:
+            raise ValueError(self.err())
+        return out, iw.value, ow.value
 
     def run_segment(self, edges, mats, t_begin, t_end, seed, step, histories_total, batches,
                     source, h_begin, centers=None, rho=1.25, chunk=256, tallies=None,

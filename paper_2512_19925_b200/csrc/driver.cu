@@ -104,6 +104,7 @@ struct hwwg_driver {
   DevBuf<unsigned long long> counter;
   DevBuf<DevError> err;
   DevBuf<double> chunk_mem;
+  ExactLogBuf xlog;  // history-parallel exact path
 
   // throughput (Philox) mode: SoA banks, warp split stacks, refill cursor
   bool fast = false;
@@ -814,6 +815,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     ea.census_count = d->counter.p;
     ea.census_cap = d->stage.records.n;
     ea.err = d->err.p;
+    if (!d->fast) d->xlog.reset_need(s);
     uint64_t h_done = 0;
     for (size_t u = 0; u <= thr.size(); ++u) {
       const uint64_t h_stop = u < thr.size() ? thr[u] : H;
@@ -824,6 +826,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         ea.chunks = chunk_layout(ea.n, h_done, H, I, B);
         d->chunk_mem.reserve(std::max<size_t>((size_t)ea.chunks.count * ea.chunks.stride, 1));
         ea.chunks.base = d->chunk_mem.p;
+        ea.log = d->xlog.view(ea.n);
       }
       const int nseg = (int)u;
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
@@ -905,7 +908,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         }
       } else {
         launch_exact_segment(ea, s);
-        if (ea.n) d->launches += 3;  // chunk init, chunk histories, ordered merge
+        // chunk init, histories (+ log replay), ordered merge
+        if (ea.n) d->launches += ea.log.slot ? 4 : 3;
       }
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg + 1], s));
       h_done = h_stop;
@@ -988,6 +992,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->fcensus.reserve(d->census_hwm);  // replay the step with room
       continue;
     }
+    if (derr.code == kLogOverflow && attempt < 3) {  // replay with a log arena that fits
+      d->xlog.ensure_blocks(d->xlog.need(s) + 1024);
+      continue;
+    }
     if (derr.code || count <= ea.census_cap) break;
     d->stage.ensure(count + count / 4 + 4096);
   }
@@ -1055,6 +1063,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   if (derr.code == HWWG_ESTACK)
     throw ApiError(HWWG_ESTACK, "history " + std::to_string(derr.history) +
                                     " exceeded the daughter-stack run capacity");
+  if (derr.code == kLogOverflow)
+    throw ApiError(HWWG_ENOMEM, "exact tally log exceeds 2^32 blocks");
 
   // ---- finalize (driver.cpp:221-222)
   if (d->world > 1) {  // step-end reduction of the whole tally slab and counters

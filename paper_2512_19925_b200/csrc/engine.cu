@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +82,7 @@ struct hwwg_ctx {
   DevBuf<hwwg_particle> comb_in, comb_out;
   DevBuf<CellInfo> comp_cells;
   DevBuf<double> chunk_mem;
+  ExactLogBuf xlog;
 
   ~hwwg_ctx() {
     if (stream) cudaStreamDestroy(stream);
@@ -196,7 +198,7 @@ int hwwg_run_segment_parallel(hwwg_ctx* c, const hwwg_step_context* st,
   }
   unsigned long long count = 0;
   DevError derr{};
-  for (int attempt = 0; attempt < 3; ++attempt) {
+  for (int attempt = 0; attempt < 4; ++attempt) {
     HWWG_CUDA(cudaMemcpyAsync(c->tal.slab.p, up.data(), up.size() * 8, cudaMemcpyHostToDevice, s));
     HWWG_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned long long), s));
     HWWG_CUDA(cudaMemsetAsync(c->err.p, 0, sizeof(DevError), s));
@@ -206,14 +208,24 @@ int hwwg_run_segment_parallel(hwwg_ctx* c, const hwwg_step_context* st,
     a.census = c->stage.records.p;
     a.census_keys = c->stage.keys.p;
     a.census_cap = c->stage.records.n;
+    a.log = c->xlog.view(n);
+    if (a.log.slot) c->xlog.reset_need(s);
     launch_exact_segment(a, s);
     HWWG_CUDA(cudaMemcpyAsync(&count, c->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaMemcpyAsync(&derr, c->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaStreamSynchronize(s));
+    if (derr.code == kLogOverflow) {  // replay with a log arena of the right size
+      const unsigned long long need = c->xlog.need(s);
+      if (std::getenv("HWWG_XLOG_DEBUG"))
+        std::fprintf(stderr, "[xlog] attempt %d need %llu cap %llu\n", attempt, need, c->xlog.cap);
+      c->xlog.ensure_blocks(need + 1024);
+      continue;
+    }
     if (derr.code) break;
     if (count <= a.census_cap) break;
     c->stage.ensure(count + count / 4 + 1024);  // deterministic replay with room
   }
+  if (derr.code == kLogOverflow) return fail(HWWG_ENOMEM, "exact tally log exceeds 2^32 blocks");
   if (derr.code == HWWG_EINVAL)
     return fail(HWWG_EINVAL, "history " + std::to_string(derr.history) +
                                  " starts outside the mesh or the time step");

@@ -910,60 +910,182 @@ __global__ void k_finalize(FinalizeArgs a) {
   }
 }
 
-// popctrl.cpp:15-30 — the cumulative-weight walk, sequential in bank order.
-// One thread carries the fp64 running sum; the other 255 threads of the CTA
-// stage the next weights into shared memory so the serial chain never waits
-// on HBM.
-__global__ void __launch_bounds__(256) k_comb_prefix(CombArgs a) {
-  constexpr int kTile = 2048;
-  __shared__ double w[2][kTile];
-  double cum = 0.0;
-  const uint64_t tiles = (a.n + kTile - 1) / kTile;
-  auto load = [&](uint64_t tile, int buf) {
-    const uint64_t base = tile * kTile;
-    for (int j = threadIdx.x; j < kTile; j += blockDim.x) {
-      const uint64_t k = base + j;
-      w[buf][j] = k < a.n ? a.bank[k].w : 0.0;
-    }
-  };
-  if (tiles) load(0, 0);
-  __syncthreads();
-  for (uint64_t tl = 0; tl < tiles; ++tl) {
-    const int buf = (int)(tl & 1);
-    if (threadIdx.x == 0) {
-      const uint64_t base = tl * kTile;
-      const uint64_t m = a.n - base < (uint64_t)kTile ? a.n - base : (uint64_t)kTile;
-      for (uint64_t j = 0; j < m; ++j) {
-        cum += w[buf][j];
-        a.prefix[base + j] = cum;
+// popctrl.cpp:15-30 — the cumulative-weight walk s_k = fl(s_{k-1} + w_k),
+// sequential in bank order, computed by one CTA in parallel and bit for bit.
+//
+// While s stays in one binade [2^e, 2^{e+1}) every s_k is an integer multiple
+// S_k of u = ulp = 2^{e-52}, and with q = w_k / u = a + r (a integer, r in
+// [0, 1), both exact) round-to-nearest-even gives
+//   S_k = S_{k-1} + a + [r > 1/2] + [r == 1/2 and S_{k-1} + a odd]
+// as long as S_{k-1} + a < 2^53. Each element is then a map S -> S + inc(S mod
+// 2); maps compose associatively (an increment per input parity), so a tile
+// of 4096 weights is one block-wide scan of integer pairs. The first element
+// that would leave the binade (or any weight the rule does not cover: zero
+// sum, negative, non-finite, huge) is added by one thread with a real fp64
+// add, and the scan restarts after it in the new binade — ~log2(n) times per
+// bank, as s only grows.
+namespace combscan {
+constexpr int kThreads = 512, kItems = 8, kTile = kThreads * kItems;
+constexpr uint64_t kTop = 1ULL << 53;
+
+struct Map {  // S -> S + inc[S & 1]
+  uint64_t i0, i1;
+};
+__device__ __forceinline__ Map compose(const Map& f, const Map& g) {  // f then g
+  return Map{f.i0 + ((f.i0 & 1) ? g.i1 : g.i0), f.i1 + (((1 + f.i1) & 1) ? g.i1 : g.i0)};
+}
+__device__ __forceinline__ uint64_t apply(const Map& f, uint64_t S) { return S + ((S & 1) ? f.i1 : f.i0); }
+
+// floor(w / u) (saturated at 2^53) and the rounding class of the remainder
+__device__ __forceinline__ void split(double w, int e, uint64_t& a, int& cls) {
+  if (!(w >= 0.0) || w >= ldexp(1.0, e + 1)) {  // off the rule: negative, NaN, inf, huge
+    a = kTop;
+    cls = 0;
+    return;
+  }
+  const double q = ldexp(w, 52 - e);  // exact power-of-two scaling
+  const double fa = floor(q);
+  const double r = q - fa;  // exact
+  a = (uint64_t)fa;
+  cls = r > 0.5 ? 2 : (r == 0.5 ? 1 : 0);
+}
+__device__ __forceinline__ Map elem_map(uint64_t a, int cls) {
+  const uint64_t b = a + (cls == 2 ? 1 : 0);
+  const int tie = cls == 1;
+  // input parity p: tie rounds up when S + a is odd
+  return Map{b + (uint64_t)(tie && (b & 1)), b + (uint64_t)(tie && !(b & 1))};
+}
+__device__ __forceinline__ bool in_rule(double s) { return s >= 0x1p-1000 && s < 0x1p1000; }
+
+// Sequential sum of w(k), k in [0, n); prefix (optional) receives s_k. Returns
+// the final sum in every thread. W is a functor k -> weight.
+template <class WF>
+__device__ double serial_sum(WF W, uint64_t n, double* prefix, double* wt) {
+  __shared__ Map warp_agg[kThreads / 32];
+  __shared__ unsigned long long cross;
+  __shared__ double s_sh;
+  __shared__ unsigned long long k_sh;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double s = 0.0;
+  uint64_t k = 0;
+  while (k < n) {
+    if (!in_rule(s)) {  // one thread until s is a normal, finite, positive sum
+      if (tid == 0) {
+        while (k < n && !in_rule(s)) {
+          s += W(k);
+          if (prefix) prefix[k] = s;
+          ++k;
+        }
+        s_sh = s;
+        k_sh = k;
       }
-    } else if (tl + 1 < tiles) {
-      // threads 1.. stage the next tile
-      const uint64_t base = (tl + 1) * kTile;
-      for (int j = threadIdx.x - 1; j < kTile; j += blockDim.x - 1) {
-        const uint64_t k = base + j;
-        w[buf ^ 1][j] = k < a.n ? a.bank[k].w : 0.0;
+      __syncthreads();
+      s = s_sh;
+      k = k_sh;
+      __syncthreads();
+      continue;
+    }
+    int e;
+    frexp(s, &e);
+    e -= 1;  // s in [2^e, 2^{e+1})
+    const double u = ldexp(1.0, e - 52);
+    const uint64_t S0 = (uint64_t)ldexp(s, 52 - e);
+    const uint64_t m = n - k < (uint64_t)kTile ? n - k : (uint64_t)kTile;
+    for (int j = tid; j < kTile; j += kThreads) wt[j] = (uint64_t)j < m ? W(k + j) : 0.0;
+    if (tid == 0) cross = ~0ULL;
+    __syncthreads();
+    // per-thread map over its kItems consecutive weights
+    uint64_t a[kItems];
+    int cls[kItems];
+    Map agg{0, 0};
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      split(wt[tid * kItems + i], e, a[i], cls[i]);
+      agg = compose(agg, elem_map(a[i], cls[i]));
+    }
+    // block-wide exclusive scan of the thread maps
+    Map inc = agg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      Map p;
+      p.i0 = __shfl_up_sync(0xffffffffu, inc.i0, o);
+      p.i1 = __shfl_up_sync(0xffffffffu, inc.i1, o);
+      if (lane >= o) inc = compose(p, inc);
+    }
+    if (lane == 31) warp_agg[wid] = inc;
+    __syncthreads();
+    Map before{0, 0};
+    for (int w = 0; w < wid; ++w) before = compose(before, warp_agg[w]);
+    Map ex;
+    ex.i0 = __shfl_up_sync(0xffffffffu, inc.i0, 1);
+    ex.i1 = __shfl_up_sync(0xffffffffu, inc.i1, 1);
+    if (lane > 0) before = compose(before, ex);
+    // the thread's elements: values, and the first that leaves the binade
+    uint64_t S = apply(before, S0);
+    unsigned long long first = ~0ULL;
+    double out[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint64_t j = (uint64_t)tid * kItems + i;
+      if (j < m && first == ~0ULL && S + a[i] >= kTop) first = j;
+      S = apply(elem_map(a[i], cls[i]), S);
+      out[i] = (double)S * u;
+    }
+    if (first != ~0ULL) atomicMin(&cross, first);
+    __syncthreads();
+    const uint64_t valid = cross < m ? cross : m;
+    if (prefix) {
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        const uint64_t j = (uint64_t)tid * kItems + i;
+        if (j < valid) prefix[k + j] = out[i];
       }
     }
+    // the last valid value seeds the next round
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+      if (valid > 0 && (uint64_t)tid * kItems + i == valid - 1) s_sh = out[i];
+    __syncthreads();
+    if (valid > 0) s = s_sh;
+    if (valid < m && tid == 0) {  // the binade-leaving element, added for real
+      s += wt[valid];
+      if (prefix) prefix[k + valid] = s;
+      s_sh = s;
+    }
+    k += valid < m ? valid + 1 : m;
+    __syncthreads();
+    s = s_sh;
     __syncthreads();
   }
+  return s;
+}
+
+struct BankW {
+  const hwwg_particle* b;
+  __device__ double operator()(uint64_t k) const { return b[k].w; }
+};
+struct ConstW {
+  double v;
+  __device__ double operator()(uint64_t) const { return v; }
+};
+}  // namespace combscan
+
+__global__ void __launch_bounds__(combscan::kThreads) k_comb_prefix(CombArgs a) {
+  // total_weight(bank) (particle.hpp:18-22) is the same sequential sum
+  __shared__ double wt[combscan::kTile];
+  const double W = combscan::serial_sum(combscan::BankW{a.bank}, a.n, a.prefix, wt);
+  const double spacing = W / (double)a.target;
+  // total_weight(result.bank): every tooth carries `spacing`
+  const double ow = a.exact_out_weight ? combscan::serial_sum(combscan::ConstW{spacing}, a.target, nullptr, wt)
+                                       : spacing * (double)a.target;
   if (threadIdx.x == 0) {
-    // total_weight(bank) (particle.hpp:18-22) is the same sequential sum
-    const double W = cum;
-    const double spacing = W / (double)a.target;
     Xoshiro r;
     r.seed(a.seed, a.stream);
     const double offset = r.uniform() * spacing;
     a.scalars[0] = W;
     a.scalars[1] = spacing;
     a.scalars[2] = offset;
-    if (a.exact_out_weight) {
-      double ow = 0.0;  // total_weight(result.bank), every tooth carries `spacing`
-      for (uint64_t k = 0; k < a.target; ++k) ow += spacing;
-      a.scalars[3] = ow;
-    } else {
-      a.scalars[3] = spacing * (double)a.target;
-    }
+    a.scalars[3] = ow;
   }
 }
 
@@ -1041,7 +1163,7 @@ void launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
 }
 
 void launch_comb(const CombArgs& a, cudaStream_t st) {
-  k_comb_prefix<<<1, 256, 0, st>>>(a);
+  k_comb_prefix<<<1, combscan::kThreads, 0, st>>>(a);
   const unsigned blocks = (unsigned)((a.target + 255) / 256);
   k_comb_teeth<<<blocks, 256, 0, st>>>(a);
   HWWG_CUDA(cudaGetLastError());

@@ -21,6 +21,24 @@ struct ChunkLayout {
 };
 ChunkLayout chunk_layout(uint64_t n, uint64_t h_begin, uint64_t H, int I, int B);
 
+// Tally log of the history-parallel exact path: every history (one thread)
+// appends its fp64 contributions (chunk-layout slot, value) in event order to
+// its own chain of kLogBlock-entry blocks; a replay kernel then adds each
+// chunk's entries in history and event order — the reference's chunk-
+// sequential summation — so the physics runs one thread per history instead
+// of one per 256-history chunk.
+constexpr int kLogBlock = 32;
+constexpr int kLogOverflow = -100;  // DevError code: the arena was too small (replay)
+struct ExactLog {
+  unsigned* slot;                 // cap_blocks * kLogBlock
+  double* val;                    // cap_blocks * kLogBlock
+  unsigned* next;                 // cap_blocks: next block of the same history
+  unsigned* first;                // per history: first block (or ~0u)
+  unsigned* count;                // per history: entries
+  unsigned long long* blocks;     // allocated blocks (zeroed per segment)
+  unsigned long long cap_blocks;
+};
+
 // One exact-mode segment: histories [h_begin, h_begin + n) of a step.
 struct ExactArgs {
   const hwwg_particle* src;  // n source particles (AoS, device)
@@ -42,9 +60,12 @@ struct ExactArgs {
   unsigned long long* census_count;
   uint64_t census_cap;
   DevError* err;
+  ExactLog log;  // slot == null: the chunk-serial kernel
 };
 
 void launch_exact_segment(const ExactArgs& a, cudaStream_t s);
+// Whether a segment with this chunk layout takes the history-parallel path
+// (the chunk accumulators of one chunk fit a warp's shared memory).
 
 struct CensusSortArgs {
   const hwwg_particle* records;

@@ -50,7 +50,8 @@ struct Local {
   double leak, aborted;  // chunk-sequential, like StepCounters of a chunk
 };
 
-// Chunk-private fp64 accumulators (one hww::TallySet per chunk).
+// Chunk-private fp64 accumulators (one hww::TallySet per chunk), added to in
+// place by the chunk-serial kernel.
 struct Sink {
   double* track;  // I
   double* cphi;   // I
@@ -61,6 +62,23 @@ struct Sink {
   double* cwb;    // B
   double* trackb; // span*I, batch b stored at (b - b0)
   int b0;
+  int I;
+  Local* c;       // leak / aborted: chunk-sequential registers
+  __device__ __forceinline__ void track_add(int cell, int batch, double v) const {
+    track[cell] += v;
+    trackb[(size_t)(batch - b0) * I + cell] += v;
+  }
+  __device__ __forceinline__ void census_add(int cell, int batch, double phi, double J, double F,
+                                             double w) const {
+    cphi[cell] += phi;
+    cJ[cell] += J;
+    cF[cell] += F;
+    cwb[batch] += w;
+  }
+  __device__ __forceinline__ void edge_add(int e, double v) const { edge[e] += v; }
+  __device__ __forceinline__ void bclo_add(int side, double v) const { bclo[side] += v; }
+  __device__ __forceinline__ void leak_add(double w) const { c->leak += w; }
+  __device__ __forceinline__ void aborted_add(double w) const { c->aborted += w; }
 };
 
 __device__ __forceinline__ void set_error(DevError* e, int code, unsigned long long h) {
@@ -122,8 +140,10 @@ struct History {
   }
 };
 
-// advance_history (transport.cpp:81-192) for source index i into sink S.
-__device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, const Sink& S) {
+// advance_history (transport.cpp:81-192) for source index i into sink S
+// (chunk accumulators, or the tally log of the history-parallel path).
+template <class SinkT>
+__device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, SinkT& S) {
   const unsigned long long h = a.h_begin + i;
   const double2 s0 = reinterpret_cast<const double2*>(a.src)[2 * i];
   const double2 s1 = reinterpret_cast<const double2*>(a.src)[2 * i + 1];
@@ -145,7 +165,6 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
   const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
   const int I = a.mesh.I;
   const double* edges = a.mesh.edges;
-  double* trackb = S.trackb + (size_t)(batch - S.b0) * I;
 
   hs.push(s0.x, s0.y, s1.x, s1.y, start_cell, 1u);
   unsigned long long events = 0;
@@ -161,9 +180,9 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
     while (alive) {
       if (++events > kMaxEventsPerHistory) {  // transport.cpp:111-118
         ++c.u[kEventCapAborts];
-        c.aborted += w;
+        S.aborted_add(w);
         for (int r = 0; r < hs.sp; ++r)
-          for (unsigned j = 0; j < stk[r].count; ++j) c.aborted += stk[r].w;
+          for (unsigned j = 0; j < stk[r].count; ++j) S.aborted_add(stk[r].w);
         hs.sp = 0;
         break;
       }
@@ -185,8 +204,7 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
 
       if (d > 0.0) {  // score_track, tally.hpp:51-56
         const double sc = w * d * (ci.inv_dx * a.inv_dt);
-        S.track[cell] += sc;
-        trackb[cell] += sc;
+        S.track_add(cell, batch, sc);
         atomicAdd(&a.t.tracks[cell], 1ULL);
       }
 
@@ -194,10 +212,7 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
         x += d * mu;
         t = a.t_end;
         const double base = ci.speed * w * ci.inv_dx;  // score_census, tally.hpp:65-72
-        S.cphi[cell] += base;
-        S.cJ[cell] += base * mu;
-        S.cF[cell] += base * (1.0 / 3.0 - mu * mu);
-        S.cwb[batch] += w;
+        S.census_add(cell, batch, base, base * mu, base * (1.0 / 3.0 - mu * mu), w);
         ++c.u[kCensusCount];
         const unsigned long long slot = atomicAdd(a.census_count, 1ULL);
         if (slot < a.census_cap) {
@@ -215,15 +230,15 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
         x = edges[edge];
         t += d / ci.speed;
         const bool domain = edge == 0 || edge == I;
-        S.edge[edge] += (mu > 0 ? w : -w) * a.inv_dt;  // tally.hpp:77-92
+        S.edge_add(edge, (mu > 0 ? w : -w) * a.inv_dt);  // tally.hpp:77-92
         if (domain) {
           const double amu = mu > 0 ? mu : -mu;
           if (amu < kGrazingMu) {
             ++c.u[kGrazingDiscarded];
           } else {
-            S.bclo[edge == 0 ? 0 : 1] += w * (0.5 - amu) / amu * a.inv_dt;
+            S.bclo_add(edge == 0 ? 0 : 1, w * (0.5 - amu) / amu * a.inv_dt);
           }
-          c.leak += w;
+          S.leak_add(w);
           alive = false;
           continue;
         }
@@ -277,6 +292,8 @@ __device__ __forceinline__ Sink chunk_sink(const ExactArgs& a, int c) {
   s.cwb = b + 5 * I + 5;
   s.trackb = b + 5 * I + 5 + a.B;
   s.b0 = batch_of(a.h_begin + (uint64_t)c * kChunk, a.H, a.B);
+  s.I = I;
+  s.c = nullptr;
   return s;
 }
 
@@ -286,9 +303,10 @@ __global__ void __launch_bounds__(64) k_exact_chunks(ExactArgs a) {
   Run stk[kMaxRuns];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.chunks.count) return;
-  const Sink S = chunk_sink(a, c);
+  Sink S = chunk_sink(a, c);
   double* dcnt = a.chunks.base + (size_t)c * a.chunks.stride + 5 * a.mesh.I + 3;
   Local l;
+  S.c = &l;
 #pragma unroll
   for (int k = 0; k < kNumUCounters; ++k) l.u[k] = 0;
   l.leak = dcnt[0];
@@ -302,6 +320,148 @@ __global__ void __launch_bounds__(64) k_exact_chunks(ExactArgs a) {
 #pragma unroll
   for (int k = 0; k < kNumUCounters; ++k)
     if (l.u[k]) atomicAdd(&a.t.ucount[k], l.u[k]);
+}
+
+constexpr size_t kReplaySmemMax = 96 * 1024;
+
+// ---- history-parallel path ------------------------------------------------
+// The tally contributions of one history, in event order, appended to its own
+// block chain in the log (slots of the chunk layout: track 0, census phi I,
+// J 2I, F 3I, edge 4I, bclosure 5I+1, leak 5I+3, aborted 5I+4, census weight
+// by batch 5I+5, track by batch 5I+5+B).
+struct LogSink {
+  ExactLog L;
+  DevError* err;
+  unsigned I, B;
+  int b0;
+  unsigned cur = ~0u, pos = kLogBlock, first = ~0u, total = 0;
+  bool full = false;
+  __device__ __forceinline__ void put(unsigned slot, double v) {
+    if (pos == kLogBlock) {
+      const unsigned long long nb = atomicAdd(L.blocks, 1ULL);
+      if (nb >= L.cap_blocks) {  // the step replays with a larger arena; a full
+        if (!full) atomicCAS(&err->code, 0, kLogOverflow);  // history keeps
+        full = true;                                         // counting its demand
+        atomicMax(L.blocks + 1, nb + 1);
+      } else if (!full) {
+        if (cur == ~0u) first = (unsigned)nb;
+        else L.next[cur] = (unsigned)nb;
+        cur = (unsigned)nb;
+      }
+      pos = 0;
+    }
+    if (!full) {
+      const size_t e = (size_t)cur * kLogBlock + pos;
+      L.slot[e] = slot;
+      L.val[e] = v;
+    }
+    ++pos;
+    ++total;
+  }
+  __device__ __forceinline__ void track_add(int cell, int batch, double v) {
+    put((unsigned)cell, v);
+    put(5 * I + 5 + B + (unsigned)(batch - b0) * I + (unsigned)cell, v);
+  }
+  __device__ __forceinline__ void census_add(int cell, int batch, double phi, double J, double F,
+                                             double w) {
+    put(I + (unsigned)cell, phi);
+    put(2 * I + (unsigned)cell, J);
+    put(3 * I + (unsigned)cell, F);
+    put(5 * I + 5 + (unsigned)batch, w);
+  }
+  __device__ __forceinline__ void edge_add(int e, double v) { put(4 * I + (unsigned)e, v); }
+  __device__ __forceinline__ void bclo_add(int side, double v) { put(5 * I + 1 + side, v); }
+  __device__ __forceinline__ void leak_add(double w) { put(5 * I + 3, w); }
+  __device__ __forceinline__ void aborted_add(double w) { put(5 * I + 4, w); }
+};
+
+// One thread per history: the physics of every history runs concurrently; the
+// fp64 tallies go to the log, integer tallies and counters straight to their
+// (order-free) atomics, census records as in the chunk path.
+__global__ void __launch_bounds__(128) k_exact_histories(ExactArgs a) {
+  Run stk[kMaxRuns];
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool on = i < a.n;
+  Local l;
+#pragma unroll
+  for (int k = 0; k < kNumUCounters; ++k) l.u[k] = 0;
+  if (on) {
+    LogSink S;
+    S.L = a.log;
+    S.err = a.err;
+    S.I = (unsigned)a.mesh.I;
+    S.B = (unsigned)a.B;
+    S.b0 = batch_of(a.h_begin + (i / kChunk) * kChunk, a.H, a.B);
+    run_history(a, i, l, stk, S);
+    a.log.first[i] = S.first;
+    a.log.count[i] = S.total;
+    l.u[kHistoriesScored] = 1;
+  }
+#pragma unroll
+  for (int k = 0; k < kNumUCounters; ++k) {
+    unsigned long long v = l.u[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&a.t.ucount[k], v);
+  }
+}
+
+// One warp per chunk: the chunk's accumulators in shared memory, the log of
+// its histories added in history and event order. 32 consecutive entries are
+// loaded at once; entries with distinct slots commute, entries with the same
+// slot (MATCH.ANY group) are added by the group's first lane in lane order —
+// exactly the chunk-serial sequence of adds per slot.
+template <bool kSmem>
+__global__ void __launch_bounds__(32) k_exact_replay(ExactArgs a) {
+  extern __shared__ double smem_acc[];
+  if (a.err->code == kLogOverflow) return;  // the step replays
+  const ChunkLayout& L = a.chunks;
+  const int c = blockIdx.x;
+  const int lane = threadIdx.x;
+  double* base = L.base + (size_t)c * L.stride;
+  double* acc = kSmem ? smem_acc : base;
+  if (kSmem) {
+    for (size_t k = lane; k < L.stride; k += 32) acc[k] = base[k];
+    __syncwarp();
+  }
+  const uint64_t lo = (uint64_t)c * kChunk;
+  const uint64_t hi = lo + kChunk < a.n ? lo + kChunk : a.n;
+  for (uint64_t h = lo; h < hi; ++h) {
+    unsigned blk = a.log.first[h];
+    unsigned left = a.log.count[h];
+    while (left) {
+      const unsigned n_in = left < kLogBlock ? left : kLogBlock;
+      const bool valid = (unsigned)lane < n_in;
+      unsigned slot = 0;
+      double v = 0.0;
+      if (valid) {
+        slot = a.log.slot[(size_t)blk * kLogBlock + lane];
+        v = a.log.val[(size_t)blk * kLogBlock + lane];
+      }
+      const unsigned grp = __match_any_sync(0xffffffffu, valid ? slot : 0xffffffffu - lane);
+      const bool leader = valid && lane == __ffs(grp) - 1;
+      double s = 0.0;
+      unsigned rest = 0;
+      if (leader) {
+        s = acc[slot] + v;
+        rest = grp & (grp - 1);  // the group's other lanes, ascending
+      }
+      while (__any_sync(0xffffffffu, rest != 0)) {
+        const int src = rest ? __ffs(rest) - 1 : lane;
+        const double o = __shfl_sync(0xffffffffu, v, src);
+        if (rest) {
+          s += o;
+          rest &= rest - 1;
+        }
+      }
+      if (leader) acc[slot] = s;
+      __syncwarp();
+      left -= n_in;
+      if (left) blk = a.log.next[blk];
+    }
+  }
+  if (kSmem)
+    for (size_t k = lane; k < L.stride; k += 32) base[k] = acc[k];
 }
 
 // Chunk accumulators start at zero (a fresh TallySet per chunk,
@@ -425,11 +585,29 @@ ChunkLayout chunk_layout(uint64_t n, uint64_t h_begin, uint64_t H, int I, int B)
   return L;
 }
 
+
 void launch_exact_segment(const ExactArgs& a, cudaStream_t s) {
   if (a.n == 0) return;
   const size_t total = (size_t)a.chunks.count * a.chunks.stride;
   k_chunk_init<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a);
-  k_exact_chunks<<<(unsigned)((a.chunks.count + 63) / 64), 64, 0, s>>>(a);
+  if (a.log.slot) {
+    HWWG_CUDA(cudaMemsetAsync(a.log.blocks, 0, sizeof(unsigned long long), s));
+    k_exact_histories<<<(unsigned)((a.n + 127) / 128), 128, 0, s>>>(a);
+    const size_t smem = a.chunks.stride * sizeof(double);
+    if (smem <= kReplaySmemMax) {  // chunk accumulators in shared memory
+      static size_t configured = 0;
+      if (smem > configured) {
+        HWWG_CUDA(cudaFuncSetAttribute(k_exact_replay<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+      }
+      k_exact_replay<true><<<(unsigned)a.chunks.count, 32, smem, s>>>(a);
+    } else {
+      k_exact_replay<false><<<(unsigned)a.chunks.count, 32, 0, s>>>(a);
+    }
+  } else {
+    k_exact_chunks<<<(unsigned)((a.chunks.count + 63) / 64), 64, 0, s>>>(a);
+  }
   const int slots = 5 * a.mesh.I + 5 + a.B + a.B * a.mesh.I;
   k_merge_chunks<<<(slots + 255) / 256, 256, 0, s>>>(a);
   HWWG_CUDA(cudaGetLastError());

@@ -204,6 +204,51 @@ def test_component_known_answers(engine):
         engine.uniform_comb(np.zeros(0, PARTICLE_DT), 10, 1, 1)
 
 
+def comb_banks():
+    """Adversarial banks for the cumulative-weight walk (popctrl.cpp:15-30): rounding
+    ties at every add, equal weights, a dynamic range of 2^80, zeros, a subnormal
+    head, and a bank larger than one 4096-weight tile many times over."""
+    rng = np.random.default_rng(5)
+    banks = {}
+
+    def bank(w):
+        b = np.zeros(len(w), PARTICLE_DT)
+        b["x"] = rng.uniform(-1, 1, len(w))
+        b["mu"] = rng.uniform(-1, 1, len(w))
+        b["w"] = w
+        b["t"] = 1.0
+        return b
+
+    banks["ones"] = bank(np.ones(70_000))
+    banks["tenths"] = bank(np.full(50_000, 0.1))
+    ulp = 2.0 ** -32  # ulp of 2^20: half- and one-and-a-half-ulp adds tie
+    w = rng.choice(np.array([0.5, 1.5, 1.0, 0.25, 2.5, 0.75]) * ulp, 60_000)
+    w[0] = 2.0 ** 20
+    banks["ties"] = bank(w)
+    w = np.exp(rng.normal(0, 8, 200_000))
+    w[rng.integers(0, w.size, 500)] = 0.0
+    banks["lognormal"] = bank(w)
+    w = rng.exponential(1.0, 30_000)
+    w[:40] = 1e-310
+    w[40:45] = 0.0
+    banks["subnormal_head"] = bank(w)
+    banks["one"] = bank(np.array([3.0]))
+    return banks
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(comb_banks()))
+def test_comb_walk_bit_exact_adversarial(engine, oracle, name):
+    """The parallel binade scan of the comb's sequential fp64 walk equals the serial
+    walk bit for bit: the teeth, W and the output weight."""
+    b = comb_banks()[name]
+    for tgt in (1, 997, 100_003):
+        out, iw, ow = engine.uniform_comb(b, tgt, 3, 17)
+        ro, riw, row = oracle.uniform_comb(b, tgt, 3, 17)
+        assert iw == riw and ow == row, (name, tgt, iw, riw, ow, row)
+        assert out.tobytes() == ro.tobytes(), (name, tgt)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("I,seed", [(400, 1), (37, 2), (510, 3)])
 def test_losm_cached_factorization_is_identical(engine, I, seed):

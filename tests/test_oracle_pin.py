@@ -272,3 +272,15 @@ def test_oracle_config3_components_match_live_reference(oracle):
             out.append((po, Jo))
         assert out[0][0].tobytes() == out[1][0].tobytes()
         assert out[0][1].tobytes() == out[1][1].tobytes()
+
+
+def test_oracle_comb_walk_is_sequential(oracle):
+    """The oracle's comb sums in bank order (np.add.accumulate is the same serial
+    fp64 chain) on the adversarial banks the GPU comb test uses."""
+    from tests.test_gpu_parity import comb_banks
+    for name, b in comb_banks().items():
+        out, iw, ow = oracle.uniform_comb(b, 997, 3, 17)
+        assert iw == np.add.accumulate(b["w"])[-1], name
+        sp = iw / 997
+        assert np.all(out["w"] == sp)
+        assert ow == np.add.accumulate(np.full(997, sp))[-1], name
