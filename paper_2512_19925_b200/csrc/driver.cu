@@ -666,7 +666,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   } else if (do_comb) {
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     d->source.reserve(d->target + vol_cap);
-    d->comb_mem.reserve(4 + d->bank_n);
+    d->comb_mem.reserve(4 + d->bank_n + comb_tile_words(d->bank_n));
     CombArgs a{};
     a.bank = d->bank.p;
     a.n = d->bank_n;
@@ -677,8 +677,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.scalars = d->comb_mem.p;
     a.out = d->source.p;
     a.exact_out_weight = 1;
+    a.tiles = d->comb_mem.p + 4 + d->bank_n;
     launch_comb(a, s);
-    d->launches += 2;
+    d->launches += 6;
     H = d->target;
     rec->comb_in = d->bank_n;
     rec->comb_out = d->target;

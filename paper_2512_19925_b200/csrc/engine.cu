@@ -424,7 +424,7 @@ int hwwg_uniform_comb(hwwg_ctx* c, const hwwg_particle* bank, uint64_t n, uint64
   cudaStream_t s = c->stream;
   c->comb_in.reserve(n);
   c->comb_out.reserve(target);
-  c->scratch.reserve(n + 4);
+  c->scratch.reserve(n + 4 + comb_tile_words(n));
   HWWG_CUDA(cudaMemcpyAsync(c->comb_in.p, bank, n * sizeof(hwwg_particle), cudaMemcpyHostToDevice, s));
   CombArgs a{};
   a.bank = c->comb_in.p;
@@ -436,6 +436,7 @@ int hwwg_uniform_comb(hwwg_ctx* c, const hwwg_particle* bank, uint64_t n, uint64
   a.scalars = c->scratch.p;
   a.out = c->comb_out.p;
   a.exact_out_weight = 1;
+  a.tiles = c->scratch.p + 4 + n;
   launch_comb(a, s);
   double sc[4];
   HWWG_CUDA(cudaMemcpyAsync(sc, c->scratch.p, sizeof sc, cudaMemcpyDeviceToHost, s));

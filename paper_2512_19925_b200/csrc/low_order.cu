@@ -911,30 +911,53 @@ __global__ void k_finalize(FinalizeArgs a) {
 }
 
 // popctrl.cpp:15-30 — the cumulative-weight walk s_k = fl(s_{k-1} + w_k),
-// sequential in bank order, computed by one CTA in parallel and bit for bit.
+// sequential in bank order, computed in parallel and bit for bit.
 //
 // While s stays in one binade [2^e, 2^{e+1}) every s_k is an integer multiple
 // S_k of u = ulp = 2^{e-52}, and with q = w_k / u = a + r (a integer, r in
 // [0, 1), both exact) round-to-nearest-even gives
 //   S_k = S_{k-1} + a + [r > 1/2] + [r == 1/2 and S_{k-1} + a odd]
-// as long as S_{k-1} + a < 2^53. Each element is then a map S -> S + inc(S mod
-// 2); maps compose associatively (an increment per input parity), so a tile
-// of 4096 weights is one block-wide scan of integer pairs. The first element
-// that would leave the binade (or any weight the rule does not cover: zero
-// sum, negative, non-finite, huge) is added by one thread with a real fp64
-// add, and the scan restarts after it in the new binade — ~log2(n) times per
-// bank, as s only grows.
+// as long as S_{k-1} + a < 2^53. Each weight is then a map S -> S + inc(S mod
+// 2); maps compose associatively (an increment per input parity), so a run of
+// weights inside one binade is an integer scan. s only grows, so it changes
+// binade ~log2(n) times; the weight that leaves a binade (or any weight the
+// rule does not cover: zero sum, negative, non-finite, huge) is added with a
+// real fp64 add and the scan restarts after it.
+//
+// Across the bank (4096-weight tiles): an approximate parallel prefix of tile
+// sums predicts each tile's binade; a tile whose predicted range stays well
+// inside one binade gets its composed map (all tiles in parallel); one CTA
+// then walks the tiles in order, applying maps where the exact running sum
+// confirms the prediction and running the in-tile restart scan on the rest
+// (the first tiles and the ~log2(n) binade crossings); all tiles then write
+// their prefix values in parallel.
 namespace combscan {
 constexpr int kThreads = 512, kItems = 8, kTile = kThreads * kItems;
 constexpr uint64_t kTop = 1ULL << 53;
+constexpr uint64_t kSat = 1ULL << 62;
+constexpr int kDirty = -100000;
 
 struct Map {  // S -> S + inc[S & 1]
   uint64_t i0, i1;
 };
-__device__ __forceinline__ Map compose(const Map& f, const Map& g) {  // f then g
-  return Map{f.i0 + ((f.i0 & 1) ? g.i1 : g.i0), f.i1 + (((1 + f.i1) & 1) ? g.i1 : g.i0)};
+__device__ __forceinline__ uint64_t sat_add(uint64_t x, uint64_t y) {
+  const uint64_t z = x + y;
+  return (z < x || z > kSat) ? kSat : z;
 }
-__device__ __forceinline__ uint64_t apply(const Map& f, uint64_t S) { return S + ((S & 1) ? f.i1 : f.i0); }
+// f then g (saturating: a saturated map only ever lands at or past 2^53)
+__device__ __forceinline__ Map compose(const Map& f, const Map& g) {
+  return Map{sat_add(f.i0, (f.i0 & 1) ? g.i1 : g.i0),
+             sat_add(f.i1, ((1 + f.i1) & 1) ? g.i1 : g.i0)};
+}
+__device__ __forceinline__ uint64_t apply(const Map& f, uint64_t S) {
+  return sat_add(S, (S & 1) ? f.i1 : f.i0);
+}
+__device__ __forceinline__ bool in_rule(double s) { return s >= 0x1p-1000 && s < 0x1p1000; }
+__device__ __forceinline__ int binade(double s) {  // s in [2^e, 2^{e+1})
+  int e;
+  frexp(s, &e);
+  return e - 1;
+}
 
 // floor(w / u) (saturated at 2^53) and the rounding class of the remainder
 __device__ __forceinline__ void split(double w, int e, uint64_t& a, int& cls) {
@@ -952,26 +975,51 @@ __device__ __forceinline__ void split(double w, int e, uint64_t& a, int& cls) {
 __device__ __forceinline__ Map elem_map(uint64_t a, int cls) {
   const uint64_t b = a + (cls == 2 ? 1 : 0);
   const int tie = cls == 1;
-  // input parity p: tie rounds up when S + a is odd
+  // input parity p: a tie rounds up when S + a is odd
   return Map{b + (uint64_t)(tie && (b & 1)), b + (uint64_t)(tie && !(b & 1))};
 }
-__device__ __forceinline__ bool in_rule(double s) { return s >= 0x1p-1000 && s < 0x1p1000; }
 
-// Sequential sum of w(k), k in [0, n); prefix (optional) receives s_k. Returns
-// the final sum in every thread. W is a functor k -> weight.
+// Block-wide exclusive scan of one map per thread (thread order); also returns
+// the block aggregate. Uses smem[kThreads / 32].
+__device__ __forceinline__ Map block_exclusive(Map v, Map* smem, Map& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Map inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Map p;
+    p.i0 = __shfl_up_sync(0xffffffffu, inc.i0, o);
+    p.i1 = __shfl_up_sync(0xffffffffu, inc.i1, o);
+    if (lane >= o) inc = compose(p, inc);
+  }
+  if (lane == 31) smem[wid] = inc;
+  __syncthreads();
+  Map before{0, 0};
+  for (int w = 0; w < wid; ++w) before = compose(before, smem[w]);
+  total = before;
+  for (int w = wid; w < kThreads / 32; ++w) total = compose(total, smem[w]);
+  Map ex;
+  ex.i0 = __shfl_up_sync(0xffffffffu, inc.i0, 1);
+  ex.i1 = __shfl_up_sync(0xffffffffu, inc.i1, 1);
+  if (lane > 0) before = compose(before, ex);
+  __syncthreads();
+  return before;
+}
+
+// The sequential walk over weights [k0, k1) from running sum s (one CTA, all
+// threads; every thread returns the final sum); prefix (optional) receives
+// s_k at index k. wt: kTile doubles of shared memory.
 template <class WF>
-__device__ double serial_sum(WF W, uint64_t n, double* prefix, double* wt) {
-  __shared__ Map warp_agg[kThreads / 32];
+__device__ double walk(WF W, uint64_t k0, uint64_t k1, double s, double* prefix, double* wt) {
+  __shared__ Map wagg[kThreads / 32];
   __shared__ unsigned long long cross;
   __shared__ double s_sh;
   __shared__ unsigned long long k_sh;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double s = 0.0;
-  uint64_t k = 0;
-  while (k < n) {
+  const int tid = threadIdx.x;
+  uint64_t k = k0;
+  while (k < k1) {
     if (!in_rule(s)) {  // one thread until s is a normal, finite, positive sum
       if (tid == 0) {
-        while (k < n && !in_rule(s)) {
+        while (k < k1 && !in_rule(s)) {
           s += W(k);
           if (prefix) prefix[k] = s;
           ++k;
@@ -985,16 +1033,13 @@ __device__ double serial_sum(WF W, uint64_t n, double* prefix, double* wt) {
       __syncthreads();
       continue;
     }
-    int e;
-    frexp(s, &e);
-    e -= 1;  // s in [2^e, 2^{e+1})
+    const int e = binade(s);
     const double u = ldexp(1.0, e - 52);
     const uint64_t S0 = (uint64_t)ldexp(s, 52 - e);
-    const uint64_t m = n - k < (uint64_t)kTile ? n - k : (uint64_t)kTile;
+    const uint64_t m = k1 - k < (uint64_t)kTile ? k1 - k : (uint64_t)kTile;
     for (int j = tid; j < kTile; j += kThreads) wt[j] = (uint64_t)j < m ? W(k + j) : 0.0;
     if (tid == 0) cross = ~0ULL;
     __syncthreads();
-    // per-thread map over its kItems consecutive weights
     uint64_t a[kItems];
     int cls[kItems];
     Map agg{0, 0};
@@ -1003,24 +1048,8 @@ __device__ double serial_sum(WF W, uint64_t n, double* prefix, double* wt) {
       split(wt[tid * kItems + i], e, a[i], cls[i]);
       agg = compose(agg, elem_map(a[i], cls[i]));
     }
-    // block-wide exclusive scan of the thread maps
-    Map inc = agg;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Map p;
-      p.i0 = __shfl_up_sync(0xffffffffu, inc.i0, o);
-      p.i1 = __shfl_up_sync(0xffffffffu, inc.i1, o);
-      if (lane >= o) inc = compose(p, inc);
-    }
-    if (lane == 31) warp_agg[wid] = inc;
-    __syncthreads();
-    Map before{0, 0};
-    for (int w = 0; w < wid; ++w) before = compose(before, warp_agg[w]);
-    Map ex;
-    ex.i0 = __shfl_up_sync(0xffffffffu, inc.i0, 1);
-    ex.i1 = __shfl_up_sync(0xffffffffu, inc.i1, 1);
-    if (lane > 0) before = compose(before, ex);
-    // the thread's elements: values, and the first that leaves the binade
+    Map total;
+    const Map before = block_exclusive(agg, wagg, total);
     uint64_t S = apply(before, S0);
     unsigned long long first = ~0ULL;
     double out[kItems];
@@ -1041,13 +1070,13 @@ __device__ double serial_sum(WF W, uint64_t n, double* prefix, double* wt) {
         if (j < valid) prefix[k + j] = out[i];
       }
     }
-    // the last valid value seeds the next round
 #pragma unroll
     for (int i = 0; i < kItems; ++i)
       if (valid > 0 && (uint64_t)tid * kItems + i == valid - 1) s_sh = out[i];
     __syncthreads();
     if (valid > 0) s = s_sh;
-    if (valid < m && tid == 0) {  // the binade-leaving element, added for real
+    __syncthreads();
+    if (valid < m && tid == 0) {  // the binade-leaving weight, added for real
       s += wt[valid];
       if (prefix) prefix[k + valid] = s;
       s_sh = s;
@@ -1060,25 +1089,254 @@ __device__ double serial_sum(WF W, uint64_t n, double* prefix, double* wt) {
   return s;
 }
 
+// Sum of `count` copies of v, sequentially (total_weight of the combed bank):
+// inside a binade the m-fold map is found by binary powering.
+__device__ double const_walk(double v, uint64_t count) {
+  double s = 0.0;
+  uint64_t k = 0;
+  while (k < count) {
+    if (!in_rule(s)) {
+      s += v;
+      ++k;
+      continue;
+    }
+    const int e = binade(s);
+    uint64_t a;
+    int cls;
+    split(v, e, a, cls);
+    if (a >= kTop) {
+      s += v;
+      ++k;
+      continue;
+    }
+    const uint64_t S = (uint64_t)ldexp(s, 52 - e);
+    Map pw[64];
+    pw[0] = elem_map(a, cls);
+    for (int b = 1; b < 64; ++b) pw[b] = compose(pw[b - 1], pw[b - 1]);
+    Map acc{0, 0};
+    uint64_t m = 0;
+    for (int b = 63; b >= 0; --b) {
+      const uint64_t step = 1ULL << b;
+      if (step > count - k - m) continue;
+      const Map t = compose(acc, pw[b]);
+      if (apply(t, S) < kTop) {
+        acc = t;
+        m += step;
+      }
+    }
+    s = (double)apply(acc, S) * ldexp(1.0, e - 52);
+    k += m;
+    if (k < count) {  // the binade-leaving add
+      s += v;
+      ++k;
+    }
+  }
+  return s;
+}
+
 struct BankW {
   const hwwg_particle* b;
   __device__ double operator()(uint64_t k) const { return b[k].w; }
 };
-struct ConstW {
-  double v;
-  __device__ double operator()(uint64_t) const { return v; }
+
+// tile scratch layout (doubles): [0, nt) approximate tile sums, [nt, 2nt)
+// approximate tile starts, [2nt, 3nt) map i0, [3nt, 4nt) map i1, [4nt, 5nt)
+// predicted binade (kDirty: walk the tile), [5nt, 6nt) exact tile start (NaN:
+// the walk wrote the tile)
+struct Tiles {
+  double* base;
+  uint64_t nt;
+  __device__ double* sum() const { return base; }
+  __device__ double* start() const { return base + nt; }
+  __device__ uint64_t* i0() const { return reinterpret_cast<uint64_t*>(base + 2 * nt); }
+  __device__ uint64_t* i1() const { return reinterpret_cast<uint64_t*>(base + 3 * nt); }
+  __device__ int64_t* ebin() const { return reinterpret_cast<int64_t*>(base + 4 * nt); }
+  __device__ double* exact() const { return base + 5 * nt; }
 };
 }  // namespace combscan
 
-__global__ void __launch_bounds__(combscan::kThreads) k_comb_prefix(CombArgs a) {
-  // total_weight(bank) (particle.hpp:18-22) is the same sequential sum
-  __shared__ double wt[combscan::kTile];
-  const double W = combscan::serial_sum(combscan::BankW{a.bank}, a.n, a.prefix, wt);
-  const double spacing = W / (double)a.target;
-  // total_weight(result.bank): every tooth carries `spacing`
-  const double ow = a.exact_out_weight ? combscan::serial_sum(combscan::ConstW{spacing}, a.target, nullptr, wt)
-                                       : spacing * (double)a.target;
+__global__ void __launch_bounds__(256) k_comb_tile_sums(CombArgs a) {
+  using namespace combscan;
+  __shared__ double red[8];
+  const Tiles T{a.tiles, (a.n + kTile - 1) / kTile};
+  const uint64_t k0 = (uint64_t)blockIdx.x * kTile;
+  const uint64_t k1 = k0 + kTile < a.n ? k0 + kTile : a.n;
+  double v = 0.0;
+  for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) v += a.bank[k].w;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
   if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    T.sum()[blockIdx.x] = t;
+  }
+}
+
+// approximate exclusive prefix of the tile sums (one CTA)
+__global__ void __launch_bounds__(1024) k_comb_tile_starts(CombArgs a) {
+  using namespace combscan;
+  __shared__ double part[1024];
+  const Tiles T{a.tiles, (a.n + kTile - 1) / kTile};
+  const uint64_t per = (T.nt + 1023) / 1024;
+  const uint64_t lo = threadIdx.x * per, hi = lo + per < T.nt ? lo + per : T.nt;
+  double v = 0.0;
+  for (uint64_t t = lo; t < hi; ++t) v += T.sum()[t];
+  part[threadIdx.x] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int i = 0; i < 1024; ++i) {
+      const double x = part[i];
+      part[i] = r;
+      r += x;
+    }
+  }
+  __syncthreads();
+  double r = part[threadIdx.x];
+  for (uint64_t t = lo; t < hi; ++t) {
+    T.start()[t] = r;
+    r += T.sum()[t];
+  }
+}
+
+// per tile: the predicted binade and, when the prediction has margin, the
+// tile's composed map
+__global__ void __launch_bounds__(combscan::kThreads) k_comb_tile_maps(CombArgs a) {
+  using namespace combscan;
+  __shared__ Map wagg[kThreads / 32];
+  const Tiles T{a.tiles, (a.n + kTile - 1) / kTile};
+  const uint64_t t = blockIdx.x;
+  const double lo = T.start()[t] * (1.0 - 0x1p-16);
+  const double hi = (T.start()[t] + T.sum()[t]) * (1.0 + 0x1p-16);
+  const bool ok = in_rule(lo) && in_rule(hi) && binade(lo) == binade(hi);
+  if (!ok) {
+    if (threadIdx.x == 0) T.ebin()[t] = kDirty;
+    return;
+  }
+  const int e = binade(lo);
+  const uint64_t k0 = t * kTile;
+  Map agg{0, 0};
+  bool off = false;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = k0 + threadIdx.x * kItems + i;
+    if (k < a.n) {
+      uint64_t q;
+      int cls;
+      split(a.bank[k].w, e, q, cls);
+      off |= q >= kTop;
+      agg = compose(agg, elem_map(q, cls));
+    }
+  }
+  Map total;
+  block_exclusive(agg, wagg, total);
+  off = __syncthreads_or(off);
+  if (threadIdx.x == 0) {
+    T.ebin()[t] = off ? kDirty : e;
+    T.i0()[t] = total.i0;
+    T.i1()[t] = total.i1;
+  }
+}
+
+// One CTA, tiles in order: warp 0 applies maps (32 tiles' maps loaded per
+// round) while the exact running sum confirms each tile's predicted binade and
+// stays inside it; everything else goes through the in-tile walk.
+__global__ void __launch_bounds__(combscan::kThreads) k_comb_tile_walk(CombArgs a) {
+  using namespace combscan;
+  __shared__ double wt[kTile];
+  __shared__ double s_sh;
+  __shared__ unsigned long long t_sh;
+  const Tiles T{a.tiles, (a.n + kTile - 1) / kTile};
+  double s = 0.0;
+  uint64_t t = 0;
+  while (t < T.nt) {
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      bool stop = false;
+      while (!stop && t < T.nt) {
+        const uint64_t tl = t + lane;
+        int64_t e = kDirty;
+        uint64_t i0 = 0, i1 = 0;
+        if (tl < T.nt) {
+          e = T.ebin()[tl];
+          i0 = T.i0()[tl];
+          i1 = T.i1()[tl];
+        }
+        const int cnt = T.nt - t < 32 ? (int)(T.nt - t) : 32;
+        // fast path: the group's tiles predicted in the binade s is in — one warp
+        // scan of their maps, valid up to the first tile that would end at 2^53
+        if (in_rule(s)) {
+          const int es = binade(s);
+          const unsigned same = __ballot_sync(0xffffffffu, lane < cnt && e == es);
+          const int run = same == 0xffffffffu ? 32 : __ffs(~same) - 1;  // leading lanes
+          if (run > 1) {
+            Map inc{i0, i1};
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              Map p;
+              p.i0 = __shfl_up_sync(0xffffffffu, inc.i0, o);
+              p.i1 = __shfl_up_sync(0xffffffffu, inc.i1, o);
+              if (lane >= o) inc = compose(p, inc);
+            }
+            const uint64_t S = (uint64_t)ldexp(s, 52 - es);
+            const uint64_t Se = apply(inc, S);
+            const unsigned good = __ballot_sync(0xffffffffu, lane < run && Se < kTop);
+            const int n_ok = good == 0xffffffffu ? 32 : __ffs(~good) - 1;
+            if (n_ok > 0) {
+              const double u = ldexp(1.0, es - 52);
+              const double s_end = (double)Se * u;
+              const double s_before = __shfl_up_sync(0xffffffffu, s_end, 1);
+              if (lane < n_ok) T.exact()[tl] = lane == 0 ? s : s_before;
+              s = __shfl_sync(0xffffffffu, s_end, n_ok - 1);
+              t += n_ok;
+              if (n_ok < run) stop = true;  // the next tile leaves the binade
+              continue;
+            }
+          }
+        }
+        for (int j = 0; j < cnt; ++j) {  // serial in lane order, every lane in step
+          const int64_t ej = __shfl_sync(0xffffffffu, e, j);
+          const Map f{__shfl_sync(0xffffffffu, i0, j), __shfl_sync(0xffffffffu, i1, j)};
+          if (ej == kDirty || !in_rule(s) || binade(s) != (int)ej) {
+            stop = true;
+            break;
+          }
+          const uint64_t S = (uint64_t)ldexp(s, 52 - (int)ej);
+          const uint64_t Se = apply(f, S);
+          if (Se >= kTop) {
+            stop = true;
+            break;
+          }
+          if (lane == 0) T.exact()[t] = s;
+          s = (double)Se * ldexp(1.0, (int)ej - 52);
+          ++t;
+        }
+      }
+      if (lane == 0) {
+        s_sh = s;
+        t_sh = t;
+      }
+    }
+    __syncthreads();
+    s = s_sh;
+    t = t_sh;
+    __syncthreads();
+    if (t >= T.nt) break;
+    // tile t by the in-tile walk, which writes its prefix values
+    const uint64_t k0 = t * kTile;
+    const uint64_t k1 = k0 + kTile < a.n ? k0 + kTile : a.n;
+    s = walk(BankW{a.bank}, k0, k1, s, a.prefix, wt);
+    if (threadIdx.x == 0) T.exact()[t] = __longlong_as_double(0x7ff8000000000001LL);
+    ++t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // total_weight(bank) (particle.hpp:18-22) is the same sequential sum
+    const double W = s;
+    const double spacing = W / (double)a.target;
+    // total_weight(result.bank): every tooth carries `spacing`
+    const double ow = a.exact_out_weight ? const_walk(spacing, a.target) : spacing * (double)a.target;
     Xoshiro r;
     r.seed(a.seed, a.stream);
     const double offset = r.uniform() * spacing;
@@ -1086,6 +1344,37 @@ __global__ void __launch_bounds__(combscan::kThreads) k_comb_prefix(CombArgs a) 
     a.scalars[1] = spacing;
     a.scalars[2] = offset;
     a.scalars[3] = ow;
+  }
+}
+
+// the mapped tiles' prefix values, from their exact starts (all tiles in parallel)
+__global__ void __launch_bounds__(combscan::kThreads) k_comb_tile_prefix(CombArgs a) {
+  using namespace combscan;
+  __shared__ Map wagg[kThreads / 32];
+  const Tiles T{a.tiles, (a.n + kTile - 1) / kTile};
+  const uint64_t t = blockIdx.x;
+  const double s = T.exact()[t];
+  if (s != s) return;  // walked (NaN marker)
+  const int e = (int)T.ebin()[t];
+  const double u = ldexp(1.0, e - 52);
+  const uint64_t k0 = t * kTile + (uint64_t)threadIdx.x * kItems;
+  uint64_t q[kItems];
+  int cls[kItems];
+  Map agg{0, 0};
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    q[i] = 0;
+    cls[i] = 0;
+    if (k0 + i < a.n) split(a.bank[k0 + i].w, e, q[i], cls[i]);
+    agg = compose(agg, elem_map(q[i], cls[i]));
+  }
+  Map total;
+  const Map before = block_exclusive(agg, wagg, total);
+  uint64_t S = apply(before, (uint64_t)ldexp(s, 52 - e));
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    S = apply(elem_map(q[i], cls[i]), S);
+    if (k0 + i < a.n) a.prefix[k0 + i] = (double)S * u;
   }
 }
 
@@ -1162,8 +1451,15 @@ void launch_finalize(const FinalizeArgs& a, cudaStream_t st) {
   HWWG_CUDA(cudaGetLastError());
 }
 
+size_t comb_tile_words(uint64_t n) { return 6 * ((n + combscan::kTile - 1) / combscan::kTile) + 1; }
+
 void launch_comb(const CombArgs& a, cudaStream_t st) {
-  k_comb_prefix<<<1, combscan::kThreads, 0, st>>>(a);
+  const unsigned nt = (unsigned)((a.n + combscan::kTile - 1) / combscan::kTile);
+  k_comb_tile_sums<<<nt, 256, 0, st>>>(a);
+  k_comb_tile_starts<<<1, 1024, 0, st>>>(a);
+  k_comb_tile_maps<<<nt, combscan::kThreads, 0, st>>>(a);
+  k_comb_tile_walk<<<1, combscan::kThreads, 0, st>>>(a);
+  k_comb_tile_prefix<<<nt, combscan::kThreads, 0, st>>>(a);
   const unsigned blocks = (unsigned)((a.target + 255) / 256);
   k_comb_teeth<<<blocks, 256, 0, st>>>(a);
   HWWG_CUDA(cudaGetLastError());

@@ -96,7 +96,9 @@ struct CombArgs {
   double* scalars;   // [0] W, [1] spacing, [2] offset, [3] output weight
   hwwg_particle* out;
   int exact_out_weight;
+  double* tiles;     // comb_tile_words(n) scratch
 };
+size_t comb_tile_words(uint64_t n);
 void launch_comb(const CombArgs& a, cudaStream_t st);
 
 // Component entry points used by the C ABI (hwwg_build_centers etc.).

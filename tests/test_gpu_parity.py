@@ -2,6 +2,7 @@
 and the golden vectors produced by the real reference. Run on a B200:
 ``python -m pytest tests -m gpu``."""
 import ctypes as C
+import functools
 
 import numpy as np
 import pytest
@@ -204,6 +205,7 @@ def test_component_known_answers(engine):
         engine.uniform_comb(np.zeros(0, PARTICLE_DT), 10, 1, 1)
 
 
+@functools.lru_cache(maxsize=1)
 def comb_banks():
     """Adversarial banks for the cumulative-weight walk (popctrl.cpp:15-30): rounding
     ties at every add, equal weights, a dynamic range of 2^80, zeros, a subnormal
@@ -233,6 +235,9 @@ def comb_banks():
     w[40:45] = 0.0
     banks["subnormal_head"] = bank(w)
     banks["one"] = bank(np.array([3.0]))
+    w = rng.exponential(1.0, 3_000_000)  # ~730 tiles: the mapped-tile path
+    w[1_000_000:1_000_100] = 1e12  # a late jump across many binades
+    banks["exp3M"] = bank(w)
     return banks
 
 
