@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,6 +33,12 @@ struct DevBuf {
       cudaError_t e = cudaMalloc(&p, count * sizeof(T));
       if (e != cudaSuccess) {
         cudaGetLastError();
+        if (std::getenv("HWWG_ALLOC_DEBUG")) {
+          size_t fr = 0, tot = 0;
+          cudaMemGetInfo(&fr, &tot);
+          std::fprintf(stderr, "[hwwg] cudaMalloc of %zu bytes failed (%zu free of %zu)\n",
+                       count * sizeof(T), fr, tot);
+        }
         throw std::bad_alloc();
       }
     }

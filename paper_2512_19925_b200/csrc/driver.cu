@@ -65,7 +65,14 @@ struct FastBankBuf {
     wt.reserve(n);
     meta.reserve(n);
   }
-  uint64_t cap() const { return xm.n; }
+  uint64_t cap() const { return std::min(xm.n, std::min(wt.n, meta.n)); }
+  void release() {
+    for (void* p : {(void*)xm.p, (void*)wt.p, (void*)meta.p})
+      if (p) cudaFree(p);
+    xm.p = wt.p = nullptr;
+    meta.p = nullptr;
+    xm.n = wt.n = meta.n = 0;
+  }
   FastBank view() { return FastBank{xm.p, wt.p, meta.p}; }
   void swap(FastBankBuf& o) {
     std::swap(xm.p, o.xm.p);
@@ -109,6 +116,7 @@ struct hwwg_driver {
   // throughput (Philox) mode: SoA banks, warp split stacks, refill cursor
   bool fast = false;
   uint64_t census_hwm = 0;  // census capacity high-water mark (banks swap each step)
+  uint64_t census_floor = 0;  // the creation-time capacity (64 x H)
   FastBankBuf fbank, fsrc, fcensus;
   DevBuf<FastStackRec> stacks;
   int stack_cap = 1024;
@@ -120,6 +128,7 @@ struct hwwg_driver {
   int smem_mode = 1;  // fast tallies (FastArgs::smem_tallies) outside the cold start
   int scramble = 1;   // FastArgs::scramble outside the cold start
   int agg_all = 0;    // HWWG_FAST_AGG=1: warp-aggregated tallies in every step
+  int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
   DevBuf<double> q_dev;
   const double* q_step = nullptr;
@@ -343,10 +352,12 @@ void init_driver(hwwg_driver* d) {
     // Everything a step can grow into is allocated here, up front: a cudaMalloc
     // inside a step synchronises the device (the step-1 census is x60+ of H,
     // and it becomes step 2's comb input in the other bank of the swap pair).
-    d->census_hwm = 64 * local_target + 4096;
+    d->census_hwm = d->census_floor = 64 * local_target + 4096;
     d->fcensus.reserve(d->census_hwm);
     d->fbank.reserve(d->census_hwm);
     d->fsrc.reserve(std::max<uint64_t>(d->target + (c.vol_rate > 0.0 ? c.vol_histories : 0), 1));
+    // an n-sized fp64 prefix for banks up to the creation-time census mark;
+    // larger banks (single GPU) comb through integer tiles without one
     d->comb_mem.reserve(4 + d->census_hwm);
     d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
     if (c.host_bank) d->bank.reserve(d->census_hwm);
@@ -642,22 +653,27 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     d->fsrc.reserve(d->target + vol_cap);
-    d->comb_mem.reserve(4 + d->bank_n);
-    const size_t tb = fast_comb_temp_bytes(d->bank_n);
-    d->comb_temp.reserve(tb);
+    const bool tiled = d->comb_tiled || d->bank_n > d->census_floor;
+    if (!tiled) {
+      d->comb_mem.reserve(4 + d->bank_n);
+      d->comb_temp.reserve(fast_comb_temp_bytes(d->bank_n));
+    } else {
+      d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
+    }
     FastCombArgs a{};
     a.bank = d->fbank.view();
     a.n = d->bank_n;
     a.target = d->target;
     a.seed = c.seed;
     a.stream = stream_id_host(step, 0, 3);
+    a.temp = d->comb_temp.p;
+    a.temp_bytes = d->comb_temp.n;
     a.prefix = d->comb_mem.p + 4;
     a.scalars = d->comb_mem.p;
     a.out = d->fsrc.view();
-    a.temp = d->comb_temp.p;
-    a.temp_bytes = tb;
     d->ph_mark("comb", s);
-    launch_fast_comb(a, s);
+    if (tiled) launch_fast_comb_tiled(a, s);
+    else launch_fast_comb(a, s);
     d->ph_mark("-", s);
     d->launches += 3;
     H = d->target;
@@ -734,7 +750,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
   }
 
-  if (d->fast) d->fcensus.reserve(d->census_hwm);  // the swapped-in buffer may be short
+  if (d->fast) {  // the swapped-in buffer may be short of the high-water mark
+    try {
+      d->fcensus.reserve(d->census_hwm);
+    } catch (const std::bad_alloc&) {
+      // memory wall: the high-water mark (the cold-start census, x150 of H at
+      // config 4) does not fit next to the bank being combed. Later censuses
+      // are far smaller: size for the creation-time mark and replay if short.
+      d->fcensus.release();
+      d->census_hwm = d->census_floor;
+      d->fcensus.reserve(d->census_hwm);
+    }
+  }
 
   // ---- thresholds (driver.cpp:170-177)
   std::vector<uint64_t> thr;
@@ -1113,8 +1140,16 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     // target particles instead of the raw census (x60 of H after step 1).
     // Enqueued after the record readbacks above, so they see this step's
     // comb scalars.
-    const size_t tb = fast_comb_temp_bytes(d->bank_n);
+    const bool tiled = d->comb_tiled || d->bank_n > d->census_floor;
+    if (!tiled) {
+      d->comb_mem.reserve(4 + d->bank_n);
+      d->comb_temp.reserve(fast_comb_temp_bytes(d->bank_n));
+    } else {
+      d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
+    }
     FastCombArgs a{};
+    a.temp = d->comb_temp.p;
+    a.temp_bytes = d->comb_temp.n;
     a.bank = d->fbank.view();
     a.n = d->bank_n;
     a.target = d->target;
@@ -1123,10 +1158,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.prefix = d->comb_mem.p + 4;
     a.scalars = d->comb_mem.p;
     a.out = d->fsrc.view();
-    a.temp = d->comb_temp.p;
-    a.temp_bytes = tb;
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
-    launch_fast_comb(a, s);
+    if (tiled) launch_fast_comb_tiled(a, s);
+    else launch_fast_comb(a, s);
     launch_fast_to_aos(d->fsrc.view(), d->target, d->bank.p, s);
     d->launches += 4;
     d->pre_comb_in = d->bank_n;
@@ -1257,6 +1291,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_FAST_SMEM")) d->smem_mode = std::atoi(m) % 3;
   if (const char* m = std::getenv("HWWG_FAST_SCRAMBLE")) d->scramble = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_AGG")) d->agg_all = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_COMB_TILED")) d->comb_tiled = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
   d->world = d->opt.world > 1 ? d->opt.world : 1;
   d->rank = d->world > 1 ? d->opt.rank : 0;

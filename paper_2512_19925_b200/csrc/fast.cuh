@@ -107,6 +107,11 @@ struct FastCombArgs {
 };
 size_t fast_comb_temp_bytes(uint64_t n);
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s);
+// The same comb without an n-sized prefix (integer tiles): `prefix` is
+// fast_comb_scratch_words(n) words of scratch, `temp` unused. For banks larger
+// than the preallocated prefix (the config-4 cold-start census).
+size_t fast_comb_scratch_words(uint64_t n);
+void launch_fast_comb_tiled(const FastCombArgs& a, cudaStream_t s);
 // Multi-GPU comb pieces: local inclusive scan (scalars[0] = local total, 0 for
 // an empty bank), and teeth [k_lo, k_hi) placed against origin + local prefix.
 void launch_fast_comb_local_scan(const FastCombArgs& a, cudaStream_t s);

@@ -3,8 +3,9 @@
 //
 // The comb keeps the reference's estimator — teeth spaced W/target apart with
 // one random offset walk the cumulative-weight axis of the bank — but the
-// cumulative weights come from a parallel fp64 scan (CUB decoupled look-back,
-// deterministic for a given bank order) instead of a serial walk, and each
+// cumulative weights come from a parallel scan (CUB fp64 scan into an n-sized
+// prefix; exact fixed-point integers in tiles, with O(n/2048) scratch, for
+// banks beyond the preallocated prefix) instead of a serial walk, and each
 // particle writes the teeth that fall in its cumulative-weight interval.
 // Teeth land in bank order.
 #include <cub/device/device_scan.cuh>
@@ -63,6 +64,191 @@ __global__ void k_comb_scatter(FastCombArgs a) {
     uint64_t s = i;
     while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
     write_teeth(a, s, k1, a.target, spacing);
+  }
+}
+
+// ---- single-GPU comb without an n-sized prefix (memory-wall banks) ---------
+// The cumulative weights are exact integers: every weight becomes
+// floor(w * 2^k) (k chosen so the bank total stays below 2^62), tiles of 2048
+// sum and scan in uint64, so prefixes are associative, monotone and identical
+// on both sides of every tile boundary — each particle recomputes its own
+// prefix in its tile's block scan and writes its teeth. Scratch is O(n/2048)
+// words instead of 8 B per census slot (the step-1 census of config 4 is 1.9e9
+// particles). Quantisation moves a tooth boundary by < n * 2^-62 of the total.
+constexpr int kFcThreads = 256, kFcItems = 8, kFcTile = kFcThreads * kFcItems;
+
+// scratch layout (8-byte words): [0] scale, [1] integer total, [2] spacing in
+// integer units, [3] offset in integer units, [4] done-block counter, then tile
+// sums (fp64) [nt], tile integer sums [nt], tile integer starts [nt]
+struct FcScratch {
+  double* base;
+  uint64_t nt;
+  __device__ double& scale() const { return base[0]; }
+  __device__ unsigned long long& total() const { return reinterpret_cast<unsigned long long*>(base)[1]; }
+  __device__ double& spacing_i() const { return base[2]; }
+  __device__ double& offset_i() const { return base[3]; }
+  __device__ unsigned* done() const { return reinterpret_cast<unsigned*>(base + 4); }
+  __device__ double* fsum() const { return base + 5; }
+  __device__ unsigned long long* isum() const { return reinterpret_cast<unsigned long long*>(base + 5 + nt); }
+  __device__ unsigned long long* istart() const {
+    return reinterpret_cast<unsigned long long*>(base + 5 + 2 * nt);
+  }
+};
+
+__device__ __forceinline__ unsigned long long fixed_w(double w, double scale) {
+  return w > 0.0 ? (unsigned long long)(w * scale) : 0ULL;  // truncation: monotone
+}
+
+// Block (kFcThreads) exclusive scan of one value per thread; returns the
+// thread's exclusive prefix, `total` the block sum (all threads).
+template <class T>
+__device__ __forceinline__ T block_exclusive_256(T v, T* red, T& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T p = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += p;
+  }
+  __syncthreads();  // red reuse
+  if (lane == 31) red[wid] = inc;
+  __syncthreads();
+  T before = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kFcThreads / 32; ++w) {
+    if (w < wid) before += red[w];
+    all += red[w];
+  }
+  total = all;
+  return before + inc - v;
+}
+
+// Is this the last block of the grid to finish? (the counter resets itself)
+__device__ __forceinline__ bool last_block(unsigned* done) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(done, 1u);
+    last = prev == gridDim.x - 1;
+    if (last) *done = 0;
+  }
+  __syncthreads();
+  return last;
+}
+
+// pass 1 (kInteger = false): fp64 tile sums, then the last block derives the
+// fixed-point scale from their total; pass 2: integer tile sums, then the last
+// block scans them into tile starts and writes the comb scalars.
+template <bool kInteger>
+__global__ void __launch_bounds__(kFcThreads) k_fc_tile_sums(FastCombArgs a) {
+  __shared__ double fred[kFcThreads / 32];
+  __shared__ unsigned long long ired[kFcThreads / 32];
+  const FcScratch S{a.prefix, (a.n + kFcTile - 1) / kFcTile};
+  const uint64_t k0 = (uint64_t)blockIdx.x * kFcTile;
+  const double scale = kInteger ? S.scale() : 0.0;
+  double f = 0.0;
+  unsigned long long q = 0;
+  for (int j = threadIdx.x; j < kFcTile; j += kFcThreads) {
+    const uint64_t k = k0 + j;
+    if (k < a.n) {
+      const double w = a.bank.wt[k].x;
+      if (kInteger) q += fixed_w(w, scale);
+      else f += w > 0.0 ? w : 0.0;
+    }
+  }
+  if (kInteger) {
+    unsigned long long t;
+    block_exclusive_256(q, ired, t);
+    if (threadIdx.x == 0) S.isum()[blockIdx.x] = t;
+  } else {
+    double t;
+    block_exclusive_256(f, fred, t);
+    if (threadIdx.x == 0) S.fsum()[blockIdx.x] = t;
+  }
+  if (!last_block(S.done())) return;
+  // the last block: every tile sum is visible (fence + counter)
+  const uint64_t per = (S.nt + kFcThreads - 1) / kFcThreads;
+  const uint64_t lo = threadIdx.x * per < S.nt ? threadIdx.x * per : S.nt;
+  const uint64_t hi = lo + per < S.nt ? lo + per : S.nt;
+  if (!kInteger) {
+    double v = 0.0;
+    for (uint64_t t = lo; t < hi; ++t) v += S.fsum()[t];
+    double W;
+    block_exclusive_256(v, fred, W);
+    if (threadIdx.x == 0) {
+      // total * scale < 2^62 with room for the fp64 sum's own rounding
+      int e = 0;
+      frexp(W > 0.0 ? W * (1.0 + 0x1p-20) : 1.0, &e);
+      S.scale() = ldexp(1.0, 62 - e);
+      a.scalars[0] = W;
+    }
+    return;
+  }
+  unsigned long long v = 0;
+  for (uint64_t t = lo; t < hi; ++t) v += S.isum()[t];
+  unsigned long long r_total;
+  unsigned long long r = block_exclusive_256(v, ired, r_total);
+  for (uint64_t t = lo; t < hi; ++t) {
+    S.istart()[t] = r;
+    r += S.isum()[t];
+  }
+  if (threadIdx.x == 0) {
+    S.total() = r_total;
+    const double W = a.scalars[0];
+    const double spacing = W / (double)a.target;
+    Xoshiro rng;
+    rng.seed(a.seed, a.stream);
+    const double u = rng.uniform();
+    a.scalars[1] = spacing;
+    a.scalars[2] = u * spacing;
+    a.scalars[3] = spacing * (double)a.target;
+    const double sp_i = (double)r_total / (double)a.target;
+    S.spacing_i() = sp_i;
+    S.offset_i() = u * sp_i;
+  }
+}
+
+// Per tile: weights staged through shared memory, exact integer prefixes by a
+// block scan (blocked order), then the teeth written particle-parallel in
+// striped order so consecutive lanes write consecutive teeth.
+__global__ void __launch_bounds__(kFcThreads) k_fc_scatter(FastCombArgs a) {
+  __shared__ double wv[kFcTile];
+  __shared__ unsigned long long P[kFcTile];
+  __shared__ unsigned long long red[kFcThreads / 32];
+  const FcScratch S{a.prefix, (a.n + kFcTile - 1) / kFcTile};
+  const double scale = S.scale(), sp_i = S.spacing_i(), off_i = S.offset_i();
+  const double spacing = a.scalars[1];
+  const uint64_t t0 = (uint64_t)blockIdx.x * kFcTile;
+  const int m = a.n - t0 < (uint64_t)kFcTile ? (int)(a.n - t0) : kFcTile;
+  for (int j = threadIdx.x; j < kFcTile; j += kFcThreads) wv[j] = j < m ? a.bank.wt[t0 + j].x : 0.0;
+  __syncthreads();
+  unsigned long long q[kFcItems];
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int i = 0; i < kFcItems; ++i) {
+    q[i] = fixed_w(wv[threadIdx.x * kFcItems + i], scale);
+    mine += q[i];
+  }
+  unsigned long long tot;
+  unsigned long long run = S.istart()[blockIdx.x] + block_exclusive_256(mine, red, tot);
+#pragma unroll
+  for (int i = 0; i < kFcItems; ++i) {
+    run += q[i];
+    P[threadIdx.x * kFcItems + i] = run;  // inclusive
+  }
+  __syncthreads();
+  const unsigned long long start = S.istart()[blockIdx.x];
+  for (int j = threadIdx.x; j < m; j += kFcThreads) {
+    const uint64_t k = t0 + j;
+    const uint64_t lo = teeth_below((double)(j ? P[j - 1] : start), off_i, sp_i, a.target);
+    const uint64_t hi = teeth_below((double)P[j], off_i, sp_i, a.target);
+    if (lo < hi) write_teeth(a, k, lo, hi, spacing);
+    if (k == a.n - 1 && hi < a.target) {  // stranded teeth (popctrl.cpp:31-37)
+      uint64_t src = k;
+      while (src > 0 && !(fixed_w(a.bank.wt[src].x, scale) > 0)) --src;
+      write_teeth(a, src, hi, a.target, spacing);
+    }
   }
 }
 
@@ -165,13 +351,24 @@ size_t fast_comb_temp_bytes(uint64_t n) {
   return bytes > b2 ? bytes : b2;
 }
 
+size_t fast_comb_scratch_words(uint64_t n) { return 5 + 3 * ((n + kFcTile - 1) / kFcTile) + 4; }
+
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s) {
-  // inclusive scan of the weights straight from the SoA bank
+  // inclusive fp64 scan of the weights straight from the SoA bank (n-sized prefix)
   size_t bytes = a.temp_bytes;
   HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, WeightIt(a.bank.wt, WeightOf()), a.prefix,
                                           (int)a.n, s));
   k_comb_scalars<<<1, 1, 0, s>>>(a.prefix, a.n, a.target, a.seed, a.stream, a.scalars);
   k_comb_scatter<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fast_comb_tiled(const FastCombArgs& a, cudaStream_t s) {
+  const unsigned nt = (unsigned)((a.n + kFcTile - 1) / kFcTile);
+  HWWG_CUDA(cudaMemsetAsync(a.prefix + 4, 0, sizeof(double), s));  // done-block counter
+  k_fc_tile_sums<false><<<nt, kFcThreads, 0, s>>>(a);  // + the scale (last block)
+  k_fc_tile_sums<true><<<nt, kFcThreads, 0, s>>>(a);   // + tile starts, scalars
+  k_fc_scatter<<<nt, kFcThreads, 0, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
 

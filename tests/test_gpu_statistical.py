@@ -127,3 +127,24 @@ def test_config3_philox_step1_within_batch_sigma():
     z = (af["phi_track"][m] - ae["phi_track"][m]) / np.sqrt(ae["sigma"][m] ** 2 + af["sigma"][m] ** 2)
     assert np.mean(np.abs(z) < 3) >= 0.95, np.mean(np.abs(z) < 3)
     assert abs(rf.census_weight / re.census_weight - 1) < 5 * (re.census_weight_sigma + rf.census_weight_sigma) / re.census_weight
+
+
+def test_tiled_comb_matches_prefix_comb(monkeypatch):
+    """The integer-tile comb (banks beyond the preallocated prefix, e.g. the
+    config-4 cold-start census) against the fp64-prefix comb: the same weight
+    bookkeeping, and runs within statistics of each other (the census order of
+    the Philox engine is scheduling-dependent, so runs are not bitwise repeatable)."""
+    H, steps = 100_000, 4
+    base = run(cfg(2, H, steps, 21), hw.RNG_PHILOX)
+    monkeypatch.setenv("HWWG_COMB_TILED", "1")
+    tiled = run(cfg(2, H, steps, 21), hw.RNG_PHILOX)
+    for k, ((r, a), (q, b)) in enumerate(zip(base, tiled)):
+        assert q.comb_out == r.comb_out
+        if k:
+            np.testing.assert_allclose(q.comb_out_weight, q.comb_in_weight, rtol=1e-12)
+        assert abs(q.segments / r.segments - 1) < 0.02
+        assert abs(q.census_weight / r.census_weight - 1) < 0.02
+        sig = np.sqrt(a["sigma"] ** 2 + b["sigma"] ** 2)
+        mask = a["phi_track"] > 1e-2 * a["phi_track"].max()
+        z = np.abs(a["phi_track"] - b["phi_track"])[mask] / sig[mask]
+        assert np.mean(z < 4.0) >= 0.9, (k, np.sort(z)[-8:])
