@@ -127,7 +127,10 @@ struct hwwg_driver {
   DevBuf<unsigned long long> pool_ctl;
   int smem_mode = 1;  // fast tallies (FastArgs::smem_tallies) outside the cold start
   int scramble = 1;   // FastArgs::scramble outside the cold start
-  int agg_all = 0;    // HWWG_FAST_AGG=1: warp-aggregated tallies in every step
+  // warp-aggregated tallies: step 1 always; later steps when the tally
+  // histograms do not fit shared memory (-1, default), every step (1), or
+  // step 1 only (0) — HWWG_FAST_AGG
+  int agg_all = -1;
   int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
   DevBuf<double> q_dev;
@@ -900,9 +903,14 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.b_lo = b_lo;
         fa.nb = b_hi - b_lo + 1;
         // the first step starts from a point pulse: most lanes share a few cells
-        fa.aggregate = (step == 1 || d->agg_all) ? 1 : 0;
+        fa.aggregate = (step == 1 || d->agg_all == 1) ? 1 : 0;
         size_t smem = fast_smem_bytes(I, fa.nb);
         fa.smem_tallies = smem <= 96 * 1024 ? 1 : 0;
+        // global-memory tallies (I >~ 1000 at 20 batches, config 4): same-cell
+        // REDs from ~1e5 resident lanes saturate the L2 atomic units unless
+        // they are warp-aggregated first (config 4: 3.5e9 -> 4.8e9 seg/s at
+        // 1e6 histories, 1.7e9 -> 5.5e9 at 1.25e7)
+        if (!fa.smem_tallies && d->agg_all < 0 && d->smem_mode == 1) fa.aggregate = 1;
         if (!fa.aggregate && d->smem_mode != 1) {
           fa.smem_tallies = d->smem_mode;
           smem = d->smem_mode == 2 ? fast_smem_count_bytes(I) : 0;

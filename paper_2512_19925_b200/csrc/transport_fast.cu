@@ -838,11 +838,18 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell, p.hist, p.key, p.ctr,
                              dau, 0u, 0u};  // base 0: daughters 1..dau
       bool push_local = dau > 0 && !donate;
+      // one pair of atomics per warp: the donated records' active units, then
+      // their slots (ordered before this warp's own decrement by the fence on
+      // the idle path; the donor counts as active meanwhile)
+      const unsigned dmask = __ballot_sync(0xffffffffu, dau > 0 && donate);
+      unsigned long long dbase = 0;
+      if (dmask && lane == 0) {
+        atomicAdd(const_cast<unsigned long long*>(&ctl[2]), (unsigned long long)__popc(dmask));
+        dbase = atomicAdd(const_cast<unsigned long long*>(&ctl[0]), (unsigned long long)__popc(dmask));
+      }
+      dbase = __shfl_sync(0xffffffffu, dbase, 0);
       if (dau > 0 && donate) {
-        // the record's active unit; ordered before this warp's own decrement by
-        // the fence on the idle path, and the donor counts as active meanwhile
-        atomicAdd(const_cast<unsigned long long*>(&ctl[2]), 1ULL);
-        const unsigned long long slot = atomicAdd(const_cast<unsigned long long*>(&ctl[0]), 1ULL);
+        const unsigned long long slot = dbase + __popc(dmask & lt);
         if (slot < a.pool.cap) {
           FastStackRec* pr = a.pool.recs + slot;
           *pr = rec;
