@@ -127,7 +127,7 @@ def main():
         for r in rows:
             ref = r["reference_seg_s"]
             lines.append(
-                f"| {r['config']} | {r["histories"]:.3g} | {r['steps']} | {r['cells']} | "
+                f"| {r['config']} | {r['histories']:.3g} | {r['steps']} | {r['cells']} | "
                 f"{r['philox_seg_s']:.3e} | {r['ms_per_step']:.3f} | {r['exact_seg_s_first3']:.3e} | "
                 + (f"{ref:.3e} | {r['philox_seg_s'] / ref:.0f}x |" if ref else "n/a | n/a |"))
         with open(args.md, "w") as f:
