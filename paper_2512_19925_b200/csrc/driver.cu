@@ -145,6 +145,13 @@ struct hwwg_driver {
   // e2e (host_bank) Philox runs: the bank in host memory is already combed
   bool host_pre_combed = false;
   uint64_t pre_comb_in = 0;
+  // packed wire format of a pre-combed host bank: (x, mu) per particle, then
+  // (w, t) per particle only when they are not one shared pair (host_uniform)
+  bool host_packed = false, host_uniform = false;
+  double host_w0 = 0.0, host_t0 = 0.0;
+  DevBuf<unsigned> uni_flag;
+  DevBuf<double2> uni_first;
+  unsigned* h_uni = nullptr;  // pinned: [0] flag, then (w0, t0) at byte 16
   int flush_replicas = 0;  // FastArgs::flush_replicas (HWWG_FAST_FLUSH_R; 0 = direct REDs, measured best)
   DevBuf<double> flush_scratch;
   bool timeline_on = false;
@@ -221,6 +228,7 @@ struct hwwg_driver {
     if (aux_stream) cudaStreamDestroy(aux_stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (host_bank) cudaFreeHost(host_bank);
+    if (h_uni) cudaFreeHost(h_uni);
     if (comm) ncclCommDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -346,6 +354,9 @@ void init_driver(hwwg_driver* d) {
     HWWG_CUDA(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
     d->h2d_ev.resize(9);
     for (auto& e : d->h2d_ev) HWWG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    HWWG_CUDA(cudaMallocHost(&d->h_uni, 64));
+    d->uni_flag.reserve(1);
+    d->uni_first.reserve(1);
   }
   if (d->fast) {
     const uint64_t local_target = d->target / (uint64_t)d->world + 1;
@@ -601,20 +612,32 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     bounds.push_back(Hs);
     d->bank.reserve(std::max<uint64_t>(Hs, 1));
     const FastBank f = d->fsrc.view();
+    const double2* hb = reinterpret_cast<const double2*>(d->host_bank);
     uint64_t lo = 0;
     for (size_t u = 0; u < bounds.size() && u < d->h2d_ev.size(); ++u) {
       const uint64_t hi = bounds[u];
-      HWWG_CUDA(cudaMemcpyAsync(d->bank.p + lo, d->host_bank + lo, (hi - lo) * sizeof(hwwg_particle),
-                                cudaMemcpyHostToDevice, d->copy_stream));
-      launch_aos_to_fast(d->bank.p + lo, hi - lo, d->prob.view,
-                         FastBank{f.xm + lo, f.wt + lo, f.meta + lo}, lo, d->copy_stream);
+      const FastBank fu{f.xm + lo, f.wt + lo, f.meta + lo};
+      if (d->host_packed) {  // (x, mu) [+ (w, t)] straight into the SoA source
+        HWWG_CUDA(cudaMemcpyAsync(fu.xm, hb + lo, (hi - lo) * sizeof(double2),
+                                  cudaMemcpyHostToDevice, d->copy_stream));
+        if (!d->host_uniform)
+          HWWG_CUDA(cudaMemcpyAsync(fu.wt, hb + Hs + lo, (hi - lo) * sizeof(double2),
+                                    cudaMemcpyHostToDevice, d->copy_stream));
+        launch_xm_to_fast(fu, hi - lo, d->prob.view, lo, d->host_uniform ? 1 : 0, d->host_w0,
+                          d->host_t0, d->copy_stream);
+      } else {
+        HWWG_CUDA(cudaMemcpyAsync(d->bank.p + lo, d->host_bank + lo, (hi - lo) * sizeof(hwwg_particle),
+                                  cudaMemcpyHostToDevice, d->copy_stream));
+        launch_aos_to_fast(d->bank.p + lo, hi - lo, d->prob.view, fu, lo, d->copy_stream);
+      }
       HWWG_CUDA(cudaEventRecord(d->h2d_ev[u], d->copy_stream));
       ++d->launches;
       lo = hi;
       ++n_h2d_chunks;
     }
     d->bank_n = Hs;
-    rec->h2d_bytes += Hs * sizeof(hwwg_particle);
+    rec->h2d_bytes += d->host_packed ? Hs * sizeof(double2) * (d->host_uniform ? 1 : 2)
+                                     : Hs * sizeof(hwwg_particle);
   } else if (c.host_bank) {  // e2e: the bank lives in host memory between steps
     d->bank.reserve(std::max<uint64_t>(d->host_bank_n, 1));
     HWWG_CUDA(cudaMemcpyAsync(d->bank.p, d->host_bank, d->host_bank_n * sizeof(hwwg_particle),
@@ -1169,15 +1192,30 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     if (tiled) launch_fast_comb_tiled(a, s);
     else launch_fast_comb(a, s);
-    launch_fast_to_aos(d->fsrc.view(), d->target, d->bank.p, s);
-    d->launches += 4;
+    d->launches += 3;
     d->pre_comb_in = d->bank_n;
     d->host_pre_combed = true;
     d->host_bank_n = d->target;
     d->bank_n = d->target;
-    rec->d2h_bytes += d->target * sizeof(hwwg_particle);
-    HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, d->target * sizeof(hwwg_particle),
-                              cudaMemcpyDeviceToHost, s));
+    // the packed wire format when the next step uploads by chunks (no
+    // volumetric particles to append): (x, mu) now, (w, t) only if not shared
+    d->host_packed = !(c.vol_rate > 0.0);
+    if (d->host_packed) {
+      launch_check_uniform(d->fsrc.wt.p, d->target, d->uni_flag.p, d->uni_first.p, s);
+      ++d->launches;
+      rec->d2h_bytes += d->target * sizeof(double2) + 32;
+      HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->fsrc.xm.p, d->target * sizeof(double2),
+                                cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaMemcpyAsync(d->h_uni, d->uni_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d->h_uni) + 16, d->uni_first.p,
+                                sizeof(double2), cudaMemcpyDeviceToHost, s));
+    } else {
+      launch_fast_to_aos(d->fsrc.view(), d->target, d->bank.p, s);
+      ++d->launches;
+      rec->d2h_bytes += d->target * sizeof(hwwg_particle);
+      HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, d->target * sizeof(hwwg_particle),
+                                cudaMemcpyDeviceToHost, s));
+    }
   } else if (c.host_bank) {
     if (count > d->host_bank_cap) {
       HWWG_CUDA(cudaStreamSynchronize(s));
@@ -1191,6 +1229,20 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                               cudaMemcpyDeviceToHost, s));
   }
   d->host_tal.fetch(d->tal, s);  // synchronises the stream
+  if (d->host_pre_combed && d->host_packed) {
+    const double* f = reinterpret_cast<const double*>(reinterpret_cast<char*>(d->h_uni) + 16);
+    const bool force_full = std::getenv("HWWG_HOST_FULL") != nullptr;  // tests
+    d->host_uniform = d->h_uni[0] == 0 && !force_full;
+    d->host_w0 = f[0];
+    d->host_t0 = f[1];
+    if (!d->host_uniform) {  // (w, t) differ: they cross too, after the (x, mu) block
+      double2* hb = reinterpret_cast<double2*>(d->host_bank);
+      HWWG_CUDA(cudaMemcpyAsync(hb + d->target, d->fsrc.wt.p, d->target * sizeof(double2),
+                                cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaStreamSynchronize(s));
+      rec->d2h_bytes += d->target * sizeof(double2);
+    }
+  }
   float ms = 0.f;
   HWWG_CUDA(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
   rec->device_ms = ms;
@@ -1412,6 +1464,10 @@ int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t*
     HWWG_CUDA(cudaMemcpyAsync(&c, d->counter.p, sizeof c, cudaMemcpyDeviceToHost, d->stream));
     HWWG_CUDA(cudaStreamSynchronize(d->stream));
     count = c;
+  } else if (d->fast && d->host_pre_combed && d->host_packed) {
+    // the pre-combed source crossed PCIe packed; hand out AoS particles
+    d->bank.reserve(std::max<uint64_t>(d->bank_n, 1));
+    launch_fast_to_aos(d->fsrc.view(), d->bank_n, d->bank.p, d->stream);
   }
   *n = count;
   if (!out || cap < count) return fail(HWWG_ENOSPC, "bank buffer too small");

@@ -121,5 +121,12 @@ void launch_fast_comb_teeth_range(const FastCombArgs& a, double spacing, double 
 // track_flux[i] = sum_b track_flux_batch[b][i] (fast mode scores batches only)
 void launch_track_from_batches(TallyPtrs t, int I, int B, cudaStream_t s);
 void launch_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out, cudaStream_t s);
+// e2e packed host round trip: flag (zeroed here) = 1 unless every (w, t) equals
+// wt[0] (copied to *first); and (x, mu) already in out.xm -> cell, identity
+// hist0 + i, and (w0, t0) when uniform.
+void launch_check_uniform(const double2* wt, uint64_t n, unsigned* flag, double2* first,
+                          cudaStream_t s);
+void launch_xm_to_fast(FastBank out, uint64_t n, const MeshView& m, uint64_t hist0, int uniform,
+                       double w0, double t0, cudaStream_t s);
 
 }  // namespace hwwg

@@ -340,7 +340,46 @@ __global__ void k_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out) {
   o[1] = in.wt[i];
 }
 
+// e2e host round trip, packed wire format: a combed bank carries one (w, t)
+// pair for every particle (w = the comb spacing, t = the census time), so only
+// (x, mu) crosses PCIe. The check flags a bank where that does not hold.
+__global__ void k_check_uniform(const double2* __restrict__ wt, uint64_t n, unsigned* flag,
+                                double2* first) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 v = wt[i], f = wt[0];
+  if (i == 0) *first = f;
+  if (v.x != f.x || v.y != f.y) *flag = 1u;
+}
+
+// (x, mu) from the host into the SoA bank: cell, identity, and (w, t) when the
+// host bank was packed uniform.
+__global__ void k_xm_to_fast(FastBank out, uint64_t n, const MeshView m, uint64_t hist0,
+                             int uniform, double w0, double t0) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = out.xm[i].x;
+  if (uniform) out.wt[i] = make_double2(w0, t0);
+  const int c = locate_cell(m, x);
+  out.meta[i] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)(hist0 + i), 0u, 0u);
+}
+
 }  // namespace
+
+void launch_check_uniform(const double2* wt, uint64_t n, unsigned* flag, double2* first,
+                          cudaStream_t s) {
+  HWWG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned), s));
+  if (!n) return;
+  k_check_uniform<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(wt, n, flag, first);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_xm_to_fast(FastBank out, uint64_t n, const MeshView& m, uint64_t hist0, int uniform,
+                       double w0, double t0, cudaStream_t s) {
+  if (!n) return;
+  k_xm_to_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, m, hist0, uniform, w0, t0);
+  HWWG_CUDA(cudaGetLastError());
+}
 
 using WeightIt = cub::TransformInputIterator<double, WeightOf, const double2*>;
 

@@ -107,11 +107,30 @@ def test_philox_bank_and_host_round_trip():
     for k in range(1, steps):  # steps 2.. open with the device-side pre-comb
         assert erecs[k].comb_out == H
         assert erecs[k].comb_in >= erecs[k - 1].counters.census_count
-        assert erecs[k].h2d_bytes == H * 32
+        assert erecs[k].h2d_bytes == H * 16  # packed: (x, mu); (w, t) shared by the combed bank
         np.testing.assert_allclose(erecs[k].comb_out_weight, erecs[k].comb_in_weight, rtol=1e-12)
     for r, q in zip(recs, erecs):
         assert abs(q.segments / r.segments - 1) < 0.02
         assert abs(q.census_weight / r.census_weight - 1) < 0.02
+
+
+def test_host_round_trip_full_wire_format(monkeypatch):
+    """The packed host round trip's fallback (per-particle (w, t) after the (x, mu)
+    block, used when the combed bank's (w, t) are not one shared pair)."""
+    H, steps = 100_000, 3
+    c = cfg(2, H, steps, 9)
+    c.host_bank = True
+    base = [r for r in (lambda d: [d.step() for _ in range(steps)] + [d.close()])(
+        hw.Driver(c, rng_mode=hw.RNG_PHILOX))[:steps]]
+    monkeypatch.setenv("HWWG_HOST_FULL", "1")
+    d = hw.Driver(c, rng_mode=hw.RNG_PHILOX)
+    full = [d.step() for _ in range(steps)]
+    d.close()
+    for k in range(1, steps):
+        assert full[k].h2d_bytes == H * 32 and base[k].h2d_bytes == H * 16
+        assert full[k].comb_out == H
+        assert abs(full[k].segments / base[k].segments - 1) < 0.02
+        assert abs(full[k].census_weight / base[k].census_weight - 1) < 0.02
 
 
 def test_config3_philox_step1_within_batch_sigma():
