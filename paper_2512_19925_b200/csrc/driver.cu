@@ -1051,12 +1051,19 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->fcensus.reserve(d->census_hwm);  // replay the step with room
       continue;
     }
-    if (derr.code == kLogOverflow && attempt < 3) {  // replay with a log arena that fits
-      d->xlog.ensure_blocks(d->xlog.need(s) + 1024);
-      continue;
+    // replay with room: a log arena that fits (the overflowing histories
+    // counted the demand) and/or a census stage that fits — both at once
+    bool again = false;
+    if (derr.code == kLogOverflow && attempt < 3) {
+      const unsigned long long need = d->xlog.need(s);
+      d->xlog.ensure_blocks(need + need / 4 + 1024);
+      again = true;
     }
-    if (derr.code || count <= ea.census_cap) break;
-    d->stage.ensure(count + count / 4 + 4096);
+    if ((derr.code == 0 || again) && count > ea.census_cap) {
+      d->stage.ensure(count + count / 4 + 4096);
+      again = true;
+    }
+    if (!again) break;
   }
   if (d->timeline_on) print_timeline(d, (int)thr.size() + 1, step);
   unsigned long long fp[12];

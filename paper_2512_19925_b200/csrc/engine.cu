@@ -214,16 +214,19 @@ int hwwg_run_segment_parallel(hwwg_ctx* c, const hwwg_step_context* st,
     HWWG_CUDA(cudaMemcpyAsync(&count, c->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaMemcpyAsync(&derr, c->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaStreamSynchronize(s));
-    if (derr.code == kLogOverflow) {  // replay with a log arena of the right size
+    // deterministic replay with room: the log arena the overflowing histories
+    // counted and/or the census stage, both at once
+    bool again = false;
+    if (derr.code == kLogOverflow) {
       const unsigned long long need = c->xlog.need(s);
-      if (std::getenv("HWWG_XLOG_DEBUG"))
-        std::fprintf(stderr, "[xlog] attempt %d need %llu cap %llu\n", attempt, need, c->xlog.cap);
-      c->xlog.ensure_blocks(need + 1024);
-      continue;
+      c->xlog.ensure_blocks(need + need / 4 + 1024);
+      again = true;
     }
-    if (derr.code) break;
-    if (count <= a.census_cap) break;
-    c->stage.ensure(count + count / 4 + 1024);  // deterministic replay with room
+    if ((derr.code == 0 || again) && count > a.census_cap) {
+      c->stage.ensure(count + count / 4 + 1024);
+      again = true;
+    }
+    if (!again) break;
   }
   if (derr.code == kLogOverflow) return fail(HWWG_ENOMEM, "exact tally log exceeds 2^32 blocks");
   if (derr.code == HWWG_EINVAL)

@@ -43,7 +43,7 @@ struct ExactLogBuf {
     ExactLog L{};
     if (off || n == 0) return L;
     blocks.reserve(2);
-    ensure_blocks(std::max<unsigned long long>(65536, n + n / 2));
+    ensure_blocks(std::max<unsigned long long>(65536, 4 * (unsigned long long)n));
     first.reserve(n);
     count.reserve(n);
     L.slot = slot.p;

@@ -424,40 +424,77 @@ __global__ void __launch_bounds__(32) k_exact_replay(ExactArgs a) {
     for (size_t k = lane; k < L.stride; k += 32) acc[k] = base[k];
     __syncwarp();
   }
+  __shared__ unsigned s_blk[32], s_ord[32];
   const uint64_t lo = (uint64_t)c * kChunk;
   const uint64_t hi = lo + kChunk < a.n ? lo + kChunk : a.n;
-  for (uint64_t h = lo; h < hi; ++h) {
-    unsigned blk = a.log.first[h];
-    unsigned left = a.log.count[h];
-    while (left) {
-      const unsigned n_in = left < kLogBlock ? left : kLogBlock;
-      const bool valid = (unsigned)lane < n_in;
-      unsigned slot = 0;
+  // 32 histories at a time: their logs concatenated in history order, taken
+  // 32 entries per window (lane = entry), so short logs share a window
+  for (uint64_t g = lo; g < hi; g += 32) {
+    const uint64_t h = g + lane;
+    const unsigned cnt = h < hi ? a.log.count[h] : 0u;
+    unsigned cur_blk = h < hi ? a.log.first[h] : 0u;  // lane j: history g + j's block
+    unsigned cur_ord = 0;                             // ... and its ordinal in the chain
+    unsigned inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned p = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += p;
+    }
+    const unsigned off = inc - cnt;  // exclusive: the history's first entry
+    const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+    for (unsigned p = 0; p < total; p += 32) {
+      const unsigned q = p + lane;
+      const bool valid = q < total;
+      // the history holding entry q: the last j with off_j <= q
+      int j = 0;
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1) {
+        const unsigned oc = __shfl_sync(0xffffffffu, off, (j + st) & 31);
+        if (j + st < 32 && oc <= q) j += st;
+      }
+      const unsigned e = q - __shfl_sync(0xffffffffu, off, j);
+      const unsigned ord = e / kLogBlock;
+      const unsigned bj = __shfl_sync(0xffffffffu, cur_blk, j);
+      const unsigned oj = __shfl_sync(0xffffffffu, cur_ord, j);
+      unsigned slot = 0, blk = bj;
       double v = 0.0;
       if (valid) {
-        slot = a.log.slot[(size_t)blk * kLogBlock + lane];
-        v = a.log.val[(size_t)blk * kLogBlock + lane];
+        if (ord != oj) blk = a.log.next[bj];  // a window moves at most one block on
+        const size_t ent = (size_t)blk * kLogBlock + (e % kLogBlock);
+        slot = a.log.slot[ent];
+        v = a.log.val[ent];
+      }
+      // the history's last entry in this window carries its chain position on
+      const int jn = __shfl_down_sync(0xffffffffu, j, 1);
+      if (valid && (lane == 31 || jn != j || q + 1 >= total)) {
+        s_blk[j] = blk;
+        s_ord[j] = ord;
       }
       const unsigned grp = __match_any_sync(0xffffffffu, valid ? slot : 0xffffffffu - lane);
       const bool leader = valid && lane == __ffs(grp) - 1;
-      double s = 0.0;
+      double sum = 0.0;
       unsigned rest = 0;
       if (leader) {
-        s = acc[slot] + v;
+        sum = acc[slot] + v;
         rest = grp & (grp - 1);  // the group's other lanes, ascending
       }
       while (__any_sync(0xffffffffu, rest != 0)) {
         const int src = rest ? __ffs(rest) - 1 : lane;
         const double o = __shfl_sync(0xffffffffu, v, src);
         if (rest) {
-          s += o;
+          sum += o;
           rest &= rest - 1;
         }
       }
-      if (leader) acc[slot] = s;
+      if (leader) acc[slot] = sum;
       __syncwarp();
-      left -= n_in;
-      if (left) blk = a.log.next[blk];
+      // histories seen in this window advance; the others keep their position
+      const bool seen = cnt > 0 && off < p + 32 && off + cnt > p;
+      if (seen) {
+        cur_blk = s_blk[lane];
+        cur_ord = s_ord[lane];
+      }
+      __syncwarp();
     }
   }
   if (kSmem)
@@ -532,15 +569,49 @@ __global__ void k_merge_chunks(ExactArgs a) {
     }
     return;
   }
+  // chunks in order; loads run kAhead chunks ahead of the (sequential) adds
+  constexpr int kAhead = 8;
   double acc = *dst;
-  for (int c = 0; c < L.count; ++c) {
-    const double* cb = L.base + (size_t)c * L.stride;
-    if (local >= 0) {
-      acc += cb[local];
-    } else {
-      const int b0 = batch_of(a.h_begin + (uint64_t)c * kChunk, a.H, B);
-      if (b >= b0 && b < b0 + L.span) acc += cb[5 * I + 5 + B + (size_t)(b - b0) * I + cell];
+  if (local >= 0) {
+    const double* p = L.base + local;
+    int c = 0;
+    for (; c + kAhead <= L.count; c += kAhead) {
+      double v[kAhead];
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) v[k] = p[(size_t)(c + k) * L.stride];
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) acc += v[k];
     }
+    for (; c < L.count; ++c) acc += p[(size_t)c * L.stride];
+  } else {
+    // the chunks whose batch window [b0, b0 + span) holds b form one run
+    // (b0 is non-decreasing in c): find it, then add in chunk order
+    auto b0_of = [&](int c) { return batch_of(a.h_begin + (uint64_t)c * kChunk, a.H, B); };
+    int lo = 0, hi = L.count;  // first c with b0 + span > b
+    while (lo < hi) {
+      const int m = (lo + hi) >> 1;
+      if (b0_of(m) + L.span > b) hi = m;
+      else lo = m + 1;
+    }
+    const int c_lo = lo;
+    hi = L.count;  // first c with b0 > b
+    while (lo < hi) {
+      const int m = (lo + hi) >> 1;
+      if (b0_of(m) > b) hi = m;
+      else lo = m + 1;
+    }
+    const int c_hi = lo;
+    const size_t row = 5 * I + 5 + B + (size_t)cell;
+    int c = c_lo;
+    for (; c + kAhead <= c_hi; c += kAhead) {
+      double v[kAhead];
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k)
+        v[k] = L.base[(size_t)(c + k) * L.stride + row + (size_t)(b - b0_of(c + k)) * I];
+#pragma unroll
+      for (int k = 0; k < kAhead; ++k) acc += v[k];
+    }
+    for (; c < c_hi; ++c) acc += L.base[(size_t)c * L.stride + row + (size_t)(b - b0_of(c)) * I];
   }
   *dst = acc;
 }
