@@ -214,7 +214,15 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
         const double base = ci.speed * w * ci.inv_dx;  // score_census, tally.hpp:65-72
         S.census_add(cell, batch, base, base * mu, base * (1.0 / 3.0 - mu * mu), w);
         ++c.u[kCensusCount];
-        const unsigned long long slot = atomicAdd(a.census_count, 1ULL);
+        // one atomic per group of converged lanes (one thread per history
+        // here, so lanes reach the census at different times)
+        const unsigned amask = __activemask();
+        const int lead = __ffs(amask) - 1;
+        const unsigned lane_id = threadIdx.x & 31;
+        unsigned long long cbase = 0;
+        if ((int)lane_id == lead) cbase = atomicAdd(a.census_count, (unsigned long long)__popc(amask));
+        cbase = __shfl_sync(amask, cbase, lead);
+        const unsigned long long slot = cbase + __popc(amask & ((1u << lane_id) - 1u));
         if (slot < a.census_cap) {
           double2* dst = reinterpret_cast<double2*>(a.census) + 2 * slot;
           dst[0] = make_double2(x, mu);
@@ -335,10 +343,12 @@ struct LogSink {
   unsigned I, B;
   int b0;
   unsigned cur = ~0u, pos = kLogBlock, first = ~0u, total = 0;
+  unsigned long long own = 0;      // the history's first block: its own index, no atomic
+  unsigned long long dyn_base = 0;  // later blocks: dyn_base + a shared counter
   bool full = false;
   __device__ __forceinline__ void put(unsigned slot, double v) {
     if (pos == kLogBlock) {
-      const unsigned long long nb = atomicAdd(L.blocks, 1ULL);
+      const unsigned long long nb = cur == ~0u ? own : dyn_base + atomicAdd(L.blocks, 1ULL);
       if (nb >= L.cap_blocks) {  // the step replays with a larger arena; a full
         if (!full) atomicCAS(&err->code, 0, kLogOverflow);  // history keeps
         full = true;                                         // counting its demand
@@ -392,6 +402,8 @@ __global__ void __launch_bounds__(128) k_exact_histories(ExactArgs a) {
     S.I = (unsigned)a.mesh.I;
     S.B = (unsigned)a.B;
     S.b0 = batch_of(a.h_begin + (i / kChunk) * kChunk, a.H, a.B);
+    S.own = i;
+    S.dyn_base = a.n;
     run_history(a, i, l, stk, S);
     a.log.first[i] = S.first;
     a.log.count[i] = S.total;

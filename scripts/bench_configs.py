@@ -100,6 +100,8 @@ def main():
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
     rows = []
+    run_gpu(cfg(2, 100_000, 3), hw.RNG_PHILOX)  # warm-up: lazy module loading, first launches
+    run_gpu(cfg(2, 100_000, 3), hw.RNG_EXACT)
     for name, which, size, gkw, okw in CASES:
         if args.only and not name.startswith(args.only):
             continue

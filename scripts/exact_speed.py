@@ -15,6 +15,7 @@ import paper_2512_19925_b200 as hw  # noqa: E402
 which = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 H = int(float(sys.argv[2])) if len(sys.argv) > 2 else 1_000_000
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+run_gpu(cfg(which, 100_000, 2), hw.RNG_EXACT)  # warm-up: lazy module loading
 v, ms, seg = run_gpu(cfg(which, H, steps), hw.RNG_EXACT)
 path = "chunks" if os.environ.get("HWWG_EXACT_CHUNKS") else "log"
 print(f"exact[{path}] config {which} H={H} steps={steps}: {v:.3e} seg/s, {ms:.2f} ms/step, {seg} segments")
