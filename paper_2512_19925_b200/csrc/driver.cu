@@ -397,6 +397,10 @@ void init_driver(hwwg_driver* d) {
     }
   } else {
     d->stage.ensure(64 * d->target + 4096);
+    // the tally log arena, up front: the cold-start step logs ~10 blocks per
+    // history at config 2, and growing a multi-GB arena inside a step (free +
+    // malloc + a replay) costs 0.1-0.7 s
+    d->xlog.ensure_blocks(16 * (d->target + 1) + 65536);
   }
   HWWG_CUDA(cudaStreamSynchronize(d->stream));
 }

@@ -436,16 +436,20 @@ __global__ void __launch_bounds__(32) k_exact_replay(ExactArgs a) {
     for (size_t k = lane; k < L.stride; k += 32) acc[k] = base[k];
     __syncwarp();
   }
-  __shared__ unsigned s_blk[32], s_ord[32];
+  __shared__ unsigned s_blk[32], s_ord[32], s_last[32];
   const uint64_t lo = (uint64_t)c * kChunk;
   const uint64_t hi = lo + kChunk < a.n ? lo + kChunk : a.n;
   // 32 histories at a time: their logs concatenated in history order, taken
-  // 32 entries per window (lane = entry), so short logs share a window
+  // 32 entries per window (lane = entry), so short logs share a window. Two-
+  // stage pipeline: window w+1's entries are located and loaded before window
+  // w is summed; a history's first block is its own index, later blocks come
+  // from the chain, whose next link is fetched one window ahead.
   for (uint64_t g = lo; g < hi; g += 32) {
     const uint64_t h = g + lane;
     const unsigned cnt = h < hi ? a.log.count[h] : 0u;
-    unsigned cur_blk = h < hi ? a.log.first[h] : 0u;  // lane j: history g + j's block
-    unsigned cur_ord = 0;                             // ... and its ordinal in the chain
+    unsigned cur_blk = (unsigned)h;  // lane j: history g + j's current block ...
+    unsigned cur_ord = 0;            // ... its ordinal in the chain ...
+    unsigned nreg = ~0u;             // a next link this lane fetched for some history
     unsigned inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -454,10 +458,16 @@ __global__ void __launch_bounds__(32) k_exact_replay(ExactArgs a) {
     }
     const unsigned off = inc - cnt;  // exclusive: the history's first entry
     const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
-    for (unsigned p = 0; p < total; p += 32) {
+    if (lane < 32) s_last[lane] = 32u;  // no prefetched link yet
+    __syncwarp();
+    // locate window p's entries and issue their loads (advances the chain state)
+    auto locate = [&](unsigned p, unsigned& slot, double& v, bool& valid) {
+      // the link prefetched for this lane's history (by the lane in s_last)
+      const unsigned src = s_last[lane];
+      const unsigned got = __shfl_sync(0xffffffffu, nreg, src & 31);
+      const unsigned my_nxt = src < 32 ? got : ~0u;
       const unsigned q = p + lane;
-      const bool valid = q < total;
-      // the history holding entry q: the last j with off_j <= q
+      valid = q < total;
       int j = 0;
 #pragma unroll
       for (int st = 16; st > 0; st >>= 1) {
@@ -468,20 +478,42 @@ __global__ void __launch_bounds__(32) k_exact_replay(ExactArgs a) {
       const unsigned ord = e / kLogBlock;
       const unsigned bj = __shfl_sync(0xffffffffu, cur_blk, j);
       const unsigned oj = __shfl_sync(0xffffffffu, cur_ord, j);
-      unsigned slot = 0, blk = bj;
-      double v = 0.0;
+      const unsigned nj = __shfl_sync(0xffffffffu, my_nxt, j);
+      const unsigned cj = __shfl_sync(0xffffffffu, cnt, j);
+      unsigned blk = bj;
+      slot = 0;
+      v = 0.0;
       if (valid) {
-        if (ord != oj) blk = a.log.next[bj];  // a window moves at most one block on
+        if (ord != oj) blk = nj != ~0u ? nj : a.log.next[bj];  // one block on at most
         const size_t ent = (size_t)blk * kLogBlock + (e % kLogBlock);
         slot = a.log.slot[ent];
         v = a.log.val[ent];
       }
+      __syncwarp();
       // the history's last entry in this window carries its chain position on
+      // and fetches the following link when the log continues past this block
       const int jn = __shfl_down_sync(0xffffffffu, j, 1);
-      if (valid && (lane == 31 || jn != j || q + 1 >= total)) {
+      const bool last = valid && (lane == 31 || jn != j || q + 1 >= total);
+      nreg = ~0u;
+      if (last) {
         s_blk[j] = blk;
         s_ord[j] = ord;
+        if ((ord + 1) * kLogBlock < cj) {
+          nreg = a.log.next[blk];
+          s_last[j] = (unsigned)lane;
+        } else {
+          s_last[j] = 32u;
+        }
       }
+      __syncwarp();
+      const bool seen = cnt > 0 && off < p + 32 && off + cnt > p;
+      if (seen) {
+        cur_blk = s_blk[lane];
+        cur_ord = s_ord[lane];
+      }
+      __syncwarp();
+    };
+    auto add = [&](unsigned slot, double v, bool valid) {
       const unsigned grp = __match_any_sync(0xffffffffu, valid ? slot : 0xffffffffu - lane);
       const bool leader = valid && lane == __ffs(grp) - 1;
       double sum = 0.0;
@@ -500,13 +532,19 @@ __global__ void __launch_bounds__(32) k_exact_replay(ExactArgs a) {
       }
       if (leader) acc[slot] = sum;
       __syncwarp();
-      // histories seen in this window advance; the others keep their position
-      const bool seen = cnt > 0 && off < p + 32 && off + cnt > p;
-      if (seen) {
-        cur_blk = s_blk[lane];
-        cur_ord = s_ord[lane];
-      }
-      __syncwarp();
+    };
+    if (total == 0) continue;
+    unsigned slot_a, slot_b = 0;
+    double v_a, v_b = 0.0;
+    bool ok_a, ok_b = false;
+    locate(0, slot_a, v_a, ok_a);
+    for (unsigned p = 0; p < total; p += 32) {
+      const bool more = p + 32 < total;
+      if (more) locate(p + 32, slot_b, v_b, ok_b);  // in flight while window p is added
+      add(slot_a, v_a, ok_a);
+      slot_a = slot_b;
+      v_a = v_b;
+      ok_a = ok_b;
     }
   }
   if (kSmem)
