@@ -169,6 +169,19 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
   hs.push(s0.x, s0.y, s1.x, s1.y, start_cell, 1u);
   unsigned long long events = 0;
   unsigned seq = 0;
+  // A census record is written one census later (or at the history's end):
+  // the slot atomic's round trip then overlaps the events in between.
+  unsigned long long pend_slot = ~0ULL, pend_key = 0;
+  double2 pend_a = make_double2(0.0, 0.0), pend_b = make_double2(0.0, 0.0);
+  auto flush_census = [&]() {
+    if (pend_slot < a.census_cap) {
+      double2* dst = reinterpret_cast<double2*>(a.census) + 2 * pend_slot;
+      dst[0] = pend_a;
+      dst[1] = pend_b;
+      a.census_keys[pend_slot] = pend_key;
+    }
+    pend_slot = ~0ULL;
+  };
 
   while (hs.sp > 0) {
     Run& top = stk[hs.sp - 1];
@@ -214,21 +227,11 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
         const double base = ci.speed * w * ci.inv_dx;  // score_census, tally.hpp:65-72
         S.census_add(cell, batch, base, base * mu, base * (1.0 / 3.0 - mu * mu), w);
         ++c.u[kCensusCount];
-        // one atomic per group of converged lanes (one thread per history
-        // here, so lanes reach the census at different times)
-        const unsigned amask = __activemask();
-        const int lead = __ffs(amask) - 1;
-        const unsigned lane_id = threadIdx.x & 31;
-        unsigned long long cbase = 0;
-        if ((int)lane_id == lead) cbase = atomicAdd(a.census_count, (unsigned long long)__popc(amask));
-        cbase = __shfl_sync(amask, cbase, lead);
-        const unsigned long long slot = cbase + __popc(amask & ((1u << lane_id) - 1u));
-        if (slot < a.census_cap) {
-          double2* dst = reinterpret_cast<double2*>(a.census) + 2 * slot;
-          dst[0] = make_double2(x, mu);
-          dst[1] = make_double2(w, t);
-          a.census_keys[slot] = (h << 24) | seq;
-        }
+        flush_census();
+        pend_slot = atomicAdd(a.census_count, 1ULL);
+        pend_a = make_double2(x, mu);
+        pend_b = make_double2(w, t);
+        pend_key = (h << 24) | seq;
         ++seq;
         alive = false;
         continue;
@@ -284,6 +287,7 @@ __device__ void run_history(const ExactArgs& a, uint64_t i, Local& c, Run* stk, 
       }
     }
   }
+  flush_census();
 }
 
 __device__ __forceinline__ Sink chunk_sink(const ExactArgs& a, int c) {
