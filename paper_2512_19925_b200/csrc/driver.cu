@@ -408,37 +408,44 @@ void init_driver(hwwg_driver* d) {
 // Diagnostics (HWWG_FAST_TIMELINE=1): per segment, the spread of warp exit
 // times and work, to separate load imbalance from per-event cost.
 void print_timeline(hwwg_driver* d, int nseg, int step) {
-  const size_t per = (size_t)d->timeline_warps * 4;
+  constexpr int K = kTimelineWords;
+  const size_t per = (size_t)d->timeline_warps * K;
   std::vector<unsigned long long> h(per * nseg);
   HWWG_CUDA(cudaMemcpy(h.data(), d->timeline.p, h.size() * 8, cudaMemcpyDeviceToHost));
   for (int s = 0; s < nseg; ++s) {
     const unsigned long long* t = h.data() + per * s;
     unsigned long long t0 = ~0ULL, tmax = 0, evs = 0, evmax = 0;
+    unsigned wmax = 0;  // the warp with the most loop trips
     std::vector<double> ex, sd;
     for (unsigned w = 0; w < d->timeline_warps; ++w) {
-      if (!t[4 * w]) continue;
-      t0 = std::min(t0, t[4 * w]);
-      tmax = std::max(tmax, t[4 * w + 2]);
-      evs += t[4 * w + 3];
-      evmax = std::max(evmax, t[4 * w + 3]);
+      if (!t[K * w]) continue;
+      t0 = std::min(t0, t[K * w]);
+      tmax = std::max(tmax, t[K * w + 2]);
+      evs += t[K * w + 3];
+      evmax = std::max(evmax, t[K * w + 3]);
+      if (t[K * w + 1] > t[K * wmax + 1]) wmax = w;
     }
     for (unsigned w = 0; w < d->timeline_warps; ++w) {
-      if (!t[4 * w]) continue;
-      ex.push_back(1e-3 * (double)(t[4 * w + 2] - t0));
-      sd.push_back((double)t[4 * w + 1]);
+      if (!t[K * w]) continue;
+      ex.push_back(1e-3 * (double)(t[K * w + 2] - t0));
+      sd.push_back((double)t[K * w + 1]);
     }
     std::sort(ex.begin(), ex.end());
     std::sort(sd.begin(), sd.end());
     auto q = [](const std::vector<double>& v, double f) {
       return v.empty() ? 0.0 : v[std::min(v.size() - 1, (size_t)(f * v.size()))];
     };
+    const unsigned long long* m = t + (size_t)K * wmax;
     std::fprintf(stderr,
                  "[timeline] step %d seg %d: span %.1f us, loop trips p50 %.0f max %.0f, "
                  "exit p10 %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f us, events %llu "
-                 "(per warp mean %.0f max %llu)\n",
+                 "(per warp mean %.0f max %llu) | busiest warp %u: start %.1f exit %.1f us, "
+                 "events %llu, max pending %llu, shared %llu, donated %llu, taken %llu\n",
                  step, s, 1e-3 * (double)(tmax - t0), q(sd, 0.5), q(sd, 1.0), q(ex, 0.1),
                  q(ex, 0.5), q(ex, 0.9), q(ex, 0.99), q(ex, 1.0), evs,
-                 (double)evs / std::max<size_t>(ex.size(), 1), evmax);
+                 (double)evs / std::max<size_t>(ex.size(), 1), evmax, wmax,
+                 1e-3 * (double)(m[0] - t0), 1e-3 * (double)(m[2] - t0), m[3], m[4], m[5], m[6],
+                 m[7]);
   }
 }
 
@@ -958,7 +965,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.w_gen = d->prob.w_gen;
         fa.cell0 = d->prob.cells_h[0];
         if (d->timeline_on) {  // HWWG_FAST_TIMELINE: per-warp phase timestamps
-          const size_t per = (size_t)fa.pool.warps * 4;
+          const size_t per = (size_t)fa.pool.warps * kTimelineWords;
           d->timeline.reserve(per * 9);
           fa.timeline = d->timeline.p + per * nseg;
           HWWG_CUDA(cudaMemsetAsync(fa.timeline, 0, per * 8, s));

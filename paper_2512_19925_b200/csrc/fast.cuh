@@ -61,7 +61,7 @@ struct FastArgs {
   FastPool pool;
   DevError* err;
   int seg;  // segment index within the step (diagnostics)
-  unsigned long long* timeline;  // optional per-warp {t0, loop trips, t_exit, events}
+  unsigned long long* timeline;  // optional per-warp words (kTimelineWords)
   unsigned long long* warp_cursor;  // per warp {next, end} of its census chunk (zeroed per step)
   // shared-memory tallies flush into flush_replicas zeroed global replicas
   // (fast_flush_stride words each), folded in by a reduce kernel; 0: direct
@@ -83,6 +83,10 @@ int fast_blocks_per_sm(size_t smem);
 int fast_threads_per_block();
 // per-warp census cursor words (FastArgs::warp_cursor: next, end)
 constexpr int kWarpCursorWords = 2;
+// timeline words per warp: {t0, loop trips, t_exit, events} and, in
+// -DHWWG_FAST_PROF builds, {max pending daughters, pieces shared, split
+// records donated, pool records taken}
+constexpr int kTimelineWords = 8;
 // -DHWWG_FAST_PROF builds: loop phase sums; hist (optional, 8 x 120 x 2
 // unsigned): trips and live lanes per 5 us bin of each segment
 int fast_prof_read(unsigned long long out[12], unsigned* hist);
