@@ -129,8 +129,13 @@ struct hwwg_driver {
   int scramble = 1;   // FastArgs::scramble outside the cold start
   // warp-aggregated tallies: step 1 always; later steps when the tally
   // histograms do not fit shared memory (-1, default), every step (1), or
-  // step 1 only (0) — HWWG_FAST_AGG
+  // step 1 only (0), never (2, tests) — HWWG_FAST_AGG
   int agg_all = -1;
+  // fixed-point track/edge tallies (FastArgs::fix; HWWG_FAST_FIX=0 disables);
+  // step_wref: the largest source weight the step is expected to carry (the
+  // pulse strength, the volumetric source's particle weight)
+  int fix_tallies = 1;
+  double step_wref = 1.0;
   int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
   DevBuf<double> q_dev;
@@ -749,11 +754,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // ---- config-3 volumetric source: this step's particles follow the combed
   // census (histories [H, H + n)); the LOSM gets the step's q
   d->q_step = nullptr;
+  d->step_wref = c.strength;
   if (c.vol_rate > 0.0) {
     const double ta = std::max(rec->t_begin, c.vol_t_lo);
     const double tb = std::min(rec->t_end, c.vol_t_hi);
     if (tb > ta) {
       const uint64_t nv = c.vol_histories;
+      if (nv)
+        d->step_wref = std::max(d->step_wref, c.vol_rate * (tb - ta) *
+                                                  (double)c.histories_per_step / (double)nv);
       std::vector<hwwg_particle> vh(nv);
       sample_volume_source_host(c.seed, step, nv, c.vol_x_lo, c.vol_x_hi, ta, tb, c.vol_rate,
                                 c.histories_per_step, vh.data());
@@ -937,7 +946,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.b_lo = b_lo;
         fa.nb = b_hi - b_lo + 1;
         // the first step starts from a point pulse: most lanes share a few cells
-        fa.aggregate = (step == 1 || d->agg_all == 1) ? 1 : 0;
+        fa.aggregate = ((step == 1 && d->agg_all != 2) || d->agg_all == 1) ? 1 : 0;
         size_t smem = fast_smem_bytes(I, fa.nb);
         fa.smem_tallies = smem <= 96 * 1024 ? 1 : 0;
         // global-memory tallies (I >~ 1000 at 20 batches, config 4): same-cell
@@ -952,6 +961,25 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         if (!fa.smem_tallies) smem = 0;
         smem += fast_smem_centers_bytes(I);
         fa.scramble = fa.aggregate ? 0 : d->scramble;
+        // fixed-point track/edge tallies, where the wider slots keep the
+        // occupancy. Largest expected scores: a window survivor or source
+        // weight (<= max(rho * max centre = rho, step_wref)) times speed/dx
+        // for a track, divided by dt for an edge crossing.
+        fa.fix = 0;
+        if (fa.smem_tallies == 1 && !fa.aggregate && d->flush_replicas == 0 && d->fix_tallies) {
+          const size_t fsm = fast_smem_fix_bytes(I, fa.nb) + fast_smem_centers_bytes(I);
+          double vmax = 0.0;
+          for (const CellInfo& ci : d->prob.cells_h) vmax = std::max(vmax, ci.speed * ci.inv_dx);
+          const double w = std::max(c.rho, d->step_wref);
+          int kt = 0, ke = 0;
+          if (fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
+              fast_blocks_per_sm(fsm) >= fast_blocks_per_sm(smem)) {
+            fa.fix = 1;
+            fa.fix_k_trk = kt;
+            fa.fix_k_edge = ke;
+            smem = fsm;
+          }
+        }
         const int blocks = d->sms * fast_blocks_per_sm(smem);
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
         fa.warp_cursor = d->warp_cursor.p;
@@ -1368,7 +1396,11 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   d->losm_cache = std::getenv("HWWG_LOSM_NOCACHE") == nullptr;
   if (const char* m = std::getenv("HWWG_FAST_SMEM")) d->smem_mode = std::atoi(m) % 3;
   if (const char* m = std::getenv("HWWG_FAST_SCRAMBLE")) d->scramble = std::atoi(m) ? 1 : 0;
-  if (const char* m = std::getenv("HWWG_FAST_AGG")) d->agg_all = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_FAST_AGG")) {
+    const int v = std::atoi(m);
+    d->agg_all = v == 2 ? 2 : (v ? 1 : 0);
+  }
+  if (const char* m = std::getenv("HWWG_FAST_FIX")) d->fix_tallies = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_COMB_TILED")) d->comb_tiled = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
   d->world = d->opt.world > 1 ? d->opt.world : 1;

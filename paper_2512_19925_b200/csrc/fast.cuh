@@ -46,6 +46,9 @@ struct FastArgs {
   int smem_tallies;  // 0 global REDs, 1 shared-memory tallies, 2 fp64 global + counts shared
   int aggregate;     // 1: warp-aggregate tally atomics (cold start: lanes share cells)
   int scramble;      // 1: claim source particles in bit-reversed order within 1024-blocks
+  // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
+  // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
+  int fix, fix_k_trk, fix_k_edge;
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,
   // no per-event table loads.
@@ -93,6 +96,8 @@ int fast_prof_read(unsigned long long out[12], unsigned* hist);
 constexpr int kFastHistWords = 8 * 120 * 2;
 size_t fast_smem_bytes(int I, int nb);
 size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
+size_t fast_smem_fix_bytes(int I, int nb);  // smem_tallies == 1 with fixed-point track/edge slots
+bool fast_fix_exponent(double vmax, int* k);  // grid exponent for the largest expected score
 size_t fast_smem_centers_bytes(int I);  // window centres (after the tallies)
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);
 void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,

@@ -32,6 +32,7 @@
 // when the histograms do not fit in shared memory (I = 4000). The cold-start
 // step warp-aggregates them (MATCH.ANY groups, REDUX fixed-point sums); census
 // scores are run-aggregated across the warp in every step.
+#include <cmath>
 #include <vector>
 
 #include "common.cuh"
@@ -303,27 +304,66 @@ __device__ __forceinline__ void agg_add_count_global(double* base, unsigned long
   agg_add_count_t<unsigned long long>(base, cnt, key, v, cell);
 }
 
+// Fixed-point track and edge tallies (kFix). Shared-memory fp64 adds are CAS
+// loops on sm_100 (ATOMS.CAST.SPIN.64: load, add, compare-and-swap, retry) and
+// sat on every event's dependency chain; 32-bit integer ATOMS.ADD is native
+// and needs no reply. A score v is put on the launch's grid 2^-k (k chosen on
+// the host so the largest expected score is ~2^40 grid units: see
+// fast_fix_exponent) as a 64-bit integer q and added as four 16-bit limbs
+// into four 32-bit words of its slot: independent, fire-and-forget adds.
+// A word takes at most 2^16 adds before it could wrap, so the block reserves
+// its events against a 65535-event budget (s_fixbudget) and a warp past it,
+// or a score beyond 2^62 grid units (and NaN), goes to the global fp64 tally
+// with a native RED instead. The flush recombines the limbs exactly into one
+// fp64 value per slot (three roundings), so a tally carries the fp64 sum of
+// the quantised scores: 2^-40 of the expected largest score, ~1e-12 relative.
+constexpr unsigned kFixBudget = 65535;  // events per block with fixed-point adds
+
+__device__ __forceinline__ double pow2(int k) {  // 2^k, |k| <= 1022
+  return __hiloint2double((k + 1023) << 20, 0);
+}
+
+__device__ __forceinline__ bool fix_add(double* slot, double v, double scale) {
+  const double sv = v * scale;
+  if (!(fabs(sv) < 0x1p62)) return false;  // also NaN
+  const long long q = __double2ll_rn(sv);
+  unsigned* w = reinterpret_cast<unsigned*>(slot);
+  atomicAdd(w + 0, (unsigned)q & 0xffffu);
+  atomicAdd(w + 1, (unsigned)(q >> 16) & 0xffffu);
+  atomicAdd(w + 2, (unsigned)(q >> 32) & 0xffffu);
+  atomicAdd(w + 3, (unsigned)(q >> 48));  // signed top limb, two's complement
+  return true;
+}
+
+__device__ __forceinline__ double fix_value(const double* slot, double inv_scale) {
+  const unsigned* w = reinterpret_cast<const unsigned*>(slot);
+  const double v = (double)(int)w[3] * 0x1p48 + (double)w[2] * 0x1p32 +
+                   (double)w[1] * 0x1p16 + (double)w[0];  // each term exact
+  return v * inv_scale;
+}
+
 // Shared-memory tally views (block-private).
 struct SmemTally {
-  double* trk;    // nb * I, batch b at (b - b_lo)
+  double* trk;    // nb * I, batch b at (b - b_lo); kFix: 16-B limb slots
   double* cphi;   // I
   double* cJ;     // I
   double* cF;     // I
-  double* edge;   // I + 1
+  double* edge;   // I + 1; kFix: 16-B limb slots
   double* cwb;    // nb
   double* bclo;   // 2
   unsigned* trc;  // I
 };
 
-__device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb) {
+// slotw: doubles per track/edge slot (1 fp64, 2 fixed-point limbs)
+__device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb, int slotw) {
   SmemTally s;
   s.trc = reinterpret_cast<unsigned*>(base);  // first: mode 2 keeps only the counts
   s.trk = base + (I + 1) / 2;
-  s.cphi = s.trk + (size_t)nb * I;
+  s.cphi = s.trk + (size_t)slotw * nb * I;
   s.cJ = s.cphi + I;
   s.cF = s.cJ + I;
   s.edge = s.cF + I;
-  s.cwb = s.edge + I + 1;
+  s.cwb = s.edge + (size_t)slotw * (I + 1);
   s.bclo = s.cwb + nb;
   return s;
 }
@@ -331,8 +371,9 @@ __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb) {
 // kShf: the fp64 tallies live in block-private shared memory (smem_tallies ==
 // 1), statically, so the atomics compile to shared-memory CAS loops with no
 // generic-address dispatch.
-template <bool kUniform, bool kShf>
+template <bool kUniform, bool kShf, bool kFix>
 __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastArgs a) {
+  static_assert(kShf || !kFix, "fixed-point tallies live in shared memory");
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -356,10 +397,17 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   // counts in shared memory (shared fp64 adds are CAS loops on sm_100)
   const bool sh = a.smem_tallies != 0;       // shared memory in use (zero + flush)
   constexpr bool shf = kShf;                 // fp64 tallies in shared memory
-  SmemTally S = smem_view(smem, I, a.nb);
+  constexpr int slotw = kFix ? 2 : 1;
+  SmemTally S = smem_view(smem, I, a.nb, slotw);
   // dynamic shared memory: [tallies (mode-dependent words) | window centres I]
-  const size_t tally_words = shf ? (size_t)(a.nb + 4) * I + 1 + a.nb + 2 + (I + 1) / 2
-                                 : (sh ? (size_t)(I + 1) / 2 : 0);
+  const size_t tally_words =
+      shf ? (size_t)slotw * ((size_t)a.nb * I + I + 1) + 3 * (size_t)I + a.nb + 2 + (I + 1) / 2
+          : (sh ? (size_t)(I + 1) / 2 : 0);
+  const double fix_trk = kFix ? pow2(a.fix_k_trk) : 0.0;
+  const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
+  __shared__ unsigned s_fixbudget;  // kFix: events reserved against kFixBudget
+  bool fix_ok = kFix;               // warp-uniform: this warp still adds limbs
+  if (kFix && threadIdx.x == 0) s_fixbudget = 0u;
   for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
   double* s_cent = smem + tally_words;  // read at every window site: keep it on chip
   if (windows)
@@ -628,6 +676,13 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       continue;
     }
     if (!any_alive) continue;
+    if (kFix && fix_ok) {  // reserve this trip's events against the limb budget
+      unsigned used = 0;
+      const unsigned k = __popc(~need);
+      if (lane == 0) used = atomicAdd(&s_fixbudget, k);
+      used = __shfl_sync(0xffffffffu, used, 0);
+      if (used + k > kFixBudget) fix_ok = false;
+    }
     if (p.alive) ++n_ev;
     ++n_iter;
 #ifdef HWWG_FAST_PROF
@@ -792,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     FPROF(2);
     // ---- commit the event's tallies, warp-aggregated (lanes sharing a cell
     // are summed with shuffles first: one CAS per distinct address, not per lane)
-    if (a.aggregate) {  // cold-start segments: most lanes share a few cells
+    if (!kFix && a.aggregate) {  // cold-start segments (never with fixed-point slots): most lanes share a few cells
       if (shf) {
         agg_add_count(S.trk, S.trc, trk_key, trk_v, trk_cell);
         agg_add3(S.cphi, S.cJ, S.cF, cen_cell, cen_phi, cen_J, cen_F);
@@ -813,7 +868,9 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       double* cwb = kShf ? S.cwb : a.t.census_weight_batch;
       double* edg = kShf ? S.edge : a.t.edge_current;
       if (trk_key >= 0) {
-        atomicAdd(trk + trk_key, trk_v);
+        if (!kFix) atomicAdd(trk + trk_key, trk_v);
+        else if (!(fix_ok && fix_add(S.trk + 2 * trk_key, trk_v, fix_trk)))
+          atomicAdd(a.t.track_flux_batch + (size_t)a.b_lo * I + trk_key, trk_v);
         if (sh) atomicAdd(S.trc + trk_cell, 1u);
         else atomicAdd(a.t.tracks + trk_cell, 1ULL);
       }
@@ -828,7 +885,11 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         atomicAdd(cwb + cen_b, cen_w);
       }
 #endif
-      if (edge_key >= 0) atomicAdd(edg + edge_key, edge_v);
+      if (edge_key >= 0) {
+        if (!kFix) atomicAdd(edg + edge_key, edge_v);
+        else if (!(fix_ok && fix_add(S.edge + 2 * edge_key, edge_v, fix_edge)))
+          atomicAdd(a.t.edge_current + edge_key, edge_v);
+      }
     }
 
     FPROF(3);
@@ -926,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   }
 
   // ---- flush block-private tallies
-  if (shf && a.flush_replicas) {
+  if (shf && !kFix && a.flush_replicas) {
     // into one of R global replicas of the smem layout (R-fold less same-address
     // contention than every block adding into the one tally set at segment end);
     // k_flush_reduce folds the replicas into the tallies
@@ -943,8 +1004,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   } else if (shf) {
     __syncthreads();
     const int nb = a.nb;
+    const double inv_trk = kFix ? pow2(-a.fix_k_trk) : 0.0;
+    const double inv_edge = kFix ? pow2(-a.fix_k_edge) : 0.0;
     for (int i = threadIdx.x; i < nb * I; i += blockDim.x) {
-      const double v = S.trk[i];
+      const double v = kFix ? fix_value(S.trk + 2 * i, inv_trk) : S.trk[i];
       if (v != 0.0) atomicAdd(&a.t.track_flux_batch[(size_t)a.b_lo * I + i], v);
     }
     for (int i = threadIdx.x; i < I; i += blockDim.x) {
@@ -953,8 +1016,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (S.cF[i] != 0.0) atomicAdd(&a.t.census_closure[i], S.cF[i]);
       if (S.trc[i]) atomicAdd(&a.t.tracks[i], (unsigned long long)S.trc[i]);
     }
-    for (int i = threadIdx.x; i <= I; i += blockDim.x)
-      if (S.edge[i] != 0.0) atomicAdd(&a.t.edge_current[i], S.edge[i]);
+    for (int i = threadIdx.x; i <= I; i += blockDim.x) {
+      const double v = kFix ? fix_value(S.edge + 2 * i, inv_edge) : S.edge[i];
+      if (v != 0.0) atomicAdd(&a.t.edge_current[i], v);
+    }
     for (int i = threadIdx.x; i < nb; i += blockDim.x)
       if (S.cwb[i] != 0.0) atomicAdd(&a.t.census_weight_batch[a.b_lo + i], S.cwb[i]);
     if (threadIdx.x < 2 && S.bclo[threadIdx.x] != 0.0)
@@ -1045,6 +1110,20 @@ size_t fast_smem_bytes(int I, int nb) {
   return ((size_t)(nb + 4) * I + 1 + nb + 2) * sizeof(double) + (size_t)(I + 1) / 2 * 8 + 16;
 }
 size_t fast_smem_count_bytes(int I) { return (size_t)(I + 1) / 2 * 8 + 16; }
+size_t fast_smem_fix_bytes(int I, int nb) {
+  return ((size_t)2 * ((size_t)nb * I + I + 1) + 3 * (size_t)I + nb + 2) * sizeof(double) +
+         (size_t)(I + 1) / 2 * 8 + 16;
+}
+// Grid exponent k for the fixed-point tallies: the largest expected score
+// (vmax) lands near 2^40 grid units, leaving 2^22 of headroom below the 2^62
+// guard and 2^-40 of vmax as resolution. False when vmax is unusable (the
+// driver then keeps the fp64 layout).
+bool fast_fix_exponent(double vmax, int* k) {
+  if (!(vmax > 0.0) || !std::isfinite(vmax)) return false;
+  const int e = 40 - std::ilogb(vmax);
+  *k = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+  return true;
+}
 size_t fast_smem_centers_bytes(int I) { return (size_t)I * 8; }
 size_t fast_flush_stride(int I, int B) { return (size_t)(B + 4) * I + 1 + B + 2 + I; }
 
@@ -1074,7 +1153,7 @@ void configure_fast_kernel();
 int fast_blocks_per_sm(size_t smem) {
   configure_fast_kernel();
   int n = 0;
-  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment<true, true>, kThreads, smem));
+  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment<true, true, false>, kThreads, smem));
   return n;
 }
 
@@ -1095,8 +1174,9 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
 void configure_fast_kernel() {
   static bool configured = false;
   if (!configured) {
-    for (auto k : {k_fast_segment<false, false>, k_fast_segment<false, true>,
-                   k_fast_segment<true, false>, k_fast_segment<true, true>})
+    for (auto k : {k_fast_segment<false, false, false>, k_fast_segment<false, true, false>,
+                   k_fast_segment<true, false, false>, k_fast_segment<true, true, false>,
+                   k_fast_segment<false, true, true>, k_fast_segment<true, true, true>})
       HWWG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
@@ -1107,12 +1187,15 @@ void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_
   k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head,
                                   (unsigned long long)blocks * kWarpsPerBlock);
   const bool shf = a.smem_tallies == 1;
-  if (a.uniform && shf) k_fast_segment<true, true><<<blocks, kThreads, smem, s>>>(a);
-  else if (a.uniform) k_fast_segment<true, false><<<blocks, kThreads, smem, s>>>(a);
-  else if (shf) k_fast_segment<false, true><<<blocks, kThreads, smem, s>>>(a);
-  else k_fast_segment<false, false><<<blocks, kThreads, smem, s>>>(a);
+  const bool fix = shf && a.fix;
+  if (a.uniform && fix) k_fast_segment<true, true, true><<<blocks, kThreads, smem, s>>>(a);
+  else if (a.uniform && shf) k_fast_segment<true, true, false><<<blocks, kThreads, smem, s>>>(a);
+  else if (a.uniform) k_fast_segment<true, false, false><<<blocks, kThreads, smem, s>>>(a);
+  else if (fix) k_fast_segment<false, true, true><<<blocks, kThreads, smem, s>>>(a);
+  else if (shf) k_fast_segment<false, true, false><<<blocks, kThreads, smem, s>>>(a);
+  else k_fast_segment<false, false, false><<<blocks, kThreads, smem, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
-  if (shf && a.flush_replicas) {
+  if (shf && !fix && a.flush_replicas) {
     k_flush_reduce<<<32, 256, 0, s>>>(a.flush_scratch, a.flush_replicas, a.flush_stride, a.mesh.I,
                                       a.nb, a.b_lo, a.t);
     HWWG_CUDA(cudaGetLastError());

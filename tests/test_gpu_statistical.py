@@ -167,3 +167,28 @@ def test_tiled_comb_matches_prefix_comb(monkeypatch):
         mask = a["phi_track"] > 1e-2 * a["phi_track"].max()
         z = np.abs(a["phi_track"] - b["phi_track"])[mask] / sig[mask]
         assert np.mean(z < 4.0) >= 0.9, (k, np.sort(z)[-8:])
+
+
+def test_fixed_point_tallies_match_fp64(monkeypatch):
+    """The fixed-point track/edge tallies (16-bit limbs on native 32-bit shared
+    atomics) against the fp64 CAS tallies on the same events: one config-2 step
+    with per-lane (not warp-aggregated) tallies throughout, so both runs see
+    the same counter-based Philox histories and differ only in the tally
+    arithmetic (quantisation 2^-40 of the largest expected score, and fp64
+    summation order)."""
+    monkeypatch.setenv("HWWG_FAST_AGG", "2")
+    out = {}
+    for fix in ("1", "0"):
+        monkeypatch.setenv("HWWG_FAST_FIX", fix)
+        out[fix] = run(cfg(2, 100_000, 1, 13), hw.RNG_PHILOX)[0]
+    (rq, aq), (rd, ad) = out["1"], out["0"]
+    kq, kd = rq.counters.as_dict(), rd.counters.as_dict()
+    for k in ("collisions", "census_count", "splits", "split_daughters", "roulette_kills"):
+        assert kq[k] == kd[k], (k, kq[k], kd[k])
+    assert rq.segments == rd.segments
+    np.testing.assert_array_equal(aq["tracks_per_cell"], ad["tracks_per_cell"])
+    np.testing.assert_allclose(aq["phi_track"], ad["phi_track"], rtol=1e-10,
+                               atol=1e-12 * ad["phi_track"].max())
+    np.testing.assert_allclose(aq["sigma"], ad["sigma"], rtol=1e-7, atol=1e-12 * ad["sigma"].max())
+    scale = np.abs(ad["edge_current"]).max()
+    np.testing.assert_allclose(aq["edge_current"], ad["edge_current"], rtol=0, atol=1e-10 * scale)
