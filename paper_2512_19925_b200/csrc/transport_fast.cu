@@ -229,9 +229,10 @@ __device__ __forceinline__ void agg_add3(double* b0, double* b1, double* b2, int
 // slot, so per-lane CAS loops on these addresses serialise (measured: about
 // half of the steady-state transport time). A segmented Hillis-Steele scan
 // over the warp (non-census lanes carry zeros) costs a fixed 5 steps.
-__device__ __forceinline__ void census_runs(double* cphi, double* cJ, double* cF, double* cwb,
-                                            int cell, int b, double v0, double v1, double v2,
-                                            double v3) {
+// AddCell(cell, s0, s1, s2): the run's phi/J/F adds (fp64 or fixed-point slots)
+template <class AddCell>
+__device__ __forceinline__ void census_runs(AddCell add_cell, double* cwb, int cell, int b,
+                                            double v0, double v1, double v2, double v3) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const bool c = cell >= 0;
@@ -260,11 +261,7 @@ __device__ __forceinline__ void census_runs(double* cphi, double* cJ, double* cF
   }
   const unsigned above = cm & ~upto;  // census lanes after this one
   const int next = above ? __ffs(above) - 1 : -1;
-  if (c && (next < 0 || ((heads >> next) & 1u))) {  // last census lane of its run
-    atomicAdd(cphi + cell, s0);
-    atomicAdd(cJ + cell, s1);
-    atomicAdd(cF + cell, s2);
-  }
+  if (c && (next < 0 || ((heads >> next) & 1u))) add_cell(cell, s0, s1, s2);  // last lane of its run
   // the census weight by batch: runs keyed by the batch slot alone (usually one
   // run per warp: all its census lanes hold histories of one batch)
   const int pb = __shfl_sync(full, b, prev);
@@ -304,7 +301,7 @@ __device__ __forceinline__ void agg_add_count_global(double* base, unsigned long
   agg_add_count_t<unsigned long long>(base, cnt, key, v, cell);
 }
 
-// Fixed-point track and edge tallies (kFix). Shared-memory fp64 adds are CAS
+// Fixed-point track, edge and census phi/J/F tallies (kFix). Shared-memory fp64 adds are CAS
 // loops on sm_100 (ATOMS.CAST.SPIN.64: load, add, compare-and-swap, retry) and
 // sat on every event's dependency chain; 32-bit integer ATOMS.ADD is native
 // and needs no reply. A score v is put on the launch's grid 2^-k (k chosen on
@@ -360,9 +357,9 @@ __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb, int 
   s.trc = reinterpret_cast<unsigned*>(base);  // first: mode 2 keeps only the counts
   s.trk = base + (I + 1) / 2;
   s.cphi = s.trk + (size_t)slotw * nb * I;
-  s.cJ = s.cphi + I;
-  s.cF = s.cJ + I;
-  s.edge = s.cF + I;
+  s.cJ = s.cphi + (size_t)slotw * I;
+  s.cF = s.cJ + (size_t)slotw * I;
+  s.edge = s.cF + (size_t)slotw * I;
   s.cwb = s.edge + (size_t)slotw * (I + 1);
   s.bclo = s.cwb + nb;
   return s;
@@ -401,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   SmemTally S = smem_view(smem, I, a.nb, slotw);
   // dynamic shared memory: [tallies (mode-dependent words) | window centres I]
   const size_t tally_words =
-      shf ? (size_t)slotw * ((size_t)a.nb * I + I + 1) + 3 * (size_t)I + a.nb + 2 + (I + 1) / 2
+      shf ? (size_t)slotw * ((size_t)a.nb * I + 4 * (size_t)I + 1) + a.nb + 2 + (I + 1) / 2
           : (sh ? (size_t)(I + 1) / 2 : 0);
   const double fix_trk = kFix ? pow2(a.fix_k_trk) : 0.0;
   const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
@@ -876,7 +873,26 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       }
 #if !defined(HWWG_CENSUS_PER_LANE)
       // census scores: run-aggregated across the warp (census_runs)
-      census_runs(cphi, cJ, cF, cwb, cen_cell, cen_b, cen_phi, cen_J, cen_F, cen_w);
+      if (kFix) {
+        census_runs(
+            [&](int cell, double s0, double s1, double s2) {
+              if (!(fix_ok && fix_add(S.cphi + 2 * cell, s0, fix_trk)))
+                atomicAdd(a.t.census_phi + cell, s0);
+              if (!(fix_ok && fix_add(S.cJ + 2 * cell, s1, fix_trk)))
+                atomicAdd(a.t.census_current + cell, s1);
+              if (!(fix_ok && fix_add(S.cF + 2 * cell, s2, fix_trk)))
+                atomicAdd(a.t.census_closure + cell, s2);
+            },
+            cwb, cen_cell, cen_b, cen_phi, cen_J, cen_F, cen_w);
+      } else {
+        census_runs(
+            [&](int cell, double s0, double s1, double s2) {
+              atomicAdd(cphi + cell, s0);
+              atomicAdd(cJ + cell, s1);
+              atomicAdd(cF + cell, s2);
+            },
+            cwb, cen_cell, cen_b, cen_phi, cen_J, cen_F, cen_w);
+      }
 #else
       if (cen_cell >= 0) {
         atomicAdd(cphi + cen_cell, cen_phi);
@@ -1011,9 +1027,12 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (v != 0.0) atomicAdd(&a.t.track_flux_batch[(size_t)a.b_lo * I + i], v);
     }
     for (int i = threadIdx.x; i < I; i += blockDim.x) {
-      if (S.cphi[i] != 0.0) atomicAdd(&a.t.census_phi[i], S.cphi[i]);
-      if (S.cJ[i] != 0.0) atomicAdd(&a.t.census_current[i], S.cJ[i]);
-      if (S.cF[i] != 0.0) atomicAdd(&a.t.census_closure[i], S.cF[i]);
+      const double vp = kFix ? fix_value(S.cphi + 2 * i, inv_trk) : S.cphi[i];
+      const double vj = kFix ? fix_value(S.cJ + 2 * i, inv_trk) : S.cJ[i];
+      const double vf = kFix ? fix_value(S.cF + 2 * i, inv_trk) : S.cF[i];
+      if (vp != 0.0) atomicAdd(&a.t.census_phi[i], vp);
+      if (vj != 0.0) atomicAdd(&a.t.census_current[i], vj);
+      if (vf != 0.0) atomicAdd(&a.t.census_closure[i], vf);
       if (S.trc[i]) atomicAdd(&a.t.tracks[i], (unsigned long long)S.trc[i]);
     }
     for (int i = threadIdx.x; i <= I; i += blockDim.x) {
@@ -1111,7 +1130,7 @@ size_t fast_smem_bytes(int I, int nb) {
 }
 size_t fast_smem_count_bytes(int I) { return (size_t)(I + 1) / 2 * 8 + 16; }
 size_t fast_smem_fix_bytes(int I, int nb) {
-  return ((size_t)2 * ((size_t)nb * I + I + 1) + 3 * (size_t)I + nb + 2) * sizeof(double) +
+  return ((size_t)2 * ((size_t)nb * I + 4 * (size_t)I + 1) + nb + 2) * sizeof(double) +
          (size_t)(I + 1) / 2 * 8 + 16;
 }
 // Grid exponent k for the fixed-point tallies: the largest expected score

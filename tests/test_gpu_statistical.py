@@ -170,7 +170,7 @@ def test_tiled_comb_matches_prefix_comb(monkeypatch):
 
 
 def test_fixed_point_tallies_match_fp64(monkeypatch):
-    """The fixed-point track/edge tallies (16-bit limbs on native 32-bit shared
+    """The fixed-point track, edge and census tallies (16-bit limbs on native 32-bit shared
     atomics) against the fp64 CAS tallies on the same events: one config-2 step
     with per-lane (not warp-aggregated) tallies throughout, so both runs see
     the same counter-based Philox histories and differ only in the tally
@@ -192,3 +192,6 @@ def test_fixed_point_tallies_match_fp64(monkeypatch):
     np.testing.assert_allclose(aq["sigma"], ad["sigma"], rtol=1e-7, atol=1e-12 * ad["sigma"].max())
     scale = np.abs(ad["edge_current"]).max()
     np.testing.assert_allclose(aq["edge_current"], ad["edge_current"], rtol=0, atol=1e-10 * scale)
+    for k in ("phi_census", "current_census", "closure_census", "ww_centers"):
+        scale = np.abs(ad[k]).max()
+        np.testing.assert_allclose(aq[k], ad[k], rtol=0, atol=1e-10 * scale, err_msg=k)
