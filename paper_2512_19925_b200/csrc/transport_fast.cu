@@ -263,7 +263,16 @@ __device__ __forceinline__ void census_runs(AddCell add_cell, double* cwb, int c
   const int next = above ? __ffs(above) - 1 : -1;
   if (c && (next < 0 || ((heads >> next) & 1u))) add_cell(cell, s0, s1, s2);  // last lane of its run
   // the census weight by batch: runs keyed by the batch slot alone (usually one
-  // run per warp: all its census lanes hold histories of one batch)
+  // run per warp: all its census lanes hold histories of one batch, which
+  // takes a plain butterfly sum)
+  const int b0 = __shfl_sync(full, b, __ffs(cm) - 1);
+  if (!__any_sync(full, c && b != b0)) {
+    double w = c ? v3 : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(full, w, o);
+    if (lane == __ffs(cm) - 1) atomicAdd(cwb + b0, w);
+    return;
+  }
   const int pb = __shfl_sync(full, b, prev);
   const bool hb_head = c && (prev == lane || pb != b);
   const unsigned bheads = __ballot_sync(full, hb_head);
@@ -315,6 +324,7 @@ __device__ __forceinline__ void agg_add_count_global(double* base, unsigned long
 // fp64 value per slot (three roundings), so a tally carries the fp64 sum of
 // the quantised scores: 2^-40 of the expected largest score, ~1e-12 relative.
 constexpr unsigned kFixBudget = 65535;  // events per block with fixed-point adds
+constexpr unsigned kFixChunk = 256;     // budget a warp reserves at a time
 
 __device__ __forceinline__ double pow2(int k) {  // 2^k, |k| <= 1022
   return __hiloint2double((k + 1023) << 20, 0);
@@ -404,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
   __shared__ unsigned s_fixbudget;  // kFix: events reserved against kFixBudget
   bool fix_ok = kFix;               // warp-uniform: this warp still adds limbs
+  unsigned fix_left = 0;            // events of this warp's current budget reservation
   if (kFix && threadIdx.x == 0) s_fixbudget = 0u;
   for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
   double* s_cent = smem + tally_words;  // read at every window site: keep it on chip
@@ -673,12 +684,16 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       continue;
     }
     if (!any_alive) continue;
-    if (kFix && fix_ok) {  // reserve this trip's events against the limb budget
-      unsigned used = 0;
+    if (kFix && fix_ok) {  // this trip's events against the limb budget, reserved 256 at a time
       const unsigned k = __popc(~need);
-      if (lane == 0) used = atomicAdd(&s_fixbudget, k);
-      used = __shfl_sync(0xffffffffu, used, 0);
-      if (used + k > kFixBudget) fix_ok = false;
+      if (fix_left < k) {
+        unsigned used = 0;
+        if (lane == 0) used = atomicAdd(&s_fixbudget, kFixChunk);
+        used = __shfl_sync(0xffffffffu, used, 0);
+        if (used + kFixChunk > kFixBudget) fix_ok = false;
+        else fix_left += kFixChunk;
+      }
+      fix_left -= k;
     }
     if (p.alive) ++n_ev;
     ++n_iter;
