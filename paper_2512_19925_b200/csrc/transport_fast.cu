@@ -87,7 +87,10 @@ constexpr int kThreads = 32 * kWarpsPerBlock;
 #endif
 constexpr unsigned kDonate = HWWG_KDONATE;  // pending local daughters above which splits go global
 constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
-constexpr unsigned kClaim = 32;  // source particles a warp reserves per claim
+#ifndef HWWG_KCLAIM
+#define HWWG_KCLAIM 16  // measured: 32 -> 16 is +2% on config 2 (fewer late-started reservations)
+#endif
+constexpr unsigned kClaim = HWWG_KCLAIM;  // source particles a warp reserves per claim
 constexpr unsigned kShare = HWWG_KSHARE;
 #ifndef HWWG_POLL_EVERY
 #define HWWG_POLL_EVERY 4
