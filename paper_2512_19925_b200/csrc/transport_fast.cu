@@ -88,9 +88,18 @@ constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kDonate = HWWG_KDONATE;  // pending local daughters above which splits go global
 constexpr unsigned kCensusChunk = 64;  // census slots a warp reserves at a time
 #ifndef HWWG_KCLAIM
-#define HWWG_KCLAIM 16  // measured: 32 -> 16 is +2% on config 2 (fewer late-started reservations)
+#define HWWG_KCLAIM 32
 #endif
 constexpr unsigned kClaim = HWWG_KCLAIM;  // source particles a warp reserves per claim
+#ifndef HWWG_KCLAIM_TAIL
+#define HWWG_KCLAIM_TAIL 4
+#endif
+constexpr unsigned kClaimTail = HWWG_KCLAIM_TAIL;  // claim size near the end of the source
+// (measured on config 2: 32 static + 4 in the last 2 claims per warp, 8.0e9 ->
+// 8.3e9 seg/s against uniform 16-particle claims)
+#ifndef HWWG_CLAIM_ZONE
+#define HWWG_CLAIM_ZONE 2  // the tail zone, in kClaim-particle claims per warp
+#endif
 constexpr unsigned kShare = HWWG_KSHARE;
 #ifndef HWWG_POLL_EVERY
 #define HWWG_POLL_EVERY 4
@@ -451,6 +460,11 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   else if (r_hi > n_src) r_hi = n_src;
   unsigned r_next = 0;
   bool r_pend = false;
+  // claim size: kClaim, then kClaimTail once a claim lands in the last
+  // HWWG_CLAIM_ZONE * kClaim particles per warp of the source, so the final reservations do
+  // not pin a warp's worth of unstarted histories while other warps idle
+  unsigned csz = kClaim;
+  const unsigned tail_zone = gridDim.x * kWarpsPerBlock * kClaim * (unsigned)HWWG_CLAIM_ZONE;
   unsigned long long ticket = ~0ULL;  // lane 0: pool slot this warp waits on
 
   FPROF_DECL
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (r_lo == r_hi) {
         unsigned nb = 0;
         if (lane == 0)
-          nb = r_pend ? r_next : (unsigned)atomicAdd(a.src_head, (unsigned long long)kClaim);
+          nb = r_pend ? r_next : (unsigned)atomicAdd(a.src_head, (unsigned long long)csz);
         nb = __shfl_sync(0xffffffffu, nb, 0);
         r_pend = false;
         if (nb >= n_src) {
@@ -572,7 +586,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           break;
         }
         r_lo = nb;
-        r_hi = nb + kClaim < n_src ? nb + kClaim : n_src;
+        r_hi = nb + csz < n_src ? nb + csz : n_src;
+        if (n_src - nb < tail_zone) csz = kClaimTail;
       }
       const unsigned k = __popc(need);
       const unsigned avail = r_hi - r_lo;
@@ -821,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     // ---- look-ahead source claim: the reservation is spent and lanes will need
     // particles; the atomic's latency hides behind the census and tally work
     if (r_lo == r_hi && !r_pend && !src_done) {
-      if (lane == 0) r_next = (unsigned)atomicAdd(a.src_head, (unsigned long long)kClaim);
+      if (lane == 0) r_next = (unsigned)atomicAdd(a.src_head, (unsigned long long)csz);
       r_pend = true;
     }
     // ---- bank census particles. Slots come from a per-warp chunk of the census
