@@ -135,6 +135,10 @@ struct hwwg_driver {
   // step_wref: the largest source weight the step is expected to carry (the
   // pulse strength, the volumetric source's particle weight)
   int fix_tallies = 1;
+  // transport events per history of the last completed step (segments per
+  // history; 100 before any: config 2's cold start runs 73), to predict
+  // whether a launch stays inside the fixed-point tallies' per-block budget
+  double events_per_history = 100.0;
   double step_wref = 1.0;
   int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
@@ -960,26 +964,34 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         }
         if (!fa.smem_tallies) smem = 0;
         smem += fast_smem_centers_bytes(I);
-        fa.scramble = fa.aggregate ? 0 : d->scramble;
-        // fixed-point track/edge tallies, where the wider slots keep the
-        // occupancy. Largest expected scores: a window survivor or source
-        // weight (<= max(rho * max centre = rho, step_wref)) times speed/dx
-        // for a track, divided by dt for an edge crossing.
+        // fixed-point track/edge/census tallies, where the wider slots keep the
+        // occupancy — in the cold start too, where native same-address limb
+        // adds beat the warp aggregation (config 2 step 1: 5.97 -> 4.84 ms of
+        // transport) unless aggregation is forced (HWWG_FAST_AGG=1). Largest
+        // expected scores: a window survivor or source weight (<= max(rho *
+        // max centre = rho, step_wref)) times speed/dx for a track, divided by
+        // dt for an edge crossing.
         fa.fix = 0;
-        if (fa.smem_tallies == 1 && !fa.aggregate && d->flush_replicas == 0 && d->fix_tallies) {
+        if (fa.smem_tallies == 1 && (!fa.aggregate || d->agg_all != 1) && d->flush_replicas == 0 &&
+            d->fix_tallies) {
           const size_t fsm = fast_smem_fix_bytes(I, fa.nb) + fast_smem_centers_bytes(I);
           double vmax = 0.0;
           for (const CellInfo& ci : d->prob.cells_h) vmax = std::max(vmax, ci.speed * ci.inv_dx);
           const double w = std::max(c.rho, d->step_wref);
           int kt = 0, ke = 0;
+          const int bps = fast_blocks_per_sm(fsm);
+          const double per_block = (double)(g_hi - g_lo) * d->events_per_history /
+                                   (double)std::max(1, d->sms * bps);
           if (fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
-              fast_blocks_per_sm(fsm) >= fast_blocks_per_sm(smem)) {
+              bps >= fast_blocks_per_sm(smem) && per_block <= (double)kFastFixBudget) {
             fa.fix = 1;
             fa.fix_k_trk = kt;
             fa.fix_k_edge = ke;
+            fa.aggregate = 0;
             smem = fsm;
           }
         }
+        fa.scramble = fa.aggregate ? 0 : d->scramble;
         const int blocks = d->sms * fast_blocks_per_sm(smem);
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
         fa.warp_cursor = d->warp_cursor.p;
@@ -1324,6 +1336,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   for (int i = 0; i < I; ++i) seg += d->h_tracks[i];
   rec->segments = seg;
   rec->histories = H;
+  if (H) d->events_per_history = (double)seg / (double)H;
   // banked particles (fast mode: the census slots also hold zero-weight chunk tails)
   rec->census_size = d->fast ? (uint64_t)u[kCensusCount] : count;
   rec->comb_in_weight = comb_sc[0];

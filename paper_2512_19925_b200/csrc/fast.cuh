@@ -97,6 +97,7 @@ constexpr int kFastHistWords = 8 * 120 * 2;
 size_t fast_smem_bytes(int I, int nb);
 size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
 size_t fast_smem_fix_bytes(int I, int nb);  // smem_tallies == 1 with fixed-point track/edge slots
+constexpr unsigned kFastFixBudget = 65535;  // transport events per block with fixed-point adds
 bool fast_fix_exponent(double vmax, int* k);  // grid exponent for the largest expected score
 size_t fast_smem_centers_bytes(int I);  // window centres (after the tallies)
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);

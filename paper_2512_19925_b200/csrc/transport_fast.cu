@@ -335,7 +335,7 @@ __device__ __forceinline__ void agg_add_count_global(double* base, unsigned long
 // with a native RED instead. The flush recombines the limbs exactly into one
 // fp64 value per slot (three roundings), so a tally carries the fp64 sum of
 // the quantised scores: 2^-40 of the expected largest score, ~1e-12 relative.
-constexpr unsigned kFixBudget = 65535;  // events per block with fixed-point adds
+constexpr unsigned kFixBudget = kFastFixBudget;  // events per block with fixed-point adds
 constexpr unsigned kFixChunk = 256;     // budget a warp reserves at a time
 
 __device__ __forceinline__ double pow2(int k) {  // 2^k, |k| <= 1022
@@ -890,6 +890,16 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         agg_add(a.t.census_weight_batch, cen_b, cen_w);
         agg_add(a.t.edge_current, edge_key, edge_v);
       }
+    } else if (kFix && !fix_ok) {
+      // this block's limb budget is spent: warp-aggregated adds straight to
+      // the global fp64 tallies (per-lane REDs would saturate the L2 atomic
+      // units on same-cell adds, cf. the cold start)
+      agg_add(a.t.track_flux_batch + (size_t)a.b_lo * I, trk_key, trk_v);
+      if (trk_key >= 0) atomicAdd(S.trc + trk_cell, 1u);
+      agg_add3(a.t.census_phi, a.t.census_current, a.t.census_closure, cen_cell, cen_phi, cen_J,
+               cen_F);
+      agg_add(S.cwb, cen_b, cen_w);
+      agg_add(a.t.edge_current, edge_key, edge_v);
     } else {  // spread population: per-lane atomics, no warp synchronisation
       double* trk = kShf ? S.trk : a.t.track_flux_batch;
       double* cphi = kShf ? S.cphi : a.t.census_phi;
