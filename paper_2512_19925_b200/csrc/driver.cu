@@ -895,6 +895,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     ea.err = d->err.p;
     if (!d->fast) d->xlog.reset_need(s);
     uint64_t h_done = 0;
+    bool pool_reset_done = false;  // the mid-step update reset the pool counters
     for (size_t u = 0; u <= thr.size(); ++u) {
       const uint64_t h_stop = u < thr.size() ? thr[u] : H;
       ea.src = d->source.p + h_done;
@@ -910,6 +911,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
       if (d->fast) {
         FastArgs fa{};
+        fa.pool_reset_done = pool_reset_done ? 1 : 0;
+        pool_reset_done = false;
         // this rank's part of the segment: global [h_done, h_stop) ∩ its shard
         uint64_t g_lo = h_done, g_hi = h_stop;
         if (d->world > 1) {
@@ -1054,6 +1057,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       }
       const double effective = (double)c.histories_per_step * (double)h_done / (double)H;
       a.snapshot_inv_norm = 1.0 / effective;
+      if (d->fast) {  // the next segment's pool reset rides on this launch
+        a.pool_ctl = d->pool_ctl.p;
+        a.pool_src_head = d->src_head.p;
+        pool_reset_done = true;
+      }
       a.s = d->lo;
       d->ph_mark("losm1", s);
       launch_low_order_update(a, s);

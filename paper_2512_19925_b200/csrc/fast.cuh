@@ -30,6 +30,22 @@ struct FastPool {
   unsigned warps;  // warps in the grid
 };
 
+// Pool counter reset before a transport launch, independent of its grid:
+// active warps = kPoolSentinel (the kernel's first thread swaps in its warp
+// count), source claims counted from the end of the static reservations.
+constexpr unsigned long long kPoolSentinel = 1ULL << 40;
+__device__ __forceinline__ void fast_pool_reset(unsigned long long* ctl,
+                                                unsigned long long* src_head) {
+  ctl[0] = 0;
+  ctl[1] = 0;
+  ctl[2] = kPoolSentinel;  // every warp starts active (holding source work)
+  ctl[3] = 0;              // no backlog declared yet
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  ctl[4] = t;  // segment start (diagnostics)
+  *src_head = 0;
+}
+
 struct FastArgs {
   FastBank src;  // this segment's source particles
   unsigned long long n_src;
@@ -49,6 +65,7 @@ struct FastArgs {
   // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
   // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
   int fix, fix_k_trk, fix_k_edge;
+  int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,
   // no per-event table loads.

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "fast.cuh"
 #include "low_order.cuh"
 #include "rng.cuh"
 
@@ -702,6 +703,7 @@ constexpr int kSmemStateMaxI = 1200;
 __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a);
 
 __global__ void __launch_bounds__(kCtaThreads) k_low_order_update(LowOrderArgs a) {
+  if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head);
   if (!a.smem_state) {
     low_order_update_body(a);
     return;

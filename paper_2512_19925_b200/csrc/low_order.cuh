@@ -67,6 +67,10 @@ struct LowOrderArgs {
   const double* closure_tally;  // mode 1: census_closure accumulator (I)
   const double* bclosure_tally; // mode 1: boundary closure accumulators (2)
   double snapshot_inv_norm;     // mode 1: 1 / (H_cfg * h_done / H)
+  // throughput mode: reset the transport pool counters for the next segment
+  // (fast_pool_reset) so that launch needs no reset kernel of its own
+  unsigned long long* pool_ctl;
+  unsigned long long* pool_src_head;
   LowOrderState s;
 };
 

@@ -466,6 +466,15 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   unsigned csz = kClaim;
   const unsigned tail_zone = gridDim.x * kWarpsPerBlock * kClaim * (unsigned)HWWG_CLAIM_ZONE;
   unsigned long long ticket = ~0ULL;  // lane 0: pool slot this warp waits on
+  // The pool counters are reset without knowing this grid (fast_pool_reset:
+  // active = kPoolSentinel, source head = 0), so the reset can ride on the
+  // kernel before this one; the first thread turns the sentinel into the warp
+  // count (until it lands, `active` cannot read zero) and claims start after
+  // the static first reservations.
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(const_cast<unsigned long long*>(&ctl[2]),
+              (unsigned long long)gridDim.x * kWarpsPerBlock - kPoolSentinel);
+  const unsigned claim0 = gridDim.x * kWarpsPerBlock * kClaim;
 
   FPROF_DECL
 #ifdef HWWG_FAST_PROF
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (r_lo == r_hi) {
         unsigned nb = 0;
         if (lane == 0)
-          nb = r_pend ? r_next : (unsigned)atomicAdd(a.src_head, (unsigned long long)csz);
+          nb = r_pend ? r_next : claim0 + (unsigned)atomicAdd(a.src_head, (unsigned long long)csz);
         nb = __shfl_sync(0xffffffffu, nb, 0);
         r_pend = false;
         if (nb >= n_src) {
@@ -836,7 +845,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     // ---- look-ahead source claim: the reservation is spent and lanes will need
     // particles; the atomic's latency hides behind the census and tally work
     if (r_lo == r_hi && !r_pend && !src_done) {
-      if (lane == 0) r_next = (unsigned)atomicAdd(a.src_head, (unsigned long long)csz);
+      if (lane == 0) r_next = claim0 + (unsigned)atomicAdd(a.src_head, (unsigned long long)csz);
       r_pend = true;
     }
     // ---- bank census particles. Slots come from a per-warp chunk of the census
@@ -1220,16 +1229,8 @@ int fast_blocks_per_sm(size_t smem) {
 }
 
 namespace {
-__global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src_head,
-                                unsigned long long warps) {
-  ctl[0] = 0;
-  ctl[1] = 0;
-  ctl[2] = warps;  // every warp starts active (holding source work)
-  ctl[3] = 0;      // no backlog declared yet
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  ctl[4] = t;  // segment start (diagnostics)
-  *src_head = warps * kClaim;  // every warp's first reservation is static
+__global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src_head) {
+  fast_pool_reset(ctl, src_head);
 }
 }  // namespace
 
@@ -1246,8 +1247,7 @@ void configure_fast_kernel() {
 
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
   configure_fast_kernel();
-  k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head,
-                                  (unsigned long long)blocks * kWarpsPerBlock);
+  if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head);
   const bool shf = a.smem_tallies == 1;
   const bool fix = shf && a.fix;
   if (a.uniform && fix) k_fast_segment<true, true, true><<<blocks, kThreads, smem, s>>>(a);
