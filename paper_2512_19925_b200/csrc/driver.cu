@@ -832,11 +832,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const int cur = d->rep_cur;
   // finalize (driver.cpp:221-222): device-side from the tallies alone
   auto enqueue_finalize = [&]() {
-    if (d->fast) {  // the fast kernels score the batch table only
-      launch_track_from_batches(d->tal.p, I, B, s);
-      ++d->launches;
-    }
     FinalizeArgs f{};
+    f.track_from_batches = d->fast ? 1 : 0;  // the fast kernels score the batch table only
     f.I = I;
     f.B = B;
     f.t = d->tal.p;

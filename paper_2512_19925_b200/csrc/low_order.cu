@@ -871,6 +871,11 @@ __global__ void k_finalize(FinalizeArgs a) {
     const uint64_t nb = batch_size(a.histories, B, b);
     return nb ? 1.0 / (double)nb : 0.0;
   };
+  if (i < I && a.track_from_batches) {
+    double s = 0.0;
+    for (int b = 0; b < B; ++b) s += a.t.track_flux_batch[(size_t)b * I + i];
+    a.t.track_flux[i] = s;  // read back below by this thread only
+  }
   if (i < I) {
     a.phi_track[i] = a.t.track_flux[i] * inv_h;
     a.phi_census[i] = a.t.census_phi[i] * inv_h;

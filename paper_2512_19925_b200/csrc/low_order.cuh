@@ -85,6 +85,9 @@ struct FinalizeArgs {
   // outputs (device)
   double *phi_track, *sigma, *phi_census, *current, *closure, *edge;  // I / I+1
   double* scalars;  // PL, PR, census_weight, census_weight_sigma, sigma_valid
+  // throughput mode scores the batch table only: track_flux[i] = sum over b of
+  // track_flux_batch[b][i] (b ascending) is formed here first
+  int track_from_batches;
 };
 void launch_finalize(const FinalizeArgs& a, cudaStream_t st);
 
