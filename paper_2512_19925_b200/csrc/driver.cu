@@ -135,6 +135,7 @@ struct hwwg_driver {
   // step_wref: the largest source weight the step is expected to carry (the
   // pulse strength, the volumetric source's particle weight)
   int fix_tallies = 1;
+  unsigned fix_budget = kFastFixBudget;  // HWWG_FAST_FIX_BUDGET (tests: exercise the overflow path)
   // transport events per history of the last completed step (segments per
   // history; 100 before any: config 2's cold start runs 73), to predict
   // whether a launch stays inside the fixed-point tallies' per-block budget
@@ -985,6 +986,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           if (fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
               bps >= fast_blocks_per_sm(smem) && per_block <= (double)kFastFixBudget) {
             fa.fix = 1;
+            fa.fix_budget = d->fix_budget;
             fa.fix_k_trk = kt;
             fa.fix_k_edge = ke;
             fa.aggregate = 0;
@@ -1419,6 +1421,8 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     d->agg_all = v == 2 ? 2 : (v ? 1 : 0);
   }
   if (const char* m = std::getenv("HWWG_FAST_FIX")) d->fix_tallies = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_FAST_FIX_BUDGET"))
+    d->fix_budget = (unsigned)std::min<long>(std::max<long>(std::atol(m), 0), (long)kFastFixBudget);
   if (const char* m = std::getenv("HWWG_COMB_TILED")) d->comb_tiled = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
   d->world = d->opt.world > 1 ? d->opt.world : 1;

@@ -65,6 +65,7 @@ struct FastArgs {
   // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
   // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
   int fix, fix_k_trk, fix_k_edge;
+  unsigned fix_budget;  // events per block with limb adds (<= kFastFixBudget)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,

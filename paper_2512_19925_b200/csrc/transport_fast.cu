@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         unsigned used = 0;
         if (lane == 0) used = atomicAdd(&s_fixbudget, kFixChunk);
         used = __shfl_sync(0xffffffffu, used, 0);
-        if (used + kFixChunk > kFixBudget) fix_ok = false;
+        if (used + kFixChunk > a.fix_budget) fix_ok = false;
         else fix_left += kFixChunk;
       }
       fix_left -= k;

@@ -169,14 +169,18 @@ def test_tiled_comb_matches_prefix_comb(monkeypatch):
         assert np.mean(z < 4.0) >= 0.9, (k, np.sort(z)[-8:])
 
 
-def test_fixed_point_tallies_match_fp64(monkeypatch):
+@pytest.mark.parametrize("budget", [None, 3000])
+def test_fixed_point_tallies_match_fp64(monkeypatch, budget):
     """The fixed-point track, edge and census tallies (16-bit limbs on native 32-bit shared
     atomics) against the fp64 CAS tallies on the same events: one config-2 step
     with per-lane (not warp-aggregated) tallies throughout, so both runs see
     the same counter-based Philox histories and differ only in the tally
     arithmetic (quantisation 2^-40 of the largest expected score, and fp64
-    summation order)."""
+    summation order). budget = 3000: blocks exhaust the limb budget early and
+    finish through the warp-aggregated global fp64 fallback."""
     monkeypatch.setenv("HWWG_FAST_AGG", "2")
+    if budget is not None:
+        monkeypatch.setenv("HWWG_FAST_FIX_BUDGET", str(budget))
     out = {}
     for fix in ("1", "0"):
         monkeypatch.setenv("HWWG_FAST_FIX", fix)
