@@ -135,6 +135,12 @@ struct hwwg_driver {
   // step_wref: the largest source weight the step is expected to carry (the
   // pulse strength, the volumetric source's particle weight)
   int fix_tallies = 1;
+  int pdl = 1;  // programmatic dependent launches across segment boundaries (HWWG_PDL)
+  // transport_ms: exact mode times its segments with CUDA events; the
+  // throughput mode with in-kernel launch spans (FastArgs::span), because
+  // events between its segment kernels cost 4% (HWWG_SEG_EVENTS=1 restores them)
+  int seg_events = 1;
+  DevBuf<unsigned long long> span;  // 2 words per segment
   unsigned fix_budget = kFastFixBudget;  // HWWG_FAST_FIX_BUDGET (tests: exercise the overflow path)
   // transport events per history of the last completed step (segments per
   // history; 100 before any: config 2's cold start runs 73), to predict
@@ -906,10 +912,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         ea.log = d->xlog.view(ea.n);
       }
       const int nseg = (int)u;
-      HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
+      if (d->seg_events) HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg], s));
       if (d->fast) {
         FastArgs fa{};
         fa.pool_reset_done = pool_reset_done ? 1 : 0;
+        fa.span = d->seg_events ? nullptr : d->span.p + 2 * nseg;
+        fa.pdl = pool_reset_done && d->pdl && !d->phases_on;  // right after the window update
         pool_reset_done = false;
         // this rank's part of the segment: global [h_done, h_stop) ∩ its shard
         uint64_t g_lo = h_done, g_hi = h_stop;
@@ -1023,7 +1031,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         // chunk init, histories (+ log replay), ordered merge
         if (ea.n) d->launches += ea.log.slot ? 4 : 3;
       }
-      HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg + 1], s));
+      if (d->seg_events) HWWG_CUDA(cudaEventRecord(d->seg_ev[2 * nseg + 1], s));
       h_done = h_stop;
       if (u == thr.size()) break;
       // partial_snapshot + implicit closure update (driver.cpp:206-217)
@@ -1060,6 +1068,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         a.pool_ctl = d->pool_ctl.p;
         a.pool_src_head = d->src_head.p;
         pool_reset_done = true;
+        a.pdl = d->pdl && d->world == 1 && !d->phases_on;  // right after the transport launch
+        a.pool_span = d->seg_events ? nullptr : d->span.p + 2 * (nseg + 1);
       }
       a.s = d->lo;
       d->ph_mark("losm1", s);
@@ -1312,9 +1322,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   HWWG_CUDA(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
   rec->device_ms = ms;
   double tms = 0.0;
+  std::vector<unsigned long long> spans;
+  if (!d->seg_events) {
+    spans.resize(2 * (thr.size() + 1));
+    HWWG_CUDA(cudaMemcpy(spans.data(), d->span.p, spans.size() * 8, cudaMemcpyDeviceToHost));
+  }
   for (size_t u = 0; u <= thr.size(); ++u) {
     float e = 0.f;
-    HWWG_CUDA(cudaEventElapsedTime(&e, d->seg_ev[2 * u], d->seg_ev[2 * u + 1]));
+    if (d->seg_events) HWWG_CUDA(cudaEventElapsedTime(&e, d->seg_ev[2 * u], d->seg_ev[2 * u + 1]));
+    else if (spans[2 * u + 1] > spans[2 * u]) e = (float)(1e-6 * (double)(spans[2 * u + 1] - spans[2 * u]));
     tms += e;
     if (u < thr.size() ? thr[u] > (u ? thr[u - 1] : 0) : H > (thr.empty() ? 0 : thr.back()))
       ++rec->transport_launches;
@@ -1421,6 +1437,9 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     d->agg_all = v == 2 ? 2 : (v ? 1 : 0);
   }
   if (const char* m = std::getenv("HWWG_FAST_FIX")) d->fix_tallies = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
+  d->seg_events = d->fast ? (std::getenv("HWWG_SEG_EVENTS") ? 1 : 0) : 1;
+  d->span.reserve(64);
   if (const char* m = std::getenv("HWWG_FAST_FIX_BUDGET"))
     d->fix_budget = (unsigned)std::min<long>(std::max<long>(std::atol(m), 0), (long)kFastFixBudget);
   if (const char* m = std::getenv("HWWG_COMB_TILED")) d->comb_tiled = std::atoi(m) ? 1 : 0;

@@ -34,8 +34,15 @@ struct FastPool {
 // active warps = kPoolSentinel (the kernel's first thread swaps in its warp
 // count), source claims counted from the end of the static reservations.
 constexpr unsigned long long kPoolSentinel = 1ULL << 40;
+// span (nullable): the launch's [first block start, last block end] in
+// globaltimer ns, reset to [~0, 0] here and stamped by the transport blocks
 __device__ __forceinline__ void fast_pool_reset(unsigned long long* ctl,
-                                                unsigned long long* src_head) {
+                                                unsigned long long* src_head,
+                                                unsigned long long* span) {
+  if (span) {
+    span[0] = ~0ULL;
+    span[1] = 0ULL;
+  }
   ctl[0] = 0;
   ctl[1] = 0;
   ctl[2] = kPoolSentinel;  // every warp starts active (holding source work)
@@ -67,6 +74,11 @@ struct FastArgs {
   int fix, fix_k_trk, fix_k_edge;
   unsigned fix_budget;  // events per block with limb adds (<= kFastFixBudget)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
+  int pdl;              // 1: programmatic dependent launch after the previous kernel
+  // [first block start, last block end] (globaltimer ns) of this launch, reset
+  // with the pool counters: the transport time without per-launch CUDA events
+  // (events between the segment kernels serialised the launch pipeline: -4%)
+  unsigned long long* span;
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,
   // no per-event table loads.

@@ -703,7 +703,8 @@ constexpr int kSmemStateMaxI = 1200;
 __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a);
 
 __global__ void __launch_bounds__(kCtaThreads) k_low_order_update(LowOrderArgs a) {
-  if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
+  if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head, a.pool_span);
   if (!a.smem_state) {
     low_order_update_body(a);
     return;
@@ -1448,8 +1449,17 @@ void launch_low_order_update(const LowOrderArgs& a_in, cudaStream_t st) {
                                    (int)smem));
     configured = smem;
   }
-  k_low_order_update<<<1, kCtaThreads, smem, st>>>(a);
-  HWWG_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kCtaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  HWWG_CUDA(cudaLaunchKernelEx(&cfg, k_low_order_update, a));
 }
 
 void launch_finalize(const FinalizeArgs& a, cudaStream_t st) {

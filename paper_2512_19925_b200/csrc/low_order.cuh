@@ -71,6 +71,8 @@ struct LowOrderArgs {
   // (fast_pool_reset) so that launch needs no reset kernel of its own
   unsigned long long* pool_ctl;
   unsigned long long* pool_src_head;
+  unsigned long long* pool_span;  // the next segment's launch span (FastArgs::span)
+  int pdl;  // 1: programmatic dependent launch after the previous kernel
   LowOrderState s;
 };
 

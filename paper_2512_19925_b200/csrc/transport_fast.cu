@@ -393,6 +393,7 @@ __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb, int 
 template <bool kUniform, bool kShf, bool kFix>
 __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastArgs a) {
   static_assert(kShf || !kFix, "fixed-point tallies live in shared memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   if (windows)
     for (int i = threadIdx.x; i < I; i += blockDim.x) s_cent[i] = a.centers[i];
   __syncthreads();
+  if (a.span && threadIdx.x == 0) atomicMin(&a.span[0], globaltimer());
   // per-lane event counters: 32 bits is plenty within one launch (registers
   // are what bounds occupancy here)
   unsigned n_coll = 0, n_cen = 0;
@@ -1121,6 +1123,10 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     if (coll) atomicAdd(&u[kCollisions], coll);
     if (cen) atomicAdd(&u[kCensusCount], cen);
   }
+  if (a.span) {  // the block's end, after all its warps
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&a.span[1], globaltimer());
+  }
 }
 
 #undef STK
@@ -1229,8 +1235,9 @@ int fast_blocks_per_sm(size_t smem) {
 }
 
 namespace {
-__global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src_head) {
-  fast_pool_reset(ctl, src_head);
+__global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src_head,
+                                unsigned long long* span) {
+  fast_pool_reset(ctl, src_head, span);
 }
 }  // namespace
 
@@ -1247,16 +1254,29 @@ void configure_fast_kernel() {
 
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
   configure_fast_kernel();
-  if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head);
+  if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head, a.span);
   const bool shf = a.smem_tallies == 1;
   const bool fix = shf && a.fix;
-  if (a.uniform && fix) k_fast_segment<true, true, true><<<blocks, kThreads, smem, s>>>(a);
-  else if (a.uniform && shf) k_fast_segment<true, true, false><<<blocks, kThreads, smem, s>>>(a);
-  else if (a.uniform) k_fast_segment<true, false, false><<<blocks, kThreads, smem, s>>>(a);
-  else if (fix) k_fast_segment<false, true, true><<<blocks, kThreads, smem, s>>>(a);
-  else if (shf) k_fast_segment<false, true, false><<<blocks, kThreads, smem, s>>>(a);
-  else k_fast_segment<false, false, false><<<blocks, kThreads, smem, s>>>(a);
-  HWWG_CUDA(cudaGetLastError());
+  void (*k)(FastArgs) = a.uniform && fix   ? k_fast_segment<true, true, true>
+                        : a.uniform && shf ? k_fast_segment<true, true, false>
+                        : a.uniform        ? k_fast_segment<true, false, false>
+                        : fix              ? k_fast_segment<false, true, true>
+                        : shf              ? k_fast_segment<false, true, false>
+                                           : k_fast_segment<false, false, false>;
+  // programmatic dependent launch: the grid may be scheduled while the kernel
+  // before it (the window update) drains; every block waits for it
+  // (griddepcontrol.wait) before touching memory
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  HWWG_CUDA(cudaLaunchKernelEx(&cfg, k, a));
   if (shf && !fix && a.flush_replicas) {
     k_flush_reduce<<<32, 256, 0, s>>>(a.flush_scratch, a.flush_replicas, a.flush_stride, a.mesh.I,
                                       a.nb, a.b_lo, a.t);
