@@ -873,11 +873,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     else enqueue_windows(s);
 
     // ---- segments with window-update barriers (driver.cpp:181-219)
-    d->tal.zero(s);
-    if (d->fast)
-      HWWG_CUDA(cudaMemsetAsync(d->warp_cursor.p, 0, d->warp_cursor.n * 8, s));
-    HWWG_CUDA(cudaMemsetAsync(d->counter.p, 0, sizeof(unsigned long long), s));
-    HWWG_CUDA(cudaMemsetAsync(d->err.p, 0, sizeof(DevError), s));
+    bool start_reset = false;  // the first segment's pool counters are reset here
+    if (d->fast) {
+      launch_step_start(d->tal.slab.p, d->tal.words(), d->warp_cursor.p, d->warp_cursor.n,
+                        d->counter.p, d->err.p, d->pool_ctl.p, d->src_head.p,
+                        d->seg_events ? nullptr : d->span.p, d->sms, s);
+      ++d->launches;
+      start_reset = true;
+    } else {
+      d->tal.zero(s);
+      HWWG_CUDA(cudaMemsetAsync(d->counter.p, 0, sizeof(unsigned long long), s));
+      HWWG_CUDA(cudaMemsetAsync(d->err.p, 0, sizeof(DevError), s));
+    }
     ExactArgs ea{};
     ea.mesh = d->prob.view;
     ea.t_begin = rec->t_begin;
@@ -899,7 +906,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     ea.err = d->err.p;
     if (!d->fast) d->xlog.reset_need(s);
     uint64_t h_done = 0;
-    bool pool_reset_done = false;  // the mid-step update reset the pool counters
+    bool pool_reset_done = start_reset;  // the step start or the mid-step update reset the pool
     for (size_t u = 0; u <= thr.size(); ++u) {
       const uint64_t h_stop = u < thr.size() ? thr[u] : H;
       ea.src = d->source.p + h_done;

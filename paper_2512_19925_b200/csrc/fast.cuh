@@ -108,6 +108,13 @@ size_t fast_flush_stride(int I, int B);  // words per flush replica (nb <= B)
 // count of slots the census bank spans.
 void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,
                               int warps, double x_fill, double t_fill, cudaStream_t s);
+// Step start of the throughput mode in one launch: zero the tally slab, the
+// warp census cursors, the census counter and the error word; reset the first
+// segment's pool counters (fast_pool_reset).
+void launch_step_start(double* slab, size_t slab_words, unsigned long long* cursor,
+                       size_t cursor_words, unsigned long long* counter, DevError* err,
+                       unsigned long long* ctl, unsigned long long* src_head,
+                       unsigned long long* span, int sms, cudaStream_t s);
 // Compact the census bank (drop zero-weight holes) into AoS particles.
 void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
                              unsigned long long* count, cudaStream_t s);

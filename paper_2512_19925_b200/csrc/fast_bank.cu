@@ -324,6 +324,27 @@ __global__ void k_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
   }
 }
 
+// The throughput step's start in one launch (instead of four memsets and a
+// reset kernel, each of which serialised the launch pipeline): zero the tally
+// slab and the warps' census cursors, the census counter and the error word,
+// and reset the first segment's pool counters.
+__global__ void k_step_start(double* slab, size_t slab_words, unsigned long long* cursor,
+                             size_t cursor_words, unsigned long long* counter, DevError* err,
+                             unsigned long long* ctl, unsigned long long* src_head,
+                             unsigned long long* span) {
+  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = i0; i < slab_words; i += stride) slab[i] = 0.0;
+  for (size_t i = i0; i < cursor_words; i += stride) cursor[i] = 0ULL;
+  if (i0 == 0) {
+    *counter = 0ULL;
+    err->code = 0;
+    err->pad = 0;
+    err->history = 0ULL;
+    fast_pool_reset(ctl, src_head, span);
+  }
+}
+
 __global__ void k_track_from_batches(TallyPtrs t, int I, int B) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= I) return;
@@ -442,6 +463,15 @@ void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
   HWWG_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s));
   if (!n) return;
   k_compact_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, out, count);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_step_start(double* slab, size_t slab_words, unsigned long long* cursor,
+                       size_t cursor_words, unsigned long long* counter, DevError* err,
+                       unsigned long long* ctl, unsigned long long* src_head,
+                       unsigned long long* span, int sms, cudaStream_t s) {
+  k_step_start<<<2 * sms, 256, 0, s>>>(slab, slab_words, cursor, cursor_words, counter, err, ctl,
+                                       src_head, span);
   HWWG_CUDA(cudaGetLastError());
 }
 
