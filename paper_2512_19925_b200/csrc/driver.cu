@@ -560,9 +560,13 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
 
   // ---- the start-of-step windows (driver.cpp:136-167) on stream st: record
   // flags, then lww centres or the lagged hybrid solve
-  auto enqueue_windows = [&](cudaStream_t st) {
+  // fold_backup: the hybrid solve kernel also takes the replay backup of the
+  // incoming windows and zeroes the record flags (two copies and a memset less
+  // ahead of the comb)
+  auto enqueue_windows = [&](cudaStream_t st, bool fold_backup) {
     // per-step record flags: has_hybrid, updates_applied, failed, status
-    HWWG_CUDA(cudaMemsetAsync(d->lo.flags + 1, 0, 4 * sizeof(int), st));
+    if (!(fold_backup && d->hybrid()))
+      HWWG_CUDA(cudaMemsetAsync(d->lo.flags + 1, 0, 4 * sizeof(int), st));
     if (c.mode == 1) {  // lww: lagged track-length flux of the previous step
       HWWG_CUDA(cudaMemsetAsync(d->lo.flags, 0, sizeof(int), st));
       if (d->has_prev_report) {
@@ -602,6 +606,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.s.rep_current = d->rep(prev, 3);
       a.s.rep_closure = d->rep(prev, 4);
       a.s.rep_PLPR = d->rep(prev, 6);
+      if (fold_backup) {
+        a.backup_centers = d->centers_backup.p;
+        a.backup_flags = d->flags_backup.p;
+      }
       d->ph_mark("losm0", st);
       launch_low_order_update(a, st);
       d->ph_mark("-", st);
@@ -614,11 +622,14 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const bool early_windows = d->fast && d->world == 1 && !(c.vol_rate > 0.0) && !d->phases_on;
   if (early_windows) {
     // backup of the windows so an overflowing step can be replayed exactly
-    HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
-    HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    // (taken by the hybrid solve kernel itself when there is one)
+    if (!d->hybrid()) {
+      HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
+      HWWG_CUDA(cudaMemcpyAsync(d->flags_backup.p, d->lo.flags, 8 * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    }
     HWWG_CUDA(cudaEventRecord(d->ev_fork, s));
     HWWG_CUDA(cudaStreamWaitEvent(d->aux_stream, d->ev_fork, 0));
-    enqueue_windows(d->aux_stream);
+    enqueue_windows(d->aux_stream, true);
     HWWG_CUDA(cudaEventRecord(d->ev_join, d->aux_stream));
   }
 
@@ -870,7 +881,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     // ---- windows (driver.cpp:136-167): already on the auxiliary stream for the
     // first attempt of an early-window step, else here
     if (attempt == 0 && early_windows) HWWG_CUDA(cudaStreamWaitEvent(s, d->ev_join, 0));
-    else enqueue_windows(s);
+    else enqueue_windows(s, false);
 
     // ---- segments with window-update barriers (driver.cpp:181-219)
     bool start_reset = false;  // the first segment's pool counters are reset here

@@ -705,6 +705,13 @@ __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a);
 __global__ void __launch_bounds__(kCtaThreads) k_low_order_update(LowOrderArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
   if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head, a.pool_span);
+  if (a.backup_centers) {  // the step-start windows backup, then the record flags
+    for (int i = threadIdx.x; i < a.I; i += blockDim.x) a.backup_centers[i] = a.s.centers[i];
+    if (threadIdx.x < 8) a.backup_flags[threadIdx.x] = a.s.flags[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x >= 1 && threadIdx.x <= 4) a.s.flags[threadIdx.x] = 0;
+    __syncthreads();
+  }
   if (!a.smem_state) {
     low_order_update_body(a);
     return;

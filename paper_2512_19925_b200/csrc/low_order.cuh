@@ -73,6 +73,10 @@ struct LowOrderArgs {
   unsigned long long* pool_src_head;
   unsigned long long* pool_span;  // the next segment's launch span (FastArgs::span)
   int pdl;  // 1: programmatic dependent launch after the previous kernel
+  // mode 0 at a step start (nullable): copy the incoming centres (I) and
+  // flags (8) here first (the replay backup), then zero the record flags 1..4
+  double* backup_centers;
+  int* backup_flags;
   LowOrderState s;
 };
 
