@@ -53,10 +53,37 @@ __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src,
   }
 }
 
+// popctrl.cpp:15-20 comb scalars (W, spacing, the offset drawn from the
+// step's comb stream, the output weight), formed by every block from the
+// scan's last prefix (the same values everywhere); block 0 records them.
+__device__ __forceinline__ void comb_scalars(const FastCombArgs& a, double& spacing,
+                                             double& offset) {
+  __shared__ double sc[2];
+  if (threadIdx.x == 0) {
+    const double W = a.prefix[a.n - 1];
+    const double sp = W / (double)a.target;
+    Xoshiro r;
+    r.seed(a.seed, a.stream);
+    const double off = r.uniform() * sp;
+    sc[0] = sp;
+    sc[1] = off;
+    if (blockIdx.x == 0) {
+      a.scalars[0] = W;
+      a.scalars[1] = sp;
+      a.scalars[2] = off;
+      a.scalars[3] = sp * (double)a.target;
+    }
+  }
+  __syncthreads();
+  spacing = sc[0];
+  offset = sc[1];
+}
+
 __global__ void k_comb_scatter(FastCombArgs a) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double spacing, offset;
+  comb_scalars(a, spacing, offset);
   if (i >= a.n) return;
-  const double spacing = a.scalars[1], offset = a.scalars[2];
   const uint64_t k0 = i ? teeth_below(a.prefix[i - 1], offset, spacing, a.target) : 0;
   const uint64_t k1 = teeth_below(a.prefix[i], offset, spacing, a.target);
   if (k0 < k1) write_teeth(a, i, k0, k1, spacing);
@@ -256,18 +283,6 @@ struct WeightOf {
   __host__ __device__ double operator()(const double2& v) const { return v.x; }
 };
 
-__global__ void k_comb_scalars(const double* prefix, uint64_t n, uint64_t target, uint64_t seed,
-                               uint64_t stream, double* sc) {
-  const double W = prefix[n - 1];
-  const double spacing = W / (double)target;
-  Xoshiro r;
-  r.seed(seed, stream);
-  sc[0] = W;
-  sc[1] = spacing;
-  sc[2] = r.uniform() * spacing;
-  sc[3] = spacing * (double)target;
-}
-
 __global__ void k_local_total(const double* prefix, uint64_t n, double* sc) {
   sc[0] = n ? prefix[n - 1] : 0.0;
 }
@@ -418,7 +433,6 @@ void launch_fast_comb(const FastCombArgs& a, cudaStream_t s) {
   size_t bytes = a.temp_bytes;
   HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, WeightIt(a.bank.wt, WeightOf()), a.prefix,
                                           (int)a.n, s));
-  k_comb_scalars<<<1, 1, 0, s>>>(a.prefix, a.n, a.target, a.seed, a.stream, a.scalars);
   k_comb_scatter<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
