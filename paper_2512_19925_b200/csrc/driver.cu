@@ -918,6 +918,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (!d->fast) d->xlog.reset_need(s);
     uint64_t h_done = 0;
     bool pool_reset_done = start_reset;  // the step start or the mid-step update reset the pool
+    int grid_warps_max = 0;     // largest transport grid of this step so far
+    bool tail_filled = false;   // the last segment filled the census chunk tails
     for (size_t u = 0; u <= thr.size(); ++u) {
       const uint64_t h_stop = u < thr.size() ? thr[u] : H;
       ea.src = d->source.p + h_done;
@@ -1021,6 +1023,14 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         }
         fa.scramble = fa.aggregate ? 0 : d->scramble;
         const int blocks = d->sms * fast_blocks_per_sm(smem);
+        const int gw = blocks * (fast_threads_per_block() / 32);
+        grid_warps_max = std::max(grid_warps_max, gw);
+        if (u == thr.size() && gw >= grid_warps_max && fa.n_src) {
+          fa.fill_tail = 1;
+          fa.x_fill = d->prob.edges.front();
+          fa.t_fill = rec->t_end;
+          tail_filled = true;
+        }
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
         fa.warp_cursor = d->warp_cursor.p;
         fa.seg = nseg;
@@ -1099,7 +1109,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       d->ph_mark("-", s);
       ++d->launches;
     }
-    if (d->fast) {  // zero-weight records in the unused tails of the warps' chunks
+    if (d->fast && !tail_filled) {  // zero-weight records in the unused tails of the warps' chunks
       d->ph_mark("fill", s);
       launch_fill_census_holes(d->fcensus.view(), d->fcensus.cap(), d->warp_cursor.p,
                                d->max_warps, d->prob.edges.front(), rec->t_end, s);

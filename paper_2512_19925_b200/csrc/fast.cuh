@@ -79,6 +79,11 @@ struct FastArgs {
   // with the pool counters: the transport time without per-launch CUDA events
   // (events between the segment kernels serialised the launch pipeline: -4%)
   unsigned long long* span;
+  // 1 (the step's last segment, whose grid holds every warp with a census
+  // chunk): each warp writes zero-weight records (x_fill, t_fill) into the
+  // unused tail of its chunk on exit, instead of a separate fill launch
+  int fill_tail;
+  double x_fill, t_fill;
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,
   // no per-event table loads.

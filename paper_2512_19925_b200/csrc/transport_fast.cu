@@ -1034,6 +1034,16 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     for (int k = 0; k < 12; ++k) atomicAdd(&g_fprof[k], fp_c[k]);
 #endif
 
+  if (a.fill_tail) {  // k_fill_holes for this warp's chunk tail
+    for (unsigned k = lane; k < wleft; k += 32) {
+      const unsigned long long slot = wcur + k;
+      if (slot < a.census_cap) {
+        a.census.xm[slot] = make_double2(a.x_fill, 0.5);
+        a.census.wt[slot] = make_double2(0.0, a.t_fill);
+        a.census.meta[slot] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  }
   if (lane == 0) {
     a.warp_cursor[2 * gwarp] = wcur;
     a.warp_cursor[2 * gwarp + 1] = wcur + wleft;
