@@ -146,6 +146,7 @@ struct hwwg_driver {
   // history; 100 before any: config 2's cold start runs 73), to predict
   // whether a launch stays inside the fixed-point tallies' per-block budget
   double events_per_history = 100.0;
+  bool events_measured = false;
   double step_wref = 1.0;
   int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
@@ -1009,7 +1010,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           const double w = std::max(c.rho, d->step_wref);
           int kt = 0, ke = 0;
           const int bps = fast_blocks_per_sm(fsm);
-          const double per_block = (double)(g_hi - g_lo) * d->events_per_history /
+          // (a measured rate varies step to step: 30% margin; the cold-start
+          // prior is already generous)
+          const double margin = d->events_measured ? 1.3 : 1.0;
+          const double per_block = (double)(g_hi - g_lo) * d->events_per_history * margin /
                                    (double)std::max(1, d->sms * bps);
           if (fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
               bps >= fast_blocks_per_sm(smem) && per_block <= (double)kFastFixBudget) {
@@ -1387,7 +1391,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   for (int i = 0; i < I; ++i) seg += d->h_tracks[i];
   rec->segments = seg;
   rec->histories = H;
-  if (H) d->events_per_history = (double)seg / (double)H;
+  if (H) {
+    d->events_per_history = (double)seg / (double)H;
+    d->events_measured = true;
+  }
   // banked particles (fast mode: the census slots also hold zero-weight chunk tails)
   rec->census_size = d->fast ? (uint64_t)u[kCensusCount] : count;
   rec->comb_in_weight = comb_sc[0];
