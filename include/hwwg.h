@@ -48,6 +48,7 @@ extern "C" {
 
 typedef struct hwwg_ctx hwwg_ctx;
 typedef struct hwwg_driver hwwg_driver;
+typedef struct hwwg_loopback hwwg_loopback;
 
 /* == hww::Particle (proj/include/hww/particle.hpp:9-14), 32 bytes. */
 typedef struct { double x, mu, w, t; } hwwg_particle;
@@ -123,10 +124,19 @@ typedef struct {
   int32_t rank;
   int32_t world;
   uint8_t nccl_id[128];
+  /* Non-NULL: the ranks are host threads of THIS process on one device and
+   * exchange through this in-process hub instead of NCCL (tests of the
+   * multi-rank driver on one GPU; world must equal the hub's). */
+  hwwg_loopback* loopback;
 } hwwg_options;
 
 /* ncclGetUniqueId for the multi-GPU driver (out: 128 bytes). */
 int hwwg_nccl_unique_id(uint8_t* out);
+/* In-process collective hub for `world` driver ranks on `device`: the drivers
+ * share one CUDA stream and meet at a host barrier in every collective (each
+ * rank's hwwg_driver_step must run on its own host thread). */
+int hwwg_loopback_create(int32_t world, int32_t device, hwwg_loopback** out);
+void hwwg_loopback_destroy(hwwg_loopback* hub);
 
 /* Host-side sharding plan shared by every rank (pure functions):
  * shard(rank) = [H*rank/world, H*(rank+1)/world). */

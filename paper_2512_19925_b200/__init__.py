@@ -6,10 +6,10 @@ include/hwwg.h); this package is the thin Python mirror of the reference's API.
 """
 from ._capi import PARTICLE_DT, RNG_EXACT, RNG_PHILOX, HwwgError, LIB_PATH  # noqa: F401
 from .hww import (  # noqa: F401
-    Driver, Engine, Material, Mesh1D, RunConfig, StepContext, StepOutcome, TallySet,
+    Driver, Engine, Loopback, Material, Mesh1D, RunConfig, StepContext, StepOutcome, TallySet,
     WeightWindowGrid, build_uniform_mesh, default_engine, run, run_segment_parallel)
 
 __all__ = [
-    "Driver", "Engine", "Material", "Mesh1D", "RunConfig", "StepContext", "StepOutcome",
+    "Driver", "Engine", "Loopback", "Material", "Mesh1D", "RunConfig", "StepContext", "StepOutcome",
     "TallySet", "WeightWindowGrid", "build_uniform_mesh", "default_engine", "run",
     "run_segment_parallel", "PARTICLE_DT", "RNG_EXACT", "RNG_PHILOX", "HwwgError", "LIB_PATH"]

@@ -73,7 +73,8 @@ class StepOutcomeC(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("rng_mode", C.c_int32), ("bank_capacity", C.c_uint64),
-                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
+                ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+                ("loopback", C.c_void_p)]
 
 
 class RunConfigC(C.Structure):
@@ -119,7 +120,8 @@ EXPORTS = (
     "hwwg_default_config", "hwwg_validate_config", "hwwg_losm_assemble_solve",
     "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log",
     "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan",
-    "hwwg_fourier_lowpass", "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write")
+    "hwwg_fourier_lowpass", "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write",
+    "hwwg_loopback_create", "hwwg_loopback_destroy")
 
 _lib = None
 
@@ -164,6 +166,9 @@ def lib():
                                     C.c_uint64, C.c_void_p, dptr, dptr]
     L.hwwg_device_log.argtypes = [C.c_void_p, dptr, C.c_uint64, dptr]
     L.hwwg_nccl_unique_id.argtypes = [C.c_void_p]
+    L.hwwg_loopback_create.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+    L.hwwg_loopback_destroy.argtypes = [C.c_void_p]
+    L.hwwg_loopback_destroy.restype = None
     L.hwwg_shard_range.argtypes = [C.c_uint64, C.c_int32, C.c_int32, u64ptr, u64ptr]
     L.hwwg_shard_range.restype = None
     L.hwwg_comb_plan.argtypes = [dptr, C.c_int32, C.c_int32, C.c_uint64, C.c_double, dptr, dptr,

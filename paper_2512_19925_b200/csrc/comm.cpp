@@ -1,0 +1,263 @@
+// NCCL and loopback implementations of the driver's collectives (comm.h).
+#include "comm.h"
+
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "capi_util.h"
+
+#define COMM_CUDA(call)                                                                 \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::hwwg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define COMM_NCCL(call)                                                                   \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      throw ::hwwg::ApiError(HWWG_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// In-process hub of the loopback ranks: one stream, staging, mailboxes, barrier.
+struct hwwg_loopback {
+  int world = 1;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool broken = false;  // a rank failed mid-collective: release the others
+  std::vector<std::vector<unsigned char>> stage;
+  std::map<std::pair<int, int>, std::deque<std::vector<unsigned char>>> mail;
+
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    if (broken) throw hwwg::ApiError(HWWG_ESTATE, "loopback peer failed");
+    const unsigned long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    cv.wait(lk, [&] { return gen != g || broken; });
+    if (broken && gen == g) throw hwwg::ApiError(HWWG_ESTATE, "loopback peer failed");
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
+namespace hwwg {
+
+namespace {
+
+ncclDataType_t nccl_type(DType t) {
+  return t == DType::kF64 ? ncclDouble : (t == DType::kU64 ? ncclUint64 : ncclUint32);
+}
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(const uint8_t id_bytes[128], int rank, int world) : rank_(rank), world_(world) {
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    COMM_NCCL(ncclCommInitRank(&comm_, world, id, rank));
+  }
+  ~NcclComm() override {
+    if (comm_) ncclCommDestroy(comm_);
+  }
+  int rank() const override { return rank_; }
+  int world() const override { return world_; }
+  void all_reduce(const void* send, void* recv, size_t count, DType t, RedOp op,
+                  cudaStream_t s) override {
+    COMM_NCCL(ncclAllReduce(send, recv, count, nccl_type(t), op == RedOp::kSum ? ncclSum : ncclMax,
+                            comm_, s));
+  }
+  void all_gather(const void* send, void* recv, size_t count, DType t, cudaStream_t s) override {
+    COMM_NCCL(ncclAllGather(send, recv, count, nccl_type(t), comm_, s));
+  }
+  void group_start() override { COMM_NCCL(ncclGroupStart()); }
+  void send(const void* buf, size_t count, DType t, int peer, cudaStream_t s) override {
+    COMM_NCCL(ncclSend(buf, count, nccl_type(t), peer, comm_, s));
+  }
+  void recv(void* buf, size_t count, DType t, int peer, cudaStream_t s) override {
+    COMM_NCCL(ncclRecv(buf, count, nccl_type(t), peer, comm_, s));
+  }
+  void group_end(cudaStream_t) override { COMM_NCCL(ncclGroupEnd()); }
+
+ private:
+  int rank_, world_;
+  ncclComm_t comm_ = nullptr;
+};
+
+class LoopbackComm final : public Comm {
+ public:
+  LoopbackComm(hwwg_loopback* hub, int rank) : hub_(hub), rank_(rank) {}
+  int rank() const override { return rank_; }
+  int world() const override { return hub_->world; }
+  cudaStream_t shared_stream() const override { return hub_->stream; }
+
+  void all_reduce(const void* send, void* recv, size_t count, DType t, RedOp op,
+                  cudaStream_t s) override {
+    guarded([&] {
+      const size_t bytes = count * dtype_bytes(t);
+      post(send, bytes, s);
+      hub_->barrier();
+      std::vector<unsigned char> out(hub_->stage[0]);  // rank order: deterministic
+      for (int r = 1; r < hub_->world; ++r) {
+        const unsigned char* in = hub_->stage[r].data();
+        for (size_t i = 0; i < count; ++i) combine(out.data(), in, i, t, op);
+      }
+      hub_->barrier();  // every rank has read the staging buffers
+      COMM_CUDA(cudaMemcpyAsync(recv, out.data(), bytes, cudaMemcpyHostToDevice, s));
+      COMM_CUDA(cudaStreamSynchronize(s));
+    });
+  }
+  void all_gather(const void* send, void* recv, size_t count, DType t, cudaStream_t s) override {
+    guarded([&] {
+      const size_t bytes = count * dtype_bytes(t);
+      post(send, bytes, s);
+      hub_->barrier();
+      std::vector<unsigned char> out(bytes * hub_->world);
+      for (int r = 0; r < hub_->world; ++r)
+        if (bytes) std::memcpy(out.data() + bytes * r, hub_->stage[r].data(), bytes);
+      hub_->barrier();
+      COMM_CUDA(cudaMemcpyAsync(recv, out.data(), out.size(), cudaMemcpyHostToDevice, s));
+      COMM_CUDA(cudaStreamSynchronize(s));
+    });
+  }
+  void group_start() override { pending_.clear(); }
+  void send(const void* buf, size_t count, DType t, int peer, cudaStream_t s) override {
+    guarded([&] {
+      std::vector<unsigned char> v(count * dtype_bytes(t));
+      COMM_CUDA(cudaStreamSynchronize(s));
+      if (!v.empty()) COMM_CUDA(cudaMemcpy(v.data(), buf, v.size(), cudaMemcpyDeviceToHost));
+      std::lock_guard<std::mutex> lk(hub_->m);
+      hub_->mail[{rank_, peer}].push_back(std::move(v));
+    });
+  }
+  void recv(void* buf, size_t count, DType t, int peer, cudaStream_t) override {
+    pending_.push_back(Pending{buf, count * dtype_bytes(t), peer});
+  }
+  void group_end(cudaStream_t s) override {
+    guarded([&] {
+      hub_->barrier();  // every send of the group is posted
+      for (const Pending& p : pending_) {
+        std::vector<unsigned char> v;
+        {
+          std::lock_guard<std::mutex> lk(hub_->m);
+          auto& q = hub_->mail[{p.peer, rank_}];
+          if (q.empty()) throw ApiError(HWWG_ESTATE, "loopback recv without a matching send");
+          v = std::move(q.front());
+          q.pop_front();
+        }
+        if (v.size() != p.bytes) throw ApiError(HWWG_ESTATE, "loopback send/recv size mismatch");
+        if (!v.empty()) COMM_CUDA(cudaMemcpy(p.buf, v.data(), v.size(), cudaMemcpyHostToDevice));
+      }
+      pending_.clear();
+      COMM_CUDA(cudaStreamSynchronize(s));
+      hub_->barrier();
+    });
+  }
+
+ private:
+  struct Pending {
+    void* buf;
+    size_t bytes;
+    int peer;
+  };
+  hwwg_loopback* hub_;
+  int rank_;
+  std::vector<Pending> pending_;
+
+  // a failing rank releases its peers (they would wait at the barrier forever)
+  template <class F>
+  void guarded(F f) {
+    try {
+      f();
+    } catch (...) {
+      hub_->abort();
+      throw;
+    }
+  }
+  void post(const void* send, size_t bytes, cudaStream_t s) {
+    COMM_CUDA(cudaStreamSynchronize(s));
+    std::vector<unsigned char>& st = hub_->stage[rank_];
+    st.resize(bytes);
+    if (bytes) COMM_CUDA(cudaMemcpy(st.data(), send, bytes, cudaMemcpyDeviceToHost));
+  }
+  static void combine(unsigned char* out, const unsigned char* in, size_t i, DType t, RedOp op) {
+    if (t == DType::kF64) {
+      double a, b;
+      std::memcpy(&a, out + 8 * i, 8);
+      std::memcpy(&b, in + 8 * i, 8);
+      const double r = op == RedOp::kSum ? a + b : (b > a ? b : a);
+      std::memcpy(out + 8 * i, &r, 8);
+    } else if (t == DType::kU64) {
+      unsigned long long a, b;
+      std::memcpy(&a, out + 8 * i, 8);
+      std::memcpy(&b, in + 8 * i, 8);
+      const unsigned long long r = op == RedOp::kSum ? a + b : (b > a ? b : a);
+      std::memcpy(out + 8 * i, &r, 8);
+    } else {
+      unsigned a, b;
+      std::memcpy(&a, out + 4 * i, 4);
+      std::memcpy(&b, in + 4 * i, 4);
+      const unsigned r = op == RedOp::kSum ? a + b : (b > a ? b : a);
+      std::memcpy(out + 4 * i, &r, 4);
+    }
+  }
+};
+
+}  // namespace
+
+Comm* make_nccl_comm(const uint8_t id[128], int rank, int world) {
+  return new NcclComm(id, rank, world);
+}
+Comm* make_loopback_comm(hwwg_loopback* hub, int rank) { return new LoopbackComm(hub, rank); }
+int loopback_world(const hwwg_loopback* hub) { return hub->world; }
+
+}  // namespace hwwg
+
+extern "C" {
+
+int hwwg_loopback_create(int32_t world, int32_t device, hwwg_loopback** out) {
+  HWWG_API_BEGIN
+  if (!out || world < 1) return hwwg::fail(HWWG_EINVAL, "loopback: world >= 1 and out required");
+  *out = nullptr;
+  auto* h = new hwwg_loopback();
+  h->world = world;
+  h->device = device;
+  h->stage.resize(world);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return hwwg::fail(HWWG_ECUDA, std::string("loopback: ") + cudaGetErrorString(e));
+  }
+  *out = h;
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+void hwwg_loopback_destroy(hwwg_loopback* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

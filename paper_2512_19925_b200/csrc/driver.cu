@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "capi_util.h"
+#include "comm.h"
 #include "common.cuh"
 #include "device_state.cuh"
 #include "driver_host.h"
@@ -150,9 +151,11 @@ struct hwwg_driver {
   double step_wref = 1.0;
   int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
-  DevBuf<double> q_dev;
+  // q of every step the box overlaps, precomputed at creation (q_row[step]:
+  // row of q_all, -1 when the step sees no emission)
+  DevBuf<double> q_all;
+  std::vector<int> q_row;
   const double* q_step = nullptr;
-  DevBuf<hwwg_particle> vol_dev;
   // start-of-step window update overlapping the comb (auxiliary stream)
   cudaStream_t aux_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -197,8 +200,10 @@ struct hwwg_driver {
   // at every window-update barrier and at step end, census combed globally and
   // rebalanced with grouped send/recv
   int rank = 0, world = 1;
-  uint64_t shard_lo = 0;
-  ncclComm_t comm = nullptr;
+  uint64_t shard_lo = 0;  // first history of this rank's shard of the combed bank
+  uint64_t fsrc_local = 0;  // particles of that shard (the front of fsrc)
+  Comm* comm = nullptr;      // NCCL or the in-process loopback (comm.h)
+  bool own_stream = true;    // false: the loopback hub's shared stream
   DevBuf<double> nccl_buf;    // all-gathered census weights, snapshot slabs
   FastBankBuf fteeth;         // teeth this rank produced, before the rebalance
 
@@ -246,8 +251,8 @@ struct hwwg_driver {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (host_bank) cudaFreeHost(host_bank);
     if (h_uni) cudaFreeHost(h_uni);
-    if (comm) ncclCommDestroy(comm);
-    if (stream) cudaStreamDestroy(stream);
+    delete comm;
+    if (stream && own_stream) cudaStreamDestroy(stream);
   }
 
   double* rep(int which, int field) {  // field: 0 phi_track,1 sigma,2 phi_census,3 current,
@@ -266,7 +271,16 @@ void init_driver(hwwg_driver* d) {
   d->B = c.batches;
   d->target = c.target_population ? c.target_population : c.histories_per_step;
   HWWG_CUDA(cudaSetDevice(d->opt.device));
-  HWWG_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  if (d->world > 1) {  // communicator first: a loopback hub supplies the stream
+    if (d->opt.loopback) d->comm = make_loopback_comm(d->opt.loopback, d->rank);
+    else d->comm = make_nccl_comm(d->opt.nccl_id, d->rank, d->world);
+  }
+  if (d->comm && d->comm->shared_stream()) {
+    d->stream = d->comm->shared_stream();
+    d->own_stream = false;
+  } else {
+    HWWG_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  }
   HWWG_CUDA(cudaEventCreate(&d->ev0));
   HWWG_CUDA(cudaEventCreate(&d->ev1));
   const int I = d->I;
@@ -339,6 +353,22 @@ void init_driver(hwwg_driver* d) {
   d->counter.reserve(1);
   d->err.reserve(1);
   d->comb_mem.reserve(4);
+  if (c.vol_rate > 0.0) {  // config-3 LOSM q per step (volume_q_host), uploaded once
+    d->q_row.assign(c.time_steps + 1, -1);
+    std::vector<double> qh;
+    for (int n = 1; n <= c.time_steps; ++n) {
+      const double ta = std::max(d->layers[n - 1], c.vol_t_lo);
+      const double tb = std::min(d->layers[n], c.vol_t_hi);
+      if (!(tb > ta)) continue;
+      d->q_row[n] = (int)(qh.size() / I);
+      qh.resize(qh.size() + I);
+      volume_q_host(d->prob.edges.data(), I, c.vol_x_lo, c.vol_x_hi, ta, tb,
+                    d->layers[n] - d->layers[n - 1], c.vol_rate, qh.data() + qh.size() - I);
+    }
+    d->q_all.reserve(std::max<size_t>(qh.size(), 1));
+    if (!qh.empty())
+      HWWG_CUDA(cudaMemcpyAsync(d->q_all.p, qh.data(), qh.size() * 8, cudaMemcpyHostToDevice, d->stream));
+  }
 
   // source sampling (driver.cpp:309-316) on the host: one sequential stream
   std::vector<hwwg_particle> src(c.no_pulse ? 0 : c.histories_per_step);
@@ -347,7 +377,7 @@ void init_driver(hwwg_driver* d) {
                              c.strength * (double)c.histories_per_step, 0.0, src.data());
   if (d->world > 1) {  // this rank's shard of the step-1 histories
     uint64_t lo, hi;
-    hwwg_shard_range(c.histories_per_step, d->rank, d->world, &lo, &hi);
+    hwwg_shard_range(src.size(), d->rank, d->world, &lo, &hi);  // empty without a pulse
     src = std::vector<hwwg_particle>(src.begin() + lo, src.begin() + hi);
     d->shard_lo = lo;
   }
@@ -356,8 +386,11 @@ void init_driver(hwwg_driver* d) {
                             cudaMemcpyHostToDevice, d->stream));
   d->bank_n = src.size();
   if (c.host_bank) {
-    // room for the cold-start census (x60+ of H) so no step re-pins host memory
-    d->host_bank_cap = std::max<uint64_t>(src.size(), 64 * d->target + 4096);
+    // exact mode: room for the cold-start census (x60+ of H) so no step re-pins
+    // host memory; Philox mode hands the host the combed bank (target
+    // particles; multi-rank runs grow it on demand)
+    d->host_bank_cap = std::max<uint64_t>(
+        src.size(), (d->fast ? 1 : 64) * d->target + 4096);
     HWWG_CUDA(cudaMallocHost(&d->host_bank, d->host_bank_cap * sizeof(hwwg_particle)));
     std::memcpy(d->host_bank, src.data(), src.size() * sizeof(hwwg_particle));
     d->host_bank_n = src.size();
@@ -392,12 +425,7 @@ void init_driver(hwwg_driver* d) {
     d->comb_mem.reserve(4 + d->census_hwm);
     d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
     if (c.host_bank) d->bank.reserve(d->census_hwm);
-    if (d->world > 1) {
-      ncclUniqueId id;
-      std::memcpy(&id, d->opt.nccl_id, sizeof(id));
-      NCCL_CHECK(ncclCommInitRank(&d->comm, d->world, id, d->rank));
-      d->nccl_buf.reserve(4 * (size_t)d->world + 16);
-    }
+    if (d->world > 1) d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)d->world + 16, (size_t)I + 8));
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
     const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
     d->max_warps = warps;
@@ -470,7 +498,9 @@ void print_timeline(hwwg_driver* d, int nseg, int step) {
 // local weight scan -> all-gather of the rank totals -> the same host plan on
 // every rank (hwwg_comb_plan) -> this rank's teeth -> grouped NCCL send/recv so
 // rank r ends up holding next-step histories shard(r), in history order.
-void multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
+// Returns the number of combed histories (the target, or 0 when the global
+// census is empty: a volumetric-source run before its first census).
+uint64_t multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
   const int W = d->world, R = d->rank;
   const uint64_t n = d->bank_n;
   d->comb_mem.reserve(4 + std::max<uint64_t>(n, 1));
@@ -485,10 +515,18 @@ void multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
   a.temp_bytes = tb;
   launch_fast_comb_local_scan(a, s);  // scalars[0] = this rank's census weight
   d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)W + 16, (size_t)d->I + 8));
-  NCCL_CHECK(ncclAllGather(d->comb_mem.p, d->nccl_buf.p, 1, ncclDouble, d->comm, s));
+  d->comm->all_gather(d->comb_mem.p, d->nccl_buf.p, 1, DType::kF64, s);
   std::vector<double> wr(W);
   HWWG_CUDA(cudaMemcpyAsync(wr.data(), d->nccl_buf.p, W * 8, cudaMemcpyDeviceToHost, s));
   HWWG_CUDA(cudaStreamSynchronize(s));
+  double total = 0.0;
+  for (double w : wr) total += w;
+  if (!(total > 0.0)) {  // same decision on every rank (same gathered totals)
+    HWWG_CUDA(cudaMemsetAsync(d->comb_mem.p, 0, 4 * sizeof(double), s));
+    d->shard_lo = 0;
+    d->fsrc_local = 0;
+    return 0;
+  }
   Xoshiro rng;  // the comb stream of the step (driver.cpp:119-121), same on every rank
   rng.seed(d->cfg.seed, stream_id_host(step, 0, 3));
   const double frac = rng.uniform();
@@ -513,9 +551,10 @@ void multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
   uint64_t lo, hi;
   hwwg_shard_range(d->target, R, W, &lo, &hi);
   d->shard_lo = lo;
+  d->fsrc_local = hi - lo;
   d->fsrc.reserve(std::max<uint64_t>(hi - lo, 1));
   const FastBank src = d->fsrc.view(), th = d->fteeth.view();
-  NCCL_CHECK(ncclGroupStart());
+  d->comm->group_start();
   for (int q = 0; q < W; ++q) {
     if (send[q]) {
       const uint64_t o = first[q] - klo[R];
@@ -525,20 +564,25 @@ void multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
         HWWG_CUDA(cudaMemcpyAsync(src.wt + dst, th.wt + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
         HWWG_CUDA(cudaMemcpyAsync(src.meta + dst, th.meta + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
       } else {
-        NCCL_CHECK(ncclSend(th.xm + o, 2 * send[q], ncclDouble, q, d->comm, s));
-        NCCL_CHECK(ncclSend(th.wt + o, 2 * send[q], ncclDouble, q, d->comm, s));
-        NCCL_CHECK(ncclSend(th.meta + o, 4 * send[q], ncclUint32, q, d->comm, s));
+        d->comm->send(th.xm + o, 2 * send[q], DType::kF64, q, s);
+        d->comm->send(th.wt + o, 2 * send[q], DType::kF64, q, s);
+        d->comm->send(th.meta + o, 4 * send[q], DType::kU32, q, s);
       }
     }
     if (recv[q] && q != R) {
       const uint64_t dst = std::max(klo[q], lo) - lo;
-      NCCL_CHECK(ncclRecv(src.xm + dst, 2 * recv[q], ncclDouble, q, d->comm, s));
-      NCCL_CHECK(ncclRecv(src.wt + dst, 2 * recv[q], ncclDouble, q, d->comm, s));
-      NCCL_CHECK(ncclRecv(src.meta + dst, 4 * recv[q], ncclUint32, q, d->comm, s));
+      d->comm->recv(src.xm + dst, 2 * recv[q], DType::kF64, q, s);
+      d->comm->recv(src.wt + dst, 2 * recv[q], DType::kF64, q, s);
+      d->comm->recv(src.meta + dst, 4 * recv[q], DType::kU32, q, s);
     }
   }
-  NCCL_CHECK(ncclGroupEnd());
+  d->comm->group_end(s);
   d->launches += 3;
+  // the step record's comb scalars: global input weight and combed weight
+  const double sc[4] = {total, spacing, offset, spacing * (double)d->target};
+  // (pageable source: staged before the call returns)
+  HWWG_CUDA(cudaMemcpyAsync(d->comb_mem.p, sc, sizeof sc, cudaMemcpyHostToDevice, s));
+  return d->target;
 }
 
 // One time step (driver.cpp:99-284).
@@ -558,6 +602,16 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const double theta_eff = step == 1 ? 1.0 : c.theta;
   const int ma_k = c.mode == 3 ? c.ma_base_k : 0;
   const int prev = d->rep_cur ^ 1;  // report of the previous step lives in the other buffer
+  // config-3: the step's LOSM q (precomputed) and the volumetric particles' weight
+  d->q_step = nullptr;
+  d->step_wref = c.strength;
+  if (c.vol_rate > 0.0 && d->q_row[step] >= 0) {
+    d->q_step = d->q_all.p + (size_t)d->q_row[step] * I;
+    const double ta = std::max(rec->t_begin, c.vol_t_lo), tb = std::min(rec->t_end, c.vol_t_hi);
+    if (c.vol_histories)
+      d->step_wref = std::max(d->step_wref, c.vol_rate * (tb - ta) *
+                                                (double)c.histories_per_step / (double)c.vol_histories);
+  }
 
   // ---- the start-of-step windows (driver.cpp:136-167) on stream st: record
   // flags, then lww centres or the lagged hybrid solve
@@ -620,7 +674,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // Single-GPU Philox steps without a volumetric source (whose q is known only
   // after the comb): the window update depends on the previous step alone, so
   // it runs on the auxiliary stream alongside the comb.
-  const bool early_windows = d->fast && d->world == 1 && !(c.vol_rate > 0.0) && !d->phases_on;
+  const bool early_windows = d->fast && d->world == 1 && !d->phases_on;
   if (early_windows) {
     // backup of the windows so an overflowing step can be replayed exactly
     // (taken by the hybrid solve kernel itself when there is one)
@@ -698,7 +752,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // config-3 runs: room after the source for the step's volumetric particles
   const uint64_t vol_cap = c.vol_rate > 0.0 ? c.vol_histories : 0;
   uint64_t H;
-  if (d->bank_n == 0 && (c.no_pulse || c.vol_rate > 0.0)) {
+  if (d->world == 1 && d->bank_n == 0 && (c.no_pulse || c.vol_rate > 0.0)) {
     // volumetric-source run before any census exists: nothing to comb
     H = 0;
     rec->comb_in = rec->comb_out = 0;
@@ -706,10 +760,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (!d->fast) d->source.reserve(std::max<uint64_t>(vol_cap, 1));
   } else if (d->fast && d->world > 1) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
-    multi_gpu_comb(d, step, s);
-    H = d->target;
+    H = multi_gpu_comb(d, step, s);
     rec->comb_in = d->bank_n;  // this rank's census slots
-    rec->comb_out = d->target;
+    rec->comb_out = H;
+    if (H == 0 && !d->fast) d->source.reserve(std::max<uint64_t>(vol_cap, 1));
   } else if (d->fast && c.host_bank && d->host_pre_combed) {
     H = d->target;  // combed on the device at the end of the previous step
     rec->comb_in = d->pre_comb_in;
@@ -775,41 +829,37 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   }
 
   // ---- config-3 volumetric source: this step's particles follow the combed
-  // census (histories [H, H + n)); the LOSM gets the step's q
-  d->q_step = nullptr;
-  d->step_wref = c.strength;
+  // census (histories [H, H + n)); the LOSM gets the step's q (set above).
+  // Philox mode samples them on the device, each rank its shard of the n; exact
+  // mode replays the reference-style sequential source stream on the host.
+  const uint64_t H_comb = H;
+  uint64_t v_lo = 0, v_hi = 0;  // this rank's slice of the step's volumetric particles
   if (c.vol_rate > 0.0) {
     const double ta = std::max(rec->t_begin, c.vol_t_lo);
     const double tb = std::min(rec->t_end, c.vol_t_hi);
-    if (tb > ta) {
+    if (tb > ta && c.vol_histories) {
       const uint64_t nv = c.vol_histories;
-      if (nv)
-        d->step_wref = std::max(d->step_wref, c.vol_rate * (tb - ta) *
-                                                  (double)c.histories_per_step / (double)nv);
-      std::vector<hwwg_particle> vh(nv);
-      sample_volume_source_host(c.seed, step, nv, c.vol_x_lo, c.vol_x_hi, ta, tb, c.vol_rate,
-                                c.histories_per_step, vh.data());
-      std::vector<double> qh(I);
-      volume_q_host(d->prob.edges.data(), I, c.vol_x_lo, c.vol_x_hi, ta, tb, dt, c.vol_rate,
-                    qh.data());
-      d->q_dev.reserve(I);
-      HWWG_CUDA(cudaMemcpyAsync(d->q_dev.p, qh.data(), I * 8, cudaMemcpyHostToDevice, s));
-      d->q_step = d->q_dev.p;
+      const double wv = c.vol_rate * (tb - ta) * (double)c.histories_per_step / (double)nv;
+      v_hi = nv;
+      if (d->world > 1) hwwg_shard_range(nv, d->rank, d->world, &v_lo, &v_hi);
       if (d->fast) {
-        d->vol_dev.reserve(nv);
-        HWWG_CUDA(cudaMemcpyAsync(d->vol_dev.p, vh.data(), nv * sizeof(hwwg_particle),
-                                  cudaMemcpyHostToDevice, s));
+        // after this rank's combed shard in the SoA source
+        const uint64_t at = d->world > 1 ? d->fsrc_local : H_comb;
         const FastBank f = d->fsrc.view();
-        launch_aos_to_fast(d->vol_dev.p, nv, d->prob.view, FastBank{f.xm + H, f.wt + H, f.meta + H},
-                           H, s);
+        launch_volume_source(FastBank{f.xm + at, f.wt + at, f.meta + at}, v_hi - v_lo, v_lo,
+                             H_comb + v_lo, d->prob.view, (unsigned)c.seed,
+                             (unsigned)(c.seed >> 32) ^ 0x6a09e667u, (unsigned)step, c.vol_x_lo,
+                             c.vol_x_hi, ta, tb, wv, s);
         ++d->launches;
       } else {
+        std::vector<hwwg_particle> vh(nv);
+        sample_volume_source_host(c.seed, step, nv, c.vol_x_lo, c.vol_x_hi, ta, tb, c.vol_rate,
+                                  c.histories_per_step, vh.data());
+        // pageable: staged before the call returns, so vh may go out of scope
         HWWG_CUDA(cudaMemcpyAsync(d->source.p + H, vh.data(), nv * sizeof(hwwg_particle),
                                   cudaMemcpyHostToDevice, s));
+        rec->h2d_bytes += nv * sizeof(hwwg_particle);
       }
-      // pageable sources: the copies complete before this returns to the loop
-      HWWG_CUDA(cudaStreamSynchronize(s));
-      rec->h2d_bytes += nv * sizeof(hwwg_particle) + I * 8;
       H += nv;
     }
   }
@@ -918,6 +968,17 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     ea.err = d->err.p;
     if (!d->fast) d->xlog.reset_need(s);
     uint64_t h_done = 0;
+    // this rank's histories: combed [c_lo, c_hi), volumetric H_comb + [v_lo, v_hi)
+    const uint64_t c_lo = d->world > 1 ? d->shard_lo : 0;
+    const uint64_t c_hi = d->world > 1 ? d->shard_lo + d->fsrc_local : H_comb;
+    auto owned_before = [&](uint64_t g) -> uint64_t {  // owned histories below global g
+      const uint64_t a = std::min(std::max(g, c_lo), c_hi) - c_lo;
+      const uint64_t gv = g > H_comb ? g - H_comb : 0;
+      return a + (std::min(std::max(gv, v_lo), v_hi) - v_lo);
+    };
+    auto global_of = [&](uint64_t l) -> uint64_t {  // global history of local index l
+      return l < c_hi - c_lo ? c_lo + l : H_comb + v_lo + (l - (c_hi - c_lo));
+    };
     bool pool_reset_done = start_reset;  // the step start or the mid-step update reset the pool
     int grid_warps_max = 0;     // largest transport grid of this step so far
     bool tail_filled = false;   // the last segment filled the census chunk tails
@@ -938,20 +999,19 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         FastArgs fa{};
         fa.pool_reset_done = pool_reset_done ? 1 : 0;
         fa.span = d->seg_events ? nullptr : d->span.p + 2 * nseg;
-        fa.pdl = pool_reset_done && d->pdl && !d->phases_on;  // right after the window update
+        // right after the window update (one rank per stream: a loopback hub's
+        // shared stream interleaves the ranks' kernels)
+        fa.pdl = pool_reset_done && d->pdl && !d->phases_on && d->world == 1;
         pool_reset_done = false;
-        // this rank's part of the segment: global [h_done, h_stop) ∩ its shard
-        uint64_t g_lo = h_done, g_hi = h_stop;
-        if (d->world > 1) {
-          uint64_t s_lo, s_hi;
-          hwwg_shard_range(H, d->rank, d->world, &s_lo, &s_hi);
-          g_lo = std::min(std::max(h_done, s_lo), s_hi);
-          g_hi = std::min(std::max(h_stop, s_lo), s_hi);
-        }
-        const uint64_t l_lo = g_lo - d->shard_lo;
+        // this rank's part of the segment: global [h_done, h_stop) ∩ (its shard
+        // of the combed histories ∪ its slice of the volumetric ones), which is
+        // one contiguous range of its local source (combed shard, then slice)
+        const uint64_t l_lo = owned_before(h_done), l_hi = owned_before(h_stop);
+        const uint64_t g_lo = global_of(l_lo);
+        const uint64_t g_hi = l_hi > l_lo ? global_of(l_hi - 1) + 1 : g_lo;
         const FastBank src = d->fsrc.view();
         fa.src = FastBank{src.xm + l_lo, src.wt + l_lo, src.meta + l_lo};
-        fa.n_src = g_hi - g_lo;
+        fa.n_src = l_hi - l_lo;
         fa.src_head = d->src_head.p;
         fa.census = d->fcensus.view();
         fa.census_count = d->counter.p;
@@ -1013,7 +1073,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           // (a measured rate varies step to step: 30% margin; the cold-start
           // prior is already generous)
           const double margin = d->events_measured ? 1.3 : 1.0;
-          const double per_block = (double)(g_hi - g_lo) * d->events_per_history * margin /
+          const double per_block = (double)fa.n_src * d->events_per_history * margin /
                                    (double)std::max(1, d->sms * bps);
           if (fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
               bps >= fast_blocks_per_sm(smem) && per_block <= (double)kFastFixBudget) {
@@ -1087,10 +1147,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       a.bclosure_tally = d->tal.p.boundary_closure;
       if (d->world > 1) {  // the snapshot is of ALL ranks' histories so far
         d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)d->world + 16, (size_t)I + 8));
-        NCCL_CHECK(ncclAllReduce(d->tal.p.census_closure, d->nccl_buf.p, I, ncclDouble, ncclSum,
-                                 d->comm, s));
-        NCCL_CHECK(ncclAllReduce(d->tal.p.boundary_closure, d->nccl_buf.p + I, 2, ncclDouble,
-                                 ncclSum, d->comm, s));
+        d->comm->all_reduce(d->tal.p.census_closure, d->nccl_buf.p, I, DType::kF64, RedOp::kSum, s);
+        d->comm->all_reduce(d->tal.p.boundary_closure, d->nccl_buf.p + I, 2, DType::kF64,
+                            RedOp::kSum, s);
         a.closure_tally = d->nccl_buf.p;
         a.bclosure_tally = d->nccl_buf.p + I;
       }
@@ -1136,7 +1195,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                                      derr.code ? 1ULL : 0ULL};
       unsigned long long* dflag = reinterpret_cast<unsigned long long*>(d->nccl_buf.p);
       HWWG_CUDA(cudaMemcpyAsync(dflag, flags, sizeof flags, cudaMemcpyHostToDevice, s));
-      NCCL_CHECK(ncclAllReduce(dflag, dflag, 2, ncclUint64, ncclMax, d->comm, s));
+      d->comm->all_reduce(dflag, dflag, 2, DType::kU64, RedOp::kMax, s);
       HWWG_CUDA(cudaMemcpyAsync(flags, dflag, sizeof flags, cudaMemcpyDeviceToHost, s));
       HWWG_CUDA(cudaStreamSynchronize(s));
       if (flags[1] && !derr.code) derr.code = HWWG_EINVAL;  // a peer failed
@@ -1234,11 +1293,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
 
   // ---- finalize (driver.cpp:221-222)
   if (d->world > 1) {  // step-end reduction of the whole tally slab and counters
-    NCCL_CHECK(ncclAllReduce(d->tal.slab.p, d->tal.slab.p, d->tal.doubles, ncclDouble, ncclSum,
-                             d->comm, s));
+    d->comm->all_reduce(d->tal.slab.p, d->tal.slab.p, d->tal.doubles, DType::kF64, RedOp::kSum, s);
     unsigned long long* u64part = reinterpret_cast<unsigned long long*>(d->tal.slab.p + d->tal.doubles);
-    NCCL_CHECK(ncclAllReduce(u64part, u64part, (size_t)I + kNumUCounters, ncclUint64, ncclSum,
-                             d->comm, s));
+    d->comm->all_reduce(u64part, u64part, (size_t)I + kNumUCounters, DType::kU64, RedOp::kSum, s);
   }
   if (!early_finalize) enqueue_finalize();
 
@@ -1486,9 +1543,9 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     return fail(HWWG_EINVAL, "multi-GPU runs need HWWG_RNG_PHILOX and 0 <= rank < world "
                              "(exact mode replays one sequential comb)");
   }
-  if (d->world > 1 && cfg->vol_rate > 0.0) {
+  if (d->opt.loopback && d->world != loopback_world(d->opt.loopback)) {
     delete d;
-    return fail(HWWG_EINVAL, "the volumetric source runs on one GPU");
+    return fail(HWWG_EINVAL, "loopback hub world differs from the driver's world");
   }
   if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
     delete d;

@@ -178,6 +178,11 @@ void launch_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out, cudaStream_
 // hist0 + i, and (w0, t0) when uniform.
 void launch_check_uniform(const double2* wt, uint64_t n, unsigned* flag, double2* first,
                           cudaStream_t s);
+// Config-3 volumetric source particles j0 .. j0+n-1 of a step (Philox mode),
+// written to out[0..n) as histories hist0 .. hist0+n-1.
+void launch_volume_source(FastBank out, uint64_t n, uint64_t j0, uint64_t hist0, const MeshView& m,
+                          unsigned k0, unsigned k1, unsigned step, double x_lo, double x_hi,
+                          double ta, double tb, double w, cudaStream_t s);
 void launch_xm_to_fast(FastBank out, uint64_t n, const MeshView& m, uint64_t hist0, int uniform,
                        double w0, double t0, cudaStream_t s);
 

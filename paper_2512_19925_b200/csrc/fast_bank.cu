@@ -400,7 +400,41 @@ __global__ void k_xm_to_fast(FastBank out, uint64_t n, const MeshView m, uint64_
   out.meta[i] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)(hist0 + i), 0u, 0u);
 }
 
+// Config-3 volumetric source on the device (Philox mode; DESIGN.md "Config-3
+// features"): particle j of the step's box emission gets x ~ U[x_lo, x_hi],
+// t ~ U[ta, tb], mu ~ U(-1, 1) from two Philox blocks keyed by (seed ^ a source
+// constant; j, step) — a stream no transport event uses — weight w, history
+// hist0 + i.  j = j0 + i: any rank samples any slice of the same emission.
+__global__ void k_volume_source(FastBank out, uint64_t n, uint64_t j0, uint64_t hist0,
+                                const MeshView m, unsigned k0, unsigned k1, unsigned step,
+                                double x_lo, double x_hi, double ta, double tb, double w) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t j = j0 + i;
+  const unsigned sk0 = k0 ^ 0x3c6ef372u, sk1 = k1 ^ 0xa54ff53au;
+  double ux, ut, umu, unused;
+  philox_uniform2(philox4x32_10(U4{(unsigned)j, (unsigned)(j >> 32), step, 0u}, sk0, sk1), ux, ut);
+  philox_uniform2(philox4x32_10(U4{(unsigned)j, (unsigned)(j >> 32), step, 1u}, sk0, sk1), umu,
+                  unused);
+  const double x = x_lo + (x_hi - x_lo) * ux;
+  const double t = ta + (tb - ta) * ut;
+  const double mu = 2.0 * umu - 1.0;
+  const int c = locate_cell(m, x);
+  out.xm[i] = make_double2(x, mu);
+  out.wt[i] = make_double2(w, t);
+  out.meta[i] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)(hist0 + i), 0u, 0u);
+}
+
 }  // namespace
+
+void launch_volume_source(FastBank out, uint64_t n, uint64_t j0, uint64_t hist0, const MeshView& m,
+                          unsigned k0, unsigned k1, unsigned step, double x_lo, double x_hi,
+                          double ta, double tb, double w, cudaStream_t s) {
+  if (!n) return;
+  k_volume_source<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, j0, hist0, m, k0, k1, step,
+                                                              x_lo, x_hi, ta, tb, w);
+  HWWG_CUDA(cudaGetLastError());
+}
 
 void launch_check_uniform(const double2* wt, uint64_t n, unsigned* flag, double2* first,
                           cudaStream_t s) {

@@ -765,7 +765,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       double d = d_census;
       if (d_coll < d) d = d_coll;
       if (d_b < d) d = d_b;
-      if (d < 0.0) d = 0.0;  // rounding at an edge: zero-length step
+      // (a d_b < 0 from rounding at an edge is a crossing, as in the reference:
+      // transport.cpp:135-164 takes min{} as is and tests d == d_boundary)
       if (d > 0.0) {
         trk_v = p.w * d * ci.inv_dx * a.inv_dt;
         trk_key = p.bslot * I + p.cell;

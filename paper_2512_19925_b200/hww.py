@@ -441,16 +441,20 @@ class Driver:
     Multi-GPU (one process per GPU): pass rank, world and the 128-byte NCCL id
     that rank 0 made with nccl_unique_id(); every rank then runs its shard of
     each step's histories and the driver all-reduces tallies / rebalances the
-    census itself (Philox mode)."""
+    census itself (Philox mode).  With `loopback` (a Loopback hub) the ranks are
+    threads of this process on one device instead (tests)."""
 
     def __init__(self, config: RunConfig, device=0, rng_mode=RNG_EXACT, rank=0, world=1,
-                 nccl_id: bytes = b""):
+                 nccl_id: bytes = b"", loopback=None):
         self.config = config
         self._cfg = config.to_c()
         self._h = C.c_void_p()
         opts = A.Options(device, rng_mode, 0, rank, world)
         for i, b in enumerate(bytes(nccl_id)[:128]):
             opts.nccl_id[i] = b
+        if loopback is not None:
+            opts.loopback = loopback.handle
+            self._hub = loopback  # the hub outlives its drivers
         _raise(A.lib().hwwg_driver_create(C.byref(self._cfg), C.byref(opts), C.byref(self._h)))
         self.I = config.cells
 
@@ -491,6 +495,31 @@ class Driver:
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             A.lib().hwwg_driver_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Loopback:
+    """hwwg_loopback: an in-process collective hub for `world` driver ranks on
+    one device (each rank's Driver.step must run on its own thread)."""
+
+    def __init__(self, world, device=0):
+        self.world = world
+        self._h = C.c_void_p()
+        _raise(A.lib().hwwg_loopback_create(world, device, C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            A.lib().hwwg_loopback_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

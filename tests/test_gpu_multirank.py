@@ -1,0 +1,160 @@
+"""The multi-GPU driver path run for real on ONE GPU.
+
+W driver ranks are host threads of this process sharing an in-process
+collective hub (hwwg_loopback, csrc/comm.cpp) instead of NCCL: the same
+driver_step code shards the histories, all-reduces the census-closure snapshot
+at every window-update barrier and the tally slab at step end, gathers the
+rank census weights for the global comb and rebalances the combed particles
+with grouped send/recv — only the transport of the bytes differs.
+
+Checks: integer bookkeeping (histories, comb_out, census counts summed over
+the ranks' banks), identical records on every rank, step 1 equal to the
+single-GPU run (the pulse source, the global comb of equal weights and the
+counter-based streams make step 1 the same histories), and later steps within
+replicate standard errors of W = 1."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2512_19925_b200 as hw
+
+pytestmark = pytest.mark.gpu
+
+
+def c2(H, steps, seed):
+    return hw.RunConfig(mode="hww_ma", ma_base_k=1, histories_per_step=H, rho=5.0, seed=seed,
+                        material=hw.Material(1.0, 0.9, 0.0, 0.0, 1.0), x_min=-20.0, x_max=20.0,
+                        cells=400, t_end=0.5 * steps, time_steps=steps)
+
+
+def c3(H, steps, seed, cells=300):
+    regions = [(10.0, hw.Material(1.0, 0.5, 0.0, 0.0, 1.0)),
+               (20.0, hw.Material(10.0, 1.0, 0.0, 0.0, 1.0)),
+               (30.0, hw.Material(1.0, 0.99, 0.0, 0.0, 1.0))]
+    return hw.RunConfig(mode="hww", histories_per_step=H, rho=4.0, seed=seed,
+                        material=hw.Material(1.0, 0.5, 0.0, 0.0, 1.0), x_min=0.0, x_max=30.0,
+                        cells=cells, t_end=0.5 * steps, time_steps=steps, regions=regions,
+                        volume_source=(0.0, 2.0, 0.0, 1.0, 1.0), no_pulse=True)
+
+
+def run_world(cfg, W, steps, with_bank=False):
+    """Steps 1..steps on W loopback ranks; per rank a list of (record, arrays, bank size)."""
+    if W == 1:
+        d = hw.Driver(cfg, rng_mode=hw.RNG_PHILOX)
+        out = []
+        for _ in range(steps):
+            r = d.step()
+            out.append((r, d.arrays(), len(d.bank()) if with_bank else None))
+        d.close()
+        return [out]
+    hub = hw.Loopback(W)
+    drivers = [hw.Driver(cfg, rng_mode=hw.RNG_PHILOX, rank=r, world=W, loopback=hub)
+               for r in range(W)]
+    res = [[] for _ in range(W)]
+    err = [None] * W
+
+    def work(r):
+        try:
+            for _ in range(steps):
+                rec = drivers[r].step()
+                res[r].append((rec, drivers[r].arrays(),
+                               len(drivers[r].bank()) if with_bank else None))
+        except Exception as e:  # noqa: BLE001 (re-raised below)
+            err[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(W)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for d in drivers:
+        d.close()
+    hub.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return res
+
+
+COUNTERS = ("collisions", "splits", "split_daughters", "roulette_kills", "roulette_survivals",
+            "census_count")
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_ranks_agree_and_bookkeeping(W):
+    H, steps = 30_000, 4
+    res = run_world(c2(H, steps, 5), W, steps, with_bank=True)
+    for n in range(steps):
+        r0, a0, _ = res[0][n]
+        assert r0.histories == H and r0.comb_out == H
+        # the comb conserves the global weight (popctrl.cpp:7-42)
+        np.testing.assert_allclose(r0.comb_out_weight, r0.comb_in_weight, rtol=1e-12)
+        # every rank reports the same all-reduced step
+        for r in range(1, W):
+            rr, ar, _ = res[r][n]
+            assert rr.segments == r0.segments and rr.histories == r0.histories
+            assert rr.counters.as_dict() == r0.counters.as_dict()
+            for k in ("phi_track", "sigma", "phi_census", "closure_census", "ww_centers"):
+                np.testing.assert_array_equal(ar[k], a0[k], err_msg=k)
+        # the ranks' banks hold exactly the global census
+        assert sum(res[r][n][2] for r in range(W)) == r0.counters.census_count
+        assert int(a0["tracks_per_cell"].sum()) == r0.segments
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_step1_equals_single_gpu(W):
+    """Step 1 runs the same histories on any number of ranks: the host-sampled
+    pulse, a global comb of equal weights (tooth k = particle k) and streams
+    keyed by history id.  Only fp64 summation order differs (the all-reduce
+    adds rank sums), so the counters are identical and tallies agree to 1e-9."""
+    H = 40_000
+    one = run_world(c2(H, 1, 17), 1, 1)[0][0]
+    many = run_world(c2(H, 1, 17), W, 1)[0][0]
+    (r1, a1, _), (rw, aw, _) = one, many
+    assert rw.segments == r1.segments
+    k1, kw = r1.counters.as_dict(), rw.counters.as_dict()
+    for k in COUNTERS:
+        assert kw[k] == k1[k], (k, kw[k], k1[k])
+    np.testing.assert_array_equal(aw["tracks_per_cell"], a1["tracks_per_cell"])
+    for k in ("phi_track", "phi_census", "ww_centers", "phi_hybrid"):
+        s = np.abs(a1[k]).max()
+        np.testing.assert_allclose(aw[k], a1[k], rtol=0, atol=1e-9 * s, err_msg=k)
+
+
+def test_config3_volumetric_source_sharded():
+    """Config 3 (regions, volumetric source sampled on the device, LOSM q) on two
+    ranks: step 1 (volumetric particles only, keyed by their global index) equals
+    the single-GPU step; histories include the sharded volumetric particles."""
+    H, steps = 20_000, 3
+    cfg = c3(H, steps, 3)
+    cfg.vol_histories = 10_000
+    one = run_world(cfg, 1, steps)[0]
+    two = run_world(cfg, 2, steps)
+    (r1, a1, _), (r2, a2, _) = one[0], two[0][0]
+    assert r1.histories == r2.histories == 10_000
+    assert r2.segments == r1.segments
+    np.testing.assert_array_equal(a2["tracks_per_cell"], a1["tracks_per_cell"])
+    assert two[1][0][0].segments == r2.segments
+    # step 2: combed census (H) + the step's volumetric particles on both ranks
+    assert two[0][1][0].histories == H + 10_000 == one[1][0].histories
+    assert two[0][2][0].histories == H  # the box ends at t = 1
+
+
+def test_later_steps_within_replicate_se():
+    """Steps 2-4 (census order, and so the comb, depend on scheduling): per-cell
+    replicate means of phi_track and census phi at W = 2 within 3 combined
+    standard errors of W = 1 on >= 95% of well-sampled cells."""
+    H, steps, R = 20_000, 4, 6
+    one = [run_world(c2(H, steps, 300 + i), 1, steps)[0] for i in range(R)]
+    two = [run_world(c2(H, steps, 400 + i), 2, steps)[0] for i in range(R)]
+    for n in range(1, steps):
+        for key in ("phi_track", "phi_census"):
+            a = np.array([one[i][n][1][key] for i in range(R)])
+            b = np.array([two[i][n][1][key] for i in range(R)])
+            ma, mb = a.mean(0), b.mean(0)
+            se = np.sqrt(a.var(0, ddof=1) / R + b.var(0, ddof=1) / R)
+            m = (ma > 1e-2 * ma.max()) & (se > 0)
+            z = (mb - ma)[m] / se[m]
+            assert np.mean(np.abs(z) < 3) >= 0.95, (n, key, np.sort(np.abs(z))[-5:])
+            assert abs(z.mean()) < 1.0, (n, key, z.mean())
