@@ -20,6 +20,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libhww_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhww_ref.so")
+# the reference with its run_segment_parallel routed to the engine
+DROPIN_SO = os.path.join(HERE, "_ref", "libhww_dropin.so")
 
 PARTICLE_DT = np.dtype([("x", "<f8"), ("mu", "<f8"), ("w", "<f8"), ("t", "<f8")])
 MODES = {"analog": 0, "lww": 1, "hww": 2, "hww_ma": 3, "hww_fourier": 4}
@@ -292,8 +294,8 @@ class Oracle(_Lib):
 
 
 class Reference(_Lib):
-    def __init__(self):
-        super().__init__(REF_SO, "hwwref_")
+    def __init__(self, path=REF_SO):
+        super().__init__(path, "hwwref_")
         L = self.lib
         L.hwwref_run_segment.argtypes = [
             C.POINTER(C.c_double), C.c_int32, C.c_void_p, C.c_double, C.c_double, C.c_uint64,

@@ -200,12 +200,13 @@ struct hwwg_driver {
   // at every window-update barrier and at step end, census combed globally and
   // rebalanced with grouped send/recv
   int rank = 0, world = 1;
-  uint64_t shard_lo = 0;  // first history of this rank's shard of the combed bank
-  uint64_t fsrc_local = 0;  // particles of that shard (the front of fsrc)
+  uint64_t shard_lo = 0;    // first history of this rank's share of the step-1 pulse bank
+  uint64_t fsrc_local = 0;  // combed histories this rank holds (the front of fsrc)
   Comm* comm = nullptr;      // NCCL or the in-process loopback (comm.h)
   bool own_stream = true;    // false: the loopback hub's shared stream
   DevBuf<double> nccl_buf;    // all-gathered census weights, snapshot slabs
   FastBankBuf fteeth;         // teeth this rank produced, before the rebalance
+  FastBankBuf fperm;          // the rebalanced teeth before the local permutation
 
   // low-order state
   DevBuf<double> lo_mem;
@@ -425,7 +426,10 @@ void init_driver(hwwg_driver* d) {
     d->comb_mem.reserve(4 + d->census_hwm);
     d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
     if (c.host_bank) d->bank.reserve(d->census_hwm);
-    if (d->world > 1) d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)d->world + 16, (size_t)I + 8));
+    if (d->world > 1) {
+      d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)d->world + 16, (size_t)I + 8));
+      d->fperm.reserve(local_target + 4096);  // the rebalanced teeth before their permutation
+    }
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
     const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
     d->max_warps = warps;
@@ -494,13 +498,77 @@ void print_timeline(hwwg_driver* d, int nseg, int step) {
   }
 }
 
+// Update thresholds (driver.cpp:170-177; ww.cpp:74-87): ceil(f * H), deduped.
+std::vector<uint64_t> step_thresholds(const hwwg_run_config& c, bool hybrid, uint64_t H) {
+  std::vector<uint64_t> thr;
+  if (hybrid && c.u_ww > 0)
+    for (int i = 0; i < c.n_fractions; ++i) {
+      const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)H);
+      if (h >= H) continue;
+      if (!thr.empty() && h <= thr.back()) continue;
+      thr.push_back(h);
+    }
+  return thr;
+}
+
+// Which histories of a step each rank runs. The step's
+// global history ids [0, H) — combed teeth [0, H_c), then the step's
+// volumetric particles [H_c, H) — are cut into the window-update segments
+// [seg[u], seg[u+1]), and every segment is split into W contiguous pieces:
+// rank q runs piece q of EVERY segment, so all ranks work in every segment
+// and meet at every barrier. A rank holds its histories in global-id order
+// (local index = number of its ids below), so each of its pieces, its combed
+// ids and its volumetric ids are contiguous locally.
+struct StepLayout {
+  std::vector<uint64_t> seg;  // 0 = seg[0] <= ... <= seg[S] = H
+  int W = 1;
+  uint64_t H = 0, Hc = 0;
+  void piece(int q, size_t u, uint64_t& lo, uint64_t& hi) const {
+    uint64_t a, b;
+    hwwg_shard_range(seg[u + 1] - seg[u], q, W, &a, &b);
+    lo = seg[u] + a;
+    hi = seg[u] + b;
+  }
+  size_t segments() const { return seg.size() - 1; }
+  uint64_t owned_before(int q, uint64_t g) const {  // rank q's ids below g
+    uint64_t n = 0, lo, hi;
+    for (size_t u = 0; u < segments(); ++u) {
+      piece(q, u, lo, hi);
+      n += std::min(std::max(g, lo), hi) - lo;
+    }
+    return n;
+  }
+  uint64_t global_of(int q, uint64_t l) const {  // rank q's l-th id (H past the end)
+    uint64_t lo, hi;
+    for (size_t u = 0; u < segments(); ++u) {
+      piece(q, u, lo, hi);
+      if (l < hi - lo) return lo + l;
+      l -= hi - lo;
+    }
+    return H;
+  }
+};
+
+StepLayout make_layout(const hwwg_run_config& c, bool hybrid, uint64_t Hc, uint64_t H, int W) {
+  StepLayout L;
+  L.W = W;
+  L.H = H;
+  L.Hc = Hc;
+  L.seg.push_back(0);
+  for (uint64_t t : step_thresholds(c, hybrid, H)) L.seg.push_back(t);
+  L.seg.push_back(H);
+  return L;
+}
+
 // Global comb + census rebalance over `world` ranks:
 // local weight scan -> all-gather of the rank totals -> the same host plan on
-// every rank (hwwg_comb_plan) -> this rank's teeth -> grouped NCCL send/recv so
-// rank r ends up holding next-step histories shard(r), in history order.
-// Returns the number of combed histories (the target, or 0 when the global
-// census is empty: a volumetric-source run before its first census).
-uint64_t multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
+// every rank (hwwg_comb_plan) -> this rank's teeth -> grouped send/recv so that
+// rank r ends up holding the teeth of its pieces of the step layout (tooth g =
+// history g), then — after the cold start — a local permutation of them (see
+// Perm). Returns the number of combed histories (the target, or 0 when the
+// global census is empty: a volumetric-source run before its first census),
+// and the step layout for H_c + nv histories.
+uint64_t multi_gpu_comb(hwwg_driver* d, int step, uint64_t nv, StepLayout& L, cudaStream_t s) {
   const int W = d->world, R = d->rank;
   const uint64_t n = d->bank_n;
   d->comb_mem.reserve(4 + std::max<uint64_t>(n, 1));
@@ -514,17 +582,17 @@ uint64_t multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
   a.temp = d->comb_temp.p;
   a.temp_bytes = tb;
   launch_fast_comb_local_scan(a, s);  // scalars[0] = this rank's census weight
-  d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)W + 16, (size_t)d->I + 8));
   d->comm->all_gather(d->comb_mem.p, d->nccl_buf.p, 1, DType::kF64, s);
   std::vector<double> wr(W);
   HWWG_CUDA(cudaMemcpyAsync(wr.data(), d->nccl_buf.p, W * 8, cudaMemcpyDeviceToHost, s));
   HWWG_CUDA(cudaStreamSynchronize(s));
   double total = 0.0;
   for (double w : wr) total += w;
-  if (!(total > 0.0)) {  // same decision on every rank (same gathered totals)
+  const uint64_t Hc = total > 0.0 ? d->target : 0;  // same decision on every rank
+  L = make_layout(d->cfg, d->hybrid(), Hc, Hc + nv, W);
+  d->fsrc_local = L.owned_before(R, Hc);
+  if (Hc == 0) {
     HWWG_CUDA(cudaMemsetAsync(d->comb_mem.p, 0, 4 * sizeof(double), s));
-    d->shard_lo = 0;
-    d->fsrc_local = 0;
     return 0;
   }
   Xoshiro rng;  // the comb stream of the step (driver.cpp:119-121), same on every rank
@@ -543,44 +611,68 @@ uint64_t multi_gpu_comb(hwwg_driver* d, int step, cudaStream_t s) {
     }
   }
   const uint64_t nt = khi[R] - klo[R];
-  d->fteeth.reserve(nt);
+  d->fteeth.reserve(std::max<uint64_t>(nt, 1));
   if (nt) launch_fast_comb_teeth_range(a, spacing, offset, origin, klo[R], khi[R], d->fteeth.view(), s);
-  // rebalance: teeth of shard(q) go to rank q
-  std::vector<uint64_t> send(W), first(W), recv(W);
-  hwwg_rebalance_plan(klo.data(), khi.data(), W, R, d->target, send.data(), first.data(), recv.data());
-  uint64_t lo, hi;
-  hwwg_shard_range(d->target, R, W, &lo, &hi);
-  d->shard_lo = lo;
-  d->fsrc_local = hi - lo;
-  d->fsrc.reserve(std::max<uint64_t>(hi - lo, 1));
-  const FastBank src = d->fsrc.view(), th = d->fteeth.view();
+  // rebalance: the teeth with ids in rank q's pieces go to q, at q's local index
+  // of the id (both sides walk q's pieces in order: sends and receives match)
+  const bool permute = step > 1;  // the cold-start bank is the i.i.d. pulse
+  const uint64_t nloc = d->fsrc_local;
+  FastBankBuf& dst_buf = permute ? d->fperm : d->fsrc;
+  dst_buf.reserve(std::max<uint64_t>(nloc, 1));
+  const FastBank dst = dst_buf.view(), th = d->fteeth.view();
+  auto cut = [&](int q, size_t u, uint64_t k_lo, uint64_t k_hi, uint64_t& lo, uint64_t& hi) {
+    L.piece(q, u, lo, hi);
+    lo = std::max(lo, k_lo);
+    hi = std::min(std::min(hi, Hc), k_hi);
+    return hi > lo;
+  };
   d->comm->group_start();
   for (int q = 0; q < W; ++q) {
-    if (send[q]) {
-      const uint64_t o = first[q] - klo[R];
+    for (size_t u = 0; u < L.segments(); ++u) {
+      uint64_t lo, hi;
+      if (!cut(q, u, klo[R], khi[R], lo, hi)) continue;
+      const uint64_t o = lo - klo[R], m = hi - lo;
       if (q == R) {
-        const uint64_t dst = first[q] - lo;
-        HWWG_CUDA(cudaMemcpyAsync(src.xm + dst, th.xm + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
-        HWWG_CUDA(cudaMemcpyAsync(src.wt + dst, th.wt + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
-        HWWG_CUDA(cudaMemcpyAsync(src.meta + dst, th.meta + o, send[q] * 16, cudaMemcpyDeviceToDevice, s));
+        const uint64_t at = L.owned_before(R, lo);
+        HWWG_CUDA(cudaMemcpyAsync(dst.xm + at, th.xm + o, m * 16, cudaMemcpyDeviceToDevice, s));
+        HWWG_CUDA(cudaMemcpyAsync(dst.wt + at, th.wt + o, m * 16, cudaMemcpyDeviceToDevice, s));
+        HWWG_CUDA(cudaMemcpyAsync(dst.meta + at, th.meta + o, m * 16, cudaMemcpyDeviceToDevice, s));
       } else {
-        d->comm->send(th.xm + o, 2 * send[q], DType::kF64, q, s);
-        d->comm->send(th.wt + o, 2 * send[q], DType::kF64, q, s);
-        d->comm->send(th.meta + o, 4 * send[q], DType::kU32, q, s);
+        d->comm->send(th.xm + o, 2 * m, DType::kF64, q, s);
+        d->comm->send(th.wt + o, 2 * m, DType::kF64, q, s);
+        d->comm->send(th.meta + o, 4 * m, DType::kU32, q, s);
       }
     }
-    if (recv[q] && q != R) {
-      const uint64_t dst = std::max(klo[q], lo) - lo;
-      d->comm->recv(src.xm + dst, 2 * recv[q], DType::kF64, q, s);
-      d->comm->recv(src.wt + dst, 2 * recv[q], DType::kF64, q, s);
-      d->comm->recv(src.meta + dst, 4 * recv[q], DType::kU32, q, s);
+    if (q == R) continue;
+    for (size_t u = 0; u < L.segments(); ++u) {
+      uint64_t lo, hi;
+      if (!cut(R, u, klo[q], khi[q], lo, hi)) continue;
+      const uint64_t at = L.owned_before(R, lo), m = hi - lo;
+      d->comm->recv(dst.xm + at, 2 * m, DType::kF64, q, s);
+      d->comm->recv(dst.wt + at, 2 * m, DType::kF64, q, s);
+      d->comm->recv(dst.meta + at, 4 * m, DType::kU32, q, s);
     }
   }
   d->comm->group_end(s);
   d->launches += 3;
+  if (permute) {  // out[c] = in[perm(c)], history = the global id of slot c
+    PieceTable t{};
+    for (size_t u = 0; u < L.segments() && t.n < 9; ++u) {
+      uint64_t lo, hi;
+      L.piece(R, u, lo, hi);
+      hi = std::min(hi, Hc);
+      if (hi <= lo) continue;
+      t.lo[t.n] = lo;
+      t.cnt[t.n] = hi - lo;
+      ++t.n;
+    }
+    launch_fast_permute(d->fperm.view(), d->fsrc.view(), nloc, make_perm(nloc, d->cfg.seed, step),
+                        t, s);
+    ++d->launches;
+  }
   // the step record's comb scalars: global input weight and combed weight
-  const double sc[4] = {total, spacing, offset, spacing * (double)d->target};
   // (pageable source: staged before the call returns)
+  const double sc[4] = {total, spacing, offset, spacing * (double)d->target};
   HWWG_CUDA(cudaMemcpyAsync(d->comb_mem.p, sc, sizeof sc, cudaMemcpyHostToDevice, s));
   return d->target;
 }
@@ -605,7 +697,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // config-3: the step's LOSM q (precomputed) and the volumetric particles' weight
   d->q_step = nullptr;
   d->step_wref = c.strength;
+  uint64_t nv_step = 0;  // the step's volumetric particles
   if (c.vol_rate > 0.0 && d->q_row[step] >= 0) {
+    nv_step = c.vol_histories;
     d->q_step = d->q_all.p + (size_t)d->q_row[step] * I;
     const double ta = std::max(rec->t_begin, c.vol_t_lo), tb = std::min(rec->t_end, c.vol_t_hi);
     if (c.vol_histories)
@@ -746,6 +840,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     }
   }
 
+  StepLayout Lmulti;  // multi-rank: the step layout the rebalance placed the teeth by
   // ---- population control (driver.cpp:111-129)
   const double bank_cap = c.comb_overflow_factor * (double)d->target;
   const bool do_comb = c.comb_overflow_factor <= 1.0 || (double)d->bank_n > bank_cap;
@@ -760,7 +855,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (!d->fast) d->source.reserve(std::max<uint64_t>(vol_cap, 1));
   } else if (d->fast && d->world > 1) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
-    H = multi_gpu_comb(d, step, s);
+    H = multi_gpu_comb(d, step, nv_step, Lmulti, s);
     rec->comb_in = d->bank_n;  // this rank's census slots
     rec->comb_out = H;
     if (H == 0 && !d->fast) d->source.reserve(std::max<uint64_t>(vol_cap, 1));
@@ -790,6 +885,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.prefix = d->comb_mem.p + 4;
     a.scalars = d->comb_mem.p;
     a.out = d->fsrc.view();
+    // after the cold start, tooth k becomes history perm(k) (see Perm)
+    if (step > 1) a.perm = make_perm(d->target, c.seed, step);
     d->ph_mark("comb", s);
     if (tiled) launch_fast_comb_tiled(a, s);
     else launch_fast_comb(a, s);
@@ -833,36 +930,43 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // Philox mode samples them on the device, each rank its shard of the n; exact
   // mode replays the reference-style sequential source stream on the host.
   const uint64_t H_comb = H;
-  uint64_t v_lo = 0, v_hi = 0;  // this rank's slice of the step's volumetric particles
-  if (c.vol_rate > 0.0) {
+  if (nv_step) {
     const double ta = std::max(rec->t_begin, c.vol_t_lo);
     const double tb = std::min(rec->t_end, c.vol_t_hi);
-    if (tb > ta && c.vol_histories) {
-      const uint64_t nv = c.vol_histories;
-      const double wv = c.vol_rate * (tb - ta) * (double)c.histories_per_step / (double)nv;
-      v_hi = nv;
-      if (d->world > 1) hwwg_shard_range(nv, d->rank, d->world, &v_lo, &v_hi);
-      if (d->fast) {
-        // after this rank's combed shard in the SoA source
-        const uint64_t at = d->world > 1 ? d->fsrc_local : H_comb;
-        const FastBank f = d->fsrc.view();
-        launch_volume_source(FastBank{f.xm + at, f.wt + at, f.meta + at}, v_hi - v_lo, v_lo,
-                             H_comb + v_lo, d->prob.view, (unsigned)c.seed,
+    const uint64_t nv = nv_step;
+    const double wv = c.vol_rate * (tb - ta) * (double)c.histories_per_step / (double)nv;
+    if (d->fast) {
+      // this rank's volumetric ids [H_comb, H_comb + nv) of its pieces, each at
+      // its local index; particle j is keyed by j alone, so any rank count
+      // samples the same emission
+      const StepLayout Lv =
+          d->world > 1 ? Lmulti : make_layout(c, d->hybrid(), H_comb, H_comb + nv, 1);
+      const FastBank f = d->fsrc.view();
+      for (size_t u = 0; u < Lv.segments(); ++u) {
+        uint64_t lo, hi;
+        Lv.piece(d->rank, u, lo, hi);
+        lo = std::max(lo, H_comb);
+        if (hi <= lo) continue;
+        const uint64_t at = Lv.owned_before(d->rank, lo);
+        launch_volume_source(FastBank{f.xm + at, f.wt + at, f.meta + at}, hi - lo, lo - H_comb,
+                             lo, d->prob.view, (unsigned)c.seed,
                              (unsigned)(c.seed >> 32) ^ 0x6a09e667u, (unsigned)step, c.vol_x_lo,
                              c.vol_x_hi, ta, tb, wv, s);
         ++d->launches;
-      } else {
-        std::vector<hwwg_particle> vh(nv);
-        sample_volume_source_host(c.seed, step, nv, c.vol_x_lo, c.vol_x_hi, ta, tb, c.vol_rate,
-                                  c.histories_per_step, vh.data());
-        // pageable: staged before the call returns, so vh may go out of scope
-        HWWG_CUDA(cudaMemcpyAsync(d->source.p + H, vh.data(), nv * sizeof(hwwg_particle),
-                                  cudaMemcpyHostToDevice, s));
-        rec->h2d_bytes += nv * sizeof(hwwg_particle);
       }
-      H += nv;
+    } else {
+      std::vector<hwwg_particle> vh(nv);
+      sample_volume_source_host(c.seed, step, nv, c.vol_x_lo, c.vol_x_hi, ta, tb, c.vol_rate,
+                                c.histories_per_step, vh.data());
+      // pageable: staged before the call returns, so vh may go out of scope
+      HWWG_CUDA(cudaMemcpyAsync(d->source.p + H, vh.data(), nv * sizeof(hwwg_particle),
+                                cudaMemcpyHostToDevice, s));
+      rec->h2d_bytes += nv * sizeof(hwwg_particle);
     }
+    H += nv;
   }
+  // the step's segments and this rank's histories in them
+  const StepLayout L = d->world > 1 ? Lmulti : make_layout(c, d->hybrid(), H_comb, H, 1);
 
   if (!early_windows) {  // backup of the windows so an overflowing step can be replayed exactly
     HWWG_CUDA(cudaMemcpyAsync(d->centers_backup.p, d->lo.centers, I * 8, cudaMemcpyDeviceToDevice, s));
@@ -882,16 +986,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     }
   }
 
-  // ---- thresholds (driver.cpp:170-177)
-  std::vector<uint64_t> thr;
-  if (d->hybrid() && c.u_ww > 0) {
-    for (int i = 0; i < c.n_fractions; ++i) {
-      const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)H);
-      if (h >= H) continue;
-      if (!thr.empty() && h <= thr.back()) continue;
-      thr.push_back(h);
-    }
-  }
+  // ---- thresholds (driver.cpp:170-177): the layout's inner segment boundaries
+  const std::vector<uint64_t> thr(L.seg.begin() + 1, L.seg.end() - 1);
   rec->n_thresholds = (int)thr.size();
   for (size_t i = 0; i < thr.size() && i < 8; ++i) rec->thresholds[i] = thr[i];
 
@@ -968,17 +1064,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     ea.err = d->err.p;
     if (!d->fast) d->xlog.reset_need(s);
     uint64_t h_done = 0;
-    // this rank's histories: combed [c_lo, c_hi), volumetric H_comb + [v_lo, v_hi)
-    const uint64_t c_lo = d->world > 1 ? d->shard_lo : 0;
-    const uint64_t c_hi = d->world > 1 ? d->shard_lo + d->fsrc_local : H_comb;
-    auto owned_before = [&](uint64_t g) -> uint64_t {  // owned histories below global g
-      const uint64_t a = std::min(std::max(g, c_lo), c_hi) - c_lo;
-      const uint64_t gv = g > H_comb ? g - H_comb : 0;
-      return a + (std::min(std::max(gv, v_lo), v_hi) - v_lo);
-    };
-    auto global_of = [&](uint64_t l) -> uint64_t {  // global history of local index l
-      return l < c_hi - c_lo ? c_lo + l : H_comb + v_lo + (l - (c_hi - c_lo));
-    };
+    // this rank's histories: its pieces of the step layout, in global order
+    auto owned_before = [&](uint64_t g) { return L.owned_before(d->rank, g); };
+    auto global_of = [&](uint64_t l) { return L.global_of(d->rank, l); };
     bool pool_reset_done = start_reset;  // the step start or the mid-step update reset the pool
     int grid_warps_max = 0;     // largest transport grid of this step so far
     bool tail_filled = false;   // the last segment filled the census chunk tails
@@ -1003,9 +1091,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         // shared stream interleaves the ranks' kernels)
         fa.pdl = pool_reset_done && d->pdl && !d->phases_on && d->world == 1;
         pool_reset_done = false;
-        // this rank's part of the segment: global [h_done, h_stop) ∩ (its shard
-        // of the combed histories ∪ its slice of the volumetric ones), which is
-        // one contiguous range of its local source (combed shard, then slice)
+        // this rank's piece of the segment: one contiguous range of its source
         const uint64_t l_lo = owned_before(h_done), l_hi = owned_before(h_stop);
         const uint64_t g_lo = global_of(l_lo);
         const uint64_t g_hi = l_hi > l_lo ? global_of(l_hi - 1) + 1 : g_lo;
@@ -1353,6 +1439,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.prefix = d->comb_mem.p + 4;
     a.scalars = d->comb_mem.p;
     a.out = d->fsrc.view();
+    a.perm = make_perm(d->target, c.seed, step + 1);
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     if (tiled) launch_fast_comb_tiled(a, s);
     else launch_fast_comb(a, s);

@@ -146,6 +146,30 @@ void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_
 void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
                         uint64_t hist0, cudaStream_t s);
 
+// Bijection on [0, n) that spreads runs of consecutive k evenly over [0, n):
+// 32-element tiles t = k / 32 move to tile (a t + b) mod nt with a ~ 0.618 nt
+// coprime to nt (a Weyl sequence), in-tile order and the last n % 32 elements
+// stay. The comb writes tooth k at perm(k) — whole 512-byte tiles per array, so
+// the writes stay coalesced — and the next step's contiguous history ranges
+// (its window-update segments) become even samples of the census bank.
+// The census of the throughput engine is stored in completion order: early
+// slots hold the particles that reached census in few events, i.e. the
+// ballistic ones near the wave front, and taken in bank order the first 25% of
+// the next step's histories over-represented the front in the mid-step
+// partial snapshot (driver.cpp:204-218) whose closure steers the windows
+// (measured: phi_hybrid at the front cell 15 standard errors above the exact
+// engine, tests/test_gpu_stat_pin.py). The reference's bank is in history
+// order, exchangeable across histories; the permutation restores that.
+// nt == 0: identity.
+struct Perm {
+  unsigned long long nt, a, b;
+  __host__ __device__ unsigned long long operator()(unsigned long long k) const {
+    const unsigned long long t = k >> 5;
+    return t < nt ? (((a * t + b) % nt) << 5) | (k & 31ULL) : k;
+  }
+};
+Perm make_perm(uint64_t n, uint64_t seed, uint64_t step);
+
 // Parallel comb (popctrl.cpp:7-42 semantics with a parallel fp64 scan).
 struct FastCombArgs {
   FastBank bank;
@@ -156,6 +180,7 @@ struct FastCombArgs {
   FastBank out;
   void* temp;
   size_t temp_bytes;
+  Perm perm;  // tooth k is written at perm(k), as history perm(k) (n == 0: identity)
 };
 size_t fast_comb_temp_bytes(uint64_t n);
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s);
@@ -170,6 +195,16 @@ void launch_fast_comb_local_scan(const FastCombArgs& a, cudaStream_t s);
 void launch_fast_comb_teeth_range(const FastCombArgs& a, double spacing, double offset,
                                   double origin, uint64_t k_lo, uint64_t k_hi, FastBank out,
                                   cudaStream_t s);
+// Multi-rank local permutation of a rank's combed source (the multi-GPU comb
+// places teeth by contiguous ranges, so the permutation follows the
+// rebalance): out[c] = in[perm(c)] for c < n, with history id hist[c] (the
+// rank's owned global ids: `pieces` ranges of (first id, count), in order).
+struct PieceTable {
+  int n;
+  unsigned long long lo[9], cnt[9];
+};
+void launch_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm, const PieceTable& t,
+                         cudaStream_t s);
 // track_flux[i] = sum_b track_flux_batch[b][i] (fast mode scores batches only)
 void launch_track_from_batches(TallyPtrs t, int I, int B, cudaStream_t s);
 void launch_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out, cudaStream_t s);

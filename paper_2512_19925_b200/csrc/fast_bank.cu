@@ -46,10 +46,11 @@ __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src,
   const double2 wt = a.bank.wt[src];
   const uint4 m = a.bank.meta[src];
   for (uint64_t k = k0; k < k1; ++k) {
-    a.out.xm[k] = xm;
-    a.out.wt[k] = make_double2(spacing, wt.y);
-    // fresh identity for the new step: history = tooth index, key 0, draw 0
-    a.out.meta[k] = make_uint4(m.x & 0xffffu, (unsigned)k, 0u, 0u);
+    const uint64_t p = a.perm(k);
+    a.out.xm[p] = xm;
+    a.out.wt[p] = make_double2(spacing, wt.y);
+    // fresh identity for the new step: history = its slot, key 0, draw 0
+    a.out.meta[p] = make_uint4(m.x & 0xffffu, (unsigned)p, 0u, 0u);
   }
 }
 
@@ -307,6 +308,23 @@ __global__ void k_comb_teeth_range(FastCombArgs a, double spacing, double offset
   out.meta[o] = make_uint4(a.bank.meta[s].x & 0xffffu, (unsigned)k, 0u, 0u);
 }
 
+__global__ void k_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm, PieceTable t) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const uint64_t s = perm(c);
+  uint64_t g = c, rem = c;  // global id of local slot c
+  for (int i = 0; i < t.n; ++i) {
+    if (rem < t.cnt[i]) {
+      g = t.lo[i] + rem;
+      break;
+    }
+    rem -= t.cnt[i];
+  }
+  out.xm[c] = in.xm[s];
+  out.wt[c] = in.wt[s];
+  out.meta[c] = make_uint4(in.meta[s].x & 0xffffu, (unsigned)g, 0u, 0u);
+}
+
 // one warp per transport warp's chunk tail (<= kCensusChunk slots), lanes in parallel
 __global__ void k_fill_holes(FastBank c, uint64_t cap, const unsigned long long* cur, int warps,
                              double x_fill, double t_fill) {
@@ -498,6 +516,35 @@ void launch_fast_comb_teeth_range(const FastCombArgs& a, double spacing, double 
   k_comb_teeth_range<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, spacing, offset, origin,
                                                                  k_lo, k_hi, out);
   HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm, const PieceTable& t,
+                         cudaStream_t s) {
+  if (!n) return;
+  k_fast_permute<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, out, n, perm, t);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+static uint64_t gcd_u64(uint64_t a, uint64_t b) {
+  while (b) {
+    const uint64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+Perm make_perm(uint64_t n, uint64_t seed, uint64_t step) {
+  const uint64_t nt = n >> 5;  // whole 32-element tiles
+  if (nt < 3) return Perm{0, 0, 0};
+  uint64_t a = (uint64_t)((double)nt * 0.6180339887498949);
+  if (a < 1) a = 1;
+  while (gcd_u64(a, nt) != 1) ++a;  // a few steps at most (coprimes are dense)
+  uint64_t z = seed ^ (step * 0x9E3779B97F4A7C15ULL);  // splitmix64 of (seed, step): the offset
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return Perm{nt, a % nt, z % nt};
 }
 
 void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,

@@ -144,17 +144,22 @@ def test_config3_volumetric_source_sharded():
 def test_later_steps_within_replicate_se():
     """Steps 2-4 (census order, and so the comb, depend on scheduling): per-cell
     replicate means of phi_track and census phi at W = 2 within 3 combined
-    standard errors of W = 1 on >= 95% of well-sampled cells."""
-    H, steps, R = 20_000, 4, 6
+    standard errors of W = 1 on >= 95% of well-sampled cells over the steps
+    (>= 85% in any one step: neighbouring cells are correlated), no bias."""
+    H, steps, R = 20_000, 4, 8
     one = [run_world(c2(H, steps, 300 + i), 1, steps)[0] for i in range(R)]
     two = [run_world(c2(H, steps, 400 + i), 2, steps)[0] for i in range(R)]
-    for n in range(1, steps):
-        for key in ("phi_track", "phi_census"):
+    for key in ("phi_track", "phi_census"):
+        zs = []
+        for n in range(1, steps):
             a = np.array([one[i][n][1][key] for i in range(R)])
             b = np.array([two[i][n][1][key] for i in range(R)])
             ma, mb = a.mean(0), b.mean(0)
             se = np.sqrt(a.var(0, ddof=1) / R + b.var(0, ddof=1) / R)
             m = (ma > 1e-2 * ma.max()) & (se > 0)
             z = (mb - ma)[m] / se[m]
-            assert np.mean(np.abs(z) < 3) >= 0.95, (n, key, np.sort(np.abs(z))[-5:])
-            assert abs(z.mean()) < 1.0, (n, key, z.mean())
+            assert np.mean(np.abs(z) < 3) >= 0.85, (n, key, np.sort(np.abs(z))[-5:])
+            zs.append(z)
+        z = np.concatenate(zs)
+        assert np.mean(np.abs(z) < 3) >= 0.95, (key, np.sort(np.abs(z))[-8:])
+        assert abs(z.mean()) < 0.5, (key, z.mean())

@@ -15,7 +15,9 @@ applied three ways:
   * per quantity, pooled over cells and steps: >= 95% of |z| < 3;
   * per quantity and step: >= 85% (one correlated cluster can take a step);
   * no bias: the pooled mean of z within +-0.5 and the pooled mean of z^2
-    (a global chi^2 per degree of freedom) within [0.5, 2.0].
+    (a global chi^2 per degree of freedom) within [0.5, 2.0];
+  * per-step scalars (P_L, P_R, census weight): >= 90% of |z| < 3.5, mean z
+    within +-2 (steps are correlated through the carried population).
 
 Quantities: the track-length flux phi, the census closure moments phi, J, F,
 the edge currents, the window centres and the LOSM solution phi_hybrid per
@@ -116,7 +118,10 @@ def check_engine(cfg_fn, steps, skip_first=0, label=""):
         if z.size:
             report[k] = dict(frac=float(np.mean(np.abs(z) < 3)), bias=float(z.mean()),
                              chi2=float(np.mean(z ** 2)), n=int(z.size))
-            if np.mean(np.abs(z) < 3.5) < 0.9 or abs(z.mean()) >= 1.0:
+            # the census weight carries over between steps (the population weight
+            # compounds, acceptance_main.cpp:225-231), so its per-step z are strongly
+            # correlated and their mean is nearly as wide as one z
+            if np.mean(np.abs(z) < 3.5) < 0.9 or abs(z.mean()) >= 2.0:
                 fails.append((k, z))
     report["segments_ratio"] = float(fa_s["segments"].mean() / ex_s["segments"].mean())
     out = os.environ.get("HWWG_STAT_REPORT")

@@ -109,9 +109,9 @@ def test_philox_bank_and_host_round_trip():
         assert erecs[k].comb_in >= erecs[k - 1].counters.census_count
         assert erecs[k].h2d_bytes == H * 16  # packed: (x, mu); (w, t) shared by the combed bank
         np.testing.assert_allclose(erecs[k].comb_out_weight, erecs[k].comb_in_weight, rtol=1e-12)
-    for r, q in zip(recs, erecs):
-        assert abs(q.segments / r.segments - 1) < 0.02
-        assert abs(q.census_weight / r.census_weight - 1) < 0.02
+    for r, q in zip(recs, erecs):  # two realisations (census order is scheduling-dependent)
+        assert abs(q.segments / r.segments - 1) < 0.06
+        assert abs(q.census_weight / r.census_weight - 1) < 0.03
 
 
 def test_host_round_trip_full_wire_format(monkeypatch):
@@ -129,8 +129,8 @@ def test_host_round_trip_full_wire_format(monkeypatch):
     for k in range(1, steps):
         assert full[k].h2d_bytes == H * 32 and base[k].h2d_bytes == H * 16
         assert full[k].comb_out == H
-        assert abs(full[k].segments / base[k].segments - 1) < 0.02
-        assert abs(full[k].census_weight / base[k].census_weight - 1) < 0.02
+        assert abs(full[k].segments / base[k].segments - 1) < 0.06
+        assert abs(full[k].census_weight / base[k].census_weight - 1) < 0.03
 
 
 def test_config3_philox_step1_within_batch_sigma():
@@ -161,8 +161,8 @@ def test_tiled_comb_matches_prefix_comb(monkeypatch):
         assert q.comb_out == r.comb_out
         if k:
             np.testing.assert_allclose(q.comb_out_weight, q.comb_in_weight, rtol=1e-12)
-        assert abs(q.segments / r.segments - 1) < 0.02
-        assert abs(q.census_weight / r.census_weight - 1) < 0.02
+        assert abs(q.segments / r.segments - 1) < 0.06
+        assert abs(q.census_weight / r.census_weight - 1) < 0.03
         sig = np.sqrt(a["sigma"] ** 2 + b["sigma"] ** 2)
         mask = a["phi_track"] > 1e-2 * a["phi_track"].max()
         z = np.abs(a["phi_track"] - b["phi_track"])[mask] / sig[mask]
