@@ -142,14 +142,7 @@ struct hwwg_driver {
   // events between its segment kernels cost 4% (HWWG_SEG_EVENTS=1 restores them)
   int seg_events = 1;
   DevBuf<unsigned long long> span;  // 2 words per segment
-  unsigned fix_budget = kFastFixBudget;  // HWWG_FAST_FIX_BUDGET (tests: exercise the overflow path)
-  // transport events per history of the last completed step (segments per
-  // history; 100 before any: config 2's cold start runs 73), to predict
-  // whether a launch stays inside the fixed-point tallies' per-block budget
-  double events_per_history = 100.0;
-  bool events_measured = false;
   double step_wref = 1.0;
-  int comb_tiled = 0; // HWWG_COMB_TILED=1: integer-tile comb for every bank (tests)
   // config-3 volumetric source: the step's LOSM q (device) and particle staging
   // q of every step the box overlaps, precomputed at creation (q_row[step]:
   // row of q_all, -1 when the step sees no emission)
@@ -421,10 +414,13 @@ void init_driver(hwwg_driver* d) {
     d->fcensus.reserve(d->census_hwm);
     d->fbank.reserve(d->census_hwm);
     d->fsrc.reserve(std::max<uint64_t>(d->target + (c.vol_rate > 0.0 ? c.vol_histories : 0), 1));
-    // an n-sized fp64 prefix for banks up to the creation-time census mark;
-    // larger banks (single GPU) comb through integer tiles without one
-    d->comb_mem.reserve(4 + d->census_hwm);
-    d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
+    // comb scratch: O(n / 4096) words (single GPU); the multi-GPU local scan
+    // keeps an n-sized prefix, sized per step
+    d->comb_mem.reserve(4 + fast_comb_scratch_words(d->census_hwm));
+    if (d->world > 1) {
+      d->comb_temp.reserve(fast_comb_temp_bytes(d->census_hwm));
+      d->comb_mem.reserve(4 + d->census_hwm);
+    }
     if (c.host_bank) d->bank.reserve(d->census_hwm);
     if (d->world > 1) {
       d->nccl_buf.reserve(std::max<size_t>(4 * (size_t)d->world + 16, (size_t)I + 8));
@@ -867,13 +863,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     d->fsrc.reserve(d->target + vol_cap);
-    const bool tiled = d->comb_tiled || d->bank_n > d->census_floor;
-    if (!tiled) {
-      d->comb_mem.reserve(4 + d->bank_n);
-      d->comb_temp.reserve(fast_comb_temp_bytes(d->bank_n));
-    } else {
-      d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
-    }
+    d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
     FastCombArgs a{};
     a.bank = d->fbank.view();
     a.n = d->bank_n;
@@ -887,9 +877,16 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.out = d->fsrc.view();
     // after the cold start, tooth k becomes history perm(k) (see Perm)
     if (step > 1) a.perm = make_perm(d->target, c.seed, step);
+    // the integer scale from the bank's weight: the previous step's census
+    // weight tallies (still in the slab), or the pulse source's strength
+    if (d->has_prev_report) {
+      a.hint_batches = d->tal.p.census_weight_batch;
+      a.hint_n = B;
+    } else {
+      a.hint_host = c.strength * (double)c.histories_per_step;
+    }
     d->ph_mark("comb", s);
-    if (tiled) launch_fast_comb_tiled(a, s);
-    else launch_fast_comb(a, s);
+    launch_fast_comb(a, s);
     d->ph_mark("-", s);
     d->launches += 3;
     H = d->target;
@@ -1153,18 +1150,22 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           const size_t fsm = fast_smem_fix_bytes(I, fa.nb) + fast_smem_centers_bytes(I);
           double vmax = 0.0;
           for (const CellInfo& ci : d->prob.cells_h) vmax = std::max(vmax, ci.speed * ci.inv_dx);
+          double vmin = vmax;
+          for (const CellInfo& ci : d->prob.cells_h) vmin = std::min(vmin, ci.speed * ci.inv_dx);
           const double w = std::max(c.rho, d->step_wref);
           int kt = 0, ke = 0;
           const int bps = fast_blocks_per_sm(fsm);
-          // (a measured rate varies step to step: 30% margin; the cold-start
-          // prior is already generous)
-          const double margin = d->events_measured ? 1.3 : 1.0;
-          const double per_block = (double)fa.n_src * d->events_per_history * margin /
-                                   (double)std::max(1, d->sms * bps);
-          if (fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
-              bps >= fast_blocks_per_sm(smem) && per_block <= (double)kFastFixBudget) {
+          // dynamic range: the smallest census score (a weight near the lowest
+          // window floor eps_min / rho) must keep >= 2^20 grid units, or its
+          // rounding would bias low-window cells: beyond 20 binades below the
+          // largest expected score the fp64 slots are kept
+          const double smallest = c.mode != 0 ? c.eps_min / c.rho * vmin : w * vmin;
+          const bool range_ok = smallest > 0.0 &&
+                                std::ilogb(w * vmax) - std::ilogb(smallest) <= 20;
+          if (range_ok && fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
+              bps >= fast_blocks_per_sm(smem)) {
             fa.fix = 1;
-            fa.fix_budget = d->fix_budget;
+            fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             fa.fix_k_trk = kt;
             fa.fix_k_edge = ke;
             fa.aggregate = 0;
@@ -1421,13 +1422,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     // target particles instead of the raw census (x60 of H after step 1).
     // Enqueued after the record readbacks above, so they see this step's
     // comb scalars.
-    const bool tiled = d->comb_tiled || d->bank_n > d->census_floor;
-    if (!tiled) {
-      d->comb_mem.reserve(4 + d->bank_n);
-      d->comb_temp.reserve(fast_comb_temp_bytes(d->bank_n));
-    } else {
-      d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
-    }
+    d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
     FastCombArgs a{};
     a.temp = d->comb_temp.p;
     a.temp_bytes = d->comb_temp.n;
@@ -1440,9 +1435,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.scalars = d->comb_mem.p;
     a.out = d->fsrc.view();
     a.perm = make_perm(d->target, c.seed, step + 1);
+    a.hint_batches = d->tal.p.census_weight_batch;  // this step's census weight
+    a.hint_n = B;
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
-    if (tiled) launch_fast_comb_tiled(a, s);
-    else launch_fast_comb(a, s);
+    launch_fast_comb(a, s);
     d->launches += 3;
     d->pre_comb_in = d->bank_n;
     d->host_pre_combed = true;
@@ -1535,10 +1531,6 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   for (int i = 0; i < I; ++i) seg += d->h_tracks[i];
   rec->segments = seg;
   rec->histories = H;
-  if (H) {
-    d->events_per_history = (double)seg / (double)H;
-    d->events_measured = true;
-  }
   // banked particles (fast mode: the census slots also hold zero-weight chunk tails)
   rec->census_size = d->fast ? (uint64_t)u[kCensusCount] : count;
   rec->comb_in_weight = comb_sc[0];
@@ -1619,9 +1611,6 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
   d->seg_events = d->fast ? (std::getenv("HWWG_SEG_EVENTS") ? 1 : 0) : 1;
   d->span.reserve(64);
-  if (const char* m = std::getenv("HWWG_FAST_FIX_BUDGET"))
-    d->fix_budget = (unsigned)std::min<long>(std::max<long>(std::atol(m), 0), (long)kFastFixBudget);
-  if (const char* m = std::getenv("HWWG_COMB_TILED")) d->comb_tiled = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));
   d->world = d->opt.world > 1 ? d->opt.world : 1;
   d->rank = d->world > 1 ? d->opt.rank : 0;
@@ -1641,10 +1630,10 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   // history ids are 32-bit and the batch of history h is one fp64 division
   // (exact while h * batches < 2^53)
   const uint64_t tgt = cfg->target_population ? cfg->target_population : cfg->histories_per_step;
-  if (d->fast && (tgt >= (1ULL << 32) - (1ULL << 26) || cfg->batches > (1 << 20))) {
+  if (d->fast && (tgt >= (1ULL << 32) - (1ULL << 26) || cfg->batches >= (1 << 16))) {
     delete d;
     return fail(HWWG_EINVAL, "philox mode: histories per step must stay below 2^32 - 2^26 "
-                             "and batches below 2^20");
+                             "and batches below 2^16");
   }
   try {
     init_driver(d);

@@ -68,11 +68,11 @@ struct FastArgs {
   int b_lo, nb;  // batches touched by this segment: [b_lo, b_lo + nb)
   int smem_tallies;  // 0 global REDs, 1 shared-memory tallies, 2 fp64 global + counts shared
   int aggregate;     // 1: warp-aggregate tally atomics (cold start: lanes share cells)
+  int census_runs;   // fixed-point slots: 1 run-aggregates census scores (cold start)
   int scramble;      // 1: claim source particles in bit-reversed order within 1024-blocks
   // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
   // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
   int fix, fix_k_trk, fix_k_edge;
-  unsigned fix_budget;  // events per block with limb adds (<= kFastFixBudget)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   int pdl;              // 1: programmatic dependent launch after the previous kernel
   // [first block start, last block end] (globaltimer ns) of this launch, reset
@@ -139,7 +139,6 @@ constexpr int kFastHistWords = 8 * 120 * 2;
 size_t fast_smem_bytes(int I, int nb);
 size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
 size_t fast_smem_fix_bytes(int I, int nb);  // smem_tallies == 1 with fixed-point track/edge slots
-constexpr unsigned kFastFixBudget = 65535;  // transport events per block with fixed-point adds
 bool fast_fix_exponent(double vmax, int* k);  // grid exponent for the largest expected score
 size_t fast_smem_centers_bytes(int I);  // window centres (after the tallies)
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);
@@ -163,9 +162,18 @@ void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, 
 // nt == 0: identity.
 struct Perm {
   unsigned long long nt, a, b;
+  unsigned long long m;  // floor(2^64 / nt): Barrett reduction (no 64-bit division call)
   __host__ __device__ unsigned long long operator()(unsigned long long k) const {
     const unsigned long long t = k >> 5;
-    return t < nt ? (((a * t + b) % nt) << 5) | (k & 31ULL) : k;
+    if (t >= nt) return k;
+    const unsigned long long x = a * t + b;  // < 2^64 (a, b < nt < 2^27, t < nt)
+#if defined(__CUDA_ARCH__)
+    unsigned long long r = x - __umul64hi(x, m) * nt;
+    if (r >= nt) r -= nt;
+#else
+    const unsigned long long r = x % nt;
+#endif
+    return (r << 5) | (k & 31ULL);
   }
 };
 Perm make_perm(uint64_t n, uint64_t seed, uint64_t step);
@@ -181,14 +189,18 @@ struct FastCombArgs {
   void* temp;
   size_t temp_bytes;
   Perm perm;  // tooth k is written at perm(k), as history perm(k) (n == 0: identity)
+  // a bound-grade estimate of the bank's total weight (hint_host plus the
+  // hint_n device doubles at hint_batches: the step's census weight per
+  // batch), which fixes the comb's integer scale before it reads the bank
+  const double* hint_batches;
+  int hint_n;
+  double hint_host;
 };
 size_t fast_comb_temp_bytes(uint64_t n);
+// Single-GPU comb of a bank of any size: `prefix` is fast_comb_scratch_words(n)
+// words of scratch, `temp` unused.
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s);
-// The same comb without an n-sized prefix (integer tiles): `prefix` is
-// fast_comb_scratch_words(n) words of scratch, `temp` unused. For banks larger
-// than the preallocated prefix (the config-4 cold-start census).
 size_t fast_comb_scratch_words(uint64_t n);
-void launch_fast_comb_tiled(const FastCombArgs& a, cudaStream_t s);
 // Multi-GPU comb pieces: local inclusive scan (scalars[0] = local total, 0 for
 // an empty bank), and teeth [k_lo, k_hi) placed against origin + local prefix.
 void launch_fast_comb_local_scan(const FastCombArgs& a, cudaStream_t s);

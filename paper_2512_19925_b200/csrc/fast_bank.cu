@@ -3,11 +3,11 @@
 //
 // The comb keeps the reference's estimator — teeth spaced W/target apart with
 // one random offset walk the cumulative-weight axis of the bank — but the
-// cumulative weights come from a parallel scan (CUB fp64 scan into an n-sized
-// prefix; exact fixed-point integers in tiles, with O(n/2048) scratch, for
-// banks beyond the preallocated prefix) instead of a serial walk, and each
-// particle writes the teeth that fall in its cumulative-weight interval.
-// Teeth land in bank order.
+// cumulative weights are exact fixed-point integers summed in tiles (two
+// passes, O(n/4096) scratch) instead of a serial fp64 walk, and each particle
+// writes the teeth that fall in its cumulative-weight interval. Tooth k lands
+// at perm(k) (fast.cuh Perm). The multi-GPU pieces (a local CUB scan, teeth
+// placed by binary search against a global origin) are at the end.
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
@@ -24,22 +24,6 @@ __global__ void k_extract_w(FastBank b, uint64_t n, double* w) {
   if (i < n) w[i] = b.wt[i].x;
 }
 
-// Particle-parallel teeth: particle i owns the teeth k with
-// prefix[i-1] <= T_k < prefix[i], T_k = offset + k * spacing — exactly the
-// teeth whose first index with T_k < prefix[idx] is i (the search definition),
-// since cnt(v) = #{k : T_k < v} is evaluated with the same fp64 T_k on both
-// sides of every boundary. Reads and writes are coalesced and there is no
-// search; teeth stranded past the total by round-off go to the last particle
-// with weight (popctrl.cpp:31-37).
-__device__ __forceinline__ uint64_t teeth_below(double v, double offset, double spacing,
-                                                uint64_t target) {
-  double e = ceil((v - offset) / spacing);
-  uint64_t k = e <= 0.0 ? 0 : (e >= (double)target ? target : (uint64_t)e);
-  while (k > 0 && !(offset + (double)(k - 1) * spacing < v)) --k;
-  while (k < target && offset + (double)k * spacing < v) ++k;
-  return k;
-}
-
 __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src, uint64_t k0,
                                             uint64_t k1, double spacing) {
   const double2 xm = a.bank.xm[src];
@@ -54,61 +38,25 @@ __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src,
   }
 }
 
-// popctrl.cpp:15-20 comb scalars (W, spacing, the offset drawn from the
-// step's comb stream, the output weight), formed by every block from the
-// scan's last prefix (the same values everywhere); block 0 records them.
-__device__ __forceinline__ void comb_scalars(const FastCombArgs& a, double& spacing,
-                                             double& offset) {
-  __shared__ double sc[2];
-  if (threadIdx.x == 0) {
-    const double W = a.prefix[a.n - 1];
-    const double sp = W / (double)a.target;
-    Xoshiro r;
-    r.seed(a.seed, a.stream);
-    const double off = r.uniform() * sp;
-    sc[0] = sp;
-    sc[1] = off;
-    if (blockIdx.x == 0) {
-      a.scalars[0] = W;
-      a.scalars[1] = sp;
-      a.scalars[2] = off;
-      a.scalars[3] = sp * (double)a.target;
-    }
-  }
-  __syncthreads();
-  spacing = sc[0];
-  offset = sc[1];
-}
-
-__global__ void k_comb_scatter(FastCombArgs a) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double spacing, offset;
-  comb_scalars(a, spacing, offset);
-  if (i >= a.n) return;
-  const uint64_t k0 = i ? teeth_below(a.prefix[i - 1], offset, spacing, a.target) : 0;
-  const uint64_t k1 = teeth_below(a.prefix[i], offset, spacing, a.target);
-  if (k0 < k1) write_teeth(a, i, k0, k1, spacing);
-  if (i == a.n - 1 && k1 < a.target) {  // stranded teeth
-    uint64_t s = i;
-    while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
-    write_teeth(a, s, k1, a.target, spacing);
-  }
-}
-
-// ---- single-GPU comb without an n-sized prefix (memory-wall banks) ---------
+// ---- single-GPU comb: two passes over the bank in 4096-particle tiles ------
 // The cumulative weights are exact integers: every weight becomes
-// floor(w * 2^k) (k chosen so the bank total stays below 2^62), tiles of 2048
-// sum and scan in uint64, so prefixes are associative, monotone and identical
-// on both sides of every tile boundary — each particle recomputes its own
-// prefix in its tile's block scan and writes its teeth. Scratch is O(n/2048)
-// words instead of 8 B per census slot (the step-1 census of config 4 is 1.9e9
-// particles). Quantisation moves a tooth boundary by < n * 2^-62 of the total.
-constexpr int kFcThreads = 256, kFcItems = 8, kFcTile = kFcThreads * kFcItems;
+// floor(w * 2^s), with 2^s chosen from a bound on the bank total known before
+// the comb (the step's census-weight tallies, or the pulse strength) so the
+// total stays below 2^61. Integer tile sums are associative, so tile starts are
+// exact and both sides of every tile boundary see the same prefix; each tile
+// then recomputes its particles' prefixes in a block scan and every particle
+// writes the teeth in its cumulative-weight interval (particle j owns teeth
+// [cnt(P_{j-1}), cnt(P_j)), cnt(v) = #{k : T_k < v}, T_k = offset + k *
+// spacing: monotone in v and evaluated identically on both sides of every
+// boundary, so the teeth partition [0, target)). Two reads of the weights,
+// O(n / 4096) scratch, no n-sized prefix. Quantisation moves a tooth
+// boundary by < n * 2^-60 of the total.
+constexpr int kCbThreads = 256, kCbItems = 16, kCbTile = kCbThreads * kCbItems;
 
-// scratch layout (8-byte words): [0] scale, [1] integer total, [2] spacing in
-// integer units, [3] offset in integer units, [4] done-block counter, then tile
-// sums (fp64) [nt], tile integer sums [nt], tile integer starts [nt]
-struct FcScratch {
+// scratch (8-byte words of FastCombArgs::prefix): [0] scale, [1] integer
+// total, [2] spacing and [3] offset in integer units, [4] done-block counter,
+// then tile sums [nt] and tile starts [nt] (uint64)
+struct CbScratch {
   double* base;
   uint64_t nt;
   __device__ double& scale() const { return base[0]; }
@@ -116,10 +64,9 @@ struct FcScratch {
   __device__ double& spacing_i() const { return base[2]; }
   __device__ double& offset_i() const { return base[3]; }
   __device__ unsigned* done() const { return reinterpret_cast<unsigned*>(base + 4); }
-  __device__ double* fsum() const { return base + 5; }
-  __device__ unsigned long long* isum() const { return reinterpret_cast<unsigned long long*>(base + 5 + nt); }
-  __device__ unsigned long long* istart() const {
-    return reinterpret_cast<unsigned long long*>(base + 5 + 2 * nt);
+  __device__ unsigned long long* tsum() const { return reinterpret_cast<unsigned long long*>(base + 8); }
+  __device__ unsigned long long* tstart() const {
+    return reinterpret_cast<unsigned long long*>(base + 8 + nt);
   }
 };
 
@@ -127,8 +74,7 @@ __device__ __forceinline__ unsigned long long fixed_w(double w, double scale) {
   return w > 0.0 ? (unsigned long long)(w * scale) : 0ULL;  // truncation: monotone
 }
 
-// Block (kFcThreads) exclusive scan of one value per thread; returns the
-// thread's exclusive prefix, `total` the block sum (all threads).
+// Block (kCbThreads) exclusive scan of one value per thread; `total` = block sum.
 template <class T>
 __device__ __forceinline__ T block_exclusive_256(T v, T* red, T& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -143,7 +89,7 @@ __device__ __forceinline__ T block_exclusive_256(T v, T* red, T& total) {
   __syncthreads();
   T before = 0, all = 0;
 #pragma unroll
-  for (int w = 0; w < kFcThreads / 32; ++w) {
+  for (int w = 0; w < kCbThreads / 32; ++w) {
     if (w < wid) before += red[w];
     all += red[w];
   }
@@ -165,117 +111,110 @@ __device__ __forceinline__ bool last_block(unsigned* done) {
   return last;
 }
 
-// pass 1 (kInteger = false): fp64 tile sums, then the last block derives the
-// fixed-point scale from their total; pass 2: integer tile sums, then the last
-// block scans them into tile starts and writes the comb scalars.
-template <bool kInteger>
-__global__ void __launch_bounds__(kFcThreads) k_fc_tile_sums(FastCombArgs a) {
-  __shared__ double fred[kFcThreads / 32];
-  __shared__ unsigned long long ired[kFcThreads / 32];
-  const FcScratch S{a.prefix, (a.n + kFcTile - 1) / kFcTile};
-  const uint64_t k0 = (uint64_t)blockIdx.x * kFcTile;
-  const double scale = kInteger ? S.scale() : 0.0;
-  double f = 0.0;
+// 2^s with W * (1 + 2^-10) < 2^(61 - s): the integer total stays below 2^61
+__device__ __forceinline__ double comb_scale(const FastCombArgs& a) {
+  double W = a.hint_host;
+  for (int b = 0; b < a.hint_n; ++b) W += a.hint_batches[b];
+  int e = 0;
+  frexp(W > 0.0 ? W * (1.0 + 0x1p-10) : 1.0, &e);
+  return ldexp(1.0, 61 - e);
+}
+
+// pass 1: integer tile sums; the last block scans them into tile starts and
+// forms the comb scalars (popctrl.cpp:15-20: spacing W/target, one offset
+// from the step's comb stream)
+__global__ void __launch_bounds__(kCbThreads) k_cb_sums(FastCombArgs a) {
+  __shared__ unsigned long long red[kCbThreads / 32];
+  const CbScratch S{a.prefix, (a.n + kCbTile - 1) / kCbTile};
+  const double scale = comb_scale(a);
+  const uint64_t t0 = (uint64_t)blockIdx.x * kCbTile;
   unsigned long long q = 0;
-  for (int j = threadIdx.x; j < kFcTile; j += kFcThreads) {
-    const uint64_t k = k0 + j;
-    if (k < a.n) {
-      const double w = a.bank.wt[k].x;
-      if (kInteger) q += fixed_w(w, scale);
-      else f += w > 0.0 ? w : 0.0;
-    }
-  }
-  if (kInteger) {
-    unsigned long long t;
-    block_exclusive_256(q, ired, t);
-    if (threadIdx.x == 0) S.isum()[blockIdx.x] = t;
-  } else {
-    double t;
-    block_exclusive_256(f, fred, t);
-    if (threadIdx.x == 0) S.fsum()[blockIdx.x] = t;
-  }
+#pragma unroll 4
+  for (int j = threadIdx.x; j < kCbTile; j += kCbThreads)
+    if (t0 + j < a.n) q += fixed_w(a.bank.wt[t0 + j].x, scale);
+  unsigned long long t;
+  block_exclusive_256(q, red, t);
+  if (threadIdx.x == 0) S.tsum()[blockIdx.x] = t;
   if (!last_block(S.done())) return;
-  // the last block: every tile sum is visible (fence + counter)
-  const uint64_t per = (S.nt + kFcThreads - 1) / kFcThreads;
+  const uint64_t per = (S.nt + kCbThreads - 1) / kCbThreads;
   const uint64_t lo = threadIdx.x * per < S.nt ? threadIdx.x * per : S.nt;
   const uint64_t hi = lo + per < S.nt ? lo + per : S.nt;
-  if (!kInteger) {
-    double v = 0.0;
-    for (uint64_t t = lo; t < hi; ++t) v += S.fsum()[t];
-    double W;
-    block_exclusive_256(v, fred, W);
-    if (threadIdx.x == 0) {
-      // total * scale < 2^62 with room for the fp64 sum's own rounding
-      int e = 0;
-      frexp(W > 0.0 ? W * (1.0 + 0x1p-20) : 1.0, &e);
-      S.scale() = ldexp(1.0, 62 - e);
-      a.scalars[0] = W;
-    }
-    return;
-  }
   unsigned long long v = 0;
-  for (uint64_t t = lo; t < hi; ++t) v += S.isum()[t];
-  unsigned long long r_total;
-  unsigned long long r = block_exclusive_256(v, ired, r_total);
-  for (uint64_t t = lo; t < hi; ++t) {
-    S.istart()[t] = r;
-    r += S.isum()[t];
+  for (uint64_t i = lo; i < hi; ++i) v += S.tsum()[i];
+  unsigned long long total;
+  unsigned long long r = block_exclusive_256(v, red, total);
+  for (uint64_t i = lo; i < hi; ++i) {
+    S.tstart()[i] = r;
+    r += S.tsum()[i];
   }
   if (threadIdx.x == 0) {
-    S.total() = r_total;
-    const double W = a.scalars[0];
+    S.scale() = scale;
+    S.total() = total;
+    const double W = (double)total / scale;
     const double spacing = W / (double)a.target;
     Xoshiro rng;
     rng.seed(a.seed, a.stream);
     const double u = rng.uniform();
+    a.scalars[0] = W;
     a.scalars[1] = spacing;
     a.scalars[2] = u * spacing;
     a.scalars[3] = spacing * (double)a.target;
-    const double sp_i = (double)r_total / (double)a.target;
+    const double sp_i = (double)total / (double)a.target;
     S.spacing_i() = sp_i;
     S.offset_i() = u * sp_i;
   }
 }
 
-// Per tile: weights staged through shared memory, exact integer prefixes by a
-// block scan (blocked order), then the teeth written particle-parallel in
-// striped order so consecutive lanes write consecutive teeth.
-__global__ void __launch_bounds__(kFcThreads) k_fc_scatter(FastCombArgs a) {
-  __shared__ double wv[kFcTile];
-  __shared__ unsigned long long P[kFcTile];
-  __shared__ unsigned long long red[kFcThreads / 32];
-  const FcScratch S{a.prefix, (a.n + kFcTile - 1) / kFcTile};
-  const double scale = S.scale(), sp_i = S.spacing_i(), off_i = S.offset_i();
+// #{k : offset + k * spacing < v} (as ceil((v - offset) / spacing), the
+// division by a multiplication with the reciprocal: a monotone function of v,
+// evaluated identically on both sides of every particle boundary), clamped to
+// [0, target]. (A division per boundary ran fp64 division's slow path.)
+__device__ __forceinline__ uint64_t teeth_below_i(double v, double off, double inv_sp,
+                                                  uint64_t target) {
+  if (!(v > off)) return 0;
+  const double e = ceil((v - off) * inv_sp);
+  return e >= (double)target ? target : (uint64_t)e;
+}
+
+// pass 2: per tile, weights staged through shared memory, integer prefixes by
+// a block scan (blocked order: thread i owns particles 16i .. 16i+15), teeth
+// written per particle
+__global__ void __launch_bounds__(kCbThreads) k_cb_scatter(FastCombArgs a) {
+  __shared__ double wv[kCbTile];
+  __shared__ unsigned long long red[kCbThreads / 32];
+  const CbScratch S{a.prefix, (a.n + kCbTile - 1) / kCbTile};
+  const double scale = S.scale(), inv_sp = 1.0 / S.spacing_i(), off_i = S.offset_i();
   const double spacing = a.scalars[1];
-  const uint64_t t0 = (uint64_t)blockIdx.x * kFcTile;
-  const int m = a.n - t0 < (uint64_t)kFcTile ? (int)(a.n - t0) : kFcTile;
-  for (int j = threadIdx.x; j < kFcTile; j += kFcThreads) wv[j] = j < m ? a.bank.wt[t0 + j].x : 0.0;
+  const uint64_t t0 = (uint64_t)blockIdx.x * kCbTile;
+  const int m = a.n - t0 < (uint64_t)kCbTile ? (int)(a.n - t0) : kCbTile;
+  for (int j = threadIdx.x; j < kCbTile; j += kCbThreads) wv[j] = j < m ? a.bank.wt[t0 + j].x : 0.0;
   __syncthreads();
-  unsigned long long q[kFcItems];
+  unsigned long long q[kCbItems];
   unsigned long long mine = 0;
 #pragma unroll
-  for (int i = 0; i < kFcItems; ++i) {
-    q[i] = fixed_w(wv[threadIdx.x * kFcItems + i], scale);
+  for (int i = 0; i < kCbItems; ++i) {
+    q[i] = fixed_w(wv[threadIdx.x * kCbItems + i], scale);
     mine += q[i];
   }
   unsigned long long tot;
-  unsigned long long run = S.istart()[blockIdx.x] + block_exclusive_256(mine, red, tot);
+  unsigned long long run = S.tstart()[blockIdx.x] + block_exclusive_256(mine, red, tot);
+  uint64_t k_lo = teeth_below_i((double)run, off_i, inv_sp, a.target);
 #pragma unroll
-  for (int i = 0; i < kFcItems; ++i) {
+  for (int i = 0; i < kCbItems; ++i) {
     run += q[i];
-    P[threadIdx.x * kFcItems + i] = run;  // inclusive
+    const int j = threadIdx.x * kCbItems + i;
+    const uint64_t k_hi = teeth_below_i((double)run, off_i, inv_sp, a.target);
+    if (k_lo < k_hi && j < m) write_teeth(a, t0 + j, k_lo, k_hi, spacing);
+    k_lo = k_hi;
   }
-  __syncthreads();
-  const unsigned long long start = S.istart()[blockIdx.x];
-  for (int j = threadIdx.x; j < m; j += kFcThreads) {
-    const uint64_t k = t0 + j;
-    const uint64_t lo = teeth_below((double)(j ? P[j - 1] : start), off_i, sp_i, a.target);
-    const uint64_t hi = teeth_below((double)P[j], off_i, sp_i, a.target);
-    if (lo < hi) write_teeth(a, k, lo, hi, spacing);
-    if (k == a.n - 1 && hi < a.target) {  // stranded teeth (popctrl.cpp:31-37)
-      uint64_t src = k;
+  // teeth stranded past the integer total by round-off go to the last particle
+  // with weight (popctrl.cpp:31-37)
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kCbThreads - 1) {
+    const uint64_t k_end = teeth_below_i((double)S.total(), off_i, inv_sp, a.target);
+    if (k_end < a.target) {
+      uint64_t src = a.n - 1;
       while (src > 0 && !(fixed_w(a.bank.wt[src].x, scale) > 0)) --src;
-      write_teeth(a, src, hi, a.target, spacing);
+      write_teeth(a, src, k_end, a.target, spacing);
     }
   }
 }
@@ -478,23 +417,13 @@ size_t fast_comb_temp_bytes(uint64_t n) {
   return bytes > b2 ? bytes : b2;
 }
 
-size_t fast_comb_scratch_words(uint64_t n) { return 5 + 3 * ((n + kFcTile - 1) / kFcTile) + 4; }
+size_t fast_comb_scratch_words(uint64_t n) { return 8 + 2 * ((n + kCbTile - 1) / kCbTile) + 8; }
 
 void launch_fast_comb(const FastCombArgs& a, cudaStream_t s) {
-  // inclusive fp64 scan of the weights straight from the SoA bank (n-sized prefix)
-  size_t bytes = a.temp_bytes;
-  HWWG_CUDA(cub::DeviceScan::InclusiveSum(a.temp, bytes, WeightIt(a.bank.wt, WeightOf()), a.prefix,
-                                          (int)a.n, s));
-  k_comb_scatter<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
-  HWWG_CUDA(cudaGetLastError());
-}
-
-void launch_fast_comb_tiled(const FastCombArgs& a, cudaStream_t s) {
-  const unsigned nt = (unsigned)((a.n + kFcTile - 1) / kFcTile);
+  const unsigned nt = (unsigned)((a.n + kCbTile - 1) / kCbTile);
   HWWG_CUDA(cudaMemsetAsync(a.prefix + 4, 0, sizeof(double), s));  // done-block counter
-  k_fc_tile_sums<false><<<nt, kFcThreads, 0, s>>>(a);  // + the scale (last block)
-  k_fc_tile_sums<true><<<nt, kFcThreads, 0, s>>>(a);   // + tile starts, scalars
-  k_fc_scatter<<<nt, kFcThreads, 0, s>>>(a);
+  k_cb_sums<<<nt, kCbThreads, 0, s>>>(a);  // + tile starts, scalars (last block)
+  k_cb_scatter<<<nt, kCbThreads, 0, s>>>(a);
   HWWG_CUDA(cudaGetLastError());
 }
 
@@ -536,7 +465,7 @@ static uint64_t gcd_u64(uint64_t a, uint64_t b) {
 
 Perm make_perm(uint64_t n, uint64_t seed, uint64_t step) {
   const uint64_t nt = n >> 5;  // whole 32-element tiles
-  if (nt < 3) return Perm{0, 0, 0};
+  if (nt < 3) return Perm{0, 0, 0, 0};
   uint64_t a = (uint64_t)((double)nt * 0.6180339887498949);
   if (a < 1) a = 1;
   while (gcd_u64(a, nt) != 1) ++a;  // a few steps at most (coprimes are dense)
@@ -544,7 +473,8 @@ Perm make_perm(uint64_t n, uint64_t seed, uint64_t step) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   z ^= z >> 31;
-  return Perm{nt, a % nt, z % nt};
+  const unsigned long long m = (unsigned long long)(((unsigned __int128)1 << 64) / nt);
+  return Perm{nt, a % nt, z % nt, m};
 }
 
 void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,

@@ -28,10 +28,13 @@
 //
 // Tallies: block-private shared-memory histograms over the segment's batch
 // range (track-length by batch and cell, census phi/J/F, edge currents,
-// per-cell track counts), flushed once per block with fp64 REDs; global REDs
-// when the histograms do not fit in shared memory (I = 4000). The cold-start
-// step warp-aggregates them (MATCH.ANY groups, REDUX fixed-point sums); census
-// scores are run-aggregated across the warp in every step.
+// per-cell track counts), flushed once per block with fp64 REDs. Where the
+// wider slots fit, track/edge/census scores are fixed-point integers added as
+// 16-bit limbs with native 32-bit shared atomics, kept from wrapping by a
+// rolling carry sweep (see fix_add / fix_sweep); otherwise fp64 slots (CAS
+// loops) with census scores run-aggregated across the warp, and global REDs
+// warp-aggregated (MATCH.ANY groups, REDUX fixed-point sums) when the
+// histograms do not fit in shared memory (I = 4000).
 #include <cmath>
 #include <vector>
 
@@ -112,7 +115,7 @@ constexpr int kSmemStack = HWWG_SMEM_STACK;  // split-stack records per warp kep
 #ifndef HWWG_KPIECE
 #define HWWG_KPIECE 32
 #endif
-constexpr unsigned kPiece = HWWG_KPIECE;  // smallest run piece handed to an idle warp  // split-stack records per warp kept in shared memory  // pending daughters above which a warp shares runs with idle warps
+constexpr unsigned kPiece = HWWG_KPIECE;  // smallest run piece handed to an idle warp
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -147,12 +150,15 @@ __device__ __forceinline__ int batch_fast(unsigned h, double H, int B) {
   return b < B ? b : B - 1;
 }
 
+// split records carry the parent's cell | batch slot << 16 (daughters keep the
+// history's batch: no per-daughter batch division)
 __device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigned j) {
   p.x = r.x;
   p.mu = r.mu;
   p.w = r.w;
   p.t = r.t;
-  p.cell = (int)r.cell;
+  p.cell = (int)(r.cell & 0xffffu);
+  p.bslot = (int)(r.cell >> 16);
   p.hist = r.hist;
   p.key = mix64(r.key ^ ((unsigned long long)r.ctr << 40) ^ ((unsigned long long)j << 8) ^
                 0x5bd1e995ULL);
@@ -234,6 +240,42 @@ __device__ __forceinline__ void agg_add3(double* b0, double* b1, double* b2, int
   }
 }
 
+// The census weight by batch (tally.hpp:65-72 census_weight_batch) of one
+// trip: runs of census lanes keyed by the batch slot alone — usually one run
+// per warp (all its census lanes hold histories of one batch), which takes a
+// plain butterfly sum and one add.
+__device__ __forceinline__ void census_weight_runs(double* cwb, bool c, int b, double v) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned cm = __ballot_sync(full, c);
+  if (!cm) return;
+  const int b0 = __shfl_sync(full, b, __ffs(cm) - 1);
+  if (!__any_sync(full, c && b != b0)) {
+    double w = c ? v : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(full, w, o);
+    if (lane == __ffs(cm) - 1) atomicAdd(cwb + b0, w);
+    return;
+  }
+  const unsigned below = cm & ((1u << lane) - 1u);
+  const int prev = below ? 31 - __clz(below) : lane;
+  const unsigned upto = (2u << lane) - 1u;
+  const int pb = __shfl_sync(full, b, prev);
+  const bool hb_head = c && (prev == lane || pb != b);
+  const unsigned bheads = __ballot_sync(full, hb_head);
+  const unsigned bhb = bheads & upto;
+  const int bstart = bhb ? 31 - __clz(bhb) : 0;
+  double w = c ? v : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(full, w, o);
+    if (lane - o >= bstart) w += t;
+  }
+  const unsigned above = cm & ~upto;
+  const int next = above ? __ffs(above) - 1 : -1;
+  if (c && (next < 0 || ((bheads >> next) & 1u))) atomicAdd(cwb + b, w);
+}
+
 // Census scores of one trip, summed over runs of census lanes with equal
 // (batch slot, cell) in lane order, then one set of adds per run. Split copies
 // that reach census without colliding are identical and were handed to
@@ -274,29 +316,7 @@ __device__ __forceinline__ void census_runs(AddCell add_cell, double* cwb, int c
   const unsigned above = cm & ~upto;  // census lanes after this one
   const int next = above ? __ffs(above) - 1 : -1;
   if (c && (next < 0 || ((heads >> next) & 1u))) add_cell(cell, s0, s1, s2);  // last lane of its run
-  // the census weight by batch: runs keyed by the batch slot alone (usually one
-  // run per warp: all its census lanes hold histories of one batch, which
-  // takes a plain butterfly sum)
-  const int b0 = __shfl_sync(full, b, __ffs(cm) - 1);
-  if (!__any_sync(full, c && b != b0)) {
-    double w = c ? v3 : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(full, w, o);
-    if (lane == __ffs(cm) - 1) atomicAdd(cwb + b0, w);
-    return;
-  }
-  const int pb = __shfl_sync(full, b, prev);
-  const bool hb_head = c && (prev == lane || pb != b);
-  const unsigned bheads = __ballot_sync(full, hb_head);
-  const unsigned bhb = bheads & upto;
-  const int bstart = bhb ? 31 - __clz(bhb) : 0;
-  double w = c ? v3 : 0.0;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double t = __shfl_up_sync(full, w, o);
-    if (lane - o >= bstart) w += t;
-  }
-  if (c && (next < 0 || ((bheads >> next) & 1u))) atomicAdd(cwb + b, w);
+  census_weight_runs(cwb, c, b, v3);
 }
 
 // track-length score (keyed by batch slot and cell) plus the per-cell count
@@ -322,21 +342,25 @@ __device__ __forceinline__ void agg_add_count_global(double* base, unsigned long
   agg_add_count_t<unsigned long long>(base, cnt, key, v, cell);
 }
 
-// Fixed-point track, edge and census phi/J/F tallies (kFix). Shared-memory fp64 adds are CAS
-// loops on sm_100 (ATOMS.CAST.SPIN.64: load, add, compare-and-swap, retry) and
-// sat on every event's dependency chain; 32-bit integer ATOMS.ADD is native
-// and needs no reply. A score v is put on the launch's grid 2^-k (k chosen on
-// the host so the largest expected score is ~2^40 grid units: see
-// fast_fix_exponent) as a 64-bit integer q and added as four 16-bit limbs
-// into four 32-bit words of its slot: independent, fire-and-forget adds.
-// A word takes at most 2^16 adds before it could wrap, so the block reserves
-// its events against a 65535-event budget (s_fixbudget) and a warp past it,
-// or a score beyond 2^62 grid units (and NaN), goes to the global fp64 tally
-// with a native RED instead. The flush recombines the limbs exactly into one
-// fp64 value per slot (three roundings), so a tally carries the fp64 sum of
-// the quantised scores: 2^-40 of the expected largest score, ~1e-12 relative.
-constexpr unsigned kFixBudget = kFastFixBudget;  // events per block with fixed-point adds
-constexpr unsigned kFixChunk = 256;     // budget a warp reserves at a time
+// Fixed-point track, edge and census phi/J/F tallies (kFix). Shared-memory fp64
+// adds are CAS loops on sm_100 (ATOMS.CAST.SPIN.64: load, add, compare-and-swap,
+// retry) and sat on every event's dependency chain; 32-bit integer ATOMS.ADD is
+// native and needs no reply. A score v is put on the launch's grid 2^-k (k
+// chosen on the host so the largest expected score is ~2^40 grid units: see
+// fast_fix_exponent) as a 64-bit integer q and added as four 16-bit limbs into
+// the four 32-bit words of its slot: independent, fire-and-forget adds. A limb
+// word would wrap after 2^16 adds; instead of capping the adds, every warp
+// sweeps the next 32 slots of a block-shared cursor every 8 loop trips and
+// moves each low word's carry (its high half) into the next word with two
+// atomics (fix_sweep: the slot's value is unchanged, concurrent adds are not
+// lost). Each sweep takes ceil(slots / 4096) slots per lane, so a slot is
+// swept at least once per 8 x 4096 / 32 = 1024 warp trips of the block, i.e.
+// before 2^15 lane adds: a word stays below 2^16 + 2^15 x 2^16 < 2^32. A score beyond 2^62 grid units (and NaN)
+// goes to the global tally with a native fp64 RED. The flush recombines the
+// limbs exactly into one fp64 value per slot (three roundings), so a tally
+// carries the fp64 sum of the quantised scores: 2^-40 of the expected largest
+// score, ~1e-12 relative.
+constexpr unsigned kSweepEvery = 8;  // warp loop trips between carry sweeps
 
 __device__ __forceinline__ double pow2(int k) {  // 2^k, |k| <= 1022
   return __hiloint2double((k + 1023) << 20, 0);
@@ -352,6 +376,19 @@ __device__ __forceinline__ bool fix_add(double* slot, double v, double scale) {
   atomicAdd(w + 2, (unsigned)(q >> 32) & 0xffffu);
   atomicAdd(w + 3, (unsigned)(q >> 48));  // signed top limb, two's complement
   return true;
+}
+
+// Carry of one slot's low words into the next word (slot: 4 limb words).
+__device__ __forceinline__ void fix_sweep_slot(unsigned* w) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const unsigned v = *(volatile unsigned*)(w + i);
+    const unsigned c = v >> 16;
+    if (c) {
+      atomicSub(w + i, c << 16);
+      atomicAdd(w + i + 1, c);
+    }
+  }
 }
 
 __device__ __forceinline__ double fix_value(const double* slot, double inv_scale) {
@@ -425,10 +462,13 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           : (sh ? (size_t)(I + 1) / 2 : 0);
   const double fix_trk = kFix ? pow2(a.fix_k_trk) : 0.0;
   const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
-  __shared__ unsigned s_fixbudget;  // kFix: events reserved against kFixBudget
-  bool fix_ok = kFix;               // warp-uniform: this warp still adds limbs
-  unsigned fix_left = 0;            // events of this warp's current budget reservation
-  if (kFix && threadIdx.x == 0) s_fixbudget = 0u;
+  __shared__ unsigned s_sweep;  // kFix: the carry sweep's slot cursor
+  // kFix: the fixed-point slots, contiguous from S.trk (track nb*I, census
+  // phi/J/F 3*I, edges I+1)
+  const unsigned fix_slots = (unsigned)(a.nb * I + 4 * I + 1);
+  // slots per lane per sweep: every slot is swept within 4096 / 32 sweeps
+  const unsigned fix_spl = (fix_slots + 4095u) / 4096u;
+  if (kFix && threadIdx.x == 0) s_sweep = 0u;
   for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
   double* s_cent = smem + tally_words;  // read at every window site: keep it on chip
   if (windows)
@@ -570,7 +610,6 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       const unsigned rank = __popc(need & lt);
       if (!p.alive && rank < take) {
         load_rec(p, r, r.base + cnt - rank);
-        p.bslot = batch_fast(p.hist, Hd, a.B) - (shf ? a.b_lo : 0);
       }
       __syncwarp();
       if (lane == 0) r.count = cnt - take;
@@ -713,16 +752,12 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       continue;
     }
     if (!any_alive) continue;
-    if (kFix && fix_ok) {  // this trip's events against the limb budget, reserved 256 at a time
-      const unsigned k = __popc(~need);
-      if (fix_left < k) {
-        unsigned used = 0;
-        if (lane == 0) used = atomicAdd(&s_fixbudget, kFixChunk);
-        used = __shfl_sync(0xffffffffu, used, 0);
-        if (used + kFixChunk > a.fix_budget) fix_ok = false;
-        else fix_left += kFixChunk;
-      }
-      fix_left -= k;
+    if (kFix && (n_iter % kSweepEvery) == 0) {  // carry sweep of the next 32 * spl slots
+      unsigned c0 = 0;
+      if (lane == 0) c0 = atomicAdd(&s_sweep, 32u * fix_spl);
+      c0 = __shfl_sync(0xffffffffu, c0, 0);
+      for (unsigned k = 0; k < fix_spl; ++k)
+        fix_sweep_slot(reinterpret_cast<unsigned*>(S.trk) + 4 * ((c0 + 32u * k + lane) % fix_slots));
     }
     if (p.alive) ++n_ev;
     ++n_iter;
@@ -902,16 +937,6 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         agg_add(a.t.census_weight_batch, cen_b, cen_w);
         agg_add(a.t.edge_current, edge_key, edge_v);
       }
-    } else if (kFix && !fix_ok) {
-      // this block's limb budget is spent: warp-aggregated adds straight to
-      // the global fp64 tallies (per-lane REDs would saturate the L2 atomic
-      // units on same-cell adds, cf. the cold start)
-      agg_add(a.t.track_flux_batch + (size_t)a.b_lo * I, trk_key, trk_v);
-      if (trk_key >= 0) atomicAdd(S.trc + trk_cell, 1u);
-      agg_add3(a.t.census_phi, a.t.census_current, a.t.census_closure, cen_cell, cen_phi, cen_J,
-               cen_F);
-      agg_add(S.cwb, cen_b, cen_w);
-      agg_add(a.t.edge_current, edge_key, edge_v);
     } else {  // spread population: per-lane atomics, no warp synchronisation
       double* trk = kShf ? S.trk : a.t.track_flux_batch;
       double* cphi = kShf ? S.cphi : a.t.census_phi;
@@ -921,22 +946,28 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       double* edg = kShf ? S.edge : a.t.edge_current;
       if (trk_key >= 0) {
         if (!kFix) atomicAdd(trk + trk_key, trk_v);
-        else if (!(fix_ok && fix_add(S.trk + 2 * trk_key, trk_v, fix_trk)))
+        else if (!fix_add(S.trk + 2 * trk_key, trk_v, fix_trk))
           atomicAdd(a.t.track_flux_batch + (size_t)a.b_lo * I + trk_key, trk_v);
         if (sh) atomicAdd(S.trc + trk_cell, 1u);
         else atomicAdd(a.t.tracks + trk_cell, 1ULL);
       }
 #if !defined(HWWG_CENSUS_PER_LANE)
-      // census scores: run-aggregated across the warp (census_runs)
-      if (kFix) {
+      // census scores: fixed-point slots take per-lane native adds in a spread
+      // population (no conflict cost worth a warp scan); in the cold start and
+      // with fp64 slots they are run-aggregated (census_runs)
+      if (kFix && !a.census_runs) {
+        if (cen_cell >= 0) {
+          if (!fix_add(S.cphi + 2 * cen_cell, cen_phi, fix_trk)) atomicAdd(a.t.census_phi + cen_cell, cen_phi);
+          if (!fix_add(S.cJ + 2 * cen_cell, cen_J, fix_trk)) atomicAdd(a.t.census_current + cen_cell, cen_J);
+          if (!fix_add(S.cF + 2 * cen_cell, cen_F, fix_trk)) atomicAdd(a.t.census_closure + cen_cell, cen_F);
+        }
+        census_weight_runs(cwb, cen_cell >= 0, cen_b, cen_w);
+      } else if (kFix) {  // cold start: identical split copies reach census together
         census_runs(
             [&](int cell, double s0, double s1, double s2) {
-              if (!(fix_ok && fix_add(S.cphi + 2 * cell, s0, fix_trk)))
-                atomicAdd(a.t.census_phi + cell, s0);
-              if (!(fix_ok && fix_add(S.cJ + 2 * cell, s1, fix_trk)))
-                atomicAdd(a.t.census_current + cell, s1);
-              if (!(fix_ok && fix_add(S.cF + 2 * cell, s2, fix_trk)))
-                atomicAdd(a.t.census_closure + cell, s2);
+              if (!fix_add(S.cphi + 2 * cell, s0, fix_trk)) atomicAdd(a.t.census_phi + cell, s0);
+              if (!fix_add(S.cJ + 2 * cell, s1, fix_trk)) atomicAdd(a.t.census_current + cell, s1);
+              if (!fix_add(S.cF + 2 * cell, s2, fix_trk)) atomicAdd(a.t.census_closure + cell, s2);
             },
             cwb, cen_cell, cen_b, cen_phi, cen_J, cen_F, cen_w);
       } else {
@@ -958,7 +989,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
 #endif
       if (edge_key >= 0) {
         if (!kFix) atomicAdd(edg + edge_key, edge_v);
-        else if (!(fix_ok && fix_add(S.edge + 2 * edge_key, edge_v, fix_edge)))
+        else if (!fix_add(S.edge + 2 * edge_key, edge_v, fix_edge))
           atomicAdd(a.t.edge_current + edge_key, edge_v);
       }
     }
@@ -982,8 +1013,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         declared = true;
         donate = __shfl_sync(0xffffffffu, open, 0) != 0;
       }
-      const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell, p.hist, p.key, p.ctr,
-                             dau, 0u, 0u};  // base 0: daughters 1..dau
+      const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell | ((unsigned)p.bslot << 16),
+                             p.hist, p.key, p.ctr, dau, 0u, 0u};  // base 0: daughters 1..dau
       bool push_local = dau > 0 && !donate;
       // one pair of atomics per warp: the donated records' active units, then
       // their slots (ordered before this warp's own decrement by the fence on
