@@ -129,9 +129,14 @@ __global__ void __launch_bounds__(kCbThreads) k_cb_sums(FastCombArgs a) {
   const double scale = comb_scale(a);
   const uint64_t t0 = (uint64_t)blockIdx.x * kCbTile;
   unsigned long long q = 0;
-#pragma unroll 4
-  for (int j = threadIdx.x; j < kCbTile; j += kCbThreads)
-    if (t0 + j < a.n) q += fixed_w(a.bank.wt[t0 + j].x, scale);
+  double ld[kCbItems];  // all loads in flight first
+#pragma unroll
+  for (int i = 0; i < kCbItems; ++i) {
+    const uint64_t j = t0 + threadIdx.x + i * kCbThreads;
+    ld[i] = j < a.n ? a.bank.wt[j].x : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < kCbItems; ++i) q += fixed_w(ld[i], scale);
   unsigned long long t;
   block_exclusive_256(q, red, t);
   if (threadIdx.x == 0) S.tsum()[blockIdx.x] = t;
@@ -177,35 +182,67 @@ __device__ __forceinline__ uint64_t teeth_below_i(double v, double off, double i
 }
 
 // pass 2: per tile, weights staged through shared memory, integer prefixes by
-// a block scan (blocked order: thread i owns particles 16i .. 16i+15), teeth
-// written per particle
+// a block scan (blocked order: thread i owns particles 16i .. 16i+15), every
+// particle's tooth bound cnt(P_j) into shared memory; the tile's teeth are the
+// contiguous range [cnt(tile start), cnt(tile end)), written by consecutive
+// threads, each finding its source particle by binary search over the bounds
+// (writing per particle diverged: with ~1 tooth per 60 particles after the
+// cold start, most warps ran the write path for one lane)
+// padded shared-memory indices: blocked reads (thread t, item i at 16t + i)
+// and striped writes both stay free of bank conflicts
+__device__ __forceinline__ int pad_d(int j) { return j + (j >> 4); }  // doubles
+__device__ __forceinline__ int pad_u(int j) { return j + (j >> 5); }  // 32-bit words
+
 __global__ void __launch_bounds__(kCbThreads) k_cb_scatter(FastCombArgs a) {
-  __shared__ double wv[kCbTile];
+  __shared__ double wv[kCbTile + kCbTile / 16];  // weights, then the tooth bounds
   __shared__ unsigned long long red[kCbThreads / 32];
+  __shared__ unsigned long long s_k0;
   const CbScratch S{a.prefix, (a.n + kCbTile - 1) / kCbTile};
   const double scale = S.scale(), inv_sp = 1.0 / S.spacing_i(), off_i = S.offset_i();
   const double spacing = a.scalars[1];
   const uint64_t t0 = (uint64_t)blockIdx.x * kCbTile;
   const int m = a.n - t0 < (uint64_t)kCbTile ? (int)(a.n - t0) : kCbTile;
-  for (int j = threadIdx.x; j < kCbTile; j += kCbThreads) wv[j] = j < m ? a.bank.wt[t0 + j].x : 0.0;
+  {  // all 16 loads in flight before the first use (one round trip per tile)
+    double ld[kCbItems];
+#pragma unroll
+    for (int i = 0; i < kCbItems; ++i) {
+      const int j = threadIdx.x + i * kCbThreads;
+      ld[i] = j < m ? a.bank.wt[t0 + j].x : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kCbItems; ++i) wv[pad_d(threadIdx.x + i * kCbThreads)] = ld[i];
+  }
   __syncthreads();
   unsigned long long q[kCbItems];
   unsigned long long mine = 0;
 #pragma unroll
   for (int i = 0; i < kCbItems; ++i) {
-    q[i] = fixed_w(wv[threadIdx.x * kCbItems + i], scale);
+    q[i] = fixed_w(wv[pad_d(threadIdx.x * kCbItems + i)], scale);
     mine += q[i];
   }
   unsigned long long tot;
-  unsigned long long run = S.tstart()[blockIdx.x] + block_exclusive_256(mine, red, tot);
-  uint64_t k_lo = teeth_below_i((double)run, off_i, inv_sp, a.target);
+  const unsigned long long start = S.tstart()[blockIdx.x];
+  unsigned long long run = start + block_exclusive_256(mine, red, tot);
+  if (threadIdx.x == 0) s_k0 = teeth_below_i((double)start, off_i, inv_sp, a.target);
+  __syncthreads();  // every weight is read: wv becomes the bound table
+  const uint64_t k0 = s_k0;
+  unsigned* khi = reinterpret_cast<unsigned*>(wv);  // cnt(P_j) - k0 per particle
 #pragma unroll
   for (int i = 0; i < kCbItems; ++i) {
     run += q[i];
-    const int j = threadIdx.x * kCbItems + i;
-    const uint64_t k_hi = teeth_below_i((double)run, off_i, inv_sp, a.target);
-    if (k_lo < k_hi && j < m) write_teeth(a, t0 + j, k_lo, k_hi, spacing);
-    k_lo = k_hi;
+    khi[pad_u(threadIdx.x * kCbItems + i)] =
+        (unsigned)(teeth_below_i((double)run, off_i, inv_sp, a.target) - k0);
+  }
+  __syncthreads();
+  const unsigned nT = khi[pad_u(kCbTile - 1)];  // the tile's teeth (padding holds the last bound)
+  for (unsigned r = threadIdx.x; r < nT; r += kCbThreads) {
+    int lo = 0, hi = m - 1;  // first particle j with khi[j] > r
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (khi[pad_u(mid)] > r) hi = mid;
+      else lo = mid + 1;
+    }
+    write_teeth(a, t0 + lo, k0 + r, k0 + r + 1, spacing);
   }
   // teeth stranded past the integer total by round-off go to the last particle
   // with weight (popctrl.cpp:31-37)
