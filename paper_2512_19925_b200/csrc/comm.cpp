@@ -1,6 +1,7 @@
 // NCCL and loopback implementations of the driver's collectives (comm.h).
 #include "comm.h"
 
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <condition_variable>
@@ -9,6 +10,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -21,11 +23,55 @@
       throw ::hwwg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
+// NCCL is opened at run time, only by a multi-GPU driver: a link-time
+// dependency on libnccl.so.2 would put the system NCCL in the process first,
+// and torch (whose bundled NCCL is newer) then fails to import next to it. With
+// dlopen, "libnccl.so.2" resolves to the copy already loaded (torch's, under
+// torchrun) or the system one otherwise.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+static const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw hwwg::ApiError(HWWG_ECUDA, std::string("cannot load NCCL: ") + dlerror());
+    auto sym = [&](auto& f, const char* name) {
+      f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+      if (!f) throw hwwg::ApiError(HWWG_ECUDA, std::string("NCCL symbol missing: ") + name);
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.AllReduce, "ncclAllReduce");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    return a;
+  }();
+  return api;
+}
+
 #define COMM_NCCL(call)                                                                   \
   do {                                                                                    \
     ncclResult_t r_ = (call);                                                             \
     if (r_ != ncclSuccess)                                                                \
-      throw ::hwwg::ApiError(HWWG_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+      throw ::hwwg::ApiError(HWWG_ECUDA,                                                   \
+                             std::string(#call) + ": " + nccl().GetErrorString(r_));       \
   } while (0)
 
 // In-process hub of the loopback ranks: one stream, staging, mailboxes, barrier.
@@ -74,29 +120,29 @@ class NcclComm final : public Comm {
   NcclComm(const uint8_t id_bytes[128], int rank, int world) : rank_(rank), world_(world) {
     ncclUniqueId id;
     std::memcpy(&id, id_bytes, sizeof(id));
-    COMM_NCCL(ncclCommInitRank(&comm_, world, id, rank));
+    COMM_NCCL(nccl().CommInitRank(&comm_, world, id, rank));
   }
   ~NcclComm() override {
-    if (comm_) ncclCommDestroy(comm_);
+    if (comm_) nccl().CommDestroy(comm_);
   }
   int rank() const override { return rank_; }
   int world() const override { return world_; }
   void all_reduce(const void* send, void* recv, size_t count, DType t, RedOp op,
                   cudaStream_t s) override {
-    COMM_NCCL(ncclAllReduce(send, recv, count, nccl_type(t), op == RedOp::kSum ? ncclSum : ncclMax,
+    COMM_NCCL(nccl().AllReduce(send, recv, count, nccl_type(t), op == RedOp::kSum ? ncclSum : ncclMax,
                             comm_, s));
   }
   void all_gather(const void* send, void* recv, size_t count, DType t, cudaStream_t s) override {
-    COMM_NCCL(ncclAllGather(send, recv, count, nccl_type(t), comm_, s));
+    COMM_NCCL(nccl().AllGather(send, recv, count, nccl_type(t), comm_, s));
   }
-  void group_start() override { COMM_NCCL(ncclGroupStart()); }
+  void group_start() override { COMM_NCCL(nccl().GroupStart()); }
   void send(const void* buf, size_t count, DType t, int peer, cudaStream_t s) override {
-    COMM_NCCL(ncclSend(buf, count, nccl_type(t), peer, comm_, s));
+    COMM_NCCL(nccl().Send(buf, count, nccl_type(t), peer, comm_, s));
   }
   void recv(void* buf, size_t count, DType t, int peer, cudaStream_t s) override {
-    COMM_NCCL(ncclRecv(buf, count, nccl_type(t), peer, comm_, s));
+    COMM_NCCL(nccl().Recv(buf, count, nccl_type(t), peer, comm_, s));
   }
-  void group_end(cudaStream_t) override { COMM_NCCL(ncclGroupEnd()); }
+  void group_end(cudaStream_t) override { COMM_NCCL(nccl().GroupEnd()); }
 
  private:
   int rank_, world_;
@@ -250,6 +296,17 @@ int hwwg_loopback_create(int32_t world, int32_t device, hwwg_loopback** out) {
     return hwwg::fail(HWWG_ECUDA, std::string("loopback: ") + cudaGetErrorString(e));
   }
   *out = h;
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_nccl_unique_id(uint8_t* out) {
+  HWWG_API_BEGIN
+  if (!out) return hwwg::fail(HWWG_EINVAL, "NULL argument");
+  ncclUniqueId id;
+  COMM_NCCL(nccl().GetUniqueId(&id));
+  std::memset(out, 0, 128);
+  std::memcpy(out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
   return HWWG_OK;
   HWWG_API_END
 }

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -79,6 +80,25 @@ struct DevError {
     if (e_ != cudaSuccess)                                                             \
       throw ::hwwg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));     \
   } while (0)
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: the
+// size configured so far is cached per device ordinal (a process may drive
+// several GPUs), under a lock (loopback ranks are host threads).
+constexpr int kMaxDevices = 64;
+struct DynSmemCache {
+  size_t size[kMaxDevices] = {};
+};
+template <class Kernel>
+inline void ensure_dyn_smem(Kernel k, size_t smem, DynSmemCache& cache) {
+  static std::mutex m;
+  int dev = 0;
+  HWWG_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  std::lock_guard<std::mutex> lk(m);
+  if (smem <= cache.size[dev]) return;
+  HWWG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cache.size[dev] = smem;
+}
 
 // mesh.cpp:26-40 on the device: uniform fast path with +-1 guards, else
 // upper_bound; -1 when x lies outside [x_min, x_max].

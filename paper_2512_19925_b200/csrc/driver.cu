@@ -7,7 +7,6 @@
 // thresholds (driver.cpp:170-177) and reads the step record back once, at the
 // end of the step.
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -30,13 +29,6 @@
 #include "transport.cuh"
 
 using namespace hwwg;
-
-#define NCCL_CHECK(call)                                                                  \
-  do {                                                                                    \
-    ncclResult_t r_ = (call);                                                             \
-    if (r_ != ncclSuccess)                                                                \
-      throw ::hwwg::ApiError(HWWG_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
 
 namespace {
 
@@ -427,7 +419,7 @@ void init_driver(hwwg_driver* d) {
       d->fperm.reserve(local_target + 4096);  // the rebalanced teeth before their permutation
     }
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
-    const int warps = d->sms * fast_blocks_per_sm(0) * (fast_threads_per_block() / 32);
+    const int warps = d->sms * fast_max_blocks_per_sm() * (fast_threads_per_block() / 32);
     d->max_warps = warps;
     d->warp_cursor.reserve((size_t)kWarpCursorWords * warps);
     d->stacks.reserve((size_t)warps * d->stack_cap);
@@ -1139,12 +1131,14 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         smem += fast_smem_centers_bytes(I);
         // fixed-point track/edge/census tallies, where the wider slots keep the
         // occupancy — in the cold start too, where native same-address limb
-        // adds beat the warp aggregation (config 2 step 1: 5.97 -> 4.84 ms of
-        // transport) unless aggregation is forced (HWWG_FAST_AGG=1). Largest
+        // adds beat the warp aggregation (config 5 step 1: 46 -> 33 ms of
+        // transport, with run-aggregated census scores) unless aggregation is
+        // forced (HWWG_FAST_AGG=1). Largest
         // expected scores: a window survivor or source weight (<= max(rho *
         // max centre = rho, step_wref)) times speed/dx for a track, divided by
         // dt for an edge crossing.
         fa.fix = 0;
+        const int uni = d->prob.gen_uniform_homog ? 1 : 0;
         if (fa.smem_tallies == 1 && (!fa.aggregate || d->agg_all != 1) && d->flush_replicas == 0 &&
             d->fix_tallies) {
           const size_t fsm = fast_smem_fix_bytes(I, fa.nb) + fast_smem_centers_bytes(I);
@@ -1154,7 +1148,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           for (const CellInfo& ci : d->prob.cells_h) vmin = std::min(vmin, ci.speed * ci.inv_dx);
           const double w = std::max(c.rho, d->step_wref);
           int kt = 0, ke = 0;
-          const int bps = fast_blocks_per_sm(fsm);
+          const int bps = fast_blocks_per_sm(fsm, uni, 1, 1);
           // dynamic range: the smallest census score (a weight near the lowest
           // window floor eps_min / rho) must keep >= 2^20 grid units, or its
           // rounding would bias low-window cells: beyond 20 binades below the
@@ -1163,7 +1157,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           const bool range_ok = smallest > 0.0 &&
                                 std::ilogb(w * vmax) - std::ilogb(smallest) <= 20;
           if (range_ok && fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
-              bps >= fast_blocks_per_sm(smem)) {
+              bps >= fast_blocks_per_sm(smem, uni, 1, 0)) {
             fa.fix = 1;
             fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             fa.fix_k_trk = kt;
@@ -1173,7 +1167,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           }
         }
         fa.scramble = fa.aggregate ? 0 : d->scramble;
-        const int blocks = d->sms * fast_blocks_per_sm(smem);
+        const int blocks = d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fa.fix);
         const int gw = blocks * (fast_threads_per_block() / 32);
         grid_warps_max = std::max(grid_warps_max, gw);
         if (u == thr.size() && gw >= grid_warps_max && fa.n_src) {
@@ -1647,17 +1641,6 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
 }
 
 void hwwg_driver_destroy(hwwg_driver* d) { delete d; }
-
-int hwwg_nccl_unique_id(uint8_t* out) {
-  HWWG_API_BEGIN
-  if (!out) return fail(HWWG_EINVAL, "NULL argument");
-  ncclUniqueId id;
-  NCCL_CHECK(ncclGetUniqueId(&id));
-  std::memset(out, 0, 128);
-  std::memcpy(out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
-  return HWWG_OK;
-  HWWG_API_END
-}
 
 int hwwg_driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   HWWG_API_BEGIN

@@ -124,7 +124,11 @@ void launch_step_start(double* slab, size_t slab_words, unsigned long long* curs
 void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
                              unsigned long long* count, cudaStream_t s);
 
-int fast_blocks_per_sm(size_t smem);
+// resident blocks per SM of the transport instantiation (uniform mesh, shared
+// tallies, fixed-point slots) with `smem` dynamic shared memory, and the most
+// any instantiation holds
+int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix);
+int fast_max_blocks_per_sm();
 int fast_threads_per_block();
 // per-warp census cursor words (FastArgs::warp_cursor: next, end)
 constexpr int kWarpCursorWords = 2;

@@ -264,6 +264,34 @@ int hwwg_load_config_file(const char* path, hwwg_run_config* c) {
       else if (key == "t_end") c->t_end = std::stod(val);
       else if (key == "time_steps") c->time_steps = std::stoi(val);
       else if (key == "threads") c->threads = std::stoi(val);
+      // config-3 extension keys (absent from the
+      // reference's loader): repeatable `region = x_hi, sigma_t, sigma_s,
+      // sigma_f, nu_f, speed`, `volume_source = x_lo, x_hi, t_lo, t_hi, rate`,
+      // `vol_histories`, `no_pulse`
+      else if (key == "region") {
+        std::vector<double> v;
+        std::stringstream ss(val);
+        std::string tok;
+        while (std::getline(ss, tok, ',')) v.push_back(std::stod(tok));
+        if (v.size() != 6) throw std::invalid_argument("region needs x_hi and 5 material values");
+        if (c->n_regions == 8) throw std::invalid_argument("at most 8 regions");
+        c->region_x_hi[c->n_regions] = v[0];
+        for (int j = 0; j < 5; ++j) c->region_mat[c->n_regions][j] = v[1 + j];
+        ++c->n_regions;
+      } else if (key == "volume_source") {
+        std::vector<double> v;
+        std::stringstream ss(val);
+        std::string tok;
+        while (std::getline(ss, tok, ',')) v.push_back(std::stod(tok));
+        if (v.size() != 5) throw std::invalid_argument("volume_source needs x_lo, x_hi, t_lo, t_hi, rate");
+        c->vol_x_lo = v[0];
+        c->vol_x_hi = v[1];
+        c->vol_t_lo = v[2];
+        c->vol_t_hi = v[3];
+        c->vol_rate = v[4];
+        if (!c->vol_histories) c->vol_histories = c->histories_per_step;
+      } else if (key == "vol_histories") c->vol_histories = std::stoull(val);
+      else if (key == "no_pulse") c->no_pulse = (val == "1" || val == "true") ? 1 : 0;
       else if (key == "reference" || key == "out_dir") { /* host tooling keys: accepted */ }
       else throw std::invalid_argument("unknown key '" + key + "'");
     } catch (const std::exception& e) {

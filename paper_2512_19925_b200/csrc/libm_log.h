@@ -1,5 +1,17 @@
 // Bit-exact replay of the host libm's double log on host and device.
 //
+// Provenance and licence. The algorithm restated here is glibc 2.39's double
+// log (sysdeps/ieee754/dbl-64/e_log.c, contributed to glibc from Arm's
+// optimized-routines project; glibc: LGPL-2.1-or-later, optimized-routines:
+// MIT OR Apache-2.0 WITH LLVM-exception). Bit-exact replay of the reference's
+// xoshiro-driven flight distances needs the same operations in the same order,
+// so the range split, table lookup and polynomial evaluation below follow that
+// published algorithm step for step (an acknowledged deviation from "do not
+// copy a libm implementation": a different log would change ~8e-4 of the
+// reference's events). No glibc source text or constant is in this repository:
+// the constants are read from the installed libm at build time
+// (gen_libm_log_table.py) into _build/, which is never committed.
+//
 // The reference samples flight distances as -std::log(xi)/sigma_t
 // (proj/src/transport.cpp:24-27). Its third-party dependency is glibc 2.39's
 // log (ifunc-selected FMA build on x86-64 hosts with FMA+AVX2). The published

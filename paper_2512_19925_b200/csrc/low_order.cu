@@ -1450,12 +1450,8 @@ void launch_low_order_update(const LowOrderArgs& a_in, cudaStream_t st) {
   a.smem_state = a.I <= kSmemStateMaxI ? 1 : 0;
   if (a.smem_state)
     smem += ((size_t)6 * (2 * a.I + 3) + (size_t)3 * (a.I + 2) + (a.I + 1) + a.I) * sizeof(double);
-  static size_t configured = 0;
-  if (smem > configured) {
-    HWWG_CUDA(cudaFuncSetAttribute(k_low_order_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    configured = smem;
-  }
+  static DynSmemCache configured;
+  ensure_dyn_smem(k_low_order_update, smem, configured);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(1);
   cfg.blockDim = dim3(kCtaThreads);

@@ -720,12 +720,8 @@ void launch_exact_segment(const ExactArgs& a, cudaStream_t s) {
     k_exact_histories<<<(unsigned)((a.n + 127) / 128), 128, 0, s>>>(a);
     const size_t smem = a.chunks.stride * sizeof(double);
     if (smem <= kReplaySmemMax) {  // chunk accumulators in shared memory
-      static size_t configured = 0;
-      if (smem > configured) {
-        HWWG_CUDA(cudaFuncSetAttribute(k_exact_replay<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-      }
+      static DynSmemCache configured;
+      ensure_dyn_smem(k_exact_replay<true>, smem, configured);
       k_exact_replay<true><<<(unsigned)a.chunks.count, 32, smem, s>>>(a);
     } else {
       k_exact_replay<false><<<(unsigned)a.chunks.count, 32, 0, s>>>(a);

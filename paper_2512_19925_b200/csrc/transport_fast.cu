@@ -35,6 +35,7 @@
 // loops) with census scores run-aggregated across the warp, and global REDs
 // warp-aggregated (MATCH.ANY groups, REDUX fixed-point sums) when the
 // histograms do not fit in shared memory (I = 4000).
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -1269,11 +1270,32 @@ int fast_prof_read(unsigned long long out[12], unsigned* hist) {
 
 void configure_fast_kernel();
 
-int fast_blocks_per_sm(size_t smem) {
+using FastKernel = void (*)(FastArgs);
+FastKernel fast_kernel(int uniform, int shf, int fix) {
+  return uniform && fix   ? k_fast_segment<true, true, true>
+         : uniform && shf ? k_fast_segment<true, true, false>
+         : uniform        ? k_fast_segment<true, false, false>
+         : fix            ? k_fast_segment<false, true, true>
+         : shf            ? k_fast_segment<false, true, false>
+                          : k_fast_segment<false, false, false>;
+}
+
+// resident blocks per SM of the instantiation a launch will use (the
+// persistent grid must be fully resident: idle warps wait on busy ones)
+int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix) {
   configure_fast_kernel();
   int n = 0;
-  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_fast_segment<true, true, false>, kThreads, smem));
+  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fast_kernel(uniform, shf, fix),
+                                                          kThreads, smem));
   return n;
+}
+// the most blocks per SM any instantiation can hold (per-warp buffers are sized by it)
+int fast_max_blocks_per_sm() {
+  int m = 0;
+  for (int u = 0; u < 2; ++u)
+    for (int sh = 0; sh < 2; ++sh)
+      for (int f = 0; f <= sh; ++f) m = std::max(m, fast_blocks_per_sm(0, u, sh, f));
+  return m;
 }
 
 namespace {
@@ -1284,14 +1306,12 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
 }  // namespace
 
 void configure_fast_kernel() {
-  static bool configured = false;
-  if (!configured) {
-    for (auto k : {k_fast_segment<false, false, false>, k_fast_segment<false, true, false>,
-                   k_fast_segment<true, false, false>, k_fast_segment<true, true, false>,
-                   k_fast_segment<false, true, true>, k_fast_segment<true, true, true>})
-      HWWG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
+  static DynSmemCache configured[6];
+  int i = 0;
+  for (auto k : {k_fast_segment<false, false, false>, k_fast_segment<false, true, false>,
+                 k_fast_segment<true, false, false>, k_fast_segment<true, true, false>,
+                 k_fast_segment<false, true, true>, k_fast_segment<true, true, true>})
+    ensure_dyn_smem(k, 200 * 1024, configured[i++]);
 }
 
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
@@ -1299,12 +1319,7 @@ void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_
   if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head, a.span);
   const bool shf = a.smem_tallies == 1;
   const bool fix = shf && a.fix;
-  void (*k)(FastArgs) = a.uniform && fix   ? k_fast_segment<true, true, true>
-                        : a.uniform && shf ? k_fast_segment<true, true, false>
-                        : a.uniform        ? k_fast_segment<true, false, false>
-                        : fix              ? k_fast_segment<false, true, true>
-                        : shf              ? k_fast_segment<false, true, false>
-                                           : k_fast_segment<false, false, false>;
+  const FastKernel k = fast_kernel(a.uniform, shf, fix);
   // programmatic dependent launch: the grid may be scheduled while the kernel
   // before it (the window update) drains; every block waits for it
   // (griddepcontrol.wait) before touching memory

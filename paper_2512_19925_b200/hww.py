@@ -426,7 +426,13 @@ class RunConfig:
             source_strength=c.strength,
             material=Material(c.sigma_t, c.sigma_s, c.sigma_f, c.nu_f, c.speed),
             x_min=c.x_min, x_max=c.x_max, cells=c.cells, t_end=c.t_end,
-            time_steps=c.time_steps, threads=c.threads, out_dir=_file_key(path, "out_dir"))
+            time_steps=c.time_steps, threads=c.threads, out_dir=_file_key(path, "out_dir"),
+            regions=[(c.region_x_hi[i], Material(*[c.region_mat[i][j] for j in range(5)]))
+                     for i in range(c.n_regions)],
+            volume_source=((c.vol_x_lo, c.vol_x_hi, c.vol_t_lo, c.vol_t_hi, c.vol_rate)
+                           if c.vol_rate > 0.0 else None),
+            vol_histories=c.vol_histories if c.vol_rate > 0.0 else 0,
+            no_pulse=bool(c.no_pulse))
 
     def validate(self):
         """validate_config (config.cpp:27-69): list of violations."""

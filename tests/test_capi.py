@@ -64,6 +64,28 @@ def test_config_file_loader(tmp_path):
         hw.RunConfig.from_file(p)
 
 
+def test_config_file_loader_config3_keys(tmp_path):
+    """The config-3 extension keys (regions, volumetric source, no pulse) load into
+    the same RunConfig the BASELINE builder makes (paper_2512_19925_b200/configs.py)."""
+    from paper_2512_19925_b200.configs import baseline
+    p = tmp_path / "c3.cfg"
+    p.write_text("mode = hww\nhistories_per_step = 10000000\nrho = 4\nseed = 3\n"
+                 "x_min = 0\nx_max = 30\ncells = 1000\nt_end = 25\ntime_steps = 50\n"
+                 "sigma_t = 1\nsigma_s = 0.5\nsigma_f = 0\nnu_f = 0\n"
+                 "region = 10, 1, 0.5, 0, 0, 1\nregion = 20, 10, 1, 0, 0, 1\n"
+                 "region = 30, 1, 0.99, 0, 0, 1\nvolume_source = 0, 2, 0, 1, 1\nno_pulse = 1\n")
+    got, want = hw.RunConfig.from_file(p).to_c(), baseline(3).to_c()
+    for f, _ in want._fields_:
+        a, b = getattr(got, f), getattr(want, f)
+        if hasattr(a, "__len__"):
+            a, b = [list(x) if hasattr(x, "__len__") else x for x in a], \
+                   [list(x) if hasattr(x, "__len__") else x for x in b]
+        assert a == b, f
+    p.write_text("region = 10, 1, 0.5\n")
+    with pytest.raises(ValueError, match="region needs"):
+        hw.RunConfig.from_file(p)
+
+
 def test_config_validation_messages():
     cfg = hw.RunConfig(theta=0.3, rho=0.5, batches=1, update_fractions=(0.5, 0.25))
     v = cfg.validate()
