@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_build", "libhwwg.so")
+# HWWG_LIB: an alternative build of the same library (tests: the bounds-checked
+# variant in _build_checked/, built by __graft_entry__.build())
+LIB_PATH = os.environ.get("HWWG_LIB") or os.path.join(PKG, "_build", "libhwwg.so")
 
 HWWG_OK = 0
 HWWG_EINVAL = -1

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -80,6 +81,25 @@ struct DevError {
     if (e_ != cudaSuccess)                                                             \
       throw ::hwwg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));     \
   } while (0)
+
+// Device-side bounds checks of the builds with -DHWWG_CHECKS
+// (_build_checked/, tests/test_gpu_checked.py): a failed check prints its
+// site and traps, which fails the launch. compute-sanitizer is not available
+// on the GPU pool, so these stand in for memcheck on the indices that matter.
+#ifdef HWWG_CHECKS
+#define HWWG_CHECK(cond)                                                               \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("HWWG_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,  \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define HWWG_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: the
 // size configured so far is cached per device ordinal (a process may drive

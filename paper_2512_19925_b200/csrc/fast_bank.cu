@@ -29,8 +29,10 @@ __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src,
   const double2 xm = a.bank.xm[src];
   const double2 wt = a.bank.wt[src];
   const uint4 m = a.bank.meta[src];
+  HWWG_CHECK(src < a.n && k1 <= a.target);
   for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t p = a.perm(k);
+    HWWG_CHECK(p < a.target);
     a.out.xm[p] = xm;
     a.out.wt[p] = make_double2(spacing, wt.y);
     // fresh identity for the new step: history = its slot, key 0, draw 0
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(kCbThreads) k_cb_scatter(FastCombArgs a) {
       if (khi[pad_u(mid)] > r) hi = mid;
       else lo = mid + 1;
     }
+    HWWG_CHECK(lo < m && khi[pad_u(lo)] > r && (lo == 0 || khi[pad_u(lo - 1)] <= r));
     write_teeth(a, t0 + lo, k0 + r, k0 + r + 1, spacing);
   }
   // teeth stranded past the integer total by round-off go to the last particle
@@ -288,6 +291,7 @@ __global__ void k_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm,
   const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   const uint64_t s = perm(c);
+  HWWG_CHECK(s < n);
   uint64_t g = c, rem = c;  // global id of local slot c
   for (int i = 0; i < t.n; ++i) {
     if (rem < t.cnt[i]) {

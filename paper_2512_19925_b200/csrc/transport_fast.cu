@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       declared = true;
       open = __shfl_sync(0xffffffffu, open, 0);
       if (open) {
+        HWWG_CHECK(sp >= 1 && sp <= a.stack_cap);
         FastStackRec& top = STK(sp - 1);
         const unsigned cnt = top.count;
         const bool split_top = cnt >= 2 * kPiece;
@@ -604,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     FPROF(8);
     unsigned need = __ballot_sync(0xffffffffu, !p.alive);
     while (need && sp > 0) {
+      HWWG_CHECK(sp >= 1 && sp <= a.stack_cap);
       FastStackRec& r = STK(sp - 1);
       const unsigned k = __popc(need);
       const unsigned cnt = r.count;
@@ -663,6 +665,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         const unsigned k = base + rank;
         const unsigned idx = a.scramble && (k | 1023u) < n_src ? (k & ~1023u) | (__brev(k) >> 22) : k;
         {
+          HWWG_CHECK(idx < n_src);
           const double2 xm = a.src.xm[idx];
           const double2 wt = a.src.wt[idx];
           const uint4 m = a.src.meta[idx];
@@ -707,6 +710,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         if (ticket >= a.pool.cap) {
           got = -1;
         } else {
+          HWWG_CHECK(ticket < a.pool.cap);
           const FastStackRec* pr = a.pool.recs + ticket;
           unsigned backoff = 32;
           while (true) {
@@ -806,6 +810,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       if (d > 0.0) {
         trk_v = p.w * d * ci.inv_dx * a.inv_dt;
         trk_key = p.bslot * I + p.cell;
+        HWWG_CHECK(p.cell >= 0 && p.cell < I && p.bslot >= 0 && (!shf || p.bslot < a.nb) &&
+                   p.bslot < a.B);
         trk_cell = p.cell;
       }
       bool window_site = false;
@@ -826,6 +832,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         const bool domain = edge == 0 || edge == I;
         edge_v = (p.mu > 0 ? p.w : -p.w) * a.inv_dt;
         edge_key = edge;
+        HWWG_CHECK(edge >= 0 && edge <= I);
         if (domain) {
           const double amu = fabs(p.mu);
           if (amu < 1e-10) {
@@ -858,6 +865,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         }
       }
       if (window_site && windows) {  // ww.cpp:46-72 (split conserves, roulette unbiased)
+        HWWG_CHECK(p.cell >= 0 && p.cell < I);
         const double c = s_cent[p.cell];
         if (p.w > c * a.rho) {
           double n = ceil(p.w / c);
