@@ -1617,9 +1617,9 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     delete d;
     return fail(HWWG_EINVAL, "loopback hub world differs from the driver's world");
   }
-  if (d->fast && (cfg->sigma_f > 0.0 || cfg->cells > 65535)) {
+  if (d->fast && cfg->cells > 65535) {
     delete d;
-    return fail(HWWG_EINVAL, "philox mode: fission and > 65535 cells are not supported");
+    return fail(HWWG_EINVAL, "philox mode: more than 65535 cells are not supported");
   }
   // history ids are 32-bit and the batch of history h is one fp64 division
   // (exact while h * batches < 2^53)

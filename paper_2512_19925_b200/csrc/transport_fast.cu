@@ -131,7 +131,12 @@ struct Lane {
   unsigned hist, ctr;
   unsigned long long key;
   bool alive;
+  bool fis;  // a fission secondary whose direction and window game are pending
 };
+
+// split records with this bit in `ctr` hold fission secondaries (each draws its
+// own direction and plays the window game when popped), not identical copies
+constexpr unsigned kFissionRec = 0x80000000u;
 
 // One Philox4x32-10 block per event: flight, collision type and scattering
 // deviates (the roulette deviate after a scatter is the collision-type one
@@ -166,6 +171,7 @@ __device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigne
   p.ctr = 0;
   p.inv_mu = 1.0 / p.mu;
   p.alive = true;
+  p.fis = (r.ctr & kFissionRec) != 0;
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -493,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   const unsigned long long t_start = a.timeline ? globaltimer() : 0ULL;
   Lane p;
   p.alive = false;
+  p.fis = false;
   bool holding = true;  // this warp counts in pool.ctl[2] (active warps)
   bool declared = false;  // this warp has set pool.ctl[3] (backlog declared)
   // source reservation (warp-uniform) and the claim in flight (lane 0)
@@ -680,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           p.inv_mu = 1.0 / p.mu;
           p.bslot = batch_fast(p.hist, Hd, a.B) - (shf ? a.b_lo : 0);
           p.alive = p.w > 0.0;
+          p.fis = false;
         }
       }
       need = __ballot_sync(0xffffffffu, !p.alive);
@@ -780,6 +788,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     // ---- one event per live lane; tally contributions are collected per lane
     // and committed warp-aggregated after the event (see agg_add)
     unsigned split_n = 0;
+    bool fis_rec = false;  // the record pushed this trip holds fission secondaries
     int trk_key = -1, cen_cell = -1, cen_b = -1, edge_key = -1, trk_cell = 0;
     double trk_v = 0.0, cen_phi = 0.0, cen_J = 0.0, cen_F = 0.0, cen_w = 0.0, edge_v = 0.0;
     if (p.alive) {
@@ -791,77 +800,98 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       };
       double u0, u1, u2;
       draw3(a, p, u0, u1, u2);
-      const double d_census = ci.speed * (a.t_end - p.t);
-      const double d_coll = -log(u0) * ci.inv_sigma_t;
-      double d_b = __longlong_as_double(0x7ff0000000000000LL);
-      int edge = -1;
-      if (p.mu > 0.0) {
-        edge = p.cell + 1;
-        d_b = (edge_x(edge) - p.x) * p.inv_mu;
-      } else if (p.mu < 0.0) {
-        edge = p.cell;
-        d_b = (edge_x(edge) - p.x) * p.inv_mu;
-      }
-      double d = d_census;
-      if (d_coll < d) d = d_coll;
-      if (d_b < d) d = d_b;
-      // (a d_b < 0 from rounding at an edge is a crossing, as in the reference:
-      // transport.cpp:135-164 takes min{} as is and tests d == d_boundary)
-      if (d > 0.0) {
-        trk_v = p.w * d * ci.inv_dx * a.inv_dt;
-        trk_key = p.bslot * I + p.cell;
-        HWWG_CHECK(p.cell >= 0 && p.cell < I && p.bslot >= 0 && (!shf || p.bslot < a.nb) &&
-                   p.bslot < a.B);
-        trk_cell = p.cell;
-      }
       bool window_site = false;
-      if (d == d_census) {
-        p.x += d * p.mu;
-        p.t = a.t_end;
-        cen_phi = ci.speed * p.w * ci.inv_dx;
-        cen_J = cen_phi * p.mu;
-        cen_F = cen_phi * (1.0 / 3.0 - p.mu * p.mu);
-        cen_cell = p.cell;
-        cen_w = p.w;
-        cen_b = p.bslot;
-        ++n_cen;
-        p.alive = false;  // banked below, after the warp reconverges
-      } else if (d == d_b) {
-        p.x = edge_x(edge);
-        p.t += d * ci.inv_speed;
-        const bool domain = edge == 0 || edge == I;
-        edge_v = (p.mu > 0 ? p.w : -p.w) * a.inv_dt;
-        edge_key = edge;
-        HWWG_CHECK(edge >= 0 && edge <= I);
-        if (domain) {
-          const double amu = fabs(p.mu);
-          if (amu < 1e-10) {
-            atomicAdd(&s_rare[5], 1u);
-          } else {
-            const double bc = p.w * (0.5 - amu) / amu * a.inv_dt;
-            if (shf) atomicAdd(&S.bclo[edge == 0 ? 0 : 1], bc);
-            else atomicAdd(&a.t.boundary_closure[edge == 0 ? 0 : 1], bc);
-          }
-          atomicAdd(&a.t.dcount[0], p.w);
-          p.alive = false;
-        } else {
-          p.cell += p.mu > 0.0 ? 1 : -1;
-          window_site = true;
+      if (p.fis) {  // a fission secondary: its direction, then the window game (transport.cpp:181-185)
+        p.fis = false;
+        p.mu = 2.0 * u2 - 1.0;
+        p.inv_mu = 1.0 / p.mu;
+        window_site = true;
+      } else {
+        const double d_census = ci.speed * (a.t_end - p.t);
+        const double d_coll = -log(u0) * ci.inv_sigma_t;
+        double d_b = __longlong_as_double(0x7ff0000000000000LL);
+        int edge = -1;
+        if (p.mu > 0.0) {
+          edge = p.cell + 1;
+          d_b = (edge_x(edge) - p.x) * p.inv_mu;
+        } else if (p.mu < 0.0) {
+          edge = p.cell;
+          d_b = (edge_x(edge) - p.x) * p.inv_mu;
         }
-      } else {  // collision
-        p.x += d * p.mu;
-        p.t += d * ci.inv_speed;
-        ++n_coll;
-        const double xi = u1 * ci.sigma_t;
-        if (xi < ci.sigma_s) {
-          p.mu = 2.0 * u2 - 1.0;
-          p.inv_mu = 1.0 / p.mu;
-          u1 = xi / ci.sigma_s;  // recycled roulette deviate for the window game below
-          window_site = true;
-        } else {
-          // capture (fission is rejected for this mode at driver creation: the
-          // BASELINE slabs have sigma_f = 0)
-          p.alive = false;
+        double d = d_census;
+        if (d_coll < d) d = d_coll;
+        if (d_b < d) d = d_b;
+        // (a d_b < 0 from rounding at an edge is a crossing, as in the reference:
+        // transport.cpp:135-164 takes min{} as is and tests d == d_boundary)
+        if (d > 0.0) {
+          trk_v = p.w * d * ci.inv_dx * a.inv_dt;
+          trk_key = p.bslot * I + p.cell;
+          HWWG_CHECK(p.cell >= 0 && p.cell < I && p.bslot >= 0 && (!shf || p.bslot < a.nb) &&
+                     p.bslot < a.B);
+          trk_cell = p.cell;
+        }
+        if (d == d_census) {
+          p.x += d * p.mu;
+          p.t = a.t_end;
+          cen_phi = ci.speed * p.w * ci.inv_dx;
+          cen_J = cen_phi * p.mu;
+          cen_F = cen_phi * (1.0 / 3.0 - p.mu * p.mu);
+          cen_cell = p.cell;
+          cen_w = p.w;
+          cen_b = p.bslot;
+          ++n_cen;
+          p.alive = false;  // banked below, after the warp reconverges
+        } else if (d == d_b) {
+          p.x = edge_x(edge);
+          p.t += d * ci.inv_speed;
+          const bool domain = edge == 0 || edge == I;
+          edge_v = (p.mu > 0 ? p.w : -p.w) * a.inv_dt;
+          edge_key = edge;
+          HWWG_CHECK(edge >= 0 && edge <= I);
+          if (domain) {
+            const double amu = fabs(p.mu);
+            if (amu < 1e-10) {
+              atomicAdd(&s_rare[5], 1u);
+            } else {
+              const double bc = p.w * (0.5 - amu) / amu * a.inv_dt;
+              if (shf) atomicAdd(&S.bclo[edge == 0 ? 0 : 1], bc);
+              else atomicAdd(&a.t.boundary_closure[edge == 0 ? 0 : 1], bc);
+            }
+            atomicAdd(&a.t.dcount[0], p.w);
+            p.alive = false;
+          } else {
+            p.cell += p.mu > 0.0 ? 1 : -1;
+            window_site = true;
+          }
+        } else {  // collision
+          p.x += d * p.mu;
+          p.t += d * ci.inv_speed;
+          ++n_coll;
+          const double xi = u1 * ci.sigma_t;
+          if (xi < ci.sigma_s) {
+            p.mu = 2.0 * u2 - 1.0;
+            p.inv_mu = 1.0 / p.mu;
+            u1 = xi / ci.sigma_s;  // recycled roulette deviate for the window game below
+            window_site = true;
+          } else if (xi < ci.sigma_s + ci.sigma_f) {
+            // fission (transport.cpp:29-40, 179-188): floor(nu) + Bernoulli(frac)
+            // secondaries, the Bernoulli deviate the unused scattering one; this
+            // lane becomes the first secondary, the rest go on the stack as one
+            // fission record; each secondary's direction and window game follow
+            // on its own next trip (the parent itself is not windowed)
+            const double fl = floor(ci.nu_f);
+            const double frac = ci.nu_f - fl;
+            const unsigned n = (unsigned)fl + (frac > 0.0 && u2 < frac ? 1u : 0u);
+            if (n == 0) {
+              p.alive = false;
+            } else {
+              p.fis = true;
+              split_n = n;
+              fis_rec = true;
+            }
+          } else {  // capture
+            p.alive = false;
+          }
         }
       }
       if (window_site && windows) {  // ww.cpp:46-72 (split conserves, roulette unbiased)
@@ -1023,7 +1053,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         donate = __shfl_sync(0xffffffffu, open, 0) != 0;
       }
       const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell | ((unsigned)p.bslot << 16),
-                             p.hist, p.key, p.ctr, dau, 0u, 0u};  // base 0: daughters 1..dau
+                             p.hist, p.key, p.ctr | (fis_rec ? kFissionRec : 0u), dau, 0u,
+                             0u};  // base 0: daughters 1..dau
       bool push_local = dau > 0 && !donate;
       // one pair of atomics per warp: the donated records' active units, then
       // their slots (ordered before this warp's own decrement by the fence on

@@ -158,3 +158,12 @@ def test_config3_first_steps():
         c.vol_histories = 50_000
         return c
     check_engine(cfg, 5, label="C3")
+
+
+def test_reference_benchmark_fission():
+    """The reference's own benchmark (proj/configs/benchmark.cfg: a supercritical
+    medium, sigma_s = sigma_f = 1/3, nu = 2.3 — the one configuration with fission)
+    in the throughput engine: fission secondaries (floor(nu) + Bernoulli), each
+    with its own direction and window game (transport.cpp:29-40, 179-188)."""
+    check_engine(lambda s: baseline(0, histories=20_000, time_steps=6, seed=s), 6,
+                 label="benchmark.cfg")
