@@ -417,11 +417,13 @@ def run_ours(args):
     peak, peak_kind = measured_peak()
     # per GPU: this GPU's share of the segments over its transport-kernel time
     achieved = (m["seg"] / world) * BYTES_PER_SEGMENT / (tr_max * 1e-3) / 1e9 if tr_max > 0 else 0.0
+    # DRAM bytes of one steady-state transport launch of this configuration from
+    # an ncu --set full capture (profiles/round2_<config>_steady.md), or null
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.rng == "philox":
         try:
-            traffic = json.load(open(tp)).get(args.config, {}).get(args.rng)
+            traffic = json.load(open(tp)).get(f"{args.config.replace(':', '_')}_steady")
         except Exception:
             traffic = None
 

@@ -818,6 +818,137 @@ __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a) {
   }
 }
 
+// Mid-step window update of the throughput mode through the cached
+// factorization, latency-first (the general kernel took ~11 us of
+// in-kernel time per update at I = 400, ~30 us with its launch, on the
+// critical path between segments). One row per thread; every global value the
+// row needs — its cached factorization coefficients, the lagged state, the
+// live closure tallies of the partial snapshot around it and q — is loaded up
+// front in one round trip; the moving-average filter is evaluated per row
+// from those loads; shared memory carries only the Schur right-hand side
+// exchange and the PCR levels (one barrier each); the currents are not formed
+// (the update keeps only phi_hybrid and the centres). Same arithmetic as
+// low_order_update_body -> solve_and_center -> solve_cached on the same values.
+__device__ __forceinline__ double snap_filtered(const LowOrderArgs& a, int m) {
+  // partial_snapshot (tally.cpp:116-128) -> with_boundary_extrapolated ->
+  // filter_cell_avg_with_boundary (filters.cpp:11-24, 63-70): element m of F
+  const int I = a.I;
+  if (m == 0) return a.closure_tally[0] * a.snapshot_inv_norm;
+  if (m == I + 1) return a.closure_tally[I - 1] * a.snapshot_inv_norm;
+  if (a.ma_k <= 0 || I <= 0) return a.closure_tally[m - 1] * a.snapshot_inv_norm;
+  const int mi = m - 1;  // index in the interior g = F[1..I], g[j] = closure[j] * norm
+  int km = a.ma_k;
+  if (mi < km) km = mi;
+  if (I - 1 - mi < km) km = I - 1 - mi;
+  double sum = 0.0;
+  for (int l = -km; l <= km; ++l) sum += a.closure_tally[mi + l] * a.snapshot_inv_norm;
+  return sum / (2 * km + 1);
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_losm_mid_fast(LowOrderArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
+  __shared__ double P[kCtaThreads + 1], R0[kCtaThreads], R1[kCtaThreads], red[32];
+  __shared__ int s_flags[2];
+  if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head, a.pool_span);
+  const LowOrderState& st = a.s;
+  const int I = a.I, N = I + 2, i = threadIdx.x;
+  const FacView F = fac_view(st.fac, I);
+  // ---- every global load of row i, issued before any is used
+  double al[kFacLevels], ga[kFacLevels];
+#pragma unroll
+  for (int l = 0; l < kFacLevels; ++l) {
+    al[l] = i < N ? F.al[(size_t)l * N + i] : 0.0;
+    ga[l] = i < N ? F.ga[(size_t)l * N + i] : 0.0;
+  }
+  const bool row = i < N, mrow = i <= I;
+  const double tau_b = row ? F.tau_b[i] : 0.0, remdx_b = row ? F.remdx_b[i] : 0.0;
+  const double lo_b = row ? F.lo_b[i] : 0.0, up_b = row ? F.up_b[i] : 0.0;
+  const double dfin = row ? F.dfin[i] : 1.0;
+  const double tau_m = mrow ? F.tau_m[i] : 0.0, sdx_m = mrow ? F.sdx_m[i] : 0.0;
+  const double inv_m = mrow ? F.inv_m[i] : 0.0;
+  const double phi_i = row ? st.phi_prev[i] : 0.0, phi_n = mrow ? st.phi_prev[i + 1] : 0.0;
+  const double J_i = mrow ? st.J_prev[i] : 0.0;
+  const double J_p = (row && i >= 1 && i <= I) ? st.J_prev[i - 1] : 0.0;
+  const double Fp_i = row ? st.F_prev[i] : 0.0, Fp_n = mrow ? st.F_prev[i + 1] : 0.0;
+  const double qi = (a.q && i >= 1 && i <= I) ? a.q[i - 1] : 0.0;
+  const double Fs_i = mrow ? snap_filtered(a, i) : 0.0, Fs_n = mrow ? snap_filtered(a, i + 1) : 0.0;
+  const double PLs = a.bclosure_tally[0] * a.snapshot_inv_norm;
+  const double PRs = a.bclosure_tally[1] * a.snapshot_inv_norm;
+  const double fac_bad = *F.bad;
+  // check_inputs (losm.cpp:43-66): finite lagged state and closures
+  bool bad_in = false;
+  if (row && (!isfinite(phi_i) || !isfinite(Fp_i))) bad_in = true;
+  if (i <= I && !isfinite(J_i)) bad_in = true;
+  // ---- Schur right-hand side (solve_cached)
+  double rb = 0.0, rm = 0.0;
+  if (row) {
+    if (i == 0) rb = 2.0 * 0.0 + PLs;
+    else if (i == N - 1) rb = 2.0 * 0.0 - PRs;
+    else
+      rb = tau_b * phi_i + a.theta * qi +
+           (a.theta - 1.0) * (J_i - J_p + remdx_b * phi_i - qi);
+    if (mrow) {
+      rm = tau_m * J_i + a.theta * (Fs_n - Fs_i) +
+           (a.theta - 1.0) * ((phi_n - phi_i) / 3.0 + sdx_m * J_i - (Fp_n - Fp_i));
+      P[i] = rm * inv_m;
+    }
+  }
+  const int any_bad = __syncthreads_or(bad_in ? 1 : 0);
+  const int status = any_bad ? 1 : (fac_bad == 2.0 ? 1 : (fac_bad != 0.0 ? 2 : 0));
+  if (status == 0) {
+    if (row) {
+      double r = rb;
+      if (i > 0) r -= lo_b * P[i - 1];
+      if (i < N - 1) r -= up_b * P[i];
+      R0[i] = r;
+    }
+    __syncthreads();
+    double* Rc = R0;
+    double* Rn = R1;
+#pragma unroll
+    for (int lv = 0; lv < kFacLevels; ++lv) {
+      const int sft = 1 << lv;
+      if (sft >= N) break;
+      if (row) {
+        double r = Rc[i];
+        if (i - sft >= 0) r += al[lv] * Rc[i - sft];
+        if (i + sft < N) r += ga[lv] * Rc[i + sft];
+        Rn[i] = r;
+      }
+      __syncthreads();
+      double* t = Rc;
+      Rc = Rn;
+      Rn = t;
+    }
+    // phi_hybrid = interior phi (driver.cpp:80), then build_centers (ww.cpp:8-32)
+    const double phi = row ? Rc[i] / dfin : 0.0;
+    const bool cell = i >= 1 && i <= I;
+    const double mx = block_max(cell && phi > 0.0 ? phi : 0.0, red);
+    const bool fallback = !(mx > 0.0) || !isfinite(mx);
+    if (cell) {
+      st.phi_hybrid[i - 1] = phi;
+      const double cl = phi > 0.0 ? phi : 0.0;
+      st.centers[i - 1] = fallback ? 1.0 : (cl / mx) * (1.0 - a.eps_min) + a.eps_min;
+    }
+    if (i == 0) {
+      st.flags[0] = 1;
+      st.flags[1] = 1;
+      ++st.flags[2];
+      st.flags[4] = 0;
+    }
+  } else {  // keep the previous windows (driver.cpp:84-94)
+    if (i == 0) s_flags[0] = st.flags[0];
+    __syncthreads();
+    if (!s_flags[0])
+      for (int c = i; c < I; c += blockDim.x) st.centers[c] = 1.0;
+    if (i == 0) {
+      st.flags[0] = 1;
+      st.flags[3] = 1;
+      st.flags[4] = status;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kCtaThreads) k_raw_losm(RawLosmArgs a) {
   const int I = a.I, n = 2 * I + 3;
   double* lo = a.sys;
@@ -1445,7 +1576,22 @@ size_t lo_fac_words(int I) { return I + 2 <= 512 ? fac_words_for(I) : 0; }
 void launch_low_order_update(const LowOrderArgs& a_in, cudaStream_t st) {
   LowOrderArgs a = a_in;
   static const bool dbg = std::getenv("HWWG_LOSM_DEBUG") != nullptr;
+  static const bool general = std::getenv("HWWG_LOSM_GENERAL") != nullptr;  // tests
   a.debug = dbg ? 1 : 0;
+  if (a.mode == 1 && a.fast_solve && a.s.fac && !a.refactor && !a.fourier_tab_cell &&
+      a.I + 2 <= kCtaThreads && a.I + 2 <= (1 << kFacLevels) && !dbg && !general) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(kCtaThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HWWG_CUDA(cudaLaunchKernelEx(&cfg, k_losm_mid_fast, a));
+    return;
+  }
   size_t smem = a.fast_solve ? (size_t)4 * (a.I + 2) * sizeof(double) : 0;
   a.smem_state = a.I <= kSmemStateMaxI ? 1 : 0;
   if (a.smem_state)
