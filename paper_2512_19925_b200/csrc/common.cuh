@@ -24,9 +24,9 @@
 
 namespace hwwg {
 
-struct CellInfo {  // 64 B: one cache sector pair per cell
+struct CellInfo {
   double sigma_t, sigma_s, sigma_f, nu_f, speed, inv_dx;
-  double inv_sigma_t, inv_speed;  // throughput mode only (exact mode divides)
+  double inv_sigma_t, inv_speed, inv_sigma_s;  // throughput mode only (exact mode divides)
 };
 
 // Views into the device tally slab (== hww::TallySet, tally.hpp:16-45).

@@ -107,7 +107,8 @@ struct DeviceProblem {
     for (int c = 0; c < cells; ++c)
       cells_h[c] = CellInfo{mats[c].sigma_t, mats[c].sigma_s, mats[c].sigma_f,
                             mats[c].nu_f,    mats[c].speed,   1.0 / widths[c],
-                            1.0 / mats[c].sigma_t, 1.0 / mats[c].speed};
+                            1.0 / mats[c].sigma_t, 1.0 / mats[c].speed,
+                            mats[c].sigma_s > 0.0 ? 1.0 / mats[c].sigma_s : 0.0};
     d_edges.reserve(cells + 1);
     d_cells.reserve(cells);
     HWWG_CUDA(cudaMemcpyAsync(d_edges.p, edges.data(), sizeof(double) * (cells + 1),

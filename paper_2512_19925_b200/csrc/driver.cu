@@ -1099,6 +1099,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.step = (unsigned)step;
         fa.H = H;
         fa.B = B;
+        fa.bmul = H ? (double)B / (double)H : 0.0;
         fa.centers = ea.centers;
         fa.active = ea.active;
         fa.rho = c.rho;

@@ -65,6 +65,7 @@ struct FastArgs {
   unsigned k0, k1, step;  // Philox key (seed) and step
   uint64_t H;
   int B;
+  double bmul;  // B / H (batch_of without a division)
   int b_lo, nb;  // batches touched by this segment: [b_lo, b_lo + nb)
   int smem_tallies;  // 0 global REDs, 1 shared-memory tallies, 2 fp64 global + counts shared
   int aggregate;     // 1: warp-aggregate tally atomics (cold start: lanes share cells)
@@ -144,7 +145,7 @@ size_t fast_smem_bytes(int I, int nb);
 size_t fast_smem_count_bytes(int I);  // smem_tallies == 2: the track counts only
 size_t fast_smem_fix_bytes(int I, int nb);  // smem_tallies == 1 with fixed-point track/edge slots
 bool fast_fix_exponent(double vmax, int* k);  // grid exponent for the largest expected score
-size_t fast_smem_centers_bytes(int I);  // window centres (after the tallies)
+size_t fast_smem_centers_bytes(int I);  // window centres and mesh edges (after the tallies)
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s);
 void launch_aos_to_fast(const hwwg_particle* in, uint64_t n, const MeshView& m, FastBank out,
                         uint64_t hist0, cudaStream_t s);

@@ -41,6 +41,7 @@
 
 #include "common.cuh"
 #include "fast.cuh"
+#include "libm_log_table.h"
 #include "rng.cuh"
 
 namespace hwwg {
@@ -149,11 +150,41 @@ __device__ __forceinline__ void draw3(const FastArgs& a, Lane& p, double& u0, do
   philox_uniform3(philox4x32_10(c, a.k0, a.k1), u0, u1, u2);
 }
 
-// tally.hpp:130-134 batch_of, by one fp64 division: exact while h * B < 2^53
-// (then floor of the correctly rounded quotient is the integer quotient)
-__device__ __forceinline__ int batch_fast(unsigned h, double H, int B) {
-  const int b = (int)(((double)h * (double)B) / H);
+// tally.hpp:130-134 batch_of = floor(h B / H): an fp64 estimate from the
+// precomputed B / H, corrected by one integer comparison (the estimate is off
+// by at most one; no division)
+__device__ __forceinline__ int batch_fast(unsigned h, unsigned long long H, int B, double bmul) {
+  const unsigned long long hb = (unsigned long long)h * (unsigned)B;
+  int b = (int)((double)h * bmul);
+  if ((unsigned long long)(b + 1) * H <= hb) ++b;
+  else if (b > 0 && (unsigned long long)b * H > hb) --b;
   return b < B ? b : B - 1;
+}
+
+__constant__ double c_logtab[256] = HWWG_LOG_TAB;
+
+// -ln(u) for a deviate u in (0, 1) (the flight distance in mean free paths):
+// the table-driven algorithm of libm_log.h (k ln2 + log c + log1p(r), 128-entry
+// (1/c, log c) table from the installed libm, degree-6 polynomial) with the
+// table in shared memory and no special-case paths (u is normal and below 1).
+// Near u = 1 the near-1 branch the exact replay keeps is dropped: the absolute
+// error stays ~1e-17 (a distance of 1e-17 mean free paths), which no estimator
+// can see; the exact mode keeps the bit-exact replay.
+__device__ __forceinline__ double neg_log_unit(double u, const double* __restrict__ T) {
+  const double A[5] = HWWG_LOG_A;
+  const unsigned long long ix = (unsigned long long)__double_as_longlong(u);
+  const unsigned long long tmp = ix - 0x3fe6000000000000ULL;
+  const int i = (int)((tmp >> 45) & 127u);
+  const int k = (int)((long long)tmp >> 52);
+  const double z = __longlong_as_double((long long)(ix - (tmp & (0xfffULL << 52))));
+  const double invc = T[2 * i], logc = T[2 * i + 1];
+  const double kd = (double)k;
+  const double w = fma(kd, HWWG_LOG_LN2HI, logc);
+  const double r = fma(z, invc, -1.0);
+  const double r2 = r * r;
+  const double p = fma(fma(r, A[4], A[3]), r2, fma(r, A[2], A[1]));
+  const double lo = fma(r2, A[0], fma(kd, HWWG_LOG_LN2LO, (w - (r + w)) + r));
+  return -((r + w) + fma(r2 * r, p, lo));
 }
 
 // split records carry the parent's cell | batch slot << 16 (daughters keep the
@@ -452,7 +483,6 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   unsigned pend = 0;  // daughters pending in the local stack (warp-uniform)
   bool src_done = false;
   const int I = a.mesh.I;
-  const double Hd = (double)a.H;
   const double* __restrict__ edges = a.mesh.edges;
   const CellInfo* __restrict__ cells = a.mesh.cells;
   const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
@@ -480,6 +510,11 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   double* s_cent = smem + tally_words;  // read at every window site: keep it on chip
   if (windows)
     for (int i = threadIdx.x; i < I; i += blockDim.x) s_cent[i] = a.centers[i];
+  // mesh edges (read at every event) and the log table, on chip
+  double* s_edge = s_cent + I;
+  for (int e = threadIdx.x; e <= I; e += blockDim.x) s_edge[e] = edges[e];
+  __shared__ double s_logtab[256];
+  for (int j = threadIdx.x; j < 256; j += blockDim.x) s_logtab[j] = c_logtab[j];
   __syncthreads();
   if (a.span && threadIdx.x == 0) atomicMin(&a.span[0], globaltimer());
   // per-lane event counters: 32 bits is plenty within one launch (registers
@@ -685,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           p.hist = m.y;
           p.key = ((unsigned long long)m.w << 32) | m.z;
           p.inv_mu = 1.0 / p.mu;
-          p.bslot = batch_fast(p.hist, Hd, a.B) - (shf ? a.b_lo : 0);
+          p.bslot = batch_fast(p.hist, a.H, a.B, a.bmul) - (shf ? a.b_lo : 0);
           p.alive = p.w > 0.0;
           p.fis = false;
         }
@@ -794,10 +829,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
     if (p.alive) {
       const CellInfo ci = kUniform ? a.cell0 : cells[p.cell];
       // edge position: the host table, or the same x_min + e*w (unfused) in registers
-      auto edge_x = [&](int e) {
-        if (!kUniform) return edges[e];
-        return e == I ? a.x_max : __dadd_rn(a.x_min, __dmul_rn((double)e, a.w_gen));
-      };
+      auto edge_x = [&](int e) { return s_edge[e]; };
       double u0, u1, u2;
       draw3(a, p, u0, u1, u2);
       bool window_site = false;
@@ -808,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         window_site = true;
       } else {
         const double d_census = ci.speed * (a.t_end - p.t);
-        const double d_coll = -log(u0) * ci.inv_sigma_t;
+        const double d_coll = neg_log_unit(u0, s_logtab) * ci.inv_sigma_t;
         double d_b = __longlong_as_double(0x7ff0000000000000LL);
         int edge = -1;
         if (p.mu > 0.0) {
@@ -871,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
           if (xi < ci.sigma_s) {
             p.mu = 2.0 * u2 - 1.0;
             p.inv_mu = 1.0 / p.mu;
-            u1 = xi / ci.sigma_s;  // recycled roulette deviate for the window game below
+            u1 = xi * ci.inv_sigma_s;  // recycled roulette deviate for the window game below
             window_site = true;
           } else if (xi < ci.sigma_s + ci.sigma_f) {
             // fission (transport.cpp:29-40, 179-188): floor(nu) + Bernoulli(frac)
@@ -1283,7 +1315,7 @@ bool fast_fix_exponent(double vmax, int* k) {
   *k = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
   return true;
 }
-size_t fast_smem_centers_bytes(int I) { return (size_t)I * 8; }
+size_t fast_smem_centers_bytes(int I) { return (size_t)(2 * I + 1) * 8; }  // centres + edges
 size_t fast_flush_stride(int I, int B) { return (size_t)(B + 4) * I + 1 + B + 2 + I; }
 
 int fast_threads_per_block() { return kThreads; }
