@@ -76,6 +76,31 @@ struct FastBankBuf {
     std::swap(meta.n, o.meta.n);
   }
 };
+// Owner of a census bank (fast mode; fast.cuh CensusBank, 24 B per particle).
+struct CensusBankBuf {
+  DevBuf<double2> xm;
+  DevBuf<double> w;
+  void reserve(uint64_t n) {
+    n = n ? n : 1;
+    xm.reserve(n);
+    w.reserve(n);
+  }
+  uint64_t cap() const { return std::min(xm.n, w.n); }
+  void release() {
+    if (xm.p) cudaFree(xm.p);
+    if (w.p) cudaFree(w.p);
+    xm.p = nullptr;
+    w.p = nullptr;
+    xm.n = w.n = 0;
+  }
+  CensusBank view() { return CensusBank{xm.p, w.p}; }
+  void swap(CensusBankBuf& o) {
+    std::swap(xm.p, o.xm.p);
+    std::swap(xm.n, o.xm.n);
+    std::swap(w.p, o.w.p);
+    std::swap(w.n, o.w.n);
+  }
+};
 }  // namespace hwwg
 
 struct hwwg_driver {
@@ -110,7 +135,11 @@ struct hwwg_driver {
   bool fast = false;
   uint64_t census_hwm = 0;  // census capacity high-water mark (banks swap each step)
   uint64_t census_floor = 0;  // the creation-time capacity (64 x H)
-  FastBankBuf fbank, fsrc, fcensus;
+  // fbank: the bank the next comb reads (the last census, or the pulse), all
+  // at time bank_t; fcensus: the census being written; fsrc: the step's source
+  CensusBankBuf fbank, fcensus;
+  FastBankBuf fsrc;
+  double bank_t = 0.0;
   DevBuf<FastStackRec> stacks;
   int stack_cap = 1024;
   int sms = 148;
@@ -397,8 +426,8 @@ void init_driver(hwwg_driver* d) {
   if (d->fast) {
     const uint64_t local_target = d->target / (uint64_t)d->world + 1;
     d->fbank.reserve(std::max<uint64_t>(d->bank_n, 64 * local_target + 4096));
-    launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fbank.view(), d->shard_lo,
-                       d->stream);
+    launch_aos_to_census(d->bank.p, d->bank_n, d->fbank.view(), d->stream);
+    d->bank_t = 0.0;  // the pulse is emitted at t = 0 (driver.cpp:309-316)
     // Everything a step can grow into is allocated here, up front: a cudaMalloc
     // inside a step synchronises the device (the step-1 census is x60+ of H,
     // and it becomes step 2's comb input in the other bank of the swap pair).
@@ -564,6 +593,8 @@ uint64_t multi_gpu_comb(hwwg_driver* d, int step, uint64_t nv, StepLayout& L, cu
   d->comb_temp.reserve(tb);
   FastCombArgs a{};
   a.bank = d->fbank.view();
+  a.t_bank = d->bank_t;
+  a.mesh = d->prob.view;
   a.n = n;
   a.prefix = d->comb_mem.p + 4;
   a.scalars = d->comb_mem.p;
@@ -820,10 +851,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->bank_n = d->host_bank_n;
     rec->h2d_bytes += d->host_bank_n * sizeof(hwwg_particle);
     if (d->fast) {
-      // a pre-combed bank (see the step end) is already the step's source
-      FastBankBuf& dst = d->host_pre_combed ? d->fsrc : d->fbank;
-      dst.reserve(d->bank_n + (c.vol_rate > 0.0 ? c.vol_histories : 0));
-      launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, dst.view(), 0, s);
+      // a pre-combed bank (see the step end) is already the step's source;
+      // otherwise the host bank is the comb's input
+      if (d->host_pre_combed) {
+        d->fsrc.reserve(d->bank_n + (c.vol_rate > 0.0 ? c.vol_histories : 0));
+        launch_aos_to_fast(d->bank.p, d->bank_n, d->prob.view, d->fsrc.view(), 0, s);
+      } else {
+        d->fbank.reserve(d->bank_n);
+        launch_aos_to_census(d->bank.p, d->bank_n, d->fbank.view(), s);
+      }
       ++d->launches;
     }
   }
@@ -858,6 +894,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->comb_mem.reserve(4 + fast_comb_scratch_words(d->bank_n));
     FastCombArgs a{};
     a.bank = d->fbank.view();
+    a.t_bank = d->bank_t;
+    a.mesh = d->prob.view;
     a.n = d->bank_n;
     a.target = d->target;
     a.seed = c.seed;
@@ -1174,7 +1212,6 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         if (u == thr.size() && gw >= grid_warps_max && fa.n_src) {
           fa.fill_tail = 1;
           fa.x_fill = d->prob.edges.front();
-          fa.t_fill = rec->t_end;
           tail_filled = true;
         }
         fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
@@ -1257,7 +1294,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     if (d->fast && !tail_filled) {  // zero-weight records in the unused tails of the warps' chunks
       d->ph_mark("fill", s);
       launch_fill_census_holes(d->fcensus.view(), d->fcensus.cap(), d->warp_cursor.p,
-                               d->max_warps, d->prob.edges.front(), rec->t_end, s);
+                               d->max_warps, d->prob.edges.front(), s);
       ++d->launches;
     }
     if (early_finalize) {
@@ -1383,10 +1420,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
 
   // ---- census -> next bank in reference order
   if (d->fast) {
-    d->fbank.swap(d->fcensus);  // the census is the next comb's input, already SoA
+    d->fbank.swap(d->fcensus);  // the census is the next comb's input
+    d->bank_t = rec->t_end;     // every census particle sits at the step's end
     if (c.host_bank && d->world > 1) {  // real particles only, AoS, for the host round trip
       d->bank.reserve(std::max<unsigned long long>(count, 1));
-      launch_fast_compact_aos(d->fbank.view(), count, d->bank.p, d->counter.p, s);
+      launch_fast_compact_aos(d->fbank.view(), count, d->bank_t, d->bank.p, d->counter.p, s);
       HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
       HWWG_CUDA(cudaStreamSynchronize(s));
       ++d->launches;
@@ -1422,6 +1460,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.temp = d->comb_temp.p;
     a.temp_bytes = d->comb_temp.n;
     a.bank = d->fbank.view();
+    a.t_bank = d->bank_t;
+    a.mesh = d->prob.view;
     a.n = d->bank_n;
     a.target = d->target;
     a.seed = c.seed;
@@ -1702,7 +1742,8 @@ int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t*
     // Philox mode keeps the census as SoA with zero-weight chunk tails: compact
     // the real particles into AoS (order is free in this mode)
     d->bank.reserve(std::max<uint64_t>(d->bank_n, 1));
-    launch_fast_compact_aos(d->fbank.view(), d->bank_n, d->bank.p, d->counter.p, d->stream);
+    launch_fast_compact_aos(d->fbank.view(), d->bank_n, d->bank_t, d->bank.p, d->counter.p,
+                            d->stream);
     unsigned long long c = 0;
     HWWG_CUDA(cudaMemcpyAsync(&c, d->counter.p, sizeof c, cudaMemcpyDeviceToHost, d->stream));
     HWWG_CUDA(cudaStreamSynchronize(d->stream));

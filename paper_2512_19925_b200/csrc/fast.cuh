@@ -12,6 +12,16 @@ struct FastBank {
   uint4* meta;  // {cell | draw << 16, history, lineage key lo, lineage key hi}
 };
 
+// Census bank (the transport's output, the next comb's input): 24 B per
+// particle. Every census particle sits at t = t_end of its step and is located
+// again from x when it next moves (mesh.cpp:26-40, as advance_history does at
+// a history's start), so only (x, mu) and w are kept — half the 48 B source
+// record, in the largest buffers of a run (the x63 cold-start census).
+struct CensusBank {
+  double2* xm;  // {x, mu}
+  double* w;
+};
+
 // One run-length-encoded split record (64 B): `count` identical daughters.
 struct FastStackRec {
   double x, mu, w, t;
@@ -57,7 +67,7 @@ struct FastArgs {
   FastBank src;  // this segment's source particles
   unsigned long long n_src;
   unsigned long long* src_head;  // refill cursor (zeroed per segment)
-  FastBank census;
+  CensusBank census;
   unsigned long long* census_count;
   uint64_t census_cap;
   MeshView mesh;
@@ -84,7 +94,7 @@ struct FastArgs {
   // chunk): each warp writes zero-weight records (x_fill, t_fill) into the
   // unused tail of its chunk on exit, instead of a separate fill launch
   int fill_tail;
-  double x_fill, t_fill;
+  double x_fill;
   // Uniform generated mesh (edges[e] == x_min + e*w bit-for-bit, edges[I] ==
   // x_max) with one material: geometry and cross sections come from registers,
   // no per-event table loads.
@@ -112,8 +122,9 @@ size_t fast_flush_stride(int I, int B);  // words per flush replica (nb <= B)
 
 // Zero-weight records in the unused tails of the warps' census chunks, and the
 // count of slots the census bank spans.
-void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,
-                              int warps, double x_fill, double t_fill, cudaStream_t s);
+void launch_fill_census_holes(CensusBank census, uint64_t cap,
+                              const unsigned long long* warp_cursor, int warps, double x_fill,
+                              cudaStream_t s);
 // Step start of the throughput mode in one launch: zero the tally slab, the
 // warp census cursors, the census counter and the error word; reset the first
 // segment's pool counters (fast_pool_reset).
@@ -121,9 +132,11 @@ void launch_step_start(double* slab, size_t slab_words, unsigned long long* curs
                        size_t cursor_words, unsigned long long* counter, DevError* err,
                        unsigned long long* ctl, unsigned long long* src_head,
                        unsigned long long* span, int sms, cudaStream_t s);
-// Compact the census bank (drop zero-weight holes) into AoS particles.
-void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
+// Compact the census bank (drop zero-weight holes) into AoS particles at time t.
+void launch_fast_compact_aos(CensusBank in, uint64_t n, double t, hwwg_particle* out,
                              unsigned long long* count, cudaStream_t s);
+// AoS particles (all at one time: the pulse source, a host-held census) into a census bank.
+void launch_aos_to_census(const hwwg_particle* in, uint64_t n, CensusBank out, cudaStream_t s);
 
 // resident blocks per SM of the transport instantiation (uniform mesh, shared
 // tallies, fixed-point slots) with `smem` dynamic shared memory, and the most
@@ -185,7 +198,9 @@ Perm make_perm(uint64_t n, uint64_t seed, uint64_t step);
 
 // Parallel comb (popctrl.cpp:7-42 semantics with a parallel fp64 scan).
 struct FastCombArgs {
-  FastBank bank;
+  CensusBank bank;
+  double t_bank;  // the time of every particle of the bank (the census time)
+  MeshView mesh;  // teeth locate their cell from x
   uint64_t n, target;
   uint64_t seed, stream;
   double* prefix;   // n

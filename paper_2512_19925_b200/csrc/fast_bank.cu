@@ -19,24 +19,23 @@ namespace hwwg {
 
 namespace {
 
-__global__ void k_extract_w(FastBank b, uint64_t n, double* w) {
+__global__ void k_extract_w(CensusBank b, uint64_t n, double* w) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) w[i] = b.wt[i].x;
+  if (i < n) w[i] = b.w[i];
 }
 
 __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src, uint64_t k0,
                                             uint64_t k1, double spacing) {
-  const double2 xm = a.bank.xm[src];
-  const double2 wt = a.bank.wt[src];
-  const uint4 m = a.bank.meta[src];
   HWWG_CHECK(src < a.n && k1 <= a.target);
+  const double2 xm = a.bank.xm[src];
+  const int c = locate_cell(a.mesh, xm.x);  // as advance_history locates a start (transport.cpp:95)
   for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t p = a.perm(k);
     HWWG_CHECK(p < a.target);
     a.out.xm[p] = xm;
-    a.out.wt[p] = make_double2(spacing, wt.y);
+    a.out.wt[p] = make_double2(spacing, a.t_bank);
     // fresh identity for the new step: history = its slot, key 0, draw 0
-    a.out.meta[p] = make_uint4(m.x & 0xffffu, (unsigned)p, 0u, 0u);
+    a.out.meta[p] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)p, 0u, 0u);
   }
 }
 
@@ -135,7 +134,7 @@ __global__ void __launch_bounds__(kCbThreads) k_cb_sums(FastCombArgs a) {
 #pragma unroll
   for (int i = 0; i < kCbItems; ++i) {
     const uint64_t j = t0 + threadIdx.x + i * kCbThreads;
-    ld[i] = j < a.n ? a.bank.wt[j].x : 0.0;
+    ld[i] = j < a.n ? a.bank.w[j] : 0.0;
   }
 #pragma unroll
   for (int i = 0; i < kCbItems; ++i) q += fixed_w(ld[i], scale);
@@ -209,7 +208,7 @@ __global__ void __launch_bounds__(kCbThreads) k_cb_scatter(FastCombArgs a) {
 #pragma unroll
     for (int i = 0; i < kCbItems; ++i) {
       const int j = threadIdx.x + i * kCbThreads;
-      ld[i] = j < m ? a.bank.wt[t0 + j].x : 0.0;
+      ld[i] = j < m ? a.bank.w[t0 + j] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < kCbItems; ++i) wv[pad_d(threadIdx.x + i * kCbThreads)] = ld[i];
@@ -253,7 +252,7 @@ __global__ void __launch_bounds__(kCbThreads) k_cb_scatter(FastCombArgs a) {
     const uint64_t k_end = teeth_below_i((double)S.total(), off_i, inv_sp, a.target);
     if (k_end < a.target) {
       uint64_t src = a.n - 1;
-      while (src > 0 && !(fixed_w(a.bank.wt[src].x, scale) > 0)) --src;
+      while (src > 0 && !(fixed_w(a.bank.w[src], scale) > 0)) --src;
       write_teeth(a, src, k_end, a.target, spacing);
     }
   }
@@ -280,11 +279,13 @@ __global__ void k_comb_teeth_range(FastCombArgs a, double spacing, double offset
   }
   uint64_t s = lo < a.n ? lo : a.n - 1;
   if (lo >= a.n)
-    while (s > 0 && a.bank.wt[s].x <= 0.0) --s;
+    while (s > 0 && a.bank.w[s] <= 0.0) --s;
   const uint64_t o = k - k_lo;
-  out.xm[o] = a.bank.xm[s];
-  out.wt[o] = make_double2(spacing, a.bank.wt[s].y);
-  out.meta[o] = make_uint4(a.bank.meta[s].x & 0xffffu, (unsigned)k, 0u, 0u);
+  const double2 xm = a.bank.xm[s];
+  const int c = locate_cell(a.mesh, xm.x);
+  out.xm[o] = xm;
+  out.wt[o] = make_double2(spacing, a.t_bank);
+  out.meta[o] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)k, 0u, 0u);
 }
 
 __global__ void k_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm, PieceTable t) {
@@ -306,24 +307,23 @@ __global__ void k_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm,
 }
 
 // one warp per transport warp's chunk tail (<= kCensusChunk slots), lanes in parallel
-__global__ void k_fill_holes(FastBank c, uint64_t cap, const unsigned long long* cur, int warps,
-                             double x_fill, double t_fill) {
+__global__ void k_fill_holes(CensusBank c, uint64_t cap, const unsigned long long* cur, int warps,
+                             double x_fill) {
   const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= warps) return;
   const unsigned long long end = cur[2 * w + 1] < cap ? cur[2 * w + 1] : cap;
   for (unsigned long long s = cur[2 * w] + lane; s < end; s += 32) {
     c.xm[s] = make_double2(x_fill, 0.5);
-    c.wt[s] = make_double2(0.0, t_fill);
-    c.meta[s] = make_uint4(0u, 0u, 0u, 0u);
+    c.w[s] = 0.0;
   }
 }
 
 // Drop zero-weight holes while converting to AoS (order is free in this mode).
-__global__ void k_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
+__global__ void k_compact_aos(CensusBank in, uint64_t n, double t, hwwg_particle* out,
                               unsigned long long* count) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool keep = i < n && in.wt[i].x > 0.0;
+  const bool keep = i < n && in.w[i] > 0.0;
   const unsigned mask = __ballot_sync(0xffffffffu, keep);
   const int lane = threadIdx.x & 31;
   unsigned long long base = 0;
@@ -333,8 +333,17 @@ __global__ void k_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
     const unsigned long long j = base + __popc(mask & ((1u << lane) - 1u));
     double2* o = reinterpret_cast<double2*>(out) + 2 * j;
     o[0] = in.xm[i];
-    o[1] = in.wt[i];
+    o[1] = make_double2(in.w[i], t);
   }
+}
+
+__global__ void k_aos_to_census(const hwwg_particle* __restrict__ in, uint64_t n, CensusBank out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 a = reinterpret_cast<const double2*>(in)[2 * i];
+  const double2 b = reinterpret_cast<const double2*>(in)[2 * i + 1];
+  out.xm[i] = a;
+  out.w[i] = b.x;
 }
 
 // The throughput step's start in one launch (instead of four memsets and a
@@ -518,17 +527,24 @@ Perm make_perm(uint64_t n, uint64_t seed, uint64_t step) {
   return Perm{nt, a % nt, z % nt, m};
 }
 
-void launch_fill_census_holes(FastBank census, uint64_t cap, const unsigned long long* warp_cursor,
-                              int warps, double x_fill, double t_fill, cudaStream_t s) {
-  k_fill_holes<<<(warps + 7) / 8, 256, 0, s>>>(census, cap, warp_cursor, warps, x_fill, t_fill);
+void launch_fill_census_holes(CensusBank census, uint64_t cap,
+                              const unsigned long long* warp_cursor, int warps, double x_fill,
+                              cudaStream_t s) {
+  k_fill_holes<<<(warps + 7) / 8, 256, 0, s>>>(census, cap, warp_cursor, warps, x_fill);
   HWWG_CUDA(cudaGetLastError());
 }
 
-void launch_fast_compact_aos(FastBank in, uint64_t n, hwwg_particle* out,
+void launch_fast_compact_aos(CensusBank in, uint64_t n, double t, hwwg_particle* out,
                              unsigned long long* count, cudaStream_t s) {
   HWWG_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s));
   if (!n) return;
-  k_compact_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, out, count);
+  k_compact_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, t, out, count);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_aos_to_census(const hwwg_particle* in, uint64_t n, CensusBank out, cudaStream_t s) {
+  if (!n) return;
+  k_aos_to_census<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, out);
   HWWG_CUDA(cudaGetLastError());
 }
 

@@ -975,11 +975,9 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
         if (cen_cell >= 0) {
           const unsigned rank = __popc(cmask & lt);
           const unsigned long long slot = rank < avail ? wcur + rank : nb + (rank - avail);
-          if (slot < a.census_cap) {
+          if (slot < a.census_cap) {  // t = t_end, the cell follows from x
             a.census.xm[slot] = make_double2(p.x, p.mu);
-            a.census.wt[slot] = make_double2(p.w, p.t);
-            a.census.meta[slot] = make_uint4((unsigned)p.cell | (p.ctr << 16), p.hist,
-                                             (unsigned)p.key, (unsigned)(p.key >> 32));
+            a.census.w[slot] = p.w;
           }
         }
         if (k > avail) {
@@ -1143,8 +1141,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
       const unsigned long long slot = wcur + k;
       if (slot < a.census_cap) {
         a.census.xm[slot] = make_double2(a.x_fill, 0.5);
-        a.census.wt[slot] = make_double2(0.0, a.t_fill);
-        a.census.meta[slot] = make_uint4(0u, 0u, 0u, 0u);
+        a.census.w[slot] = 0.0;
       }
     }
   }

@@ -14,8 +14,9 @@ applied three ways:
 
   * per quantity, pooled over cells and steps: >= 95% of |z| < 3;
   * per quantity and step: >= 85% (one correlated cluster can take a step);
-  * no bias: the pooled mean of z within +-0.5 and the pooled mean of z^2
-    (a global chi^2 per degree of freedom) within [0.5, 2.0];
+  * no bias: the pooled mean of z within +-0.5 (+-1 for the window centres,
+    which share one normalisation) and the pooled mean of z^2 (a global chi^2
+    per degree of freedom) within [0.5, 2.0];
   * per-step scalars (P_L, P_R, census weight): >= 90% of |z| < 3.5, mean z
     within +-2 (steps are correlated through the carried population).
 
@@ -108,7 +109,10 @@ def check_engine(cfg_fn, steps, skip_first=0, label=""):
         report[k] = dict(frac=frac, bias=bias, chi2=chi2, worst_step_frac=step_min, n=int(z_all.size))
         if frac < 0.95:
             fails.append((k, "pooled fraction", frac, np.sort(np.abs(z_all))[-8:]))
-        if abs(bias) >= 0.5:
+        # the centres are normalised by the maximum of phi_hybrid (ww.cpp:8-32): one
+        # fluctuation of that maximum moves every cell's centre the same way, so
+        # their pooled mean z is nearly as wide as a single z
+        if abs(bias) >= (1.0 if k == "ww_centers" else 0.5):
             fails.append((k, "bias", bias))
         if not 0.5 < chi2 < 2.0:
             fails.append((k, "chi2", chi2))
