@@ -158,6 +158,7 @@ struct hwwg_driver {
   // pulse strength, the volumetric source's particle weight)
   int fix_tallies = 1;
   int pdl = 1;  // programmatic dependent launches across segment boundaries (HWWG_PDL)
+  int block_warps = 0;  // transport block shape: 0 per launch, else 12 or 24 (HWWG_FAST_BLOCK_WARPS)
   // transport_ms: exact mode times its segments with CUDA events; the
   // throughput mode with in-kernel launch spans (FastArgs::span), because
   // events between its segment kernels cost 4% (HWWG_SEG_EVENTS=1 restores them)
@@ -448,7 +449,7 @@ void init_driver(hwwg_driver* d) {
       d->fperm.reserve(local_target + 4096);  // the rebalanced teeth before their permutation
     }
     HWWG_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->opt.device));
-    const int warps = d->sms * fast_max_blocks_per_sm() * (fast_threads_per_block() / 32);
+    const int warps = d->sms * fast_max_warps_per_sm();
     d->max_warps = warps;
     d->warp_cursor.reserve((size_t)kWarpCursorWords * warps);
     d->stacks.reserve((size_t)warps * d->stack_cap);
@@ -1178,6 +1179,20 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         // dt for an edge crossing.
         fa.fix = 0;
         const int uni = d->prob.gen_uniform_homog ? 1 : 0;
+        // the block shape with the most resident warps for a tally layout (2 x 12
+        // warps on ties; HWWG_FAST_BLOCK_WARPS forces one)
+        auto shape = [&](size_t sm, int sh, int fx, int& warps) {
+          int best = 0;
+          for (int w : {12, 24}) {
+            if (d->block_warps && w != d->block_warps) continue;
+            const int r = fast_blocks_per_sm(sm, uni, sh, fx, w) * w;
+            if (r > best) {
+              best = r;
+              warps = w;
+            }
+          }
+          return best;
+        };
         if (fa.smem_tallies == 1 && (!fa.aggregate || d->agg_all != 1) && d->flush_replicas == 0 &&
             d->fix_tallies) {
           const size_t fsm = fast_smem_fix_bytes(I, fa.nb) + fast_smem_centers_bytes(I);
@@ -1187,7 +1202,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           for (const CellInfo& ci : d->prob.cells_h) vmin = std::min(vmin, ci.speed * ci.inv_dx);
           const double w = std::max(c.rho, d->step_wref);
           int kt = 0, ke = 0;
-          const int bps = fast_blocks_per_sm(fsm, uni, 1, 1);
+          int wfix = 12, wbase = 12;
+          const int fix_warps = shape(fsm, 1, 1, wfix);
           // dynamic range: the smallest census score (a weight near the lowest
           // window floor eps_min / rho) must keep >= 2^20 grid units, or its
           // rounding would bias low-window cells: beyond 20 binades below the
@@ -1196,7 +1212,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           const bool range_ok = smallest > 0.0 &&
                                 std::ilogb(w * vmax) - std::ilogb(smallest) <= 20;
           if (range_ok && fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
-              bps >= fast_blocks_per_sm(smem, uni, 1, 0)) {
+              fix_warps >= shape(smem, 1, 0, wbase)) {
             fa.fix = 1;
             fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             fa.fix_k_trk = kt;
@@ -1206,15 +1222,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           }
         }
         fa.scramble = fa.aggregate ? 0 : d->scramble;
-        const int blocks = d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fa.fix);
-        const int gw = blocks * (fast_threads_per_block() / 32);
+        int wsel = 12;
+        shape(smem, fa.smem_tallies == 1, fa.fix, wsel);
+        fa.warps = wsel;
+        const int blocks = d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fa.fix, wsel);
+        const int gw = blocks * wsel;
         grid_warps_max = std::max(grid_warps_max, gw);
         if (u == thr.size() && gw >= grid_warps_max && fa.n_src) {
           fa.fill_tail = 1;
           fa.x_fill = d->prob.edges.front();
           tail_filled = true;
         }
-        fa.pool.warps = (unsigned)(blocks * (fast_threads_per_block() / 32));
+        fa.pool.warps = (unsigned)gw;
         fa.warp_cursor = d->warp_cursor.p;
         fa.seg = nseg;
         fa.flush_scratch = d->flush_scratch.p;
@@ -1644,6 +1663,10 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   }
   if (const char* m = std::getenv("HWWG_FAST_FIX")) d->fix_tallies = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
+    const int w = std::atoi(m);
+    d->block_warps = (w == 12 || w == 24) ? w : 0;
+  }
   d->seg_events = d->fast ? (std::getenv("HWWG_SEG_EVENTS") ? 1 : 0) : 1;
   d->span.reserve(64);
   if (const char* m = std::getenv("HWWG_FAST_FLUSH_R")) d->flush_replicas = std::max(0, std::atoi(m));

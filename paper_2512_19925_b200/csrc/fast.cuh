@@ -84,6 +84,7 @@ struct FastArgs {
   // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
   // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
   int fix, fix_k_trk, fix_k_edge;
+  int warps;            // warps per block: 12 (2 blocks per SM) or 24 (1 block per SM)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   int pdl;              // 1: programmatic dependent launch after the previous kernel
   // [first block start, last block end] (globaltimer ns) of this launch, reset
@@ -139,11 +140,10 @@ void launch_fast_compact_aos(CensusBank in, uint64_t n, double t, hwwg_particle*
 void launch_aos_to_census(const hwwg_particle* in, uint64_t n, CensusBank out, cudaStream_t s);
 
 // resident blocks per SM of the transport instantiation (uniform mesh, shared
-// tallies, fixed-point slots) with `smem` dynamic shared memory, and the most
-// any instantiation holds
-int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix);
-int fast_max_blocks_per_sm();
-int fast_threads_per_block();
+// tallies, fixed-point slots, warps per block: 12 or 24) with `smem` dynamic
+// shared memory, and the most warps per SM any instantiation holds
+int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix, int warps);
+int fast_max_warps_per_sm();
 // per-warp census cursor words (FastArgs::warp_cursor: next, end)
 constexpr int kWarpCursorWords = 2;
 // timeline words per warp: {t0, loop trips, t_exit, events} and, in

@@ -48,13 +48,13 @@ namespace hwwg {
 
 namespace {
 
-#ifndef HWWG_FAST_WARPS
-#define HWWG_FAST_WARPS 8  // warps per block (one shared-memory tally set each)
-#endif
-#ifndef HWWG_FAST_MINB
-#define HWWG_FAST_MINB (24 / HWWG_FAST_WARPS)  // resident blocks per SM (register budget)
-#endif
-constexpr int kWarpsPerBlock = HWWG_FAST_WARPS;
+// Two block shapes, both 24 resident warps per SM (the register budget at
+// 80 registers): 2 blocks of 12 warps, or 1 block of 24 warps when the
+// block's shared-memory tallies fit only once per SM (config 3's 1000 cells:
+// 2 blocks of 8 warps before, 16 warps per SM). One shared-memory tally set per
+// block; the driver picks the shape per launch (measured against 3 blocks of
+// 8 warps: C5 77.0 -> 76.2 ms, C3 73.7 -> 41 ms for 20 steps).
+constexpr int kMaxWarpsPerSm = 24;
 
 // -DHWWG_FAST_PROF: per-phase clock64 accounting of the loop (lane 0 of every
 // warp), summed over the grid into g_fprof: [0] refill [1] event [2] census
@@ -80,7 +80,6 @@ __device__ unsigned int g_fhist[8][kHistBins][2];
   do {           \
   } while (0)
 #endif
-constexpr int kThreads = 32 * kWarpsPerBlock;
 #ifndef HWWG_KDONATE
 #define HWWG_KDONATE 256
 #endif
@@ -465,8 +464,8 @@ __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb, int 
 // kShf: the fp64 tallies live in block-private shared memory (smem_tallies ==
 // 1), statically, so the atomics compile to shared-memory CAS loops with no
 // generic-address dispatch.
-template <bool kUniform, bool kShf, bool kFix>
-__global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastArgs a) {
+template <bool kUniform, bool kShf, bool kFix, int kW>
+__global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(FastArgs a) {
   static_assert(kShf || !kFix, "fixed-point tallies live in shared memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
   extern __shared__ double smem[];
@@ -476,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   // per-warp RLE split stack: the bottom kSmemStack records on chip (steady
   // state rarely goes deeper), the rest in global memory
   FastStackRec* stk = a.stacks + (size_t)gwarp * a.stack_cap;
-  __shared__ FastStackRec s_stk[kWarpsPerBlock][kSmemStack];
+  __shared__ FastStackRec s_stk[kW][kSmemStack];
   FastStackRec* s_my = s_stk[threadIdx.x >> 5];
 #define STK(i) (*((i) < kSmemStack ? &s_my[(i)] : &stk[(i)]))
   int sp = 0;
@@ -549,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   // HWWG_CLAIM_ZONE * kClaim particles per warp of the source, so the final reservations do
   // not pin a warp's worth of unstarted histories while other warps idle
   unsigned csz = kClaim;
-  const unsigned tail_zone = gridDim.x * kWarpsPerBlock * kClaim * (unsigned)HWWG_CLAIM_ZONE;
+  const unsigned tail_zone = gridDim.x * kW * kClaim * (unsigned)HWWG_CLAIM_ZONE;
   unsigned long long ticket = ~0ULL;  // lane 0: pool slot this warp waits on
   // The pool counters are reset without knowing this grid (fast_pool_reset:
   // active = kPoolSentinel, source head = 0), so the reset can ride on the
@@ -558,8 +557,8 @@ __global__ void __launch_bounds__(kThreads, HWWG_FAST_MINB) k_fast_segment(FastA
   // the static first reservations.
   if (blockIdx.x == 0 && threadIdx.x == 0)
     atomicAdd(const_cast<unsigned long long*>(&ctl[2]),
-              (unsigned long long)gridDim.x * kWarpsPerBlock - kPoolSentinel);
-  const unsigned claim0 = gridDim.x * kWarpsPerBlock * kClaim;
+              (unsigned long long)gridDim.x * kW - kPoolSentinel);
+  const unsigned claim0 = gridDim.x * kW * kClaim;
 
   FPROF_DECL
 #ifdef HWWG_FAST_PROF
@@ -1315,7 +1314,7 @@ bool fast_fix_exponent(double vmax, int* k) {
 size_t fast_smem_centers_bytes(int I) { return (size_t)(2 * I + 1) * 8; }  // centres + edges
 size_t fast_flush_stride(int I, int B) { return (size_t)(B + 4) * I + 1 + B + 2 + I; }
 
-int fast_threads_per_block() { return kThreads; }
+int fast_max_warps_per_sm() { return kMaxWarpsPerSm; }
 
 // -DHWWG_FAST_PROF builds: read and clear the loop phase accounting (0 otherwise)
 int fast_prof_read(unsigned long long out[12], unsigned* hist) {
@@ -1339,31 +1338,27 @@ int fast_prof_read(unsigned long long out[12], unsigned* hist) {
 void configure_fast_kernel();
 
 using FastKernel = void (*)(FastArgs);
-FastKernel fast_kernel(int uniform, int shf, int fix) {
-  return uniform && fix   ? k_fast_segment<true, true, true>
-         : uniform && shf ? k_fast_segment<true, true, false>
-         : uniform        ? k_fast_segment<true, false, false>
-         : fix            ? k_fast_segment<false, true, true>
-         : shf            ? k_fast_segment<false, true, false>
-                          : k_fast_segment<false, false, false>;
+template <int kW>
+FastKernel fast_kernel_w(int uniform, int shf, int fix) {
+  return uniform && fix   ? k_fast_segment<true, true, true, kW>
+         : uniform && shf ? k_fast_segment<true, true, false, kW>
+         : uniform        ? k_fast_segment<true, false, false, kW>
+         : fix            ? k_fast_segment<false, true, true, kW>
+         : shf            ? k_fast_segment<false, true, false, kW>
+                          : k_fast_segment<false, false, false, kW>;
+}
+FastKernel fast_kernel(int uniform, int shf, int fix, int warps) {
+  return warps == 24 ? fast_kernel_w<24>(uniform, shf, fix) : fast_kernel_w<12>(uniform, shf, fix);
 }
 
 // resident blocks per SM of the instantiation a launch will use (the
 // persistent grid must be fully resident: idle warps wait on busy ones)
-int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix) {
+int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix, int warps) {
   configure_fast_kernel();
   int n = 0;
-  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fast_kernel(uniform, shf, fix),
-                                                          kThreads, smem));
+  HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &n, fast_kernel(uniform, shf, fix, warps), 32 * warps, smem));
   return n;
-}
-// the most blocks per SM any instantiation can hold (per-warp buffers are sized by it)
-int fast_max_blocks_per_sm() {
-  int m = 0;
-  for (int u = 0; u < 2; ++u)
-    for (int sh = 0; sh < 2; ++sh)
-      for (int f = 0; f <= sh; ++f) m = std::max(m, fast_blocks_per_sm(0, u, sh, f));
-  return m;
 }
 
 namespace {
@@ -1374,12 +1369,12 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
 }  // namespace
 
 void configure_fast_kernel() {
-  static DynSmemCache configured[6];
+  static DynSmemCache configured[12];
   int i = 0;
-  for (auto k : {k_fast_segment<false, false, false>, k_fast_segment<false, true, false>,
-                 k_fast_segment<true, false, false>, k_fast_segment<true, true, false>,
-                 k_fast_segment<false, true, true>, k_fast_segment<true, true, true>})
-    ensure_dyn_smem(k, 200 * 1024, configured[i++]);
+  for (int w : {12, 24})
+    for (int u = 0; u < 2; ++u)
+      for (int sh = 0; sh < 2; ++sh)
+        for (int f = 0; f <= sh; ++f) ensure_dyn_smem(fast_kernel(u, sh, f, w), 200 * 1024, configured[i++]);
 }
 
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
@@ -1387,13 +1382,13 @@ void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_
   if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head, a.span);
   const bool shf = a.smem_tallies == 1;
   const bool fix = shf && a.fix;
-  const FastKernel k = fast_kernel(a.uniform, shf, fix);
+  const FastKernel k = fast_kernel(a.uniform, shf, fix, a.warps);
   // programmatic dependent launch: the grid may be scheduled while the kernel
   // before it (the window update) drains; every block waits for it
   // (griddepcontrol.wait) before touching memory
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(32 * a.warps);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
