@@ -118,10 +118,13 @@ constexpr int kSmemStack = HWWG_SMEM_STACK;  // split-stack records per warp kep
 #endif
 constexpr unsigned kPiece = HWWG_KPIECE;  // smallest run piece handed to an idle warp
 
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  return z ^ (z >> 31);
+// A daughter's lineage key (the Philox counter's middle words): a bijective
+// one-multiply mix of (parent key, parent draw counter, daughter index) — the
+// keys only need to stay distinct within a history (Philox does the mixing),
+// and the cold start draws ~6e8 of them.
+__device__ __forceinline__ unsigned long long mix_lineage(unsigned long long z) {
+  z *= 0x9E3779B97F4A7C15ULL;
+  return z ^ (z >> 32);
 }
 
 struct Lane {
@@ -196,7 +199,7 @@ __device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigne
   p.cell = (int)(r.cell & 0xffffu);
   p.bslot = (int)(r.cell >> 16);
   p.hist = r.hist;
-  p.key = mix64(r.key ^ ((unsigned long long)r.ctr << 40) ^ ((unsigned long long)j << 8) ^
+  p.key = mix_lineage(r.key ^ ((unsigned long long)r.ctr << 40) ^ ((unsigned long long)j << 8) ^
                 0x5bd1e995ULL);
   p.ctr = 0;
   p.inv_mu = 1.0 / p.mu;
