@@ -180,6 +180,7 @@ struct hwwg_driver {
   // e2e (host_bank) Philox runs: the bank in host memory is already combed
   bool host_pre_combed = false;
   uint64_t pre_comb_in = 0;
+  uint64_t pre_Hc = 0, pre_nv = 0;  // multi-rank: combed / volumetric histories of the pre-combed step
   // packed wire format of a pre-combed host bank: (x, mu) per particle, then
   // (w, t) per particle only when they are not one shared pair (host_uniform)
   bool host_packed = false, host_uniform = false;
@@ -578,6 +579,21 @@ StepLayout make_layout(const hwwg_run_config& c, bool hybrid, uint64_t Hc, uint6
   return L;
 }
 
+// The rank's combed histories as (first global id, count) ranges, in its local order.
+PieceTable comb_pieces(const StepLayout& L, int R) {
+  PieceTable t{};
+  for (size_t u = 0; u < L.segments() && t.n < 9; ++u) {
+    uint64_t lo, hi;
+    L.piece(R, u, lo, hi);
+    hi = std::min(hi, L.Hc);
+    if (hi <= lo) continue;
+    t.lo[t.n] = lo;
+    t.cnt[t.n] = hi - lo;
+    ++t.n;
+  }
+  return t;
+}
+
 // Global comb + census rebalance over `world` ranks:
 // local weight scan -> all-gather of the rank totals -> the same host plan on
 // every rank (hwwg_comb_plan) -> this rank's teeth -> grouped send/recv so that
@@ -633,59 +649,82 @@ uint64_t multi_gpu_comb(hwwg_driver* d, int step, uint64_t nv, StepLayout& L, cu
   const uint64_t nt = khi[R] - klo[R];
   d->fteeth.reserve(std::max<uint64_t>(nt, 1));
   if (nt) launch_fast_comb_teeth_range(a, spacing, offset, origin, klo[R], khi[R], d->fteeth.view(), s);
-  // rebalance: the teeth with ids in rank q's pieces go to q, at q's local index
-  // of the id (both sides walk q's pieces in order: sends and receives match)
   const bool permute = step > 1;  // the cold-start bank is the i.i.d. pulse
   const uint64_t nloc = d->fsrc_local;
   FastBankBuf& dst_buf = permute ? d->fperm : d->fsrc;
   dst_buf.reserve(std::max<uint64_t>(nloc, 1));
   const FastBank dst = dst_buf.view(), th = d->fteeth.view();
-  auto cut = [&](int q, size_t u, uint64_t k_lo, uint64_t k_hi, uint64_t& lo, uint64_t& hi) {
-    L.piece(q, u, lo, hi);
-    lo = std::max(lo, k_lo);
-    hi = std::min(std::min(hi, Hc), k_hi);
-    return hi > lo;
+  auto copy = [&](uint64_t to, uint64_t from, uint64_t m) {
+    HWWG_CUDA(cudaMemcpyAsync(dst.xm + to, th.xm + from, m * 16, cudaMemcpyDeviceToDevice, s));
+    HWWG_CUDA(cudaMemcpyAsync(dst.wt + to, th.wt + from, m * 16, cudaMemcpyDeviceToDevice, s));
+    HWWG_CUDA(cudaMemcpyAsync(dst.meta + to, th.meta + from, m * 16, cudaMemcpyDeviceToDevice, s));
+  };
+  auto send = [&](uint64_t from, uint64_t m, int q) {
+    d->comm->send(th.xm + from, 2 * m, DType::kF64, q, s);
+    d->comm->send(th.wt + from, 2 * m, DType::kF64, q, s);
+    d->comm->send(th.meta + from, 4 * m, DType::kU32, q, s);
+  };
+  auto recv = [&](uint64_t to, uint64_t m, int q) {
+    d->comm->recv(dst.xm + to, 2 * m, DType::kF64, q, s);
+    d->comm->recv(dst.wt + to, 2 * m, DType::kF64, q, s);
+    d->comm->recv(dst.meta + to, 4 * m, DType::kU32, q, s);
   };
   d->comm->group_start();
-  for (int q = 0; q < W; ++q) {
-    for (size_t u = 0; u < L.segments(); ++u) {
-      uint64_t lo, hi;
-      if (!cut(q, u, klo[R], khi[R], lo, hi)) continue;
-      const uint64_t o = lo - klo[R], m = hi - lo;
-      if (q == R) {
-        const uint64_t at = L.owned_before(R, lo);
-        HWWG_CUDA(cudaMemcpyAsync(dst.xm + at, th.xm + o, m * 16, cudaMemcpyDeviceToDevice, s));
-        HWWG_CUDA(cudaMemcpyAsync(dst.wt + at, th.wt + o, m * 16, cudaMemcpyDeviceToDevice, s));
-        HWWG_CUDA(cudaMemcpyAsync(dst.meta + at, th.meta + o, m * 16, cudaMemcpyDeviceToDevice, s));
-      } else {
-        d->comm->send(th.xm + o, 2 * m, DType::kF64, q, s);
-        d->comm->send(th.wt + o, 2 * m, DType::kF64, q, s);
-        d->comm->send(th.meta + o, 4 * m, DType::kU32, q, s);
+  if (!permute) {
+    // Cold start: the teeth with ids in rank q's pieces go to q, at q's local
+    // index of the id (both sides walk q's pieces in order: sends and receives
+    // match), so history g gets tooth g on any rank count — step 1 is the
+    // single-GPU step (tests/test_gpu_multirank.py).
+    auto cut = [&](int q, size_t u, uint64_t k_lo, uint64_t k_hi, uint64_t& lo, uint64_t& hi) {
+      L.piece(q, u, lo, hi);
+      lo = std::max(lo, k_lo);
+      hi = std::min(std::min(hi, Hc), k_hi);
+      return hi > lo;
+    };
+    for (int q = 0; q < W; ++q) {
+      for (size_t u = 0; u < L.segments(); ++u) {
+        uint64_t lo, hi;
+        if (!cut(q, u, klo[R], khi[R], lo, hi)) continue;
+        if (q == R) copy(L.owned_before(R, lo), lo - klo[R], hi - lo);
+        else send(lo - klo[R], hi - lo, q);
+      }
+      if (q == R) continue;
+      for (size_t u = 0; u < L.segments(); ++u) {
+        uint64_t lo, hi;
+        if (cut(R, u, klo[q], khi[q], lo, hi)) recv(L.owned_before(R, lo), hi - lo, q);
       }
     }
-    if (q == R) continue;
-    for (size_t u = 0; u < L.segments(); ++u) {
-      uint64_t lo, hi;
-      if (!cut(R, u, klo[q], khi[q], lo, hi)) continue;
-      const uint64_t at = L.owned_before(R, lo), m = hi - lo;
-      d->comm->recv(dst.xm + at, 2 * m, DType::kF64, q, s);
-      d->comm->recv(dst.wt + at, 2 * m, DType::kF64, q, s);
-      d->comm->recv(dst.meta + at, 4 * m, DType::kU32, q, s);
+  } else {
+    // Later steps: the rank's teeth are about its share already (a census
+    // weight share of ~1/W, off by a few 1e-3 at 1e7 histories per rank), and
+    // its histories are a permutation of its slots anyway, so a rank keeps
+    // min(teeth, slots) of its own teeth and only the excess moves: excess
+    // rank tails are matched to deficit ranks in rank order, identically on
+    // every rank (round 2's first version moved (W-1)/W of all teeth).
+    std::vector<uint64_t> own(W), have(W);
+    for (int q = 0; q < W; ++q) {
+      own[q] = L.owned_before(q, Hc);
+      have[q] = khi[q] - klo[q];
+    }
+    const uint64_t keep = std::min(have[R], own[R]);
+    if (keep) copy(0, 0, keep);
+    int qe = 0, qd = 0;            // next excess / deficit rank
+    uint64_t oe = 0, od = 0;       // consumed within them
+    while (true) {
+      while (qe < W && (have[qe] <= own[qe] || oe == have[qe] - own[qe])) ++qe, oe = 0;
+      while (qd < W && (own[qd] <= have[qd] || od == own[qd] - have[qd])) ++qd, od = 0;
+      if (qe >= W || qd >= W) break;
+      const uint64_t m = std::min(have[qe] - own[qe] - oe, own[qd] - have[qd] - od);
+      if (qe == R) send(own[R] + oe, m, qd);  // the excess is the tail of the rank's teeth
+      if (qd == R) recv(have[R] + od, m, qe);
+      oe += m;
+      od += m;
     }
   }
   d->comm->group_end(s);
   d->launches += 3;
   if (permute) {  // out[c] = in[perm(c)], history = the global id of slot c
-    PieceTable t{};
-    for (size_t u = 0; u < L.segments() && t.n < 9; ++u) {
-      uint64_t lo, hi;
-      L.piece(R, u, lo, hi);
-      hi = std::min(hi, Hc);
-      if (hi <= lo) continue;
-      t.lo[t.n] = lo;
-      t.cnt[t.n] = hi - lo;
-      ++t.n;
-    }
+    const PieceTable t = comb_pieces(L, R);
     launch_fast_permute(d->fperm.view(), d->fsrc.view(), nloc, make_perm(nloc, d->cfg.seed, step),
                         t, s);
     ++d->launches;
@@ -845,6 +884,21 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->bank_n = Hs;
     rec->h2d_bytes += d->host_packed ? Hs * sizeof(double2) * (d->host_uniform ? 1 : 2)
                                      : Hs * sizeof(hwwg_particle);
+  } else if (c.host_bank && d->fast && d->host_pre_combed && d->world > 1) {
+    // multi-rank e2e: this rank's share of the global comb, combed at the end
+    // of the previous step, back from the host in the packed format
+    const uint64_t nl = d->host_bank_n;
+    const FastBank f = d->fsrc.view();
+    const double2* hb = reinterpret_cast<const double2*>(d->host_bank);
+    HWWG_CUDA(cudaMemcpyAsync(f.xm, hb, nl * sizeof(double2), cudaMemcpyHostToDevice, s));
+    if (!d->host_uniform)
+      HWWG_CUDA(cudaMemcpyAsync(f.wt, hb + nl, nl * sizeof(double2), cudaMemcpyHostToDevice, s));
+    const StepLayout Lp = make_layout(c, d->hybrid(), d->pre_Hc, d->pre_Hc + d->pre_nv, d->world);
+    const PieceTable t = comb_pieces(Lp, d->rank);
+    launch_xm_to_fast(f, nl, d->prob.view, 0, d->host_uniform ? 1 : 0, d->host_w0, d->host_t0, s,
+                      &t);
+    ++d->launches;
+    rec->h2d_bytes += nl * sizeof(double2) * (d->host_uniform ? 1 : 2);
   } else if (c.host_bank) {  // e2e: the bank lives in host memory between steps
     d->bank.reserve(std::max<uint64_t>(d->host_bank_n, 1));
     HWWG_CUDA(cudaMemcpyAsync(d->bank.p, d->host_bank, d->host_bank_n * sizeof(hwwg_particle),
@@ -878,6 +932,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     rec->comb_in = rec->comb_out = 0;
     HWWG_CUDA(cudaMemsetAsync(d->comb_mem.p, 0, 4 * sizeof(double), s));
     if (!d->fast) d->source.reserve(std::max<uint64_t>(vol_cap, 1));
+  } else if (d->fast && d->world > 1 && c.host_bank && d->host_pre_combed) {
+    H = d->pre_Hc;  // the global comb ran at the end of the previous step
+    Lmulti = make_layout(c, d->hybrid(), H, H + nv_step, d->world);
+    rec->comb_in = d->pre_comb_in;
+    rec->comb_out = H;
   } else if (d->fast && d->world > 1) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
     H = multi_gpu_comb(d, step, nv_step, Lmulti, s);
@@ -1441,13 +1500,6 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   if (d->fast) {
     d->fbank.swap(d->fcensus);  // the census is the next comb's input
     d->bank_t = rec->t_end;     // every census particle sits at the step's end
-    if (c.host_bank && d->world > 1) {  // real particles only, AoS, for the host round trip
-      d->bank.reserve(std::max<unsigned long long>(count, 1));
-      launch_fast_compact_aos(d->fbank.view(), count, d->bank_t, d->bank.p, d->counter.p, s);
-      HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
-      HWWG_CUDA(cudaStreamSynchronize(s));
-      ++d->launches;
-    }
   } else {
     d->bank.reserve(std::max<unsigned long long>(count, 1));
     d->stage.sort_into(d->bank.p, count, ((unsigned long long)H << 24) | 0xffffffULL, s);
@@ -1517,6 +1569,37 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, d->target * sizeof(hwwg_particle),
                                 cudaMemcpyDeviceToHost, s));
     }
+  } else if (c.host_bank && d->fast && d->world > 1) {
+    // multi-rank e2e: the next step's global comb now (it is collective), then
+    // this rank's combed source crosses PCIe packed, as on one GPU — not the
+    // raw census (x60 of the rank's histories after the cold start)
+    const int nstep = step + 1;
+    if (nstep <= c.time_steps) {
+      const uint64_t nv_next =
+          (c.vol_rate > 0.0 && d->q_row[nstep] >= 0) ? c.vol_histories : 0;
+      StepLayout Ln;
+      d->pre_Hc = multi_gpu_comb(d, nstep, nv_next, Ln, s);
+      d->pre_nv = nv_next;
+      d->pre_comb_in = d->bank_n;
+      d->host_pre_combed = true;
+      const uint64_t nl = d->fsrc_local;
+      if (2 * nl > d->host_bank_cap) {
+        HWWG_CUDA(cudaStreamSynchronize(s));
+        if (d->host_bank) HWWG_CUDA(cudaFreeHost(d->host_bank));
+        d->host_bank_cap = nl + nl / 4 + 4096;
+        HWWG_CUDA(cudaMallocHost(&d->host_bank, d->host_bank_cap * sizeof(hwwg_particle)));
+      }
+      d->host_bank_n = nl;
+      d->host_packed = true;
+      launch_check_uniform(d->fsrc.wt.p, nl, d->uni_flag.p, d->uni_first.p, s);
+      ++d->launches;
+      rec->d2h_bytes += nl * sizeof(double2) + 32;
+      HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->fsrc.xm.p, nl * sizeof(double2),
+                                cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaMemcpyAsync(d->h_uni, d->uni_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d->h_uni) + 16, d->uni_first.p,
+                                sizeof(double2), cudaMemcpyDeviceToHost, s));
+    }
   } else if (c.host_bank) {
     if (count > d->host_bank_cap) {
       HWWG_CUDA(cudaStreamSynchronize(s));
@@ -1538,10 +1621,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->host_t0 = f[1];
     if (!d->host_uniform) {  // (w, t) differ: they cross too, after the (x, mu) block
       double2* hb = reinterpret_cast<double2*>(d->host_bank);
-      HWWG_CUDA(cudaMemcpyAsync(hb + d->target, d->fsrc.wt.p, d->target * sizeof(double2),
-                                cudaMemcpyDeviceToHost, s));
+      HWWG_CUDA(cudaMemcpyAsync(hb + d->host_bank_n, d->fsrc.wt.p,
+                                d->host_bank_n * sizeof(double2), cudaMemcpyDeviceToHost, s));
       HWWG_CUDA(cudaStreamSynchronize(s));
-      rec->d2h_bytes += d->target * sizeof(double2);
+      rec->d2h_bytes += d->host_bank_n * sizeof(double2);
     }
   }
   float ms = 0.f;

@@ -250,7 +250,8 @@ void launch_check_uniform(const double2* wt, uint64_t n, unsigned* flag, double2
 void launch_volume_source(FastBank out, uint64_t n, uint64_t j0, uint64_t hist0, const MeshView& m,
                           unsigned k0, unsigned k1, unsigned step, double x_lo, double x_hi,
                           double ta, double tb, double w, cudaStream_t s);
+// (pieces: multi-rank, history of slot i = the rank's i-th owned id; null: hist0 + i)
 void launch_xm_to_fast(FastBank out, uint64_t n, const MeshView& m, uint64_t hist0, int uniform,
-                       double w0, double t0, cudaStream_t s);
+                       double w0, double t0, cudaStream_t s, const PieceTable* pieces = nullptr);
 
 }  // namespace hwwg

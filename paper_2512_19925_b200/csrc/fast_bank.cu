@@ -398,13 +398,24 @@ __global__ void k_check_uniform(const double2* __restrict__ wt, uint64_t n, unsi
 // (x, mu) from the host into the SoA bank: cell, identity, and (w, t) when the
 // host bank was packed uniform.
 __global__ void k_xm_to_fast(FastBank out, uint64_t n, const MeshView m, uint64_t hist0,
-                             int uniform, double w0, double t0) {
+                             int uniform, double w0, double t0, PieceTable pieces) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double x = out.xm[i].x;
   if (uniform) out.wt[i] = make_double2(w0, t0);
   const int c = locate_cell(m, x);
-  out.meta[i] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)(hist0 + i), 0u, 0u);
+  uint64_t g = hist0 + i;  // history: hist0 + i, or the rank's i-th owned id (pieces)
+  if (pieces.n) {
+    uint64_t rem = i;
+    for (int k = 0; k < pieces.n; ++k) {
+      if (rem < pieces.cnt[k]) {
+        g = pieces.lo[k] + rem;
+        break;
+      }
+      rem -= pieces.cnt[k];
+    }
+  }
+  out.meta[i] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)g, 0u, 0u);
 }
 
 // Config-3 volumetric source on the device (Philox mode; DESIGN.md "Config-3
@@ -452,9 +463,11 @@ void launch_check_uniform(const double2* wt, uint64_t n, unsigned* flag, double2
 }
 
 void launch_xm_to_fast(FastBank out, uint64_t n, const MeshView& m, uint64_t hist0, int uniform,
-                       double w0, double t0, cudaStream_t s) {
+                       double w0, double t0, cudaStream_t s, const PieceTable* pieces) {
   if (!n) return;
-  k_xm_to_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, m, hist0, uniform, w0, t0);
+  PieceTable t{};
+  if (pieces) t = *pieces;
+  k_xm_to_fast<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, n, m, hist0, uniform, w0, t0, t);
   HWWG_CUDA(cudaGetLastError());
 }
 

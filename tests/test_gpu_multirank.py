@@ -163,3 +163,24 @@ def test_later_steps_within_replicate_se():
         z = np.concatenate(zs)
         assert np.mean(np.abs(z) < 3) >= 0.95, (key, np.sort(np.abs(z))[-8:])
         assert abs(z.mean()) < 0.5, (key, z.mean())
+
+
+def test_host_round_trip_multirank():
+    """Multi-rank e2e (host_bank): the next step's global comb runs at the end of a
+    step and each rank's combed share crosses PCIe packed ((x, mu), 16 B per
+    particle), not the raw census; the records match the device-resident run's
+    bookkeeping and statistics."""
+    H, steps, W = 30_000, 4, 2
+    dev = run_world(c2(H, steps, 23), W, steps)
+    cfg = c2(H, steps, 23)
+    cfg.host_bank = True
+    host = run_world(cfg, W, steps)
+    for n in range(steps):
+        rd, rh = dev[0][n][0], host[0][n][0]
+        assert rh.histories == H and rh.comb_out == H
+        np.testing.assert_allclose(rh.comb_out_weight, rh.comb_in_weight, rtol=1e-12)
+        assert abs(rh.segments / rd.segments - 1) < 0.06, (n, rh.segments, rd.segments)
+        assert abs(rh.census_weight / rd.census_weight - 1) < 0.03
+        if n >= 1:  # steps after the first open with a pre-combed share from the host
+            per_rank = [host[r][n][0].h2d_bytes for r in range(W)]
+            assert sum(per_rank) == H * 16, per_rank
