@@ -37,6 +37,9 @@
 // histograms do not fit in shared memory (I = 4000).
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -1357,10 +1360,24 @@ FastKernel fast_kernel(int uniform, int shf, int fix, int warps) {
 // resident blocks per SM of the instantiation a launch will use (the
 // persistent grid must be fully resident: idle warps wait on busy ones)
 int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix, int warps) {
+  // memoised per device: the driver asks several times per segment, and the
+  // host must stay ahead of ~20 us segments (config 1)
+  static std::mutex m;
+  static std::map<std::tuple<int, size_t, int, int, int, int>, int> memo;
+  int dev = 0;
+  HWWG_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, smem, uniform, shf, fix, warps);
+  {
+    std::lock_guard<std::mutex> lk(m);
+    const auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
   configure_fast_kernel();
   int n = 0;
   HWWG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       &n, fast_kernel(uniform, shf, fix, warps), 32 * warps, smem));
+  std::lock_guard<std::mutex> lk(m);
+  memo[key] = n;
   return n;
 }
 
@@ -1372,12 +1389,17 @@ __global__ void k_segment_reset(unsigned long long* ctl, unsigned long long* src
 }  // namespace
 
 void configure_fast_kernel() {
+  static thread_local int done_dev = -1;  // this thread configured this device already
+  int dev = 0;
+  HWWG_CUDA(cudaGetDevice(&dev));
+  if (dev == done_dev) return;
   static DynSmemCache configured[12];
   int i = 0;
   for (int w : {12, 24})
     for (int u = 0; u < 2; ++u)
       for (int sh = 0; sh < 2; ++sh)
         for (int f = 0; f <= sh; ++f) ensure_dyn_smem(fast_kernel(u, sh, f, w), 200 * 1024, configured[i++]);
+  done_dev = dev;
 }
 
 void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
