@@ -42,6 +42,8 @@ extern "C" {
 #define HWWG_ESINGULAR (-5) /* LOSM system singular (reference: std::runtime_error) */
 #define HWWG_ENOSPC (-6)    /* caller buffer too small; *needed is set */
 #define HWWG_ESTACK (-7)    /* exact-mode daughter stack exceeded its run capacity */
+#define HWWG_EFORMAT (-8)   /* reference file missing, malformed or of the wrong shape
+                               (reference: std::runtime_error from load_reference) */
 
 #define HWWG_RNG_EXACT 0  /* replay the reference's xoshiro256** streams bit-for-bit */
 #define HWWG_RNG_PHILOX 1 /* event-based throughput mode, counter-based Philox4x32-10 */
@@ -202,6 +204,11 @@ typedef struct {
   double vol_t_lo, vol_t_hi; /* ... and in t */
   double vol_rate;           /* emitted weight per unit time (same normalisation as strength) */
   uint64_t vol_histories;    /* particles sampled in every step the box overlaps */
+  /* RunConfig::reference (config.hpp:64): "auto" | reference file path | "" (none).
+   * Carried for the tools and run.json; the driver takes the reference itself
+   * through hwwg_driver_set_reference / hwwg_driver_load_reference, as hww::run
+   * takes a ReferenceSolution* (driver.hpp:88). */
+  char reference[256];
 } hwwg_run_config;
 
 /* == hww::StepRecord scalars (proj/include/hww/driver.hpp:41-56). */
@@ -230,6 +237,10 @@ typedef struct {
   uint64_t transport_launches; /* transport kernel launches in the step */
   uint64_t kernel_launches;    /* all engine kernel launches in the step */
   uint64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by the step (host_bank mode) */
+  /* StepMetrics against a deterministic reference (metrics.hpp:41-51; driver.cpp:231-271);
+   * NaN without one (fom_sigma_l2 above is set either way). */
+  double rel_l2_error, rel_mod_l2_error, hybrid_rel_l2_error;
+  double fom_err_l2, fom_err_mod, fom_sigma_mod, alpha;
 } hwwg_step_record;
 
 int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts,
@@ -245,6 +256,16 @@ int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma,
 /* Census bank after the last step (the next step's comb input), reference
  * order.  Returns HWWG_ENOSPC with *n = size when cap is too small. */
 int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t* n);
+/* The deterministic reference for the step diagnostics (hww::run's
+ * ReferenceSolution*, driver.hpp:88): phi_layer[(steps+1)*cells] layer values,
+ * phi_interval[steps*cells] interval averages of steps 1..N (ReferenceSolution,
+ * reference.hpp:76-85).  name goes to run.json's "reference" (NULL keeps
+ * cfg.reference).  After this every step fills the record's metric fields. */
+int hwwg_driver_set_reference(hwwg_driver* d, const double* phi_layer,
+                              const double* phi_interval, const char* name);
+/* hww::load_reference on the driver's own mesh and time grid, then
+ * hwwg_driver_set_reference(d, ..., path) (hww_main.cpp:250-252). */
+int hwwg_driver_load_reference(hwwg_driver* d, const char* path);
 /* Key = value config file (proj/tools/hww_main.cpp:20-92 key names). */
 int hwwg_load_config_file(const char* path, hwwg_run_config* cfg);
 /* Reference defaults (config.hpp:33-66). */
@@ -257,8 +278,8 @@ int hwwg_validate_config(const hwwg_run_config* cfg, char* buf, uint64_t buf_len
 /* The reference's run outputs (proj/src/driver.cpp:355-438), same bytes for
  * equal records: step_<n>.csv (write_step_csv; ww_centers / phi_hybrid NULL
  * print as nan, sigma prints as nan unless rec->sigma_valid), summary.csv over
- * recs[0..n) (write_summary_csv; the S_N error metrics, fom_sigma_mod and alpha
- * are nan: no reference solution), run.json (write_run_json; "reference" = "").
+ * recs[0..n) (write_summary_csv; the metric fields as the records carry them, NaN
+ * without a reference), run.json (write_run_json; "reference" = cfg->reference).
  * dir is created if missing. */
 int hwwg_write_step_csv(const char* dir, const hwwg_step_record* rec, int32_t cells,
                         const double* edges, const double* phi_track, const double* sigma,
@@ -272,6 +293,33 @@ int hwwg_write_run_json(const char* dir, const hwwg_run_config* cfg, double tota
  * summary.csv of every step so far; final != 0 also writes run.json with
  * total_seconds. */
 int hwwg_driver_write(hwwg_driver* d, const char* dir, int32_t final, double total_seconds);
+
+/* ------------------------------------------------- reference solution */
+/* hww::save_reference (proj/src/reference.cpp:374-393), same bytes: one row per
+ * (layer, cell) "t_layer, cell_index, x_center, phi_layer, phi_interval_avg",
+ * precision 17, layer 0's interval as nan.  edges[cells+1], layers[steps+1],
+ * phi_layer[(steps+1)*cells], phi_interval[steps*cells]. */
+int hwwg_save_reference_csv(const char* path, int32_t cells, const double* edges,
+                            int32_t steps, const double* layers, const double* phi_layer,
+                            const double* phi_interval);
+/* hww::load_reference (reference.cpp:395-456): same parse and shape checks (cell
+ * index, layer time within 1e-9, centre within 1e-9 of the mesh span, row count),
+ * failing with HWWG_EFORMAT and the reference's message; outputs untouched on
+ * failure.  phi_interval may be NULL. */
+int hwwg_load_reference_csv(const char* path, int32_t cells, const double* edges,
+                            int32_t steps, const double* layers, double* phi_layer,
+                            double* phi_interval);
+/* RunConfig::make_time_grid layers (config.hpp:88; time_grid.hpp:22-29): steps+1 values. */
+int hwwg_time_layers(const hwwg_run_config* cfg, double* layers);
+/* hww::run_step's diagnostics (driver.cpp:231-275; metrics.cpp:8-66) from a step's
+ * arrays: reads rec->tau and rec->sigma_valid, writes rec's fom_sigma_l2 and metric
+ * fields.  ref_interval == NULL: no reference (fom_sigma_l2 only); otherwise
+ * ref_layer / ref_layer_prev are the reference's layers n and n-1.  phi_hybrid NULL:
+ * no hybrid solve.  HWWG_EINVAL when the reference layer is all zero (relative_change). */
+int hwwg_step_metrics(int32_t cells, const double* edges, const double* phi_track,
+                      const double* phi_sigma, const double* phi_hybrid,
+                      const double* ref_interval, const double* ref_layer,
+                      const double* ref_layer_prev, hwwg_step_record* rec);
 
 /* ----------------------------------------------------- device components */
 /* hww::assemble_solve (losm.cpp:143-165) on the device, single CTA.

@@ -220,6 +220,20 @@ class DriverRun:
         arr["tracks_per_cell"] = tracks
         return out, arr
 
+    def load_reference(self, path):
+        """hwwref_driver_load_reference: later steps run against the file (reference lib only)."""
+        if self.lib.lib.hwwref_driver_load_reference(self.h, str(path).encode()) != 0:
+            raise RuntimeError(self.lib.err())
+
+    METRICS = ("rel_l2_error", "rel_mod_l2_error", "hybrid_rel_l2_error", "fom_err_l2",
+               "fom_err_mod", "fom_sigma_l2", "fom_sigma_mod", "alpha", "tau")
+
+    def metrics(self):
+        """StepMetrics of the last step (reference lib only)."""
+        v = np.zeros(9)
+        self.lib.lib.hwwref_driver_metrics(self.h, _dp(v))
+        return dict(zip(self.METRICS, v.tolist()))
+
     def bank(self):
         n = self.lib.fn("driver_bank")(self.h, None, 0)
         b = np.zeros(n, PARTICLE_DT)
@@ -306,14 +320,48 @@ class Reference(_Lib):
         L.hwwref_take_census.argtypes = [C.c_void_p, C.c_uint64]
         L.hwwref_num_threads.restype = C.c_int
         L.hwwref_set_threads.argtypes = [C.c_int]
-        L.hwwref_run_to_dir.argtypes = [C.POINTER(Config), C.c_char_p]
+        L.hwwref_run_to_dir.argtypes = [C.POINTER(Config), C.c_char_p, C.c_char_p]
+        L.hwwref_driver_load_reference.argtypes = [C.c_void_p, C.c_char_p]
+        L.hwwref_driver_metrics.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        L.hwwref_driver_metrics.restype = None
+        dp = C.POINTER(C.c_double)
+        L.hwwref_compute_reference.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32,
+                                               C.c_int32, dp, dp]
+        L.hwwref_save_reference.argtypes = [C.POINTER(Config), C.c_char_p, dp, dp]
+        L.hwwref_load_reference.argtypes = [C.POINTER(Config), C.c_char_p, dp, dp]
         L.hwwref_write_outputs.argtypes = [C.c_char_p, C.POINTER(Config), C.c_int32, C.c_int32] + [
-            C.c_void_p] * 11 + [C.c_double]
+            C.c_void_p] * 12 + [C.c_double]
 
-    def run_to_dir(self, config: Config, out_dir):
-        """hww::run with out_dir: the reference's own output files."""
-        if self.lib.hwwref_run_to_dir(C.byref(config), str(out_dir).encode()) != 0:
+    def run_to_dir(self, config: Config, out_dir, reference=None):
+        """hww::run with out_dir: the reference's own output files (against the
+        reference file `reference` when given, as hww_main runs it)."""
+        ref = str(reference).encode() if reference else None
+        if self.lib.hwwref_run_to_dir(C.byref(config), str(out_dir).encode(), ref) != 0:
             raise ValueError(self.err())
+
+    def compute_reference(self, config: Config, space_refine=5, time_refine=20, sn_order=16):
+        """hww::compute_reference (reference.cpp:364-372): (phi_layer, phi_interval)."""
+        N, I = config.time_steps, config.cells
+        lay, itv = np.zeros((N + 1, I)), np.zeros((N, I))
+        if self.lib.hwwref_compute_reference(C.byref(config), space_refine, time_refine,
+                                             sn_order, _dp(lay), _dp(itv)) != 0:
+            raise RuntimeError(self.err())
+        return lay, itv
+
+    def save_reference(self, config: Config, path, phi_layer, phi_interval):
+        lay = np.ascontiguousarray(phi_layer, np.float64)
+        itv = np.ascontiguousarray(phi_interval, np.float64)
+        if self.lib.hwwref_save_reference(C.byref(config), str(path).encode(), _dp(lay),
+                                          _dp(itv)) != 0:
+            raise RuntimeError(self.err())
+
+    def load_reference(self, config: Config, path):
+        N, I = config.time_steps, config.cells
+        lay, itv = np.zeros((N + 1, I)), np.zeros((N, I))
+        if self.lib.hwwref_load_reference(C.byref(config), str(path).encode(), _dp(lay),
+                                          _dp(itv)) != 0:
+            raise RuntimeError(self.err())
+        return lay, itv
 
     def write_outputs(self, out_dir, config: Config, steps, total_seconds):
         """The reference writers on synthetic records. steps: list of dicts with
@@ -321,7 +369,9 @@ class Reference(_Lib):
         hybrid (or None), tracks and scalars t_end, tau, fom_sigma_l2,
         census_weight, census_weight_sigma, normalization, sigma_valid,
         hybrid_solve_failed, step, histories, comb_in, comb_out,
-        updates_applied, counters (Counters)."""
+        updates_applied, counters (Counters), and optionally metrics (7 values:
+        rel_l2_error, rel_mod_l2_error, hybrid_rel_l2_error, fom_err_l2,
+        fom_err_mod, fom_sigma_mod, alpha)."""
         n, I = len(steps), config.cells
         def stack(key, dt=np.float64):
             parts = [np.asarray(s[key] if s[key] is not None else np.zeros(I), dt) for s in steps]
@@ -337,10 +387,12 @@ class Reference(_Lib):
                           (1 if s["centers"] is not None else 0) |
                           (2 if s["hybrid"] is not None else 0)] for s in steps], np.uint64)
         cnt = (Counters * max(n, 1))(*[s["counters"] for s in steps])
+        met = np.ascontiguousarray([s.get("metrics", (np.nan,) * 7) for s in steps] or
+                                   [(np.nan,) * 7], np.float64)
         rc = self.lib.hwwref_write_outputs(
             str(out_dir).encode(), C.byref(config), n, I, *[a.ctypes.data for a in arrs],
             tracks.ctypes.data, sc.ctypes.data, ints.ctypes.data, C.addressof(cnt),
-            total_seconds)
+            met.ctypes.data, total_seconds)
         if rc != 0:
             raise ValueError(self.err())
 

@@ -32,6 +32,7 @@
 #include "hww/filters.hpp"
 #include "hww/losm.hpp"
 #include "hww/popctrl.hpp"
+#include "hww/reference.hpp"
 #include "hww/tally.hpp"
 #include "hww/transport.hpp"
 #include "hww/ww.hpp"
@@ -201,6 +202,7 @@ struct Driver {
   hww::RunState state;
   int next_step = 1;
   hww::StepRecord last;
+  std::optional<hww::ReferenceSolution> reference;  // hww::run's ReferenceSolution*
 };
 
 }  // namespace
@@ -246,7 +248,7 @@ int hwwref_driver_step(void* h, hwwref_step_out* out) {
       return -1;
     }
     d->last = hww::run_step(d->next_step, d->state, d->config, d->mesh, d->tgrid,
-                            d->materials, nullptr);
+                            d->materials, d->reference ? &*d->reference : nullptr);
     ++d->next_step;
     const auto& r = d->last;
     std::memset(out, 0, sizeof(*out));
@@ -631,13 +633,104 @@ int32_t hwwref_locate(const double* edges, int32_t cells, double x) {
   return c ? *c : -1;
 }
 
+// hww::load_reference (reference.cpp:395-456) on the driver's grids; the
+// following steps run against it (driver.cpp:231-271).
+int hwwref_driver_load_reference(void* h, const char* path) {
+  auto* d = static_cast<Driver*>(h);
+  try {
+    d->reference = hww::load_reference(path, d->mesh, d->tgrid);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// StepMetrics of the last step (metrics.hpp:41-51): rel_l2_error,
+// rel_mod_l2_error, hybrid_rel_l2_error, fom_err_l2, fom_err_mod, fom_sigma_l2,
+// fom_sigma_mod, alpha, tau.
+void hwwref_driver_metrics(void* h, double* out) {
+  const auto& m = static_cast<Driver*>(h)->last.metrics;
+  const double v[9] = {m.rel_l2_error, m.rel_mod_l2_error, m.hybrid_rel_l2_error,
+                       m.fom_err_l2,   m.fom_err_mod,      m.fom_sigma_l2,
+                       m.fom_sigma_mod, m.alpha,           m.tau};
+  std::memcpy(out, v, sizeof v);
+}
+
+// hww::compute_reference (reference.cpp:364-372): the S_N oracle projected onto
+// the config's tally grids; phi_layer (N+1)*I, phi_interval N*I.
+int hwwref_compute_reference(const hwwref_config* c, int32_t space_refine, int32_t time_refine,
+                             int32_t sn_order, double* phi_layer, double* phi_interval) {
+  try {
+    const auto ref =
+        hww::compute_reference(to_config(*c), space_refine, time_refine, sn_order);
+    const size_t I = ref.mesh.cells();
+    for (size_t n = 0; n < ref.phi_layer.size(); ++n)
+      std::memcpy(phi_layer + n * I, ref.phi_layer[n].data(), I * sizeof(double));
+    for (size_t n = 0; n < ref.phi_interval.size(); ++n)
+      std::memcpy(phi_interval + n * I, ref.phi_interval[n].data(), I * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// hww::save_reference (reference.cpp:374-393) of arrays on the config's grids.
+int hwwref_save_reference(const hwwref_config* c, const char* path, const double* phi_layer,
+                          const double* phi_interval) {
+  try {
+    const hww::RunConfig config = to_config(*c);
+    hww::ReferenceSolution ref;
+    ref.mesh = config.make_mesh();
+    ref.tgrid = config.make_time_grid();
+    const int I = ref.mesh.cells(), N = ref.tgrid.steps();
+    for (int n = 0; n <= N; ++n)
+      ref.phi_layer.emplace_back(phi_layer + (size_t)n * I, phi_layer + (size_t)(n + 1) * I);
+    for (int n = 0; n < N; ++n)
+      ref.phi_interval.emplace_back(phi_interval + (size_t)n * I,
+                                    phi_interval + (size_t)(n + 1) * I);
+    hww::save_reference(ref, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// hww::load_reference (reference.cpp:395-456) on the config's grids.
+int hwwref_load_reference(const hwwref_config* c, const char* path, double* phi_layer,
+                          double* phi_interval) {
+  try {
+    const hww::RunConfig config = to_config(*c);
+    const auto ref = hww::load_reference(path, config.make_mesh(), config.make_time_grid());
+    const size_t I = ref.mesh.cells();
+    for (size_t n = 0; n < ref.phi_layer.size(); ++n)
+      std::memcpy(phi_layer + n * I, ref.phi_layer[n].data(), I * sizeof(double));
+    for (size_t n = 0; n < ref.phi_interval.size(); ++n)
+      std::memcpy(phi_interval + n * I, ref.phi_interval[n].data(), I * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // hww::build_uniform_mesh edges (proj/src/mesh.cpp:42-50).
 // hww::run with out_dir (proj/src/driver.cpp:286-342): the reference's own
 // writers produce step_<n>.csv, summary.csv and run.json in dir.
-int hwwref_run_to_dir(const hwwref_config* c, const char* dir) {
+int hwwref_run_to_dir(const hwwref_config* c, const char* dir, const char* reference) {
   try {
     hww::RunConfig config = to_config(*c);
     config.out_dir = dir;
+    if (reference && *reference) {
+      // hww_main.cpp:250-256: config.reference holds the path, the run gets the file
+      config.reference = reference;
+      const auto ref =
+          hww::load_reference(reference, config.make_mesh(), config.make_time_grid());
+      hww::run(config, &ref);
+      return 0;
+    }
     hww::run(config);
     return 0;
   } catch (const std::exception& e) {
@@ -651,14 +744,15 @@ int hwwref_run_to_dir(const hwwref_config* c, const char* dir) {
 // scalars[k*8 + ...] = {t_end, tau, fom_sigma_l2, census_weight,
 // census_weight_sigma, normalization, sigma_valid, hybrid_solve_failed};
 // ints[k*6 + ...] = {step, histories, comb_in, comb_out, updates_applied,
-// has_centers | has_hybrid << 1}. Writes every step_<n>.csv, summary.csv and
-// run.json (total_seconds) to dir.
+// has_centers | has_hybrid << 1}; metrics[k*7 + ...] (NULL: NaN) = {rel_l2_error,
+// rel_mod_l2_error, hybrid_rel_l2_error, fom_err_l2, fom_err_mod, fom_sigma_mod,
+// alpha}. Writes every step_<n>.csv, summary.csv and run.json (total_seconds) to dir.
 int hwwref_write_outputs(const char* dir, const hwwref_config* c, int32_t n, int32_t cells,
                          const double* phi_track, const double* sigma, const double* phi_census,
                          const double* current, const double* closure, const double* centers,
                          const double* hybrid, const uint64_t* tracks, const double* scalars,
                          const uint64_t* ints, const hwwref_counters* counters,
-                         double total_seconds) {
+                         const double* metrics, double total_seconds) {
   try {
     std::filesystem::create_directories(dir);  // as hww::run does (driver.cpp:301)
     hww::RunRecord run;
@@ -690,6 +784,16 @@ int hwwref_write_outputs(const char* dir, const hwwref_config* c, int32_t n, int
       if (ints[6 * k + 5] & 2) r.phi_hybrid.assign(hybrid + o, hybrid + o + cells);
       r.tracks_per_cell.assign(tracks + o, tracks + o + cells);
       r.counters = get_counters(&counters[k]);
+      if (metrics) {  // metrics[k*7 + ...] = StepMetrics' reference diagnostics
+        const double* m = metrics + 7 * k;
+        r.metrics.rel_l2_error = m[0];
+        r.metrics.rel_mod_l2_error = m[1];
+        r.metrics.hybrid_rel_l2_error = m[2];
+        r.metrics.fom_err_l2 = m[3];
+        r.metrics.fom_err_mod = m[4];
+        r.metrics.fom_sigma_mod = m[5];
+        r.metrics.alpha = m[6];
+      }
       run.steps.push_back(r);
       hww::write_step_csv(dir, run.steps.back(), mesh);
     }

@@ -7,9 +7,11 @@ include/hwwg.h); this package is the thin Python mirror of the reference's API.
 from ._capi import PARTICLE_DT, RNG_EXACT, RNG_PHILOX, HwwgError, LIB_PATH  # noqa: F401
 from .hww import (  # noqa: F401
     Driver, Engine, Loopback, Material, Mesh1D, RunConfig, StepContext, StepOutcome, TallySet,
-    WeightWindowGrid, build_uniform_mesh, default_engine, run, run_segment_parallel)
+    WeightWindowGrid, build_uniform_mesh, default_engine, run, run_segment_parallel,
+    ReferenceSolution, load_reference, save_reference, step_metrics)
 
 __all__ = [
     "Driver", "Engine", "Loopback", "Material", "Mesh1D", "RunConfig", "StepContext", "StepOutcome",
     "TallySet", "WeightWindowGrid", "build_uniform_mesh", "default_engine", "run",
-    "run_segment_parallel", "PARTICLE_DT", "RNG_EXACT", "RNG_PHILOX", "HwwgError", "LIB_PATH"]
+    "run_segment_parallel", "ReferenceSolution", "load_reference", "save_reference",
+    "step_metrics", "PARTICLE_DT", "RNG_EXACT", "RNG_PHILOX", "HwwgError", "LIB_PATH"]

@@ -23,6 +23,7 @@ HWWG_ESTATE = -4
 HWWG_ESINGULAR = -5
 HWWG_ENOSPC = -6
 HWWG_ESTACK = -7
+HWWG_EFORMAT = -8
 RNG_EXACT = 0
 RNG_PHILOX = 1
 
@@ -94,7 +95,7 @@ class RunConfigC(C.Structure):
         ("n_regions", C.c_int32), ("no_pulse", C.c_int32), ("region_x_hi", C.c_double * 8),
         ("region_mat", (C.c_double * 5) * 8), ("vol_x_lo", C.c_double), ("vol_x_hi", C.c_double),
         ("vol_t_lo", C.c_double), ("vol_t_hi", C.c_double), ("vol_rate", C.c_double),
-        ("vol_histories", C.c_uint64)]
+        ("vol_histories", C.c_uint64), ("reference", C.c_char * 256)]
 
 
 class StepRecordC(C.Structure):
@@ -111,7 +112,19 @@ class StepRecordC(C.Structure):
         ("sigma_valid", C.c_int32), ("has_windows", C.c_int32), ("has_hybrid", C.c_int32),
         ("pad_", C.c_int32), ("device_ms", C.c_double), ("transport_ms", C.c_double),
         ("transport_launches", C.c_uint64), ("kernel_launches", C.c_uint64),
-        ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+        ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+        ("rel_l2_error", C.c_double), ("rel_mod_l2_error", C.c_double),
+        ("hybrid_rel_l2_error", C.c_double), ("fom_err_l2", C.c_double),
+        ("fom_err_mod", C.c_double), ("fom_sigma_mod", C.c_double), ("alpha", C.c_double)]
+
+    METRICS = ("rel_l2_error", "rel_mod_l2_error", "hybrid_rel_l2_error", "fom_err_l2",
+               "fom_err_mod", "fom_sigma_l2", "fom_sigma_mod", "alpha")
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        for k in self.METRICS:  # StepMetrics' NaN defaults (metrics.hpp:41-51)
+            if k not in kw:
+                setattr(self, k, float("nan"))
 
 
 # Every symbol include/hwwg.h declares (tests check the library exports them).
@@ -123,7 +136,9 @@ EXPORTS = (
     "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log",
     "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan",
     "hwwg_fourier_lowpass", "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write",
-    "hwwg_loopback_create", "hwwg_loopback_destroy")
+    "hwwg_loopback_create", "hwwg_loopback_destroy", "hwwg_driver_set_reference",
+    "hwwg_driver_load_reference", "hwwg_save_reference_csv", "hwwg_load_reference_csv",
+    "hwwg_time_layers", "hwwg_step_metrics")
 
 _lib = None
 
@@ -183,6 +198,13 @@ def lib():
     L.hwwg_write_summary_csv.argtypes = [C.c_char_p, C.POINTER(StepRecordC), C.c_uint64]
     L.hwwg_write_run_json.argtypes = [C.c_char_p, C.POINTER(RunConfigC), C.c_double, C.c_uint64]
     L.hwwg_driver_write.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_double]
+    L.hwwg_driver_set_reference.argtypes = [C.c_void_p, dptr, dptr, C.c_char_p]
+    L.hwwg_driver_load_reference.argtypes = [C.c_void_p, C.c_char_p]
+    L.hwwg_save_reference_csv.argtypes = [C.c_char_p, C.c_int32, dptr, C.c_int32, dptr, dptr, dptr]
+    L.hwwg_load_reference_csv.argtypes = [C.c_char_p, C.c_int32, dptr, C.c_int32, dptr, dptr, dptr]
+    L.hwwg_time_layers.argtypes = [C.POINTER(RunConfigC), dptr]
+    L.hwwg_step_metrics.argtypes = [C.c_int32, dptr, dptr, dptr, dptr, dptr, dptr, dptr,
+                                    C.POINTER(StepRecordC)]
     _lib = L
     return L
 

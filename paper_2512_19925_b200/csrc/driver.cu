@@ -24,6 +24,7 @@
 #include "driver_host.h"
 #include "engine.cuh"
 #include "low_order.cuh"
+#include "reference_io.h"
 #include "rng.cuh"
 #include "fast.cuh"
 #include "transport.cuh"
@@ -112,6 +113,8 @@ struct hwwg_driver {
   DeviceTallies tal;
   HostTallies host_tal;
   std::vector<double> layers;
+  // deterministic reference for the step diagnostics (hwwg_driver_set_reference)
+  std::vector<double> ref_layer, ref_interval;
   int I = 0, B = 0;
   uint64_t target = 0;
   int next_step = 1;
@@ -1692,18 +1695,13 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   d->h_has_centers = rec->has_windows;
   d->h_has_hybrid = flags[1] != 0;
   rec->tau = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  // FOM without a reference (driver.cpp:272-275; metrics.cpp:34-55)
-  rec->fom_sigma_l2 = NAN;
-  if (rec->sigma_valid) {
-    const double tau = std::max(rec->tau, 1e-9);
-    double sum = 0.0;
-    for (int i = 0; i < I; ++i) {
-      if (d->h_sigma[i] == 0.0) continue;
-      const double fv = 1.0 / (tau * d->h_sigma[i] * d->h_sigma[i]);
-      sum += fv * fv * (d->prob.edges[i + 1] - d->prob.edges[i]);
-    }
-    rec->fom_sigma_l2 = std::sqrt(sum);
-  }
+  // diagnostics, against the reference when one is set (driver.cpp:231-275)
+  const bool ref = !d->ref_interval.empty();
+  step_metrics(I, d->prob.edges.data(), d->h_phi_track.data(), d->h_sigma.data(),
+               d->h_has_hybrid ? d->h_hybrid.data() : nullptr,
+               ref ? d->ref_interval.data() + (size_t)(step - 1) * I : nullptr,
+               ref ? d->ref_layer.data() + (size_t)step * I : nullptr,
+               ref ? d->ref_layer.data() + (size_t)(step - 1) * I : nullptr, rec);
   // state hand-off (driver.cpp:278-281)
   d->has_prev_report = true;
   d->rep_cur ^= 1;
@@ -1819,6 +1817,33 @@ int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma, dou
   if (tracks_per_cell)
     for (int i = 0; i < d->I; ++i) tracks_per_cell[i] = d->h_tracks[i];
   return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_driver_set_reference(hwwg_driver* d, const double* phi_layer,
+                              const double* phi_interval, const char* name) {
+  HWWG_API_BEGIN
+  if (!d || !phi_layer || !phi_interval) return fail(HWWG_EINVAL, "NULL argument");
+  const size_t I = d->I, N = d->cfg.time_steps;
+  if (name) {
+    if (std::strlen(name) >= sizeof d->cfg.reference)
+      return fail(HWWG_EINVAL, "reference name longer than 255 bytes");
+    std::memset(d->cfg.reference, 0, sizeof d->cfg.reference);
+    std::memcpy(d->cfg.reference, name, std::strlen(name));
+  }
+  d->ref_layer.assign(phi_layer, phi_layer + (N + 1) * I);
+  d->ref_interval.assign(phi_interval, phi_interval + N * I);
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_driver_load_reference(hwwg_driver* d, const char* path) {
+  HWWG_API_BEGIN
+  if (!d || !path) return fail(HWWG_EINVAL, "NULL argument");
+  const int I = d->I, N = d->cfg.time_steps;
+  std::vector<double> lay((size_t)(N + 1) * I), itv((size_t)N * I);
+  load_reference(path, I, d->prob.edges.data(), N, d->layers.data(), lay.data(), itv.data());
+  return hwwg_driver_set_reference(d, lay.data(), itv.data(), path);
   HWWG_API_END
 }
 

@@ -292,7 +292,12 @@ int hwwg_load_config_file(const char* path, hwwg_run_config* c) {
         if (!c->vol_histories) c->vol_histories = c->histories_per_step;
       } else if (key == "vol_histories") c->vol_histories = std::stoull(val);
       else if (key == "no_pulse") c->no_pulse = (val == "1" || val == "true") ? 1 : 0;
-      else if (key == "reference" || key == "out_dir") { /* host tooling keys: accepted */ }
+      else if (key == "reference") {  // hww_main.cpp:82
+        if (val.size() >= sizeof c->reference)
+          throw std::invalid_argument("reference path longer than 255 bytes");
+        std::memset(c->reference, 0, sizeof c->reference);
+        std::memcpy(c->reference, val.data(), val.size());
+      } else if (key == "out_dir") { /* host tooling key: accepted */ }
       else throw std::invalid_argument("unknown key '" + key + "'");
     } catch (const std::exception& e) {
       return fail(HWWG_EINVAL, "line " + std::to_string(line_no) + ": " + e.what());

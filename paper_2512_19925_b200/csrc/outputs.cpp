@@ -197,15 +197,15 @@ int hwwg_write_summary_csv(const char* dir, const hwwg_step_record* recs, uint64
          "split_daughters, roulette_kills, roulette_survivals, census_count, "
          "event_cap_aborts, aborted_weight, updates_applied, "
          "hybrid_solve_failed\n";
-  // without a deterministic S_N reference the error metrics, fom_sigma_mod and
-  // alpha stay NaN (metrics.hpp:41-48; driver.cpp:268-271)
-  const double nan = std::numeric_limits<double>::quiet_NaN();
+  // the metric fields are NaN unless the step ran against a reference
+  // (metrics.hpp:41-51; driver.cpp:231-275)
   for (uint64_t k = 0; k < n; ++k) {
     const hwwg_step_record& s = recs[k];
     const hwwg_counters& c = s.counters;
-    out << s.step << ", " << s.t_end << ", " << s.histories << ", " << s.tau << ", " << nan
-        << ", " << nan << ", " << nan << ", " << nan << ", " << nan << ", " << s.fom_sigma_l2
-        << ", " << nan << ", " << nan << ", " << s.census_weight << ", "
+    out << s.step << ", " << s.t_end << ", " << s.histories << ", " << s.tau << ", "
+        << s.rel_l2_error << ", " << s.rel_mod_l2_error << ", " << s.hybrid_rel_l2_error
+        << ", " << s.fom_err_l2 << ", " << s.fom_err_mod << ", " << s.fom_sigma_l2 << ", "
+        << s.fom_sigma_mod << ", " << s.alpha << ", " << s.census_weight << ", "
         << s.census_weight_sigma << ", " << s.comb_in << ", " << s.comb_out << ", "
         << c.leakage_weight << ", " << c.collisions << ", " << c.splits << ", "
         << c.split_daughters << ", " << c.roulette_kills << ", " << c.roulette_survivals
@@ -258,7 +258,7 @@ int hwwg_write_run_json(const char* dir, const hwwg_run_config* c, double total_
   tm.obj["t_end"] = JVal::F(c->t_end);
   tm.obj["steps"] = JVal::I(c->time_steps);
   cfg.obj["time"] = tm;
-  cfg.obj["reference"] = JVal::S("");  // this engine carries no S_N reference
+  cfg.obj["reference"] = JVal::S(std::string(c->reference, strnlen(c->reference, sizeof c->reference)));
   cfg.obj["threads"] = JVal::I(c->threads);
   JVal root = JVal::O();
   root.obj["config"] = cfg;

@@ -366,6 +366,9 @@ class RunConfig:
     threads: int = 0
     host_bank: bool = False
     out_dir: str = ""  # config.hpp:63: empty -> no file output
+    # config.hpp:64 ("auto" | file path | ""): carried to run.json; the driver
+    # takes the reference itself (Driver.set_reference / run(reference=...))
+    reference: str = ""
     # Config-3 extensions (absent from the
     # reference driver): material regions [(x_hi, Material), ...] (a cell takes
     # the first region whose x_hi exceeds its centre), an isotropic volumetric
@@ -407,7 +410,21 @@ class RunConfig:
             (c.vol_x_lo, c.vol_x_hi, c.vol_t_lo, c.vol_t_hi, c.vol_rate) = self.volume_source
             c.vol_histories = self.vol_histories or self.histories_per_step
         c.no_pulse = 1 if self.no_pulse else 0
+        ref = self.reference.encode()
+        if len(ref) >= 256:
+            raise ValueError("reference path longer than 255 bytes")
+        c.reference = ref
         return c
+
+    def make_mesh(self):
+        """config.hpp:87."""
+        return build_uniform_mesh(self.x_min, self.x_max, self.cells)
+
+    def time_layers(self):
+        """make_time_grid().layer(0..N) (config.hpp:88; time_grid.hpp:22-29)."""
+        out = np.zeros(self.time_steps + 1)
+        _raise(A.lib().hwwg_time_layers(C.byref(self.to_c()), A.as_dptr(out)))
+        return out
 
     @staticmethod
     def from_file(path) -> "RunConfig":
@@ -432,7 +449,7 @@ class RunConfig:
             volume_source=((c.vol_x_lo, c.vol_x_hi, c.vol_t_lo, c.vol_t_hi, c.vol_rate)
                            if c.vol_rate > 0.0 else None),
             vol_histories=c.vol_histories if c.vol_rate > 0.0 else 0,
-            no_pulse=bool(c.no_pulse))
+            no_pulse=bool(c.no_pulse), reference=c.reference.decode())
 
     def validate(self):
         """validate_config (config.cpp:27-69): list of violations."""
@@ -489,6 +506,22 @@ class Driver:
         of the last step and summary.csv of all steps; run.json when final."""
         _raise(A.lib().hwwg_driver_write(self._h, str(out_dir).encode(), 1 if final else 0,
                                          float(total_seconds)))
+
+    def set_reference(self, ref: "ReferenceSolution", name=None):
+        """Run every following step against `ref` (hww::run's ReferenceSolution*,
+        driver.hpp:88): the step records then carry rel_l2_error, rel_mod_l2_error,
+        hybrid_rel_l2_error, fom_err_l2/mod, fom_sigma_mod and alpha."""
+        lay = np.ascontiguousarray(ref.phi_layer, np.float64)
+        itv = np.ascontiguousarray(ref.phi_interval, np.float64)
+        if lay.shape != (self.config.time_steps + 1, self.I) or \
+                itv.shape != (self.config.time_steps, self.I):
+            raise ValueError("reference shape does not match the run's mesh and time grid")
+        _raise(A.lib().hwwg_driver_set_reference(
+            self._h, A.as_dptr(lay), A.as_dptr(itv), None if name is None else str(name).encode()))
+
+    def load_reference(self, path):
+        """load_reference(path, mesh, tgrid) + set_reference (hww_main.cpp:250-252)."""
+        _raise(A.lib().hwwg_driver_load_reference(self._h, str(path).encode()))
 
     def bank(self):
         n = C.c_uint64()
@@ -571,7 +604,8 @@ def rebalance_plan(k_lo_all, k_hi_all, rank, H):
     return send, first, recv
 
 
-def run(config: RunConfig, device=0, rng_mode=RNG_EXACT, out_dir=None):
+def run(config: RunConfig, device=0, rng_mode=RNG_EXACT, out_dir=None,
+        reference: "Optional[ReferenceSolution]" = None):
     """hww::run (driver.hpp:88, driver.cpp:286-342): returns the list of
     (record, arrays) per step. With out_dir (or config.out_dir) the reference's
     files are written as it writes them: step_<n>.csv and summary.csv after every
@@ -580,6 +614,8 @@ def run(config: RunConfig, device=0, rng_mode=RNG_EXACT, out_dir=None):
     import time
     out_dir = out_dir if out_dir is not None else getattr(config, "out_dir", "")
     d = Driver(config, device, rng_mode)
+    if reference is not None:
+        d.set_reference(reference)
     out = []
     t0 = time.perf_counter()
     try:
@@ -599,3 +635,62 @@ def run(config: RunConfig, device=0, rng_mode=RNG_EXACT, out_dir=None):
     finally:
         d.close()
     return out
+
+
+# ------------------------------------------------- deterministic reference
+class ReferenceSolution:
+    """hww::ReferenceSolution (reference.hpp:76-85): layer values phi_layer[0..N]
+    and interval averages phi_interval[0..N-1] (steps 1..N) on the tally grids."""
+
+    def __init__(self, mesh: Mesh1D, layers, phi_layer, phi_interval):
+        self.mesh = mesh
+        self.layers = np.ascontiguousarray(layers, np.float64)
+        self.phi_layer = np.ascontiguousarray(phi_layer, np.float64)
+        self.phi_interval = np.ascontiguousarray(phi_interval, np.float64)
+        N, I = self.layers.size - 1, mesh.cells()
+        if self.phi_layer.shape != (N + 1, I) or self.phi_interval.shape != (N, I):
+            raise ValueError("reference arrays do not match the mesh and time grid")
+
+    def layer(self, n):
+        return self.phi_layer[n]
+
+    def interval_avg(self, step):
+        return self.phi_interval[step - 1]
+
+
+def save_reference(ref: ReferenceSolution, path):
+    """hww::save_reference (reference.cpp:374-393): same bytes."""
+    N, I = ref.layers.size - 1, ref.mesh.cells()
+    _raise(A.lib().hwwg_save_reference_csv(
+        str(path).encode(), I, A.as_dptr(ref.mesh.edges), N, A.as_dptr(ref.layers),
+        A.as_dptr(ref.phi_layer), A.as_dptr(ref.phi_interval)))
+
+
+def load_reference(path, mesh: Mesh1D, layers) -> ReferenceSolution:
+    """hww::load_reference (reference.cpp:395-456). Raises RuntimeError (the
+    reference's std::runtime_error) on a missing, malformed or mis-shaped file."""
+    layers = np.ascontiguousarray(layers, np.float64)
+    N, I = layers.size - 1, mesh.cells()
+    lay, itv = np.zeros((N + 1, I)), np.zeros((N, I))
+    _raise(A.lib().hwwg_load_reference_csv(str(path).encode(), I, A.as_dptr(mesh.edges), N,
+                                           A.as_dptr(layers), A.as_dptr(lay), A.as_dptr(itv)))
+    return ReferenceSolution(mesh, layers, lay, itv)
+
+
+def step_metrics(mesh: Mesh1D, rec, phi_track, phi_sigma=None, phi_hybrid=None,
+                 reference: Optional[ReferenceSolution] = None):
+    """hww::run_step's diagnostics (driver.cpp:231-275) for the step rec.step from
+    its arrays and rec.tau / rec.sigma_valid; fills rec's metric fields."""
+    edges = mesh.edges
+    cvt = (lambda a: None if a is None else np.ascontiguousarray(a, np.float64))
+    phi_track, phi_sigma, phi_hybrid = cvt(phi_track), cvt(phi_sigma), cvt(phi_hybrid)
+    n = rec.step
+    ri = rl = rp = None
+    if reference is not None:
+        ri = np.ascontiguousarray(reference.interval_avg(n))
+        rl = np.ascontiguousarray(reference.layer(n))
+        rp = np.ascontiguousarray(reference.layer(n - 1))
+    _raise(A.lib().hwwg_step_metrics(mesh.cells(), A.as_dptr(edges), A.as_dptr(phi_track),
+                                     A.as_dptr(phi_sigma), A.as_dptr(phi_hybrid), A.as_dptr(ri),
+                                     A.as_dptr(rl), A.as_dptr(rp), C.byref(rec)))
+    return rec

@@ -214,3 +214,39 @@ def test_fixed_point_dynamic_range_guard(monkeypatch):
     assert rq.segments == rd.segments
     for k in ("phi_census", "phi_track"):
         np.testing.assert_allclose(aq[k], ad[k], rtol=1e-12, atol=1e-14 * ad[k].max(), err_msg=k)
+
+
+@pytest.mark.gpu
+def test_philox_error_metrics_against_sn_reference(tmp_path):
+    """The throughput engine run against the reference's S_N solution (written by
+    hww::save_reference, read by the engine's loader): the step error metrics
+    exist every step and the track flux is close to the deterministic interval
+    average (config 1 at 2e5 histories: relative L2 error of a few percent),
+    and they match the exact engine's metrics statistically."""
+    from oracle import bind
+    from paper_2512_19925_b200 import hww
+    if not bind.have_reference():
+        pytest.skip("oracle/_ref not built")
+    R = bind.Reference()
+    r = bind.baseline_config(1, histories=200000, time_steps=6)
+    h = hww.RunConfig(mode="hww_ma", ma_base_k=3, histories_per_step=200000, rho=5.0, seed=42,
+                      material=hww.Material(1.0, 1.0, 0.0, 0.0, 1.0), x_min=-20.0, x_max=20.0,
+                      cells=200, t_end=r.t_end, time_steps=6)
+    path = tmp_path / "reference.csv"
+    R.save_reference(r, path, *R.compute_reference(r))
+    errs = {}
+    for mode in (hww.RNG_PHILOX, hww.RNG_EXACT):
+        d = hww.Driver(h, rng_mode=mode)
+        d.load_reference(path)
+        errs[mode] = []
+        for _ in range(6):
+            rec = d.step()
+            assert np.isfinite(rec.rel_l2_error) and np.isfinite(rec.alpha)
+            assert np.isfinite(rec.fom_err_l2) and np.isfinite(rec.fom_sigma_mod)
+            assert np.isfinite(rec.hybrid_rel_l2_error)
+            errs[mode].append(rec.rel_l2_error)
+        d.close()
+    ph, ex = np.array(errs[hww.RNG_PHILOX]), np.array(errs[hww.RNG_EXACT])
+    assert np.all(ph < 0.1) and np.all(ex < 0.1), (ph, ex)
+    # same estimator: the errors agree to within their own spread
+    assert abs(ph.mean() - ex.mean()) < 0.5 * max(ph.mean(), ex.mean()), (ph, ex)

@@ -36,7 +36,11 @@ def _records(rng, I, n, with_windows):
              "normalization": 1000.0, "sigma_valid": 1.0 if k != 1 else 0.0,
              "hybrid_solve_failed": 1.0 if k == 2 else 0.0, "step": k + 1,
              "histories": 1000 + k, "comb_in": 5000 + k, "comb_out": 1000,
-             "updates_applied": 3 - (k == 2)}
+             "updates_applied": 3 - (k == 2),
+             # reference diagnostics: some steps without a reference (NaN), some with
+             "metrics": tuple(float("nan") if (k % 2 and j != 6) else
+                              float(rng.random() * 10.0 ** rng.integers(-6, 20))
+                              for j in range(7))}
         cn = bind.Counters()
         for j, (f, _) in enumerate(cn._fields_):
             setattr(cn, f, float(rng.random() * 7) if f.endswith("weight") else int(rng.integers(0, 10**12)))
@@ -54,6 +58,9 @@ def _ours(out_dir, cfg_h, steps, edges, total_seconds):
         r.sigma_valid, r.hybrid_solve_failed = int(s["sigma_valid"]), int(s["hybrid_solve_failed"])
         r.histories, r.comb_in, r.comb_out = s["histories"], s["comb_in"], s["comb_out"]
         r.updates_applied = s["updates_applied"]
+        for f, v in zip(("rel_l2_error", "rel_mod_l2_error", "hybrid_rel_l2_error", "fom_err_l2",
+                         "fom_err_mod", "fom_sigma_mod", "alpha"), s["metrics"]):
+            setattr(r, f, v)
         for f, _ in s["counters"]._fields_:
             setattr(r.counters, f, getattr(s["counters"], f))
     d = str(out_dir).encode()
@@ -130,12 +137,26 @@ def _mask_summary(p):
 
 @pytest.mark.gpu
 @needs_ref
-@pytest.mark.parametrize("mode", ["hww_ma", "analog"])
-def test_exact_run_outputs_match_reference_run(tmp_path, mode):
+@pytest.mark.parametrize("mode,with_reference", [("hww_ma", False), ("analog", False),
+                                                 ("hww_ma", True), ("analog", True)])
+def test_exact_run_outputs_match_reference_run(tmp_path, mode, with_reference):
+    """With a reference file (hww_main.cpp:250-256) the summary's error metrics
+    (rel_l2_error, rel_mod_l2_error, hybrid_rel_l2_error, alpha) must match byte
+    for byte too; the FOM columns carry the wall-clock tau and stay masked."""
     cfg_h, cfg_r = _cfg_pair(mode=mode, cells=80)
     ref_dir, our_dir = tmp_path / "ref", tmp_path / "ours"
-    bind.Reference().run_to_dir(cfg_r, ref_dir)
-    hww.run(cfg_h, rng_mode=hww.RNG_EXACT, out_dir=str(our_dir))
+    R = bind.Reference()
+    reference = None
+    if with_reference:
+        path = tmp_path / "reference.csv"
+        R.save_reference(cfg_r, path, *R.compute_reference(cfg_r, 3, 8, 8))
+        cfg_h.reference = str(path)
+        reference = hww.load_reference(path, cfg_h.make_mesh(), cfg_h.time_layers())
+    R.run_to_dir(cfg_r, ref_dir, reference=cfg_h.reference)
+    hww.run(cfg_h, rng_mode=hww.RNG_EXACT, out_dir=str(our_dir), reference=reference)
+    if with_reference:
+        rows = _slurp(our_dir / "summary.csv").decode().splitlines()[1:]
+        assert all("nan" not in r.split(",")[4] for r in rows)
     for k in range(1, cfg_h.time_steps + 1):
         assert _slurp(our_dir / f"step_{k}.csv") == _slurp(ref_dir / f"step_{k}.csv"), k
     assert _mask_summary(our_dir / "summary.csv") == _mask_summary(ref_dir / "summary.csv")
