@@ -266,6 +266,10 @@ int hwwg_driver_set_reference(hwwg_driver* d, const double* phi_layer,
 /* hww::load_reference on the driver's own mesh and time grid, then
  * hwwg_driver_set_reference(d, ..., path) (hww_main.cpp:250-252). */
 int hwwg_driver_load_reference(hwwg_driver* d, const char* path);
+/* reference = "auto" (hww_main.cpp:240-249): hww::compute_reference on the driver's
+ * device (hwwg_compute_reference), then hwwg_driver_set_reference(d, ..., "auto"). */
+int hwwg_driver_compute_reference(hwwg_driver* d, int32_t space_refine, int32_t time_refine,
+                                  int32_t sn_order);
 /* Key = value config file (proj/tools/hww_main.cpp:20-92 key names). */
 int hwwg_load_config_file(const char* path, hwwg_run_config* cfg);
 /* Reference defaults (config.hpp:33-66). */
@@ -320,6 +324,30 @@ int hwwg_step_metrics(int32_t cells, const double* edges, const double* phi_trac
                       const double* phi_sigma, const double* phi_hybrid,
                       const double* ref_interval, const double* ref_layer,
                       const double* ref_layer_prev, hwwg_step_record* rec);
+
+/* ------------------------------------------------------ S_N reference */
+/* GaussLegendre::order (reference.cpp:14-42): same nodes and weights. */
+int hwwg_gauss_legendre(int32_t n, double* mu, double* weight);
+/* hww::sn_solve (reference.cpp:151-233) on the device: diamond difference in space,
+ * backward Euler in time, source iteration to `tolerance` (max-norm, relative) on the
+ * isotropic scatter + fission source.  psi0[order*cells] ([k*cells + i]); inc_left /
+ * inc_right[order] (NULL = vacuum); q[cells] source density constant in time (NULL =
+ * none).  Outputs (NULL to skip): phi_layers[(steps+1)*cells] scalar flux per layer,
+ * iterations[steps+1].  Non-convergence is HWWG_ESINGULAR with the reference's
+ * message.  One persistent cooperative launch, one CTA per direction (order <= 256). */
+int hwwg_sn_solve(hwwg_ctx* ctx, int32_t cells, const double* edges,
+                  const hwwg_material* materials, int32_t steps, const double* layers,
+                  int32_t order, const double* psi0, const double* inc_left,
+                  const double* inc_right, const double* q, double tolerance,
+                  int32_t max_iterations, double* phi_layers, int32_t* iterations);
+/* hww::compute_reference (reference.cpp:302-372) on the device: the pulse problem on
+ * a mesh refined space_refine times per cell and time_refine layers per step, S_N of
+ * sn_order, projected onto cfg's tally grids (phi_layer[(N+1)*I], phi_interval[N*I],
+ * the ReferenceSolution layout).  Config-3 extensions: material regions per tally
+ * cell, no_pulse, and the volumetric source as a time-boxed q. */
+int hwwg_compute_reference(hwwg_ctx* ctx, const hwwg_run_config* cfg, int32_t space_refine,
+                           int32_t time_refine, int32_t sn_order, double* phi_layer,
+                           double* phi_interval);
 
 /* ----------------------------------------------------- device components */
 /* hww::assemble_solve (losm.cpp:143-165) on the device, single CTA.

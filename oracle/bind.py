@@ -348,6 +348,34 @@ class Reference(_Lib):
             raise RuntimeError(self.err())
         return lay, itv
 
+    def gauss_legendre(self, n):
+        mu, w = np.zeros(n), np.zeros(n)
+        L = self.lib
+        L.hwwref_gauss_legendre.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        if L.hwwref_gauss_legendre(n, _dp(mu), _dp(w)) != 0:
+            raise ValueError(self.err())
+        return mu, w
+
+    def sn_solve(self, edges, mats, layers, order, psi0, inc_left, inc_right, q,
+                 tolerance=1e-9, max_iterations=1000):
+        """hww::sn_solve (reference.cpp:151-233): (phi per layer, iterations per step)."""
+        edges = np.ascontiguousarray(edges, np.float64)
+        I = edges.size - 1
+        mats = np.ascontiguousarray(mats, np.float64).reshape(I, 5)
+        layers = np.ascontiguousarray(layers, np.float64)
+        N = layers.size - 1
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (psi0, inc_left, inc_right, q)]
+        phi, its = np.zeros((N + 1, I)), np.zeros(N + 1, np.int32)
+        L = self.lib
+        dp = C.POINTER(C.c_double)
+        L.hwwref_sn_solve.argtypes = [C.c_int32, dp, C.c_void_p, C.c_int32, dp, C.c_int32, dp,
+                                      dp, dp, dp, C.c_double, C.c_int32, dp, C.c_void_p]
+        if L.hwwref_sn_solve(I, _dp(edges), mats.ctypes.data, N, _dp(layers), order,
+                             *[_dp(a) for a in arrs], tolerance, max_iterations, _dp(phi),
+                             its.ctypes.data) != 0:
+            raise RuntimeError(self.err())
+        return phi, its
+
     def save_reference(self, config: Config, path, phi_layer, phi_interval):
         lay = np.ascontiguousarray(phi_layer, np.float64)
         itv = np.ascontiguousarray(phi_interval, np.float64)

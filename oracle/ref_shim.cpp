@@ -716,6 +716,53 @@ int hwwref_load_reference(const hwwref_config* c, const char* path, double* phi_
   }
 }
 
+// GaussLegendre::order (reference.cpp:14-42).
+int hwwref_gauss_legendre(int32_t n, double* mu, double* w) {
+  try {
+    const auto q = hww::GaussLegendre::order(n);
+    std::memcpy(mu, q.mu.data(), n * sizeof(double));
+    std::memcpy(w, q.weight.data(), n * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// hww::sn_solve (reference.cpp:151-233) on a problem given as arrays; writes the
+// scalar flux of every layer and the source-iteration count of every step.
+int hwwref_sn_solve(int32_t cells, const double* edges, const hwwref_material* mats,
+                    int32_t steps, const double* layers, int32_t order, const double* psi0,
+                    const double* inc_left, const double* inc_right, const double* q,
+                    double tolerance, int32_t max_iterations, double* phi_layers,
+                    int32_t* iterations) {
+  try {
+    hww::SnProblem prob;
+    prob.mesh = hww::Mesh1D::from_edges(std::vector<double>(edges, edges + cells + 1));
+    for (int i = 0; i < cells; ++i)
+      prob.materials.push_back(
+          {mats[i].sigma_t, mats[i].sigma_s, mats[i].sigma_f, mats[i].nu_f, mats[i].speed});
+    prob.tgrid = hww::TimeGrid::from_layers(std::vector<double>(layers, layers + steps + 1));
+    prob.psi0.assign(psi0, psi0 + (size_t)order * cells);
+    prob.inc_left.assign(inc_left, inc_left + order);
+    prob.inc_right.assign(inc_right, inc_right + order);
+    prob.q.assign(q, q + cells);
+    hww::SnConfig sn;
+    sn.quadrature_order = order;
+    sn.tolerance = tolerance;
+    sn.max_iterations = max_iterations;
+    const hww::SnSolution sol = hww::sn_solve(prob, sn);
+    for (int n = 0; n <= steps; ++n) {
+      std::memcpy(phi_layers + (size_t)n * cells, sol.layers[n].phi.data(), cells * sizeof(double));
+      iterations[n] = sol.iterations[n];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // hww::build_uniform_mesh edges (proj/src/mesh.cpp:42-50).
 // hww::run with out_dir (proj/src/driver.cpp:286-342): the reference's own
 // writers produce step_<n>.csv, summary.csv and run.json in dir.

@@ -8,10 +8,11 @@ from ._capi import PARTICLE_DT, RNG_EXACT, RNG_PHILOX, HwwgError, LIB_PATH  # no
 from .hww import (  # noqa: F401
     Driver, Engine, Loopback, Material, Mesh1D, RunConfig, StepContext, StepOutcome, TallySet,
     WeightWindowGrid, build_uniform_mesh, default_engine, run, run_segment_parallel,
-    ReferenceSolution, load_reference, save_reference, step_metrics)
+    ReferenceSolution, load_reference, save_reference, step_metrics, gauss_legendre, sn_solve,
+    compute_reference)
 
 __all__ = [
     "Driver", "Engine", "Loopback", "Material", "Mesh1D", "RunConfig", "StepContext", "StepOutcome",
     "TallySet", "WeightWindowGrid", "build_uniform_mesh", "default_engine", "run",
     "run_segment_parallel", "ReferenceSolution", "load_reference", "save_reference",
-    "step_metrics", "PARTICLE_DT", "RNG_EXACT", "RNG_PHILOX", "HwwgError", "LIB_PATH"]
+    "step_metrics", "gauss_legendre", "sn_solve", "compute_reference", "PARTICLE_DT", "RNG_EXACT", "RNG_PHILOX", "HwwgError", "LIB_PATH"]

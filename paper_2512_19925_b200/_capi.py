@@ -138,7 +138,8 @@ EXPORTS = (
     "hwwg_fourier_lowpass", "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write",
     "hwwg_loopback_create", "hwwg_loopback_destroy", "hwwg_driver_set_reference",
     "hwwg_driver_load_reference", "hwwg_save_reference_csv", "hwwg_load_reference_csv",
-    "hwwg_time_layers", "hwwg_step_metrics")
+    "hwwg_time_layers", "hwwg_step_metrics", "hwwg_gauss_legendre", "hwwg_sn_solve",
+    "hwwg_compute_reference", "hwwg_driver_compute_reference")
 
 _lib = None
 
@@ -203,6 +204,13 @@ def lib():
     L.hwwg_save_reference_csv.argtypes = [C.c_char_p, C.c_int32, dptr, C.c_int32, dptr, dptr, dptr]
     L.hwwg_load_reference_csv.argtypes = [C.c_char_p, C.c_int32, dptr, C.c_int32, dptr, dptr, dptr]
     L.hwwg_time_layers.argtypes = [C.POINTER(RunConfigC), dptr]
+    L.hwwg_gauss_legendre.argtypes = [C.c_int32, dptr, dptr]
+    L.hwwg_sn_solve.argtypes = [C.c_void_p, C.c_int32, dptr, C.c_void_p, C.c_int32, dptr,
+                                C.c_int32, dptr, dptr, dptr, dptr, C.c_double, C.c_int32, dptr,
+                                C.c_void_p]
+    L.hwwg_compute_reference.argtypes = [C.c_void_p, C.POINTER(RunConfigC), C.c_int32,
+                                         C.c_int32, C.c_int32, dptr, dptr]
+    L.hwwg_driver_compute_reference.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]
     L.hwwg_step_metrics.argtypes = [C.c_int32, dptr, dptr, dptr, dptr, dptr, dptr, dptr,
                                     C.POINTER(StepRecordC)]
     _lib = L

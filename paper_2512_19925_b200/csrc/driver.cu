@@ -25,6 +25,7 @@
 #include "engine.cuh"
 #include "low_order.cuh"
 #include "reference_io.h"
+#include "sn.cuh"
 #include "rng.cuh"
 #include "fast.cuh"
 #include "transport.cuh"
@@ -1844,6 +1845,18 @@ int hwwg_driver_load_reference(hwwg_driver* d, const char* path) {
   std::vector<double> lay((size_t)(N + 1) * I), itv((size_t)N * I);
   load_reference(path, I, d->prob.edges.data(), N, d->layers.data(), lay.data(), itv.data());
   return hwwg_driver_set_reference(d, lay.data(), itv.data(), path);
+  HWWG_API_END
+}
+
+int hwwg_driver_compute_reference(hwwg_driver* d, int32_t space_refine, int32_t time_refine,
+                                  int32_t sn_order) {
+  HWWG_API_BEGIN
+  if (!d) return fail(HWWG_EINVAL, "NULL argument");
+  const int I = d->I, N = d->cfg.time_steps;
+  std::vector<double> lay((size_t)(N + 1) * I), itv((size_t)N * I);
+  const SnHostProblem p = reference_problem(d->cfg, space_refine, time_refine, sn_order);
+  sn_solve_device(p, d->opt.device, d->stream, nullptr, nullptr, lay.data(), itv.data());
+  return hwwg_driver_set_reference(d, lay.data(), itv.data(), "auto");
   HWWG_API_END
 }
 

@@ -14,6 +14,7 @@
 #include "device_state.cuh"
 #include "engine.cuh"
 #include "low_order.cuh"
+#include "sn.cuh"
 #include "transport.cuh"
 
 namespace hwwg {
@@ -542,6 +543,54 @@ int hwwg_internal_losm_cache_check(hwwg_ctx* c, int32_t I, uint32_t seed, double
   }
   *max_abs_diff = mx;
   return diff;
+  HWWG_API_END
+}
+
+int hwwg_gauss_legendre(int32_t n, double* mu, double* weight) {
+  HWWG_API_BEGIN
+  if (!mu || !weight) return fail(HWWG_EINVAL, "NULL argument");
+  gauss_legendre(n, mu, weight);
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_sn_solve(hwwg_ctx* c, int32_t cells, const double* edges,
+                  const hwwg_material* materials, int32_t steps, const double* layers,
+                  int32_t order, const double* psi0, const double* inc_left,
+                  const double* inc_right, const double* q, double tolerance,
+                  int32_t max_iterations, double* phi_layers, int32_t* iterations) {
+  HWWG_API_BEGIN
+  if (!c || !edges || !materials || !layers || !psi0 || cells < 1 || steps < 1 || order < 1)
+    return fail(HWWG_EINVAL, "NULL argument");
+  SnHostProblem p;
+  p.edges.assign(edges, edges + cells + 1);
+  p.materials.assign(materials, materials + cells);
+  p.layers.assign(layers, layers + steps + 1);
+  p.order = order;
+  p.psi0.assign(psi0, psi0 + (size_t)order * cells);
+  p.inc_left = inc_left ? std::vector<double>(inc_left, inc_left + order)
+                        : std::vector<double>(order, 0.0);
+  p.inc_right = inc_right ? std::vector<double>(inc_right, inc_right + order)
+                          : std::vector<double>(order, 0.0);
+  if (q) {  // constant in time (SnProblem::q): one row for every step
+    p.q_rows.assign(q, q + cells);
+    p.q_index.assign(steps + 1, 0);
+  }
+  p.tolerance = tolerance;
+  p.max_iterations = max_iterations;
+  sn_solve_device(p, c->device, c->stream, phi_layers, iterations, nullptr, nullptr);
+  return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_compute_reference(hwwg_ctx* c, const hwwg_run_config* cfg, int32_t space_refine,
+                           int32_t time_refine, int32_t sn_order, double* phi_layer,
+                           double* phi_interval) {
+  HWWG_API_BEGIN
+  if (!c || !cfg || !phi_layer || !phi_interval) return fail(HWWG_EINVAL, "NULL argument");
+  const SnHostProblem p = reference_problem(*cfg, space_refine, time_refine, sn_order);
+  sn_solve_device(p, c->device, c->stream, nullptr, nullptr, phi_layer, phi_interval);
+  return HWWG_OK;
   HWWG_API_END
 }
 

@@ -27,8 +27,9 @@ MODES = ("analog", "lww", "hww", "hww_ma", "hww_fourier")
 def _raise(rc):
     if rc < 0:
         msg = A.lib().hwwg_last_error().decode()
-        if rc in (A.HWWG_EINVAL, A.HWWG_ESINGULAR):
+        if rc == A.HWWG_EINVAL:  # std::invalid_argument
             raise ValueError(msg)
+        # HWWG_ESINGULAR / HWWG_EFORMAT: the reference's std::runtime_error
         raise HwwgError(rc, msg)
     return rc
 
@@ -523,6 +524,11 @@ class Driver:
         """load_reference(path, mesh, tgrid) + set_reference (hww_main.cpp:250-252)."""
         _raise(A.lib().hwwg_driver_load_reference(self._h, str(path).encode()))
 
+    def compute_reference(self, space_refine=5, time_refine=20, sn_order=16):
+        """reference = "auto" (hww_main.cpp:240-249): the device S_N reference."""
+        _raise(A.lib().hwwg_driver_compute_reference(self._h, space_refine, time_refine,
+                                                     sn_order))
+
     def bank(self):
         n = C.c_uint64()
         A.lib().hwwg_driver_bank(self._h, None, 0, C.byref(n))
@@ -694,3 +700,43 @@ def step_metrics(mesh: Mesh1D, rec, phi_track, phi_sigma=None, phi_hybrid=None,
                                      A.as_dptr(phi_sigma), A.as_dptr(phi_hybrid), A.as_dptr(ri),
                                      A.as_dptr(rl), A.as_dptr(rp), C.byref(rec)))
     return rec
+
+
+# ------------------------------------------------------ S_N reference (f4)
+def gauss_legendre(n):
+    """GaussLegendre::order (reference.cpp:14-42): (mu, weight)."""
+    mu, w = np.zeros(n), np.zeros(n)
+    _raise(A.lib().hwwg_gauss_legendre(n, A.as_dptr(mu), A.as_dptr(w)))
+    return mu, w
+
+
+def sn_solve(mesh: Mesh1D, materials, layers, order, psi0, inc_left=None, inc_right=None,
+             q=None, tolerance=1e-9, max_iterations=1000, engine=None):
+    """hww::sn_solve (reference.cpp:151-233) on the device: (phi per layer
+    [(steps+1), cells], source iterations per step). RuntimeError (the reference's
+    std::runtime_error) when a step does not converge."""
+    eng = engine or default_engine()
+    I = mesh.cells()
+    mats = _materials_array(materials, I)
+    layers = np.ascontiguousarray(layers, np.float64)
+    N = layers.size - 1
+    psi0 = np.ascontiguousarray(psi0, np.float64)
+    cvt = (lambda a: None if a is None else np.ascontiguousarray(a, np.float64))
+    inc_left, inc_right, q = cvt(inc_left), cvt(inc_right), cvt(q)
+    phi, its = np.zeros((N + 1, I)), np.zeros(N + 1, np.int32)
+    _raise(A.lib().hwwg_sn_solve(eng._h, I, A.as_dptr(mesh.edges), mats.ctypes.data, N,
+                                 A.as_dptr(layers), order, A.as_dptr(psi0), A.as_dptr(inc_left),
+                                 A.as_dptr(inc_right), A.as_dptr(q), tolerance, max_iterations,
+                                 A.as_dptr(phi), its.ctypes.data))
+    return phi, its
+
+
+def compute_reference(config: RunConfig, space_refine=5, time_refine=20, sn_order=16,
+                      engine=None) -> ReferenceSolution:
+    """hww::compute_reference (reference.cpp:364-372) on the device."""
+    eng = engine or default_engine()
+    N, I = config.time_steps, config.cells
+    lay, itv = np.zeros((N + 1, I)), np.zeros((N, I))
+    _raise(A.lib().hwwg_compute_reference(eng._h, C.byref(config.to_c()), space_refine,
+                                          time_refine, sn_order, A.as_dptr(lay), A.as_dptr(itv)))
+    return ReferenceSolution(config.make_mesh(), config.time_layers(), lay, itv)
