@@ -231,7 +231,10 @@ typedef struct {
   int32_t sigma_valid;
   int32_t has_windows;
   int32_t has_hybrid;
-  int32_t pad_;
+  /* 1: the step's census was thinned on the fly (throughput mode): the bank the
+   * next comb reads holds ~k x target records of weight n * s0 (an unbiased
+   * equal-quantum restatement of the census), not census_size */
+  int32_t thinned;
   double device_ms;    /* CUDA-event time of the whole step on the engine stream */
   double transport_ms; /* CUDA-event time of the transport (history) kernels only */
   uint64_t transport_launches; /* transport kernel launches in the step */

@@ -110,7 +110,7 @@ class StepRecordC(C.Structure):
         ("census_weight_sigma", C.c_double), ("boundary_closure_left", C.c_double),
         ("boundary_closure_right", C.c_double), ("fom_sigma_l2", C.c_double),
         ("sigma_valid", C.c_int32), ("has_windows", C.c_int32), ("has_hybrid", C.c_int32),
-        ("pad_", C.c_int32), ("device_ms", C.c_double), ("transport_ms", C.c_double),
+        ("thinned", C.c_int32), ("device_ms", C.c_double), ("transport_ms", C.c_double),
         ("transport_launches", C.c_uint64), ("kernel_launches", C.c_uint64),
         ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
         ("rel_l2_error", C.c_double), ("rel_mod_l2_error", C.c_double),

@@ -215,6 +215,13 @@ struct hwwg_driver {
   unsigned timeline_warps = 0;
   DevBuf<unsigned long long> warp_cursor;  // per-warp census chunks
   int max_warps = 0;
+  // census thinning (FastArgs::precomb): on in the cold start and whenever the
+  // previous census held more than precomb_k x target particles; the thinned
+  // census holds ~precomb_k x target records (HWWG_PRECOMB=0 disables it,
+  // HWWG_PRECOMB_K sets k)
+  int precomb = 1;
+  double precomb_k = 8.0;
+  DevBuf<double> pc_need;  // per-lane comb residuals (32 per warp)
 
   // multi-GPU: histories sharded by rank, tallies all-reduced
   // at every window-update barrier and at step end, census combed globally and
@@ -437,7 +444,10 @@ void init_driver(hwwg_driver* d) {
     // Everything a step can grow into is allocated here, up front: a cudaMalloc
     // inside a step synchronises the device (the step-1 census is x60+ of H,
     // and it becomes step 2's comb input in the other bank of the swap pair).
-    d->census_hwm = d->census_floor = 64 * local_target + 4096;
+    // (with census thinning the cold start banks ~precomb_k x H records, not the
+    // x60-x150 raw census; a larger census replays its step with room)
+    const uint64_t mult = d->precomb ? (uint64_t)(2.0 * d->precomb_k) : 64;
+    d->census_hwm = d->census_floor = mult * local_target + 4096;
     d->fcensus.reserve(d->census_hwm);
     d->fbank.reserve(d->census_hwm);
     d->fsrc.reserve(std::max<uint64_t>(d->target + (c.vol_rate > 0.0 ? c.vol_histories : 0), 1));
@@ -457,6 +467,7 @@ void init_driver(hwwg_driver* d) {
     const int warps = d->sms * fast_max_warps_per_sm();
     d->max_warps = warps;
     d->warp_cursor.reserve((size_t)kWarpCursorWords * warps);
+    d->pc_need.reserve((size_t)32 * warps);
     d->stacks.reserve((size_t)warps * d->stack_cap);
     d->src_head.reserve(1);
     d->pool_recs.reserve(1u << 20);  // 64 MB of donated split records per segment
@@ -1083,6 +1094,36 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   for (size_t i = 0; i < thr.size() && i < 8; ++i) rec->thresholds[i] = thr[i];
 
 
+  // ---- census thinning (FastArgs::precomb): the comb spacing pc_s0 puts
+  // ~precomb_k x target teeth on the census weight W_est, a bound-grade
+  // estimate every rank computes alike: the step's source weight in the cold
+  // start (census weight <= source weight up to roulette noise), else the
+  // previous census weight (all-reduced). Thin when the census is expected to
+  // exceed precomb_k x target: the cold start, or (after step 2) when the
+  // previous raw census did.
+  double pc_s0 = 0.0;
+  if (d->fast && d->precomb) {
+    const double Hc = (double)c.histories_per_step;
+    double W_est = 0.0;
+    bool thin = false;
+    if (d->history.empty()) {
+      thin = true;
+      W_est = c.no_pulse ? 0.0 : c.strength * Hc;
+      if (nv_step) {
+        const double ta = std::max(rec->t_begin, c.vol_t_lo), tb = std::min(rec->t_end, c.vol_t_hi);
+        W_est += c.vol_rate * (tb - ta) * Hc;
+      }
+    } else {
+      // (the cold start's x60 census says nothing about the next step's)
+      const hwwg_step_record& pr = d->history.back();
+      thin = d->history.size() > 1 && (double)pr.census_size > d->precomb_k * (double)d->target;
+      W_est = pr.census_weight * Hc;
+    }
+    if (thin && W_est > 0.0 && std::isfinite(W_est))
+      pc_s0 = W_est / (d->precomb_k * (double)d->target);
+  }
+  rec->thinned = pc_s0 > 0.0 ? 1 : 0;
+
   unsigned long long count = 0;
   DevError derr{};
   const int cur = d->rep_cur;
@@ -1307,6 +1348,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.x_max = d->prob.edges.back();
         fa.w_gen = d->prob.w_gen;
         fa.cell0 = d->prob.cells_h[0];
+        fa.precomb = pc_s0 > 0.0 ? 1 : 0;
+        fa.pc_s0 = pc_s0;
+        fa.pc_inv_s0 = pc_s0 > 0.0 ? 1.0 / pc_s0 : 0.0;
+        fa.pc_key = ((unsigned)d->rank << 16) | ((unsigned)attempt << 8) | (unsigned)nseg;
+        fa.pc_need = d->pc_need.p;
         if (d->timeline_on) {  // HWWG_FAST_TIMELINE: per-warp phase timestamps
           const size_t per = (size_t)fa.pool.warps * kTimelineWords;
           d->timeline.reserve(per * 9);
@@ -1744,6 +1790,8 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
     d->agg_all = v == 2 ? 2 : (v ? 1 : 0);
   }
   if (const char* m = std::getenv("HWWG_FAST_FIX")) d->fix_tallies = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_PRECOMB")) d->precomb = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_PRECOMB_K")) d->precomb_k = std::max(1.0, std::atof(m));
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
     const int w = std::atoi(m);

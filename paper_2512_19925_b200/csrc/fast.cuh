@@ -118,6 +118,21 @@ struct FastArgs {
   double* flush_scratch;
   size_t flush_stride;
   int flush_replicas;
+  // Census thinning (precomb = 1; the cold start, where the census is x60-x150
+  // the next step's histories). Every lane carries its own systematic comb of
+  // spacing pc_s0 over the census particles it banks: a particle of weight w
+  // starting at lane position P (the lane's census weight so far plus a uniform
+  // offset in [0, s0) drawn per launch from pc_key) holds n = #{k : k s0 in
+  // [P, P + w)} teeth and is banked once, with weight n s0, or not at all
+  // (n = 0). E[n s0] = w for every particle, so the banked census is an
+  // unbiased, equal-quantum restatement of the census; the comb at the next
+  // step start (popctrl.cpp:7-42) then combs this ~(W / s0)-record bank to the
+  // target instead of the raw census. Census tallies and counters score the
+  // unthinned particles.
+  int precomb;
+  double pc_s0, pc_inv_s0;
+  unsigned pc_key;
+  double* pc_need;  // 32 per warp of the grid
 };
 size_t fast_flush_stride(int I, int B);  // words per flush replica (nb <= B)
 

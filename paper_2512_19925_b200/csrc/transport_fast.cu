@@ -520,6 +520,17 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   for (int e = threadIdx.x; e <= I; e += blockDim.x) s_edge[e] = edges[e];
   __shared__ double s_logtab[256];
   for (int j = threadIdx.x; j < 256; j += blockDim.x) s_logtab[j] = c_logtab[j];
+  // census thinning (FastArgs::precomb): each lane's distance to its next tooth,
+  // in (0, s0], starting at a uniform offset; kept in global memory (L1-resident,
+  // touched only at census events) off the event loop's registers and shared memory
+  double* pc_need = a.pc_need + (size_t)gwarp * 32 + lane;
+  if (a.precomb) {
+    const U4 r = philox4x32_10(U4{(unsigned)gwarp, (unsigned)lane, a.pc_key, a.step}, a.k0 ^ 0x85ebca6bu,
+                               a.k1 ^ 0xc2b2ae35u);
+    double u, v;
+    philox_uniform2(r, u, v);
+    *pc_need = u * a.pc_s0;
+  }
   __syncthreads();
   if (a.span && threadIdx.x == 0) atomicMin(&a.span[0], globaltimer());
   // per-lane event counters: 32 bits is plenty within one launch (registers
@@ -968,7 +979,24 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
     // segments). Chunk tails left at the end of a step become zero-weight
     // records (fill_census_holes), which the comb never selects.
     {
-      const unsigned cmask = __ballot_sync(0xffffffffu, cen_cell >= 0);
+      bool bank = cen_cell >= 0;
+      double w_bank = p.w;
+      if (a.precomb && bank) {  // census thinning: this particle's teeth on the lane's comb
+        double need = *pc_need;
+        if (p.w < need) {
+          need -= p.w;
+          bank = false;
+        } else {
+          const double r = p.w - need;  // past the first tooth
+          const double k = floor(r * a.pc_inv_s0);
+          double rem = r - k * a.pc_s0;  // in [0, s0) up to rounding
+          rem = rem < 0.0 ? 0.0 : (rem >= a.pc_s0 ? 0.0 : rem);
+          need = a.pc_s0 - rem;
+          w_bank = (k + 1.0) * a.pc_s0;
+        }
+        *pc_need = need;
+      }
+      const unsigned cmask = __ballot_sync(0xffffffffu, bank);
       if (cmask) {
         const unsigned k = __popc(cmask);
         const unsigned avail = wleft;
@@ -977,12 +1005,12 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
           if (lane == 0) nb = atomicAdd(a.census_count, (unsigned long long)kCensusChunk);
           nb = __shfl_sync(0xffffffffu, nb, 0);
         }
-        if (cen_cell >= 0) {
+        if (bank) {
           const unsigned rank = __popc(cmask & lt);
           const unsigned long long slot = rank < avail ? wcur + rank : nb + (rank - avail);
           if (slot < a.census_cap) {  // t = t_end, the cell follows from x
             a.census.xm[slot] = make_double2(p.x, p.mu);
-            a.census.w[slot] = p.w;
+            a.census.w[slot] = w_bank;
           }
         }
         if (k > avail) {

@@ -97,8 +97,13 @@ def test_ranks_agree_and_bookkeeping(W):
             assert rr.counters.as_dict() == r0.counters.as_dict()
             for k in ("phi_track", "sigma", "phi_census", "closure_census", "ww_centers"):
                 np.testing.assert_array_equal(ar[k], a0[k], err_msg=k)
-        # the ranks' banks hold exactly the global census
-        assert sum(res[r][n][2] for r in range(W)) == r0.counters.census_count
+        # the ranks' banks hold exactly the global census (or, for the thinned
+        # cold start, its equal-quantum restatement: fewer records)
+        nb = sum(res[r][n][2] for r in range(W))
+        if r0.thinned:
+            assert n == 0 and nb < r0.counters.census_count
+        else:
+            assert nb == r0.counters.census_count
         assert int(a0["tracks_per_cell"].sum()) == r0.segments
 
 
