@@ -22,13 +22,14 @@ struct CensusBank {
   double* w;
 };
 
-// One run-length-encoded split record (64 B): `count` identical daughters.
+// One run-length-encoded split record (72 B): `count` identical daughters.
 struct FastStackRec {
   double x, mu, w, t;
   unsigned cell, hist;
   unsigned long long key;
   unsigned ctr, count;  // daughters base+1 .. base+count remain
   unsigned ready, base;  // ready: set last when the record sits in the global pool
+  double inv_mu;  // 1 / mu, carried so a popped daughter needs no division
 };
 
 // Global pool of split records shared by all warps of a segment kernel (load

@@ -205,7 +205,7 @@ __device__ __forceinline__ void load_rec(Lane& p, const FastStackRec& r, unsigne
   p.key = mix_lineage(r.key ^ ((unsigned long long)r.ctr << 40) ^ ((unsigned long long)j << 8) ^
                 0x5bd1e995ULL);
   p.ctr = 0;
-  p.inv_mu = 1.0 / p.mu;
+  p.inv_mu = r.inv_mu;
   p.alive = true;
   p.fis = (r.ctr & kFissionRec) != 0;
 }
@@ -360,6 +360,32 @@ __device__ __forceinline__ void census_runs(AddCell add_cell, double* cwb, int c
   const int next = above ? __ffs(above) - 1 : -1;
   if (c && (next < 0 || ((heads >> next) & 1u))) add_cell(cell, s0, s1, s2);  // last lane of its run
   census_weight_runs(cwb, c, b, v3);
+}
+
+// Census scores of one trip on fixed-point slots, grouped by exact equality:
+// split copies popped from one record carry the same (w, mu), and those that
+// reach census in one cell (and batch slot) score identical phi/J/F. Three
+// MATCH.ANY ops (cell|batch, then w and mu bit patterns) give each lane the
+// lanes whose scores equal its own; the group's lowest lane adds n times the
+// score (one rounding onto the fixed-point grid, as a single add), so identical
+// copies cost one set of slot adds and no scan. Lanes with equal cells but
+// other (w, mu) form their own groups (their per-lane adds conflict rarely).
+template <class AddCell>
+__device__ __forceinline__ void census_groups(AddCell add_cell, double* cwb, int cell, int b,
+                                              double w, double mu, double v0, double v1,
+                                              double v2) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const bool c = cell >= 0;
+  if (!__any_sync(full, c)) return;
+  unsigned g = __match_any_sync(full, c ? (b << 16) | cell : -1 - lane);
+  g &= __match_any_sync(full, (unsigned long long)__double_as_longlong(w));
+  g &= __match_any_sync(full, (unsigned long long)__double_as_longlong(mu));
+  if (c && lane == __ffs(g) - 1) {
+    const double n = (double)__popc(g);
+    add_cell(cell, n * v0, n * v1, n * v2);
+  }
+  census_weight_runs(cwb, c, b, w);
 }
 
 // track-length score (keyed by batch slot and cell) plus the per-cell count
@@ -1065,13 +1091,13 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
         }
         census_weight_runs(cwb, cen_cell >= 0, cen_b, cen_w);
       } else if (kFix) {  // cold start: identical split copies reach census together
-        census_runs(
+        census_groups(
             [&](int cell, double s0, double s1, double s2) {
               if (!fix_add(S.cphi + 2 * cell, s0, fix_trk)) atomicAdd(a.t.census_phi + cell, s0);
               if (!fix_add(S.cJ + 2 * cell, s1, fix_trk)) atomicAdd(a.t.census_current + cell, s1);
               if (!fix_add(S.cF + 2 * cell, s2, fix_trk)) atomicAdd(a.t.census_closure + cell, s2);
             },
-            cwb, cen_cell, cen_b, cen_phi, cen_J, cen_F, cen_w);
+            cwb, cen_cell, cen_b, cen_w, p.mu, cen_phi, cen_J, cen_F);
       } else {
         census_runs(
             [&](int cell, double s0, double s1, double s2) {
@@ -1117,7 +1143,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       }
       const FastStackRec rec{p.x, p.mu, p.w, p.t, (unsigned)p.cell | ((unsigned)p.bslot << 16),
                              p.hist, p.key, p.ctr | (fis_rec ? kFissionRec : 0u), dau, 0u,
-                             0u};  // base 0: daughters 1..dau
+                             0u, p.inv_mu};  // base 0: daughters 1..dau
       bool push_local = dau > 0 && !donate;
       // one pair of atomics per warp: the donated records' active units, then
       // their slots (ordered before this warp's own decrement by the fence on
@@ -1426,7 +1452,14 @@ void configure_fast_kernel() {
   for (int w : {12, 24})
     for (int u = 0; u < 2; ++u)
       for (int sh = 0; sh < 2; ++sh)
-        for (int f = 0; f <= sh; ++f) ensure_dyn_smem(fast_kernel(u, sh, f, w), 200 * 1024, configured[i++]);
+        for (int f = 0; f <= sh; ++f) {
+          // the block's static shared memory (its split-stack bottoms) comes first
+          const FastKernel k = fast_kernel(u, sh, f, w);
+          cudaFuncAttributes fa{};
+          HWWG_CUDA(cudaFuncGetAttributes(&fa, k));
+          ensure_dyn_smem(k, std::min<size_t>(200 * 1024, 227 * 1024 - fa.sharedSizeBytes),
+                          configured[i++]);
+        }
   done_dev = dev;
 }
 
