@@ -105,6 +105,9 @@ struct CensusBankBuf {
 };
 }  // namespace hwwg
 
+// e2e transfer pieces per step at most (xfer_chunks)
+constexpr size_t kMaxXferChunks = 48;
+
 struct hwwg_driver {
   hwwg_run_config cfg{};
   hwwg_options opt{};
@@ -181,6 +184,18 @@ struct hwwg_driver {
   // e2e (host_bank): chunked source upload on its own stream (one event per chunk)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> h2d_ev;
+  // e2e round-trip pipeline (single GPU, packed): the combed source goes down to
+  // the host in sub-chunks on d2h_stream right after the comb, and the next
+  // step uploads sub-chunk i as soon as its download (d2h_ev[i]) landed, so the
+  // two PCIe directions overlap each other and the transport of earlier
+  // segments; xfer_end: the sub-chunks' ends (every segment end among them)
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t ev_pre = nullptr;
+  std::vector<cudaEvent_t> d2h_ev;
+  std::vector<uint64_t> xfer_end;
+  bool d2h_pending = false;
+  bool e2e_pipe = true;  // HWWG_E2E_PIPE=0: the download completes inside its step
+  cudaEvent_t xt[8] = {};  // HWWG_HOST_PROF: d2h start/end, h2d start/end, d2h p0 end, h2d p0 end, seg0 start
   // e2e (host_bank) Philox runs: the bank in host memory is already combed
   bool host_pre_combed = false;
   uint64_t pre_comb_in = 0;
@@ -273,6 +288,10 @@ struct hwwg_driver {
     for (auto e : seg_ev) cudaEventDestroy(e);
     for (auto e : ph_ev) cudaEventDestroy(e);
     for (auto e : h2d_ev) cudaEventDestroy(e);
+    if (d2h_stream) cudaStreamSynchronize(d2h_stream);
+    for (auto e : d2h_ev) cudaEventDestroy(e);
+    if (ev_pre) cudaEventDestroy(ev_pre);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (aux_stream) cudaStreamDestroy(aux_stream);
@@ -430,8 +449,12 @@ void init_driver(hwwg_driver* d) {
   HWWG_CUDA(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
   if (c.host_bank) {
     HWWG_CUDA(cudaStreamCreateWithFlags(&d->copy_stream, cudaStreamNonBlocking));
-    d->h2d_ev.resize(9);
+    d->h2d_ev.resize(kMaxXferChunks);
     for (auto& e : d->h2d_ev) HWWG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    HWWG_CUDA(cudaStreamCreateWithFlags(&d->d2h_stream, cudaStreamNonBlocking));
+    HWWG_CUDA(cudaEventCreateWithFlags(&d->ev_pre, cudaEventDisableTiming));
+    d->d2h_ev.resize(kMaxXferChunks);
+    for (auto& e : d->d2h_ev) HWWG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     HWWG_CUDA(cudaMallocHost(&d->h_uni, 64));
     d->uni_flag.reserve(1);
     d->uni_first.reserve(1);
@@ -751,6 +774,41 @@ uint64_t multi_gpu_comb(hwwg_driver* d, int step, uint64_t nv, StepLayout& L, cu
   return d->target;
 }
 
+__global__ void k_stream_mark() {}
+
+// e2e transfer sub-chunks of a combed source of Hs histories: the step's
+// segment ranges [0, h_1), [h_1, h_2), ... (the thresholds driver.cpp:170-177
+// puts at ceil(f * Hs)), each cut into pieces of about Hs / 32 particles, so
+// an upload can start as soon as its piece came down; *seg_last[u] = index of
+// the last piece of segment u.
+std::vector<uint64_t> xfer_chunks(const hwwg_run_config& c, bool hybrid, uint64_t Hs,
+                                  std::vector<size_t>* seg_last) {
+  std::vector<uint64_t> segs;
+  if (hybrid && c.u_ww > 0)
+    for (int i = 0; i < c.n_fractions; ++i) {
+      const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)Hs);
+      if (h >= Hs || (!segs.empty() && h <= segs.back())) continue;
+      segs.push_back(h);
+    }
+  segs.push_back(Hs);
+  const uint64_t piece = std::max<uint64_t>(Hs / 32, 1 << 16);
+  std::vector<uint64_t> ends;
+  if (seg_last) seg_last->clear();
+  uint64_t lo = 0;
+  for (uint64_t hi : segs) {
+    const uint64_t n = std::max<uint64_t>(1, (hi - lo + piece - 1) / piece);
+    for (uint64_t k = 1; k <= n; ++k) ends.push_back(k == n ? hi : lo + k * ((hi - lo) / n));
+    if (seg_last) seg_last->push_back(ends.size() - 1);
+    lo = hi;
+  }
+  if (ends.size() > kMaxXferChunks) {  // many thresholds: one piece per segment
+    ends = segs;
+    if (seg_last)
+      for (size_t u = 0; u < seg_last->size(); ++u) (*seg_last)[u] = u;
+  }
+  return ends;
+}
+
 // One time step (driver.cpp:99-284).
 void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   const hwwg_run_config& c = d->cfg;
@@ -764,6 +822,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   rec->t_end = d->layers[step];
   const double dt = d->layers[step] - d->layers[step - 1];
   const auto t0 = std::chrono::steady_clock::now();
+  const bool hprof = std::getenv("HWWG_HOST_PROF") != nullptr;  // host-side timestamps (stderr)
+  auto hmark = [&](const char* what) {
+    if (hprof)
+      std::fprintf(stderr, "[host] step %d %s %.3f ms\n", step, what,
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  };
   HWWG_CUDA(cudaEventRecord(d->ev0, s));
   const double theta_eff = step == 1 ? 1.0 : c.theta;
   const int ma_k = c.mode == 3 ? c.ma_base_k : 0;
@@ -860,23 +924,22 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // step's segments consume ([0, h_1), [h_1, h_2), ...) on a copy stream, and
   // segment u waits only for chunk u, so the later chunks overlap the earlier
   // segments' transport.
-  size_t n_h2d_chunks = 0;
+  std::vector<size_t> seg_wait;  // segment u waits for upload event h2d_ev[seg_wait[u]]
+  std::vector<uint64_t> seg_range;  // packed uploads: segment u converts [seg_range[u], seg_range[u+1])
   if (c.host_bank && d->fast && d->host_pre_combed && d->world == 1 && !(c.vol_rate > 0.0)) {
     const uint64_t Hs = d->host_bank_n;
-    std::vector<uint64_t> bounds;
-    if (d->hybrid() && c.u_ww > 0)  // the thresholds below, for the same H
-      for (int i = 0; i < c.n_fractions; ++i) {
-        const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)Hs);
-        if (h >= Hs || (!bounds.empty() && h <= bounds.back())) continue;
-        bounds.push_back(h);
-      }
-    bounds.push_back(Hs);
+    const std::vector<uint64_t> bounds = xfer_chunks(c, d->hybrid(), Hs, &seg_wait);
+    const bool piped = d->d2h_pending && d->host_packed && bounds == d->xfer_end && d->e2e_pipe;
+    if (d->d2h_pending && !piped) HWWG_CUDA(cudaStreamSynchronize(d->d2h_stream));
+    d->d2h_pending = false;
     d->bank.reserve(std::max<uint64_t>(Hs, 1));
     const FastBank f = d->fsrc.view();
     const double2* hb = reinterpret_cast<const double2*>(d->host_bank);
     uint64_t lo = 0;
-    for (size_t u = 0; u < bounds.size() && u < d->h2d_ev.size(); ++u) {
+    if (hprof && d->xt[2]) HWWG_CUDA(cudaEventRecord(d->xt[2], d->copy_stream));
+    for (size_t u = 0; u < bounds.size(); ++u) {
       const uint64_t hi = bounds[u];
+      if (piped) HWWG_CUDA(cudaStreamWaitEvent(d->copy_stream, d->d2h_ev[u], 0));
       const FastBank fu{f.xm + lo, f.wt + lo, f.meta + lo};
       if (d->host_packed) {  // (x, mu) [+ (w, t)] straight into the SoA source
         HWWG_CUDA(cudaMemcpyAsync(fu.xm, hb + lo, (hi - lo) * sizeof(double2),
@@ -884,17 +947,23 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         if (!d->host_uniform)
           HWWG_CUDA(cudaMemcpyAsync(fu.wt, hb + Hs + lo, (hi - lo) * sizeof(double2),
                                     cudaMemcpyHostToDevice, d->copy_stream));
-        launch_xm_to_fast(fu, hi - lo, d->prob.view, lo, d->host_uniform ? 1 : 0, d->host_w0,
-                          d->host_t0, d->copy_stream);
+        // (the conversion to SoA records runs on the step stream just before
+        // the segment: a kernel on the copy stream would wait for SMs behind
+        // the persistent transport grid and hold up the copies queued after it)
       } else {
         HWWG_CUDA(cudaMemcpyAsync(d->bank.p + lo, d->host_bank + lo, (hi - lo) * sizeof(hwwg_particle),
                                   cudaMemcpyHostToDevice, d->copy_stream));
         launch_aos_to_fast(d->bank.p + lo, hi - lo, d->prob.view, fu, lo, d->copy_stream);
       }
       HWWG_CUDA(cudaEventRecord(d->h2d_ev[u], d->copy_stream));
+      if (hprof && d->xt[5] && u == 0) HWWG_CUDA(cudaEventRecord(d->xt[5], d->copy_stream));
       ++d->launches;
       lo = hi;
-      ++n_h2d_chunks;
+    }
+    if (hprof && d->xt[3]) HWWG_CUDA(cudaEventRecord(d->xt[3], d->copy_stream));
+    if (d->host_packed) {  // segment u's particle range, converted on s before it runs
+      seg_range.assign(seg_wait.size() + 1, 0);
+      for (size_t u = 0; u < seg_wait.size(); ++u) seg_range[u + 1] = bounds[seg_wait[u]];
     }
     d->bank_n = Hs;
     rec->h2d_bytes += d->host_packed ? Hs * sizeof(double2) * (d->host_uniform ? 1 : 2)
@@ -1067,6 +1136,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     }
     H += nv;
   }
+  hmark("source ready");
   // the step's segments and this rank's histories in them
   const StepLayout L = d->world > 1 ? Lmulti : make_layout(c, d->hybrid(), H_comb, H, 1);
 
@@ -1360,7 +1430,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           HWWG_CUDA(cudaMemsetAsync(fa.timeline, 0, per * 8, s));
           d->timeline_warps = fa.pool.warps;
         }
-        if (u < n_h2d_chunks) HWWG_CUDA(cudaStreamWaitEvent(s, d->h2d_ev[u], 0));
+        if (u < seg_wait.size()) {
+          HWWG_CUDA(cudaStreamWaitEvent(s, d->h2d_ev[seg_wait[u]], 0));
+          if (u + 1 < seg_range.size() && seg_range[u + 1] > seg_range[u]) {
+            const uint64_t lo = seg_range[u], n = seg_range[u + 1] - lo;
+            const FastBank f = d->fsrc.view();
+            launch_xm_to_fast(FastBank{f.xm + lo, f.wt + lo, f.meta + lo}, n, d->prob.view, lo,
+                              d->host_uniform ? 1 : 0, d->host_w0, d->host_t0, s);
+            ++d->launches;
+            fa.pdl = 0;  // the segment now follows the conversion, not the window update
+          }
+        }
+        if (hprof && d->xt[6] && u == 0) HWWG_CUDA(cudaEventRecord(d->xt[6], s));
         if (fa.n_src) {
           launch_fast_segment(fa, blocks, smem, s);
           d->launches += 2;
@@ -1436,7 +1517,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     }
     HWWG_CUDA(cudaMemcpyAsync(&count, d->counter.p, sizeof(count), cudaMemcpyDeviceToHost, s));
     HWWG_CUDA(cudaMemcpyAsync(&derr, d->err.p, sizeof(derr), cudaMemcpyDeviceToHost, s));
+    hmark("before sync");
     HWWG_CUDA(cudaStreamSynchronize(s));
+    hmark("after sync");
     if (d->fast && d->world > 1) {  // replay decisions must be collective
       unsigned long long flags[2] = {count > d->fcensus.cap() ? 1ULL : 0ULL,
                                      derr.code ? 1ULL : 0ULL};
@@ -1607,11 +1690,13 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       launch_check_uniform(d->fsrc.wt.p, d->target, d->uni_flag.p, d->uni_first.p, s);
       ++d->launches;
       rec->d2h_bytes += d->target * sizeof(double2) + 32;
-      HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->fsrc.xm.p, d->target * sizeof(double2),
-                                cudaMemcpyDeviceToHost, s));
       HWWG_CUDA(cudaMemcpyAsync(d->h_uni, d->uni_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
       HWWG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d->h_uni) + 16, d->uni_first.p,
                                 sizeof(double2), cudaMemcpyDeviceToHost, s));
+      // (x, mu) go down at the end of this call (download_source), after the
+      // step's own readbacks: queued behind 160 MB they would wait for it
+      HWWG_CUDA(cudaEventRecord(d->ev_pre, s));
+      d->d2h_pending = true;
     } else {
       launch_fast_to_aos(d->fsrc.view(), d->target, d->bank.p, s);
       ++d->launches;
@@ -1662,7 +1747,21 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, count * sizeof(hwwg_particle),
                               cudaMemcpyDeviceToHost, s));
   }
+  hmark("before fetch");
+  if (hprof && d->xt[3] && c.host_bank) {
+    // every mark relative to the previous step's download start
+    auto at = [&](cudaEvent_t x) {
+      float v = 0;
+      cudaEventElapsedTime(&v, d->xt[0], x);
+      return v;
+    };
+    std::fprintf(stderr, "[host] step %d (ms from the download start): d2h p0 end %.3f, d2h end %.3f, "
+                 "ev0 %.3f, h2d start %.3f, h2d p0 end %.3f, seg0 start %.3f, h2d end %.3f, ev1 %.3f\n",
+                 step, at(d->xt[4]), at(d->xt[1]), at(d->ev0), at(d->xt[2]), at(d->xt[5]), at(d->xt[6]),
+                 at(d->xt[3]), at(d->ev1));
+  }
   d->host_tal.fetch(d->tal, s);  // synchronises the stream
+  hmark("after fetch");
   if (d->host_pre_combed && d->host_packed) {
     const double* f = reinterpret_cast<const double*>(reinterpret_cast<char*>(d->h_uni) + 16);
     const bool force_full = std::getenv("HWWG_HOST_FULL") != nullptr;  // tests
@@ -1698,6 +1797,37 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   rec->kernel_launches = d->launches;
   rec->d2h_bytes += rep_h.size() * 8 + sizeof flags + sizeof comb_sc + 2 * (size_t)I * 8 +
                     d->tal.words() * 8;
+  hmark("end");
+  if (d->d2h_pending) {
+    // The stream's last command was a download (the record readback), and the
+    // next command recorded on a stream after a copy queues in that copy
+    // engine — behind the 160 MB below, holding the next step back until they
+    // are done. An empty kernel puts the stream back on the compute engine.
+    k_stream_mark<<<1, 1, 0, s>>>();
+    HWWG_CUDA(cudaGetLastError());
+    // e2e: the next step's combed source down to the host in the pieces its
+    // uploads take, on the d2h stream; this call returns now and each upload
+    // of the next step waits only for its own piece (hwwg_driver_bank and
+    // destroy wait for all of them)
+    d->xfer_end = xfer_chunks(c, d->hybrid(), d->target, nullptr);
+    // (no event wait: the host synchronised the stream after the comb — fetch above)
+    if (hprof) {
+      for (auto& e : d->xt)
+        if (!e) HWWG_CUDA(cudaEventCreate(&e));
+      HWWG_CUDA(cudaEventRecord(d->xt[0], d->d2h_stream));
+    }
+    uint64_t lo = 0;
+    for (size_t i = 0; i < d->xfer_end.size(); ++i) {
+      const uint64_t hi = d->xfer_end[i];
+      HWWG_CUDA(cudaMemcpyAsync(reinterpret_cast<double2*>(d->host_bank) + lo, d->fsrc.xm.p + lo,
+                                (hi - lo) * sizeof(double2), cudaMemcpyDeviceToHost, d->d2h_stream));
+      HWWG_CUDA(cudaEventRecord(d->d2h_ev[i], d->d2h_stream));
+      if (hprof && i == 0) HWWG_CUDA(cudaEventRecord(d->xt[4], d->d2h_stream));
+      lo = hi;
+    }
+    if (hprof) HWWG_CUDA(cudaEventRecord(d->xt[1], d->d2h_stream));
+    if (!d->e2e_pipe) HWWG_CUDA(cudaStreamSynchronize(d->d2h_stream));
+  }
 
   const HostTallies& h = d->host_tal;
   if (h.ucount()[kHistoriesScored] != 0) { /* unused: histories counted on host */ }
@@ -1793,6 +1923,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_PRECOMB")) d->precomb = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_PRECOMB_K")) d->precomb_k = std::max(1.0, std::atof(m));
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_E2E_PIPE")) d->e2e_pipe = std::atoi(m) != 0;
   if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
     const int w = std::atoi(m);
     d->block_warps = (w == 12 || w == 24) ? w : 0;
@@ -1929,6 +2060,7 @@ int hwwg_driver_write(hwwg_driver* d, const char* dir, int32_t final, double tot
 int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t* n) {
   HWWG_API_BEGIN
   if (!d || !n) return fail(HWWG_EINVAL, "NULL argument");
+  if (d->d2h_stream) HWWG_CUDA(cudaStreamSynchronize(d->d2h_stream));  // the host copy is complete
   uint64_t count = d->bank_n;
   if (d->fast && !d->cfg.host_bank && d->next_step > 1) {
     // Philox mode keeps the census as SoA with zero-weight chunk tails: compact
