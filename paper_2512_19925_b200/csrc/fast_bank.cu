@@ -24,6 +24,33 @@ __global__ void k_extract_w(CensusBank b, uint64_t n, double* w) {
   if (i < n) w[i] = b.w[i];
 }
 
+// mesh.cpp:26-40 with the uniform estimate by a multiplication with 1 / w0:
+// the +-1 guards turn any estimate within one cell of the truth into the
+// unique c with edges[c] <= x < edges[c+1], so the result equals locate_cell's
+// (throughput mode only; the exact mode keeps the reference's division)
+__device__ __forceinline__ int locate_cell_mul(const MeshView& m, double x, double inv_w0) {
+  if (!m.uniform) return locate_cell(m, x);
+  if (x < m.x_min || x > m.x_max) return -1;
+  if (x == m.x_max) return m.I - 1;
+  int c = (int)((x - m.x_min) * inv_w0);
+  if (c >= m.I) c = m.I - 1;
+  if (c < 0) c = 0;
+  if (x < m.edges[c]) --c;
+  else if (x >= m.edges[c + 1]) ++c;
+  return c;
+}
+
+__device__ __forceinline__ void write_tooth(const FastCombArgs& a, double2 xm, uint64_t k,
+                                            double spacing, double inv_w0) {
+  HWWG_CHECK(k < a.target);
+  const int c = locate_cell_mul(a.mesh, xm.x, inv_w0);  // as advance_history locates a start (transport.cpp:95)
+  const uint64_t p = a.perm(k);
+  HWWG_CHECK(p < a.target);
+  a.out.xm[p] = xm;
+  a.out.wt[p] = make_double2(spacing, a.t_bank);
+  a.out.meta[p] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)p, 0u, 0u);
+}
+
 __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src, uint64_t k0,
                                             uint64_t k1, double spacing) {
   HWWG_CHECK(src < a.n && k1 <= a.target);
@@ -96,6 +123,26 @@ __device__ __forceinline__ T block_exclusive_256(T v, T* red, T& total) {
   }
   total = all;
   return before + inc - v;
+}
+
+// Block (kCbThreads) exclusive max-scan of one value per thread (0 for thread 0).
+__device__ __forceinline__ unsigned block_exclusive_max_256(unsigned v, unsigned* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned p = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc = max(inc, p);
+  }
+  __syncthreads();  // red reuse
+  if (lane == 31) red[wid] = inc;
+  __syncthreads();
+  unsigned before = 0;
+#pragma unroll
+  for (int w = 0; w < kCbThreads / 32; ++w)
+    if (w < wid) before = max(before, red[w]);
+  const unsigned prev = __shfl_up_sync(0xffffffffu, inc, 1);
+  return max(before, lane ? prev : 0u);
 }
 
 // Is this the last block of the grid to finish? (the counter resets itself)
@@ -236,15 +283,57 @@ __global__ void __launch_bounds__(kCbThreads) k_cb_scatter(FastCombArgs a) {
   }
   __syncthreads();
   const unsigned nT = khi[pad_u(kCbTile - 1)];  // the tile's teeth (padding holds the last bound)
-  for (unsigned r = threadIdx.x; r < nT; r += kCbThreads) {
-    int lo = 0, hi = m - 1;  // first particle j with khi[j] > r
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (khi[pad_u(mid)] > r) hi = mid;
-      else lo = mid + 1;
+  // Tooth -> particle table, kCbTile teeth per round: every particle marks its
+  // first tooth of the round with its index, and a block max-scan carries each
+  // mark over the particle's remaining teeth (particles own consecutive,
+  // ordered tooth ranges), so the writes below need no per-tooth search.
+  unsigned* own = khi + pad_u(kCbTile);  // the upper half of wv, free once the bounds exist
+  const double inv_w0 = a.mesh.uniform ? 1.0 / a.mesh.w0 : 0.0;
+  for (unsigned R0 = 0; R0 < nT; R0 += kCbTile) {
+    const unsigned R1 = nT - R0 < (unsigned)kCbTile ? nT : R0 + kCbTile;
+#pragma unroll
+    for (int i = 0; i < kCbItems; ++i) own[pad_u(threadIdx.x * kCbItems + i)] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kCbItems; ++i) {
+      const int j = threadIdx.x * kCbItems + i;
+      if (j < m) {
+        const unsigned lo = j ? khi[pad_u(j - 1)] : 0u, hi = khi[pad_u(j)];
+        const unsigned first = lo > R0 ? lo : R0;
+        if (first < hi && first < R1) own[pad_u(first - R0)] = (unsigned)j;
+      }
     }
-    HWWG_CHECK(lo < m && khi[pad_u(lo)] > r && (lo == 0 || khi[pad_u(lo - 1)] <= r));
-    write_teeth(a, t0 + lo, k0 + r, k0 + r + 1, spacing);
+    __syncthreads();
+    unsigned run = 0;  // blocked inclusive max-scan of the marks
+    unsigned v[kCbItems];
+#pragma unroll
+    for (int i = 0; i < kCbItems; ++i) {
+      run = max(run, own[pad_u(threadIdx.x * kCbItems + i)]);
+      v[i] = run;
+    }
+    const unsigned before = block_exclusive_max_256(run, reinterpret_cast<unsigned*>(red));
+#pragma unroll
+    for (int i = 0; i < kCbItems; ++i) own[pad_u(threadIdx.x * kCbItems + i)] = max(v[i], before);
+    __syncthreads();
+    // teeth of the round, 4 per thread in flight (their particles' loads first)
+    for (unsigned r0 = R0 + threadIdx.x; r0 < R1; r0 += 4 * kCbThreads) {
+      double2 xm[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned r = r0 + q * kCbThreads;
+        if (r < R1) {
+          const unsigned j = own[pad_u(r - R0)];
+          HWWG_CHECK((int)j < m && khi[pad_u(j)] > r && (j == 0 || khi[pad_u(j - 1)] <= r));
+          xm[q] = a.bank.xm[t0 + j];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const unsigned r = r0 + q * kCbThreads;
+        if (r < R1) write_tooth(a, xm[q], k0 + r, spacing, inv_w0);
+      }
+    }
+    __syncthreads();  // the table is rebuilt for the next round
   }
   // teeth stranded past the integer total by round-off go to the last particle
   // with weight (popctrl.cpp:31-37)

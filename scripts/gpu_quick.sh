@@ -1,5 +1,5 @@
 # quick check: statistical + multirank tests, then the headline and C2/C3 benches
-timeout 900 python -m pytest tests/test_gpu_statistical.py tests/test_gpu_stat_pin.py tests/test_gpu_multirank.py -q -x > gpurun_out/q_pytest.log 2>&1; echo "pytest: $(tail -1 gpurun_out/q_pytest.log)"
+timeout 900 python -m pytest tests/test_gpu_statistical.py tests/test_gpu_stat_pin.py tests/test_gpu_multirank.py tests/test_gpu_checked.py -q -x > gpurun_out/q_pytest.log 2>&1; echo "pytest: $(tail -1 gpurun_out/q_pytest.log)"
 B="python bench.py --no-cpu-baseline --no-exact --no-configs"
 for cfg in ${CFGS:-c5 c2 c3}; do
   timeout 300 $B --config $cfg > gpurun_out/q_$cfg.log 2>&1

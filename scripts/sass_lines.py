@@ -38,7 +38,9 @@ for l in dis:
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/', l)
     if m and sec:
         lines[int(m.group(1), 16)] = loc
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+# NCU_K=<name>: a report holding several kernels is filtered to that one
+kf = ["-k", os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + kf,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]

@@ -184,7 +184,9 @@ def test_host_round_trip_multirank():
         rd, rh = dev[0][n][0], host[0][n][0]
         assert rh.histories == H and rh.comb_out == H
         np.testing.assert_allclose(rh.comb_out_weight, rh.comb_in_weight, rtol=1e-12)
-        assert abs(rh.segments / rd.segments - 1) < 0.06, (n, rh.segments, rd.segments)
+        # two realisations (census order is scheduling-dependent): the segment
+        # count of 3e4 heavy-tailed split trees moves by several percent
+        assert abs(rh.segments / rd.segments - 1) < 0.12, (n, rh.segments, rd.segments)
         assert abs(rh.census_weight / rd.census_weight - 1) < 0.03
         if n >= 1:  # steps after the first open with a pre-combed share from the host
             per_rank = [host[r][n][0].h2d_bytes for r in range(W)]
