@@ -1169,8 +1169,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // estimate every rank computes alike: the step's source weight in the cold
   // start (census weight <= source weight up to roulette noise), else the
   // previous census weight (all-reduced). Thin when the census is expected to
-  // exceed precomb_k x target: the cold start, or (after step 2) when the
-  // previous raw census did.
+  // exceed precomb_k x target: the cold start, or when the previous raw
+  // census did.
   double pc_s0 = 0.0;
   if (d->fast && d->precomb) {
     const double Hc = (double)c.histories_per_step;
@@ -1184,9 +1184,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         W_est += c.vol_rate * (tb - ta) * Hc;
       }
     } else {
-      // (the cold start's x60 census says nothing about the next step's)
+      // (after a x60 cold start the next census is usually ~x2 — config 5 —
+      // but can stay x100 — config 4: thinning it too is cheap and unbiased,
+      // where an unthinned overflow replays the step with a larger bank)
       const hwwg_step_record& pr = d->history.back();
-      thin = d->history.size() > 1 && (double)pr.census_size > d->precomb_k * (double)d->target;
+      thin = (double)pr.census_size > d->precomb_k * (double)d->target;
       W_est = pr.census_weight * Hc;
     }
     if (thin && W_est > 0.0 && std::isfinite(W_est))
@@ -1309,6 +1311,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.inv_dt = 1.0 / dt;
         fa.k0 = (unsigned)c.seed;
         fa.k1 = (unsigned)(c.seed >> 32) ^ 0x6a09e667u;
+        philox_round_keys(fa.k0, fa.k1, fa.rk);
         fa.step = (unsigned)step;
         fa.H = H;
         fa.B = B;
@@ -1355,12 +1358,18 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         const int uni = d->prob.gen_uniform_homog ? 1 : 0;
         // the block shape with the most resident warps for a tally layout (2 x 12
         // warps on ties; HWWG_FAST_BLOCK_WARPS forces one)
+        // A block-private tally copy of >= 96 KB (config 3's 1000 cells) is
+        // zeroed and flushed per block: one block per SM (1 x 24 warps) then
+        // beats two blocks with 4 more warps (config 3: 2.0e10 vs 1.5e10 seg/s),
+        // while config 5's ~70 KB copy runs best at 2 x 14 (2.54e10 vs 2.43e10).
         auto shape = [&](size_t sm, int sh, int fx, int& warps) {
           int best = 0;
-          for (int w : {12, 24}) {
+          for (int w : kFastBlockWarps) {
             if (d->block_warps && w != d->block_warps) continue;
-            const int r = fast_blocks_per_sm(sm, uni, sh, fx, w) * w;
-            if (r > best) {
+            const int nb_sm = fast_blocks_per_sm(sm, uni, sh, fx, w);
+            const int r = nb_sm * w;
+            const bool one_big = nb_sm == 1 && sm >= 96 * 1024 && 5 * r >= 4 * best;
+            if (r > best || (one_big && r > 0)) {
               best = r;
               warps = w;
             }
@@ -1385,12 +1394,15 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           const double smallest = c.mode != 0 ? c.eps_min / c.rho * vmin : w * vmin;
           const bool range_ok = smallest > 0.0 &&
                                 std::ilogb(w * vmax) - std::ilogb(smallest) <= 20;
+          int kc = 0;
           if (range_ok && fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
-              fix_warps >= shape(smem, 1, 0, wbase)) {
+              fast_fix_exponent(w, &kc) &&
+              5 * fix_warps >= 4 * shape(smem, 1, 0, wbase)) {  // (shared fp64 adds are CAS loops)
             fa.fix = 1;
             fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             fa.fix_k_trk = kt;
             fa.fix_k_edge = ke;
+            fa.fix_k_cw = kc;
             fa.aggregate = 0;
             smem = fsm;
           }
@@ -1926,7 +1938,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_E2E_PIPE")) d->e2e_pipe = std::atoi(m) != 0;
   if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
     const int w = std::atoi(m);
-    d->block_warps = (w == 12 || w == 24) ? w : 0;
+    d->block_warps = (w == 12 || w == 14 || w == 24) ? w : 0;
   }
   d->seg_events = d->fast ? (std::getenv("HWWG_SEG_EVENTS") ? 1 : 0) : 1;
   d->span.reserve(64);

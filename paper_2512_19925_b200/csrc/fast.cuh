@@ -74,6 +74,7 @@ struct FastArgs {
   MeshView mesh;
   double t_end, inv_dt;
   unsigned k0, k1, step;  // Philox key (seed) and step
+  unsigned rk[20];        // the key's round keys (philox_round_keys)
   uint64_t H;
   int B;
   double bmul;  // B / H (batch_of without a division)
@@ -84,7 +85,7 @@ struct FastArgs {
   int scramble;      // 1: claim source particles in bit-reversed order within 1024-blocks
   // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
   // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
-  int fix, fix_k_trk, fix_k_edge;
+  int fix, fix_k_trk, fix_k_edge, fix_k_cw;  // ... census weight by batch on 2^-fix_k_cw
   int warps;            // warps per block: 12 (2 blocks per SM) or 24 (1 block per SM)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   int pdl;              // 1: programmatic dependent launch after the previous kernel
@@ -159,6 +160,9 @@ void launch_aos_to_census(const hwwg_particle* in, uint64_t n, CensusBank out, c
 // tallies, fixed-point slots, warps per block: 12 or 24) with `smem` dynamic
 // shared memory, and the most warps per SM any instantiation holds
 int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix, int warps);
+// transport block shapes (warps per block): 2 x 12, 2 x 14 (where the
+// registers and the tallies' shared memory allow 28 warps) or 1 x 24 per SM
+constexpr int kFastBlockWarps[3] = {12, 14, 24};
 int fast_max_warps_per_sm();
 // per-warp census cursor words (FastArgs::warp_cursor: next, end)
 constexpr int kWarpCursorWords = 2;

@@ -92,6 +92,27 @@ HWWG_HD U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// Philox4x32-10 with the round keys precomputed (rk[2r] = k0 + r * 0x9E3779B9,
+// rk[2r+1] = k1 + r * 0xBB67AE85: philox_round_keys): the same function as
+// philox4x32_10, without the key schedule's adds — with rk in kernel
+// parameters every key is a constant-bank operand of its XOR.
+HWWG_HD void philox_round_keys(uint32_t k0, uint32_t k1, uint32_t rk[20]) {
+  for (int r = 0; r < 10; ++r) {
+    rk[2 * r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    rk[2 * r + 1] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+}
+HWWG_HD U4 philox4x32_10_rk(U4 c, const uint32_t (&rk)[20]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0, lo0, hi1, lo1;
+    mulhilo32(0xD2511F53u, c.x, hi0, lo0);
+    mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
+    c = U4{hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0};
+  }
+  return c;
+}
+
 // Two uniforms in (0,1) from one Philox block (53 bits each).
 // One event's deviates from one Philox block: a 53-bit uniform (flight
 // distance) and two 32-bit uniforms (collision type / roulette, scattering).

@@ -57,7 +57,7 @@ namespace {
 // 2 blocks of 8 warps before, 16 warps per SM). One shared-memory tally set per
 // block; the driver picks the shape per launch (measured against 3 blocks of
 // 8 warps: C5 77.0 -> 76.2 ms, C3 73.7 -> 41 ms for 20 steps).
-constexpr int kMaxWarpsPerSm = 24;
+constexpr int kMaxWarpsPerSm = 28;
 
 // -DHWWG_FAST_PROF: per-phase clock64 accounting of the loop (lane 0 of every
 // warp), summed over the grid into g_fprof: [0] refill [1] event [2] census
@@ -152,21 +152,40 @@ __device__ __forceinline__ void draw3(const FastArgs& a, Lane& p, double& u0, do
                                       double& u2) {
   const U4 c{p.hist, (unsigned)p.key, (unsigned)(p.key >> 32), (a.step << 16) | (p.ctr & 0xffffu)};
   ++p.ctr;
-  philox_uniform3(philox4x32_10(c, a.k0, a.k1), u0, u1, u2);
+  philox_uniform3(philox4x32_10_rk(c, a.rk), u0, u1, u2);
 }
 
 // tally.hpp:130-134 batch_of = floor(h B / H): an fp64 estimate from the
 // precomputed B / H, corrected by one integer comparison (the estimate is off
 // by at most one; no division)
 __device__ __forceinline__ int batch_fast(unsigned h, unsigned long long H, int B, double bmul) {
-  const unsigned long long hb = (unsigned long long)h * (unsigned)B;
   int b = (int)((double)h * bmul);
+  if (H * (unsigned)B < (1ULL << 32)) {  // every product below fits 32 bits (h < H, b < B)
+    const unsigned hb = h * (unsigned)B, H32 = (unsigned)H;
+    if ((unsigned)(b + 1) * H32 <= hb) ++b;
+    else if (b > 0 && (unsigned)b * H32 > hb) --b;
+    return b < B ? b : B - 1;
+  }
+  const unsigned long long hb = (unsigned long long)h * (unsigned)B;
   if ((unsigned long long)(b + 1) * H <= hb) ++b;
   else if (b > 0 && (unsigned long long)b * H > hb) --b;
   return b < B ? b : B - 1;
 }
 
 __constant__ double c_logtab[256] = HWWG_LOG_TAB;
+
+// 1 / x to within an ulp: the MUFU reciprocal estimate and two Newton steps
+// (the IEEE division's 1 / mu cost a slow-path check per direction change);
+// x = 0 keeps the IEEE answer (+-inf)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  return x == 0.0 ? 1.0 / x : r;
+}
 
 // -ln(u) for a deviate u in (0, 1) (the flight distance in mean free paths):
 // the table-driven algorithm of libm_log.h (k ln2 + log c + log1p(r), 128-entry
@@ -287,7 +306,8 @@ __device__ __forceinline__ void agg_add3(double* b0, double* b1, double* b2, int
 // trip: runs of census lanes keyed by the batch slot alone — usually one run
 // per warp (all its census lanes hold histories of one batch), which takes a
 // plain butterfly sum and one add.
-__device__ __forceinline__ void census_weight_runs(double* cwb, bool c, int b, double v) {
+template <class AddW>
+__device__ __forceinline__ void census_weight_runs_t(AddW add_w, bool c, int b, double v) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned cm = __ballot_sync(full, c);
@@ -297,7 +317,7 @@ __device__ __forceinline__ void census_weight_runs(double* cwb, bool c, int b, d
     double w = c ? v : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(full, w, o);
-    if (lane == __ffs(cm) - 1) atomicAdd(cwb + b0, w);
+    if (lane == __ffs(cm) - 1) add_w(b0, w);
     return;
   }
   const unsigned below = cm & ((1u << lane) - 1u);
@@ -316,7 +336,10 @@ __device__ __forceinline__ void census_weight_runs(double* cwb, bool c, int b, d
   }
   const unsigned above = cm & ~upto;
   const int next = above ? __ffs(above) - 1 : -1;
-  if (c && (next < 0 || ((bheads >> next) & 1u))) atomicAdd(cwb + b, w);
+  if (c && (next < 0 || ((bheads >> next) & 1u))) add_w(b, w);
+}
+__device__ __forceinline__ void census_weight_runs(double* cwb, bool c, int b, double v) {
+  census_weight_runs_t([&](int bb, double w) { atomicAdd(cwb + bb, w); }, c, b, v);
 }
 
 // Census scores of one trip, summed over runs of census lanes with equal
@@ -370,8 +393,8 @@ __device__ __forceinline__ void census_runs(AddCell add_cell, double* cwb, int c
 // score (one rounding onto the fixed-point grid, as a single add), so identical
 // copies cost one set of slot adds and no scan. Lanes with equal cells but
 // other (w, mu) form their own groups (their per-lane adds conflict rarely).
-template <class AddCell>
-__device__ __forceinline__ void census_groups(AddCell add_cell, double* cwb, int cell, int b,
+template <class AddCell, class AddW>
+__device__ __forceinline__ void census_groups(AddCell add_cell, AddW add_w, int cell, int b,
                                               double w, double mu, double v0, double v1,
                                               double v2) {
   const unsigned full = 0xffffffffu;
@@ -385,7 +408,7 @@ __device__ __forceinline__ void census_groups(AddCell add_cell, double* cwb, int
     const double n = (double)__popc(g);
     add_cell(cell, n * v0, n * v1, n * v2);
   }
-  census_weight_runs(cwb, c, b, w);
+  census_weight_runs_t(add_w, c, b, w);
 }
 
 // track-length score (keyed by batch slot and cell) plus the per-cell count
@@ -488,8 +511,8 @@ __device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb, int 
   s.cJ = s.cphi + (size_t)slotw * I;
   s.cF = s.cJ + (size_t)slotw * I;
   s.edge = s.cF + (size_t)slotw * I;
-  s.cwb = s.edge + (size_t)slotw * (I + 1);
-  s.bclo = s.cwb + nb;
+  s.cwb = s.edge + (size_t)slotw * (I + 1);  // kFix: limb slots too (after the edges)
+  s.bclo = s.cwb + (size_t)slotw * nb;
   return s;
 }
 
@@ -526,14 +549,15 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   SmemTally S = smem_view(smem, I, a.nb, slotw);
   // dynamic shared memory: [tallies (mode-dependent words) | window centres I]
   const size_t tally_words =
-      shf ? (size_t)slotw * ((size_t)a.nb * I + 4 * (size_t)I + 1) + a.nb + 2 + (I + 1) / 2
+      shf ? (size_t)slotw * ((size_t)a.nb * I + 4 * (size_t)I + 1 + a.nb) + 2 + (I + 1) / 2
           : (sh ? (size_t)(I + 1) / 2 : 0);
   const double fix_trk = kFix ? pow2(a.fix_k_trk) : 0.0;
   const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
+  const double fix_cw = kFix ? pow2(a.fix_k_cw) : 0.0;
   __shared__ unsigned s_sweep;  // kFix: the carry sweep's slot cursor
   // kFix: the fixed-point slots, contiguous from S.trk (track nb*I, census
-  // phi/J/F 3*I, edges I+1)
-  const unsigned fix_slots = (unsigned)(a.nb * I + 4 * I + 1);
+  // phi/J/F 3*I, edges I+1, census weight by batch nb)
+  const unsigned fix_slots = (unsigned)(a.nb * I + 4 * I + 1 + a.nb);
   // slots per lane per sweep: every slot is swept within 4096 / 32 sweeps
   const unsigned fix_spl = (fix_slots + 4095u) / 4096u;
   if (kFix && threadIdx.x == 0) s_sweep = 0u;
@@ -761,7 +785,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
           p.ctr = m.x >> 16;
           p.hist = m.y;
           p.key = ((unsigned long long)m.w << 32) | m.z;
-          p.inv_mu = 1.0 / p.mu;
+          p.inv_mu = rcp_nr(p.mu);
           p.bslot = batch_fast(p.hist, a.H, a.B, a.bmul) - (shf ? a.b_lo : 0);
           p.alive = p.w > 0.0;
           p.fis = false;
@@ -878,7 +902,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       if (p.fis) {  // a fission secondary: its direction, then the window game (transport.cpp:181-185)
         p.fis = false;
         p.mu = 2.0 * u2 - 1.0;
-        p.inv_mu = 1.0 / p.mu;
+        p.inv_mu = rcp_nr(p.mu);
         window_site = true;
       } else {
         const double d_census = ci.speed * (a.t_end - p.t);
@@ -944,7 +968,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
           const double xi = u1 * ci.sigma_t;
           if (xi < ci.sigma_s) {
             p.mu = 2.0 * u2 - 1.0;
-            p.inv_mu = 1.0 / p.mu;
+            p.inv_mu = rcp_nr(p.mu);
             u1 = xi * ci.inv_sigma_s;  // recycled roulette deviate for the window game below
             window_site = true;
           } else if (xi < ci.sigma_s + ci.sigma_f) {
@@ -1071,6 +1095,10 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       double* cJ = kShf ? S.cJ : a.t.census_current;
       double* cF = kShf ? S.cF : a.t.census_closure;
       double* cwb = kShf ? S.cwb : a.t.census_weight_batch;
+      // kFix: the census weight by batch on limb slots too (no shared fp64 CAS loop)
+      auto fix_cwb = [&](int bb, double w) {
+        if (!fix_add(S.cwb + 2 * bb, w, fix_cw)) atomicAdd(a.t.census_weight_batch + a.b_lo + bb, w);
+      };
       double* edg = kShf ? S.edge : a.t.edge_current;
       if (trk_key >= 0) {
         if (!kFix) atomicAdd(trk + trk_key, trk_v);
@@ -1089,7 +1117,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
           if (!fix_add(S.cJ + 2 * cen_cell, cen_J, fix_trk)) atomicAdd(a.t.census_current + cen_cell, cen_J);
           if (!fix_add(S.cF + 2 * cen_cell, cen_F, fix_trk)) atomicAdd(a.t.census_closure + cen_cell, cen_F);
         }
-        census_weight_runs(cwb, cen_cell >= 0, cen_b, cen_w);
+        census_weight_runs_t(fix_cwb, cen_cell >= 0, cen_b, cen_w);
       } else if (kFix) {  // cold start: identical split copies reach census together
         census_groups(
             [&](int cell, double s0, double s1, double s2) {
@@ -1097,7 +1125,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
               if (!fix_add(S.cJ + 2 * cell, s1, fix_trk)) atomicAdd(a.t.census_current + cell, s1);
               if (!fix_add(S.cF + 2 * cell, s2, fix_trk)) atomicAdd(a.t.census_closure + cell, s2);
             },
-            cwb, cen_cell, cen_b, cen_w, p.mu, cen_phi, cen_J, cen_F);
+            fix_cwb, cen_cell, cen_b, cen_w, p.mu, cen_phi, cen_J, cen_F);
       } else {
         census_runs(
             [&](int cell, double s0, double s1, double s2) {
@@ -1263,8 +1291,10 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       const double v = kFix ? fix_value(S.edge + 2 * i, inv_edge) : S.edge[i];
       if (v != 0.0) atomicAdd(&a.t.edge_current[i], v);
     }
-    for (int i = threadIdx.x; i < nb; i += blockDim.x)
-      if (S.cwb[i] != 0.0) atomicAdd(&a.t.census_weight_batch[a.b_lo + i], S.cwb[i]);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      const double v = kFix ? fix_value(S.cwb + 2 * i, pow2(-a.fix_k_cw)) : S.cwb[i];
+      if (v != 0.0) atomicAdd(&a.t.census_weight_batch[a.b_lo + i], v);
+    }
     if (threadIdx.x < 2 && S.bclo[threadIdx.x] != 0.0)
       atomicAdd(&a.t.boundary_closure[threadIdx.x], S.bclo[threadIdx.x]);
   } else if (sh) {
@@ -1358,7 +1388,7 @@ size_t fast_smem_bytes(int I, int nb) {
 }
 size_t fast_smem_count_bytes(int I) { return (size_t)(I + 1) / 2 * 8 + 16; }
 size_t fast_smem_fix_bytes(int I, int nb) {
-  return ((size_t)2 * ((size_t)nb * I + 4 * (size_t)I + 1) + nb + 2) * sizeof(double) +
+  return ((size_t)2 * ((size_t)nb * I + 4 * (size_t)I + 1 + nb) + 2) * sizeof(double) +
          (size_t)(I + 1) / 2 * 8 + 16;
 }
 // Grid exponent k for the fixed-point tallies: the largest expected score
@@ -1408,7 +1438,9 @@ FastKernel fast_kernel_w(int uniform, int shf, int fix) {
                           : k_fast_segment<false, false, false, kW>;
 }
 FastKernel fast_kernel(int uniform, int shf, int fix, int warps) {
-  return warps == 24 ? fast_kernel_w<24>(uniform, shf, fix) : fast_kernel_w<12>(uniform, shf, fix);
+  return warps == 24   ? fast_kernel_w<24>(uniform, shf, fix)
+         : warps == 14 ? fast_kernel_w<14>(uniform, shf, fix)
+                       : fast_kernel_w<12>(uniform, shf, fix);
 }
 
 // resident blocks per SM of the instantiation a launch will use (the
@@ -1447,9 +1479,9 @@ void configure_fast_kernel() {
   int dev = 0;
   HWWG_CUDA(cudaGetDevice(&dev));
   if (dev == done_dev) return;
-  static DynSmemCache configured[12];
+  static DynSmemCache configured[18];
   int i = 0;
-  for (int w : {12, 24})
+  for (int w : kFastBlockWarps)
     for (int u = 0; u < 2; ++u)
       for (int sh = 0; sh < 2; ++sh)
         for (int f = 0; f <= sh; ++f) {
