@@ -712,21 +712,26 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
     }
     FPROF(8);
     unsigned need = __ballot_sync(0xffffffffu, !p.alive);
-    while (need && sp > 0) {
-      HWWG_CHECK(sp >= 1 && sp <= a.stack_cap);
-      FastStackRec& r = STK(sp - 1);
+    // Pops from the top record: the bottom kSmemStack records are on chip, and
+    // the two address spaces take separate paths so the on-chip one compiles
+    // to shared-memory loads (a generic pointer to either cost address
+    // resolution on every field of the record)
+    auto pop = [&](FastStackRec& r) {
       const unsigned k = __popc(need);
       const unsigned cnt = r.count;
       const unsigned take = k < cnt ? k : cnt;
       const unsigned rank = __popc(need & lt);
-      if (!p.alive && rank < take) {
-        load_rec(p, r, r.base + cnt - rank);
-      }
+      if (!p.alive && rank < take) load_rec(p, r, r.base + cnt - rank);
       __syncwarp();
       if (lane == 0) r.count = cnt - take;
       __syncwarp();
       pend -= take;
       if (cnt == take) --sp;
+    };
+    while (need && sp > 0) {
+      HWWG_CHECK(sp >= 1 && sp <= a.stack_cap);
+      if (sp <= kSmemStack) pop(s_my[sp - 1]);
+      else pop(stk[sp - 1]);
       need = __ballot_sync(0xffffffffu, !p.alive);
     }
     FPROF(9);
@@ -1201,7 +1206,8 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       const unsigned lmask = __ballot_sync(0xffffffffu, push_local);
       if (push_local) {
         const int slot = sp + (int)__popc(lmask & lt);
-        if (slot < a.stack_cap) STK(slot) = rec;
+        if (slot < kSmemStack) s_my[slot] = rec;
+        else if (slot < a.stack_cap) stk[slot] = rec;
         else atomicCAS(&a.err->code, 0, HWWG_ESTACK);
       }
       unsigned ld = push_local ? dau : 0;
