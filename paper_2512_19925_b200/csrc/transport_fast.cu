@@ -184,7 +184,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   r = fma(r, e, r);
-  return x == 0.0 ? 1.0 / x : r;
+  // (no division in the select: it would be computed on every call)
+  const long long inf = 0x7ff0000000000000LL | (__double_as_longlong(x) & (long long)0x8000000000000000ULL);
+  return x == 0.0 ? __longlong_as_double(inf) : r;
 }
 
 // -ln(u) for a deviate u in (0, 1) (the flight distance in mean free paths):
@@ -956,7 +958,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
             if (amu < 1e-10) {
               atomicAdd(&s_rare[5], 1u);
             } else {
-              const double bc = p.w * (0.5 - amu) / amu * a.inv_dt;
+              const double bc = p.w * (0.5 - amu) * rcp_nr(amu) * a.inv_dt;
               if (shf) atomicAdd(&S.bclo[edge == 0 ? 0 : 1], bc);
               else atomicAdd(&a.t.boundary_closure[edge == 0 ? 0 : 1], bc);
             }
@@ -1001,13 +1003,13 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
         HWWG_CHECK(p.cell >= 0 && p.cell < I);
         const double c = s_cent[p.cell];
         if (p.w > c * a.rho) {
-          double n = ceil(p.w / c);
+          double n = ceil(p.w * rcp_nr(c));  // (no IEEE division: its slow-path call)
           if (n > 1e6) {
             n = 1e6;
             atomicAdd(&s_rare[2], 1u);
           }
           split_n = (unsigned)n;
-          p.w = p.w / n;
+          p.w = p.w * rcp_nr(n);
           atomicAdd(&s_rare[0], 1u);
           atomicAdd(&s_rare[1], split_n - 1);
         } else if (p.w < c * a.inv_rho) {
