@@ -244,6 +244,12 @@ struct hwwg_driver {
   int rank = 0, world = 1;
   uint64_t shard_lo = 0;    // first history of this rank's share of the step-1 pulse bank
   uint64_t fsrc_local = 0;  // combed histories this rank holds (the front of fsrc)
+  // fsrc's first src_packed slots are single-GPU comb teeth stored as (x, mu)
+  // only (FastCombArgs::packed_out; FastArgs::n_packed): weight comb_mem[1]
+  // (the spacing, on the device), time src_t0
+  uint64_t src_packed = 0;
+  double src_t0 = 0.0;
+  int packed_teeth = 1;  // HWWG_PACKED_TEETH=0: full 48 B teeth (A/B and tests)
   Comm* comm = nullptr;      // NCCL or the in-process loopback (comm.h)
   bool own_stream = true;    // false: the loopback hub's shared stream
   DevBuf<double> nccl_buf;    // all-gathered census weights, snapshot slabs
@@ -926,6 +932,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   // segments' transport.
   std::vector<size_t> seg_wait;  // segment u waits for upload event h2d_ev[seg_wait[u]]
   std::vector<uint64_t> seg_range;  // packed uploads: segment u converts [seg_range[u], seg_range[u+1])
+  d->src_packed = 0;  // set below where the step's source starts with packed comb teeth
   if (c.host_bank && d->fast && d->host_pre_combed && d->world == 1 && !(c.vol_rate > 0.0)) {
     const uint64_t Hs = d->host_bank_n;
     const std::vector<uint64_t> bounds = xfer_chunks(c, d->hybrid(), Hs, &seg_wait);
@@ -961,7 +968,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
       lo = hi;
     }
     if (hprof && d->xt[3]) HWWG_CUDA(cudaEventRecord(d->xt[3], d->copy_stream));
-    if (d->host_packed) {  // segment u's particle range, converted on s before it runs
+    if (d->host_packed && d->host_uniform) {
+      // comb teeth (x, mu): the transport derives the rest (FastArgs::n_packed),
+      // no conversion; the spacing is still in comb_mem[1] from the pre-comb
+      d->src_packed = Hs;
+      d->src_t0 = d->host_t0;
+    } else if (d->host_packed) {  // segment u's particle range, converted on s before it runs
       seg_range.assign(seg_wait.size() + 1, 0);
       for (size_t u = 0; u < seg_wait.size(); ++u) seg_range[u + 1] = bounds[seg_wait[u]];
     }
@@ -1023,6 +1035,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     rec->comb_out = H;
   } else if (d->fast && d->world > 1) {
     if (!do_comb) throw ApiError(HWWG_EINVAL, "philox mode combs every step (comb_overflow_factor <= 1)");
+    d->src_packed = 0;  // the multi-rank teeth are full records
     H = multi_gpu_comb(d, step, nv_step, Lmulti, s);
     rec->comb_in = d->bank_n;  // this rank's census slots
     rec->comb_out = H;
@@ -1051,6 +1064,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.out = d->fsrc.view();
     // after the cold start, tooth k becomes history perm(k) (see Perm)
     if (step > 1) a.perm = make_perm(d->target, c.seed, step);
+    a.packed_out = d->packed_teeth;  // teeth as (x, mu): the transport derives the rest
+    d->src_packed = d->packed_teeth ? d->target : 0;
+    d->src_t0 = d->bank_t;
     // the integer scale from the bank's weight: the previous step's census
     // weight tallies (still in the slab), or the pulse source's strength
     if (d->has_prev_report) {
@@ -1302,6 +1318,12 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         const FastBank src = d->fsrc.view();
         fa.src = FastBank{src.xm + l_lo, src.wt + l_lo, src.meta + l_lo};
         fa.n_src = l_hi - l_lo;
+        // the comb teeth among them are (x, mu) only (single GPU: local = global slot)
+        fa.n_packed = d->src_packed > l_lo ? std::min<uint64_t>(d->src_packed - l_lo, fa.n_src) : 0;
+        fa.src_w0 = d->comb_mem.p + 1;
+        fa.src_t0 = d->src_t0;
+        fa.src_hist0 = (unsigned)l_lo;
+        fa.inv_w0 = d->prob.view.uniform ? 1.0 / d->prob.view.w0 : 0.0;
         fa.src_head = d->src_head.p;
         fa.census = d->fcensus.view();
         fa.census_count = d->counter.p;
@@ -1688,9 +1710,11 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     a.perm = make_perm(d->target, c.seed, step + 1);
     a.hint_batches = d->tal.p.census_weight_batch;  // this step's census weight
     a.hint_n = B;
+    a.packed_out = 1;  // (x, mu) teeth; weight comb_mem[1], time bank_t
     if (d->bank_n == 0) throw ApiError(HWWG_EINVAL, "cannot comb an empty bank");
     launch_fast_comb(a, s);
     d->launches += 3;
+    d->src_t0 = d->bank_t;
     d->pre_comb_in = d->bank_n;
     d->host_pre_combed = true;
     d->host_bank_n = d->target;
@@ -1699,18 +1723,20 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     // volumetric particles to append): (x, mu) now, (w, t) only if not shared
     d->host_packed = !(c.vol_rate > 0.0);
     if (d->host_packed) {
-      launch_check_uniform(d->fsrc.wt.p, d->target, d->uni_flag.p, d->uni_first.p, s);
-      ++d->launches;
-      rec->d2h_bytes += d->target * sizeof(double2) + 32;
-      HWWG_CUDA(cudaMemcpyAsync(d->h_uni, d->uni_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-      HWWG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d->h_uni) + 16, d->uni_first.p,
-                                sizeof(double2), cudaMemcpyDeviceToHost, s));
+      // the teeth share one (w, t) by construction (packed_out): the spacing
+      // comes down with the record, the census time is known here
+      d->h_uni[0] = 0u;
+      reinterpret_cast<double*>(reinterpret_cast<char*>(d->h_uni) + 16)[1] = d->bank_t;
+      rec->d2h_bytes += d->target * sizeof(double2) + 8;
+      HWWG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d->h_uni) + 16, d->comb_mem.p + 1,
+                                sizeof(double), cudaMemcpyDeviceToHost, s));
       // (x, mu) go down at the end of this call (download_source), after the
       // step's own readbacks: queued behind 160 MB they would wait for it
       HWWG_CUDA(cudaEventRecord(d->ev_pre, s));
       d->d2h_pending = true;
     } else {
-      launch_fast_to_aos(d->fsrc.view(), d->target, d->bank.p, s);
+      launch_fast_to_aos_packed(d->fsrc.view(), d->target, d->target, d->comb_mem.p + 1, d->bank_t,
+                                d->bank.p, s);
       ++d->launches;
       rec->d2h_bytes += d->target * sizeof(hwwg_particle);
       HWWG_CUDA(cudaMemcpyAsync(d->host_bank, d->bank.p, d->target * sizeof(hwwg_particle),
@@ -1782,6 +1808,8 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->host_t0 = f[1];
     if (!d->host_uniform) {  // (w, t) differ: they cross too, after the (x, mu) block
       double2* hb = reinterpret_cast<double2*>(d->host_bank);
+      if (d->world == 1)  // single-GPU teeth carry no (w, t) of their own: write them out
+        launch_fill_wt(d->fsrc.wt.p, d->host_bank_n, d->comb_mem.p + 1, d->host_t0, s);
       HWWG_CUDA(cudaMemcpyAsync(hb + d->host_bank_n, d->fsrc.wt.p,
                                 d->host_bank_n * sizeof(double2), cudaMemcpyDeviceToHost, s));
       HWWG_CUDA(cudaStreamSynchronize(s));
@@ -1936,6 +1964,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_PRECOMB_K")) d->precomb_k = std::max(1.0, std::atof(m));
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_E2E_PIPE")) d->e2e_pipe = std::atoi(m) != 0;
+  if (const char* m = std::getenv("HWWG_PACKED_TEETH")) d->packed_teeth = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
     const int w = std::atoi(m);
     d->block_warps = (w == 12 || w == 14 || w == 24) ? w : 0;
@@ -2086,8 +2115,10 @@ int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t*
     count = c;
   } else if (d->fast && d->host_pre_combed && d->host_packed) {
     // the pre-combed source crossed PCIe packed; hand out AoS particles
+    // (single GPU: its teeth are (x, mu) only, weight comb_mem[1], time src_t0)
     d->bank.reserve(std::max<uint64_t>(d->bank_n, 1));
-    launch_fast_to_aos(d->fsrc.view(), d->bank_n, d->bank.p, d->stream);
+    launch_fast_to_aos_packed(d->fsrc.view(), d->bank_n, d->world == 1 ? d->bank_n : 0,
+                              d->comb_mem.p + 1, d->src_t0, d->bank.p, d->stream);
   }
   *n = count;
   if (!out || cap < count) return fail(HWWG_ENOSPC, "bank buffer too small");

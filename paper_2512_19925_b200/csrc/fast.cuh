@@ -67,6 +67,14 @@ __device__ __forceinline__ void fast_pool_reset(unsigned long long* ctl,
 struct FastArgs {
   FastBank src;  // this segment's source particles
   unsigned long long n_src;
+  // Source slots [0, n_packed) are comb teeth stored as (x, mu) alone (the
+  // comb's packed output): weight *src_w0 (the comb spacing, in device
+  // memory), time src_t0, cell located from x, history src_hist0 + slot,
+  // lineage key 0, draw 0. Slots from n_packed on are full records.
+  unsigned long long n_packed;
+  const double* src_w0;
+  double src_t0, inv_w0;
+  unsigned src_hist0;
   unsigned long long* src_head;  // refill cursor (zeroed per segment)
   CensusBank census;
   unsigned long long* census_count;
@@ -229,6 +237,9 @@ struct FastCombArgs {
   void* temp;
   size_t temp_bytes;
   Perm perm;  // tooth k is written at perm(k), as history perm(k) (n == 0: identity)
+  // 1: write (x, mu) only (FastArgs::n_packed: the transport derives the
+  // rest of a tooth); 0: full 48 B records
+  int packed_out;
   // a bound-grade estimate of the bank's total weight (hint_host plus the
   // hint_n device doubles at hint_batches: the step's census weight per
   // batch), which fixes the comb's integer scale before it reads the bank
@@ -260,6 +271,12 @@ void launch_fast_permute(FastBank in, FastBank out, uint64_t n, Perm perm, const
 // track_flux[i] = sum_b track_flux_batch[b][i] (fast mode scores batches only)
 void launch_track_from_batches(TallyPtrs t, int I, int B, cudaStream_t s);
 void launch_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out, cudaStream_t s);
+// the same for a source whose first n_packed slots are comb teeth (x, mu only):
+// w = *w0 (device), t = t0
+void launch_fast_to_aos_packed(FastBank in, uint64_t n, uint64_t n_packed, const double* w0,
+                               double t0, hwwg_particle* out, cudaStream_t s);
+// (w, t) of the first n slots (comb teeth) written out: w = *w0 (device), t = t0
+void launch_fill_wt(double2* wt, uint64_t n, const double* w0, double t0, cudaStream_t s);
 // e2e packed host round trip: flag (zeroed here) = 1 unless every (w, t) equals
 // wt[0] (copied to *first); and (x, mu) already in out.xm -> cell, identity
 // hist0 + i, and (w0, t0) when uniform.

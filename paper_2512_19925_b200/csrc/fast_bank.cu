@@ -43,10 +43,11 @@ __device__ __forceinline__ int locate_cell_mul(const MeshView& m, double x, doub
 __device__ __forceinline__ void write_tooth(const FastCombArgs& a, double2 xm, uint64_t k,
                                             double spacing, double inv_w0) {
   HWWG_CHECK(k < a.target);
-  const int c = locate_cell_mul(a.mesh, xm.x, inv_w0);  // as advance_history locates a start (transport.cpp:95)
   const uint64_t p = a.perm(k);
   HWWG_CHECK(p < a.target);
   a.out.xm[p] = xm;
+  if (a.packed_out) return;  // the transport derives (w, t), cell and identity
+  const int c = locate_cell_mul(a.mesh, xm.x, inv_w0);  // as advance_history locates a start (transport.cpp:95)
   a.out.wt[p] = make_double2(spacing, a.t_bank);
   a.out.meta[p] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)p, 0u, 0u);
 }
@@ -60,6 +61,7 @@ __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src,
     const uint64_t p = a.perm(k);
     HWWG_CHECK(p < a.target);
     a.out.xm[p] = xm;
+    if (a.packed_out) continue;
     a.out.wt[p] = make_double2(spacing, a.t_bank);
     // fresh identity for the new step: history = its slot, key 0, draw 0
     a.out.meta[p] = make_uint4((unsigned)(c < 0 ? 0 : c), (unsigned)p, 0u, 0u);
@@ -464,6 +466,20 @@ __global__ void k_track_from_batches(TallyPtrs t, int I, int B) {
   t.track_flux[i] = s;
 }
 
+__global__ void k_fast_to_aos_packed(FastBank in, uint64_t n, uint64_t n_packed, const double* w0,
+                                     double t0, hwwg_particle* out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2* o = reinterpret_cast<double2*>(out) + 2 * i;
+  o[0] = in.xm[i];
+  o[1] = i < n_packed ? make_double2(*w0, t0) : in.wt[i];
+}
+
+__global__ void k_fill_wt(double2* wt, uint64_t n, const double* w0, double t0) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) wt[i] = make_double2(*w0, t0);
+}
+
 __global__ void k_fast_to_aos(FastBank in, uint64_t n, hwwg_particle* out) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -661,6 +677,19 @@ void launch_step_start(double* slab, size_t slab_words, unsigned long long* curs
 
 void launch_track_from_batches(TallyPtrs t, int I, int B, cudaStream_t s) {
   k_track_from_batches<<<(I + 255) / 256, 256, 0, s>>>(t, I, B);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fast_to_aos_packed(FastBank in, uint64_t n, uint64_t n_packed, const double* w0,
+                               double t0, hwwg_particle* out, cudaStream_t s) {
+  if (!n) return;
+  k_fast_to_aos_packed<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, n_packed, w0, t0, out);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_fill_wt(double2* wt, uint64_t n, const double* w0, double t0, cudaStream_t s) {
+  if (!n) return;
+  k_fill_wt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(wt, n, w0, t0);
   HWWG_CUDA(cudaGetLastError());
 }
 

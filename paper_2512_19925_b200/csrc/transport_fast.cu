@@ -174,6 +174,30 @@ __device__ __forceinline__ int batch_fast(unsigned h, unsigned long long H, int 
 
 __constant__ double c_logtab[256] = HWWG_LOG_TAB;
 
+// mesh.cpp:26-40 for a comb tooth's x: the uniform estimate by a multiplication
+// (any estimate within one cell becomes the unique c with edges[c] <= x <
+// edges[c+1] under the +-1 guards), else a binary search over the edges in
+// shared memory; -1 outside the mesh
+__device__ __forceinline__ int locate_cell_mul(const MeshView& m, double x, double inv_w0,
+                                               const double* e) {
+  if (x < m.x_min || x > m.x_max) return -1;
+  if (x == m.x_max) return m.I - 1;
+  if (m.uniform) {
+    int c = (int)((x - m.x_min) * inv_w0);
+    c = c < 0 ? 0 : (c >= m.I ? m.I - 1 : c);
+    if (x < e[c]) --c;
+    else if (x >= e[c + 1]) ++c;
+    return c;
+  }
+  int lo = 0, hi = m.I + 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (e[mid] > x) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo - 1;
+}
+
 // 1 / x to within an ulp: the MUFU reciprocal estimate and two Newton steps
 // (the IEEE division's 1 / mu cost a slow-path check per direction change);
 // x = 0 keeps the IEEE answer (+-inf)
@@ -572,6 +596,8 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   for (int e = threadIdx.x; e <= I; e += blockDim.x) s_edge[e] = edges[e];
   __shared__ double s_logtab[256];
   for (int j = threadIdx.x; j < 256; j += blockDim.x) s_logtab[j] = c_logtab[j];
+  __shared__ double s_w0;  // the weight of every comb tooth (the comb spacing, on the device)
+  if (threadIdx.x == 0) s_w0 = a.n_packed ? *a.src_w0 : 0.0;
   // census thinning (FastArgs::precomb): each lane's distance to its next tooth,
   // in (0, s0], starting at a uniform offset; kept in global memory (L1-resident,
   // touched only at census events) off the event loop's registers and shared memory
@@ -608,6 +634,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   // source reservation (warp-uniform) and the claim in flight (lane 0)
   // (32-bit: the driver keeps a segment's source below 2^32 - 2^26 particles)
   const unsigned n_src = (unsigned)a.n_src;
+  const unsigned n_packed = (unsigned)a.n_packed;
   unsigned r_lo = (unsigned)gwarp * kClaim, r_hi = r_lo + kClaim;
   if (r_lo >= n_src) r_lo = r_hi = 0, src_done = true;
   else if (r_hi > n_src) r_hi = n_src;
@@ -768,8 +795,10 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
         const unsigned pi =
             a.scramble && (kk | 1023u) < n_src ? (kk & ~1023u) | (__brev(kk) >> 22) : kk;
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.xm + pi));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.wt + pi));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.meta + pi));
+        if (pi >= n_packed) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.wt + pi));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.meta + pi));
+        }
       }
       const unsigned rank = __popc(need & lt);
       if (!p.alive && rank < take) {
@@ -782,16 +811,25 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
         {
           HWWG_CHECK(idx < n_src);
           const double2 xm = a.src.xm[idx];
-          const double2 wt = a.src.wt[idx];
-          const uint4 m = a.src.meta[idx];
           p.x = xm.x;
           p.mu = xm.y;
-          p.w = wt.x;
-          p.t = wt.y;
-          p.cell = (int)(m.x & 0xffffu);
-          p.ctr = m.x >> 16;
-          p.hist = m.y;
-          p.key = ((unsigned long long)m.w << 32) | m.z;
+          if (idx < n_packed) {  // a comb tooth: (x, mu) only (FastArgs::n_packed)
+            p.w = s_w0;
+            p.t = a.src_t0;
+            p.cell = locate_cell_mul(a.mesh, p.x, a.inv_w0, s_edge);
+            p.ctr = 0;
+            p.hist = a.src_hist0 + idx;
+            p.key = 0;
+          } else {
+            const double2 wt = a.src.wt[idx];
+            const uint4 m = a.src.meta[idx];
+            p.w = wt.x;
+            p.t = wt.y;
+            p.cell = (int)(m.x & 0xffffu);
+            p.ctr = m.x >> 16;
+            p.hist = m.y;
+            p.key = ((unsigned long long)m.w << 32) | m.z;
+          }
           p.inv_mu = rcp_nr(p.mu);
           p.bslot = batch_fast(p.hist, a.H, a.B, a.bmul) - (shf ? a.b_lo : 0);
           p.alive = p.w > 0.0;
