@@ -134,6 +134,10 @@ typedef struct {
 
 /* ncclGetUniqueId for the multi-GPU driver (out: 128 bytes). */
 int hwwg_nccl_unique_id(uint8_t* out);
+/* The driver's NCCL calls (run-time load, unique id, CommInitRank, sum/max
+ * all-reduce, all-gather, grouped send/recv) on a one-rank communicator on
+ * `device`, results checked; report (nullable) gets "ok" or the mismatches. */
+int hwwg_nccl_selftest(int32_t device, uint8_t* report, uint64_t report_bytes);
 /* In-process collective hub for `world` driver ranks on `device`: the drivers
  * share one CUDA stream and meet at a host barrier in every collective (each
  * rank's hwwg_driver_step must run on its own host thread). */

@@ -134,7 +134,7 @@ EXPORTS = (
     "hwwg_driver_step", "hwwg_driver_arrays", "hwwg_driver_bank", "hwwg_load_config_file",
     "hwwg_default_config", "hwwg_validate_config", "hwwg_losm_assemble_solve",
     "hwwg_build_centers", "hwwg_moving_average", "hwwg_uniform_comb", "hwwg_device_log",
-    "hwwg_nccl_unique_id", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan",
+    "hwwg_nccl_unique_id", "hwwg_nccl_selftest", "hwwg_shard_range", "hwwg_comb_plan", "hwwg_rebalance_plan",
     "hwwg_fourier_lowpass", "hwwg_write_step_csv", "hwwg_write_summary_csv", "hwwg_write_run_json", "hwwg_driver_write",
     "hwwg_loopback_create", "hwwg_loopback_destroy", "hwwg_driver_set_reference",
     "hwwg_driver_load_reference", "hwwg_save_reference_csv", "hwwg_load_reference_csv",
@@ -184,6 +184,7 @@ def lib():
                                     C.c_uint64, C.c_void_p, dptr, dptr]
     L.hwwg_device_log.argtypes = [C.c_void_p, dptr, C.c_uint64, dptr]
     L.hwwg_nccl_unique_id.argtypes = [C.c_void_p]
+    L.hwwg_nccl_selftest.argtypes = [C.c_int32, C.c_void_p, C.c_uint64]
     L.hwwg_loopback_create.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
     L.hwwg_loopback_destroy.argtypes = [C.c_void_p]
     L.hwwg_loopback_destroy.restype = None

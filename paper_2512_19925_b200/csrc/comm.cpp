@@ -4,10 +4,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -308,6 +310,73 @@ int hwwg_nccl_unique_id(uint8_t* out) {
   std::memset(out, 0, 128);
   std::memcpy(out, &id, sizeof(id) < 128 ? sizeof(id) : 128);
   return HWWG_OK;
+  HWWG_API_END
+}
+
+int hwwg_nccl_selftest(int32_t device, uint8_t* report, uint64_t report_bytes) {
+  HWWG_API_BEGIN
+  // The driver's NCCL collectives on a one-rank communicator: the run-time
+  // NCCL load, the unique-id hand-off, CommInitRank and every call the
+  // multi-GPU driver makes (sum/max all-reduce, all-gather, grouped
+  // send/recv — here to itself), with their results checked.
+  COMM_CUDA(cudaSetDevice(device));
+  uint8_t id[128];
+  {
+    ncclUniqueId u;
+    COMM_NCCL(nccl().GetUniqueId(&u));
+    std::memset(id, 0, sizeof id);
+    std::memcpy(id, &u, sizeof(u) < 128 ? sizeof(u) : 128);
+  }
+  cudaStream_t s;
+  COMM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::string msg;
+  {
+    using namespace hwwg;
+    std::unique_ptr<Comm> cp(make_nccl_comm(id, 0, 1));
+    Comm& c = *cp;
+    const double hd[3] = {1.5, -2.0, 3.25};
+    const unsigned long long hu[2] = {7ULL, 1ULL << 40};
+    void* dmem = nullptr;
+    COMM_CUDA(cudaMalloc(&dmem, 256));
+    double* d_in = static_cast<double*>(dmem);
+    double* d_out = d_in + 4;
+    unsigned long long* u_in = reinterpret_cast<unsigned long long*>(d_in + 8);
+    unsigned long long* u_out = u_in + 4;
+    COMM_CUDA(cudaMemcpy(d_in, hd, sizeof hd, cudaMemcpyHostToDevice));
+    COMM_CUDA(cudaMemcpy(u_in, hu, sizeof hu, cudaMemcpyHostToDevice));
+    c.all_reduce(d_in, d_out, 3, DType::kF64, RedOp::kSum, s);
+    c.all_reduce(u_in, u_out, 2, DType::kU64, RedOp::kMax, s);
+    double rd[3];
+    unsigned long long ru[2], rg[2], rs[2];
+    COMM_CUDA(cudaStreamSynchronize(s));
+    COMM_CUDA(cudaMemcpy(rd, d_out, sizeof rd, cudaMemcpyDeviceToHost));
+    COMM_CUDA(cudaMemcpy(ru, u_out, sizeof ru, cudaMemcpyDeviceToHost));
+    c.all_gather(u_in, u_out, 2, DType::kU64, s);
+    COMM_CUDA(cudaStreamSynchronize(s));
+    COMM_CUDA(cudaMemcpy(rg, u_out, sizeof rg, cudaMemcpyDeviceToHost));
+    COMM_CUDA(cudaMemset(u_out, 0, 16));
+    c.group_start();
+    c.send(u_in, 2, DType::kU64, 0, s);
+    c.recv(u_out, 2, DType::kU64, 0, s);
+    c.group_end(s);
+    COMM_CUDA(cudaStreamSynchronize(s));
+    COMM_CUDA(cudaMemcpy(rs, u_out, sizeof rs, cudaMemcpyDeviceToHost));
+    COMM_CUDA(cudaFree(dmem));
+    for (int i = 0; i < 3; ++i)
+      if (rd[i] != hd[i]) msg += "all_reduce sum f64 differs; ";
+    for (int i = 0; i < 2; ++i) {
+      if (ru[i] != hu[i]) msg += "all_reduce max u64 differs; ";
+      if (rg[i] != hu[i]) msg += "all_gather u64 differs; ";
+      if (rs[i] != hu[i]) msg += "send/recv u64 differs; ";
+    }
+  }
+  COMM_CUDA(cudaStreamDestroy(s));
+  if (report && report_bytes) {
+    const std::string r = msg.empty() ? "ok" : msg;
+    std::memset(report, 0, report_bytes);
+    std::memcpy(report, r.data(), std::min<size_t>(r.size(), report_bytes - 1));
+  }
+  return msg.empty() ? HWWG_OK : hwwg::fail(HWWG_ECUDA, "nccl self-test: " + msg);
   HWWG_API_END
 }
 

@@ -191,3 +191,18 @@ def test_host_round_trip_multirank():
         if n >= 1:  # steps after the first open with a pre-combed share from the host
             per_rank = [host[r][n][0].h2d_bytes for r in range(W)]
             assert sum(per_rank) == H * 16, per_rank
+
+
+def test_nccl_one_rank_selftest():
+    """The NCCL backend of the driver's Comm on a one-rank communicator (the only
+    NCCL this one-GPU pool can run): NCCL is loaded at run time next to torch's
+    copy, the unique id round-trips, and the sum/max all-reduce, all-gather and
+    grouped send/recv the multi-GPU driver issues return the right data."""
+    import ctypes as C
+
+    import torch  # noqa: F401  (torch's NCCL is the one already in the process under torchrun)
+    from paper_2512_19925_b200 import _capi as A
+    buf = C.create_string_buffer(256)
+    rc = A.lib().hwwg_nccl_selftest(0, buf, 256)
+    assert rc == 0, (rc, A.lib().hwwg_last_error())
+    assert buf.value == b"ok", buf.value
