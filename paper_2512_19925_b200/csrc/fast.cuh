@@ -64,6 +64,16 @@ __device__ __forceinline__ void fast_pool_reset(unsigned long long* ctl,
   *src_head = 0;
 }
 
+// Dynamic shared-memory layout of the transport kernel, in doubles from its
+// base (filled by launch_fast_segment): the track counts at 0, the tally
+// histograms, then the window centres and the mesh edges. Passed precomputed so
+// the event loop's address arithmetic takes constant-bank operands instead of
+// re-deriving the layout from I and nb (the compiler rematerialises it under
+// register pressure).
+struct SmemOffsets {
+  unsigned trk, cphi, cJ, cF, edge, cwb, bclo, cent, edgex;
+};
+
 struct FastArgs {
   FastBank src;  // this segment's source particles
   unsigned long long n_src;
@@ -143,6 +153,7 @@ struct FastArgs {
   double pc_s0, pc_inv_s0;
   unsigned pc_key;
   double* pc_need;  // 32 per warp of the grid
+  SmemOffsets so;   // set by launch_fast_segment
 };
 size_t fast_flush_stride(int I, int B);  // words per flush replica (nb <= B)
 

@@ -528,19 +528,6 @@ struct SmemTally {
   unsigned* trc;  // I
 };
 
-// slotw: doubles per track/edge slot (1 fp64, 2 fixed-point limbs)
-__device__ __forceinline__ SmemTally smem_view(double* base, int I, int nb, int slotw) {
-  SmemTally s;
-  s.trc = reinterpret_cast<unsigned*>(base);  // first: mode 2 keeps only the counts
-  s.trk = base + (I + 1) / 2;
-  s.cphi = s.trk + (size_t)slotw * nb * I;
-  s.cJ = s.cphi + (size_t)slotw * I;
-  s.cF = s.cJ + (size_t)slotw * I;
-  s.edge = s.cF + (size_t)slotw * I;
-  s.cwb = s.edge + (size_t)slotw * (I + 1);  // kFix: limb slots too (after the edges)
-  s.bclo = s.cwb + (size_t)slotw * nb;
-  return s;
-}
 
 // kShf: the fp64 tallies live in block-private shared memory (smem_tallies ==
 // 1), statically, so the atomics compile to shared-memory CAS loops with no
@@ -572,11 +559,18 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   const bool sh = a.smem_tallies != 0;       // shared memory in use (zero + flush)
   constexpr bool shf = kShf;                 // fp64 tallies in shared memory
   constexpr int slotw = kFix ? 2 : 1;
-  SmemTally S = smem_view(smem, I, a.nb, slotw);
-  // dynamic shared memory: [tallies (mode-dependent words) | window centres I]
-  const size_t tally_words =
-      shf ? (size_t)slotw * ((size_t)a.nb * I + 4 * (size_t)I + 1 + a.nb) + 2 + (I + 1) / 2
-          : (sh ? (size_t)(I + 1) / 2 : 0);
+  // dynamic shared memory: [tallies (mode-dependent words) | window centres I |
+  // edges I + 1], offsets precomputed on the host (FastArgs::so)
+  SmemTally S;
+  S.trc = reinterpret_cast<unsigned*>(smem);
+  S.trk = smem + a.so.trk;
+  S.cphi = smem + a.so.cphi;
+  S.cJ = smem + a.so.cJ;
+  S.cF = smem + a.so.cF;
+  S.edge = smem + a.so.edge;
+  S.cwb = smem + a.so.cwb;
+  S.bclo = smem + a.so.bclo;
+  const size_t tally_words = a.so.cent;
   const double fix_trk = kFix ? pow2(a.fix_k_trk) : 0.0;
   const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
   const double fix_cw = kFix ? pow2(a.fix_k_cw) : 0.0;
@@ -588,11 +582,11 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   const unsigned fix_spl = (fix_slots + 4095u) / 4096u;
   if (kFix && threadIdx.x == 0) s_sweep = 0u;
   for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
-  double* s_cent = smem + tally_words;  // read at every window site: keep it on chip
+  double* s_cent = smem + a.so.cent;  // read at every window site: keep it on chip
   if (windows)
     for (int i = threadIdx.x; i < I; i += blockDim.x) s_cent[i] = a.centers[i];
   // mesh edges (read at every event) and the log table, on chip
-  double* s_edge = s_cent + I;
+  double* s_edge = smem + a.so.edgex;
   for (int e = threadIdx.x; e <= I; e += blockDim.x) s_edge[e] = edges[e];
   __shared__ double s_logtab[256];
   for (int j = threadIdx.x; j < 256; j += blockDim.x) s_logtab[j] = c_logtab[j];
@@ -1541,8 +1535,23 @@ void configure_fast_kernel() {
   done_dev = dev;
 }
 
-void launch_fast_segment(const FastArgs& a, int blocks, size_t smem, cudaStream_t s) {
+void launch_fast_segment(const FastArgs& a0, int blocks, size_t smem, cudaStream_t s) {
   configure_fast_kernel();
+  FastArgs a = a0;
+  {  // the dynamic shared-memory layout (SmemOffsets; smem_view's order)
+    const unsigned I = (unsigned)a.mesh.I, nb = (unsigned)a.nb;
+    const unsigned slotw = (a.smem_tallies == 1 && a.fix) ? 2u : 1u;
+    SmemOffsets& o = a.so;
+    o.trk = (I + 1) / 2;
+    o.cphi = o.trk + slotw * nb * I;
+    o.cJ = o.cphi + slotw * I;
+    o.cF = o.cJ + slotw * I;
+    o.edge = o.cF + slotw * I;
+    o.cwb = o.edge + slotw * (I + 1);
+    o.bclo = o.cwb + slotw * nb;
+    o.cent = a.smem_tallies == 1 ? o.bclo + 2 : (a.smem_tallies ? (I + 1) / 2 : 0);
+    o.edgex = o.cent + I;
+  }
   if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head, a.span);
   const bool shf = a.smem_tallies == 1;
   const bool fix = shf && a.fix;
