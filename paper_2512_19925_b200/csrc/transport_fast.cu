@@ -9,14 +9,17 @@
 // One Philox block per event: flight, collision channel and scattering
 // deviates (the roulette deviate after a scatter is the channel one recycled).
 //
-// Work model — a persistent grid (3 CTAs of 8 warps per SM), one particle per
+// Work model — a persistent grid (2 CTAs of 14 warps per SM, or one 24-warp
+// CTA for large tally copies), one particle per
 // lane, one EVENT per loop trip (free flight -> census | cell crossing |
 // collision), with refill: a lane whose particle terminated takes the next
 // unit of work from
 //   1. its warp's run-length-encoded split stack (LIFO, like the reference;
 //      the bottom kSmemStack records in shared memory),
 //   2. the source bank, through a per-warp reservation of kClaim particles
-//      claimed one trip ahead (first one static) and prefetched into L1,
+//      claimed one trip ahead (first one static) and prefetched into L1; comb
+//      teeth are (x, mu) only (FastArgs::n_packed) and get their weight, time,
+//      cell and identity here,
 //   3. the global pool of split records other warps donated (ticket queue).
 // A split never materialises its daughters: it pushes ONE record (state, n-1
 // copies) and lanes pop daughters from it — the bank-expansion step done by
@@ -27,14 +30,21 @@
 // Roulette and unchanged windows cost no memory traffic.
 //
 // Tallies: block-private shared-memory histograms over the segment's batch
-// range (track-length by batch and cell, census phi/J/F, edge currents,
-// per-cell track counts), flushed once per block with fp64 REDs. Where the
-// wider slots fit, track/edge/census scores are fixed-point integers added as
-// 16-bit limbs with native 32-bit shared atomics, kept from wrapping by a
-// rolling carry sweep (see fix_add / fix_sweep); otherwise fp64 slots (CAS
-// loops) with census scores run-aggregated across the warp, and global REDs
+// range (track-length by batch and cell, census phi/J/F, census weight by
+// batch, edge currents, per-cell track counts), flushed once per block with
+// fp64 REDs. Where the wider slots fit, these scores are fixed-point integers
+// added as 16-bit limbs with native 32-bit shared atomics, kept from wrapping
+// by a rolling carry sweep (see fix_add / fix_sweep); in the cold start the
+// census scores of identical split copies are grouped by an exact MATCH on
+// (cell, w, mu) first (census_groups). Otherwise fp64 slots (CAS loops) with
+// census scores run-aggregated across the warp, and global REDs
 // warp-aggregated (MATCH.ANY groups, REDUX fixed-point sums) when the
 // histograms do not fit in shared memory (I = 4000).
+//
+// Census thinning (FastArgs::precomb, the cold start): every lane combs the
+// census particles it banks at the spacing s0 and banks each once with its
+// teeth' weight n s0 (or not at all), so the x60 raw census never
+// materialises; the comb at the next step start combs the ~8 x target records.
 #include <algorithm>
 #include <cmath>
 #include <map>
@@ -51,12 +61,12 @@ namespace hwwg {
 
 namespace {
 
-// Two block shapes, both 24 resident warps per SM (the register budget at
-// 80 registers): 2 blocks of 12 warps, or 1 block of 24 warps when the
-// block's shared-memory tallies fit only once per SM (config 3's 1000 cells:
-// 2 blocks of 8 warps before, 16 warps per SM). One shared-memory tally set per
-// block; the driver picks the shape per launch (measured against 3 blocks of
-// 8 warps: C5 77.0 -> 76.2 ms, C3 73.7 -> 41 ms for 20 steps).
+// Block shapes (warps per SM at <= 72 registers): 2 blocks of 14 warps (28),
+// 2 of 12 (24), or 1 block of 24 warps when the block's shared-memory tallies
+// fit only once per SM or reach 96 KB (config 3's 1000 cells). One
+// shared-memory tally set per block; the driver picks the shape per launch
+// (C5: 2 x 14 2.54e10 seg/s against 2 x 12 2.43e10; C3: 1 x 24 2.0e10
+// against 2 x 14 1.5e10).
 constexpr int kMaxWarpsPerSm = 28;
 
 // -DHWWG_FAST_PROF: per-phase clock64 accounting of the loop (lane 0 of every
