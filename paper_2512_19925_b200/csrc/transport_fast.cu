@@ -123,9 +123,14 @@ constexpr unsigned kShare = HWWG_KSHARE;
 #endif
 constexpr unsigned kPollEvery = HWWG_POLL_EVERY;  // trips between looks at the pool counters
 #ifndef HWWG_SMEM_STACK
-#define HWWG_SMEM_STACK 16  // measured: 8 -> 16 is +2% on config 2 (split stacks stay on chip)
+#define HWWG_SMEM_STACK 24  // measured: 8 -> 16 is +2% on config 2, 16 -> 24 +0.7% on config 5 (split stacks stay on chip)
 #endif
-constexpr int kSmemStack = HWWG_SMEM_STACK;  // split-stack records per warp kept in shared memory
+// split-stack records per warp kept in shared memory: HWWG_SMEM_STACK for the
+// 12/14-warp blocks, 16 for the 24-warp block, whose shared memory goes to a
+// large tally copy (config 3: 16 is 1.3% faster than 24; config 5 at 2 x 14
+// warps: 24 is 0.7% faster than 16)
+template <int kW>
+__host__ __device__ constexpr int smem_stack() { return kW >= 24 ? 16 : HWWG_SMEM_STACK; }
 #ifndef HWWG_KPIECE
 #define HWWG_KPIECE 32
 #endif
@@ -553,6 +558,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   // per-warp RLE split stack: the bottom kSmemStack records on chip (steady
   // state rarely goes deeper), the rest in global memory
   FastStackRec* stk = a.stacks + (size_t)gwarp * a.stack_cap;
+  constexpr int kSmemStack = smem_stack<kW>();
   __shared__ FastStackRec s_stk[kW][kSmemStack];
   FastStackRec* s_my = s_stk[threadIdx.x >> 5];
 #define STK(i) (*((i) < kSmemStack ? &s_my[(i)] : &stk[(i)]))
