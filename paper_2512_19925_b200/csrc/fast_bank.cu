@@ -81,7 +81,10 @@ __device__ __forceinline__ void write_teeth(const FastCombArgs& a, uint64_t src,
 // boundary, so the teeth partition [0, target)). Two reads of the weights,
 // O(n / 4096) scratch, no n-sized prefix. Quantisation moves a tooth
 // boundary by < n * 2^-60 of the total.
-constexpr int kCbThreads = 256, kCbItems = 16, kCbTile = kCbThreads * kCbItems;
+#ifndef HWWG_CB_ITEMS
+#define HWWG_CB_ITEMS 16
+#endif
+constexpr int kCbThreads = 256, kCbItems = HWWG_CB_ITEMS, kCbTile = kCbThreads * kCbItems;
 
 // scratch (8-byte words of FastCombArgs::prefix): [0] scale, [1] integer
 // total, [2] spacing and [3] offset in integer units, [4] done-block counter,
