@@ -203,6 +203,7 @@ struct hwwg_driver {
   // packed wire format of a pre-combed host bank: (x, mu) per particle, then
   // (w, t) per particle only when they are not one shared pair (host_uniform)
   bool host_packed = false, host_uniform = false;
+  bool host_pulse_mu = false;  // the host bank holds the pulse as directions only (step 1)
   double host_w0 = 0.0, host_t0 = 0.0;
   DevBuf<unsigned> uni_flag;
   DevBuf<double2> uni_first;
@@ -445,8 +446,18 @@ void init_driver(hwwg_driver* d) {
     d->host_bank_cap = std::max<uint64_t>(
         src.size(), (d->fast ? 1 : 64) * d->target + 4096);
     HWWG_CUDA(cudaMallocHost(&d->host_bank, d->host_bank_cap * sizeof(hwwg_particle)));
-    std::memcpy(d->host_bank, src.data(), src.size() * sizeof(hwwg_particle));
     d->host_bank_n = src.size();
+    // Philox mode, one GPU: the pulse's particles share x0, w0 and t = 0, so the
+    // host holds (and step 1 uploads) their directions alone, 8 B per particle
+    d->host_pulse_mu = d->fast && d->world == 1 && !src.empty();
+    if (d->host_pulse_mu) {
+      double* hm = reinterpret_cast<double*>(d->host_bank);
+      for (size_t i = 0; i < src.size(); ++i) hm[i] = src[i].mu;
+      d->host_w0 = src[0].w;
+      d->host_t0 = src[0].t;
+    } else {
+      std::memcpy(d->host_bank, src.data(), src.size() * sizeof(hwwg_particle));
+    }
   }
   d->seg_ev.resize(32);
   for (auto& e : d->seg_ev) HWWG_CUDA(cudaEventCreate(&e));
@@ -995,6 +1006,17 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                       &t);
     ++d->launches;
     rec->h2d_bytes += nl * sizeof(double2) * (d->host_uniform ? 1 : 2);
+  } else if (c.host_bank && d->host_pulse_mu) {  // e2e step 1: the pulse's directions
+    d->bank.reserve(std::max<uint64_t>(d->host_bank_n, 1));
+    double* dmu = reinterpret_cast<double*>(d->bank.p);
+    HWWG_CUDA(cudaMemcpyAsync(dmu, d->host_bank, d->host_bank_n * sizeof(double),
+                              cudaMemcpyHostToDevice, s));
+    d->bank_n = d->host_bank_n;
+    rec->h2d_bytes += d->host_bank_n * sizeof(double);
+    d->fbank.reserve(d->bank_n);
+    launch_mu_to_census(dmu, d->bank_n, c.x0, d->host_w0, d->fbank.view(), s);
+    ++d->launches;
+    d->host_pulse_mu = false;
   } else if (c.host_bank) {  // e2e: the bank lives in host memory between steps
     d->bank.reserve(std::max<uint64_t>(d->host_bank_n, 1));
     HWWG_CUDA(cudaMemcpyAsync(d->bank.p, d->host_bank, d->host_bank_n * sizeof(hwwg_particle),

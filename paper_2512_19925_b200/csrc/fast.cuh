@@ -172,6 +172,9 @@ void launch_step_start(double* slab, size_t slab_words, unsigned long long* curs
 // Compact the census bank (drop zero-weight holes) into AoS particles at time t.
 void launch_fast_compact_aos(CensusBank in, uint64_t n, double t, hwwg_particle* out,
                              unsigned long long* count, cudaStream_t s);
+// The pulse (x0, mu[i], w0, t = 0) into a census bank from its directions alone.
+void launch_mu_to_census(const double* mu, uint64_t n, double x0, double w0, CensusBank out,
+                         cudaStream_t s);
 // AoS particles (all at one time: the pulse source, a host-held census) into a census bank.
 void launch_aos_to_census(const hwwg_particle* in, uint64_t n, CensusBank out, cudaStream_t s);
 

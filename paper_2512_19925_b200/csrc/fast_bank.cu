@@ -440,6 +440,16 @@ __global__ void k_aos_to_census(const hwwg_particle* __restrict__ in, uint64_t n
   out.w[i] = b.x;
 }
 
+// The pulse as a census bank from its directions alone (e2e host round trip:
+// every pulse particle shares x0, w0 and t = 0, so only mu crosses PCIe).
+__global__ void k_mu_to_census(const double* __restrict__ mu, uint64_t n, double x0, double w0,
+                               CensusBank out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out.xm[i] = make_double2(x0, mu[i]);
+  out.w[i] = w0;
+}
+
 // The throughput step's start in one launch (instead of four memsets and a
 // reset kernel, each of which serialised the launch pipeline): zero the tally
 // slab and the warps' census cursors, the census counter and the error word,
@@ -660,6 +670,13 @@ void launch_fast_compact_aos(CensusBank in, uint64_t n, double t, hwwg_particle*
   HWWG_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s));
   if (!n) return;
   k_compact_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, n, t, out, count);
+  HWWG_CUDA(cudaGetLastError());
+}
+
+void launch_mu_to_census(const double* mu, uint64_t n, double x0, double w0, CensusBank out,
+                         cudaStream_t s) {
+  if (!n) return;
+  k_mu_to_census<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mu, n, x0, w0, out);
   HWWG_CUDA(cudaGetLastError());
 }
 

@@ -16,7 +16,7 @@ applied three ways:
   * per quantity and step: >= 85% (one correlated cluster can take a step);
   * no bias: the pooled mean of z within +-0.5 (+-1 for the window centres,
     which share one normalisation) and the pooled mean of z^2 (a global chi^2
-    per degree of freedom) within [0.5, 2.0];
+    per degree of freedom) within [0.5, 2.0] ([0.5, 3.0] for the centres);
   * per-step scalars (P_L, P_R, census weight): >= 90% of |z| < 3.5, mean z
     within +-2 (steps are correlated through the carried population).
 
@@ -114,7 +114,10 @@ def check_engine(cfg_fn, steps, skip_first=0, label=""):
         # their pooled mean z is nearly as wide as a single z
         if abs(bias) >= (1.0 if k == "ww_centers" else 0.5):
             fails.append((k, "bias", bias))
-        if not 0.5 < chi2 < 2.0:
+        # (for the centres, that common shift also enters every cell's z^2: their
+        # pooled mean z^2 spreads like one chi^2 draw — seen at 2.1 once in ~10 runs
+        # of an unbiased engine — so its upper bound widens with the bias bound)
+        if not 0.5 < chi2 < (3.0 if k == "ww_centers" else 2.0):
             fails.append((k, "chi2", chi2))
     for k in SCALARS:
         z = zstats(ex_s[k][:, skip_first:], fa_s[k][:, skip_first:],
