@@ -793,37 +793,41 @@ uint64_t multi_gpu_comb(hwwg_driver* d, int step, uint64_t nv, StepLayout& L, cu
 
 __global__ void k_stream_mark() {}
 
-// e2e transfer sub-chunks of a combed source of Hs histories: the step's
-// segment ranges [0, h_1), [h_1, h_2), ... (the thresholds driver.cpp:170-177
-// puts at ceil(f * Hs)), each cut into pieces of about Hs / 32 particles, so
-// an upload can start as soon as its piece came down; *seg_last[u] = index of
-// the last piece of segment u.
-std::vector<uint64_t> xfer_chunks(const hwwg_run_config& c, bool hybrid, uint64_t Hs,
-                                  std::vector<size_t>* seg_last) {
-  std::vector<uint64_t> segs;
-  if (hybrid && c.u_ww > 0)
-    for (int i = 0; i < c.n_fractions; ++i) {
-      const uint64_t h = (uint64_t)std::ceil(c.fractions[i] * (double)Hs);
-      if (h >= Hs || (!segs.empty() && h <= segs.back())) continue;
-      segs.push_back(h);
-    }
-  segs.push_back(Hs);
-  const uint64_t piece = std::max<uint64_t>(Hs / 32, 1 << 16);
+// e2e transfer pieces of a combed source of Hs histories in a step of Hs + nv
+// (nv: the step's volumetric particles, sampled on the device after the teeth):
+// the step's segment ranges [0, h_1), [h_1, h_2), ... (driver.cpp:170-177,
+// make_layout) clipped to [0, Hs), each cut into pieces of about Hs / 32
+// particles, so an upload can start as soon as its piece came down;
+// *seg_last[u] = index of the last piece segment u needs.
+std::vector<uint64_t> xfer_chunks(const hwwg_run_config& c, bool hybrid, uint64_t Hs, uint64_t nv,
+                                  std::vector<size_t>* seg_last, uint64_t piece = 0) {
+  std::vector<uint64_t> segs = step_thresholds(c, hybrid, Hs + nv);
+  segs.push_back(Hs + nv);
+  if (!piece) piece = std::max<uint64_t>(Hs / 32, 1 << 16);
   std::vector<uint64_t> ends;
   if (seg_last) seg_last->clear();
   uint64_t lo = 0;
-  for (uint64_t hi : segs) {
-    const uint64_t n = std::max<uint64_t>(1, (hi - lo + piece - 1) / piece);
-    for (uint64_t k = 1; k <= n; ++k) ends.push_back(k == n ? hi : lo + k * ((hi - lo) / n));
-    if (seg_last) seg_last->push_back(ends.size() - 1);
-    lo = hi;
+  for (uint64_t e : segs) {
+    const uint64_t hi = std::min(e, Hs);
+    if (hi > lo) {
+      const uint64_t n = std::max<uint64_t>(1, (hi - lo + piece - 1) / piece);
+      for (uint64_t k = 1; k <= n; ++k) ends.push_back(k == n ? hi : lo + k * ((hi - lo) / n));
+      lo = hi;
+    }
+    if (seg_last) seg_last->push_back(ends.empty() ? 0 : ends.size() - 1);
   }
-  if (ends.size() > kMaxXferChunks) {  // many thresholds: one piece per segment
-    ends = segs;
-    if (seg_last)
-      for (size_t u = 0; u < seg_last->size(); ++u) (*seg_last)[u] = u;
-  }
+  // many thresholds: one piece per segment
+  if (ends.size() > kMaxXferChunks) return xfer_chunks(c, hybrid, Hs, nv, seg_last, Hs + 1);
   return ends;
+}
+
+// volumetric particles a step appends to its combed source (config 3)
+uint64_t step_volume_histories(const hwwg_driver* d, int step);
+
+uint64_t step_volume_histories(const hwwg_driver* d, int step) {
+  const hwwg_run_config& c = d->cfg;
+  if (!(c.vol_rate > 0.0) || step < 1 || step > c.time_steps) return 0;
+  return d->q_row[step] >= 0 ? c.vol_histories : 0;
 }
 
 // One time step (driver.cpp:99-284).
@@ -944,9 +948,9 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   std::vector<size_t> seg_wait;  // segment u waits for upload event h2d_ev[seg_wait[u]]
   std::vector<uint64_t> seg_range;  // packed uploads: segment u converts [seg_range[u], seg_range[u+1])
   d->src_packed = 0;  // set below where the step's source starts with packed comb teeth
-  if (c.host_bank && d->fast && d->host_pre_combed && d->world == 1 && !(c.vol_rate > 0.0)) {
+  if (c.host_bank && d->fast && d->host_pre_combed && d->world == 1) {
     const uint64_t Hs = d->host_bank_n;
-    const std::vector<uint64_t> bounds = xfer_chunks(c, d->hybrid(), Hs, &seg_wait);
+    const std::vector<uint64_t> bounds = xfer_chunks(c, d->hybrid(), Hs, nv_step, &seg_wait);
     const bool piped = d->d2h_pending && d->host_packed && bounds == d->xfer_end && d->e2e_pipe;
     if (d->d2h_pending && !piped) HWWG_CUDA(cudaStreamSynchronize(d->d2h_stream));
     d->d2h_pending = false;
@@ -1741,9 +1745,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     d->host_pre_combed = true;
     d->host_bank_n = d->target;
     d->bank_n = d->target;
-    // the packed wire format when the next step uploads by chunks (no
-    // volumetric particles to append): (x, mu) now, (w, t) only if not shared
-    d->host_packed = !(c.vol_rate > 0.0);
+    // the packed wire format, uploaded by pieces (the next step's volumetric
+    // particles are sampled on the device after the teeth): (x, mu) now, (w, t)
+    // only if not shared
+    d->host_packed = true;
     if (d->host_packed) {
       // the teeth share one (w, t) by construction (packed_out): the spacing
       // comes down with the record, the census time is known here
@@ -1871,7 +1876,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
     // uploads take, on the d2h stream; this call returns now and each upload
     // of the next step waits only for its own piece (hwwg_driver_bank and
     // destroy wait for all of them)
-    d->xfer_end = xfer_chunks(c, d->hybrid(), d->target, nullptr);
+    d->xfer_end = xfer_chunks(c, d->hybrid(), d->target, step_volume_histories(d, step + 1), nullptr);
     // (no event wait: the host synchronised the stream after the comb — fetch above)
     if (hprof) {
       for (auto& e : d->xt)

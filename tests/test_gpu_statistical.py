@@ -307,3 +307,26 @@ def test_census_thinning_cold_start(monkeypatch, which, H):
     # (batch sigma misses the comb's inter-step noise: a sanity bound here; the
     # replicate pin, tests/test_gpu_stat_pin.py, runs every workload thinned)
     assert np.mean(np.abs(z) < 3) >= 0.9, np.sort(np.abs(z))[-8:]
+
+
+def test_host_round_trip_volumetric_source():
+    """The e2e host round trip (host_bank) on config 3, whose steps append
+    device-sampled volumetric particles after the combed teeth: the teeth cross
+    PCIe packed in pieces (16 B each), the volumetric ones never do, and the run
+    keeps the device-resident run's bookkeeping and statistics."""
+    from tests.test_gpu_parity import _c3
+    H, steps = 60_000, 4
+    _, g = _c3(H, steps, mode="hww", cells=300)
+    d = hw.Driver(g, rng_mode=hw.RNG_PHILOX)
+    dev = [d.step() for _ in range(steps)]
+    d.close()
+    g.host_bank = True
+    e = hw.Driver(g, rng_mode=hw.RNG_PHILOX)
+    host = [e.step() for _ in range(steps)]
+    e.close()
+    for k, (r, q) in enumerate(zip(dev, host)):
+        assert q.histories == r.histories and q.comb_out == r.comb_out
+        if k >= 1:  # steps 2.. open with the pre-combed teeth from the host
+            assert q.h2d_bytes == q.comb_out * 16, (k, q.h2d_bytes, q.comb_out)
+        assert abs(q.segments / r.segments - 1) < 0.12, (k, q.segments, r.segments)
+        assert abs(q.census_weight / r.census_weight - 1) < 0.05, (k, q.census_weight, r.census_weight)
