@@ -297,6 +297,8 @@ struct hwwg_driver {
     for (auto e : h2d_ev) cudaEventDestroy(e);
     if (d2h_stream) cudaStreamSynchronize(d2h_stream);
     for (auto e : d2h_ev) cudaEventDestroy(e);
+    for (auto e : xt)
+      if (e) cudaEventDestroy(e);
     if (ev_pre) cudaEventDestroy(ev_pre);
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (ev_fork) cudaEventDestroy(ev_fork);
