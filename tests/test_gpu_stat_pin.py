@@ -151,6 +151,14 @@ def test_config5_variants(rho, k):
                                     ma_base_k=k), 8, label=f"C5 rho={rho} k={k}")
 
 
+def test_config5_headline_all_timed_steps():
+    """The bench headline (config 5 at rho 5, MA3) over all 20 timed steps at
+    H = 1e5: the cold start (census thinning), step 2's comb of the thinned bank,
+    and the steady steps, every closure moment, current and window centre."""
+    check_engine(lambda s: baseline(5, histories=100_000, time_steps=20, seed=s, rho=5.0,
+                                    ma_base_k=1), 20, label="C5 headline (20 steps)")
+
+
 def test_config4_first_steps():
     """Config 4 (4000 cells, c = 0.99, hww rho 1.25): the cold start and two steady steps."""
     check_engine(lambda s: baseline(4, histories=100_000, time_steps=3, seed=s), 3, label="C4")
