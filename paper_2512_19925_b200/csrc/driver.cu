@@ -537,8 +537,18 @@ void print_timeline(hwwg_driver* d, int nseg, int step) {
   const size_t per = (size_t)d->timeline_warps * K;
   std::vector<unsigned long long> h(per * nseg);
   HWWG_CUDA(cudaMemcpy(h.data(), d->timeline.p, h.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> sp(2 * (size_t)nseg, 0);  // launch spans (block start / end)
+  if (!d->seg_events)
+    HWWG_CUDA(cudaMemcpy(sp.data(), d->span.p, sp.size() * 8, cudaMemcpyDeviceToHost));
   for (int s = 0; s < nseg; ++s) {
     const unsigned long long* t = h.data() + per * s;
+    if (sp[2 * s + 1]) {  // the flush tail: last block end after the last warp's exit
+      unsigned long long lastx = 0;
+      for (unsigned w = 0; w < d->timeline_warps; ++w) lastx = std::max(lastx, t[K * w + 2]);
+      std::fprintf(stderr, "[timeline] step %d seg %d: launch span %.1f us, flush tail %.1f us\n", step, s,
+                   1e-3 * (double)(sp[2 * s + 1] - sp[2 * s]),
+                   sp[2 * s + 1] > lastx ? 1e-3 * (double)(sp[2 * s + 1] - lastx) : 0.0);
+    }
     unsigned long long t0 = ~0ULL, tmax = 0, evs = 0, evmax = 0;
     unsigned wmax = 0;  // the warp with the most loop trips
     std::vector<double> ex, sd;
