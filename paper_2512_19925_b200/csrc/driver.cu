@@ -251,6 +251,8 @@ struct hwwg_driver {
   uint64_t src_packed = 0;
   double src_t0 = 0.0;
   int packed_teeth = 1;  // HWWG_PACKED_TEETH=0: full 48 B teeth (A/B and tests)
+  int tally_window = 1;  // HWWG_TALLY_WINDOW=0: no windowed shared tallies (config 4)
+  int tally_window_max = 0;  // HWWG_TALLY_WINDOW_MAX=n: clip the window to n cells (tests of the fallback)
   Comm* comm = nullptr;      // NCCL or the in-process loopback (comm.h)
   bool own_stream = true;    // false: the loopback hub's shared stream
   DevBuf<double> nccl_buf;    // all-gathered census weights, snapshot slabs
@@ -1250,6 +1252,53 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
   }
   rec->thinned = pc_s0 > 0.0 ? 1 : 0;
 
+  // ---- tally window (FastArgs::t_win): the cells this step's particles can
+  // reach — the previous step's track-flux support (the census sits inside
+  // it), the pulse or the volumetric box, widened by the farthest flight of the
+  // step (max speed x dt) and two cells. Used where the mesh's full fixed-point
+  // histograms do not fit shared memory (config 4); scores outside go to the
+  // global tallies, so the window only decides speed, never results.
+  int win_lo = 0, win_n = 0;
+  if (d->fast && d->fix_tallies && d->tally_window) {
+    const std::vector<double>& e = d->prob.edges;
+    double xlo = INFINITY, xhi = -INFINITY;
+    if (d->history.empty()) {
+      if (!c.no_pulse) xlo = xhi = c.x0;
+    } else {
+      int f = -1, l = -1;
+      for (int i = 0; i < I; ++i)
+        if (d->h_phi_track[i] != 0.0) {
+          if (f < 0) f = i;
+          l = i;
+        }
+      if (f >= 0) {
+        xlo = e[f];
+        xhi = e[l + 1];
+      }
+    }
+    if (nv_step) {
+      xlo = std::min(xlo, c.vol_x_lo);
+      xhi = std::max(xhi, c.vol_x_hi);
+    }
+    if (xlo <= xhi) {
+      double vmax = 0.0;
+      for (const CellInfo& ci : d->prob.cells_h) vmax = std::max(vmax, ci.speed);
+      const double reach = vmax * dt;
+      auto cell_of = [&](double x) {
+        const int k = (int)(std::upper_bound(e.begin(), e.end(), x) - e.begin()) - 1;
+        return std::max(0, std::min(I - 1, k));
+      };
+      const int lo = std::max(0, cell_of(xlo - reach) - 2);
+      const int hi = std::min(I - 1, cell_of(xhi + reach) + 2);
+      win_lo = lo;
+      win_n = hi - lo + 1;
+      if (d->tally_window_max && win_n > d->tally_window_max) {  // tests: a window too narrow
+        win_lo += (win_n - d->tally_window_max) / 2;
+        win_n = d->tally_window_max;
+      }
+    }
+  }
+
   unsigned long long count = 0;
   DevError derr{};
   const int cur = d->rep_cur;
@@ -1436,9 +1485,16 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           }
           return best;
         };
-        if (fa.smem_tallies == 1 && (!fa.aggregate || d->agg_all != 1) && d->flush_replicas == 0 &&
-            d->fix_tallies) {
-          const size_t fsm = fast_smem_fix_bytes(I, fa.nb) + fast_smem_centers_bytes(I);
+        fa.t_win = 0;
+        fa.t_lo = 0;
+        fa.t_n = I;
+        // windowed fixed-point histograms (config 4) instead of global REDs
+        const bool try_win = fa.smem_tallies == 0 && win_n > 0 && win_n < I &&
+                             d->smem_mode == 1 && d->agg_all != 1;
+        if ((fa.smem_tallies == 1 || try_win) && (!fa.aggregate || d->agg_all != 1) &&
+            d->flush_replicas == 0 && d->fix_tallies) {
+          const int T = try_win ? win_n : I;
+          const size_t fsm = fast_smem_fix_bytes(T, fa.nb) + fast_smem_centers_bytes(I);
           double vmax = 0.0;
           for (const CellInfo& ci : d->prob.cells_h) vmax = std::max(vmax, ci.speed * ci.inv_dx);
           double vmin = vmax;
@@ -1446,7 +1502,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
           const double w = std::max(c.rho, d->step_wref);
           int kt = 0, ke = 0;
           int wfix = 12, wbase = 12;
-          const int fix_warps = shape(fsm, 1, 1, wfix);
+          const int fix_warps = shape(fsm, 1, try_win ? 2 : 1, wfix);
           // dynamic range: the smallest census score (a weight near the lowest
           // window floor eps_min / rho) must keep >= 2^20 grid units, or its
           // rounding would bias low-window cells: beyond 20 binades below the
@@ -1456,9 +1512,16 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
                                 std::ilogb(w * vmax) - std::ilogb(smallest) <= 20;
           int kc = 0;
           if (range_ok && fast_fix_exponent(w * vmax, &kt) && fast_fix_exponent(w / dt, &ke) &&
-              fast_fix_exponent(w, &kc) &&
-              5 * fix_warps >= 4 * shape(smem, 1, 0, wbase)) {  // (shared fp64 adds are CAS loops)
+              fast_fix_exponent(w, &kc) && fix_warps > 0 &&
+              (try_win || 5 * fix_warps >= 4 * shape(smem, 1, 0, wbase))) {  // (shared fp64 adds are CAS loops)
             fa.fix = 1;
+            if (try_win) {
+              fa.smem_tallies = 1;
+              fa.t_win = 1;
+              fa.t_lo = win_lo;
+              fa.t_n = win_n;
+              fa.census_runs = step == 1 ? 1 : 0;  // (aggregate was forced on for the global path)
+            }
             fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             fa.fix_k_trk = kt;
             fa.fix_k_edge = ke;
@@ -1469,9 +1532,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         }
         fa.scramble = fa.aggregate ? 0 : d->scramble;
         int wsel = 12;
-        shape(smem, fa.smem_tallies == 1, fa.fix, wsel);
+        const int fxk = fa.fix ? (fa.t_win ? 2 : 1) : 0;  // the instantiation: fp64 / fixed / windowed
+        shape(smem, fa.smem_tallies == 1, fxk, wsel);
         fa.warps = wsel;
-        const int blocks = d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fa.fix, wsel);
+        const int blocks = d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fxk, wsel);
         const int gw = blocks * wsel;
         grid_warps_max = std::max(grid_warps_max, gw);
         if (u == thr.size() && gw >= grid_warps_max && fa.n_src) {
@@ -2004,6 +2068,8 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_E2E_PIPE")) d->e2e_pipe = std::atoi(m) != 0;
   if (const char* m = std::getenv("HWWG_PACKED_TEETH")) d->packed_teeth = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_TALLY_WINDOW")) d->tally_window = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_TALLY_WINDOW_MAX")) d->tally_window_max = std::max(0, std::atoi(m));
   if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
     const int w = std::atoi(m);
     d->block_warps = (w == 12 || w == 14 || w == 24) ? w : 0;

@@ -104,6 +104,10 @@ struct FastArgs {
   // 1: fixed-point track/edge tallies in shared memory (smem_tallies == 1, no
   // aggregation): scores on the grid 2^-fix_k_* (fast_fix_exponent)
   int fix, fix_k_trk, fix_k_edge, fix_k_cw;  // ... census weight by batch on 2^-fix_k_cw
+  // t_win = 1 (with fix): the fixed-point histograms cover cells [t_lo, t_lo +
+  // t_n) only (the step's particles' reach, config 4); other scores go to the
+  // global tallies with fp64 REDs
+  int t_win, t_lo, t_n;
   int warps;            // warps per block: 12 (2 blocks per SM) or 24 (1 block per SM)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   int pdl;              // 1: programmatic dependent launch after the previous kernel
@@ -181,6 +185,7 @@ void launch_aos_to_census(const hwwg_particle* in, uint64_t n, CensusBank out, c
 // resident blocks per SM of the transport instantiation (uniform mesh, shared
 // tallies, fixed-point slots, warps per block: 12 or 24) with `smem` dynamic
 // shared memory, and the most warps per SM any instantiation holds
+// (fix: 0 fp64, 1 fixed-point, 2 fixed-point over a cell window)
 int fast_blocks_per_sm(size_t smem, int uniform, int shf, int fix, int warps);
 // transport block shapes (warps per block): 2 x 12, 2 x 14 (where the
 // registers and the tallies' shared memory allow 28 warps) or 1 x 24 per SM

@@ -547,9 +547,14 @@ struct SmemTally {
 // kShf: the fp64 tallies live in block-private shared memory (smem_tallies ==
 // 1), statically, so the atomics compile to shared-memory CAS loops with no
 // generic-address dispatch.
-template <bool kUniform, bool kShf, bool kFix, int kW>
+// kWin: the fixed-point histograms cover a window of cells [t_lo, t_lo + t_n)
+// (FastArgs), where a mesh's full histograms do not fit shared memory (config
+// 4's 4000 cells) but the step's particles stay in a narrow region around the
+// pulse; scores outside the window go to the global tallies with fp64 REDs.
+template <bool kUniform, bool kShf, bool kFix, int kW, bool kWin = false>
 __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(FastArgs a) {
   static_assert(kShf || !kFix, "fixed-point tallies live in shared memory");
+  static_assert(!kWin || kFix, "windowed tallies are fixed-point");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
@@ -593,7 +598,27 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   __shared__ unsigned s_sweep;  // kFix: the carry sweep's slot cursor
   // kFix: the fixed-point slots, contiguous from S.trk (track nb*I, census
   // phi/J/F 3*I, edges I+1, census weight by batch nb)
-  const unsigned fix_slots = (unsigned)(a.nb * I + 4 * I + 1 + a.nb);
+  // tally window: cells [tlo, tlo + tn) (the whole mesh unless kWin)
+  const int tlo = kWin ? a.t_lo : 0;
+  const int tn = kWin ? a.t_n : I;
+  // window cell of a global cell (-1 outside; edges: [0, tn])
+  auto wcell = [&](int c) -> int {
+    if constexpr (kWin) {
+      const unsigned u = (unsigned)(c - tlo);
+      return u < (unsigned)tn ? (int)u : -1;
+    } else {
+      return c;
+    }
+  };
+  auto wedge = [&](int e) -> int {
+    if constexpr (kWin) {
+      const unsigned u = (unsigned)(e - tlo);
+      return u <= (unsigned)tn ? (int)u : -1;
+    } else {
+      return e;
+    }
+  };
+  const unsigned fix_slots = (unsigned)(a.nb * tn + 4 * tn + 1 + a.nb);
   // slots per lane per sweep: every slot is swept within 4096 / 32 sweeps
   const unsigned fix_spl = (fix_slots + 4095u) / 4096u;
   if (kFix && threadIdx.x == 0) s_sweep = 0u;
@@ -1156,10 +1181,11 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       };
       double* edg = kShf ? S.edge : a.t.edge_current;
       if (trk_key >= 0) {
+        const int wc = wcell(trk_cell);
         if (!kFix) atomicAdd(trk + trk_key, trk_v);
-        else if (!fix_add(S.trk + 2 * trk_key, trk_v, fix_trk))
+        else if (wc < 0 || !fix_add(S.trk + 2 * (kWin ? p.bslot * tn + wc : trk_key), trk_v, fix_trk))
           atomicAdd(a.t.track_flux_batch + (size_t)a.b_lo * I + trk_key, trk_v);
-        if (sh) atomicAdd(S.trc + trk_cell, 1u);
+        if (sh && wc >= 0) atomicAdd(S.trc + wc, 1u);
         else atomicAdd(a.t.tracks + trk_cell, 1ULL);
       }
 #if !defined(HWWG_CENSUS_PER_LANE)
@@ -1168,17 +1194,19 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       // with fp64 slots they are run-aggregated (census_runs)
       if (kFix && !a.census_runs) {
         if (cen_cell >= 0) {
-          if (!fix_add(S.cphi + 2 * cen_cell, cen_phi, fix_trk)) atomicAdd(a.t.census_phi + cen_cell, cen_phi);
-          if (!fix_add(S.cJ + 2 * cen_cell, cen_J, fix_trk)) atomicAdd(a.t.census_current + cen_cell, cen_J);
-          if (!fix_add(S.cF + 2 * cen_cell, cen_F, fix_trk)) atomicAdd(a.t.census_closure + cen_cell, cen_F);
+          const int wc = wcell(cen_cell);
+          if (wc < 0 || !fix_add(S.cphi + 2 * wc, cen_phi, fix_trk)) atomicAdd(a.t.census_phi + cen_cell, cen_phi);
+          if (wc < 0 || !fix_add(S.cJ + 2 * wc, cen_J, fix_trk)) atomicAdd(a.t.census_current + cen_cell, cen_J);
+          if (wc < 0 || !fix_add(S.cF + 2 * wc, cen_F, fix_trk)) atomicAdd(a.t.census_closure + cen_cell, cen_F);
         }
         census_weight_runs_t(fix_cwb, cen_cell >= 0, cen_b, cen_w);
       } else if (kFix) {  // cold start: identical split copies reach census together
         census_groups(
             [&](int cell, double s0, double s1, double s2) {
-              if (!fix_add(S.cphi + 2 * cell, s0, fix_trk)) atomicAdd(a.t.census_phi + cell, s0);
-              if (!fix_add(S.cJ + 2 * cell, s1, fix_trk)) atomicAdd(a.t.census_current + cell, s1);
-              if (!fix_add(S.cF + 2 * cell, s2, fix_trk)) atomicAdd(a.t.census_closure + cell, s2);
+              const int wc = wcell(cell);
+              if (wc < 0 || !fix_add(S.cphi + 2 * wc, s0, fix_trk)) atomicAdd(a.t.census_phi + cell, s0);
+              if (wc < 0 || !fix_add(S.cJ + 2 * wc, s1, fix_trk)) atomicAdd(a.t.census_current + cell, s1);
+              if (wc < 0 || !fix_add(S.cF + 2 * wc, s2, fix_trk)) atomicAdd(a.t.census_closure + cell, s2);
             },
             fix_cwb, cen_cell, cen_b, cen_w, p.mu, cen_phi, cen_J, cen_F);
       } else {
@@ -1199,8 +1227,9 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       }
 #endif
       if (edge_key >= 0) {
+        const int we = wedge(edge_key);
         if (!kFix) atomicAdd(edg + edge_key, edge_v);
-        else if (!fix_add(S.edge + 2 * edge_key, edge_v, fix_edge))
+        else if (we < 0 || !fix_add(S.edge + 2 * we, edge_v, fix_edge))
           atomicAdd(a.t.edge_current + edge_key, edge_v);
       }
     }
@@ -1330,22 +1359,24 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
     const int nb = a.nb;
     const double inv_trk = kFix ? pow2(-a.fix_k_trk) : 0.0;
     const double inv_edge = kFix ? pow2(-a.fix_k_edge) : 0.0;
-    for (int i = threadIdx.x; i < nb * I; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nb * tn; i += blockDim.x) {
       const double v = kFix ? fix_value(S.trk + 2 * i, inv_trk) : S.trk[i];
-      if (v != 0.0) atomicAdd(&a.t.track_flux_batch[(size_t)a.b_lo * I + i], v);
+      // (window slot i = batch i / tn, cell tlo + i % tn)
+      const size_t g = kWin ? (size_t)(i / tn) * I + tlo + i % tn : (size_t)i;
+      if (v != 0.0) atomicAdd(&a.t.track_flux_batch[(size_t)a.b_lo * I + g], v);
     }
-    for (int i = threadIdx.x; i < I; i += blockDim.x) {
+    for (int i = threadIdx.x; i < tn; i += blockDim.x) {
       const double vp = kFix ? fix_value(S.cphi + 2 * i, inv_trk) : S.cphi[i];
       const double vj = kFix ? fix_value(S.cJ + 2 * i, inv_trk) : S.cJ[i];
       const double vf = kFix ? fix_value(S.cF + 2 * i, inv_trk) : S.cF[i];
-      if (vp != 0.0) atomicAdd(&a.t.census_phi[i], vp);
-      if (vj != 0.0) atomicAdd(&a.t.census_current[i], vj);
-      if (vf != 0.0) atomicAdd(&a.t.census_closure[i], vf);
-      if (S.trc[i]) atomicAdd(&a.t.tracks[i], (unsigned long long)S.trc[i]);
+      if (vp != 0.0) atomicAdd(&a.t.census_phi[tlo + i], vp);
+      if (vj != 0.0) atomicAdd(&a.t.census_current[tlo + i], vj);
+      if (vf != 0.0) atomicAdd(&a.t.census_closure[tlo + i], vf);
+      if (S.trc[i]) atomicAdd(&a.t.tracks[tlo + i], (unsigned long long)S.trc[i]);
     }
-    for (int i = threadIdx.x; i <= I; i += blockDim.x) {
+    for (int i = threadIdx.x; i <= tn; i += blockDim.x) {
       const double v = kFix ? fix_value(S.edge + 2 * i, inv_edge) : S.edge[i];
-      if (v != 0.0) atomicAdd(&a.t.edge_current[i], v);
+      if (v != 0.0) atomicAdd(&a.t.edge_current[tlo + i], v);
     }
     for (int i = threadIdx.x; i < nb; i += blockDim.x) {
       const double v = kFix ? fix_value(S.cwb + 2 * i, pow2(-a.fix_k_cw)) : S.cwb[i];
@@ -1484,9 +1515,12 @@ int fast_prof_read(unsigned long long out[12], unsigned* hist) {
 void configure_fast_kernel();
 
 using FastKernel = void (*)(FastArgs);
+// fix: 0 fp64 tallies, 1 fixed-point, 2 fixed-point over a cell window (kWin)
 template <int kW>
 FastKernel fast_kernel_w(int uniform, int shf, int fix) {
-  return uniform && fix   ? k_fast_segment<true, true, true, kW>
+  return uniform && fix == 2 ? k_fast_segment<true, true, true, kW, true>
+         : fix == 2          ? k_fast_segment<false, true, true, kW, true>
+         : uniform && fix   ? k_fast_segment<true, true, true, kW>
          : uniform && shf ? k_fast_segment<true, true, false, kW>
          : uniform        ? k_fast_segment<true, false, false, kW>
          : fix            ? k_fast_segment<false, true, true, kW>
@@ -1535,12 +1569,12 @@ void configure_fast_kernel() {
   int dev = 0;
   HWWG_CUDA(cudaGetDevice(&dev));
   if (dev == done_dev) return;
-  static DynSmemCache configured[18];
+  static DynSmemCache configured[24];
   int i = 0;
   for (int w : kFastBlockWarps)
     for (int u = 0; u < 2; ++u)
       for (int sh = 0; sh < 2; ++sh)
-        for (int f = 0; f <= sh; ++f) {
+        for (int f = 0; f <= 2 * sh; ++f) {
           // the block's static shared memory (its split-stack bottoms) comes first
           const FastKernel k = fast_kernel(u, sh, f, w);
           cudaFuncAttributes fa{};
@@ -1555,22 +1589,24 @@ void launch_fast_segment(const FastArgs& a0, int blocks, size_t smem, cudaStream
   configure_fast_kernel();
   FastArgs a = a0;
   {  // the dynamic shared-memory layout (SmemOffsets; smem_view's order)
+    // (the histograms span the tally window's cells, the centres and edges the mesh)
     const unsigned I = (unsigned)a.mesh.I, nb = (unsigned)a.nb;
+    const unsigned T = (a.smem_tallies == 1 && a.fix && a.t_win) ? (unsigned)a.t_n : I;
     const unsigned slotw = (a.smem_tallies == 1 && a.fix) ? 2u : 1u;
     SmemOffsets& o = a.so;
-    o.trk = (I + 1) / 2;
-    o.cphi = o.trk + slotw * nb * I;
-    o.cJ = o.cphi + slotw * I;
-    o.cF = o.cJ + slotw * I;
-    o.edge = o.cF + slotw * I;
-    o.cwb = o.edge + slotw * (I + 1);
+    o.trk = (T + 1) / 2;
+    o.cphi = o.trk + slotw * nb * T;
+    o.cJ = o.cphi + slotw * T;
+    o.cF = o.cJ + slotw * T;
+    o.edge = o.cF + slotw * T;
+    o.cwb = o.edge + slotw * (T + 1);
     o.bclo = o.cwb + slotw * nb;
     o.cent = a.smem_tallies == 1 ? o.bclo + 2 : (a.smem_tallies ? (I + 1) / 2 : 0);
     o.edgex = o.cent + I;
   }
   if (!a.pool_reset_done) k_segment_reset<<<1, 1, 0, s>>>(a.pool.ctl, a.src_head, a.span);
   const bool shf = a.smem_tallies == 1;
-  const bool fix = shf && a.fix;
+  const int fix = shf && a.fix ? (a.t_win ? 2 : 1) : 0;
   const FastKernel k = fast_kernel(a.uniform, shf, fix, a.warps);
   // programmatic dependent launch: the grid may be scheduled while the kernel
   // before it (the window update) drains; every block waits for it

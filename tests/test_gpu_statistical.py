@@ -330,3 +330,28 @@ def test_host_round_trip_volumetric_source():
             assert q.h2d_bytes == q.comb_out * 16, (k, q.h2d_bytes, q.comb_out)
         assert abs(q.segments / r.segments - 1) < 0.12, (k, q.segments, r.segments)
         assert abs(q.census_weight / r.census_weight - 1) < 0.05, (k, q.census_weight, r.census_weight)
+
+
+@pytest.mark.parametrize("window_max", ["0", "48"])
+def test_tally_window_matches_global_tallies(monkeypatch, window_max):
+    """Config 4 (4000 cells: the full fixed-point histograms do not fit shared
+    memory) with its histograms over the window of cells the step's particles can
+    reach (FastArgs::t_win) against the global fp64 REDs, on the same events (one
+    cold-start step, per-lane tallies): equal counters and track counts, tallies
+    within fp64 summation order and the fixed-point grid. window_max = 48 clips the
+    window to 48 cells, so most scores take the out-of-window fallback."""
+    from paper_2512_19925_b200.configs import baseline
+    monkeypatch.setenv("HWWG_FAST_AGG", "2")
+    out = {}
+    for win in ("1", "0"):
+        monkeypatch.setenv("HWWG_TALLY_WINDOW", win)
+        monkeypatch.setenv("HWWG_TALLY_WINDOW_MAX", window_max)
+        c = baseline(4, histories=100_000, time_steps=1, seed=5)
+        out[win] = run(c, hw.RNG_PHILOX)[0]
+    (rw, aw), (rg, ag) = out["1"], out["0"]
+    assert rw.segments == rg.segments and rw.census_size == rg.census_size
+    assert rw.counters.collisions == rg.counters.collisions
+    np.testing.assert_array_equal(aw["tracks_per_cell"], ag["tracks_per_cell"])
+    for k in ("phi_track", "phi_census", "current_census", "closure_census", "edge_current"):
+        np.testing.assert_allclose(aw[k], ag[k], rtol=1e-9, atol=1e-12 * np.abs(ag[k]).max(), err_msg=k)
+    np.testing.assert_allclose(rw.census_weight, rg.census_weight, rtol=1e-9)
