@@ -1489,8 +1489,13 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         fa.t_lo = 0;
         fa.t_n = I;
         // windowed fixed-point histograms (config 4) instead of global REDs
-        const bool try_win = fa.smem_tallies == 0 && win_n > 0 && win_n < I &&
-                             d->smem_mode == 1 && d->agg_all != 1;
+        // (also where the full copy fits but reaches 96 KB — config 3's 1000 cells,
+        // then one 24-warp block per SM — and a window halves it: config 3 +3.5%;
+        // HWWG_TALLY_WINDOW=2 windows every layout, config 5 -1%)
+        const bool big_copy = fast_smem_fix_bytes(I, fa.nb) >= 96 * 1024;
+        const bool try_win =
+            win_n > 0 && d->smem_mode == 1 && d->agg_all != 1 &&
+            (fa.smem_tallies == 0 ? win_n < I : ((big_copy || d->tally_window > 1) && 2 * win_n <= I));
         if ((fa.smem_tallies == 1 || try_win) && (!fa.aggregate || d->agg_all != 1) &&
             d->flush_replicas == 0 && d->fix_tallies) {
           const int T = try_win ? win_n : I;
@@ -1515,6 +1520,7 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
               fast_fix_exponent(w, &kc) && fix_warps > 0 &&
               (try_win || 5 * fix_warps >= 4 * shape(smem, 1, 0, wbase))) {  // (shared fp64 adds are CAS loops)
             fa.fix = 1;
+            fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             if (try_win) {
               fa.smem_tallies = 1;
               fa.t_win = 1;
@@ -1522,7 +1528,6 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
               fa.t_n = win_n;
               fa.census_runs = step == 1 ? 1 : 0;  // (aggregate was forced on for the global path)
             }
-            fa.census_runs = fa.aggregate;  // the cold start's crowded census cells
             fa.fix_k_trk = kt;
             fa.fix_k_edge = ke;
             fa.fix_k_cw = kc;
@@ -2068,7 +2073,7 @@ int hwwg_driver_create(const hwwg_run_config* cfg, const hwwg_options* opts, hww
   if (const char* m = std::getenv("HWWG_PDL")) d->pdl = std::atoi(m) ? 1 : 0;
   if (const char* m = std::getenv("HWWG_E2E_PIPE")) d->e2e_pipe = std::atoi(m) != 0;
   if (const char* m = std::getenv("HWWG_PACKED_TEETH")) d->packed_teeth = std::atoi(m) ? 1 : 0;
-  if (const char* m = std::getenv("HWWG_TALLY_WINDOW")) d->tally_window = std::atoi(m) ? 1 : 0;
+  if (const char* m = std::getenv("HWWG_TALLY_WINDOW")) d->tally_window = std::max(0, std::atoi(m));
   if (const char* m = std::getenv("HWWG_TALLY_WINDOW_MAX")) d->tally_window_max = std::max(0, std::atoi(m));
   if (const char* m = std::getenv("HWWG_FAST_BLOCK_WARPS")) {
     const int w = std::atoi(m);

@@ -511,15 +511,18 @@ __device__ __forceinline__ bool fix_add(double* slot, double v, double scale) {
   return true;
 }
 
-// Carry of one slot's low words into the next word (slot: 4 limb words).
+// Carry of one slot's low words into the next word (slot: 4 limb words). The
+// carry is taken with one atomic AND that clears the word's high half and
+// returns what it held, so two warps sweeping the same slot at once (a narrow
+// tally window cycles its cursor through few slots) move each carry exactly
+// once: a read-then-subtract let both subtract the same carry and wrap the low
+// word below zero. Adds racing with the sweep are not lost either way.
 __device__ __forceinline__ void fix_sweep_slot(unsigned* w) {
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const unsigned v = *(volatile unsigned*)(w + i);
-    const unsigned c = v >> 16;
-    if (c) {
-      atomicSub(w + i, c << 16);
-      atomicAdd(w + i + 1, c);
+    if (*(volatile unsigned*)(w + i) >> 16) {  // (cheap look first: carries are rare)
+      const unsigned c = atomicAnd(w + i, 0xffffu) >> 16;
+      if (c) atomicAdd(w + i + 1, c);
     }
   }
 }
