@@ -1540,7 +1540,10 @@ void driver_step(hwwg_driver* d, hwwg_step_record* rec) {
         const int fxk = fa.fix ? (fa.t_win ? 2 : 1) : 0;  // the instantiation: fp64 / fixed / windowed
         shape(smem, fa.smem_tallies == 1, fxk, wsel);
         fa.warps = wsel;
-        const int blocks = d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fxk, wsel);
+        // (the per-warp arrays — split stacks, census cursors, thinning residuals —
+        // hold max_warps = sms x kMaxWarpsPerSm warps: never launch more)
+        const int blocks = std::min(d->sms * fast_blocks_per_sm(smem, uni, fa.smem_tallies == 1, fxk, wsel),
+                                    d->max_warps / wsel);
         const int gw = blocks * wsel;
         grid_warps_max = std::max(grid_warps_max, gw);
         if (u == thr.size() && gw >= grid_warps_max && fa.n_src) {
