@@ -260,8 +260,12 @@ int hwwg_driver_arrays(hwwg_driver* d, double* phi_track, double* phi_sigma,
                        double* phi_census, double* current_census, double* closure_census,
                        double* edge_current, double* ww_centers, double* phi_hybrid,
                        uint64_t* tracks_per_cell);
-/* Census bank after the last step (the next step's comb input), reference
- * order.  Returns HWWG_ENOSPC with *n = size when cap is too small. */
+/* Census bank after the last step (the next step's comb input): reference
+ * order in exact mode; in Philox mode the banked particles in completion order
+ * (after a thinned step, rec.thinned, the ~k x target equal-quantum records the
+ * next comb reads), or with host_bank the next step's combed source.  Waits for
+ * a pipelined host-bank download still in flight.  Returns HWWG_ENOSPC with
+ * *n = size when cap is too small. */
 int hwwg_driver_bank(hwwg_driver* d, hwwg_particle* out, uint64_t cap, uint64_t* n);
 /* The deterministic reference for the step diagnostics (hww::run's
  * ReferenceSolution*, driver.hpp:88): phi_layer[(steps+1)*cells] layer values,
