@@ -398,7 +398,6 @@ def run_ours(args):
     e_s = time.perf_counter() - t0
     e.close()
     e_s = max_over_ranks(e_s, world)
-    e_s = max_over_ranks(e_s, world)
     e_val = e_seg / e_s
 
     # every other BASELINE configuration, briefly (single GPU, rank 0's view)
