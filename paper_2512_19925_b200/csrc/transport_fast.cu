@@ -659,11 +659,15 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   __syncthreads();
   volatile unsigned long long* ctl = a.pool.ctl;
 
-  unsigned n_ev = 0, n_iter = 0;
+  unsigned n_iter = 0;
+#ifdef HWWG_FAST_PROF
+  unsigned n_ev = 0;  // events (timeline word 3): -DHWWG_FAST_PROF builds only (a register)
+#endif
   // this warp's census chunk [wcur, wend), carried across the step's segments
   unsigned long long wcur = a.warp_cursor[2 * gwarp];
   unsigned wleft = (unsigned)(a.warp_cursor[2 * gwarp + 1] - wcur);  // <= kCensusChunk
-  const unsigned long long t_start = a.timeline ? globaltimer() : 0ULL;
+  // (the timeline's start stamp goes out now: no register held through the loop)
+  if (a.timeline && lane == 0) a.timeline[kTimelineWords * gwarp + 0] = globaltimer();
   Lane p;
   p.alive = false;
   p.fis = false;
@@ -956,7 +960,9 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       for (unsigned k = 0; k < fix_spl; ++k)
         fix_sweep_slot(reinterpret_cast<unsigned*>(S.trk) + 4 * ((c0 + 32u * k + lane) % fix_slots));
     }
+#ifdef HWWG_FAST_PROF
     if (p.alive) ++n_ev;
+#endif
     ++n_iter;
 #ifdef HWWG_FAST_PROF
     if (lane == 0) {
@@ -1325,11 +1331,14 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
     a.warp_cursor[2 * gwarp + 1] = wcur + wleft;
   }
   if (a.timeline) {
+#ifdef HWWG_FAST_PROF
     unsigned long long ev = n_ev;
+#else
+    unsigned long long ev = 0;  // (events are counted in -DHWWG_FAST_PROF builds)
+#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ev += __shfl_down_sync(0xffffffffu, ev, o);
     if (lane == 0) {
-      a.timeline[kTimelineWords * gwarp + 0] = t_start;
       a.timeline[kTimelineWords * gwarp + 1] = n_iter;
       a.timeline[kTimelineWords * gwarp + 2] = globaltimer();
       a.timeline[kTimelineWords * gwarp + 3] = ev;
