@@ -108,6 +108,10 @@ struct FastArgs {
   // t_n) only (the step's particles' reach, config 4); other scores go to the
   // global tallies with fp64 REDs
   int t_win, t_lo, t_n;
+  // set by launch_fast_segment: the grid scales 2^fix_k_* and the carry sweep's
+  // slot count and slots per lane
+  double fix_s_trk, fix_s_edge, fix_s_cw;
+  unsigned fix_slots, fix_spl;
   int warps;            // warps per block: 12 (2 blocks per SM) or 24 (1 block per SM)
   int pool_reset_done;  // 1: the kernel before this launch reset the pool counters
   int pdl;              // 1: programmatic dependent launch after the previous kernel

@@ -595,9 +595,8 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   S.cwb = smem + a.so.cwb;
   S.bclo = smem + a.so.bclo;
   const size_t tally_words = a.so.cent;
-  const double fix_trk = kFix ? pow2(a.fix_k_trk) : 0.0;
-  const double fix_edge = kFix ? pow2(a.fix_k_edge) : 0.0;
-  const double fix_cw = kFix ? pow2(a.fix_k_cw) : 0.0;
+  // (grid scales 2^k from the launch arguments: constant-bank operands, no registers)
+  const double fix_trk = a.fix_s_trk, fix_edge = a.fix_s_edge, fix_cw = a.fix_s_cw;
   __shared__ unsigned s_sweep;  // kFix: the carry sweep's slot cursor
   // kFix: the fixed-point slots, contiguous from S.trk (track nb*I, census
   // phi/J/F 3*I, edges I+1, census weight by batch nb)
@@ -621,9 +620,9 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
       return e;
     }
   };
-  const unsigned fix_slots = (unsigned)(a.nb * tn + 4 * tn + 1 + a.nb);
+  const unsigned fix_slots = a.fix_slots;  // nb*tn + 4*tn + 1 + nb (launch_fast_segment)
   // slots per lane per sweep: every slot is swept within 4096 / 32 sweeps
-  const unsigned fix_spl = (fix_slots + 4095u) / 4096u;
+  const unsigned fix_spl = a.fix_spl;
   if (kFix && threadIdx.x == 0) s_sweep = 0u;
   for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
   double* s_cent = smem + a.so.cent;  // read at every window site: keep it on chip
@@ -1600,6 +1599,16 @@ void configure_fast_kernel() {
 void launch_fast_segment(const FastArgs& a0, int blocks, size_t smem, cudaStream_t s) {
   configure_fast_kernel();
   FastArgs a = a0;
+  // fixed-point grid scales and sweep parameters, once per launch (kernel
+  // parameters: constant-bank operands in the event loop)
+  a.fix_s_trk = std::ldexp(1.0, a.fix_k_trk);
+  a.fix_s_edge = std::ldexp(1.0, a.fix_k_edge);
+  a.fix_s_cw = std::ldexp(1.0, a.fix_k_cw);
+  {
+    const unsigned tn = (a.smem_tallies == 1 && a.fix && a.t_win) ? (unsigned)a.t_n : (unsigned)a.mesh.I;
+    a.fix_slots = (unsigned)a.nb * tn + 4 * tn + 1 + (unsigned)a.nb;
+    a.fix_spl = (a.fix_slots + 4095u) / 4096u;
+  }
   {  // the dynamic shared-memory layout (SmemOffsets; smem_view's order)
     // (the histograms span the tally window's cells, the centres and edges the mesh)
     const unsigned I = (unsigned)a.mesh.I, nb = (unsigned)a.nb;
