@@ -704,6 +704,7 @@ __device__ __noinline__ void low_order_update_body(const LowOrderArgs& a);
 
 __global__ void __launch_bounds__(kCtaThreads) k_low_order_update(LowOrderArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (see k_losm_mid_fast)
   if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head, a.pool_span);
   if (a.backup_centers) {  // the step-start windows backup, then the record flags
     for (int i = threadIdx.x; i < a.I; i += blockDim.x) a.backup_centers[i] = a.s.centers[i];
@@ -847,6 +848,9 @@ __device__ __forceinline__ double snap_filtered(const LowOrderArgs& a, int m) {
 
 __global__ void __launch_bounds__(kCtaThreads) k_losm_mid_fast(LowOrderArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
+  // the next segment's transport grid may start its block-private setup now
+  // (it waits for this kernel's completion before reading anything it writes)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ double P[kCtaThreads + 1], R0[kCtaThreads], R1[kCtaThreads], red[32];
   __shared__ int s_flags[2];
   if (a.pool_ctl && threadIdx.x == 0) fast_pool_reset(a.pool_ctl, a.pool_src_head, a.pool_span);

@@ -558,7 +558,10 @@ template <bool kUniform, bool kShf, bool kFix, int kW, bool kWin = false>
 __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(FastArgs a) {
   static_assert(kShf || !kFix, "fixed-point tallies live in shared memory");
   static_assert(!kWin || kFix, "windowed tallies are fixed-point");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch
+  // (programmatic dependent launch: the block-private setup below — zeroed
+  // histograms, mesh edges, log table — overlaps the window-update kernel this
+  // launch follows; griddepcontrol.wait comes before the first read of anything
+  // that kernel writes: the centres, the window flags, the pool counters)
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   const int I = a.mesh.I;
   const double* __restrict__ edges = a.mesh.edges;
   const CellInfo* __restrict__ cells = a.mesh.cells;
-  const bool windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
+  bool windows = false;  // (read after griddepcontrol.wait below)
   // smem_tallies: 0 all global REDs; 1 all block-private shared memory; 2 fp64
   // tallies as global REDs (native, fire-and-forget) and the integer track
   // counts in shared memory (shared fp64 adds are CAS loops on sm_100)
@@ -626,13 +629,15 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
   if (kFix && threadIdx.x == 0) s_sweep = 0u;
   for (size_t i = threadIdx.x; i < tally_words; i += blockDim.x) smem[i] = 0.0;
   double* s_cent = smem + a.so.cent;  // read at every window site: keep it on chip
-  if (windows)
-    for (int i = threadIdx.x; i < I; i += blockDim.x) s_cent[i] = a.centers[i];
   // mesh edges (read at every event) and the log table, on chip
   double* s_edge = smem + a.so.edgex;
   for (int e = threadIdx.x; e <= I; e += blockDim.x) s_edge[e] = edges[e];
   __shared__ double s_logtab[256];
   for (int j = threadIdx.x; j < 256; j += blockDim.x) s_logtab[j] = c_logtab[j];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the window update has completed
+  windows = a.centers != nullptr && (a.active == nullptr || *a.active != 0);
+  if (windows)
+    for (int i = threadIdx.x; i < I; i += blockDim.x) s_cent[i] = a.centers[i];
   __shared__ double s_w0;  // the weight of every comb tooth (the comb spacing, on the device)
   if (threadIdx.x == 0) s_w0 = a.n_packed ? *a.src_w0 : 0.0;
   // census thinning (FastArgs::precomb): each lane's distance to its next tooth,
