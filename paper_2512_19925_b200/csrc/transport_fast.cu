@@ -449,6 +449,8 @@ __device__ __forceinline__ void census_groups(AddCell add_cell, AddW add_w, int 
     const double n = (double)__popc(g);
     add_cell(cell, n * v0, n * v1, n * v2);
   }
+  // (run-aggregated: in the cold start every census lane of a warp adds to one
+  // batch slot — per-lane limb adds cost C5's step 1 27 -> 31 ms)
   census_weight_runs_t(add_w, c, b, w);
 }
 
@@ -1212,7 +1214,9 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
           if (wc < 0 || !fix_add(S.cJ + 2 * wc, cen_J, fix_trk)) atomicAdd(a.t.census_current + cen_cell, cen_J);
           if (wc < 0 || !fix_add(S.cF + 2 * wc, cen_F, fix_trk)) atomicAdd(a.t.census_closure + cen_cell, cen_F);
         }
-        census_weight_runs_t(fix_cwb, cen_cell >= 0, cen_b, cen_w);
+        // per lane, not run-aggregated: a spread population's census lanes rarely
+        // share a slot, and a run scan costs issue slots (C5 +2%, C2 +2.3%)
+        if (cen_cell >= 0) fix_cwb(cen_b, cen_w);
       } else if (kFix) {  // cold start: identical split copies reach census together
         census_groups(
             [&](int cell, double s0, double s1, double s2) {
