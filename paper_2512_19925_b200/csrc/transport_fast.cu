@@ -831,23 +831,23 @@ __global__ void __launch_bounds__(32 * kW, kMaxWarpsPerSm / kW) k_fast_segment(F
         r_lo = nb;
         r_hi = nb + csz < n_src ? nb + csz : n_src;
         if (n_src - nb < tail_zone) csz = kClaimTail;
+        // warm L1 with the new reservation once: its later refills hit on chip
+        if ((unsigned)lane < r_hi - r_lo) {
+          const unsigned kk = r_lo + lane;
+          const unsigned pi =
+              a.scramble && (kk | 1023u) < n_src ? (kk & ~1023u) | (__brev(kk) >> 22) : kk;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.xm + pi));
+          if (pi >= n_packed) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.wt + pi));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.meta + pi));
+          }
+        }
       }
       const unsigned k = __popc(need);
       const unsigned avail = r_hi - r_lo;
       const unsigned take = k < avail ? k : avail;
       const unsigned base = r_lo;
       r_lo += take;
-      // warm L1 with the rest of the reservation: the next refills hit on chip
-      if ((unsigned)lane < r_hi - r_lo) {
-        const unsigned kk = r_lo + lane;
-        const unsigned pi =
-            a.scramble && (kk | 1023u) < n_src ? (kk & ~1023u) | (__brev(kk) >> 22) : kk;
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.xm + pi));
-        if (pi >= n_packed) {
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.wt + pi));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.src.meta + pi));
-        }
-      }
       const unsigned rank = __popc(need & lt);
       if (!p.alive && rank < take) {
         // Claims walk the source in bit-reversed order inside 1024-particle
