@@ -117,7 +117,13 @@ def check_engine(cfg_fn, steps, skip_first=0, label=""):
         # (for the centres, that common shift also enters every cell's z^2: their
         # pooled mean z^2 spreads like one chi^2 draw — seen at 2.1 once in ~10 runs
         # of an unbiased engine — so its upper bound widens with the bias bound)
-        if not 0.5 < chi2 < (3.0 if k == "ww_centers" else 2.0):
+        # lower bound: a sanity check that the standard errors are not inflated
+        # (chi2 -> 0). Neighbouring cells and successive steps of one realisation
+        # are strongly correlated, so the pooled mean z^2 has far fewer degrees of
+        # freedom than cells x steps: the supercritical benchmark.cfg, whose
+        # population compounds by fission, was seen at 0.70 and 0.48 on the same
+        # unbiased engine (profiles/round2_stat_pin.jsonl)
+        if not 0.25 < chi2 < (3.0 if k == "ww_centers" else 2.0):
             fails.append((k, "chi2", chi2))
     for k in SCALARS:
         z = zstats(ex_s[k][:, skip_first:], fa_s[k][:, skip_first:],
